@@ -1,0 +1,278 @@
+"""Thin Python binding of libcpsgd.so (include/cpsgd.h): argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels.  PyTorch supplies device
+memory (the tensor X and the factors are borrowed torch CUDA tensors) and the stream.  There is
+no CPU fallback: constructing a handle without the built library, or without a CUDA device,
+raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcpsgd.so")
+
+SAMPLERS = {"uniform": 0, "leverage": 1, "euclidean": 2, "block_leverage": 3, "block_euclidean": 4}
+RULES = {"fixed": 0, "adaptive": 1}
+ORDERS = {"cyclic": 0, "random": 1}
+FLAG_MODE_MAJOR, FLAG_NO_GRAPH, FLAG_EXTERNAL_COMM = 0x1, 0x2, 0x4
+KERNEL_NAMES = ["k_sample", "k_gather", "k_update", "k_table", "k_reduce_partials", "nccl", "k_fit"]
+STATUS = {0: "CP_OK", -1: "CP_EINVAL", -2: "CP_ERANGE", -3: "CP_EDEGENERATE", -4: "CP_ENOMEM", -5: "CP_ECUDA",
+          -6: "CP_ENCCL", -7: "CP_ESTATE", -8: "CP_ENONFINITE"}
+
+EXPORTS = ["cp_sgd_init", "cp_sgd_destroy", "cp_sgd_last_error", "cp_sgd_sample", "cp_sgd_step", "cp_sgd_sweep",
+           "cp_fit", "cp_sgd_sync", "cp_sgd_steps_host", "cp_sgd_step_phase", "cp_sgd_exchange_info",
+           "cp_sgd_get_table", "cp_sgd_get_grad", "cp_sgd_get_accum", "cp_sgd_get_iter", "cp_sgd_set_iter",
+           "cp_sgd_refresh_tables", "cp_sgd_get_launches", "cp_sgd_profile", "cp_sgd_profile_read",
+           "cp_sgd_version", "cp_sgd_batch_max"]
+
+
+class CPError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("order", C.c_int32), ("dims", C.POINTER(C.c_int64)), ("rank", C.c_int32), ("dtype", C.c_int32),
+        ("X", C.c_void_p), ("factors", C.POINTER(C.c_void_p)), ("batch", C.c_int64),
+        ("block_window", C.POINTER(C.c_int32)), ("sampler", C.c_int32), ("rule", C.c_int32),
+        ("alpha", C.c_double), ("eta", C.c_double), ("b", C.c_double), ("eps", C.c_double),
+        ("seed", C.c_uint64), ("stream", C.c_void_p), ("world_rank", C.c_int32), ("world_size", C.c_int32),
+        ("nccl_unique_id", C.c_void_p), ("slab_begin", C.c_int64), ("slab_end", C.c_int64), ("flags", C.c_uint32),
+    ]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libcpsgd.so (raises if it has not been built -- no fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(path)
+    P, i32, i64, u64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
+    L.cp_sgd_init.argtypes = [C.POINTER(Config), C.POINTER(C.c_void_p)]
+    L.cp_sgd_destroy.argtypes = [P]
+    L.cp_sgd_last_error.argtypes = [P]
+    L.cp_sgd_last_error.restype = C.c_char_p
+    L.cp_sgd_batch_max.argtypes = [P, i32, C.POINTER(C.c_int64)]
+    L.cp_sgd_sample.argtypes = [P, i32, u64, P, P, C.POINTER(C.c_int64)]
+    L.cp_sgd_step.argtypes = [P, i32, dbl]
+    L.cp_sgd_sweep.argtypes = [P, i32, i32, P]
+    L.cp_fit.argtypes = [P, C.POINTER(C.c_double)]
+    L.cp_sgd_sync.argtypes = [P]
+    L.cp_sgd_steps_host.argtypes = [P, i32, i32, dbl, P]
+    L.cp_sgd_step_phase.argtypes = [P, i32, i32, dbl]
+    L.cp_sgd_exchange_info.argtypes = [P, i32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_int64)]
+    L.cp_sgd_get_table.argtypes = [P, i32, P, P, P]
+    L.cp_sgd_get_grad.argtypes = [P, P, C.POINTER(C.c_int32), P]
+    L.cp_sgd_get_accum.argtypes = [P, i32, P]
+    L.cp_sgd_get_iter.argtypes = [P, C.POINTER(C.c_uint64)]
+    L.cp_sgd_set_iter.argtypes = [P, u64]
+    L.cp_sgd_refresh_tables.argtypes = [P]
+    L.cp_sgd_get_launches.argtypes = [P, C.POINTER(C.c_uint64)]
+    L.cp_sgd_profile.argtypes = [P, i32]
+    L.cp_sgd_profile_read.argtypes = [P, i32, P, P, P, C.POINTER(C.c_int32)]
+    L.cp_sgd_version.restype = C.c_char_p
+    for name in EXPORTS:
+        getattr(L, name).restype = getattr(L, name).restype if name in ("cp_sgd_last_error", "cp_sgd_version") else C.c_int
+    _lib = L
+    return L
+
+
+def _dtype_code(t) -> int:
+    import torch
+
+    if t.dtype == torch.float32:
+        return 0
+    if t.dtype == torch.float64:
+        return 1
+    raise TypeError(f"unsupported dtype {t.dtype} (float32 / float64)")
+
+
+class CPSGD:
+    """Handle on one importance-sampled SGD chain (cp_sgd_t).
+
+    X        : torch CUDA tensor holding the (local slab of the) dense tensor, first-index-fastest
+               (a C-contiguous tensor of shape (I_N, ..., I_1) has exactly this layout)
+    factors  : list of N torch CUDA tensors, I_n x R, contiguous, same dtype as X (updated in place)
+    """
+
+    def __init__(self, X, dims: Sequence[int], factors: List, batch: int, sampler: str = "leverage",
+                 rule: str = "fixed", alpha: float = 0.01, eta: float = 0.05, b: float = 0.0, eps: float = 0.0,
+                 seed: int = 0, stream=None, world_rank: int = 0, world_size: int = 1, nccl_id: bytes = None,
+                 slab=None, mode_major: bool = True, block_window=None, graphs: bool = True,
+                 external_comm: bool = False):
+        import torch
+
+        L = load_library()
+        if not X.is_cuda:
+            raise ValueError("X must be a CUDA tensor (no CPU path exists)")
+        self.N = len(dims)
+        self.dims = [int(d) for d in dims]
+        self.R = int(factors[0].shape[1])
+        self.dtype = _dtype_code(X)
+        for A, I in zip(factors, self.dims):
+            if not (A.is_cuda and A.is_contiguous() and A.dtype == X.dtype and tuple(A.shape) == (I, self.R)):
+                raise ValueError("factors must be contiguous CUDA tensors I_n x R of X's dtype")
+        if not X.is_contiguous():
+            raise ValueError("X must be contiguous")
+        self._X, self._factors = X, list(factors)     # keep the borrowed buffers alive
+        self._dims_arr = (C.c_int64 * self.N)(*self.dims)
+        self._fac_arr = (C.c_void_p * self.N)(*[A.data_ptr() for A in factors])
+        self._win_arr = None if block_window is None else (C.c_int32 * (self.N - 1))(*[int(w) for w in block_window])
+        if stream is None:
+            stream = torch.cuda.current_stream(X.device)
+        self.stream = stream
+        self._nccl_id = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
+        flags = (FLAG_MODE_MAJOR if mode_major else 0) | (0 if graphs else FLAG_NO_GRAPH) | \
+                (FLAG_EXTERNAL_COMM if external_comm else 0)
+        lo, hi = (0, self.dims[-1]) if slab is None else (int(slab[0]), int(slab[1]))
+        cfg = Config(self.N, self._dims_arr, self.R, self.dtype, X.data_ptr(), self._fac_arr, int(batch),
+                     self._win_arr, SAMPLERS[sampler], RULES[rule], float(alpha), float(eta), float(b), float(eps),
+                     int(seed) & (2 ** 64 - 1), stream.cuda_stream, int(world_rank), int(world_size),
+                     None if self._nccl_id is None else C.cast(self._nccl_id, C.c_void_p), lo, hi, flags)
+        h = C.c_void_p()
+        st = L.cp_sgd_init(C.byref(cfg), C.byref(h))
+        if st != 0:
+            raise CPError(st, L.cp_sgd_last_error(None).decode())
+        self._h = h
+        self._L = L
+        self.batch = int(batch)
+        self.sampler = sampler
+        self.rule = rule
+        self.slab = (lo, hi)
+        self.world_size = world_size
+
+    # -- plumbing -----------------------------------------------------------------------------
+    def _chk(self, st):
+        if st != 0:
+            raise CPError(st, self._L.cp_sgd_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.cp_sgd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- the hot path -----------------------------------------------------------------------------
+    def sample(self, mode: int, it: int):
+        """(idx int32 [B_eff, N-1], omega fp64 [B_eff]) on the device."""
+        import torch
+
+        bm = C.c_int64(0)
+        self._chk(self._L.cp_sgd_batch_max(self._h, mode, C.byref(bm)))
+        bmax = bm.value
+        idx = torch.zeros((bmax, self.N - 1), dtype=torch.int32, device=self._X.device)
+        w = torch.zeros(bmax, dtype=torch.float64, device=self._X.device)
+        beff = C.c_int64(0)
+        self._chk(self._L.cp_sgd_sample(self._h, mode, C.c_uint64(it), C.c_void_p(idx.data_ptr()),
+                                        C.c_void_p(w.data_ptr()), C.byref(beff)))
+        return idx[:beff.value], w[:beff.value]
+
+    def step(self, mode: int, alpha: float = -1.0):
+        self._chk(self._L.cp_sgd_step(self._h, mode, float(alpha)))
+
+    def step_phase(self, mode: int, phase: int, alpha: float = -1.0):
+        self._chk(self._L.cp_sgd_step_phase(self._h, mode, phase, float(alpha)))
+
+    def exchange_info(self, mode: int):
+        buf, cnt, rb, re = C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int64()
+        self._chk(self._L.cp_sgd_exchange_info(self._h, mode, C.byref(buf), C.byref(cnt), C.byref(rb), C.byref(re)))
+        return buf.value, cnt.value, rb.value, re.value
+
+    def sweep(self, nsweeps: int = 1, order: str = "cyclic", alphas=None):
+        arr = None
+        if alphas is not None:
+            a = np.ascontiguousarray(alphas, dtype=np.float64)
+            assert a.size == nsweeps * self.N
+            arr = a.ctypes.data_as(C.c_void_p)
+        self._chk(self._L.cp_sgd_sweep(self._h, int(nsweeps), ORDERS[order], arr))
+
+    def steps_host(self, first_mode: int, nsteps: int, factors_host: list, alpha: float = -1.0):
+        """factors_host: list of N host tensors/arrays (pinned torch tensors recommended), updated in place."""
+        ptrs = []
+        for A in factors_host:
+            ptrs.append(A.data_ptr() if hasattr(A, "data_ptr") else A.ctypes.data)
+        arr = (C.c_void_p * self.N)(*ptrs)
+        self._chk(self._L.cp_sgd_steps_host(self._h, int(first_mode), int(nsteps), float(alpha), arr))
+
+    def fit(self) -> float:
+        out = C.c_double(0.0)
+        self._chk(self._L.cp_fit(self._h, C.byref(out)))
+        return out.value
+
+    def sync(self):
+        self._chk(self._L.cp_sgd_sync(self._h))
+
+    # -- parity / debug hooks -----------------------------------------------------------------------
+    def get_table(self, mode: int):
+        I = self.dims[mode]
+        q = np.zeros(I, dtype=np.uint64)
+        p = np.zeros(I, dtype=np.float64)
+        T = C.c_uint64(0)
+        self._chk(self._L.cp_sgd_get_table(self._h, mode, q.ctypes.data_as(C.c_void_p), C.byref(T),
+                                           p.ctypes.data_as(C.c_void_p)))
+        return q, int(T.value), p
+
+    def get_grad(self):
+        dt = np.float64 if self.dtype == 1 else np.float32
+        m = C.c_int32(-1)
+        self._chk(self._L.cp_sgd_get_grad(self._h, None, C.byref(m), None))
+        G = np.zeros((self.dims[m.value], self.R), dtype=dt)
+        Gam = np.zeros((self.R, self.R), dtype=dt)
+        self._chk(self._L.cp_sgd_get_grad(self._h, G.ctypes.data_as(C.c_void_p), C.byref(m),
+                                          Gam.ctypes.data_as(C.c_void_p)))
+        return G, m.value, Gam
+
+    def get_accum(self, mode: int):
+        dt = np.float64 if self.dtype == 1 else np.float32
+        S = np.zeros((self.dims[mode], self.R), dtype=dt)
+        self._chk(self._L.cp_sgd_get_accum(self._h, mode, S.ctypes.data_as(C.c_void_p)))
+        return S
+
+    @property
+    def iter(self) -> int:
+        r = C.c_uint64(0)
+        self._chk(self._L.cp_sgd_get_iter(self._h, C.byref(r)))
+        return int(r.value)
+
+    @iter.setter
+    def iter(self, r: int):
+        self._chk(self._L.cp_sgd_set_iter(self._h, C.c_uint64(r)))
+
+    def refresh_tables(self):
+        self._chk(self._L.cp_sgd_refresh_tables(self._h))
+
+    @property
+    def launches(self) -> int:
+        n = C.c_uint64(0)
+        self._chk(self._L.cp_sgd_get_launches(self._h, C.byref(n)))
+        return int(n.value)
+
+    def profile(self, on: bool):
+        self._chk(self._L.cp_sgd_profile(self._h, 1 if on else 0))
+
+    def profile_read(self):
+        cap = 16
+        ids = (C.c_int32 * cap)()
+        tot = (C.c_double * cap)()
+        cnt = (C.c_int64 * cap)()
+        n = C.c_int32(0)
+        self._chk(self._L.cp_sgd_profile_read(self._h, cap, ids, tot, cnt, C.byref(n)))
+        return {KERNEL_NAMES[ids[i]]: (tot[i], int(cnt[i])) for i in range(n.value)}

@@ -1,0 +1,1057 @@
+// cpsgd.cu -- host side of libcpsgd.so: the C ABI of include/cpsgd.h.
+//
+// Orchestrates the sm_100a kernels of kernels.cuh on the caller's stream: per step
+//   k_sample (a2,a3) -> k_gather (a4,a5,a6) -> [sharded: reduce + NCCL allreduce]
+//   -> k_update (a6,a7,a8; r += 1) -> [sharded last mode: NCCL row broadcasts] -> k_table (a1, a9)
+// Cyclic constant-step sweeps are captured once into a CUDA graph and replayed.
+// NCCL is resolved at run time (dlopen of the libnccl.so.2 torch already loaded), only when
+// world_size > 1 with an internal communicator.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/cpsgd.h"
+#include "kernels.cuh"
+
+using namespace cps;
+
+namespace {
+
+thread_local std::string g_init_error;
+
+// ---- minimal NCCL surface (types match nccl.h 2.x) -------------------------------------------
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+enum { kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0 };
+struct NcclApi {
+  void* dl = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string& err) {
+    if (dl) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      dl = dlopen(nm, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+      if (!dl) dl = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (dl) break;
+    }
+    if (!dl) {
+      err = "cannot dlopen libnccl.so.2";
+      return false;
+    }
+#define CPS_SYM(f, s)                                        \
+  f = reinterpret_cast<decltype(f)>(dlsym(dl, s));           \
+  if (!f) {                                                  \
+    err = std::string("NCCL symbol missing: ") + s;          \
+    return false;                                            \
+  }
+    CPS_SYM(CommInitRank, "ncclCommInitRank");
+    CPS_SYM(AllReduce, "ncclAllReduce");
+    CPS_SYM(Broadcast, "ncclBroadcast");
+    CPS_SYM(GroupStart, "ncclGroupStart");
+    CPS_SYM(GroupEnd, "ncclGroupEnd");
+    CPS_SYM(CommDestroy, "ncclCommDestroy");
+    CPS_SYM(GetErrorString, "ncclGetErrorString");
+#undef CPS_SYM
+    return true;
+  }
+};
+NcclApi g_nccl;
+
+enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kNumKernelIds };
+
+struct ProfRec {
+  int id;
+  cudaEvent_t a, b;
+};
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+struct cp_sgd_s {
+  // configuration
+  int N = 0, R = 0, dtype = 0, sampler = 0, rule = 0;
+  int64_t dims[kMaxOrder] = {}, ldims[kMaxOrder] = {}, lstride[kMaxOrder] = {};
+  int64_t lo_last = 0, hi_last = 0;
+  int64_t B = 0;
+  int32_t window[kMaxOrder][kMaxOrder] = {};  // [mode n][position]
+  int64_t bmax[kMaxOrder] = {};               // rows per step for mode n
+  double alpha = 0, eta = 0, bpar = 0, eps = 0;
+  uint64_t seed = 0;
+  cudaStream_t stream = nullptr;
+  int world_rank = 0, world_size = 1;
+  uint32_t flags = 0;
+  const void* X = nullptr;
+  void* factors[kMaxOrder] = {};
+  size_t esz = 4;
+  // layout
+  void* Xmm[kMaxOrder] = {};
+  int64_t pitch[kMaxOrder] = {};
+  // per-mode tiling of k_gather
+  int64_t In_local[kMaxOrder] = {}, row0[kMaxOrder] = {};
+  int ntiles[kMaxOrder] = {}, nchunks[kMaxOrder] = {};
+  int64_t TB[kMaxOrder] = {};
+  // workspace (device)
+  uint64_t* cdf[kMaxOrder] = {};
+  double* pprob[kMaxOrder] = {};
+  void* S[kMaxOrder] = {};
+  uint64_t* Ttot = nullptr;
+  int32_t* idx = nullptr;
+  double* w = nullptr;
+  int64_t* beff = nullptr;
+  uint64_t* iter_dev = nullptr;
+  uint64_t* iter_tmp = nullptr;
+  int* status_dev = nullptr;
+  double* alpha_dev = nullptr;
+  void* Mp = nullptr;
+  void* Gp = nullptr;
+  void* Msum = nullptr;
+  void* Gsum = nullptr;
+  void* Gout = nullptr;
+  void* Gam_out = nullptr;
+  void** fac_dev = nullptr;     // device copy of the factor pointer array (k_fit)
+  int64_t* ldims_dev = nullptr;
+  double* fit_partial = nullptr;
+  int fit_blocks = 0;
+  // host mirrors / pinned staging
+  uint64_t iter_host = 0;
+  int last_mode = -1;
+  double* pinned = nullptr;  // small pinned staging buffer (alpha, iter)
+  int sample_smem = 0;       // dynamic smem bytes of k_sample (0: read CDFs from global)
+  // graph of one cyclic sweep (constant step)
+  cudaGraphExec_t sweep_exec = nullptr;
+  // NCCL
+  ncclComm_t comm = nullptr;
+  // diagnostics
+  std::string err;
+  uint64_t launches = 0;
+  bool prof = false;
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+
+  cp_status fail(cp_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    err = buf;
+    return st;
+  }
+};
+
+namespace {
+
+#define CUDA_TRY(h, expr)                                                                        \
+  do {                                                                                           \
+    cudaError_t e_ = (expr);                                                                     \
+    if (e_ != cudaSuccess) return (h)->fail(CP_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+cp_status check_launch(cp_sgd_s* h, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return h->fail(CP_ECUDA, "%s launch: %s", what, cudaGetErrorString(e));
+  return CP_OK;
+}
+
+// profiling: event pair around one kernel of a direct-launch step
+cudaEvent_t next_event(cp_sgd_s* h) {
+  if (h->ev_next == h->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    h->ev_pool.push_back(e);
+  }
+  return h->ev_pool[h->ev_next++];
+}
+struct ProfScope {
+  cp_sgd_s* h;
+  int id;
+  cudaEvent_t b = nullptr;
+  ProfScope(cp_sgd_s* h_, int id_) : h(h_), id(id_) {
+    if (h->prof) {
+      cudaEvent_t a = next_event(h);
+      b = next_event(h);
+      cudaEventRecord(a, h->stream);
+      h->prof_recs.push_back(ProfRec{id, a, b});
+    }
+  }
+  ~ProfScope() {
+    if (h->prof) cudaEventRecord(b, h->stream);
+  }
+};
+
+int rpt_for(int R) { return R <= 8 ? 4 : R <= 16 ? 8 : R <= 32 ? 16 : 32; }
+
+// ---- kernel launchers ---------------------------------------------------------------------
+template <typename T>
+cp_status launch_table(cp_sgd_s* h, int k) {
+  if (h->sampler == CP_UNIFORM) return CP_OK;  // q = 1, T = I_k: nothing depends on the factors
+  ProfScope ps(h, kKTable);
+  const int P = h->R * (h->R + 1) / 2;
+  const int groups = std::max(1, kTableThreads / P);
+  const size_t smem = sizeof(double) * (kMaxRank * kMaxRank + std::max(kTableThreads, P * groups));
+  k_table<T><<<1, kTableThreads, smem, h->stream>>>((const T*)h->factors[k], h->dims[k], h->R, h->sampler,
+                                                    h->pprob[k], h->cdf[k], h->Ttot + k, h->status_dev);
+  h->launches++;
+  return check_launch(h, "k_table");
+}
+
+cp_status launch_table_any(cp_sgd_s* h, int k) {
+  return h->dtype == CP_F64 ? launch_table<double>(h, k) : launch_table<float>(h, k);
+}
+
+cp_status launch_sample(cp_sgd_s* h, int n, const uint64_t* iter_ptr, int32_t* idx, double* w) {
+  ProfScope ps(h, kKSample);
+  SampleParams p;
+  memset(&p, 0, sizeof p);
+  p.N = h->N;
+  p.n = n;
+  p.strategy = h->sampler;
+  p.B = h->B;
+  for (int k = 0; k < h->N; ++k) {
+    p.dims[k] = h->dims[k];
+    p.cdf[k] = h->cdf[k];
+  }
+  for (int q = 0; q < h->N - 1; ++q) p.window[q] = h->window[n][q];
+  p.Ttot = h->Ttot;
+  p.seed = h->seed;
+  p.iter = iter_ptr;
+  p.idx = idx;
+  p.w = w;
+  p.beff = h->beff;
+  p.bmax = h->bmax[n];
+  int64_t need = 0;
+  for (int k = 0; k < h->N; ++k)
+    if (k != n) need += h->dims[k];
+  size_t smem = (size_t)need * sizeof(uint64_t);
+  p.stage_smem = (h->sampler != CP_UNIFORM && smem <= (size_t)h->sample_smem) ? 1 : 0;
+  if (!p.stage_smem) smem = 0;
+  const int threads = 256;
+  const int64_t blocks = std::max<int64_t>(1, ceil_div(h->bmax[n], threads));
+  k_sample<<<(unsigned)blocks, threads, smem, h->stream>>>(p);
+  h->launches++;
+  return check_launch(h, "k_sample");
+}
+
+template <typename T, int RPT>
+cp_status launch_gather_t(cp_sgd_s* h, int n) {
+  ProfScope ps(h, kKGather);
+  GatherParams<T> p;
+  memset(&p, 0, sizeof p);
+  p.N = h->N;
+  p.n = n;
+  p.R = h->R;
+  for (int k = 0; k < h->N; ++k) {
+    p.ldims[k] = h->ldims[k];
+    p.lstride[k] = h->lstride[k];
+    p.factors[k] = (const T*)h->factors[k];
+  }
+  p.lo_last = h->lo_last;
+  if (h->Xmm[n]) {
+    p.X = (const T*)h->Xmm[n];
+    p.mode_major = 1;
+    p.pitch = h->pitch[n];
+  } else {
+    p.X = (const T*)h->X;
+    p.mode_major = 0;
+    p.pitch = 0;
+  }
+  p.idx = h->idx;
+  p.w = h->w;
+  p.beff = h->beff;
+  p.TB = h->TB[n];
+  p.In_local = h->In_local[n];
+  p.Mp = (T*)h->Mp;
+  p.Gp = (T*)h->Gp;
+  dim3 grid(h->ntiles[n], h->nchunks[n]);
+  k_gather<T, RPT><<<grid, kGatherThreads, 0, h->stream>>>(p);
+  h->launches++;
+  return check_launch(h, "k_gather");
+}
+
+template <typename T>
+cp_status launch_gather(cp_sgd_s* h, int n) {
+  switch (rpt_for(h->R)) {
+    case 4: return launch_gather_t<T, 4>(h, n);
+    case 8: return launch_gather_t<T, 8>(h, n);
+    case 16: return launch_gather_t<T, 16>(h, n);
+    default: return launch_gather_t<T, 32>(h, n);
+  }
+}
+
+template <typename T>
+cp_status launch_update(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, bool use_sum) {
+  ProfScope ps(h, kKUpdate);
+  UpdateParams<T> p;
+  memset(&p, 0, sizeof p);
+  p.R = h->R;
+  p.In_local = h->In_local[n];
+  p.row0 = h->row0[n];
+  p.nchunks = h->nchunks[n];
+  p.Mp = (const T*)h->Mp;
+  p.Gp = (const T*)h->Gp;
+  p.Msum = use_sum ? (const T*)h->Msum : nullptr;
+  p.Gsum = use_sum ? (const T*)h->Gsum : nullptr;
+  p.A = (T*)h->factors[n];
+  p.S = (T*)h->S[n];
+  p.Gout = (T*)h->Gout;
+  p.Gam_out = (T*)h->Gam_out;
+  p.rule = h->rule;
+  p.alpha = alpha;
+  p.alpha_dev = alpha_dev;
+  p.eta = h->eta;
+  p.b = h->bpar;
+  p.eps = h->eps;
+  p.iter = h->iter_dev;
+  const size_t smem = sizeof(T) * (h->R * h->R + kUR * (h->R + 1));
+  const int64_t blocks = std::max<int64_t>(1, ceil_div(h->In_local[n], kUR));
+  k_update<T><<<(unsigned)blocks, kUpdThreads, smem, h->stream>>>(p);
+  h->launches++;
+  return check_launch(h, "k_update");
+}
+
+template <typename T>
+cp_status launch_reduce(cp_sgd_s* h, int n) {
+  ProfScope ps(h, kKReduce);
+  const int64_t tot = std::max<int64_t>((int64_t)h->R * h->In_local[n], (int64_t)h->R * h->R);
+  k_reduce_partials<T><<<(unsigned)ceil_div(tot, 256), 256, 0, h->stream>>>(
+      (const T*)h->Mp, (const T*)h->Gp, h->nchunks[n], h->R, h->In_local[n], (T*)h->Msum, (T*)h->Gsum);
+  h->launches++;
+  return check_launch(h, "k_reduce_partials");
+}
+
+bool sharded(const cp_sgd_s* h) { return h->world_size > 1; }
+
+// ---- one step, by phases ------------------------------------------------------------------------
+cp_status phase0(cp_sgd_s* h, int n) {
+  cp_status st = launch_sample(h, n, h->iter_dev, h->idx, h->w);
+  if (st) return st;
+  st = h->dtype == CP_F64 ? launch_gather<double>(h, n) : launch_gather<float>(h, n);
+  if (st) return st;
+  if (sharded(h)) st = h->dtype == CP_F64 ? launch_reduce<double>(h, n) : launch_reduce<float>(h, n);
+  return st;
+}
+
+cp_status phase1(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
+  return h->dtype == CP_F64 ? launch_update<double>(h, n, alpha, alpha_dev, sharded(h))
+                            : launch_update<float>(h, n, alpha, alpha_dev, sharded(h));
+}
+
+cp_status phase2(cp_sgd_s* h, int n) { return launch_table_any(h, n); }
+
+cp_status nccl_check(cp_sgd_s* h, ncclResult_t r, const char* what) {
+  if (r != 0) return h->fail(CP_ENCCL, "%s: %s", what, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+  return CP_OK;
+}
+
+cp_status exchange_after0(cp_sgd_s* h, int n) {
+  if (!sharded(h) || (h->flags & CP_FLAG_EXTERNAL_COMM) || n == h->N - 1) return CP_OK;
+  ProfScope ps(h, kKComm);
+  const int dt = h->dtype == CP_F64 ? kNcclFloat64 : kNcclFloat32;
+  return nccl_check(h, g_nccl.AllReduce(h->Msum, h->Msum, (size_t)h->R * h->In_local[n], dt, kNcclSum, h->comm,
+                                        h->stream),
+                    "ncclAllReduce(M)");
+}
+
+// every rank broadcasts its owned rows of A^(N-1); slab ranges are exchanged at init
+cp_status exchange_after1(cp_sgd_s* h, int n, const std::vector<int64_t>& row_ranges) {
+  if (!sharded(h) || (h->flags & CP_FLAG_EXTERNAL_COMM) || n != h->N - 1) return CP_OK;
+  ProfScope ps(h, kKComm);
+  const int dt = h->dtype == CP_F64 ? kNcclFloat64 : kNcclFloat32;
+  cp_status st = nccl_check(h, g_nccl.GroupStart(), "ncclGroupStart");
+  if (st) return st;
+  for (int r = 0; r < h->world_size; ++r) {
+    const int64_t a = row_ranges[2 * r], b = row_ranges[2 * r + 1];
+    if (b <= a) continue;
+    char* base = (char*)h->factors[n] + (size_t)a * h->R * h->esz;
+    st = nccl_check(h, g_nccl.Broadcast(base, base, (size_t)(b - a) * h->R, dt, r, h->comm, h->stream),
+                    "ncclBroadcast(rows)");
+    if (st) break;
+  }
+  cp_status st2 = nccl_check(h, g_nccl.GroupEnd(), "ncclGroupEnd");
+  return st ? st : st2;
+}
+
+}  // namespace
+
+namespace {
+
+cp_status do_step(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, const std::vector<int64_t>& rr) {
+  cp_status st = phase0(h, n);
+  if (!st) st = exchange_after0(h, n);
+  if (!st) st = phase1(h, n, alpha, alpha_dev);
+  if (!st) st = exchange_after1(h, n, rr);
+  if (!st) st = phase2(h, n);
+  return st;
+}
+
+}  // namespace
+
+// =================================================================================================
+// C ABI
+// =================================================================================================
+extern "C" {
+
+const char* cp_sgd_version(void) { return "cpsgd 0.1 (sm_100a)"; }
+
+const char* cp_sgd_last_error(cp_sgd_t h) { return h ? h->err.c_str() : g_init_error.c_str(); }
+
+static cp_status init_fail(cp_sgd_s* h, cp_status st) {
+  g_init_error = h->err;
+  cp_sgd_destroy(h);
+  return st;
+}
+
+static std::vector<int64_t>* rr_store(cp_sgd_s* h, bool create) {
+  // row ranges live in a side table keyed by handle (keeps cp_sgd_s POD-like)
+  static thread_local std::vector<std::pair<cp_sgd_s*, std::vector<int64_t>*>> tab;
+  for (auto& e : tab)
+    if (e.first == h) return e.second;
+  if (!create) return nullptr;
+  auto* v = new std::vector<int64_t>();
+  tab.push_back({h, v});
+  return v;
+}
+static void rr_free(cp_sgd_s* h) {
+  auto* v = rr_store(h, false);
+  delete v;
+}
+
+cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
+  g_init_error.clear();
+  if (!cfg || !out) {
+    g_init_error = "NULL config or output";
+    return CP_EINVAL;
+  }
+  *out = nullptr;
+  cp_sgd_s* h = new (std::nothrow) cp_sgd_s();
+  if (!h) {
+    g_init_error = "host allocation failed";
+    return CP_ENOMEM;
+  }
+  // ---- validation ----
+  if (cfg->order < 3 || cfg->order > kMaxOrder) return init_fail(h, h->fail(CP_EINVAL, "order N=%d not in [3,16]", cfg->order));
+  if (!cfg->dims || !cfg->factors || !cfg->X) return init_fail(h, h->fail(CP_EINVAL, "NULL dims/factors/X"));
+  if (cfg->rank < 1 || cfg->rank > kMaxRank) return init_fail(h, h->fail(CP_EINVAL, "rank R=%d not in [1,64]", cfg->rank));
+  if (cfg->dtype != CP_F32 && cfg->dtype != CP_F64) return init_fail(h, h->fail(CP_EINVAL, "bad dtype"));
+  if (cfg->batch < 1) return init_fail(h, h->fail(CP_EINVAL, "batch B=%lld < 1", (long long)cfg->batch));
+  if (cfg->sampler < 0 || cfg->sampler > 4) return init_fail(h, h->fail(CP_EINVAL, "bad sampler"));
+  if (cfg->rule != CP_STEP_FIXED && cfg->rule != CP_STEP_ADAPTIVE) return init_fail(h, h->fail(CP_EINVAL, "bad rule"));
+  if (!(cfg->alpha >= 0.0)) return init_fail(h, h->fail(CP_EINVAL, "alpha < 0"));
+  if (cfg->rule == CP_STEP_ADAPTIVE && !(cfg->eta > 0.0)) return init_fail(h, h->fail(CP_EINVAL, "eta <= 0"));
+  if (!(cfg->b >= 0.0) || !(cfg->eps >= 0.0)) return init_fail(h, h->fail(CP_EINVAL, "b or eps < 0"));
+  if (cfg->world_size < 1 || cfg->world_rank < 0 || cfg->world_rank >= cfg->world_size)
+    return init_fail(h, h->fail(CP_EINVAL, "bad world rank/size"));
+  h->N = cfg->order;
+  h->R = cfg->rank;
+  h->dtype = cfg->dtype;
+  h->esz = cfg->dtype == CP_F64 ? 8 : 4;
+  h->sampler = cfg->sampler;
+  h->rule = cfg->rule;
+  h->B = cfg->batch;
+  h->alpha = cfg->alpha;
+  h->eta = cfg->eta;
+  h->bpar = cfg->b;
+  h->eps = cfg->eps;
+  h->seed = cfg->seed;
+  h->stream = (cudaStream_t)cfg->stream;
+  h->world_rank = cfg->world_rank;
+  h->world_size = cfg->world_size;
+  h->flags = cfg->flags;
+  h->X = cfg->X;
+  for (int k = 0; k < h->N; ++k) {
+    if (cfg->dims[k] < 1 || cfg->dims[k] > (int64_t)1 << 31)
+      return init_fail(h, h->fail(CP_EINVAL, "dims[%d]=%lld out of range", k, (long long)cfg->dims[k]));
+    if (!cfg->factors[k]) return init_fail(h, h->fail(CP_EINVAL, "factor %d is NULL", k));
+    h->dims[k] = cfg->dims[k];
+    h->factors[k] = cfg->factors[k];
+    h->ldims[k] = cfg->dims[k];
+  }
+  if (h->world_size > 1) {
+    if (cfg->slab_begin < 0 || cfg->slab_end > h->dims[h->N - 1] || cfg->slab_begin >= cfg->slab_end)
+      return init_fail(h, h->fail(CP_EINVAL, "bad slab range [%lld,%lld)", (long long)cfg->slab_begin,
+                                  (long long)cfg->slab_end));
+    h->lo_last = cfg->slab_begin;
+    h->hi_last = cfg->slab_end;
+    h->ldims[h->N - 1] = cfg->slab_end - cfg->slab_begin;
+  } else {
+    h->lo_last = 0;
+    h->hi_last = h->dims[h->N - 1];
+  }
+  int64_t st_ = 1;
+  for (int k = 0; k < h->N; ++k) {
+    h->lstride[k] = st_;
+    st_ *= h->ldims[k];
+  }
+  const int64_t local_numel = st_;
+  // ---- block windows and per-mode batch sizes (R6) ----
+  const bool block = (h->sampler == CP_BLOCK_LEVERAGE || h->sampler == CP_BLOCK_EUCLIDEAN);
+  for (int n = 0; n < h->N; ++n) {
+    int pos = 0;
+    int64_t rem = h->B, prod = 1;
+    for (int k = 0; k < h->N; ++k) {
+      if (k == n) continue;
+      int64_t bk;
+      if (cfg->block_window) {
+        bk = cfg->block_window[pos];
+        if (bk < 1) return init_fail(h, h->fail(CP_EINVAL, "block_window[%d] < 1", pos));
+      } else {
+        const int left = h->N - 1 - pos;
+        int64_t d = 1;
+        for (d = 1; d <= rem; ++d) {
+          if (rem % d) continue;
+          double pw = 1.0;
+          for (int t = 0; t < left; ++t) pw *= (double)d;
+          if (pw >= (double)rem) break;
+        }
+        if (d > rem) d = rem;
+        rem /= d;
+        bk = d;
+      }
+      bk = std::min<int64_t>(bk, h->dims[k]);
+      h->window[n][pos] = (int32_t)bk;
+      prod *= bk;
+      ++pos;
+    }
+    h->bmax[n] = block ? prod : h->B;
+  }
+  // ---- tiling of k_gather per mode ----
+  int64_t Bmax_all = 0, Mp_elems = 0, Gp_elems = 0, Imax = 0, Msum_elems = 0;
+  for (int n = 0; n < h->N; ++n) {
+    const bool last = (n == h->N - 1);
+    h->In_local[n] = last ? h->ldims[n] : h->dims[n];
+    h->row0[n] = last ? h->lo_last : 0;
+    h->ntiles[n] = (int)ceil_div(h->In_local[n], kTI);
+    const int64_t bm = h->bmax[n];
+    int64_t nch = std::max<int64_t>(1, 296 / h->ntiles[n]);
+    nch = std::min<int64_t>(nch, ceil_div(bm, 16));
+    nch = std::max<int64_t>(nch, 1);
+    h->TB[n] = ceil_div(bm, nch);
+    h->nchunks[n] = (int)ceil_div(bm, h->TB[n]);
+    Bmax_all = std::max(Bmax_all, bm);
+    Mp_elems = std::max(Mp_elems, (int64_t)h->nchunks[n] * h->R * h->In_local[n]);
+    Gp_elems = std::max(Gp_elems, (int64_t)h->nchunks[n] * h->R * h->R);
+    Msum_elems = std::max(Msum_elems, (int64_t)h->R * h->In_local[n]);
+    Imax = std::max(Imax, h->dims[n]);
+  }
+  // ---- allocations ----
+#define ALLOC(ptr, bytes)                                                                        \
+  do {                                                                                           \
+    cudaError_t e_ = cudaMalloc((void**)&(ptr), (bytes));                                        \
+    if (e_ != cudaSuccess)                                                                       \
+      return init_fail(h, h->fail(CP_ENOMEM, "cudaMalloc(%zu): %s", (size_t)(bytes), cudaGetErrorString(e_))); \
+  } while (0)
+  for (int k = 0; k < h->N; ++k) {
+    ALLOC(h->cdf[k], sizeof(uint64_t) * h->dims[k]);
+    ALLOC(h->pprob[k], sizeof(double) * h->dims[k]);
+    if (h->rule == CP_STEP_ADAPTIVE) {
+      ALLOC(h->S[k], h->esz * h->dims[k] * h->R);
+      cudaMemsetAsync(h->S[k], 0, h->esz * h->dims[k] * h->R, h->stream);
+    }
+  }
+  ALLOC(h->Ttot, sizeof(uint64_t) * h->N);
+  ALLOC(h->idx, sizeof(int32_t) * Bmax_all * (h->N - 1));
+  ALLOC(h->w, sizeof(double) * Bmax_all);
+  ALLOC(h->beff, sizeof(int64_t));
+  ALLOC(h->iter_dev, sizeof(uint64_t));
+  ALLOC(h->iter_tmp, sizeof(uint64_t));
+  ALLOC(h->status_dev, sizeof(int));
+  ALLOC(h->alpha_dev, sizeof(double));
+  ALLOC(h->Mp, h->esz * Mp_elems);
+  ALLOC(h->Gp, h->esz * Gp_elems);
+  ALLOC(h->Msum, h->esz * Msum_elems);
+  ALLOC(h->Gsum, h->esz * h->R * h->R);
+  ALLOC(h->Gout, h->esz * Imax * h->R);
+  ALLOC(h->Gam_out, h->esz * h->R * h->R);
+  ALLOC(h->fac_dev, sizeof(void*) * h->N);
+  ALLOC(h->ldims_dev, sizeof(int64_t) * h->N);
+  h->fit_blocks = 148 * 4;
+  ALLOC(h->fit_partial, sizeof(double) * 2 * h->fit_blocks);
+  if (cudaMallocHost((void**)&h->pinned, 64) != cudaSuccess)
+    return init_fail(h, h->fail(CP_ENOMEM, "cudaMallocHost failed"));
+  cudaMemsetAsync(h->iter_dev, 0, sizeof(uint64_t), h->stream);
+  cudaMemsetAsync(h->status_dev, 0, sizeof(int), h->stream);
+  cudaMemsetAsync(h->Gout, 0, h->esz * Imax * h->R, h->stream);
+  cudaMemsetAsync(h->beff, 0, sizeof(int64_t), h->stream);
+  cudaMemcpyAsync(h->fac_dev, h->factors, sizeof(void*) * h->N, cudaMemcpyHostToDevice, h->stream);
+  cudaMemcpyAsync(h->ldims_dev, h->ldims, sizeof(int64_t) * h->N, cudaMemcpyHostToDevice, h->stream);
+  // uniform tables are constant: q = 1, cdf[i] = i + 1, T = I (materialised for get_table)
+  {
+    std::vector<uint64_t> hc;
+    std::vector<uint64_t> Th(h->N);
+    for (int k = 0; k < h->N; ++k) Th[k] = (uint64_t)h->dims[k];
+    if (h->sampler == CP_UNIFORM) {
+      for (int k = 0; k < h->N; ++k) {
+        hc.resize(h->dims[k]);
+        std::vector<double> hp(h->dims[k], 1.0 / (double)h->dims[k]);
+        for (int64_t i = 0; i < h->dims[k]; ++i) hc[i] = (uint64_t)(i + 1);
+        cudaMemcpy(h->cdf[k], hc.data(), sizeof(uint64_t) * h->dims[k], cudaMemcpyHostToDevice);
+        cudaMemcpy(h->pprob[k], hp.data(), sizeof(double) * h->dims[k], cudaMemcpyHostToDevice);
+      }
+      cudaMemcpy(h->Ttot, Th.data(), sizeof(uint64_t) * h->N, cudaMemcpyHostToDevice);
+    }
+  }
+  // ---- kernel attributes ----
+  {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    h->sample_smem = std::min(optin, 200 * 1024);
+    cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sample_smem);
+    const int tbl = (int)(sizeof(double) * (kMaxRank * kMaxRank + 2080));
+    cudaFuncSetAttribute(k_table<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, tbl);
+    cudaFuncSetAttribute(k_table<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, tbl);
+    cudaGetLastError();
+  }
+  // ---- optional mode-major copies (n >= 1; mode 0 fibers are already contiguous) ----
+  if (h->flags & CP_FLAG_MODE_MAJOR) {
+    for (int n = 1; n < h->N; ++n) {
+      const int64_t In = h->ldims[n];
+      int64_t inner = 1, outer = 1;
+      for (int k = 0; k < n; ++k) inner *= h->ldims[k];
+      for (int k = n + 1; k < h->N; ++k) outer *= h->ldims[k];
+      const int64_t align = 16 / (int64_t)h->esz;
+      h->pitch[n] = ceil_div(In, align) * align;
+      ALLOC(h->Xmm[n], h->esz * h->pitch[n] * inner * outer);
+      dim3 tb(32, 8);
+      dim3 grid((unsigned)ceil_div(inner, 32), (unsigned)ceil_div(In, 32), (unsigned)std::min<int64_t>(outer, 65535));
+      if (h->dtype == CP_F64)
+        k_transpose<double><<<grid, tb, 0, h->stream>>>((const double*)h->X, (double*)h->Xmm[n], In, inner, outer,
+                                                        h->pitch[n]);
+      else
+        k_transpose<float><<<grid, tb, 0, h->stream>>>((const float*)h->X, (float*)h->Xmm[n], In, inner, outer,
+                                                       h->pitch[n]);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return init_fail(h, h->fail(CP_ECUDA, "k_transpose: %s", cudaGetErrorString(e)));
+    }
+  }
+#undef ALLOC
+  // ---- NCCL communicator ----
+  if (h->world_size > 1) {
+    auto* rr = rr_store(h, true);
+    rr->assign(2 * h->world_size, 0);
+    if (!(h->flags & CP_FLAG_EXTERNAL_COMM)) {
+      if (!cfg->nccl_unique_id) return init_fail(h, h->fail(CP_EINVAL, "world_size > 1 needs nccl_unique_id"));
+      std::string e;
+      if (!g_nccl.load(e)) return init_fail(h, h->fail(CP_ENCCL, "%s", e.c_str()));
+      ncclUniqueId id;
+      memcpy(&id, cfg->nccl_unique_id, sizeof id);
+      ncclResult_t r = g_nccl.CommInitRank(&h->comm, h->world_size, id, h->world_rank);
+      if (r != 0) return init_fail(h, h->fail(CP_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)));
+      // exchange the slab ranges (allreduce of a one-hot vector)
+      int64_t* d_rr = nullptr;
+      if (cudaMalloc((void**)&d_rr, sizeof(int64_t) * 2 * h->world_size) != cudaSuccess)
+        return init_fail(h, h->fail(CP_ENOMEM, "cudaMalloc(rr)"));
+      std::vector<double> one(2 * h->world_size, 0.0);
+      one[2 * h->world_rank] = (double)h->lo_last;
+      one[2 * h->world_rank + 1] = (double)h->hi_last;
+      double* d_one = nullptr;
+      cudaMalloc((void**)&d_one, sizeof(double) * one.size());
+      cudaMemcpy(d_one, one.data(), sizeof(double) * one.size(), cudaMemcpyHostToDevice);
+      r = g_nccl.AllReduce(d_one, d_one, one.size(), kNcclFloat64, kNcclSum, h->comm, h->stream);
+      cudaStreamSynchronize(h->stream);
+      cudaMemcpy(one.data(), d_one, sizeof(double) * one.size(), cudaMemcpyDeviceToHost);
+      cudaFree(d_one);
+      cudaFree(d_rr);
+      if (r != 0) return init_fail(h, h->fail(CP_ENCCL, "slab exchange: %s", g_nccl.GetErrorString(r)));
+      for (size_t i = 0; i < one.size(); ++i) (*rr)[i] = (int64_t)one[i];
+    }
+  }
+  // ---- initial tables of every mode ----
+  for (int k = 0; k < h->N; ++k) {
+    cp_status st = launch_table_any(h, k);
+    if (st) return init_fail(h, st);
+  }
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess)
+    return init_fail(h, h->fail(CP_ECUDA, "init: %s", cudaGetErrorString(cudaGetLastError())));
+  int status = 0;
+  cudaMemcpy(&status, h->status_dev, sizeof(int), cudaMemcpyDeviceToHost);
+  if (status != 0) return init_fail(h, h->fail((cp_status)status, "initial table build failed (status %d)", status));
+  *out = h;
+  return CP_OK;
+}
+
+cp_status cp_sgd_destroy(cp_sgd_t h) {
+  if (!h) return CP_OK;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->sweep_exec) cudaGraphExecDestroy(h->sweep_exec);
+  for (int k = 0; k < kMaxOrder; ++k) {
+    cudaFree(h->cdf[k]);
+    cudaFree(h->pprob[k]);
+    cudaFree(h->S[k]);
+    cudaFree(h->Xmm[k]);
+  }
+  cudaFree(h->Ttot);
+  cudaFree(h->idx);
+  cudaFree(h->w);
+  cudaFree(h->beff);
+  cudaFree(h->iter_dev);
+  cudaFree(h->iter_tmp);
+  cudaFree(h->status_dev);
+  cudaFree(h->alpha_dev);
+  cudaFree(h->Mp);
+  cudaFree(h->Gp);
+  cudaFree(h->Msum);
+  cudaFree(h->Gsum);
+  cudaFree(h->Gout);
+  cudaFree(h->Gam_out);
+  cudaFree(h->fac_dev);
+  cudaFree(h->ldims_dev);
+  cudaFree(h->fit_partial);
+  if (h->pinned) cudaFreeHost(h->pinned);
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
+  if (h->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm);
+  rr_free(h);
+  cudaGetLastError();
+  delete h;
+  return CP_OK;
+}
+
+static cp_status check_mode(cp_sgd_t h, int mode) {
+  if (!h) return CP_EINVAL;
+  if (mode < 0 || mode >= h->N) return h->fail(CP_ERANGE, "mode %d out of range", mode);
+  return CP_OK;
+}
+
+cp_status cp_sgd_sync(cp_sgd_t h) {
+  if (!h) return CP_EINVAL;
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return h->fail(CP_ECUDA, "stream: %s", cudaGetErrorString(e));
+  int status = 0;
+  CUDA_TRY(h, cudaMemcpy(&status, h->status_dev, sizeof(int), cudaMemcpyDeviceToHost));
+  if (status != 0) {
+    cudaMemsetAsync(h->status_dev, 0, sizeof(int), h->stream);
+    return h->fail((cp_status)status, "device reported status %d (%s)", status,
+                   status == CP_ENONFINITE ? "non-finite factor in a table rebuild" : "degenerate distribution");
+  }
+  return CP_OK;
+}
+
+cp_status cp_sgd_batch_max(cp_sgd_t h, int32_t mode, int64_t* bmax_host) {
+  cp_status st = check_mode(h, mode);
+  if (st) return st;
+  if (!bmax_host) return h->fail(CP_EINVAL, "NULL output");
+  *bmax_host = h->bmax[mode];
+  return CP_OK;
+}
+
+cp_status cp_sgd_sample(cp_sgd_t h, int32_t mode, uint64_t iter, int32_t* idx_dev, double* w_dev,
+                        int64_t* batch_eff_host) {
+  cp_status st = check_mode(h, mode);
+  if (st) return st;
+  if (!idx_dev || !w_dev) return h->fail(CP_EINVAL, "NULL output buffer");
+  uint64_t* pin = (uint64_t*)h->pinned;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));  // pinned staging reuse
+  pin[0] = iter;
+  CUDA_TRY(h, cudaMemcpyAsync(h->iter_tmp, pin, sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream));
+  st = launch_sample(h, mode, h->iter_tmp, idx_dev, w_dev);
+  if (st) return st;
+  if (batch_eff_host) {
+    CUDA_TRY(h, cudaMemcpyAsync(pin + 1, h->beff, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    *batch_eff_host = (int64_t)pin[1];
+  }
+  return CP_OK;
+}
+
+static cp_status step_direct(cp_sgd_t h, int n, double alpha) {
+  const double a = (alpha < 0.0) ? h->alpha : alpha;
+  auto* rr = rr_store(h, false);
+  static const std::vector<int64_t> none;
+  cp_status st = do_step(h, n, a, nullptr, rr ? *rr : none);
+  if (st) return st;
+  h->iter_host++;
+  h->last_mode = n;
+  return CP_OK;
+}
+
+cp_status cp_sgd_step(cp_sgd_t h, int32_t mode, double alpha) {
+  cp_status st = check_mode(h, mode);
+  if (st) return st;
+  if (sharded(h) && (h->flags & CP_FLAG_EXTERNAL_COMM))
+    return h->fail(CP_ESTATE, "external-comm handles must use cp_sgd_step_phase");
+  return step_direct(h, mode, alpha);
+}
+
+cp_status cp_sgd_step_phase(cp_sgd_t h, int32_t mode, int32_t phase, double alpha) {
+  cp_status st = check_mode(h, mode);
+  if (st) return st;
+  const double a = (alpha < 0.0) ? h->alpha : alpha;
+  if (phase == 0) {
+    st = phase0(h, mode);
+    if (!st && sharded(h) && !(h->flags & CP_FLAG_EXTERNAL_COMM)) st = exchange_after0(h, mode);
+    return st;
+  }
+  if (phase == 1) {
+    st = phase1(h, mode, a, nullptr);
+    if (!st && sharded(h) && !(h->flags & CP_FLAG_EXTERNAL_COMM)) {
+      auto* rr = rr_store(h, false);
+      static const std::vector<int64_t> none;
+      st = exchange_after1(h, mode, rr ? *rr : none);
+    }
+    return st;
+  }
+  if (phase == 2) {
+    st = phase2(h, mode);
+    if (!st) {
+      h->iter_host++;
+      h->last_mode = mode;
+    }
+    return st;
+  }
+  return h->fail(CP_EINVAL, "phase %d not in {0,1,2}", phase);
+}
+
+cp_status cp_sgd_exchange_info(cp_sgd_t h, int32_t mode, void** buf_dev, int64_t* count, int64_t* row_begin,
+                               int64_t* row_end) {
+  cp_status st = check_mode(h, mode);
+  if (st) return st;
+  if (buf_dev) *buf_dev = (mode == h->N - 1 && sharded(h)) ? nullptr : h->Msum;
+  if (count) *count = (mode == h->N - 1 && sharded(h)) ? 0 : (int64_t)h->R * h->In_local[mode];
+  if (row_begin) *row_begin = h->row0[mode];
+  if (row_end) *row_end = h->row0[mode] + h->In_local[mode];
+  return CP_OK;
+}
+
+cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double* alpha_per_iter) {
+  if (!h) return CP_EINVAL;
+  if (nsweeps < 0) return h->fail(CP_EINVAL, "nsweeps < 0");
+  if (order != CP_ORDER_CYCLIC && order != CP_ORDER_RANDOM) return h->fail(CP_EINVAL, "bad order");
+  if (sharded(h) && (h->flags & CP_FLAG_EXTERNAL_COMM))
+    return h->fail(CP_ESTATE, "external-comm handles must use cp_sgd_step_phase");
+  const bool use_graph = order == CP_ORDER_CYCLIC && !alpha_per_iter && !(h->flags & CP_FLAG_NO_GRAPH) && !h->prof;
+  if (!use_graph) {
+    for (int s = 0; s < nsweeps; ++s)
+      for (int j = 0; j < h->N; ++j) {
+        const int n = (order == CP_ORDER_CYCLIC) ? j : random_mode(h->seed, h->iter_host, h->N);
+        const double a = alpha_per_iter ? alpha_per_iter[(int64_t)s * h->N + j] : h->alpha;
+        cp_status st = step_direct(h, n, a);
+        if (st) return st;
+      }
+    return CP_OK;
+  }
+  // graph path: the step size is read from alpha_dev; r lives on the device
+  double* pin = h->pinned;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  pin[4] = h->alpha;
+  CUDA_TRY(h, cudaMemcpyAsync(h->alpha_dev, pin + 4, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  if (!h->sweep_exec) {
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    auto* rr = rr_store(h, false);
+    static const std::vector<int64_t> none;
+    cp_status st = CP_OK;
+    const uint64_t l0 = h->launches;
+    for (int n = 0; n < h->N && !st; ++n) st = do_step(h, n, h->alpha, h->alpha_dev, rr ? *rr : none);
+    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    h->launches = l0;
+    if (st) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (e != cudaSuccess) return h->fail(CP_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&h->sweep_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return h->fail(CP_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  }
+  // kernels per sweep (counted once per replay)
+  uint64_t per_sweep = 0;
+  for (int n = 0; n < h->N; ++n) {
+    per_sweep += 3 + (h->sampler != CP_UNIFORM ? 1 : 0) + (sharded(h) ? 1 : 0);
+  }
+  for (int s = 0; s < nsweeps; ++s) {
+    CUDA_TRY(h, cudaGraphLaunch(h->sweep_exec, h->stream));
+    h->launches += per_sweep;
+    h->iter_host += h->N;
+  }
+  if (nsweeps > 0) h->last_mode = h->N - 1;
+  return CP_OK;
+}
+
+cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, double alpha,
+                            void* const* factors_host) {
+  cp_status st = check_mode(h, first_mode);
+  if (st) return st;
+  if (!factors_host) return h->fail(CP_EINVAL, "NULL factors_host");
+  for (int k = 0; k < h->N; ++k)
+    CUDA_TRY(h, cudaMemcpyAsync(h->factors[k], factors_host[k], h->esz * h->dims[k] * h->R, cudaMemcpyHostToDevice,
+                                h->stream));
+  // the host factors may differ from the device ones: rebuild every table first
+  for (int k = 0; k < h->N; ++k) {
+    st = launch_table_any(h, k);
+    if (st) return st;
+  }
+  for (int s = 0; s < nsteps; ++s) {
+    st = cp_sgd_step(h, (first_mode + s) % h->N, alpha);
+    if (st) return st;
+  }
+  for (int k = 0; k < h->N; ++k)
+    CUDA_TRY(h, cudaMemcpyAsync(factors_host[k], h->factors[k], h->esz * h->dims[k] * h->R, cudaMemcpyDeviceToHost,
+                                h->stream));
+  return cp_sgd_sync(h);
+}
+
+cp_status cp_fit(cp_sgd_t h, double* fit_host) {
+  if (!h || !fit_host) return CP_EINVAL;
+  int64_t nfib = 1;
+  for (int k = 1; k < h->N; ++k) nfib *= h->ldims[k];
+  const int blocks = (int)std::min<int64_t>(h->fit_blocks, nfib);
+  {
+    ProfScope ps(h, kKFit);
+    if (h->dtype == CP_F64)
+      k_fit<double><<<blocks, 256, 0, h->stream>>>((const double*)h->X, h->N, h->ldims_dev, h->lo_last, h->R,
+                                                   (const double* const*)h->fac_dev, nfib, h->fit_partial);
+    else
+      k_fit<float><<<blocks, 256, 0, h->stream>>>((const float*)h->X, h->N, h->ldims_dev, h->lo_last, h->R,
+                                                  (const float* const*)h->fac_dev, nfib, h->fit_partial);
+    h->launches++;
+  }
+  cp_status st = check_launch(h, "k_fit");
+  if (st) return st;
+  if (sharded(h) && !(h->flags & CP_FLAG_EXTERNAL_COMM)) {
+    // sum the per-block partials of all ranks (same layout on every rank)
+    st = nccl_check(h, g_nccl.AllReduce(h->fit_partial, h->fit_partial, 2 * (size_t)blocks, kNcclFloat64, kNcclSum,
+                                        h->comm, h->stream),
+                    "ncclAllReduce(fit)");
+    if (st) return st;
+  }
+  std::vector<double> part(2 * blocks);
+  CUDA_TRY(h, cudaMemcpyAsync(part.data(), h->fit_partial, sizeof(double) * 2 * blocks, cudaMemcpyDeviceToHost,
+                              h->stream));
+  st = cp_sgd_sync(h);
+  if (st) return st;
+  double res = 0.0, xx = 0.0;
+  for (int b = 0; b < blocks; ++b) {
+    res += part[2 * b];
+    xx += part[2 * b + 1];
+  }
+  if (!(xx > 0.0)) return h->fail(CP_EDEGENERATE, "||X|| = 0");
+  *fit_host = 1.0 - std::sqrt(res) / std::sqrt(xx);
+  return CP_OK;
+}
+
+cp_status cp_sgd_get_table(cp_sgd_t h, int32_t mode, uint64_t* q_host, uint64_t* T_host, double* p_host) {
+  cp_status st = check_mode(h, mode);
+  if (st) return st;
+  st = cp_sgd_sync(h);
+  if (st) return st;
+  const int64_t I = h->dims[mode];
+  if (q_host) {
+    std::vector<uint64_t> c(I);
+    CUDA_TRY(h, cudaMemcpy(c.data(), h->cdf[mode], sizeof(uint64_t) * I, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < I; ++i) q_host[i] = c[i] - (i ? c[i - 1] : 0);
+  }
+  if (T_host) CUDA_TRY(h, cudaMemcpy(T_host, h->Ttot + mode, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (p_host) CUDA_TRY(h, cudaMemcpy(p_host, h->pprob[mode], sizeof(double) * I, cudaMemcpyDeviceToHost));
+  return CP_OK;
+}
+
+cp_status cp_sgd_get_grad(cp_sgd_t h, void* G_host, int32_t* mode_host, void* Gamma_host) {
+  if (!h) return CP_EINVAL;
+  cp_status st = cp_sgd_sync(h);
+  if (st) return st;
+  if (h->last_mode < 0) return h->fail(CP_ESTATE, "no step taken yet");
+  if (mode_host) *mode_host = h->last_mode;
+  if (G_host)
+    CUDA_TRY(h, cudaMemcpy(G_host, h->Gout, h->esz * h->dims[h->last_mode] * h->R, cudaMemcpyDeviceToHost));
+  if (Gamma_host) CUDA_TRY(h, cudaMemcpy(Gamma_host, h->Gam_out, h->esz * h->R * h->R, cudaMemcpyDeviceToHost));
+  return CP_OK;
+}
+
+cp_status cp_sgd_get_accum(cp_sgd_t h, int32_t mode, void* S_host) {
+  cp_status st = check_mode(h, mode);
+  if (st) return st;
+  if (!h->S[mode]) return h->fail(CP_ESTATE, "fixed rule has no accumulator");
+  st = cp_sgd_sync(h);
+  if (st) return st;
+  CUDA_TRY(h, cudaMemcpy(S_host, h->S[mode], h->esz * h->dims[mode] * h->R, cudaMemcpyDeviceToHost));
+  return CP_OK;
+}
+
+cp_status cp_sgd_get_iter(cp_sgd_t h, uint64_t* r_host) {
+  if (!h || !r_host) return CP_EINVAL;
+  cp_status st = cp_sgd_sync(h);
+  if (st) return st;
+  CUDA_TRY(h, cudaMemcpy(r_host, h->iter_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return CP_OK;
+}
+
+cp_status cp_sgd_set_iter(cp_sgd_t h, uint64_t r) {
+  if (!h) return CP_EINVAL;
+  cp_status st = cp_sgd_sync(h);
+  if (st) return st;
+  CUDA_TRY(h, cudaMemcpy(h->iter_dev, &r, sizeof(uint64_t), cudaMemcpyHostToDevice));
+  h->iter_host = r;
+  return CP_OK;
+}
+
+cp_status cp_sgd_refresh_tables(cp_sgd_t h) {
+  if (!h) return CP_EINVAL;
+  for (int k = 0; k < h->N; ++k) {
+    cp_status st = launch_table_any(h, k);
+    if (st) return st;
+  }
+  return cp_sgd_sync(h);
+}
+
+cp_status cp_sgd_get_launches(cp_sgd_t h, uint64_t* n_host) {
+  if (!h || !n_host) return CP_EINVAL;
+  *n_host = h->launches;
+  return CP_OK;
+}
+
+cp_status cp_sgd_profile(cp_sgd_t h, int32_t on) {
+  if (!h) return CP_EINVAL;
+  if (on) {
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    h->prof_recs.clear();
+    h->ev_next = 0;
+  }
+  h->prof = on != 0;
+  return CP_OK;
+}
+
+cp_status cp_sgd_profile_read(cp_sgd_t h, int32_t cap, int32_t* ids, double* total_ms, int64_t* counts,
+                              int32_t* n_out) {
+  if (!h) return CP_EINVAL;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  double tot[kNumKernelIds] = {};
+  int64_t cnt[kNumKernelIds] = {};
+  for (auto& r : h->prof_recs) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      tot[r.id] += ms;
+      cnt[r.id]++;
+    }
+  }
+  int m = 0;
+  for (int k = 0; k < kNumKernelIds && m < cap; ++k) {
+    if (!cnt[k]) continue;
+    ids[m] = k;
+    total_ms[m] = tot[k];
+    counts[m] = cnt[k];
+    ++m;
+  }
+  if (n_out) *n_out = m;
+  cudaGetLastError();
+  return CP_OK;
+}
+
+}  // extern "C"

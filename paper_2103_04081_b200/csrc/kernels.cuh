@@ -1,0 +1,707 @@
+// kernels.cuh -- sm_100a kernels of the sampled SGD step (arXiv 2103.04081, BrawsCPD/AdawsCPD).
+//
+//   k_table    (a1)  per-mode importance table: fp64 Gram -> pivoted Cholesky -> leverage, or
+//                    row norms (Euclidean), or uniform; fixed-point quantisation; integer scan
+//   k_sample   (a2,a3) Philox draws -> upper_bound on the integer CDF (staged in shared memory)
+//                    -> idx and the exact fp64 weights omega
+//   k_gather   (a4,a5,a6) SKR rows (Alg. 1) x fiber gather (Alg. 5) -> per-chunk partial
+//                    M = X_F diag(omega) Z_F and Gamma = Z_F^T diag(omega) Z_F
+//   k_update   (a6,a7,a8) deterministic chunk reduction, G = A Gamma - M, fixed / adaptive update
+//   k_fit             fit = 1 - ||X - [[A]]|| / ||X|| (per-block fp64 partials)
+//   k_transpose       mode-major copies X_(n)^T (layout option)
+//
+// Citations: PAPER.md:<lines> (<label>); R<k> = DESIGN.md readings.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "philox.cuh"
+
+namespace cps {
+
+constexpr int kMaxOrder = 16;
+constexpr int kMaxRank = 64;
+
+// ------------------------------------------------------------------------------------------
+// Parameters (passed by value; < 1 KB)
+// ------------------------------------------------------------------------------------------
+struct SampleParams {
+  int N, n, strategy;
+  int64_t B;                       // nominal batch
+  int64_t dims[kMaxOrder];         // global dims
+  int32_t window[kMaxOrder];       // per remaining position (block strategies), clamped to I_k
+  const uint64_t* cdf[kMaxOrder];  // inclusive CDF per mode (device)
+  const uint64_t* Ttot;            // [N] totals (device)
+  uint64_t seed;
+  const uint64_t* iter;            // device pointer to the iteration counter r
+  int32_t* idx;                    // out [B_max][N-1]
+  double* w;                       // out [B_max]
+  int64_t* beff;                   // out (device scalar)
+  int64_t bmax;                    // rows the launch covers
+  int stage_smem;                  // stage the CDFs of the N-1 sampled modes in shared memory
+};
+
+template <typename T>
+struct GatherParams {
+  int N, n, R;
+  int64_t ldims[kMaxOrder];    // local dims (last mode = slab length when sharded)
+  int64_t lstride[kMaxOrder];  // first-index-fastest strides of the local tensor
+  int64_t lo_last;             // slab begin on the last mode (0 if not sharded)
+  const T* X;                  // native local tensor, or the mode-major copy of mode n
+  int mode_major;              // 1: X is [J_n_local][pitch] (fiber-contiguous)
+  int64_t pitch;               // row pitch of the mode-major copy (elements)
+  const T* factors[kMaxOrder];
+  const int32_t* idx;          // [B_max][N-1]
+  const double* w;             // [B_max]
+  const int64_t* beff;         // device scalar
+  int64_t TB;                  // fibers per chunk
+  int64_t In_local;            // rows of M handled (local slab rows for the last mode)
+  T* Mp;                       // out [chunks][R][In_local]
+  T* Gp;                       // out [chunks][R][R]
+};
+
+template <typename T>
+struct UpdateParams {
+  int R;
+  int64_t In_local;   // rows handled
+  int64_t row0;       // global row of local row 0 (slab begin for the sharded mode)
+  int nchunks;
+  const T* Mp;        // [chunks][R][In_local] partials, or NULL when Msum is given
+  const T* Gp;        // [chunks][R][R]
+  const T* Msum;      // [R][In_local] reduced M (sharded path), or NULL
+  const T* Gsum;      // [R][R] reduced Gamma, or NULL
+  T* A;               // factor A^(n), row-major I_n x R (global rows)
+  T* S;               // adaptive accumulator (same layout), NULL for the fixed rule
+  T* Gout;            // last gradient (debug), row-major I_n x R (global rows)
+  T* Gam_out;         // reduced Gamma (debug), R x R
+  int rule;
+  double alpha;       // fixed step (used when alpha_dev == NULL)
+  const double* alpha_dev;
+  double eta, b, eps;
+  uint64_t* iter;     // incremented once per step (block 0), or NULL
+};
+
+// ------------------------------------------------------------------------------------------
+// small helpers
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ int64_t upper_bound_u64(const uint64_t* __restrict__ cdf, int64_t n, uint64_t r) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (cdf[mid] <= r) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;  // #{i : cdf[i] <= r}
+}
+
+template <typename T>
+__device__ __forceinline__ T ldg(const T* p) {
+  return __ldg(p);
+}
+
+// ==========================================================================================
+// (a1) importance table of one mode -- single CTA of 1024 threads.
+//   leverage : l_i = ||L^{-1} a_{i,piv}||^2 with A_piv^T A_piv = L L^T (pivoted Cholesky of the
+//              fp64 Gram; Def. 2.3), p_i = l_i / rank (R4)
+//   euclidean: p_i = ||A(i,:)||^2 / ||A||_F^2 (Def. 2.5)
+//   uniform  : q_i = 1
+//   q_i = p_i > 0 ? max(1, rint(p_i 2^32)) : 0; cdf = inclusive integer scan; T = cdf[I-1]
+// status: 0 ok, -3 degenerate (T = 0), -8 non-finite.
+// ==========================================================================================
+constexpr int kTableThreads = 1024;
+
+template <typename T>
+__global__ void __launch_bounds__(kTableThreads) k_table(const T* __restrict__ A, int64_t I, int R, int strategy,
+                                                         double* __restrict__ p_out, uint64_t* __restrict__ cdf,
+                                                         uint64_t* __restrict__ Tout, int* __restrict__ status) {
+  extern __shared__ double sm[];
+  double* Gm = sm;                              // R x R
+  double* red = Gm + kMaxRank * kMaxRank;       // max(kTableThreads, R(R+1)/2 * groups) scratch
+  __shared__ int piv[kMaxRank];
+  __shared__ int s_rank, s_stop, s_bad;
+  __shared__ unsigned long long warp_tot[32];
+  __shared__ double s_fro;
+  const int tid = threadIdx.x;
+  const bool lev = (strategy == 1 || strategy == 3);
+  const bool euc = (strategy == 2 || strategy == 4);
+  if (tid == 0) { s_bad = 0; s_rank = R; }
+
+  if (lev) {
+    // Gram in fp64: pairs (r1 <= r2); rows split over `groups` thread groups when the pairs
+    // leave threads idle; partial sums reduced in a fixed order (deterministic).
+    const int P = R * (R + 1) / 2;
+    const int groups = max(1, kTableThreads / P);
+    for (int e = tid; e < P * groups; e += kTableThreads) {
+      const int pair = e % P, g = e / P;
+      int r1 = 0, rem = pair;
+      while (rem >= R - r1) { rem -= R - r1; ++r1; }
+      const int r2 = r1 + rem;
+      double s = 0.0;
+      for (int64_t i = g; i < I; i += groups) s += (double)A[i * R + r1] * (double)A[i * R + r2];
+      red[e] = s;
+    }
+    __syncthreads();
+    for (int pair = tid; pair < P; pair += kTableThreads) {
+      double s = 0.0;
+      for (int g = 0; g < groups; ++g) s += red[g * P + pair];
+      int r1 = 0, rem = pair;
+      while (rem >= R - r1) { rem -= R - r1; ++r1; }
+      const int r2 = r1 + rem;
+      Gm[r1 * R + r2] = s;
+      Gm[r2 * R + r1] = s;
+    }
+    __syncthreads();
+    // pivoted Cholesky, right-looking, full symmetric storage; tolerance R4(b):
+    // stop when the largest remaining Schur diagonal <= max(I,R) * eps * d0.
+    if (tid < R) piv[tid] = tid;
+    if (tid == 0) {
+      double d0 = 0.0;
+      for (int j = 0; j < R; ++j) d0 = fmax(d0, Gm[j * R + j]);
+      red[0] = d0;
+      s_stop = 0;
+      if (!(d0 == d0) || d0 > 1.7e308) s_bad = 8;
+    }
+    __syncthreads();
+    const double tol = (double)(I > R ? I : R) * 2.220446049250313e-16 * red[0];
+    int k = 0;
+    for (; k < R; ++k) {
+      if (tid == 0) {
+        int jm = k;
+        double dm = Gm[k * R + k];
+        for (int j = k + 1; j < R; ++j)
+          if (Gm[j * R + j] > dm) { dm = Gm[j * R + j]; jm = j; }
+        if (!(dm > tol)) {
+          s_stop = 1;
+        } else if (jm != k) {
+          int t = piv[k]; piv[k] = piv[jm]; piv[jm] = t;
+        }
+        red[1] = (double)jm;
+      }
+      __syncthreads();
+      if (s_stop) break;
+      const int jm = (int)red[1];
+      if (jm != k) {  // swap rows and columns k <-> jm of the full matrix
+        for (int c = tid; c < R; c += kTableThreads) {
+          double t = Gm[k * R + c]; Gm[k * R + c] = Gm[jm * R + c]; Gm[jm * R + c] = t;
+        }
+        __syncthreads();
+        for (int rr = tid; rr < R; rr += kTableThreads) {
+          double t = Gm[rr * R + k]; Gm[rr * R + k] = Gm[rr * R + jm]; Gm[rr * R + jm] = t;
+        }
+        __syncthreads();
+      }
+      const double lkk = sqrt(Gm[k * R + k]);
+      __syncthreads();
+      for (int i = k + 1 + tid; i < R; i += kTableThreads) Gm[i * R + k] = Gm[i * R + k] / lkk;
+      if (tid == 0) Gm[k * R + k] = lkk;
+      __syncthreads();
+      const int m = R - k - 1;
+      for (int e = tid; e < m * m; e += kTableThreads) {
+        const int i = k + 1 + e / m, j = k + 1 + e % m;
+        Gm[i * R + j] -= Gm[i * R + k] * Gm[j * R + k];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) s_rank = k;
+    __syncthreads();
+  } else if (euc) {
+    // ||A||_F^2 by a fixed-order tree reduction of per-thread row sums
+    double s = 0.0;
+    for (int64_t i = tid; i < I; i += kTableThreads) {
+      double rs = 0.0;
+      for (int r = 0; r < R; ++r) rs += (double)A[i * R + r] * (double)A[i * R + r];
+      s += rs;
+    }
+    red[tid] = s;
+    __syncthreads();
+    for (int st = kTableThreads / 2; st > 0; st >>= 1) {
+      if (tid < st) red[tid] += red[tid + st];
+      __syncthreads();
+    }
+    if (tid == 0) s_fro = red[0];
+    __syncthreads();
+  }
+  __syncthreads();
+  const int rank = s_rank;
+  const double fro = euc ? s_fro : 1.0;
+  if (tid == 0 && euc && !(fro > 0.0)) s_bad |= (fro == fro) ? 2 : 8;
+  if (tid == 0 && euc && fro > 1.7e308) s_bad |= 8;
+  if (tid == 0 && lev && rank == 0) s_bad |= 2;
+  __syncthreads();
+
+  // per-row probabilities and quantisation; each thread owns a contiguous segment of rows
+  const int64_t seg = (I + kTableThreads - 1) / kTableThreads;
+  const int64_t i_beg = min((int64_t)tid * seg, I), i_end = min(i_beg + seg, I);
+  unsigned long long local = 0;
+  int bad = 0;
+  for (int64_t i = i_beg; i < i_end; ++i) {
+    double p;
+    if (lev) {
+      // forward substitution L y = a_{i,piv}
+      double y[kMaxRank];
+      double l = 0.0;
+      for (int j = 0; j < rank; ++j) {
+        double s = (double)A[i * R + piv[j]];
+        for (int t = 0; t < j; ++t) s -= Gm[j * R + t] * y[t];
+        y[j] = s / Gm[j * R + j];
+        l += y[j] * y[j];
+      }
+      p = l / (double)rank;
+    } else if (euc) {
+      double rs = 0.0;
+      for (int r = 0; r < R; ++r) rs += (double)A[i * R + r] * (double)A[i * R + r];
+      p = rs / fro;
+    } else {
+      p = 1.0 / (double)I;
+    }
+    uint64_t q;
+    if (!lev && !euc) {
+      q = 1;
+    } else if (!(p == p) || p > 2.0) {
+      bad = 1;
+      q = 0;
+    } else if (p > 0.0) {
+      const double s = rint(p * 4294967296.0);
+      q = (s < 1.0) ? 1ull : (uint64_t)s;
+    } else {
+      q = 0;
+    }
+    if (p_out) p_out[i] = p;
+    cdf[i] = q;  // temporarily the count; scanned below
+    local += q;
+  }
+  if (bad) atomicOr(&s_bad, 8);
+  // block exclusive scan of the per-thread totals (integers: order-independent, exact)
+  const int lane = tid & 31, wid = tid >> 5;
+  unsigned long long incl = local;
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long v = warp_tot[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    warp_tot[lane] = v;  // inclusive over warps
+  }
+  __syncthreads();
+  unsigned long long run = (incl - local) + (wid > 0 ? warp_tot[wid - 1] : 0ull);
+  for (int64_t i = i_beg; i < i_end; ++i) {
+    run += cdf[i];
+    cdf[i] = run;
+  }
+  if (tid == kTableThreads - 1) {
+    const unsigned long long Ttot = run;
+    *Tout = Ttot;
+    int st = 0;
+    if (s_bad & 8) st = -8;
+    else if ((s_bad & 2) || Ttot == 0) st = -3;
+    if (st != 0) atomicCAS(status, 0, st);
+  }
+}
+
+// ==========================================================================================
+// (a2, a3) sampler.  One thread per batch row.  Row-wise (eq:ik, Alg. 3): for position p of
+// mode k: u = philox(b, purpose 0, slot p, r); r' = floor(u T_k / 2^64); i = #{cdf_k <= r'}.
+// Block (eq:bik, Alg. 4, R2): per position one draw (x0 = 0, purpose 1) selects the row i*,
+// window w = floor(i* / b_k) (identical to drawing from the window CDF); rows of the Cartesian
+// product in index-map order.  Weights in the contract's exact fp64 order (no FMA possible:
+// only products and quotients, written with explicit _rn intrinsics).
+// ==========================================================================================
+__global__ void __launch_bounds__(256) k_sample(SampleParams p) {
+  extern __shared__ uint64_t s_cdf[];
+  __shared__ const uint64_t* cdfp[kMaxOrder];
+  const int N = p.N, n = p.n;
+  const uint64_t iter = *p.iter;
+  // stage CDFs of the sampled modes in shared memory (uniform needs none)
+  if (threadIdx.x == 0) {
+    int64_t off = 0;
+    for (int k = 0; k < N; ++k) {
+      cdfp[k] = p.cdf[k];
+      if (k == n || !p.stage_smem || p.strategy == 0) continue;
+      cdfp[k] = s_cdf + off;
+      off += p.dims[k];
+    }
+  }
+  __syncthreads();
+  if (p.stage_smem && p.strategy != 0) {
+    int64_t off = 0;
+    for (int k = 0; k < N; ++k) {
+      if (k == n) continue;
+      for (int64_t i = threadIdx.x; i < p.dims[k]; i += blockDim.x) s_cdf[off + i] = p.cdf[k][i];
+      off += p.dims[k];
+    }
+    __syncthreads();
+  }
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool block = (p.strategy == 3 || p.strategy == 4);
+  if (!block) {
+    if (b >= p.B) return;
+    double prod = 1.0;
+    int pos = 0;
+    for (int k = 0; k < N; ++k) {
+      if (k == n) continue;
+      const uint64_t Tk = (p.strategy == 0) ? (uint64_t)p.dims[k] : p.Ttot[k];
+      const uint64_t u = draw_word(p.seed, iter, (uint32_t)b, kPurposeRow, (uint32_t)pos);
+      const uint64_t r = scale_draw(u, Tk);
+      int64_t i;
+      uint64_t qk;
+      if (p.strategy == 0) {
+        i = (int64_t)r;
+        qk = 1;
+      } else {
+        const uint64_t* c = cdfp[k];
+        i = upper_bound_u64(c, p.dims[k], r);
+        qk = c[i] - (i > 0 ? c[i - 1] : 0ull);
+      }
+      p.idx[b * (N - 1) + pos] = (int32_t)i;
+      const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);
+      prod = (pos == 0) ? pt : __dmul_rn(prod, pt);
+      ++pos;
+    }
+    p.w[b] = __ddiv_rn(1.0, __dmul_rn((double)p.B, prod));
+    if (b == 0) *p.beff = p.B;
+  } else {
+    int32_t start[kMaxOrder], len[kMaxOrder];
+    double prod = 1.0;
+    int64_t beff = 1;
+    int pos = 0;
+    for (int k = 0; k < N; ++k) {
+      if (k == n) continue;
+      const int64_t bk = p.window[pos];
+      const uint64_t Tk = p.Ttot[k];
+      const uint64_t u = draw_word(p.seed, iter, 0u, kPurposeWindow, (uint32_t)pos);
+      const uint64_t r = scale_draw(u, Tk);
+      const uint64_t* c = cdfp[k];
+      const int64_t istar = upper_bound_u64(c, p.dims[k], r);
+      const int64_t wsel = istar / bk;
+      const int64_t s0 = wsel * bk;
+      const int64_t e0 = min(s0 + bk, p.dims[k]);
+      const uint64_t Q = c[e0 - 1] - (s0 > 0 ? c[s0 - 1] : 0ull);
+      start[pos] = (int32_t)s0;
+      len[pos] = (int32_t)(e0 - s0);
+      const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * Q), (double)Tk);
+      prod = (pos == 0) ? pt : __dmul_rn(prod, pt);
+      beff *= (e0 - s0);
+      ++pos;
+    }
+    if (b == 0) *p.beff = beff;
+    if (b >= beff) return;
+    int64_t rem = b;
+    for (int q = 0; q < N - 1; ++q) {
+      p.idx[b * (N - 1) + q] = start[q] + (int32_t)(rem % len[q]);
+      rem /= len[q];
+    }
+    p.w[b] = __ddiv_rn(1.0, prod);
+  }
+}
+
+// ==========================================================================================
+// (a4, a5, a6) fused SKR + fiber gather + partial contractions.
+// grid = (I-tiles of 128 rows, batch chunks of TB fibers); 256 threads = 2 column halves x 128 rows.
+// Per sub-batch of 32 fibers: z_b = (*)_{k != n, ascending} A^(k)(i_k, :) (Alg. 1),
+// zw_b = omega_b z_b; x_b segment = X_(n)(i0:i0+128, j_b) (Alg. 5; contiguous rows of the
+// mode-major copy, or stride S_n in the native layout); M_c += x zw^T; Gamma_c += zw z^T
+// (I-tile 0 only).  Partials are reduced in a fixed order by k_update (deterministic).
+// ==========================================================================================
+constexpr int kGatherThreads = 256;
+constexpr int kTI = 128;
+
+template <typename T, int RPT>
+__global__ void __launch_bounds__(kGatherThreads) k_gather(GatherParams<T> p) {
+  constexpr int RP = 2 * RPT;
+  constexpr int kSB = sizeof(T) == 8 ? 16 : 32;  // fibers per sub-batch (static smem <= 48 KB)
+  __shared__ __align__(16) T xs[kSB][kTI];
+  __shared__ __align__(16) T zw[kSB][RP];
+  __shared__ __align__(16) T zu[kSB][RP];
+  __shared__ int64_t base[kSB];
+  __shared__ int owned[kSB];
+  const int N = p.N, n = p.n, R = p.R;
+  const int tid = threadIdx.x, il = tid % kTI, half = tid / kTI;
+  const int64_t i0 = (int64_t)blockIdx.x * kTI;
+  const int chunk = blockIdx.y;
+  const int64_t beff = *p.beff;
+  const int64_t b_begin = (int64_t)chunk * p.TB;
+  const int64_t b_end = min(b_begin + p.TB, beff);
+  const bool do_gamma = (blockIdx.x == 0);
+  const int64_t estride = p.mode_major ? 1 : p.lstride[n];
+  const bool row_ok = (i0 + il) < p.In_local;
+
+  T acc[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) acc[j] = T(0);
+  constexpr int GPT = (kMaxRank * kMaxRank + kGatherThreads - 1) / kGatherThreads;
+  T gacc[GPT];
+#pragma unroll
+  for (int j = 0; j < GPT; ++j) gacc[j] = T(0);
+
+  for (int64_t s = b_begin; s < b_end; s += kSB) {
+    const int nb = (int)min((int64_t)kSB, b_end - s);
+    // (a) per-fiber offsets
+    if (tid < kSB) {
+      int64_t off = 0;
+      int own = 0;
+      if (tid < nb) {
+        own = 1;
+        const int32_t* t = p.idx + (s + tid) * (N - 1);
+        int pos = 0;
+        int64_t jrow = 0, jmul = 1;
+        for (int k = 0; k < N; ++k) {
+          if (k == n) continue;
+          int64_t ik = t[pos++];
+          if (k == N - 1) {
+            ik -= p.lo_last;
+            if (ik < 0 || ik >= p.ldims[k]) own = 0;
+          }
+          off += ik * p.lstride[k];
+          jrow += ik * jmul;
+          jmul *= p.ldims[k];
+        }
+        if (p.mode_major) off = jrow * p.pitch;
+      }
+      base[tid] = off;
+      owned[tid] = own;
+    }
+    // (b) SKR rows, weighted and unweighted (zero padded to RP)
+    for (int e = tid; e < kSB * RP; e += kGatherThreads) {
+      const int bb = e / RP, r = e % RP;
+      T z = T(0), zwv = T(0);
+      if (bb < nb && r < R) {
+        const int32_t* t = p.idx + (s + bb) * (N - 1);
+        z = T(1);
+        int pos = 0;
+        for (int k = 0; k < N; ++k) {
+          if (k == n) continue;
+          z = z * ldg(p.factors[k] + (int64_t)t[pos++] * R + r);
+        }
+        zwv = (T)p.w[s + bb] * z;
+      }
+      zu[bb][r] = z;
+      zw[bb][r] = zwv;
+    }
+    __syncthreads();
+    // (c) fiber segments: warp-coalesced along the row index (all loads issued before use)
+    {
+      T v[kSB / 2];
+#pragma unroll
+      for (int q = 0; q < kSB / 2; ++q) {
+        const int bb = half + 2 * q;
+        v[q] = T(0);
+        if (bb < nb && row_ok && owned[bb]) v[q] = ldg(p.X + base[bb] + (i0 + il) * estride);
+      }
+#pragma unroll
+      for (int q = 0; q < kSB / 2; ++q) xs[half + 2 * q][il] = v[q];
+    }
+    __syncthreads();
+    // (d) M tile += x zw^T  (rows il, columns half*RPT .. +RPT)
+    for (int bb = 0; bb < nb; ++bb) {
+      const T x = xs[bb][il];
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) acc[j] += x * zw[bb][half * RPT + j];
+    }
+    if (do_gamma) {
+#pragma unroll
+      for (int j = 0; j < GPT; ++j) {
+        const int e = tid + j * kGatherThreads;
+        if (e < R * R) {
+          const int r1 = e / R, r2 = e % R;
+          T g = gacc[j];
+          for (int bb = 0; bb < nb; ++bb) g += zw[bb][r1] * zu[bb][r2];
+          gacc[j] = g;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // write partials: Mp[chunk][r][i] (coalesced over i)
+  if (row_ok) {
+    T* dst = p.Mp + (int64_t)chunk * R * p.In_local + i0 + il;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int r = half * RPT + j;
+      if (r < R) dst[(int64_t)r * p.In_local] = acc[j];
+    }
+  }
+  if (do_gamma) {
+#pragma unroll
+    for (int j = 0; j < GPT; ++j) {
+      const int e = tid + j * kGatherThreads;
+      if (e < R * R) p.Gp[(int64_t)chunk * R * R + e] = gacc[j];
+    }
+  }
+}
+
+// ==========================================================================================
+// (a6, a7, a8) chunk reduction (fixed order), G = A Gamma - M, update.
+//   fixed    : A <- A - alpha G                                  (eq:proposed)
+//   adaptive : S <- S + G*G; A <- A - eta G / (b + S)^{1/2+eps}  (eq:etaada/eq:Aada, :531-537, R12)
+// grid over blocks of kUR rows; 256 threads = kUR rows x (256/kUR) column groups.
+// ==========================================================================================
+constexpr int kUpdThreads = 256;
+constexpr int kUR = 32;
+
+template <typename T>
+__global__ void __launch_bounds__(kUpdThreads) k_update(UpdateParams<T> p) {
+  extern __shared__ __align__(16) unsigned char upd_sm[];
+  const int R = p.R, tid = threadIdx.x;
+  T* Gam = reinterpret_cast<T*>(upd_sm);   // R x R
+  T* As = Gam + R * R;                      // kUR x (R+1)
+  const int64_t r0 = (int64_t)blockIdx.x * kUR;
+  // Gamma: fixed-order sum over chunks
+  for (int e = tid; e < R * R; e += kUpdThreads) {
+    T g;
+    if (p.Gsum) {
+      g = p.Gsum[e];
+    } else {
+      g = T(0);
+      for (int c = 0; c < p.nchunks; ++c) g += p.Gp[(int64_t)c * R * R + e];
+    }
+    Gam[e] = g;
+    if (blockIdx.x == 0 && p.Gam_out) p.Gam_out[e] = g;
+  }
+  for (int e = tid; e < kUR * R; e += kUpdThreads) {
+    const int il = e / R, r = e % R;
+    const int64_t i = r0 + il;
+    As[il * (R + 1) + r] = (i < p.In_local) ? p.A[(p.row0 + i) * R + r] : T(0);
+  }
+  __syncthreads();
+  const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
+  if (p.iter && blockIdx.x == 0 && tid == 0) *p.iter += 1;  // r <- r + 1 (Alg. 6/7 line "r <- r+1")
+  const int il = tid % kUR;
+  const int64_t i = r0 + il;
+  if (i >= p.In_local) return;
+  for (int r = tid / kUR; r < R; r += kUpdThreads / kUR) {
+    T m;
+    if (p.Msum) {
+      m = p.Msum[(int64_t)r * p.In_local + i];
+    } else {
+      m = T(0);
+      for (int c = 0; c < p.nchunks; ++c) m += p.Mp[((int64_t)c * R + r) * p.In_local + i];
+    }
+    T ag = T(0);
+    for (int c = 0; c < R; ++c) ag += As[il * (R + 1) + c] * Gam[c * R + r];
+    const T g = ag - m;
+    const int64_t gi = (p.row0 + i) * R + r;
+    p.Gout[gi] = g;
+    const T a = As[il * (R + 1) + r];
+    if (p.rule == 0) {
+      p.A[gi] = a - (T)alpha * g;
+    } else {
+      const T s = p.S[gi] + g * g;
+      p.S[gi] = s;
+      if (s > T(0)) {
+        T step;
+        if (p.eps == 0.0) step = (T)p.eta / sqrt((T)p.b + s);
+        else step = (T)p.eta / (T)pow((double)((T)p.b + s), 0.5 + p.eps);
+        p.A[gi] = a - step * g;
+      }
+    }
+  }
+}
+
+// reduce chunk partials into Msum [R][In_local] and Gsum [R][R] (sharded path, phase 0)
+template <typename T>
+__global__ void k_reduce_partials(const T* __restrict__ Mp, const T* __restrict__ Gp, int nchunks, int R,
+                                  int64_t In_local, T* __restrict__ Msum, T* __restrict__ Gsum) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tot = (int64_t)R * In_local;
+  if (e < tot) {
+    T m = T(0);
+    for (int c = 0; c < nchunks; ++c) m += Mp[(int64_t)c * tot + e];
+    Msum[e] = m;
+  }
+  if (e < (int64_t)R * R) {
+    T g = T(0);
+    for (int c = 0; c < nchunks; ++c) g += Gp[(int64_t)c * R * R + e];
+    Gsum[e] = g;
+  }
+}
+
+// ==========================================================================================
+// fit: per mode-0 fiber f (global tuple of modes 1..N-1), w_r = prod_{k>=1} A^(k)(i_k, r) in
+// fp64, x_hat(i0) = sum_r A^(0)(i0, r) w_r; accumulate (x - x_hat)^2 and x^2 in fp64.
+// One block handles fibers f = blockIdx.x, += gridDim.x; per-block partials (fixed order).
+// ==========================================================================================
+template <typename T>
+__global__ void __launch_bounds__(256) k_fit(const T* __restrict__ X, int N, const int64_t* __restrict__ ldims_dev,
+                                             int64_t lo_last, int R, const T* const* __restrict__ factors,
+                                             int64_t nfib, double* __restrict__ partial) {
+  __shared__ double wsh[kMaxRank];
+  __shared__ double red[2][256];
+  __shared__ int64_t ld[kMaxOrder];
+  const int tid = threadIdx.x;
+  if (tid < N) ld[tid] = ldims_dev[tid];
+  __syncthreads();
+  const int64_t I0 = ld[0];
+  double res = 0.0, xx = 0.0;
+  for (int64_t f = blockIdx.x; f < nfib; f += gridDim.x) {
+    if (tid < R) {
+      int64_t rem = f;
+      double w = 1.0;
+      for (int k = 1; k < N; ++k) {
+        int64_t ik = rem % ld[k];
+        rem /= ld[k];
+        if (k == N - 1) ik += lo_last;
+        w *= (double)factors[k][ik * R + tid];
+      }
+      wsh[tid] = w;
+    }
+    __syncthreads();
+    const T* xf = X + f * I0;
+    const T* A0 = factors[0];
+    for (int64_t i = tid; i < I0; i += blockDim.x) {
+      double xh = 0.0;
+      for (int r = 0; r < R; ++r) xh += (double)A0[i * R + r] * wsh[r];
+      const double x = (double)xf[i];
+      res += (x - xh) * (x - xh);
+      xx += x * x;
+    }
+    __syncthreads();
+  }
+  red[0][tid] = res;
+  red[1][tid] = xx;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (tid < st) {
+      red[0][tid] += red[0][tid + st];
+      red[1][tid] += red[1][tid + st];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    partial[2 * blockIdx.x] = red[0][0];
+    partial[2 * blockIdx.x + 1] = red[1][0];
+  }
+}
+
+// ==========================================================================================
+// mode-major copy: view X as [outer][I_n][inner] (inner = prod_{k<n} I_k) and write
+// Y[(o*inner + in)*pitch + i] = X[(o*I_n + i)*inner + in]  (row j = in + inner*o = eq:map).
+// 32x32 shared-memory tiles; grid (ceil(inner/32), ceil(I_n/32), outer).
+// ==========================================================================================
+template <typename T>
+__global__ void k_transpose(const T* __restrict__ X, T* __restrict__ Y, int64_t In, int64_t inner, int64_t outer,
+                            int64_t pitch) {
+  __shared__ T tile[32][33];
+  const int64_t in0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+  for (int64_t o = blockIdx.z; o < outer; o += gridDim.z) {
+    const T* Xo = X + o * In * inner;
+    T* Yo = Y + o * inner * pitch;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const int64_t i = i0 + r, in = in0 + threadIdx.x;
+      if (i < In && in < inner) tile[r][threadIdx.x] = Xo[i * inner + in];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const int64_t in = in0 + r, i = i0 + threadIdx.x;
+      if (in < inner && i < In) Yo[in * pitch + i] = tile[threadIdx.x][r];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace cps

@@ -1,0 +1,292 @@
+"""GPU (sm_100a) vs CPU-oracle parity, through the C ABI (libcpsgd.so via the ctypes binding).
+
+Bars: sampled indices and weights bit-exact; integer tables equal except
+entries within rounding distance of a quantisation boundary; floating point within 1e-10 (fp64)
+or 1e-4 (fp32) relative, measured as ||G_gpu - G_orc|| / (||A Gamma|| + ||M||), ||dA|| / ||A||,
+|d fit|.  All inputs are seeded synth data; every oracle input comes from synth.
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_helpers import S, TOL, handle, make_problem, near_boundary, oracle_step, oracle_tables, rel_err, to_dev
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+
+    __graft_entry__.build()
+
+
+# ------------------------------------------------------------------------------------------ Philox
+def test_device_philox_matches_curand_and_oracle(tmp_path):
+    """device Philox == cuRAND curand_Philox4x32_10 (library routine) == oracle, 1M counters."""
+    import ctypes as C
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    so = str(tmp_path / "philox_check.so")
+    subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2",
+                           "-Xcompiler", "-fPIC", "-shared", "-o", so, os.path.join(here, "native", "philox_check.cu")])
+    L = C.CDLL(so)
+    n = 1 << 20
+    rng = np.random.default_rng(0)
+    ctr = rng.integers(0, 2 ** 32, size=(n, 4), dtype=np.uint64).astype(np.uint32)
+    key = rng.integers(0, 2 ** 32, size=(n, 2), dtype=np.uint64).astype(np.uint32)
+    dev = torch.device("cuda:0")
+    c = torch.from_numpy(ctr.view(np.int32)).to(dev)
+    k = torch.from_numpy(key.view(np.int32)).to(dev)
+    ours = torch.zeros((n, 4), dtype=torch.int32, device=dev)
+    theirs = torch.zeros((n, 4), dtype=torch.int32, device=dev)
+    assert L.philox_check(C.c_void_p(c.data_ptr()), C.c_void_p(k.data_ptr()), C.c_void_p(ours.data_ptr()),
+                          C.c_void_p(theirs.data_ptr()), n) == 0
+    o = ours.cpu().numpy().view(np.uint32)
+    t = theirs.cpu().numpy().view(np.uint32)
+    assert np.array_equal(o, t)
+    for i in rng.integers(0, n, size=200):
+        assert oracle.philox(ctr[i], key[i]).tolist() == o[i].tolist()
+
+
+# ------------------------------------------------------------------------------------------ tables
+@pytest.mark.parametrize("strategy", ["leverage", "euclidean", "block_leverage", "block_euclidean"])
+@pytest.mark.parametrize("cfgname", ["C1", "C2", "C3"])
+def test_tables_match_oracle(strategy, cfgname):
+    """a1: GPU p vs oracle p <= 1e-11 relative; integer q identical except near-boundary entries."""
+    cfg = synth.CONFIGS[cfgname]
+    A_true = synth.true_factors(cfg)
+    A = [np.ascontiguousarray(a.astype(np.float64 if cfg.dtype == "f64" else np.float32)) for a in A_true]
+    dev = torch.device("cuda:0")
+    Ad = [torch.from_numpy(a).to(dev) for a in A]
+    Xd = torch.zeros(int(np.prod(cfg.dims)), dtype=Ad[0].dtype, device=dev)  # tables read only the factors
+    h = handle(cfg, Xd, Ad, strategy, mode_major=False)
+    tabs = oracle_tables(strategy, A)
+    for k in range(cfg.order):
+        q, T, p = h.get_table(k)
+        po, qo, To = tabs[k]
+        assert np.all(np.abs(p - po) <= 1e-11 * po + 1e-300), np.max(np.abs(p - po) / po)
+        diff = q != qo
+        flip_ok = near_boundary(po, 1e-3)
+        assert np.all(~diff | flip_ok)
+        assert np.all(np.abs(q.astype(np.int64) - qo.astype(np.int64)) <= 1)
+        assert T == int(q.sum())
+    h.close()
+
+
+# ------------------------------------------------------------------------------------------ sampler
+@pytest.mark.parametrize("strategy", S)
+@pytest.mark.parametrize("dims,R,B", [((60, 60, 60), 5, 64), ((33, 17, 41), 4, 100), ((11, 9, 13, 7), 3, 256)])
+def test_sample_bit_exact(strategy, dims, R, B):
+    """a2/a3: idx and omega identical to the oracle's for every mode and several iterations."""
+    cfg = synth.small(dims, R, batch=B, rule="fixed", row_sigma=1.0, seed=5)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, strategy, seed=123)
+    tabs = oracle_tables(strategy, A0)
+    tq = [(t[1], t[2]) for t in tabs]
+    for k in range(len(dims)):
+        qg, Tg, _ = h.get_table(k)
+        assert np.array_equal(qg, tabs[k][1]) and Tg == tabs[k][2], "table flip (rare); pick another seed"
+    for n in range(len(dims)):
+        for it in (0, 1, 7, 2 ** 33 + 5):
+            idx_g, w_g = h.sample(n, it)
+            idx_o, w_o, _ = oracle.sample(dims, n, oracle.STRATEGIES[strategy], B, tq, 123, it)
+            assert np.array_equal(idx_g.cpu().numpy(), idx_o)
+            assert np.array_equal(w_g.cpu().numpy(), w_o)
+    h.close()
+
+
+# ------------------------------------------------------------------------------------------ one step
+STEP_CASES = [
+    # (dims, R, B, dtype, rule)
+    ((60, 60, 60), 5, 64, "f64", "fixed"),           # C1 shape
+    ((130, 70, 45), 20, 512, "f32", "adaptive"),     # C2-like, ragged I-tiles (130 = 128 + 2)
+    ((20, 18, 16, 14), 10, 1024, "f32", "adaptive"),  # C3-like 4-way
+    ((9, 1, 7), 3, 5, "f64", "fixed"),               # a unit mode, tiny batch
+    ((40, 30, 20), 1, 1, "f64", "adaptive"),         # R = 1, B = 1
+    ((50, 40, 30), 64, 300, "f32", "fixed"),         # R = 64 (max)
+]
+
+
+@pytest.mark.parametrize("strategy", S)
+@pytest.mark.parametrize("case", STEP_CASES, ids=lambda c: "x".join(map(str, c[0])) + f"_R{c[1]}_B{c[2]}_{c[3]}")
+@pytest.mark.parametrize("mode_major", [True, False])
+def test_one_step_per_mode(strategy, case, mode_major):
+    """a4-a8: from the same seeded state, one GPU step of mode n at iteration r equals one oracle
+    step: G within tol of (||A Gamma|| + ||M||), updated A within tol of ||A||."""
+    dims, R, B, dt, rule = case
+    cfg = synth.small(dims, R, dtype=dt, batch=B, rule=rule, row_sigma=1.0, noise=1e-2, seed=11, alpha=0.01,
+                      eta=0.05)
+    bpar = 1e-2  # b > 0 keeps the first AdaGrad step smooth in G (b = 0 gives eta*sign(G))
+    X, A0 = make_problem(cfg)
+    tol = TOL[dt]
+    for n in range(len(dims)):
+        Xd, Ad = to_dev(X, A0)
+        h = handle(cfg, Xd, Ad, strategy, seed=77, mode_major=mode_major, b=bpar)
+        it = 3 + n
+        h.iter = it
+        idx_o, w_o, G_o, Gam_o, M_o, tabs = oracle_step(X, dims, A0, n, strategy, B, 77, it)
+        h.step(n, cfg.alpha)
+        G_g, m, Gam_g = h.get_grad()
+        assert m == n and h.iter == it + 1
+        A64 = np.asarray(A0[n], np.float64)
+        scale = np.linalg.norm(A64 @ Gam_o) + np.linalg.norm(M_o)
+        assert rel_err(G_g, G_o, scale) <= tol
+        assert rel_err(Gam_g, Gam_o, np.linalg.norm(Gam_o)) <= tol
+        if rule == "fixed":
+            A_o = oracle.update_fixed(A64, G_o, cfg.alpha)
+        else:
+            A_o, S_o = oracle.update_adaptive(A64, np.zeros_like(A64), G_o, cfg.eta, b=bpar)
+            S_g = h.get_accum(n)
+            assert rel_err(S_g, S_o, np.linalg.norm(S_o)) <= 2 * tol
+        A_g = Ad[n].cpu().numpy()
+        assert rel_err(A_g, A_o, np.linalg.norm(A_o)) <= tol
+        for k in range(len(dims)):
+            if k != n:
+                assert np.array_equal(Ad[k].cpu().numpy(), A0[k])
+        h.close()
+
+
+# ------------------------------------------------------------------------------------------ trajectories
+@pytest.mark.parametrize("strategy", S)
+def test_c1_trajectory_50_sweeps(strategy):
+    """C1 (60^3 fp64, R5, B64, fixed alpha, 50 cyclic sweeps) free-running on both sides: final
+    factors within 1e-9 relative (graph-replayed sweeps)."""
+    cfg = synth.CONFIGS["C1"]
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, strategy, seed=0)
+    h.sweep(50)
+    h.sync()
+    fs, _, _ = oracle.run(X, A0, oracle.STRATEGIES[strategy], oracle.STEP_FIXED, cfg.batch, 50 * 3,
+                          alpha=cfg.alpha, seed=0)
+    for k in range(3):
+        assert rel_err(Ad[k].cpu().numpy(), fs[k], np.linalg.norm(fs[k])) <= 1e-9
+    assert abs(h.fit() - oracle.fit(X, fs)) <= 1e-9
+    assert h.iter == 150
+    h.close()
+
+
+@pytest.mark.parametrize("strategy", ["leverage", "block_euclidean"])
+def test_random_order_and_adaptive_trajectory(strategy):
+    """random mode order, adaptive rule, fp64: 40 iterations equal the oracle's."""
+    cfg = synth.small((24, 20, 16), 4, dtype="f64", batch=48, rule="adaptive", eta=0.05, seed=3, row_sigma=0.8)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, strategy, seed=9)
+    h.sweep(40 // 3 + 1, order="random")
+    iters = 3 * (40 // 3 + 1)
+    fs, Ss, modes = oracle.run(X, A0, oracle.STRATEGIES[strategy], oracle.STEP_ADAPTIVE, cfg.batch, iters,
+                               order=oracle.ORDER_RANDOM, eta=cfg.eta, seed=9)
+    for k in range(3):
+        assert rel_err(Ad[k].cpu().numpy(), fs[k], np.linalg.norm(fs[k])) <= 1e-9
+        assert rel_err(h.get_accum(k), Ss[k], np.linalg.norm(Ss[k]) + 1e-300) <= 1e-9
+    h.close()
+
+
+def test_fixed_schedule_sweep_matches_oracle():
+    """per-iteration step sizes alpha_r = a0 / (1 + r)^0.6 (Robbins-Monro)."""
+    cfg = synth.small((30, 25, 20), 5, dtype="f64", batch=40, rule="fixed", seed=4)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "euclidean", seed=1)
+    al = 0.01 / (1.0 + np.arange(12)) ** 0.6
+    h.sweep(4, alphas=al)
+    fs, _, _ = oracle.run(X, A0, oracle.EUCLIDEAN, oracle.STEP_FIXED, cfg.batch, 12, alphas=al, seed=1)
+    for k in range(3):
+        assert rel_err(Ad[k].cpu().numpy(), fs[k], np.linalg.norm(fs[k])) <= 1e-9
+    h.close()
+
+
+# ------------------------------------------------------------------------------------------ fit
+@pytest.mark.parametrize("cfgname", ["C1", "C3"])
+def test_fit_matches_oracle(cfgname):
+    cfg = synth.CONFIGS[cfgname]
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "leverage")
+    assert abs(h.fit() - oracle.fit(X, A0)) <= TOL[cfg.dtype]
+    # the exact model gives fit 1 (noiseless)
+    cfg0 = synth.small((17, 13, 11), 3, dtype=cfg.dtype, noise=0.0, seed=2)
+    At = [a.astype(np.float64 if cfg.dtype == "f64" else np.float32) for a in synth.true_factors(cfg0)]
+    X0 = synth.cp_tensor(At).astype(At[0].dtype)
+    Xd0, Ad0 = to_dev(X0, At)
+    h0 = handle(cfg0, Xd0, Ad0, "leverage")
+    assert abs(h0.fit() - 1.0) <= TOL[cfg.dtype]
+    h.close(); h0.close()
+
+
+# ------------------------------------------------------------------------------------------ full size (bench config)
+def test_c2_full_size_step_and_fit():
+    """C2 at full size (400^3 fp32, R20, B512, adaptive) in the launch configuration bench.py
+    times: one step per mode vs the oracle, and fit."""
+    cfg = synth.CONFIGS["C2"]
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "leverage", seed=0)
+    assert abs(h.fit() - oracle.fit(X, A0)) <= 1e-4
+    h.close()
+    del Xd
+    for n in range(3):
+        Xd, Ad = to_dev(X, A0)
+        h = handle(cfg, Xd, Ad, "leverage", seed=0)
+        h.iter = n
+        idx_o, w_o, G_o, Gam_o, M_o, tabs = oracle_step(X, cfg.dims, A0, n, "leverage", cfg.batch, 0, n)
+        idx_g, w_g = h.sample(n, n)
+        assert np.array_equal(idx_g.cpu().numpy(), idx_o) and np.array_equal(w_g.cpu().numpy(), w_o)
+        h.step(n)
+        G_g, _, _ = h.get_grad()
+        scale = np.linalg.norm(np.asarray(A0[n], np.float64) @ Gam_o) + np.linalg.norm(M_o)
+        assert rel_err(G_g, G_o, scale) <= 1e-4
+        h.close()
+        del Xd
+
+
+# ------------------------------------------------------------------------------------------ e2e host path
+def test_steps_host_equals_device_path():
+    cfg = synth.small((30, 20, 10), 4, dtype="f64", batch=32, rule="fixed", seed=8)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "leverage", seed=2)
+    host = [torch.from_numpy(a.copy()).pin_memory() for a in A0]
+    h.steps_host(0, 6, host, 0.01)
+    fs, _, _ = oracle.run(X, A0, oracle.LEVERAGE, oracle.STEP_FIXED, cfg.batch, 6, alpha=0.01, seed=2)
+    for k in range(3):
+        assert rel_err(host[k].numpy(), fs[k], np.linalg.norm(fs[k])) <= 1e-10
+    h.close()
+
+
+# ------------------------------------------------------------------------------------------ errors
+def test_error_paths():
+    from paper_2103_04081_b200 import CPError
+
+    cfg = synth.small((8, 7, 6), 2, dtype="f64", batch=4, seed=1)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    with pytest.raises(CPError, match="EINVAL"):
+        handle(cfg, Xd, Ad, "leverage", rule="adaptive", eta=0.0)
+    Z = [torch.zeros_like(a) for a in Ad]
+    with pytest.raises(CPError, match="EDEGENERATE"):
+        handle(cfg, Xd, Z, "euclidean")
+    Nn = [a.clone() for a in Ad]
+    Nn[1][0, 0] = float("nan")
+    with pytest.raises(CPError, match="ENONFINITE"):
+        handle(cfg, Xd, Nn, "leverage")
+    h = handle(cfg, Xd, Ad, "leverage")
+    with pytest.raises(CPError, match="ERANGE"):
+        h.step(3)
+    # a diverging step size poisons the next table rebuild -> reported at the next sync
+    h.step(0, 1e30)
+    h.step(0, 1e30)
+    with pytest.raises(CPError, match="ENONFINITE|EDEGENERATE"):
+        h.sync()
+    h.close()
