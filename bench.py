@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark of the importance-sampled SGD hot path (arXiv 2103.04081) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C2]
+                    [--sampler leverage]
+
+A "step" is one cyclic sweep: N_modes SGD iterations (one per mode), each running the whole hot
+path -- table refresh (a1), sampling (a2, a3), SKR + fiber gather + contractions (a4-a6),
+fixed/adaptive update (a7, a8) -- i.e. every SURVEY §8(a) row including the mode loop (a9).
+metric = sampled fibers/s (whole job).  Default workload: BASELINE.json configs[1] (C2, 400^3
+fp32, R = 20, B = 512, adaptive step), seeded synthetic data.
+
+Multi-GPU (torchrun, one process per GPU): workloads that fit one GPU (C1-C4) run one independent
+chain per GPU (different Philox seed, no collective; "scaling": "weak"); C5 runs slab-sharded
+along the last mode with the NCCL allreduce / row broadcast inside the library ("strong").
+
+--impl reference times the CPU oracle (oracle/liborc.so, single thread) on rank 0 on the same
+workload (the paper publishes no GPU baseline).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "sampled fibers/s (cyclic sweeps of the importance-sampled SGD step)"
+UNIT = "fibers/s"
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_inputs(cfg, device, seed_offset=0, slab=None):
+    """seeded synthetic tensor + norm-matched U[0,1] init (synth)."""
+    import torch
+
+    if cfg.numel <= 200_000_000 and slab is None:
+        X = synth.tensor(cfg)
+        A0 = synth.init_factors(cfg, X)
+        return torch.from_numpy(X).to(device), [torch.from_numpy(a).to(device) for a in A0], X, A0
+    Xd, _, xnorm = synth.tensor_torch(cfg, device=device, slab=slab)
+    A0 = synth.init_factors_torch(cfg, xnorm, device=device)
+    return Xd, A0, None, None
+
+
+# ----------------------------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+
+    from paper_2103_04081_b200 import CPSGD
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    stream = torch.cuda.Stream(device=dev)
+    sharded = (cfg.name == "C5" and ws > 1)
+    slab = None
+    nccl_id = None
+    if sharded:
+        I_last = cfg.dims[-1]
+        per = I_last // ws
+        slab = (rank * per, I_last if rank == ws - 1 else (rank + 1) * per)
+        import torch.distributed as dist
+
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            import ctypes as C
+
+            nccl = C.CDLL("libnccl.so.2")
+            buf = C.create_string_buffer(128)
+            assert nccl.ncclGetUniqueId(buf) == 0
+            idt.copy_(torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+    Xd, Ad, Xh, A0h = make_inputs(cfg, dev, slab=slab)
+    torch.cuda.synchronize()
+    seed = cfg.seed if sharded else cfg.seed + 1000 * rank  # independent chains when replicated
+    t0 = time.time()
+    with torch.cuda.stream(stream):
+        h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=args.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta,
+                  seed=seed, stream=stream, world_rank=rank if sharded else 0, world_size=ws if sharded else 1,
+                  nccl_id=nccl_id, slab=slab, mode_major=not args.native_layout)
+    init_s = time.time() - t0
+    N = cfg.order
+    fibers_per_step = sum(h.batch_max(n) for n in range(N)) if args.sampler.startswith("block") else N * cfg.batch
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    # warm-up (captures the sweep graph)
+    h.sweep(args.warmup)
+    h.sync()
+    # ---- timed region: K sweeps (graph replays) ----
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = h.launches
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        h.sweep(args.steps)
+        ev1.record(stream)
+        stream.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = h.launches - launches0
+    h.sync()
+    if ws > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    total_fibers = fibers_per_step * args.steps * (1 if sharded else ws)
+    value = total_fibers / (ms / 1e3)
+
+    # ---- per-kernel device durations (CUDA events on the launch stream, direct launches) ----
+    h.profile(True)
+    h.sweep(max(3, min(args.steps, 20)))
+    prof = h.profile_read()
+    h.profile(False)
+    prof_sweeps = max(3, min(args.steps, 20))
+    kern = {k: {"avg_us": 1e3 * t / c, "count": c, "share": 0.0} for k, (t, c) in prof.items()}
+    tot = sum(t for t, c in prof.values()) or 1.0
+    for k, (t, c) in prof.items():
+        kern[k]["share"] = t / tot
+    dominant = max(prof.items(), key=lambda kv: kv[1][0])[0] if prof else None
+
+    peaks = load_peaks()
+    esz = cfg.itemsize
+    In_avg = sum(cfg.dims) / N
+    if sharded:
+        In_avg = (sum(cfg.dims[:-1]) + (slab[1] - slab[0])) / N
+    # algorithmic bytes per k_gather launch: the sampled fibers (B_eff x I_n x sizeof); per the
+    # sharded path only the locally owned part
+    gather_bytes = (fibers_per_step / N) * In_avg * esz
+    useful_gbs = value * (sum(cfg.dims) / N) * esz / 1e9
+    roof = None
+    if "k_gather" in kern:
+        t_g = kern["k_gather"]["avg_us"] * 1e-6
+        ach = gather_bytes / t_g / 1e9
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tfile):
+            traffic = json.load(open(tfile)).get(f"{cfg.name}/{args.sampler}/k_gather")
+        roof = {"kernel": "k_gather", "bound": "hbm", "achieved": round(ach, 2), "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "_fallback" not in peaks else "fallback",
+                "algorithmic_bytes_per_launch": gather_bytes}
+    # ---- e2e: host-buffer C-ABI call, H2D of all factors + D2H every step ----
+    host = [a.detach().cpu().pin_memory() for a in Ad]
+    h2d = sum(a.numel() * esz for a in host)
+    e2e_steps = max(2, min(args.steps, 20))
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        h.steps_host(0, N, host)
+    t1 = time.perf_counter()
+    e2e_ms = (t1 - t0) * 1e3
+    if ws > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_val = fibers_per_step * e2e_steps * (1 if sharded else ws) / (e2e_ms / 1e3)
+    clocks = clk.summary()
+    res = None
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+            "dtype": "f64" if cfg.dtype == "f64" else "f32", "data": "synthetic (seeded; synth/ recipe)",
+            "config": {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.dims))} {cfg.dtype}, R={cfg.rank}, "
+                                   f"B={cfg.batch}, {cfg.rule} step, {args.sampler} sampling, cyclic sweeps",
+                       "step": f"one cyclic sweep = {N} SGD iterations x B fibers",
+                       "iterations_per_s": round(N * args.steps * (1 if sharded else ws) / (ms / 1e3), 1),
+                       "useful_GBps": round(useful_gbs, 2),
+                       "layout": "native" if args.native_layout else "mode-major copies (CP_FLAG_MODE_MAJOR)",
+                       "parallelism": (f"slab-sharded x{ws} (NCCL)" if sharded else
+                                       (f"{ws} independent chains" if ws > 1 else "1 GPU")),
+                       "l2": "inputs larger than L2 (tensor + mode-major copies >> 126 MB); fresh fibers per step",
+                       "init_s": round(init_s, 3)},
+            "roofline": roof,
+            "kernels": {k: {"avg_us": round(v["avg_us"], 3), "share": round(v["share"], 4), "count": v["count"]}
+                        for k, v in kern.items()},
+            "kernel_timing": f"CUDA events around each launch on the library stream, {prof_sweeps} direct-launch sweeps",
+            "clocks": clocks,
+            "e2e": {"value": round(e2e_val, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": h2d,
+                    "how": "cp_sgd_steps_host: pinned host factors -> device, one sweep, factors -> host, sync"},
+            "gpu_launches": launches,
+        }
+    h.close()
+    return res
+
+
+def cpu_baseline(cfg, args, budget_s=12.0):
+    """the oracle as it stands, single thread, on a bounded sample of the same workload."""
+    import oracle
+
+    X = synth.tensor(cfg)
+    A0 = synth.init_factors(cfg, X)
+    X64 = X.astype(np.float64)
+    st = oracle.STRATEGIES[args.sampler]
+    rule = oracle.STEP_ADAPTIVE if cfg.rule == "adaptive" else oracle.STEP_FIXED
+    iters, t_used = 0, 0.0
+    fs = A0
+    while t_used < budget_s and iters < 3 * 200:
+        t0 = time.perf_counter()
+        fs, _, _ = oracle.run(X64, fs, st, rule, cfg.batch, cfg.order, alpha=cfg.alpha, eta=cfg.eta,
+                              seed=cfg.seed, r0=iters)
+        t_used += time.perf_counter() - t0
+        iters += cfg.order
+    fib = iters * cfg.batch
+    return {"value": round(fib / t_used, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{iters} oracle iterations ({iters // cfg.order} cyclic sweeps) of {cfg.name}, "
+                      f"{args.sampler}, fp64 single-threaded C (-O2), tensor host-resident; per-iteration "
+                      f"table rebuild by Householder QR included", "seconds": round(t_used, 2)}
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    import oracle
+
+    X = synth.tensor(cfg)
+    A0 = synth.init_factors(cfg, X)
+    X64 = X.astype(np.float64)
+    st = oracle.STRATEGIES[args.sampler]
+    rule = oracle.STEP_ADAPTIVE if cfg.rule == "adaptive" else oracle.STEP_FIXED
+    fs = A0
+    r = 0
+    for _ in range(args.warmup):
+        fs, _, _ = oracle.run(X64, fs, st, rule, cfg.batch, cfg.order, alpha=cfg.alpha, eta=cfg.eta, seed=cfg.seed,
+                              r0=r)
+        r += cfg.order
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fs, _, _ = oracle.run(X64, fs, st, rule, cfg.batch, cfg.order, alpha=cfg.alpha, eta=cfg.eta, seed=cfg.seed,
+                              r0=r)
+        r += cfg.order
+    dt = time.perf_counter() - t0
+    fib = args.steps * cfg.order * cfg.batch
+    val = fib / dt
+    return {"impl": "reference", "metric": METRIC, "value": round(val, 1), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded; synth/ recipe)",
+            "config": {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.dims))}, R={cfg.rank}, B={cfg.batch}, "
+                                   f"{cfg.rule} step, {args.sampler} sampling, cyclic sweeps",
+                       "step": f"one cyclic sweep = {cfg.order} SGD iterations x B fibers"},
+            "cpu_baseline": {"value": round(val, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} full sweeps of {cfg.name} (fp64 oracle, single thread)"},
+            "e2e": {"value": round(val, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2", choices=list(synth.CONFIGS))
+    ap.add_argument("--sampler", default="leverage",
+                    choices=["uniform", "leverage", "euclidean", "block_leverage", "block_euclidean"])
+    ap.add_argument("--native-layout", action="store_true", help="no mode-major copies")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = synth.CONFIGS[args.workload]
+    if args.impl == "reference":
+        res = run_reference(args, cfg)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    import __graft_entry__
+
+    ws, rank, _ = dist_env()
+    __graft_entry__.build()  # idempotent (mtime check, atomic replace)
+    if ws > 1:
+        import torch.distributed  # noqa: F401
+    res = run_ours(args, cfg)
+    if rank == 0:
+        if not args.no_cpu_baseline and ws == 1 and cfg.numel <= 200_000_000:
+            res["cpu_baseline"] = cpu_baseline(cfg, args)
+        print(json.dumps(res), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -185,6 +185,11 @@ class CPSGD:
                                         C.c_void_p(w.data_ptr()), C.byref(beff)))
         return idx[:beff.value], w[:beff.value]
 
+    def batch_max(self, mode: int) -> int:
+        bm = C.c_int64(0)
+        self._chk(self._L.cp_sgd_batch_max(self._h, mode, C.byref(bm)))
+        return bm.value
+
     def step(self, mode: int, alpha: float = -1.0):
         self._chk(self._L.cp_sgd_step(self._h, mode, float(alpha)))
 

@@ -94,7 +94,9 @@ struct cp_sgd_s {
   int64_t bmax[kMaxOrder] = {};               // rows per step for mode n
   double alpha = 0, eta = 0, bpar = 0, eps = 0;
   uint64_t seed = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;     // the caller's stream
+  cudaStream_t ls = nullptr;         // stream kernels are launched on (== stream, or cap_stream while capturing)
+  cudaStream_t cap_stream = nullptr; // private non-blocking stream used only for graph capture
   int world_rank = 0, world_size = 1;
   uint32_t flags = 0;
   const void* X = nullptr;
@@ -188,12 +190,12 @@ struct ProfScope {
     if (h->prof) {
       cudaEvent_t a = next_event(h);
       b = next_event(h);
-      cudaEventRecord(a, h->stream);
+      cudaEventRecord(a, h->ls);
       h->prof_recs.push_back(ProfRec{id, a, b});
     }
   }
   ~ProfScope() {
-    if (h->prof) cudaEventRecord(b, h->stream);
+    if (h->prof) cudaEventRecord(b, h->ls);
   }
 };
 
@@ -207,7 +209,7 @@ cp_status launch_table(cp_sgd_s* h, int k) {
   const int P = h->R * (h->R + 1) / 2;
   const int groups = std::max(1, kTableThreads / P);
   const size_t smem = sizeof(double) * (kMaxRank * kMaxRank + std::max(kTableThreads, P * groups));
-  k_table<T><<<1, kTableThreads, smem, h->stream>>>((const T*)h->factors[k], h->dims[k], h->R, h->sampler,
+  k_table<T><<<1, kTableThreads, smem, h->ls>>>((const T*)h->factors[k], h->dims[k], h->R, h->sampler,
                                                     h->pprob[k], h->cdf[k], h->Ttot + k, h->status_dev);
   h->launches++;
   return check_launch(h, "k_table");
@@ -245,7 +247,7 @@ cp_status launch_sample(cp_sgd_s* h, int n, const uint64_t* iter_ptr, int32_t* i
   if (!p.stage_smem) smem = 0;
   const int threads = 256;
   const int64_t blocks = std::max<int64_t>(1, ceil_div(h->bmax[n], threads));
-  k_sample<<<(unsigned)blocks, threads, smem, h->stream>>>(p);
+  k_sample<<<(unsigned)blocks, threads, smem, h->ls>>>(p);
   h->launches++;
   return check_launch(h, "k_sample");
 }
@@ -281,7 +283,7 @@ cp_status launch_gather_t(cp_sgd_s* h, int n) {
   p.Mp = (T*)h->Mp;
   p.Gp = (T*)h->Gp;
   dim3 grid(h->ntiles[n], h->nchunks[n]);
-  k_gather<T, RPT><<<grid, kGatherThreads, 0, h->stream>>>(p);
+  k_gather<T, RPT><<<grid, kGatherThreads, 0, h->ls>>>(p);
   h->launches++;
   return check_launch(h, "k_gather");
 }
@@ -322,7 +324,7 @@ cp_status launch_update(cp_sgd_s* h, int n, double alpha, const double* alpha_de
   p.iter = h->iter_dev;
   const size_t smem = sizeof(T) * (h->R * h->R + kUR * (h->R + 1));
   const int64_t blocks = std::max<int64_t>(1, ceil_div(h->In_local[n], kUR));
-  k_update<T><<<(unsigned)blocks, kUpdThreads, smem, h->stream>>>(p);
+  k_update<T><<<(unsigned)blocks, kUpdThreads, smem, h->ls>>>(p);
   h->launches++;
   return check_launch(h, "k_update");
 }
@@ -331,7 +333,7 @@ template <typename T>
 cp_status launch_reduce(cp_sgd_s* h, int n) {
   ProfScope ps(h, kKReduce);
   const int64_t tot = std::max<int64_t>((int64_t)h->R * h->In_local[n], (int64_t)h->R * h->R);
-  k_reduce_partials<T><<<(unsigned)ceil_div(tot, 256), 256, 0, h->stream>>>(
+  k_reduce_partials<T><<<(unsigned)ceil_div(tot, 256), 256, 0, h->ls>>>(
       (const T*)h->Mp, (const T*)h->Gp, h->nchunks[n], h->R, h->In_local[n], (T*)h->Msum, (T*)h->Gsum);
   h->launches++;
   return check_launch(h, "k_reduce_partials");
@@ -366,7 +368,7 @@ cp_status exchange_after0(cp_sgd_s* h, int n) {
   ProfScope ps(h, kKComm);
   const int dt = h->dtype == CP_F64 ? kNcclFloat64 : kNcclFloat32;
   return nccl_check(h, g_nccl.AllReduce(h->Msum, h->Msum, (size_t)h->R * h->In_local[n], dt, kNcclSum, h->comm,
-                                        h->stream),
+                                        h->ls),
                     "ncclAllReduce(M)");
 }
 
@@ -381,7 +383,7 @@ cp_status exchange_after1(cp_sgd_s* h, int n, const std::vector<int64_t>& row_ra
     const int64_t a = row_ranges[2 * r], b = row_ranges[2 * r + 1];
     if (b <= a) continue;
     char* base = (char*)h->factors[n] + (size_t)a * h->R * h->esz;
-    st = nccl_check(h, g_nccl.Broadcast(base, base, (size_t)(b - a) * h->R, dt, r, h->comm, h->stream),
+    st = nccl_check(h, g_nccl.Broadcast(base, base, (size_t)(b - a) * h->R, dt, r, h->comm, h->ls),
                     "ncclBroadcast(rows)");
     if (st) break;
   }
@@ -472,6 +474,9 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
   h->eps = cfg->eps;
   h->seed = cfg->seed;
   h->stream = (cudaStream_t)cfg->stream;
+  h->ls = h->stream;
+  if (cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return init_fail(h, h->fail(CP_ECUDA, "cudaStreamCreate failed"));
   h->world_rank = cfg->world_rank;
   h->world_size = cfg->world_size;
   h->flags = cfg->flags;
@@ -633,10 +638,10 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       dim3 tb(32, 8);
       dim3 grid((unsigned)ceil_div(inner, 32), (unsigned)ceil_div(In, 32), (unsigned)std::min<int64_t>(outer, 65535));
       if (h->dtype == CP_F64)
-        k_transpose<double><<<grid, tb, 0, h->stream>>>((const double*)h->X, (double*)h->Xmm[n], In, inner, outer,
+        k_transpose<double><<<grid, tb, 0, h->ls>>>((const double*)h->X, (double*)h->Xmm[n], In, inner, outer,
                                                         h->pitch[n]);
       else
-        k_transpose<float><<<grid, tb, 0, h->stream>>>((const float*)h->X, (float*)h->Xmm[n], In, inner, outer,
+        k_transpose<float><<<grid, tb, 0, h->ls>>>((const float*)h->X, (float*)h->Xmm[n], In, inner, outer,
                                                        h->pitch[n]);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return init_fail(h, h->fail(CP_ECUDA, "k_transpose: %s", cudaGetErrorString(e)));
@@ -692,6 +697,7 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   if (!h) return CP_OK;
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->sweep_exec) cudaGraphExecDestroy(h->sweep_exec);
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   for (int k = 0; k < kMaxOrder; ++k) {
     cudaFree(h->cdf[k]);
     cudaFree(h->pprob[k]);
@@ -854,13 +860,21 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
   CUDA_TRY(h, cudaMemcpyAsync(h->alpha_dev, pin + 4, sizeof(double), cudaMemcpyHostToDevice, h->stream));
   if (!h->sweep_exec) {
     cudaGraph_t g = nullptr;
-    CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    // capture on a private stream (the caller's may be the legacy default stream, which cannot
+    // be captured); the graph is launched on the caller's stream
+    h->ls = h->cap_stream;
+    cudaError_t eb = cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (eb != cudaSuccess) {
+      h->ls = h->stream;
+      return h->fail(CP_ECUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(eb));
+    }
     auto* rr = rr_store(h, false);
     static const std::vector<int64_t> none;
     cp_status st = CP_OK;
     const uint64_t l0 = h->launches;
     for (int n = 0; n < h->N && !st; ++n) st = do_step(h, n, h->alpha, h->alpha_dev, rr ? *rr : none);
-    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
+    h->ls = h->stream;
     h->launches = l0;
     if (st) {
       if (g) cudaGraphDestroy(g);
@@ -916,10 +930,10 @@ cp_status cp_fit(cp_sgd_t h, double* fit_host) {
   {
     ProfScope ps(h, kKFit);
     if (h->dtype == CP_F64)
-      k_fit<double><<<blocks, 256, 0, h->stream>>>((const double*)h->X, h->N, h->ldims_dev, h->lo_last, h->R,
+      k_fit<double><<<blocks, 256, 0, h->ls>>>((const double*)h->X, h->N, h->ldims_dev, h->lo_last, h->R,
                                                    (const double* const*)h->fac_dev, nfib, h->fit_partial);
     else
-      k_fit<float><<<blocks, 256, 0, h->stream>>>((const float*)h->X, h->N, h->ldims_dev, h->lo_last, h->R,
+      k_fit<float><<<blocks, 256, 0, h->ls>>>((const float*)h->X, h->N, h->ldims_dev, h->lo_last, h->R,
                                                   (const float* const*)h->fac_dev, nfib, h->fit_partial);
     h->launches++;
   }
