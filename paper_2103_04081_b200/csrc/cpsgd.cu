@@ -107,7 +107,10 @@ struct cp_sgd_s {
   int64_t pitch[kMaxOrder] = {};
   // per-mode tiling of k_gather
   int64_t In_local[kMaxOrder] = {}, row0[kMaxOrder] = {};
-  int ntiles[kMaxOrder] = {}, nchunks[kMaxOrder] = {};
+  int ntiles[kMaxOrder] = {}, nchunks[kMaxOrder] = {}, cgather[kMaxOrder] = {}, nparts[kMaxOrder] = {};
+  int cu[kMaxOrder] = {};           // cluster size of k_update_table for mode n (0: legacy kernels)
+  int64_t ut_rows[kMaxOrder] = {};  // rows per CTA of k_update_table
+  size_t ut_smem[kMaxOrder] = {};
   int64_t TB[kMaxOrder] = {};
   // workspace (device)
   uint64_t* cdf[kMaxOrder] = {};
@@ -138,6 +141,7 @@ struct cp_sgd_s {
   int sample_smem = 0;       // dynamic smem bytes of k_sample (0: read CDFs from global)
   // graph of one cyclic sweep (constant step)
   cudaGraphExec_t sweep_exec = nullptr;
+  uint64_t sweep_launches = 0;
   // NCCL
   ncclComm_t comm = nullptr;
   // diagnostics
@@ -215,7 +219,13 @@ cp_status launch_table(cp_sgd_s* h, int k) {
   return check_launch(h, "k_table");
 }
 
+cp_status launch_ut(cp_sgd_s* h, int n, int do_update, int do_table, int64_t row0, int64_t In, double alpha,
+                    const double* alpha_dev, bool use_sum);
+bool ut_fits(const cp_sgd_s* h, int64_t In);
+
 cp_status launch_table_any(cp_sgd_s* h, int k) {
+  if (h->sampler == CP_UNIFORM) return CP_OK;
+  if (ut_fits(h, h->dims[k])) return launch_ut(h, k, 0, 1, 0, h->dims[k], 0.0, nullptr, false);
   return h->dtype == CP_F64 ? launch_table<double>(h, k) : launch_table<float>(h, k);
 }
 
@@ -282,9 +292,27 @@ cp_status launch_gather_t(cp_sgd_s* h, int n) {
   p.In_local = h->In_local[n];
   p.Mp = (T*)h->Mp;
   p.Gp = (T*)h->Gp;
-  dim3 grid(h->ntiles[n], h->nchunks[n]);
-  k_gather<T, RPT><<<grid, kGatherThreads, 0, h->ls>>>(p);
+  const size_t smem = gather_smem_bytes<T, RPT>(h->R);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_gather<T, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(h->ntiles[n], h->nchunks[n], 1);
+  lc.blockDim = dim3(kGatherThreads, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = h->ls;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = h->cgather[n];
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_gather<T, RPT>, p);
   h->launches++;
+  if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_gather launch: %s", cudaGetErrorString(e));
   return check_launch(h, "k_gather");
 }
 
@@ -298,6 +326,78 @@ cp_status launch_gather(cp_sgd_s* h, int n) {
   }
 }
 
+// fused update + table (cluster kernel).  rows: [row0, row0 + In) of A^(n).
+template <typename T>
+cp_status launch_ut_t(cp_sgd_s* h, int n, int do_update, int do_table, int64_t row0, int64_t In, double alpha,
+                      const double* alpha_dev, bool use_sum) {
+  ProfScope ps(h, do_update ? kKUpdate : kKTable);
+  UTParams<T> p;
+  memset(&p, 0, sizeof p);
+  p.R = h->R;
+  p.strategy = h->sampler;
+  p.rule = h->rule;
+  p.do_update = do_update;
+  p.do_table = do_table;
+  p.In = In;
+  int CU = 1;
+  while (CU < 16 && CU * 32 < In) CU *= 2;
+  p.rows_per = ceil_div(In, CU);
+  p.nparts = h->nparts[n];
+  p.Mp = (const T*)h->Mp;
+  p.Gp = (const T*)h->Gp;
+  p.Msum = use_sum ? (const T*)h->Msum : nullptr;
+  p.Gsum = use_sum ? (const T*)h->Gsum : nullptr;
+  p.A = (T*)h->factors[n] + row0 * h->R;
+  p.S = h->S[n] ? (T*)h->S[n] + row0 * h->R : nullptr;
+  p.Gout = (T*)h->Gout + row0 * h->R;
+  p.Gam_out = (T*)h->Gam_out;
+  p.alpha = alpha;
+  p.alpha_dev = alpha_dev;
+  p.eta = h->eta;
+  p.b = h->bpar;
+  p.eps = h->eps;
+  p.iter = h->iter_dev;
+  p.p_out = h->pprob[n];
+  p.cdf = h->cdf[n];
+  p.Tout = h->Ttot + n;
+  p.status = h->status_dev;
+  const size_t smem = ut_smem_bytes(h->R, p.rows_per, sizeof(T));
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_update_table<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_update_table<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(CU, 1, 1);
+  lc.blockDim = dim3(kUTThreads, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = h->ls;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CU;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_update_table<T>, p);
+  h->launches++;
+  if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_update_table launch: %s", cudaGetErrorString(e));
+  return check_launch(h, "k_update_table");
+}
+
+cp_status launch_ut(cp_sgd_s* h, int n, int do_update, int do_table, int64_t row0, int64_t In, double alpha,
+                    const double* alpha_dev, bool use_sum) {
+  return h->dtype == CP_F64 ? launch_ut_t<double>(h, n, do_update, do_table, row0, In, alpha, alpha_dev, use_sum)
+                            : launch_ut_t<float>(h, n, do_update, do_table, row0, In, alpha, alpha_dev, use_sum);
+}
+
+bool ut_fits(const cp_sgd_s* h, int64_t In) {
+  int CU = 1;
+  while (CU < 16 && CU * 32 < In) CU *= 2;
+  return ut_smem_bytes(h->R, ceil_div(In, CU), h->esz) <= 220 * 1024;
+}
+
 template <typename T>
 cp_status launch_update(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, bool use_sum) {
   ProfScope ps(h, kKUpdate);
@@ -306,7 +406,7 @@ cp_status launch_update(cp_sgd_s* h, int n, double alpha, const double* alpha_de
   p.R = h->R;
   p.In_local = h->In_local[n];
   p.row0 = h->row0[n];
-  p.nchunks = h->nchunks[n];
+  p.nchunks = h->nparts[n];
   p.Mp = (const T*)h->Mp;
   p.Gp = (const T*)h->Gp;
   p.Msum = use_sum ? (const T*)h->Msum : nullptr;
@@ -334,7 +434,7 @@ cp_status launch_reduce(cp_sgd_s* h, int n) {
   ProfScope ps(h, kKReduce);
   const int64_t tot = std::max<int64_t>((int64_t)h->R * h->In_local[n], (int64_t)h->R * h->R);
   k_reduce_partials<T><<<(unsigned)ceil_div(tot, 256), 256, 0, h->ls>>>(
-      (const T*)h->Mp, (const T*)h->Gp, h->nchunks[n], h->R, h->In_local[n], (T*)h->Msum, (T*)h->Gsum);
+      (const T*)h->Mp, (const T*)h->Gp, h->nparts[n], h->R, h->In_local[n], (T*)h->Msum, (T*)h->Gsum);
   h->launches++;
   return check_launch(h, "k_reduce_partials");
 }
@@ -352,11 +452,21 @@ cp_status phase0(cp_sgd_s* h, int n) {
 }
 
 cp_status phase1(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
+  const bool last_sharded = sharded(h) && n == h->N - 1;
+  if (ut_fits(h, h->In_local[n])) {
+    if (!last_sharded) return launch_ut(h, n, 1, 1, 0, h->dims[n], alpha, alpha_dev, sharded(h));
+    return launch_ut(h, n, 1, 0, h->row0[n], h->In_local[n], alpha, alpha_dev, true);
+  }
   return h->dtype == CP_F64 ? launch_update<double>(h, n, alpha, alpha_dev, sharded(h))
                             : launch_update<float>(h, n, alpha, alpha_dev, sharded(h));
 }
 
-cp_status phase2(cp_sgd_s* h, int n) { return launch_table_any(h, n); }
+// table refresh of mode n (already done inside phase 1 unless the rows had to be gathered first)
+cp_status phase2(cp_sgd_s* h, int n) {
+  const bool last_sharded = sharded(h) && n == h->N - 1;
+  if (ut_fits(h, h->In_local[n]) && !last_sharded) return CP_OK;
+  return launch_table_any(h, n);
+}
 
 cp_status nccl_check(cp_sgd_s* h, ncclResult_t r, const char* what) {
   if (r != 0) return h->fail(CP_ENCCL, "%s: %s", what, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
@@ -546,13 +656,16 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
     h->ntiles[n] = (int)ceil_div(h->In_local[n], kTI);
     const int64_t bm = h->bmax[n];
     int64_t nch = std::max<int64_t>(1, 296 / h->ntiles[n]);
-    nch = std::min<int64_t>(nch, ceil_div(bm, 16));
-    nch = std::max<int64_t>(nch, 1);
+    nch = std::min<int64_t>(nch, std::max<int64_t>(1, ceil_div(bm, 8)));
+    int CG = 1;
+    while (CG * 2 <= nch && CG < 8) CG *= 2;
     h->TB[n] = ceil_div(bm, nch);
-    h->nchunks[n] = (int)ceil_div(bm, h->TB[n]);
+    h->nchunks[n] = (int)(ceil_div(ceil_div(bm, h->TB[n]), CG) * CG);
+    h->cgather[n] = CG;
+    h->nparts[n] = h->nchunks[n] / CG;
     Bmax_all = std::max(Bmax_all, bm);
-    Mp_elems = std::max(Mp_elems, (int64_t)h->nchunks[n] * h->R * h->In_local[n]);
-    Gp_elems = std::max(Gp_elems, (int64_t)h->nchunks[n] * h->R * h->R);
+    Mp_elems = std::max(Mp_elems, (int64_t)h->nparts[n] * h->R * h->In_local[n]);
+    Gp_elems = std::max(Gp_elems, (int64_t)h->nparts[n] * h->R * h->R);
     Msum_elems = std::max(Msum_elems, (int64_t)h->R * h->In_local[n]);
     Imax = std::max(Imax, h->dims[n]);
   }
@@ -875,6 +988,7 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
     for (int n = 0; n < h->N && !st; ++n) st = do_step(h, n, h->alpha, h->alpha_dev, rr ? *rr : none);
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     h->ls = h->stream;
+    h->sweep_launches = h->launches - l0;
     h->launches = l0;
     if (st) {
       if (g) cudaGraphDestroy(g);
@@ -885,14 +999,9 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return h->fail(CP_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
   }
-  // kernels per sweep (counted once per replay)
-  uint64_t per_sweep = 0;
-  for (int n = 0; n < h->N; ++n) {
-    per_sweep += 3 + (h->sampler != CP_UNIFORM ? 1 : 0) + (sharded(h) ? 1 : 0);
-  }
   for (int s = 0; s < nsweeps; ++s) {
     CUDA_TRY(h, cudaGraphLaunch(h->sweep_exec, h->stream));
-    h->launches += per_sweep;
+    h->launches += h->sweep_launches;
     h->iter_host += h->N;
   }
   if (nsweeps > 0) h->last_mode = h->N - 1;

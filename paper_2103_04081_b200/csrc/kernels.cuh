@@ -13,6 +13,7 @@
 // Citations: PAPER.md:<lines> (<label>); R<k> = DESIGN.md readings.
 #pragma once
 #include <cstdint>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "philox.cuh"
@@ -411,15 +412,34 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
 constexpr int kGatherThreads = 256;
 constexpr int kTI = 128;
 
+template <typename T>
+__host__ __device__ constexpr int gather_sb() { return sizeof(T) == 8 ? 16 : 32; }
+
+// dynamic shared memory of k_gather<T, RPT>: max(main loop buffers, reduction buffers)
+template <typename T, int RPT>
+__host__ __device__ constexpr size_t gather_smem_bytes(int R) {
+  // main: xs[SB][TI] + zw[SB][RP] + zu[SB][RP] + base[SB] (int64) + owned[SB] (int)
+  // red : M tile [R][TI] + Gamma [R][R]
+  return (size_t)(gather_sb<T>() * (kTI + 4 * RPT)) * sizeof(T) + gather_sb<T>() * 12 >
+                 (size_t)(R * kTI + R * R) * sizeof(T)
+             ? (size_t)(gather_sb<T>() * (kTI + 4 * RPT)) * sizeof(T) + gather_sb<T>() * 12
+             : (size_t)(R * kTI + R * R) * sizeof(T);
+}
+
+// grid = (I-tiles, chunks) with cluster dims (1, CG): the CG chunk-CTAs of one I-tile reduce
+// their partial tiles through distributed shared memory in rank order (deterministic), so
+// k_update_table reads chunks/CG partials.
 template <typename T, int RPT>
 __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherParams<T> p) {
+  namespace cg = cooperative_groups;
   constexpr int RP = 2 * RPT;
-  constexpr int kSB = sizeof(T) == 8 ? 16 : 32;  // fibers per sub-batch (static smem <= 48 KB)
-  __shared__ __align__(16) T xs[kSB][kTI];
-  __shared__ __align__(16) T zw[kSB][RP];
-  __shared__ __align__(16) T zu[kSB][RP];
-  __shared__ int64_t base[kSB];
-  __shared__ int owned[kSB];
+  constexpr int kSB = gather_sb<T>();
+  extern __shared__ __align__(16) unsigned char g_sm[];
+  T* xs = reinterpret_cast<T*>(g_sm);            // [kSB][kTI]
+  T* zw = xs + kSB * kTI;                         // [kSB][RP]
+  T* zu = zw + kSB * RP;                          // [kSB][RP]
+  int64_t* base = reinterpret_cast<int64_t*>(zu + kSB * RP);
+  int* owned = reinterpret_cast<int*>(base + kSB);
   const int N = p.N, n = p.n, R = p.R;
   const int tid = threadIdx.x, il = tid % kTI, half = tid / kTI;
   const int64_t i0 = (int64_t)blockIdx.x * kTI;
@@ -466,7 +486,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherParams<T> p) {
       base[tid] = off;
       owned[tid] = own;
     }
-    // (b) SKR rows, weighted and unweighted (zero padded to RP)
+    // (b) SKR rows (Alg. 1), weighted and unweighted, zero padded to RP
     for (int e = tid; e < kSB * RP; e += kGatherThreads) {
       const int bb = e / RP, r = e % RP;
       T z = T(0), zwv = T(0);
@@ -480,11 +500,11 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherParams<T> p) {
         }
         zwv = (T)p.w[s + bb] * z;
       }
-      zu[bb][r] = z;
-      zw[bb][r] = zwv;
+      zu[bb * RP + r] = z;
+      zw[bb * RP + r] = zwv;
     }
     __syncthreads();
-    // (c) fiber segments: warp-coalesced along the row index (all loads issued before use)
+    // (c) fiber segments (Alg. 5): warp-coalesced along the row index, all loads in flight first
     {
       T v[kSB / 2];
 #pragma unroll
@@ -494,14 +514,14 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherParams<T> p) {
         if (bb < nb && row_ok && owned[bb]) v[q] = ldg(p.X + base[bb] + (i0 + il) * estride);
       }
 #pragma unroll
-      for (int q = 0; q < kSB / 2; ++q) xs[half + 2 * q][il] = v[q];
+      for (int q = 0; q < kSB / 2; ++q) xs[(half + 2 * q) * kTI + il] = v[q];
     }
     __syncthreads();
-    // (d) M tile += x zw^T  (rows il, columns half*RPT .. +RPT)
+    // (d) M tile += x zw^T
     for (int bb = 0; bb < nb; ++bb) {
-      const T x = xs[bb][il];
+      const T x = xs[bb * kTI + il];
 #pragma unroll
-      for (int j = 0; j < RPT; ++j) acc[j] += x * zw[bb][half * RPT + j];
+      for (int j = 0; j < RPT; ++j) acc[j] += x * zw[bb * RP + half * RPT + j];
     }
     if (do_gamma) {
 #pragma unroll
@@ -510,29 +530,50 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherParams<T> p) {
         if (e < R * R) {
           const int r1 = e / R, r2 = e % R;
           T g = gacc[j];
-          for (int bb = 0; bb < nb; ++bb) g += zw[bb][r1] * zu[bb][r2];
+          for (int bb = 0; bb < nb; ++bb) g += zw[bb * RP + r1] * zu[bb * RP + r2];
           gacc[j] = g;
         }
       }
     }
     __syncthreads();
   }
-  // write partials: Mp[chunk][r][i] (coalesced over i)
-  if (row_ok) {
-    T* dst = p.Mp + (int64_t)chunk * R * p.In_local + i0 + il;
+  // ---- cluster reduction over the CG chunk-CTAs of this I-tile (rank order) ----
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CG = (int)cluster.dim_blocks().y;
+  const int q = (int)cluster.block_index().y;
+  T* mred = reinterpret_cast<T*>(g_sm);   // [R][kTI] (aliases the main-loop buffers; synced above)
+  T* gred = mred + R * kTI;               // [R][R]
 #pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-      const int r = half * RPT + j;
-      if (r < R) dst[(int64_t)r * p.In_local] = acc[j];
-    }
+  for (int j = 0; j < RPT; ++j) {
+    const int r = half * RPT + j;
+    if (r < R) mred[r * kTI + il] = acc[j];
   }
   if (do_gamma) {
 #pragma unroll
     for (int j = 0; j < GPT; ++j) {
       const int e = tid + j * kGatherThreads;
-      if (e < R * R) p.Gp[(int64_t)chunk * R * R + e] = gacc[j];
+      if (e < R * R) gred[e] = gacc[j];
     }
   }
+  cluster.sync();
+  const int part = chunk / CG;
+  const int E = R * kTI;
+  const int per = (E + CG - 1) / CG;
+  for (int e = q * per + tid; e < min(E, (q + 1) * per); e += kGatherThreads) {
+    T sum = T(0);
+    for (int qq = 0; qq < CG; ++qq) sum += cluster.map_shared_rank(mred, qq)[e];
+    const int r = e / kTI, ii = e % kTI;
+    if (i0 + ii < p.In_local) p.Mp[((int64_t)part * R + r) * p.In_local + i0 + ii] = sum;
+  }
+  if (do_gamma) {
+    const int EG = R * R, pg = (EG + CG - 1) / CG;
+    for (int e = q * pg + tid; e < min(EG, (q + 1) * pg); e += kGatherThreads) {
+      T sum = T(0);
+      for (int qq = 0; qq < CG; ++qq) sum += cluster.map_shared_rank(gred, qq)[e];
+      p.Gp[(int64_t)part * R * R + e] = sum;
+    }
+  }
+  cluster.sync();  // keep every CTA's shared memory alive until the others finished reading it
 }
 
 // ==========================================================================================
@@ -601,6 +642,339 @@ __global__ void __launch_bounds__(kUpdThreads) k_update(UpdateParams<T> p) {
       }
     }
   }
+}
+
+// ==========================================================================================
+// (a6, a7, a8, a1, a9) fused update + table refresh: ONE thread-block cluster of CU <= 16 CTAs
+// owns all rows of A^(n) (CTA q: rows [q*rows_per, ...)).
+//   stage A (do_update): Gamma and M from the gather partials (fixed order), G = A Gamma - M,
+//            fixed / adaptive update of the owned rows (eq:proposed / eq:Aada), r += 1
+//   stage B (do_table) : importance table of the NEW A^(n) (R9):
+//            leverage  -- partial fp64 Grams of the owned rows, summed over the cluster through
+//                         DSMEM in rank order (identical in every CTA), pivoted Cholesky (every CTA
+//                         redundantly, deterministic), l_i = ||L^{-1} a_{i,piv}||^2, p = l / rank
+//            euclidean -- ||A||_F^2 = rank-ordered sum of per-CTA partials, p = ||a_i||^2 / ||A||^2
+//            q = rint(p 2^32) (>= 1 if p > 0); CDF = integer scan: CTA-local scan + exclusive
+//            prefix of the lower ranks' totals read through DSMEM.
+// ==========================================================================================
+template <typename T>
+struct UTParams {
+  int R, strategy, rule, do_update, do_table;
+  int64_t In;            // rows of A^(n) (all rows)
+  int64_t rows_per;      // rows per CTA
+  int nparts;            // gather partials
+  const T* Mp;           // [nparts][R][In]
+  const T* Gp;           // [nparts][R][R]
+  const T* Msum;         // sharded path: reduced M [R][In] (else NULL)
+  const T* Gsum;         // sharded path: reduced Gamma (else NULL)
+  T* A;
+  T* S;
+  T* Gout;
+  T* Gam_out;
+  double alpha;
+  const double* alpha_dev;
+  double eta, b, eps;
+  uint64_t* iter;
+  double* p_out;
+  uint64_t* cdf;
+  uint64_t* Tout;
+  int* status;
+};
+
+constexpr int kUTThreads = 256;
+
+// shared-memory carve-up of k_update_table (bytes), also used by the host to size the launch
+__host__ __device__ inline size_t ut_smem_bytes(int R, int64_t rows_per, size_t esz) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) { off = (off + 15) / 16 * 16; off += bytes; };
+  take(esz * R * R);                     // Gam
+  take(esz * rows_per * (R + 1));        // Aold
+  take(esz * rows_per * (R + 1));        // Anew
+  take(sizeof(double) * (R * (R + 1) / 2 + 1));  // partial Gram / partial ||A||^2 (read by peers)
+  take(sizeof(double) * R * R);          // Gm (Gram -> Cholesky factor)
+  take(sizeof(double) * rows_per);       // per-row p
+  take(sizeof(unsigned long long) * rows_per);   // per-row q -> local inclusive scan
+  take(sizeof(unsigned long long) * 2);  // CTA total (read by peers), pad
+  return off + 16;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CU = (int)cluster.num_blocks();
+  const int q = (int)cluster.block_rank();
+  const int R = p.R, tid = threadIdx.x;
+  const int64_t r_beg = min((int64_t)q * p.rows_per, p.In);
+  const int64_t r_end = min(r_beg + p.rows_per, p.In);
+  const int nr = (int)(r_end - r_beg);
+  const int RS = R + 1;  // padded row stride
+  extern __shared__ __align__(16) unsigned char ut_sm[];
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    off = (off + 15) / 16 * 16;
+    unsigned char* ptr = ut_sm + off;
+    off += bytes;
+    return ptr;
+  };
+  T* Gam = reinterpret_cast<T*>(carve(sizeof(T) * R * R));
+  T* Aold = reinterpret_cast<T*>(carve(sizeof(T) * p.rows_per * RS));
+  T* Anew = reinterpret_cast<T*>(carve(sizeof(T) * p.rows_per * RS));
+  double* gpart = reinterpret_cast<double*>(carve(sizeof(double) * (R * (R + 1) / 2 + 1)));
+  double* Gm = reinterpret_cast<double*>(carve(sizeof(double) * R * R));
+  double* prow = reinterpret_cast<double*>(carve(sizeof(double) * p.rows_per));
+  unsigned long long* qrow = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * p.rows_per));
+  unsigned long long* qtot = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * 2));
+  __shared__ int piv[kMaxRank];
+  __shared__ int s_rank, s_bad, s_stop, s_jm;
+  __shared__ double s_red[kUTThreads / 32];
+  __shared__ unsigned long long s_wtot[kUTThreads / 32];
+  __shared__ double s_fro, s_tol;
+  if (tid == 0) { s_bad = 0; s_rank = R; s_stop = 0; }
+
+  // ---------------- stage A: update ----------------
+  for (int e = tid; e < nr * R; e += kUTThreads) {
+    const int il = e / R, c = e % R;
+    Aold[il * RS + c] = p.A[(r_beg + il) * R + c];
+  }
+  if (p.do_update) {
+    for (int e = tid; e < R * R; e += kUTThreads) {
+      T g;
+      if (p.Gsum) {
+        g = p.Gsum[e];
+      } else {
+        g = T(0);
+        for (int c = 0; c < p.nparts; ++c) g += p.Gp[(int64_t)c * R * R + e];
+      }
+      Gam[e] = g;
+      if (q == 0 && p.Gam_out) p.Gam_out[e] = g;
+    }
+    __syncthreads();
+    const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
+    if (q == 0 && tid == 0 && p.iter) *p.iter += 1;  // r <- r + 1
+    // element (il, r): consecutive threads -> consecutive rows (coalesced partial reads)
+    for (int e = tid; e < nr * R; e += kUTThreads) {
+      const int il = e % nr, r = e / nr;
+      const int64_t i = r_beg + il;
+      T m;
+      if (p.Msum) {
+        m = p.Msum[(int64_t)r * p.In + i];
+      } else {
+        m = T(0);
+        for (int c = 0; c < p.nparts; ++c) m += p.Mp[((int64_t)c * R + r) * p.In + i];
+      }
+      T ag = T(0);
+      for (int c = 0; c < R; ++c) ag += Aold[il * RS + c] * Gam[c * R + r];
+      const T g = ag - m;
+      const int64_t gi = i * R + r;
+      p.Gout[gi] = g;
+      const T a = Aold[il * RS + r];
+      T an = a;
+      if (p.rule == 0) {
+        an = a - (T)alpha * g;
+      } else {
+        const T sv = p.S[gi] + g * g;
+        p.S[gi] = sv;
+        if (sv > T(0)) {
+          T step;
+          if (p.eps == 0.0) step = (T)p.eta / sqrt((T)p.b + sv);
+          else step = (T)p.eta / (T)pow((double)((T)p.b + sv), 0.5 + p.eps);
+          an = a - step * g;
+        }
+      }
+      p.A[gi] = an;
+      Anew[il * RS + r] = an;
+    }
+  } else {
+    for (int e = tid; e < nr * R; e += kUTThreads) {
+      const int il = e / R, c = e % R;
+      Anew[il * RS + c] = Aold[il * RS + c];
+    }
+  }
+  __syncthreads();
+  if (!p.do_table || p.strategy == 0) return;  // uniform tables are constant (no cluster barrier used)
+
+  // ---------------- stage B: table of the new A^(n) ----------------
+  const bool lev = (p.strategy == 1 || p.strategy == 3);
+  const int P = R * (R + 1) / 2;
+  if (lev) {
+    for (int pair = tid; pair < P; pair += kUTThreads) {
+      int r1 = 0, rem = pair;
+      while (rem >= R - r1) { rem -= R - r1; ++r1; }
+      const int r2 = r1 + rem;
+      double acc = 0.0;
+      for (int il = 0; il < nr; ++il) acc += (double)Anew[il * RS + r1] * (double)Anew[il * RS + r2];
+      gpart[pair] = acc;
+    }
+  } else {
+    double acc = 0.0;
+    for (int il = tid; il < nr; il += kUTThreads) {
+      double rs = 0.0;
+      for (int c = 0; c < R; ++c) rs += (double)Anew[il * RS + c] * (double)Anew[il * RS + c];
+      prow[il] = rs;
+      acc += rs;
+    }
+    // fixed-order block reduction
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((tid & 31) == 0) s_red[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kUTThreads / 32; ++w) t += s_red[w];
+      gpart[0] = t;
+    }
+  }
+  cluster.sync();
+  if (lev) {
+    for (int pair = tid; pair < P; pair += kUTThreads) {
+      double sum = 0.0;
+      for (int qq = 0; qq < CU; ++qq) sum += cluster.map_shared_rank(gpart, qq)[pair];
+      int r1 = 0, rem = pair;
+      while (rem >= R - r1) { rem -= R - r1; ++r1; }
+      const int r2 = r1 + rem;
+      Gm[r1 * R + r2] = sum;
+      Gm[r2 * R + r1] = sum;
+    }
+    if (tid < R) piv[tid] = tid;
+    __syncthreads();
+    // pivoted Cholesky (right-looking, full symmetric storage); rank tolerance R4(b)
+    if (tid == 0) {
+      double d0 = 0.0;
+      bool fin = true;
+      for (int j = 0; j < R; ++j) {
+        d0 = fmax(d0, Gm[j * R + j]);
+        fin = fin && (Gm[j * R + j] == Gm[j * R + j]) && Gm[j * R + j] < 1.7e308;
+      }
+      if (!fin) s_bad |= 8;
+      s_tol = (double)(p.In > R ? p.In : R) * 2.220446049250313e-16 * d0;
+    }
+    __syncthreads();
+    int k = 0;
+    for (; k < R; ++k) {
+      if (tid < 32) {  // warp 0: pivot = argmax of the remaining diagonal (lowest index on ties)
+        double best = -1.0;
+        int bj = k;
+        for (int j = k + tid; j < R; j += 32) {
+          const double d = Gm[j * R + j];
+          if (d > best) { best = d; bj = j; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_down_sync(0xffffffffu, best, o);
+          const int oj = __shfl_down_sync(0xffffffffu, bj, o);
+          if (ob > best || (ob == best && oj < bj)) { best = ob; bj = oj; }
+        }
+        if (tid == 0) {
+          s_jm = bj;
+          s_stop = !(best > s_tol);
+          if (!s_stop && bj != k) { const int t = piv[k]; piv[k] = piv[bj]; piv[bj] = t; }
+        }
+      }
+      __syncthreads();
+      if (s_stop) break;
+      const int jm = s_jm;
+      if (jm != k) {
+        for (int c = tid; c < R; c += kUTThreads) {
+          const double t = Gm[k * R + c]; Gm[k * R + c] = Gm[jm * R + c]; Gm[jm * R + c] = t;
+        }
+        __syncthreads();
+        for (int rr = tid; rr < R; rr += kUTThreads) {
+          const double t = Gm[rr * R + k]; Gm[rr * R + k] = Gm[rr * R + jm]; Gm[rr * R + jm] = t;
+        }
+        __syncthreads();
+      }
+      const double lkk = sqrt(Gm[k * R + k]);
+      for (int i = k + 1 + tid; i < R; i += kUTThreads) Gm[i * R + k] = Gm[i * R + k] / lkk;
+      __syncthreads();
+      if (tid == 0) Gm[k * R + k] = lkk;
+      const int m = R - k - 1;
+      for (int e = tid; e < m * m; e += kUTThreads) {
+        const int i = k + 1 + e / m, j = k + 1 + e % m;
+        Gm[i * R + j] -= Gm[i * R + k] * Gm[j * R + k];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      s_rank = k;
+      if (k == 0) s_bad |= 2;
+    }
+    __syncthreads();
+    const int rank = s_rank;
+    // scores of the owned rows: forward substitution L y = a_{piv}
+    for (int il = tid; il < nr; il += kUTThreads) {
+      double y[kMaxRank];
+      double l = 0.0;
+      for (int j = 0; j < rank; ++j) {
+        double v = (double)Anew[il * RS + piv[j]];
+        for (int t = 0; t < j; ++t) v -= Gm[j * R + t] * y[t];
+        y[j] = v / Gm[j * R + j];
+        l += y[j] * y[j];
+      }
+      prow[il] = rank > 0 ? l / (double)rank : 0.0;
+    }
+  } else {
+    if (tid == 0) {
+      double fro = 0.0;
+      for (int qq = 0; qq < CU; ++qq) fro += cluster.map_shared_rank(gpart, qq)[0];
+      s_fro = fro;
+      if (!(fro == fro) || fro > 1.7e308) s_bad |= 8;
+      else if (!(fro > 0.0)) s_bad |= 2;
+    }
+    __syncthreads();
+    const double fro = s_fro;
+    for (int il = tid; il < nr; il += kUTThreads) prow[il] = prow[il] / fro;
+  }
+  __syncthreads();
+  // quantise + CTA-local inclusive scan (each thread a contiguous segment of rows)
+  const int seg = (nr + kUTThreads - 1) / kUTThreads;
+  const int a0 = min(tid * seg, nr), a1 = min(a0 + seg, nr);
+  unsigned long long local = 0;
+  int bad = 0;
+  for (int il = a0; il < a1; ++il) {
+    const double pv = prow[il];
+    unsigned long long qv;
+    if (!(pv == pv) || pv > 2.0) {
+      bad = 1;
+      qv = 0;
+    } else if (pv > 0.0) {
+      const double sc = rint(pv * 4294967296.0);
+      qv = (sc < 1.0) ? 1ull : (unsigned long long)sc;
+    } else {
+      qv = 0;
+    }
+    if (p.p_out) p.p_out[r_beg + il] = pv;
+    local += qv;
+    qrow[il] = local;  // inclusive within the segment
+  }
+  if (bad) atomicOr(&s_bad, 8);
+  const int lane = tid & 31, wid = tid >> 5;
+  unsigned long long incl = local;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_wtot[wid] = incl;
+  __syncthreads();
+  unsigned long long wpre = 0;
+  for (int w = 0; w < wid; ++w) wpre += s_wtot[w];
+  const unsigned long long seg_pre = wpre + incl - local;
+  if (tid == kUTThreads - 1) qtot[0] = seg_pre + local;  // CTA total
+  __syncthreads();
+  cluster.sync();
+  unsigned long long cta_pre = 0, total = 0;
+  for (int qq = 0; qq < CU; ++qq) {
+    const unsigned long long t = cluster.map_shared_rank(qtot, qq)[0];
+    if (qq < q) cta_pre += t;
+    total += t;
+  }
+  for (int il = a0; il < a1; ++il) p.cdf[r_beg + il] = cta_pre + seg_pre + qrow[il];
+  if (tid == 0) {
+    if (q == 0) *p.Tout = total;
+    int st = 0;
+    if (s_bad & 8) st = -8;
+    else if ((s_bad & 2) || (q == 0 && total == 0)) st = -3;
+    if (st != 0) atomicCAS(p.status, 0, st);
+  }
+  cluster.sync();  // peers may still read this CTA's shared memory
 }
 
 // reduce chunk partials into Msum [R][In_local] and Gsum [R][R] (sharded path, phase 0)

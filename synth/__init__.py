@@ -59,7 +59,7 @@ class Config:
 
 # BASELINE.json configs, index-aligned (configs[0] .. configs[4]).
 CONFIGS = {
-    "C1": Config("C1", (60, 60, 60), 5, "f64", 64, "fixed", row_sigma=1.0, noise=1e-2, alpha=0.01),
+    "C1": Config("C1", (60, 60, 60), 5, "f64", 64, "fixed", row_sigma=1.0, noise=1e-2, alpha=0.002),
     "C2": Config("C2", (400, 400, 400), 20, "f32", 512, "adaptive", row_sigma=1.5, unit_columns=True, noise=1e-2,
                  eta=0.03),
     "C3": Config("C3", (100, 100, 100, 100), 10, "f32", 1024, "adaptive", row_sigma=1.0, congruence=0.9,
