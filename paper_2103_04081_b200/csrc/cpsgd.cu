@@ -119,7 +119,11 @@ struct cp_sgd_s {
   uint64_t* Ttot = nullptr;
   int32_t* idx = nullptr;
   double* w = nullptr;
-  int64_t* beff = nullptr;
+  int64_t* beff = nullptr;       // rows of the prefetched batch
+  int64_t* beff_api = nullptr;   // rows of the last cp_sgd_sample call
+  void* zrow = nullptr;          // prefetched unweighted SKR rows [Bmax][R]
+  int64_t* fbase = nullptr;      // prefetched fiber offsets [Bmax]
+  int pref_mode = -1;            // mode whose batch (at the current r) sits in idx/w/zrow/fbase
   uint64_t* iter_dev = nullptr;
   uint64_t* iter_tmp = nullptr;
   int* status_dev = nullptr;
@@ -142,6 +146,7 @@ struct cp_sgd_s {
   // graph of one cyclic sweep (constant step)
   cudaGraphExec_t sweep_exec = nullptr;
   uint64_t sweep_launches = 0;
+  int graph_end_pref = -1;
   // NCCL
   ncclComm_t comm = nullptr;
   // diagnostics
@@ -220,44 +225,70 @@ cp_status launch_table(cp_sgd_s* h, int k) {
 }
 
 cp_status launch_ut(cp_sgd_s* h, int n, int do_update, int do_table, int64_t row0, int64_t In, double alpha,
-                    const double* alpha_dev, bool use_sum);
+                    const double* alpha_dev, bool use_sum, int next_mode);
 bool ut_fits(const cp_sgd_s* h, int64_t In);
 
 cp_status launch_table_any(cp_sgd_s* h, int k) {
   if (h->sampler == CP_UNIFORM) return CP_OK;
-  if (ut_fits(h, h->dims[k])) return launch_ut(h, k, 0, 1, 0, h->dims[k], 0.0, nullptr, false);
+  if (ut_fits(h, h->dims[k])) return launch_ut(h, k, 0, 1, 0, h->dims[k], 0.0, nullptr, false, -1);
   return h->dtype == CP_F64 ? launch_table<double>(h, k) : launch_table<float>(h, k);
 }
 
-cp_status launch_sample(cp_sgd_s* h, int n, const uint64_t* iter_ptr, int32_t* idx, double* w) {
-  ProfScope ps(h, kKSample);
-  SampleParams p;
+void fill_sample_params(cp_sgd_s* h, SampleParams& p, int n, const uint64_t* iter_ptr, uint64_t iter_add,
+                        int32_t* idx, double* w, int64_t* beff, bool prefetch) {
   memset(&p, 0, sizeof p);
   p.N = h->N;
   p.n = n;
+  p.R = h->R;
   p.strategy = h->sampler;
   p.B = h->B;
   for (int k = 0; k < h->N; ++k) {
     p.dims[k] = h->dims[k];
     p.cdf[k] = h->cdf[k];
+    p.factors[k] = h->factors[k];
+    p.ldims[k] = h->ldims[k];
+    p.lstride[k] = h->lstride[k];
   }
   for (int q = 0; q < h->N - 1; ++q) p.window[q] = h->window[n][q];
   p.Ttot = h->Ttot;
   p.seed = h->seed;
   p.iter = iter_ptr;
+  p.iter_add = iter_add;
   p.idx = idx;
   p.w = w;
-  p.beff = h->beff;
+  p.beff = beff;
   p.bmax = h->bmax[n];
+  p.lo_last = h->lo_last;
+  p.mode_major = h->Xmm[n] ? 1 : 0;
+  p.pitch = h->pitch[n];
+  if (prefetch) {
+    p.zrow = h->zrow;
+    p.fbase = h->fbase;
+  }
+}
+
+size_t sample_cdf_bytes(const cp_sgd_s* h, int n) {
+  if (h->sampler == CP_UNIFORM) return 0;
   int64_t need = 0;
   for (int k = 0; k < h->N; ++k)
     if (k != n) need += h->dims[k];
-  size_t smem = (size_t)need * sizeof(uint64_t);
-  p.stage_smem = (h->sampler != CP_UNIFORM && smem <= (size_t)h->sample_smem) ? 1 : 0;
+  return (size_t)need * sizeof(uint64_t);
+}
+
+cp_status launch_sample(cp_sgd_s* h, int n, const uint64_t* iter_ptr, int32_t* idx, double* w, int64_t* beff,
+                        bool prefetch) {
+  ProfScope ps(h, kKSample);
+  SampleParams p;
+  fill_sample_params(h, p, n, iter_ptr, 0, idx, w, beff, prefetch);
+  size_t smem = sample_cdf_bytes(h, n);
+  p.stage_smem = (smem > 0 && smem <= (size_t)h->sample_smem) ? 1 : 0;
   if (!p.stage_smem) smem = 0;
   const int threads = 256;
-  const int64_t blocks = std::max<int64_t>(1, ceil_div(h->bmax[n], threads));
-  k_sample<<<(unsigned)blocks, threads, smem, h->ls>>>(p);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(h->bmax[n], threads), 148));
+  if (h->dtype == CP_F64)
+    k_sample<double><<<(unsigned)blocks, threads, smem, h->ls>>>(p);
+  else
+    k_sample<float><<<(unsigned)blocks, threads, smem, h->ls>>>(p);
   h->launches++;
   return check_launch(h, "k_sample");
 }
@@ -273,7 +304,6 @@ cp_status launch_gather_t(cp_sgd_s* h, int n) {
   for (int k = 0; k < h->N; ++k) {
     p.ldims[k] = h->ldims[k];
     p.lstride[k] = h->lstride[k];
-    p.factors[k] = (const T*)h->factors[k];
   }
   p.lo_last = h->lo_last;
   if (h->Xmm[n]) {
@@ -285,7 +315,8 @@ cp_status launch_gather_t(cp_sgd_s* h, int n) {
     p.mode_major = 0;
     p.pitch = 0;
   }
-  p.idx = h->idx;
+  p.fbase = h->fbase;
+  p.zrow = (const T*)h->zrow;
   p.w = h->w;
   p.beff = h->beff;
   p.TB = h->TB[n];
@@ -295,7 +326,7 @@ cp_status launch_gather_t(cp_sgd_s* h, int n) {
   const size_t smem = gather_smem_bytes<T, RPT>(h->R);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_gather<T, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_gather<T, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sample_smem);
     attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
@@ -329,7 +360,7 @@ cp_status launch_gather(cp_sgd_s* h, int n) {
 // fused update + table (cluster kernel).  rows: [row0, row0 + In) of A^(n).
 template <typename T>
 cp_status launch_ut_t(cp_sgd_s* h, int n, int do_update, int do_table, int64_t row0, int64_t In, double alpha,
-                      const double* alpha_dev, bool use_sum) {
+                      const double* alpha_dev, bool use_sum, int next_mode) {
   ProfScope ps(h, do_update ? kKUpdate : kKTable);
   UTParams<T> p;
   memset(&p, 0, sizeof p);
@@ -361,10 +392,20 @@ cp_status launch_ut_t(cp_sgd_s* h, int n, int do_update, int do_table, int64_t r
   p.cdf = h->cdf[n];
   p.Tout = h->Ttot + n;
   p.status = h->status_dev;
-  const size_t smem = ut_smem_bytes(h->R, p.rows_per, sizeof(T));
+  size_t smem = ut_smem_bytes(h->R, p.rows_per, sizeof(T));
+  if (next_mode >= 0) {
+    p.sample_next = 1;
+    fill_sample_params(h, p.sp, next_mode, h->iter_dev, 0, h->idx, h->w, h->beff, true);
+    const size_t cb = sample_cdf_bytes(h, next_mode);
+    p.sp.stage_smem = (cb > 0 && smem + cb <= (size_t)h->sample_smem) ? 1 : 0;
+    if (p.sp.stage_smem) smem += cb;
+  }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_update_table<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(k_update_table<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     cudaFuncSetAttribute(k_update_table<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr_set = true;
   }
@@ -387,15 +428,16 @@ cp_status launch_ut_t(cp_sgd_s* h, int n, int do_update, int do_table, int64_t r
 }
 
 cp_status launch_ut(cp_sgd_s* h, int n, int do_update, int do_table, int64_t row0, int64_t In, double alpha,
-                    const double* alpha_dev, bool use_sum) {
-  return h->dtype == CP_F64 ? launch_ut_t<double>(h, n, do_update, do_table, row0, In, alpha, alpha_dev, use_sum)
-                            : launch_ut_t<float>(h, n, do_update, do_table, row0, In, alpha, alpha_dev, use_sum);
+                    const double* alpha_dev, bool use_sum, int next_mode) {
+  return h->dtype == CP_F64
+             ? launch_ut_t<double>(h, n, do_update, do_table, row0, In, alpha, alpha_dev, use_sum, next_mode)
+             : launch_ut_t<float>(h, n, do_update, do_table, row0, In, alpha, alpha_dev, use_sum, next_mode);
 }
 
 bool ut_fits(const cp_sgd_s* h, int64_t In) {
   int CU = 1;
   while (CU < 16 && CU * 32 < In) CU *= 2;
-  return ut_smem_bytes(h->R, ceil_div(In, CU), h->esz) <= 220 * 1024;
+  return ut_smem_bytes(h->R, ceil_div(In, CU), h->esz) <= (size_t)h->sample_smem;
 }
 
 template <typename T>
@@ -443,28 +485,44 @@ bool sharded(const cp_sgd_s* h) { return h->world_size > 1; }
 
 // ---- one step, by phases ------------------------------------------------------------------------
 cp_status phase0(cp_sgd_s* h, int n) {
-  cp_status st = launch_sample(h, n, h->iter_dev, h->idx, h->w);
-  if (st) return st;
+  cp_status st = CP_OK;
+  if (h->pref_mode != n) {  // no prefetched batch for this mode: sample it now
+    st = launch_sample(h, n, h->iter_dev, h->idx, h->w, h->beff, true);
+    if (st) return st;
+    h->pref_mode = n;
+  }
   st = h->dtype == CP_F64 ? launch_gather<double>(h, n) : launch_gather<float>(h, n);
   if (st) return st;
+  h->pref_mode = -1;  // consumed
   if (sharded(h)) st = h->dtype == CP_F64 ? launch_reduce<double>(h, n) : launch_reduce<float>(h, n);
   return st;
 }
 
-cp_status phase1(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
+// update (+ table + next batch when the rows are all local)
+cp_status phase1(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, int next_mode) {
   const bool last_sharded = sharded(h) && n == h->N - 1;
   if (ut_fits(h, h->In_local[n])) {
-    if (!last_sharded) return launch_ut(h, n, 1, 1, 0, h->dims[n], alpha, alpha_dev, sharded(h));
-    return launch_ut(h, n, 1, 0, h->row0[n], h->In_local[n], alpha, alpha_dev, true);
+    cp_status st;
+    if (!last_sharded) {
+      st = launch_ut(h, n, 1, 1, 0, h->dims[n], alpha, alpha_dev, sharded(h), next_mode);
+      if (!st && next_mode >= 0) h->pref_mode = next_mode;
+      return st;
+    }
+    return launch_ut(h, n, 1, 0, h->row0[n], h->In_local[n], alpha, alpha_dev, true, -1);
   }
   return h->dtype == CP_F64 ? launch_update<double>(h, n, alpha, alpha_dev, sharded(h))
                             : launch_update<float>(h, n, alpha, alpha_dev, sharded(h));
 }
 
-// table refresh of mode n (already done inside phase 1 unless the rows had to be gathered first)
-cp_status phase2(cp_sgd_s* h, int n) {
+// table refresh of mode n when it could not be fused into phase 1 (rows gathered first / legacy)
+cp_status phase2(cp_sgd_s* h, int n, int next_mode) {
   const bool last_sharded = sharded(h) && n == h->N - 1;
-  if (ut_fits(h, h->In_local[n]) && !last_sharded) return CP_OK;
+  if (ut_fits(h, h->In_local[n])) {
+    if (!last_sharded) return CP_OK;
+    cp_status st = launch_ut(h, n, 0, 1, 0, h->dims[n], 0.0, nullptr, false, next_mode);
+    if (!st && next_mode >= 0) h->pref_mode = next_mode;
+    return st;
+  }
   return launch_table_any(h, n);
 }
 
@@ -505,12 +563,13 @@ cp_status exchange_after1(cp_sgd_s* h, int n, const std::vector<int64_t>& row_ra
 
 namespace {
 
-cp_status do_step(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, const std::vector<int64_t>& rr) {
+cp_status do_step(cp_sgd_s* h, int n, int next_mode, double alpha, const double* alpha_dev,
+                  const std::vector<int64_t>& rr) {
   cp_status st = phase0(h, n);
   if (!st) st = exchange_after0(h, n);
-  if (!st) st = phase1(h, n, alpha, alpha_dev);
+  if (!st) st = phase1(h, n, alpha, alpha_dev, next_mode);
   if (!st) st = exchange_after1(h, n, rr);
-  if (!st) st = phase2(h, n);
+  if (!st) st = phase2(h, n, next_mode);
   return st;
 }
 
@@ -688,6 +747,9 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
   ALLOC(h->idx, sizeof(int32_t) * Bmax_all * (h->N - 1));
   ALLOC(h->w, sizeof(double) * Bmax_all);
   ALLOC(h->beff, sizeof(int64_t));
+  ALLOC(h->beff_api, sizeof(int64_t));
+  ALLOC(h->zrow, h->esz * Bmax_all * h->R);
+  ALLOC(h->fbase, sizeof(int64_t) * Bmax_all);
   ALLOC(h->iter_dev, sizeof(uint64_t));
   ALLOC(h->iter_tmp, sizeof(uint64_t));
   ALLOC(h->status_dev, sizeof(int));
@@ -731,8 +793,9 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    h->sample_smem = std::min(optin, 200 * 1024);
-    cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sample_smem);
+    h->sample_smem = optin;  // opt-in maximum dynamic shared memory per block
+    cudaFuncSetAttribute(k_sample<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sample_smem);
+    cudaFuncSetAttribute(k_sample<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sample_smem);
     const int tbl = (int)(sizeof(double) * (kMaxRank * kMaxRank + 2080));
     cudaFuncSetAttribute(k_table<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, tbl);
     cudaFuncSetAttribute(k_table<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, tbl);
@@ -821,6 +884,9 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->idx);
   cudaFree(h->w);
   cudaFree(h->beff);
+  cudaFree(h->beff_api);
+  cudaFree(h->zrow);
+  cudaFree(h->fbase);
   cudaFree(h->iter_dev);
   cudaFree(h->iter_tmp);
   cudaFree(h->status_dev);
@@ -880,21 +946,21 @@ cp_status cp_sgd_sample(cp_sgd_t h, int32_t mode, uint64_t iter, int32_t* idx_de
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));  // pinned staging reuse
   pin[0] = iter;
   CUDA_TRY(h, cudaMemcpyAsync(h->iter_tmp, pin, sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream));
-  st = launch_sample(h, mode, h->iter_tmp, idx_dev, w_dev);
+  st = launch_sample(h, mode, h->iter_tmp, idx_dev, w_dev, h->beff_api, false);
   if (st) return st;
   if (batch_eff_host) {
-    CUDA_TRY(h, cudaMemcpyAsync(pin + 1, h->beff, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(pin + 1, h->beff_api, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     *batch_eff_host = (int64_t)pin[1];
   }
   return CP_OK;
 }
 
-static cp_status step_direct(cp_sgd_t h, int n, double alpha) {
+static cp_status step_direct(cp_sgd_t h, int n, double alpha, int next_mode) {
   const double a = (alpha < 0.0) ? h->alpha : alpha;
   auto* rr = rr_store(h, false);
   static const std::vector<int64_t> none;
-  cp_status st = do_step(h, n, a, nullptr, rr ? *rr : none);
+  cp_status st = do_step(h, n, next_mode, a, nullptr, rr ? *rr : none);
   if (st) return st;
   h->iter_host++;
   h->last_mode = n;
@@ -906,7 +972,7 @@ cp_status cp_sgd_step(cp_sgd_t h, int32_t mode, double alpha) {
   if (st) return st;
   if (sharded(h) && (h->flags & CP_FLAG_EXTERNAL_COMM))
     return h->fail(CP_ESTATE, "external-comm handles must use cp_sgd_step_phase");
-  return step_direct(h, mode, alpha);
+  return step_direct(h, mode, alpha, (mode + 1) % h->N);  // prefetch guess: the cyclic successor
 }
 
 cp_status cp_sgd_step_phase(cp_sgd_t h, int32_t mode, int32_t phase, double alpha) {
@@ -919,7 +985,7 @@ cp_status cp_sgd_step_phase(cp_sgd_t h, int32_t mode, int32_t phase, double alph
     return st;
   }
   if (phase == 1) {
-    st = phase1(h, mode, a, nullptr);
+    st = phase1(h, mode, a, nullptr, -1);
     if (!st && sharded(h) && !(h->flags & CP_FLAG_EXTERNAL_COMM)) {
       auto* rr = rr_store(h, false);
       static const std::vector<int64_t> none;
@@ -928,7 +994,7 @@ cp_status cp_sgd_step_phase(cp_sgd_t h, int32_t mode, int32_t phase, double alph
     return st;
   }
   if (phase == 2) {
-    st = phase2(h, mode);
+    st = phase2(h, mode, -1);
     if (!st) {
       h->iter_host++;
       h->last_mode = mode;
@@ -960,8 +1026,9 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
     for (int s = 0; s < nsweeps; ++s)
       for (int j = 0; j < h->N; ++j) {
         const int n = (order == CP_ORDER_CYCLIC) ? j : random_mode(h->seed, h->iter_host, h->N);
+        const int nx = (order == CP_ORDER_CYCLIC) ? (j + 1) % h->N : random_mode(h->seed, h->iter_host + 1, h->N);
         const double a = alpha_per_iter ? alpha_per_iter[(int64_t)s * h->N + j] : h->alpha;
-        cp_status st = step_direct(h, n, a);
+        cp_status st = step_direct(h, n, a, nx);
         if (st) return st;
       }
     return CP_OK;
@@ -985,7 +1052,12 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
     static const std::vector<int64_t> none;
     cp_status st = CP_OK;
     const uint64_t l0 = h->launches;
-    for (int n = 0; n < h->N && !st; ++n) st = do_step(h, n, h->alpha, h->alpha_dev, rr ? *rr : none);
+    const int saved_pref = h->pref_mode;
+    h->pref_mode = 0;  // the graph assumes the batch of mode 0 is prefetched when it starts
+    for (int n = 0; n < h->N && !st; ++n)
+      st = do_step(h, n, (n + 1) % h->N, h->alpha, h->alpha_dev, rr ? *rr : none);
+    h->graph_end_pref = h->pref_mode;
+    h->pref_mode = saved_pref;
     cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
     h->ls = h->stream;
     h->sweep_launches = h->launches - l0;
@@ -1000,7 +1072,12 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
     if (e != cudaSuccess) return h->fail(CP_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
   }
   for (int s = 0; s < nsweeps; ++s) {
+    if (h->pref_mode != 0) {
+      cp_status st = launch_sample(h, 0, h->iter_dev, h->idx, h->w, h->beff, true);
+      if (st) return st;
+    }
     CUDA_TRY(h, cudaGraphLaunch(h->sweep_exec, h->stream));
+    h->pref_mode = h->graph_end_pref;
     h->launches += h->sweep_launches;
     h->iter_host += h->N;
   }
@@ -1016,6 +1093,7 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
   for (int k = 0; k < h->N; ++k)
     CUDA_TRY(h, cudaMemcpyAsync(h->factors[k], factors_host[k], h->esz * h->dims[k] * h->R, cudaMemcpyHostToDevice,
                                 h->stream));
+  h->pref_mode = -1;
   // the host factors may differ from the device ones: rebuild every table first
   for (int k = 0; k < h->N; ++k) {
     st = launch_table_any(h, k);
@@ -1122,11 +1200,13 @@ cp_status cp_sgd_set_iter(cp_sgd_t h, uint64_t r) {
   if (st) return st;
   CUDA_TRY(h, cudaMemcpy(h->iter_dev, &r, sizeof(uint64_t), cudaMemcpyHostToDevice));
   h->iter_host = r;
+  h->pref_mode = -1;
   return CP_OK;
 }
 
 cp_status cp_sgd_refresh_tables(cp_sgd_t h) {
   if (!h) return CP_EINVAL;
+  h->pref_mode = -1;
   for (int k = 0; k < h->N; ++k) {
     cp_status st = launch_table_any(h, k);
     if (st) return st;

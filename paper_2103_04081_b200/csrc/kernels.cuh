@@ -27,7 +27,7 @@ constexpr int kMaxRank = 64;
 // Parameters (passed by value; < 1 KB)
 // ------------------------------------------------------------------------------------------
 struct SampleParams {
-  int N, n, strategy;
+  int N, n, strategy, R;
   int64_t B;                       // nominal batch
   int64_t dims[kMaxOrder];         // global dims
   int32_t window[kMaxOrder];       // per remaining position (block strategies), clamped to I_k
@@ -35,11 +35,21 @@ struct SampleParams {
   const uint64_t* Ttot;            // [N] totals (device)
   uint64_t seed;
   const uint64_t* iter;            // device pointer to the iteration counter r
+  uint64_t iter_add;               // draws use r + iter_add
   int32_t* idx;                    // out [B_max][N-1]
   double* w;                       // out [B_max]
   int64_t* beff;                   // out (device scalar)
   int64_t bmax;                    // rows the launch covers
   int stage_smem;                  // stage the CDFs of the N-1 sampled modes in shared memory
+  // prefetch for k_gather (optional): unweighted SKR rows and fiber offsets of mode n
+  const void* factors[kMaxOrder];
+  void* zrow;                      // T [B_max][R] or NULL
+  int64_t* fbase;                  // [B_max] element offset of fiber b in the gather's layout (-1: not owned)
+  int64_t ldims[kMaxOrder];        // local dims (slab)
+  int64_t lstride[kMaxOrder];
+  int64_t lo_last;
+  int mode_major;
+  int64_t pitch;
 };
 
 template <typename T>
@@ -51,8 +61,8 @@ struct GatherParams {
   const T* X;                  // native local tensor, or the mode-major copy of mode n
   int mode_major;              // 1: X is [J_n_local][pitch] (fiber-contiguous)
   int64_t pitch;               // row pitch of the mode-major copy (elements)
-  const T* factors[kMaxOrder];
-  const int32_t* idx;          // [B_max][N-1]
+  const int64_t* fbase;        // [B_max] fiber offsets from the sampler (-1: not owned / padding)
+  const T* zrow;               // [B_max][R] unweighted SKR rows from the sampler
   const double* w;             // [B_max]
   const int64_t* beff;         // device scalar
   int64_t TB;                  // fibers per chunk
@@ -313,74 +323,40 @@ __global__ void __launch_bounds__(kTableThreads) k_table(const T* __restrict__ A
 // product in index-map order.  Weights in the contract's exact fp64 order (no FMA possible:
 // only products and quotients, written with explicit _rn intrinsics).
 // ==========================================================================================
-__global__ void __launch_bounds__(256) k_sample(SampleParams p) {
-  extern __shared__ uint64_t s_cdf[];
-  __shared__ const uint64_t* cdfp[kMaxOrder];
+// stage the CDFs of the sampled modes (k != n) in shared memory; cdfp[k] -> smem or global
+__device__ __forceinline__ void stage_cdfs(const SampleParams& p, uint64_t* s_cdf, const uint64_t** cdfp, int tid,
+                                           int nthreads) {
+  int64_t off = 0;
+  for (int k = 0; k < p.N; ++k) {
+    cdfp[k] = p.cdf[k];
+    if (k == p.n || !p.stage_smem || p.strategy == 0) continue;
+    for (int64_t i = tid; i < p.dims[k]; i += nthreads) s_cdf[off + i] = p.cdf[k][i];
+    cdfp[k] = s_cdf + off;
+    off += p.dims[k];
+  }
+}
+
+// rows [b0, b1) of the batch of mode p.n at iteration r: indices, exact weights, fiber offsets.
+__device__ __forceinline__ void draw_rows(const SampleParams& p, const uint64_t* const* cdfp, uint64_t r_it,
+                                          int64_t b0, int64_t b1, int tid, int nthreads) {
   const int N = p.N, n = p.n;
-  const uint64_t iter = *p.iter;
-  // stage CDFs of the sampled modes in shared memory (uniform needs none)
-  if (threadIdx.x == 0) {
-    int64_t off = 0;
-    for (int k = 0; k < N; ++k) {
-      cdfp[k] = p.cdf[k];
-      if (k == n || !p.stage_smem || p.strategy == 0) continue;
-      cdfp[k] = s_cdf + off;
-      off += p.dims[k];
-    }
-  }
-  __syncthreads();
-  if (p.stage_smem && p.strategy != 0) {
-    int64_t off = 0;
-    for (int k = 0; k < N; ++k) {
-      if (k == n) continue;
-      for (int64_t i = threadIdx.x; i < p.dims[k]; i += blockDim.x) s_cdf[off + i] = p.cdf[k][i];
-      off += p.dims[k];
-    }
-    __syncthreads();
-  }
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool block = (p.strategy == 3 || p.strategy == 4);
-  if (!block) {
-    if (b >= p.B) return;
+  int32_t start[kMaxOrder], len[kMaxOrder];
+  double wblk = 0.0;
+  int64_t beff = p.B;
+  if (block) {
     double prod = 1.0;
-    int pos = 0;
-    for (int k = 0; k < N; ++k) {
-      if (k == n) continue;
-      const uint64_t Tk = (p.strategy == 0) ? (uint64_t)p.dims[k] : p.Ttot[k];
-      const uint64_t u = draw_word(p.seed, iter, (uint32_t)b, kPurposeRow, (uint32_t)pos);
-      const uint64_t r = scale_draw(u, Tk);
-      int64_t i;
-      uint64_t qk;
-      if (p.strategy == 0) {
-        i = (int64_t)r;
-        qk = 1;
-      } else {
-        const uint64_t* c = cdfp[k];
-        i = upper_bound_u64(c, p.dims[k], r);
-        qk = c[i] - (i > 0 ? c[i - 1] : 0ull);
-      }
-      p.idx[b * (N - 1) + pos] = (int32_t)i;
-      const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);
-      prod = (pos == 0) ? pt : __dmul_rn(prod, pt);
-      ++pos;
-    }
-    p.w[b] = __ddiv_rn(1.0, __dmul_rn((double)p.B, prod));
-    if (b == 0) *p.beff = p.B;
-  } else {
-    int32_t start[kMaxOrder], len[kMaxOrder];
-    double prod = 1.0;
-    int64_t beff = 1;
+    beff = 1;
     int pos = 0;
     for (int k = 0; k < N; ++k) {
       if (k == n) continue;
       const int64_t bk = p.window[pos];
       const uint64_t Tk = p.Ttot[k];
-      const uint64_t u = draw_word(p.seed, iter, 0u, kPurposeWindow, (uint32_t)pos);
-      const uint64_t r = scale_draw(u, Tk);
+      const uint64_t u = draw_word(p.seed, r_it, 0u, kPurposeWindow, (uint32_t)pos);
+      const uint64_t rr = scale_draw(u, Tk);
       const uint64_t* c = cdfp[k];
-      const int64_t istar = upper_bound_u64(c, p.dims[k], r);
-      const int64_t wsel = istar / bk;
-      const int64_t s0 = wsel * bk;
+      const int64_t istar = upper_bound_u64(c, p.dims[k], rr);   // == window draw (R6)
+      const int64_t s0 = (istar / bk) * bk;
       const int64_t e0 = min(s0 + bk, p.dims[k]);
       const uint64_t Q = c[e0 - 1] - (s0 > 0 ? c[s0 - 1] : 0ull);
       start[pos] = (int32_t)s0;
@@ -390,14 +366,104 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
       beff *= (e0 - s0);
       ++pos;
     }
-    if (b == 0) *p.beff = beff;
-    if (b >= beff) return;
-    int64_t rem = b;
-    for (int q = 0; q < N - 1; ++q) {
-      p.idx[b * (N - 1) + q] = start[q] + (int32_t)(rem % len[q]);
-      rem /= len[q];
+    wblk = __ddiv_rn(1.0, prod);
+  }
+  if (b0 == 0 && tid == 0) *p.beff = beff;
+  for (int64_t b = b0 + tid; b < b1; b += nthreads) {
+    if (b >= beff) {
+      if (p.fbase) p.fbase[b] = -1;
+      continue;
     }
-    p.w[b] = __ddiv_rn(1.0, prod);
+    int32_t* ib = p.idx + b * (N - 1);
+    if (!block) {
+      double prod = 1.0;
+      int pos = 0;
+      for (int k = 0; k < N; ++k) {
+        if (k == n) continue;
+        const uint64_t Tk = (p.strategy == 0) ? (uint64_t)p.dims[k] : p.Ttot[k];
+        const uint64_t u = draw_word(p.seed, r_it, (uint32_t)b, kPurposeRow, (uint32_t)pos);
+        const uint64_t rr = scale_draw(u, Tk);
+        int64_t i;
+        uint64_t qk;
+        if (p.strategy == 0) {
+          i = (int64_t)rr;
+          qk = 1;
+        } else {
+          const uint64_t* c = cdfp[k];
+          i = upper_bound_u64(c, p.dims[k], rr);
+          qk = c[i] - (i > 0 ? c[i - 1] : 0ull);
+        }
+        ib[pos] = (int32_t)i;
+        const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);
+        prod = (pos == 0) ? pt : __dmul_rn(prod, pt);
+        ++pos;
+      }
+      p.w[b] = __ddiv_rn(1.0, __dmul_rn((double)p.B, prod));
+    } else {
+      int64_t rem = b;
+      for (int q = 0; q < N - 1; ++q) {
+        ib[q] = start[q] + (int32_t)(rem % len[q]);
+        rem /= len[q];
+      }
+      p.w[b] = wblk;
+    }
+    if (p.fbase) {  // fiber offset in the gather's layout (mode-major row, or native base)
+      int64_t off = 0, jrow = 0, jmul = 1;
+      bool own = true;
+      int pos = 0;
+      for (int k = 0; k < N; ++k) {
+        if (k == n) continue;
+        int64_t ik = ib[pos++];
+        if (k == N - 1) {
+          ik -= p.lo_last;
+          if (ik < 0 || ik >= p.ldims[k]) own = false;
+        }
+        off += ik * p.lstride[k];
+        jrow += ik * jmul;
+        jmul *= p.ldims[k];
+      }
+      p.fbase[b] = own ? (p.mode_major ? jrow * p.pitch : off) : -1;
+    }
+  }
+}
+
+// SKR rows (Alg. 1) of rows [b0, b1): z_b[r] = prod_{k != n, ascending} A^(k)(i_k, r)
+template <typename T>
+__device__ __forceinline__ void skr_rows(const SampleParams& p, int64_t b0, int64_t b1, int tid, int nthreads) {
+  const int N = p.N, n = p.n, R = p.R;
+  T* Z = reinterpret_cast<T*>(p.zrow);
+  for (int64_t e = b0 * R + tid; e < b1 * R; e += nthreads) {
+    const int64_t b = e / R;
+    const int r = (int)(e % R);
+    const int32_t* ib = p.idx + b * (N - 1);
+    T z = T(1);
+    int pos = 0;
+    for (int k = 0; k < N; ++k) {
+      if (k == n) continue;
+      z = z * __ldg(reinterpret_cast<const T*>(p.factors[k]) + (int64_t)ib[pos++] * R + r);
+    }
+    Z[e] = z;
+  }
+}
+
+// (a2, a3[, a4]) standalone sampler (API calls and the first step of a call).  grid-stride rows.
+template <typename T>
+__global__ void __launch_bounds__(256) k_sample(SampleParams p) {
+  extern __shared__ uint64_t s_cdf[];
+  __shared__ const uint64_t* cdfp[kMaxOrder];
+  __shared__ uint64_t s_it;
+  if (threadIdx.x == 0) s_it = *p.iter + p.iter_add;
+  const uint64_t* cp[kMaxOrder];
+  stage_cdfs(p, s_cdf, cp, threadIdx.x, blockDim.x);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < p.N; ++k) cdfp[k] = cp[k];
+  __syncthreads();
+  const int64_t per = (p.bmax + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = (int64_t)blockIdx.x * per, b1 = min(b0 + per, p.bmax);
+  draw_rows(p, cdfp, s_it, b0, b1, threadIdx.x, blockDim.x);
+  if (p.zrow) {
+    __syncthreads();
+    skr_rows<T>(p, b0, b1, threadIdx.x, blockDim.x);
   }
 }
 
@@ -440,7 +506,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherParams<T> p) {
   T* zu = zw + kSB * RP;                          // [kSB][RP]
   int64_t* base = reinterpret_cast<int64_t*>(zu + kSB * RP);
   int* owned = reinterpret_cast<int*>(base + kSB);
-  const int N = p.N, n = p.n, R = p.R;
+  const int n = p.n, R = p.R;
   const int tid = threadIdx.x, il = tid % kTI, half = tid / kTI;
   const int64_t i0 = (int64_t)blockIdx.x * kTI;
   const int chunk = blockIdx.y;
@@ -461,43 +527,18 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherParams<T> p) {
 
   for (int64_t s = b_begin; s < b_end; s += kSB) {
     const int nb = (int)min((int64_t)kSB, b_end - s);
-    // (a) per-fiber offsets
+    // (a) per-fiber offsets (computed by the sampler)
     if (tid < kSB) {
-      int64_t off = 0;
-      int own = 0;
-      if (tid < nb) {
-        own = 1;
-        const int32_t* t = p.idx + (s + tid) * (N - 1);
-        int pos = 0;
-        int64_t jrow = 0, jmul = 1;
-        for (int k = 0; k < N; ++k) {
-          if (k == n) continue;
-          int64_t ik = t[pos++];
-          if (k == N - 1) {
-            ik -= p.lo_last;
-            if (ik < 0 || ik >= p.ldims[k]) own = 0;
-          }
-          off += ik * p.lstride[k];
-          jrow += ik * jmul;
-          jmul *= p.ldims[k];
-        }
-        if (p.mode_major) off = jrow * p.pitch;
-      }
-      base[tid] = off;
-      owned[tid] = own;
+      const int64_t fb = (tid < nb) ? p.fbase[s + tid] : -1;
+      base[tid] = fb;
+      owned[tid] = fb >= 0;
     }
-    // (b) SKR rows (Alg. 1), weighted and unweighted, zero padded to RP
+    // (b) SKR rows (Alg. 1, prefetched by the sampler): weighted and unweighted, zero padded to RP
     for (int e = tid; e < kSB * RP; e += kGatherThreads) {
       const int bb = e / RP, r = e % RP;
       T z = T(0), zwv = T(0);
       if (bb < nb && r < R) {
-        const int32_t* t = p.idx + (s + bb) * (N - 1);
-        z = T(1);
-        int pos = 0;
-        for (int k = 0; k < N; ++k) {
-          if (k == n) continue;
-          z = z * ldg(p.factors[k] + (int64_t)t[pos++] * R + r);
-        }
+        z = ldg(p.zrow + (s + bb) * R + r);
         zwv = (T)p.w[s + bb] * z;
       }
       zu[bb * RP + r] = z;
@@ -679,6 +720,8 @@ struct UTParams {
   uint64_t* cdf;
   uint64_t* Tout;
   int* status;
+  int sample_next;       // 1: draw the next step's batch (mode sp.n) after the table (a9 pipelining)
+  SampleParams sp;
 };
 
 constexpr int kUTThreads = 256;
@@ -731,6 +774,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   __shared__ unsigned long long s_wtot[kUTThreads / 32];
   __shared__ double s_fro, s_tol;
   if (tid == 0) { s_bad = 0; s_rank = R; s_stop = 0; }
+  const uint64_t r_now = *p.iter;  // every CTA reads r before CTA 0 may advance it (after a cluster barrier)
 
   // ---------------- stage A: update ----------------
   for (int e = tid; e < nr * R; e += kUTThreads) {
@@ -744,6 +788,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
         g = p.Gsum[e];
       } else {
         g = T(0);
+#pragma unroll 8
         for (int c = 0; c < p.nparts; ++c) g += p.Gp[(int64_t)c * R * R + e];
       }
       Gam[e] = g;
@@ -751,7 +796,6 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     }
     __syncthreads();
     const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
-    if (q == 0 && tid == 0 && p.iter) *p.iter += 1;  // r <- r + 1
     // element (il, r): consecutive threads -> consecutive rows (coalesced partial reads)
     for (int e = tid; e < nr * R; e += kUTThreads) {
       const int il = e % nr, r = e / nr;
@@ -761,6 +805,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
         m = p.Msum[(int64_t)r * p.In + i];
       } else {
         m = T(0);
+#pragma unroll 8
         for (int c = 0; c < p.nparts; ++c) m += p.Mp[((int64_t)c * R + r) * p.In + i];
       }
       T ag = T(0);
@@ -792,8 +837,8 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     }
   }
   __syncthreads();
-  if (!p.do_table || p.strategy == 0) return;  // uniform tables are constant (no cluster barrier used)
-
+  bool synced = false;
+  if (p.do_table && p.strategy != 0) {  // uniform tables are constant
   // ---------------- stage B: table of the new A^(n) ----------------
   const bool lev = (p.strategy == 1 || p.strategy == 3);
   const int P = R * (R + 1) / 2;
@@ -827,17 +872,25 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   cluster.sync();
   if (lev) {
     for (int pair = tid; pair < P; pair += kUTThreads) {
+      double v[16];
+#pragma unroll
+      for (int qq = 0; qq < 16; ++qq) v[qq] = (qq < CU) ? cluster.map_shared_rank(gpart, qq)[pair] : 0.0;
       double sum = 0.0;
-      for (int qq = 0; qq < CU; ++qq) sum += cluster.map_shared_rank(gpart, qq)[pair];
+#pragma unroll
+      for (int qq = 0; qq < 16; ++qq) sum += v[qq];  // rank order (zeros past CU are exact)
       int r1 = 0, rem = pair;
       while (rem >= R - r1) { rem -= R - r1; ++r1; }
       const int r2 = r1 + rem;
       Gm[r1 * R + r2] = sum;
       Gm[r2 * R + r1] = sum;
     }
-    if (tid < R) piv[tid] = tid;
     __syncthreads();
-    // pivoted Cholesky (right-looking, full symmetric storage); rank tolerance R4(b)
+    // Inverse of the Gram on its numerically full-rank pivot set S by the symmetric sweep
+    // operator (Gauss-Jordan with diagonal pivoting, Goodnight 1979): sweeping pivot k maps
+    //   M_ij -= M_ik M_kj / d (i,j != k),  M_ik, M_kj /= d,  M_kk = -1/d   (d = M_kk).
+    // The unswept diagonal is the Schur-complement diagonal, so the pivot rule and the rank
+    // tolerance R4(b) are those of a pivoted Cholesky; after sweeping S, M_SS = -(G_SS)^{-1}.
+    // l_i = a_{i,S}^T (G_SS)^{-1} a_{i,S} = ||Q(i,:)||^2 (Def. 2.3) because range(A_S) = range(A).
     if (tid == 0) {
       double d0 = 0.0;
       bool fin = true;
@@ -848,48 +901,41 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
       if (!fin) s_bad |= 8;
       s_tol = (double)(p.In > R ? p.In : R) * 2.220446049250313e-16 * d0;
     }
+    if (tid < R) piv[tid] = 0;  // 1 = swept
     __syncthreads();
+    const double tol = s_tol;
     int k = 0;
     for (; k < R; ++k) {
-      if (tid < 32) {  // warp 0: pivot = argmax of the remaining diagonal (lowest index on ties)
-        double best = -1.0;
-        int bj = k;
-        for (int j = k + tid; j < R; j += 32) {
-          const double d = Gm[j * R + j];
-          if (d > best) { best = d; bj = j; }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_down_sync(0xffffffffu, best, o);
-          const int oj = __shfl_down_sync(0xffffffffu, bj, o);
-          if (ob > best || (ob == best && oj < bj)) { best = ob; bj = oj; }
-        }
-        if (tid == 0) {
-          s_jm = bj;
-          s_stop = !(best > s_tol);
-          if (!s_stop && bj != k) { const int t = piv[k]; piv[k] = piv[bj]; piv[bj] = t; }
-        }
+      // pivot: largest unswept diagonal, lowest index on ties (every warp computes it -> no barrier)
+      double best = -1.0;
+      int bj = -1;
+      for (int j = (tid & 31); j < R; j += 32) {
+        const double d = piv[j] ? -1.0 : Gm[j * R + j];
+        if (d > best) { best = d; bj = j; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ob > best || (ob == best && oj >= 0 && (bj < 0 || oj < bj))) { best = ob; bj = oj; }
+      }
+      if (!(best > tol)) break;
+      const int pk = bj;
+      const double d = Gm[pk * R + pk];
+      // rank-1 update of the entries off row/column pk (reads only row/col pk: no hazard)
+      for (int e = tid; e < R * R; e += kUTThreads) {
+        const int i = e / R, j = e % R;
+        if (i != pk && j != pk) Gm[e] -= Gm[i * R + pk] * Gm[pk * R + j] / d;
       }
       __syncthreads();
-      if (s_stop) break;
-      const int jm = s_jm;
-      if (jm != k) {
-        for (int c = tid; c < R; c += kUTThreads) {
-          const double t = Gm[k * R + c]; Gm[k * R + c] = Gm[jm * R + c]; Gm[jm * R + c] = t;
+      for (int i = tid; i < R; i += kUTThreads) {
+        if (i != pk) {
+          Gm[i * R + pk] = Gm[i * R + pk] / d;
+          Gm[pk * R + i] = Gm[pk * R + i] / d;
         }
-        __syncthreads();
-        for (int rr = tid; rr < R; rr += kUTThreads) {
-          const double t = Gm[rr * R + k]; Gm[rr * R + k] = Gm[rr * R + jm]; Gm[rr * R + jm] = t;
-        }
-        __syncthreads();
       }
-      const double lkk = sqrt(Gm[k * R + k]);
-      for (int i = k + 1 + tid; i < R; i += kUTThreads) Gm[i * R + k] = Gm[i * R + k] / lkk;
-      __syncthreads();
-      if (tid == 0) Gm[k * R + k] = lkk;
-      const int m = R - k - 1;
-      for (int e = tid; e < m * m; e += kUTThreads) {
-        const int i = k + 1 + e / m, j = k + 1 + e % m;
-        Gm[i * R + j] -= Gm[i * R + k] * Gm[j * R + k];
+      if (tid == 0) {
+        Gm[pk * R + pk] = -1.0 / d;
+        piv[pk] = 1;
       }
       __syncthreads();
     }
@@ -897,19 +943,24 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
       s_rank = k;
       if (k == 0) s_bad |= 2;
     }
+    // W = -M on S x S, zero elsewhere (in place)
+    for (int e = tid; e < R * R; e += kUTThreads) {
+      const int i = e / R, j = e % R;
+      Gm[e] = (piv[i] && piv[j]) ? -Gm[e] : 0.0;
+    }
     __syncthreads();
     const int rank = s_rank;
-    // scores of the owned rows: forward substitution L y = a_{piv}
+    // scores of the owned rows: l = a^T W a (independent FMAs)
     for (int il = tid; il < nr; il += kUTThreads) {
-      double y[kMaxRank];
+      const T* a = Anew + il * RS;
       double l = 0.0;
-      for (int j = 0; j < rank; ++j) {
-        double v = (double)Anew[il * RS + piv[j]];
-        for (int t = 0; t < j; ++t) v -= Gm[j * R + t] * y[t];
-        y[j] = v / Gm[j * R + j];
-        l += y[j] * y[j];
+      for (int i = 0; i < R; ++i) {
+        const double ai = (double)a[i];
+        double t = 0.0;
+        for (int j = 0; j < R; ++j) t += Gm[i * R + j] * (double)a[j];
+        l += ai * t;
       }
-      prow[il] = rank > 0 ? l / (double)rank : 0.0;
+      prow[il] = rank > 0 ? fmax(l, 0.0) / (double)rank : 0.0;
     }
   } else {
     if (tid == 0) {
@@ -974,7 +1025,32 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     else if ((s_bad & 2) || (q == 0 && total == 0)) st = -3;
     if (st != 0) atomicCAS(p.status, 0, st);
   }
-  cluster.sync();  // peers may still read this CTA's shared memory
+  __threadfence();
+  cluster.sync();  // peers may still read this CTA's shared memory; cdf visible cluster-wide
+  synced = true;
+  }  // stage B
+
+  // ---------------- stage C: the next step's batch (sampling contract; tables now current) ----
+  if (p.sample_next) {
+    if (!synced) {
+      __threadfence();
+      cluster.sync();  // updated A^(n) rows of every CTA visible (SKR reads them)
+      synced = true;
+    }
+    uint64_t* s_cdf = reinterpret_cast<uint64_t*>(ut_sm + ((off + 15) / 16 * 16));
+    const uint64_t* cp[kMaxOrder];
+    stage_cdfs(p.sp, s_cdf, cp, tid, kUTThreads);
+    __syncthreads();
+    const int64_t per = (p.sp.bmax + CU - 1) / CU;
+    const int64_t b0 = min((int64_t)q * per, p.sp.bmax), b1 = min(b0 + per, p.sp.bmax);
+    draw_rows(p.sp, cp, r_now + (p.do_update ? 1 : 0), b0, b1, tid, kUTThreads);
+    __syncthreads();
+    skr_rows<T>(p.sp, b0, b1, tid, kUTThreads);
+  }
+  if (p.do_update) {
+    if (!synced) cluster.sync();   // all CTAs have read r_now
+    if (q == 0 && tid == 0) *p.iter = r_now + 1;  // r <- r + 1 (Alg. 6/7)
+  }
 }
 
 // reduce chunk partials into Msum [R][In_local] and Gsum [R][R] (sharded path, phase 0)
