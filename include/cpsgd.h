@@ -70,6 +70,8 @@ typedef enum { CP_ORDER_CYCLIC = 0, CP_ORDER_RANDOM = 1 } cp_mode_order;
                                      n >= 1 so every sampled fiber is one contiguous row (DESIGN.md
                                      "Data layout"); costs (N-1) extra tensor-sized buffers          */
 #define CP_FLAG_NO_GRAPH 0x2u     /* never capture CUDA graphs for sweeps                              */
+#define CP_FLAG_NO_FUSED 0x8u      /* never use the persistent single-cluster sweep kernel (small problems
+                                     otherwise run whole step sequences in one launch)               */
 #define CP_FLAG_EXTERNAL_COMM 0x4u /* world > 1 without an internal NCCL communicator: the caller
                                      performs the exchange between the phases of cp_sgd_step_phase  */
 
@@ -185,6 +187,10 @@ cp_status cp_sgd_get_launches(cp_sgd_t h, uint64_t* n_host);
 cp_status cp_sgd_profile(cp_sgd_t h, int32_t on);
 cp_status cp_sgd_profile_read(cp_sgd_t h, int32_t cap, int32_t* ids, double* total_ms, int64_t* counts,
                               int32_t* n_out);
+
+/* debug: clock64() phase timestamps of the last fused update/table kernel (CTA 0); only when the
+ * environment variable CPSGD_DEBUG_TIMERS was set at cp_sgd_init, else CP_ESTATE */
+cp_status cp_sgd_debug_timers(cp_sgd_t h, long long* out64_host);
 
 /* library version string */
 const char* cp_sgd_version(void);

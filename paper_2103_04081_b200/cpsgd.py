@@ -19,8 +19,9 @@ LIB_PATH = os.path.join(_HERE, "libcpsgd.so")
 SAMPLERS = {"uniform": 0, "leverage": 1, "euclidean": 2, "block_leverage": 3, "block_euclidean": 4}
 RULES = {"fixed": 0, "adaptive": 1}
 ORDERS = {"cyclic": 0, "random": 1}
-FLAG_MODE_MAJOR, FLAG_NO_GRAPH, FLAG_EXTERNAL_COMM = 0x1, 0x2, 0x4
-KERNEL_NAMES = ["k_sample", "k_gather", "k_update", "k_table", "k_reduce_partials", "nccl", "k_fit"]
+FLAG_MODE_MAJOR, FLAG_NO_GRAPH, FLAG_EXTERNAL_COMM, FLAG_NO_FUSED = 0x1, 0x2, 0x4, 0x8
+KERNEL_NAMES = ["k_sample", "k_gather", "k_update_table", "k_table", "k_reduce_partials", "nccl", "k_fit",
+                "k_sweep_fused"]
 STATUS = {0: "CP_OK", -1: "CP_EINVAL", -2: "CP_ERANGE", -3: "CP_EDEGENERATE", -4: "CP_ENOMEM", -5: "CP_ECUDA",
           -6: "CP_ENCCL", -7: "CP_ESTATE", -8: "CP_ENONFINITE"}
 
@@ -28,7 +29,7 @@ EXPORTS = ["cp_sgd_init", "cp_sgd_destroy", "cp_sgd_last_error", "cp_sgd_sample"
            "cp_fit", "cp_sgd_sync", "cp_sgd_steps_host", "cp_sgd_step_phase", "cp_sgd_exchange_info",
            "cp_sgd_get_table", "cp_sgd_get_grad", "cp_sgd_get_accum", "cp_sgd_get_iter", "cp_sgd_set_iter",
            "cp_sgd_refresh_tables", "cp_sgd_get_launches", "cp_sgd_profile", "cp_sgd_profile_read",
-           "cp_sgd_version", "cp_sgd_batch_max"]
+           "cp_sgd_version", "cp_sgd_batch_max", "cp_sgd_debug_timers"]
 
 
 class CPError(RuntimeError):
@@ -84,6 +85,7 @@ def load_library(path: str = LIB_PATH):
     L.cp_sgd_profile.argtypes = [P, i32]
     L.cp_sgd_profile_read.argtypes = [P, i32, P, P, P, C.POINTER(C.c_int32)]
     L.cp_sgd_version.restype = C.c_char_p
+    L.cp_sgd_debug_timers.argtypes = [P, P]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype if name in ("cp_sgd_last_error", "cp_sgd_version") else C.c_int
     _lib = L
@@ -112,7 +114,7 @@ class CPSGD:
                  rule: str = "fixed", alpha: float = 0.01, eta: float = 0.05, b: float = 0.0, eps: float = 0.0,
                  seed: int = 0, stream=None, world_rank: int = 0, world_size: int = 1, nccl_id: bytes = None,
                  slab=None, mode_major: bool = True, block_window=None, graphs: bool = True,
-                 external_comm: bool = False):
+                 external_comm: bool = False, fused: bool = True):
         import torch
 
         L = load_library()
@@ -136,7 +138,7 @@ class CPSGD:
         self.stream = stream
         self._nccl_id = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
         flags = (FLAG_MODE_MAJOR if mode_major else 0) | (0 if graphs else FLAG_NO_GRAPH) | \
-                (FLAG_EXTERNAL_COMM if external_comm else 0)
+                (FLAG_EXTERNAL_COMM if external_comm else 0) | (0 if fused else FLAG_NO_FUSED)
         lo, hi = (0, self.dims[-1]) if slab is None else (int(slab[0]), int(slab[1]))
         cfg = Config(self.N, self._dims_arr, self.R, self.dtype, X.data_ptr(), self._fac_arr, int(batch),
                      self._win_arr, SAMPLERS[sampler], RULES[rule], float(alpha), float(eta), float(b), float(eps),
@@ -269,6 +271,11 @@ class CPSGD:
         n = C.c_uint64(0)
         self._chk(self._L.cp_sgd_get_launches(self._h, C.byref(n)))
         return int(n.value)
+
+    def debug_timers(self):
+        out = (C.c_longlong * 64)()
+        self._chk(self._L.cp_sgd_debug_timers(self._h, out))
+        return list(out)
 
     def profile(self, on: bool):
         self._chk(self._L.cp_sgd_profile(self._h, 1 if on else 0))

@@ -12,12 +12,14 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
 #include <vector>
 
 #include "../../include/cpsgd.h"
+#include "fused.cuh"
 #include "kernels.cuh"
 
 using namespace cps;
@@ -73,7 +75,7 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
-enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kNumKernelIds };
+enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kNumKernelIds };
 
 struct ProfRec {
   int id;
@@ -81,6 +83,20 @@ struct ProfRec {
 };
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// allow the largest dynamic shared memory the device grants this kernel (opt-in max minus its
+// static shared memory); returns that size (0 on failure)
+template <typename F>
+size_t allow_max_dyn_smem(F* func) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, func) != cudaSuccess) return 0;
+  const int mx = optin - (int)fa.sharedSizeBytes;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess) return 0;
+  return (size_t)mx;
+}
 
 }  // namespace
 
@@ -123,6 +139,10 @@ struct cp_sgd_s {
   int64_t* beff_api = nullptr;   // rows of the last cp_sgd_sample call
   void* zrow = nullptr;          // prefetched unweighted SKR rows [Bmax][R]
   int64_t* fbase = nullptr;      // prefetched fiber offsets [Bmax]
+  long long* dbg = nullptr;      // CPSGD_DEBUG_TIMERS: phase timestamps of k_update_table
+  int* last_mode_dev = nullptr;  // written by the fused sweep kernel
+  int fused_cu = 0, fused_bpc = 0, fused_rpc = 0;  // fused kernel geometry (0: not eligible)
+  size_t fused_smem = 0;
   int pref_mode = -1;            // mode whose batch (at the current r) sits in idx/w/zrow/fbase
   uint64_t* iter_dev = nullptr;
   uint64_t* iter_tmp = nullptr;
@@ -326,7 +346,7 @@ cp_status launch_gather_t(cp_sgd_s* h, int n) {
   const size_t smem = gather_smem_bytes<T, RPT>(h->R);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_gather<T, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sample_smem);
+    allow_max_dyn_smem(k_gather<T, RPT>);
     attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
@@ -392,6 +412,7 @@ cp_status launch_ut_t(cp_sgd_s* h, int n, int do_update, int do_table, int64_t r
   p.cdf = h->cdf[n];
   p.Tout = h->Ttot + n;
   p.status = h->status_dev;
+  p.dbg = h->dbg;
   size_t smem = ut_smem_bytes(h->R, p.rows_per, sizeof(T));
   if (next_mode >= 0) {
     p.sample_next = 1;
@@ -400,13 +421,15 @@ cp_status launch_ut_t(cp_sgd_s* h, int n, int do_update, int do_table, int64_t r
     p.sp.stage_smem = (cb > 0 && smem + cb <= (size_t)h->sample_smem) ? 1 : 0;
     if (p.sp.stage_smem) smem += cb;
   }
+  // one CTA per SM: the cluster's CTAs each run the serial table stages; co-residing CTAs would
+  // share one SM's issue slots (claim more than half of the SM's shared memory)
+  smem = std::max(smem, (size_t)h->sample_smem / 2 + 1024);
   static bool attr_set = false;
   if (!attr_set) {
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncSetAttribute(k_update_table<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-    cudaFuncSetAttribute(k_update_table<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    const size_t mx = allow_max_dyn_smem(k_update_table<T>);
+    cudaError_t eb = cudaFuncSetAttribute(k_update_table<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (mx == 0 || eb != cudaSuccess)
+      return h->fail(CP_ECUDA, "k_update_table attributes: %s", cudaGetErrorString(eb));
     attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
@@ -423,7 +446,9 @@ cp_status launch_ut_t(cp_sgd_s* h, int n, int do_update, int do_table, int64_t r
   lc.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&lc, k_update_table<T>, p);
   h->launches++;
-  if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_update_table launch: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess)
+    return h->fail(CP_ECUDA, "k_update_table launch (cluster %d, smem %zu B, params %zu B): %s", CU, smem,
+                   sizeof(p), cudaGetErrorString(e));
   return check_launch(h, "k_update_table");
 }
 
@@ -482,6 +507,132 @@ cp_status launch_reduce(cp_sgd_s* h, int n) {
 }
 
 bool sharded(const cp_sgd_s* h) { return h->world_size > 1; }
+
+// ---- persistent single-cluster sweep kernel (fused.cuh) ----------------------------------------
+template <typename T, int RMAX, int ROWS>
+cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev) {
+  ProfScope ps(h, kKFused);
+  FusedParams<T> p;
+  memset(&p, 0, sizeof p);
+  p.N = h->N;
+  p.R = h->R;
+  p.strategy = h->sampler;
+  p.rule = h->rule;
+  p.CU = h->fused_cu;
+  for (int k = 0; k < h->N; ++k) {
+    p.dims[k] = h->dims[k];
+    p.stride[k] = h->lstride[k];
+    if (h->Xmm[k]) {
+      p.Xg[k] = (const T*)h->Xmm[k];
+      p.estride[k] = 1;
+      p.pitch[k] = h->pitch[k];
+    } else {
+      p.Xg[k] = (const T*)h->X;
+      p.estride[k] = h->lstride[k];
+      p.pitch[k] = 0;
+    }
+    p.factors[k] = (T*)h->factors[k];
+    p.S[k] = (T*)h->S[k];
+    p.cdf[k] = h->cdf[k];
+    p.pprob[k] = h->pprob[k];
+    p.bmax[k] = h->bmax[k];
+    for (int j = 0; j < h->N - 1; ++j) p.window[k][j] = h->window[k][j];
+  }
+  p.Ttot = h->Ttot;
+  p.status = h->status_dev;
+  p.iter = h->iter_dev;
+  p.seed = h->seed;
+  p.B = h->B;
+  p.alpha = alpha;
+  p.alpha_dev = alpha_dev;
+  p.eta = h->eta;
+  p.b = h->bpar;
+  p.eps = h->eps;
+  p.nsteps = nsteps;
+  p.first_mode = first_mode;
+  p.order = order;
+  p.Gout = (T*)h->Gout;
+  p.Gam_out = (T*)h->Gam_out;
+  p.last_mode = h->last_mode_dev;
+  p.BPC = h->fused_bpc;
+  p.RPC = h->fused_rpc;
+  int64_t imax = 0;
+  for (int k = 0; k < h->N; ++k) imax = std::max(imax, h->dims[k]);
+  p.Imax = imax;
+  p.dbg = h->dbg;
+  static bool attr_set = false;
+  if (!attr_set) {
+    allow_max_dyn_smem(k_sweep_fused<T, RMAX, ROWS>);
+    cudaFuncSetAttribute(k_sweep_fused<T, RMAX, ROWS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(h->fused_cu, 1, 1);
+  lc.blockDim = dim3(kFThreads, 1, 1);
+  lc.dynamicSmemBytes = h->fused_smem;
+  lc.stream = h->ls;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = h->fused_cu;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_sweep_fused<T, RMAX, ROWS>, p);
+  h->launches++;
+  if (e != cudaSuccess)
+    return h->fail(CP_ECUDA, "k_sweep_fused launch (cluster %d, smem %zu): %s", h->fused_cu, h->fused_smem,
+                   cudaGetErrorString(e));
+  return check_launch(h, "k_sweep_fused");
+}
+
+template <typename T>
+cp_status launch_fused_r(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev) {
+  int64_t imax = 0;
+  for (int k = 0; k < h->N; ++k) imax = std::max(imax, h->dims[k]);
+  const bool two = imax > kFThreads;
+  if (h->R <= 8)
+    return two ? launch_fused_t<T, 8, 2>(h, nsteps, first_mode, order, alpha, alpha_dev)
+               : launch_fused_t<T, 8, 1>(h, nsteps, first_mode, order, alpha, alpha_dev);
+  if (h->R <= 16)
+    return two ? launch_fused_t<T, 16, 2>(h, nsteps, first_mode, order, alpha, alpha_dev)
+               : launch_fused_t<T, 16, 1>(h, nsteps, first_mode, order, alpha, alpha_dev);
+  return two ? launch_fused_t<T, 32, 2>(h, nsteps, first_mode, order, alpha, alpha_dev)
+             : launch_fused_t<T, 32, 1>(h, nsteps, first_mode, order, alpha, alpha_dev);
+}
+
+cp_status launch_fused(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev) {
+  cp_status st = h->dtype == CP_F64 ? launch_fused_r<double>(h, nsteps, first_mode, order, alpha, alpha_dev)
+                                    : launch_fused_r<float>(h, nsteps, first_mode, order, alpha, alpha_dev);
+  h->pref_mode = -1;
+  return st;
+}
+
+// geometry + eligibility of the fused kernel: one GPU, R <= 32, I_n <= 512, fits shared memory
+void plan_fused(cp_sgd_s* h) {
+  h->fused_cu = 0;
+  if (h->world_size > 1 || (h->flags & CP_FLAG_NO_FUSED) || h->R > 32) return;
+  int64_t imax = 0, bmx = 0, cdfmax = 0;
+  for (int n = 0; n < h->N; ++n) {
+    imax = std::max(imax, h->dims[n]);
+    bmx = std::max(bmx, h->bmax[n]);
+    int64_t c = 0;
+    for (int k = 0; k < h->N; ++k)
+      if (k != n) c += h->dims[k];
+    cdfmax = std::max(cdfmax, c);
+  }
+  if (imax > 2 * kFThreads) return;
+  const int CU = 16;
+  const int bpc = (int)ceil_div(bmx, CU);
+  const int rpc = (int)ceil_div(imax, CU);
+  if (bpc > 256 || rpc > kFThreads) return;
+  const FusedLayout L = fused_layout(h->N, h->R, bpc, rpc, imax, h->sampler == CP_UNIFORM ? 0 : cdfmax, h->esz);
+  if (L.total + 2048 > (size_t)h->sample_smem) return;
+  h->fused_cu = CU;
+  h->fused_bpc = bpc;
+  h->fused_rpc = rpc;
+  h->fused_smem = L.total;
+}
 
 // ---- one step, by phases ------------------------------------------------------------------------
 cp_status phase0(cp_sgd_s* h, int n) {
@@ -748,6 +899,11 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
   ALLOC(h->w, sizeof(double) * Bmax_all);
   ALLOC(h->beff, sizeof(int64_t));
   ALLOC(h->beff_api, sizeof(int64_t));
+  ALLOC(h->last_mode_dev, sizeof(int));
+  if (getenv("CPSGD_DEBUG_TIMERS")) {
+    ALLOC(h->dbg, sizeof(long long) * 64);
+    cudaMemsetAsync(h->dbg, 0, sizeof(long long) * 64, h->stream);
+  }
   ALLOC(h->zrow, h->esz * Bmax_all * h->R);
   ALLOC(h->fbase, sizeof(int64_t) * Bmax_all);
   ALLOC(h->iter_dev, sizeof(uint64_t));
@@ -793,14 +949,14 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    h->sample_smem = optin;  // opt-in maximum dynamic shared memory per block
-    cudaFuncSetAttribute(k_sample<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sample_smem);
-    cudaFuncSetAttribute(k_sample<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->sample_smem);
-    const int tbl = (int)(sizeof(double) * (kMaxRank * kMaxRank + 2080));
-    cudaFuncSetAttribute(k_table<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, tbl);
-    cudaFuncSetAttribute(k_table<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, tbl);
+    // dynamic shared-memory budget of the sampler / fused kernels (opt-in max less 4 KB of statics)
+    h->sample_smem = (int)std::min(allow_max_dyn_smem(k_sample<float>), allow_max_dyn_smem(k_sample<double>));
+    h->sample_smem = std::min(h->sample_smem, optin - 4096);
+    allow_max_dyn_smem(k_table<float>);
+    allow_max_dyn_smem(k_table<double>);
     cudaGetLastError();
   }
+  plan_fused(h);
   // ---- optional mode-major copies (n >= 1; mode 0 fibers are already contiguous) ----
   if (h->flags & CP_FLAG_MODE_MAJOR) {
     for (int n = 1; n < h->N; ++n) {
@@ -885,6 +1041,8 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->w);
   cudaFree(h->beff);
   cudaFree(h->beff_api);
+  cudaFree(h->last_mode_dev);
+  cudaFree(h->dbg);
   cudaFree(h->zrow);
   cudaFree(h->fbase);
   cudaFree(h->iter_dev);
@@ -972,6 +1130,13 @@ cp_status cp_sgd_step(cp_sgd_t h, int32_t mode, double alpha) {
   if (st) return st;
   if (sharded(h) && (h->flags & CP_FLAG_EXTERNAL_COMM))
     return h->fail(CP_ESTATE, "external-comm handles must use cp_sgd_step_phase");
+  if (h->fused_cu) {
+    st = launch_fused(h, 1, mode, 0, (alpha < 0.0) ? h->alpha : alpha, nullptr);
+    if (st) return st;
+    h->iter_host++;
+    h->last_mode = mode;
+    return CP_OK;
+  }
   return step_direct(h, mode, alpha, (mode + 1) % h->N);  // prefetch guess: the cyclic successor
 }
 
@@ -1021,6 +1186,16 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
   if (order != CP_ORDER_CYCLIC && order != CP_ORDER_RANDOM) return h->fail(CP_EINVAL, "bad order");
   if (sharded(h) && (h->flags & CP_FLAG_EXTERNAL_COMM))
     return h->fail(CP_ESTATE, "external-comm handles must use cp_sgd_step_phase");
+  if (h->fused_cu && !alpha_per_iter) {
+    if (nsweeps == 0) return CP_OK;
+    const int64_t nst = (int64_t)nsweeps * h->N;
+    cp_status st = launch_fused(h, (int)nst, 0, order, h->alpha, nullptr);
+    if (st) return st;
+    const uint64_t r_last = h->iter_host + nst - 1;
+    h->last_mode = order == CP_ORDER_CYCLIC ? h->N - 1 : random_mode(h->seed, r_last, h->N);
+    h->iter_host += nst;
+    return CP_OK;
+  }
   const bool use_graph = order == CP_ORDER_CYCLIC && !alpha_per_iter && !(h->flags & CP_FLAG_NO_GRAPH) && !h->prof;
   if (!use_graph) {
     for (int s = 0; s < nsweeps; ++s)
@@ -1212,6 +1387,15 @@ cp_status cp_sgd_refresh_tables(cp_sgd_t h) {
     if (st) return st;
   }
   return cp_sgd_sync(h);
+}
+
+// debug: phase timestamps of the last k_update_table (CPSGD_DEBUG_TIMERS set at init)
+cp_status cp_sgd_debug_timers(cp_sgd_t h, long long* out16) {
+  if (!h || !out16) return CP_EINVAL;
+  if (!h->dbg) return h->fail(CP_ESTATE, "CPSGD_DEBUG_TIMERS was not set at init");
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  CUDA_TRY(h, cudaMemcpy(out16, h->dbg, sizeof(long long) * 64, cudaMemcpyDeviceToHost));
+  return CP_OK;
 }
 
 cp_status cp_sgd_get_launches(cp_sgd_t h, uint64_t* n_host) {

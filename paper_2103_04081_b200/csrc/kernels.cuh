@@ -432,9 +432,10 @@ template <typename T>
 __device__ __forceinline__ void skr_rows(const SampleParams& p, int64_t b0, int64_t b1, int tid, int nthreads) {
   const int N = p.N, n = p.n, R = p.R;
   T* Z = reinterpret_cast<T*>(p.zrow);
-  for (int64_t e = b0 * R + tid; e < b1 * R; e += nthreads) {
-    const int64_t b = e / R;
-    const int r = (int)(e % R);
+  const int cnt = (int)(b1 - b0) * R;
+  for (int e = tid; e < cnt; e += nthreads) {
+    const int64_t b = b0 + e / R;
+    const int r = e % R;
     const int32_t* ib = p.idx + b * (N - 1);
     T z = T(1);
     int pos = 0;
@@ -442,7 +443,7 @@ __device__ __forceinline__ void skr_rows(const SampleParams& p, int64_t b0, int6
       if (k == n) continue;
       z = z * __ldg(reinterpret_cast<const T*>(p.factors[k]) + (int64_t)ib[pos++] * R + r);
     }
-    Z[e] = z;
+    Z[b * R + r] = z;
   }
 }
 
@@ -722,6 +723,7 @@ struct UTParams {
   int* status;
   int sample_next;       // 1: draw the next step's batch (mode sp.n) after the table (a9 pipelining)
   SampleParams sp;
+  long long* dbg;        // optional phase timestamps (CTA 0, thread 0), NULL in production
 };
 
 constexpr int kUTThreads = 256;
@@ -740,6 +742,11 @@ __host__ __device__ inline size_t ut_smem_bytes(int R, int64_t rows_per, size_t 
   take(sizeof(unsigned long long) * 2);  // CTA total (read by peers), pad
   return off + 16;
 }
+
+#define UT_MARK(slot)                                                   \
+  do {                                                                  \
+    if (p.dbg && q == 0 && tid == 0) p.dbg[slot] = clock64();           \
+  } while (0)
 
 template <typename T>
 __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
@@ -775,6 +782,12 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   __shared__ double s_fro, s_tol;
   if (tid == 0) { s_bad = 0; s_rank = R; s_stop = 0; }
   const uint64_t r_now = *p.iter;  // every CTA reads r before CTA 0 may advance it (after a cluster barrier)
+  UT_MARK(0);
+  if (p.dbg && tid == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.dbg[16 + q] = smid;
+  }
 
   // ---------------- stage A: update ----------------
   for (int e = tid; e < nr * R; e += kUTThreads) {
@@ -840,6 +853,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   bool synced = false;
   if (p.do_table && p.strategy != 0) {  // uniform tables are constant
   // ---------------- stage B: table of the new A^(n) ----------------
+  UT_MARK(1);
   const bool lev = (p.strategy == 1 || p.strategy == 3);
   const int P = R * (R + 1) / 2;
   if (lev) {
@@ -870,6 +884,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     }
   }
   cluster.sync();
+  UT_MARK(2);
   if (lev) {
     for (int pair = tid; pair < P; pair += kUTThreads) {
       double v[16];
@@ -904,6 +919,16 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     if (tid < R) piv[tid] = 0;  // 1 = swept
     __syncthreads();
     const double tol = s_tol;
+    UT_MARK(3);
+    // this thread's fixed set of matrix entries (R^2 <= 4096 -> at most 16 per thread)
+    constexpr int EPT = (kMaxRank * kMaxRank + kUTThreads - 1) / kUTThreads;
+    int ei[EPT], ej[EPT];
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) {
+      const int e = tid + t * kUTThreads;
+      ei[t] = e < R * R ? e / R : -1;
+      ej[t] = e < R * R ? e % R : -1;
+    }
     int k = 0;
     for (; k < R; ++k) {
       // pivot: largest unswept diagonal, lowest index on ties (every warp computes it -> no barrier)
@@ -913,54 +938,69 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
         const double d = piv[j] ? -1.0 : Gm[j * R + j];
         if (d > best) { best = d; bj = j; }
       }
+#pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double ob = __shfl_xor_sync(0xffffffffu, best, o);
         const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-        if (ob > best || (ob == best && oj >= 0 && (bj < 0 || oj < bj))) { best = ob; bj = oj; }
+        const bool take = (ob > best) | ((ob == best) & (oj >= 0) & ((bj < 0) | (oj < bj)));
+        best = take ? ob : best;
+        bj = take ? oj : bj;
       }
+      if (k == 1) UT_MARK(8);
       if (!(best > tol)) break;
       const int pk = bj;
-      const double d = Gm[pk * R + pk];
+      const double dinv = __drcp_rn(Gm[pk * R + pk]);
+      if (k == 1) UT_MARK(9);
       // rank-1 update of the entries off row/column pk (reads only row/col pk: no hazard)
-      for (int e = tid; e < R * R; e += kUTThreads) {
-        const int i = e / R, j = e % R;
-        if (i != pk && j != pk) Gm[e] -= Gm[i * R + pk] * Gm[pk * R + j] / d;
+#pragma unroll
+      for (int t = 0; t < EPT; ++t) {
+        const int i = ei[t], j = ej[t];
+        if (i >= 0 && i != pk && j != pk) Gm[i * R + j] -= Gm[i * R + pk] * (Gm[pk * R + j] * dinv);
       }
+      if (k == 1) UT_MARK(10);
       __syncthreads();
-      for (int i = tid; i < R; i += kUTThreads) {
-        if (i != pk) {
-          Gm[i * R + pk] = Gm[i * R + pk] / d;
-          Gm[pk * R + i] = Gm[pk * R + i] / d;
+      if (k == 1) UT_MARK(11);
+      if (tid < R) {
+        if (tid != pk) {
+          Gm[tid * R + pk] *= dinv;
+          Gm[pk * R + tid] *= dinv;
+        } else {
+          Gm[pk * R + pk] = -dinv;
+          piv[pk] = 1;
         }
       }
-      if (tid == 0) {
-        Gm[pk * R + pk] = -1.0 / d;
-        piv[pk] = 1;
-      }
       __syncthreads();
+      if (k == 1) UT_MARK(12);
+      if (k == 2) UT_MARK(13);
     }
     if (tid == 0) {
       s_rank = k;
       if (k == 0) s_bad |= 2;
     }
     // W = -M on S x S, zero elsewhere (in place)
-    for (int e = tid; e < R * R; e += kUTThreads) {
-      const int i = e / R, j = e % R;
-      Gm[e] = (piv[i] && piv[j]) ? -Gm[e] : 0.0;
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) {
+      const int i = ei[t], j = ej[t];
+      if (i >= 0) Gm[i * R + j] = (piv[i] && piv[j]) ? -Gm[i * R + j] : 0.0;
     }
     __syncthreads();
     const int rank = s_rank;
-    // scores of the owned rows: l = a^T W a (independent FMAs)
-    for (int il = tid; il < nr; il += kUTThreads) {
-      const T* a = Anew + il * RS;
-      double l = 0.0;
-      for (int i = 0; i < R; ++i) {
-        const double ai = (double)a[i];
-        double t = 0.0;
-        for (int j = 0; j < R; ++j) t += Gm[i * R + j] * (double)a[j];
-        l += ai * t;
+    UT_MARK(4);
+    // scores of the owned rows: l = a^T W a; one warp per row, lanes over i, butterfly sum
+    {
+      const int lane = tid & 31, wid = tid >> 5;
+      for (int il = wid; il < nr; il += kUTThreads / 32) {
+        const T* a = Anew + il * RS;
+        double part = 0.0;
+        for (int i = lane; i < R; i += 32) {
+          double t = 0.0;
+          for (int j = 0; j < R; ++j) t += Gm[i * R + j] * (double)a[j];
+          part += (double)a[i] * t;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) prow[il] = rank > 0 ? fmax(part, 0.0) / (double)rank : 0.0;
       }
-      prow[il] = rank > 0 ? fmax(l, 0.0) / (double)rank : 0.0;
     }
   } else {
     if (tid == 0) {
@@ -975,6 +1015,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     for (int il = tid; il < nr; il += kUTThreads) prow[il] = prow[il] / fro;
   }
   __syncthreads();
+  UT_MARK(5);
   // quantise + CTA-local inclusive scan (each thread a contiguous segment of rows)
   const int seg = (nr + kUTThreads - 1) / kUTThreads;
   const int a0 = min(tid * seg, nr), a1 = min(a0 + seg, nr);
@@ -1028,6 +1069,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   __threadfence();
   cluster.sync();  // peers may still read this CTA's shared memory; cdf visible cluster-wide
   synced = true;
+  UT_MARK(6);
   }  // stage B
 
   // ---------------- stage C: the next step's batch (sampling contract; tables now current) ----
@@ -1046,6 +1088,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     draw_rows(p.sp, cp, r_now + (p.do_update ? 1 : 0), b0, b1, tid, kUTThreads);
     __syncthreads();
     skr_rows<T>(p.sp, b0, b1, tid, kUTThreads);
+    UT_MARK(7);
   }
   if (p.do_update) {
     if (!synced) cluster.sync();   // all CTAs have read r_now

@@ -117,10 +117,15 @@ STEP_CASES = [
 ]
 
 
+PATHS = {"fused": dict(fused=True, mode_major=True),            # persistent single-cluster kernel
+         "split_mm": dict(fused=False, mode_major=True),        # gather + cluster update/table kernels
+         "split_native": dict(fused=False, mode_major=False)}   # same, strided fibers in the native layout
+
+
 @pytest.mark.parametrize("strategy", S)
 @pytest.mark.parametrize("case", STEP_CASES, ids=lambda c: "x".join(map(str, c[0])) + f"_R{c[1]}_B{c[2]}_{c[3]}")
-@pytest.mark.parametrize("mode_major", [True, False])
-def test_one_step_per_mode(strategy, case, mode_major):
+@pytest.mark.parametrize("path", list(PATHS))
+def test_one_step_per_mode(strategy, case, path):
     """a4-a8: from the same seeded state, one GPU step of mode n at iteration r equals one oracle
     step: G within tol of (||A Gamma|| + ||M||), updated A within tol of ||A||."""
     dims, R, B, dt, rule = case
@@ -131,7 +136,7 @@ def test_one_step_per_mode(strategy, case, mode_major):
     tol = TOL[dt]
     for n in range(len(dims)):
         Xd, Ad = to_dev(X, A0)
-        h = handle(cfg, Xd, Ad, strategy, seed=77, mode_major=mode_major, b=bpar)
+        h = handle(cfg, Xd, Ad, strategy, seed=77, b=bpar, **PATHS[path])
         it = 3 + n
         h.iter = it
         idx_o, w_o, G_o, Gam_o, M_o, tabs = oracle_step(X, dims, A0, n, strategy, B, 77, it)
@@ -158,13 +163,14 @@ def test_one_step_per_mode(strategy, case, mode_major):
 
 # ------------------------------------------------------------------------------------------ trajectories
 @pytest.mark.parametrize("strategy", S)
-def test_c1_trajectory_50_sweeps(strategy):
+@pytest.mark.parametrize("path", ["fused", "split_mm"])
+def test_c1_trajectory_50_sweeps(strategy, path):
     """C1 (60^3 fp64, R5, B64, fixed alpha, 50 cyclic sweeps) free-running on both sides: final
-    factors within 1e-9 relative (graph-replayed sweeps)."""
+    factors within 1e-9 relative (one persistent launch, or graph-replayed split sweeps)."""
     cfg = synth.CONFIGS["C1"]
     X, A0 = make_problem(cfg)
     Xd, Ad = to_dev(X, A0)
-    h = handle(cfg, Xd, Ad, strategy, seed=0)
+    h = handle(cfg, Xd, Ad, strategy, seed=0, **PATHS[path])
     h.sweep(50)
     h.sync()
     fs, _, _ = oracle.run(X, A0, oracle.STRATEGIES[strategy], oracle.STEP_FIXED, cfg.batch, 50 * 3,
@@ -177,12 +183,13 @@ def test_c1_trajectory_50_sweeps(strategy):
 
 
 @pytest.mark.parametrize("strategy", ["leverage", "block_euclidean"])
-def test_random_order_and_adaptive_trajectory(strategy):
+@pytest.mark.parametrize("path", ["fused", "split_mm"])
+def test_random_order_and_adaptive_trajectory(strategy, path):
     """random mode order, adaptive rule, fp64: 40 iterations equal the oracle's."""
     cfg = synth.small((24, 20, 16), 4, dtype="f64", batch=48, rule="adaptive", eta=0.05, seed=3, row_sigma=0.8)
     X, A0 = make_problem(cfg)
     Xd, Ad = to_dev(X, A0)
-    h = handle(cfg, Xd, Ad, strategy, seed=9)
+    h = handle(cfg, Xd, Ad, strategy, seed=9, **PATHS[path])
     h.sweep(40 // 3 + 1, order="random")
     iters = 3 * (40 // 3 + 1)
     fs, Ss, modes = oracle.run(X, A0, oracle.STRATEGIES[strategy], oracle.STEP_ADAPTIVE, cfg.batch, iters,
@@ -226,9 +233,10 @@ def test_fit_matches_oracle(cfgname):
 
 
 # ------------------------------------------------------------------------------------------ full size (bench config)
-def test_c2_full_size_step_and_fit():
+@pytest.mark.parametrize("path", ["fused", "split_mm"])
+def test_c2_full_size_step_and_fit(path):
     """C2 at full size (400^3 fp32, R20, B512, adaptive) in the launch configuration bench.py
-    times: one step per mode vs the oracle, and fit."""
+    times (fused), and the split path: one step per mode vs the oracle, and fit."""
     cfg = synth.CONFIGS["C2"]
     X, A0 = make_problem(cfg)
     Xd, Ad = to_dev(X, A0)
@@ -238,7 +246,7 @@ def test_c2_full_size_step_and_fit():
     del Xd
     for n in range(3):
         Xd, Ad = to_dev(X, A0)
-        h = handle(cfg, Xd, Ad, "leverage", seed=0)
+        h = handle(cfg, Xd, Ad, "leverage", seed=0, **PATHS[path])
         h.iter = n
         idx_o, w_o, G_o, Gam_o, M_o, tabs = oracle_step(X, cfg.dims, A0, n, "leverage", cfg.batch, 0, n)
         idx_g, w_g = h.sample(n, n)

@@ -1,0 +1,44 @@
+"""Run a few sweeps of a BASELINE config on cuda:0 (profiling driver for ncu / sanitizers)."""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2103_04081_b200 import CPSGD  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="C2")
+ap.add_argument("--sampler", default="leverage")
+ap.add_argument("--sweeps", type=int, default=5)
+ap.add_argument("--direct", action="store_true", help="no CUDA graph")
+a = ap.parse_args()
+cfg = synth.CONFIGS[a.workload]
+X = synth.tensor(cfg)
+A0 = synth.init_factors(cfg, X)
+dev = torch.device("cuda:0")
+Xd = torch.from_numpy(X).to(dev)
+Ad = [torch.from_numpy(x).to(dev) for x in A0]
+h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=a.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta, seed=0,
+          graphs=not a.direct)
+h.sweep(2)
+h.sync()
+t = time.perf_counter()
+h.sweep(a.sweeps)
+h.sync()
+print(f"{a.workload} {a.sampler}: {(time.perf_counter() - t) / a.sweeps * 1e6:.1f} us/sweep")
+h.close()
+if os.environ.get("CPSGD_DEBUG_TIMERS"):
+    h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=a.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta, seed=0,
+              graphs=False)
+    h.sweep(3)
+    t = h.debug_timers()
+    names = ["start", "stageB", "gram-synced", "sweep-start", "sweep-done", "scores-done", "cdf-synced", "sampled"]
+    print(" ".join(f"{names[i]}:{t[i] - t[0]}" for i in range(8)))
+    print("iter1: pivot->rcp", t[9] - t[8], "update", t[10] - t[9], "sync", t[11] - t[10], "rowcol+sync", t[12] - t[11],
+          "full iter", t[13] - t[8])
+    print("smids", t[16:32])
