@@ -8,8 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "cpsgd.cu")
-DEPS = [SRC, os.path.join(HERE, "csrc", "kernels.cuh"), os.path.join(HERE, "csrc", "philox.cuh"),
-        os.path.join(ROOT, "include", "cpsgd.h")]
+DEPS = [os.path.join(HERE, "csrc", f) for f in sorted(os.listdir(os.path.join(HERE, "csrc")))] + \
+       [os.path.join(ROOT, "include", "cpsgd.h"), os.path.abspath(__file__)]
 OUT = os.path.join(HERE, "libcpsgd.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -509,7 +509,7 @@ cp_status launch_reduce(cp_sgd_s* h, int n) {
 bool sharded(const cp_sgd_s* h) { return h->world_size > 1; }
 
 // ---- persistent single-cluster sweep kernel (fused.cuh) ----------------------------------------
-template <typename T, int RMAX, int ROWS>
+template <typename T, int ROWS>
 cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev) {
   ProfScope ps(h, kKFused);
   FusedParams<T> p;
@@ -562,8 +562,8 @@ cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, dou
   p.dbg = h->dbg;
   static bool attr_set = false;
   if (!attr_set) {
-    allow_max_dyn_smem(k_sweep_fused<T, RMAX, ROWS>);
-    cudaFuncSetAttribute(k_sweep_fused<T, RMAX, ROWS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    allow_max_dyn_smem(k_sweep_fused<T, ROWS>);
+    cudaFuncSetAttribute(k_sweep_fused<T, ROWS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
@@ -578,7 +578,7 @@ cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, dou
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&lc, k_sweep_fused<T, RMAX, ROWS>, p);
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_sweep_fused<T, ROWS>, p);
   h->launches++;
   if (e != cudaSuccess)
     return h->fail(CP_ECUDA, "k_sweep_fused launch (cluster %d, smem %zu): %s", h->fused_cu, h->fused_smem,
@@ -590,15 +590,8 @@ template <typename T>
 cp_status launch_fused_r(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev) {
   int64_t imax = 0;
   for (int k = 0; k < h->N; ++k) imax = std::max(imax, h->dims[k]);
-  const bool two = imax > kFThreads;
-  if (h->R <= 8)
-    return two ? launch_fused_t<T, 8, 2>(h, nsteps, first_mode, order, alpha, alpha_dev)
-               : launch_fused_t<T, 8, 1>(h, nsteps, first_mode, order, alpha, alpha_dev);
-  if (h->R <= 16)
-    return two ? launch_fused_t<T, 16, 2>(h, nsteps, first_mode, order, alpha, alpha_dev)
-               : launch_fused_t<T, 16, 1>(h, nsteps, first_mode, order, alpha, alpha_dev);
-  return two ? launch_fused_t<T, 32, 2>(h, nsteps, first_mode, order, alpha, alpha_dev)
-             : launch_fused_t<T, 32, 1>(h, nsteps, first_mode, order, alpha, alpha_dev);
+  return imax > kFThreads ? launch_fused_t<T, 2>(h, nsteps, first_mode, order, alpha, alpha_dev)
+                          : launch_fused_t<T, 1>(h, nsteps, first_mode, order, alpha, alpha_dev);
 }
 
 cp_status launch_fused(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev) {
@@ -611,7 +604,8 @@ cp_status launch_fused(cp_sgd_s* h, int nsteps, int first_mode, int order, doubl
 // geometry + eligibility of the fused kernel: one GPU, R <= 32, I_n <= 512, fits shared memory
 void plan_fused(cp_sgd_s* h) {
   h->fused_cu = 0;
-  if (h->world_size > 1 || (h->flags & CP_FLAG_NO_FUSED) || h->R > 32) return;
+  if (h->world_size > 1 || (h->flags & CP_FLAG_NO_FUSED)) return;
+  if (fused_rp(h->R, h->esz) / (h->esz == 8 ? 2 : 4) > 8) return;  // gather_contract supports <= 8 vector groups
   int64_t imax = 0, bmx = 0, cdfmax = 0;
   for (int n = 0; n < h->N; ++n) {
     imax = std::max(imax, h->dims[n]);

@@ -52,8 +52,12 @@ struct FusedParams {
 
 // shared memory layout (bytes) -- mirrored by the host
 struct FusedLayout {
-  size_t zw, zu, fb, wt, ix, mp, gp, gam, aold, anew, gpart, gm, prow, qrow, qtot, cdfs, total;
+  size_t zw, zu, fb, wt, ix, pt, mp, gp, gam, aold, anew, gpart, gm, prow, sc, rowbuf, swept, qtot, cdfs, total;
 };
+__host__ __device__ inline int fused_rp(int R, size_t esz) {
+  const int W = esz == 8 ? 2 : 4;
+  return (R + W - 1) / W * W;
+}
 __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int RPC, int64_t Imax, int64_t cdf_elems,
                                                     size_t esz) {
   FusedLayout L;
@@ -64,11 +68,13 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
     off += bytes;
     return at;
   };
-  L.zw = take(esz * BPC * R);
-  L.zu = take(esz * BPC * R);
+  const int RP = fused_rp(R, esz);
+  L.zw = take(esz * BPC * RP);
+  L.zu = take(esz * BPC * RP);
   L.fb = take(sizeof(int64_t) * BPC);
   L.wt = take(sizeof(double) * BPC);
   L.ix = take(sizeof(int32_t) * BPC * (N - 1));
+  L.pt = take(sizeof(double) * BPC * (N - 1));
   L.mp = take(esz * Imax * R);
   L.gp = take(esz * R * R);
   L.gam = take(esz * R * R);
@@ -77,94 +83,277 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
   L.gpart = take(sizeof(double) * (R * (R + 1) / 2 + 2));
   L.gm = take(sizeof(double) * R * (R + 1));
   L.prow = take(sizeof(double) * RPC);
-  L.qrow = take(sizeof(unsigned long long) * RPC);
+  L.sc = take(sizeof(double) * RPC * R);
+  L.rowbuf = take(sizeof(double) * 2 * R);
+  L.swept = take(sizeof(int) * R);
   L.qtot = take(sizeof(unsigned long long) * 2);
   L.cdfs = take(sizeof(uint64_t) * cdf_elems);
   L.total = off + 16;
   return L;
 }
 
-// ------------------------------------------------------------------------------------------
-// single-warp register-resident symmetric sweep (Gauss-Jordan on the SPD Gram, natural pivot
-// order, pivots with Schur diagonal <= tol skipped -- reading R4(b)); lane j owns column j.
-// On exit Gm (stride R+1) holds W = (G_SS)^{-1} on the swept set S and 0 elsewhere; returns |S|.
-// ------------------------------------------------------------------------------------------
-template <int RMAX>
-__device__ int warp_sweep_inverse(double* Gm, int R, double tol) {
-  const int lane = threadIdx.x & 31;
-  const int RS = R + 1;
-  double col[RMAX];
+
+// rank-ordered sum over the cluster of ptr[idx] in every CTA's shared memory: all remote loads are
+// issued before the (fixed-order) additions; ranks >= CU contribute exact zeros.
+template <typename T>
+__device__ __forceinline__ T cluster_sum(const cooperative_groups::cluster_group& cl, T* ptr, int idx, int CU) {
+  T v[16];
 #pragma unroll
-  for (int i = 0; i < RMAX; ++i) col[i] = (lane < R && i < R) ? Gm[i * RS + lane] : 0.0;
-  bool swept = false;
+  for (int qq = 0; qq < 16; ++qq) v[qq] = (qq < CU) ? cl.map_shared_rank(ptr, qq)[idx] : T(0);
+  T s = v[0];
+#pragma unroll
+  for (int qq = 1; qq < 16; ++qq) s += v[qq];
+  return s;
+}
+
+// CTA-wide symmetric sweep (Gauss-Jordan on the SPD Gram in natural pivot order; a pivot whose
+// Schur diagonal is <= tol is skipped -- reading R4(b)).  Every thread keeps its fixed entries
+// of the R x R matrix in registers; the pivot row (= column, by symmetry) is published through a
+// double-buffered shared row, so each pivot costs one barrier.  On exit Gm (stride R+1) holds
+// W = (G_SS)^{-1} on the swept set S and 0 elsewhere; returns |S| (same value in every thread).
+template <int kSweepEPT>  // entries per thread: R^2 <= kSweepEPT * blockDim.x
+__device__ int cta_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /* 2*R */, int* swept /* R */) {
+  const int tid = threadIdx.x, nth = blockDim.x, RS = R + 1;
+  double v[kSweepEPT];
+  int ei[kSweepEPT], ej[kSweepEPT];
+#pragma unroll
+  for (int t = 0; t < kSweepEPT; ++t) {
+    const int e = tid + t * nth;
+    ei[t] = (e < R * R) ? e / R : -1;
+    ej[t] = (e < R * R) ? e % R : 0;
+    v[t] = (e < R * R) ? Gm[ei[t] * RS + ej[t]] : 0.0;
+  }
+  for (int j = tid; j < R; j += nth) {
+    rowbuf[j] = Gm[j];  // row 0
+    swept[j] = 0;
+  }
+  __syncthreads();
   int rank = 0;
-#pragma unroll 1
   for (int k = 0; k < R; ++k) {
-    // diagonal of column k lives in lane k: M[k][k] = col_k[k]
-    double mine = 0.0;
+    const double* rk = rowbuf + (k & 1) * R;
+    double* rn = rowbuf + ((k + 1) & 1) * R;
+    const double d = rk[k];
+    const bool piv = d > tol;
+    if (piv) {
+      ++rank;
+      const double dinv = __drcp_rn(d);
 #pragma unroll
-    for (int i = 0; i < RMAX; ++i)
-      if (i == k) mine = col[i];
-    const double d = __shfl_sync(0xffffffffu, mine, k);
-    if (!(d > tol)) continue;  // numerically dependent column: leave unswept
-    ++rank;
-    const double dinv = __drcp_rn(d);
-    // my entry in row k (= M[k][lane]) and the pivot column entries M[i][k] (broadcast from lane k)
-    double mkj = 0.0;
+      for (int t = 0; t < kSweepEPT; ++t) {
+        const int i = ei[t], j = ej[t];
+        const double rki = rk[i < 0 ? 0 : i], rkj = rk[j];
+        double nv = v[t] - rki * (rkj * dinv);
+        nv = (j == k) ? rki * dinv : nv;
+        nv = (i == k) ? rkj * dinv : nv;
+        nv = (i == k && j == k) ? -dinv : nv;
+        v[t] = (i >= 0) ? nv : v[t];
+      }
+      if (tid == 0) swept[k] = 1;
+    }
+    // publish row k+1 of the (possibly updated) matrix for the next pivot
 #pragma unroll
-    for (int i = 0; i < RMAX; ++i)
-      if (i == k) mkj = col[i];
+    for (int t = 0; t < kSweepEPT; ++t)
+      if (ei[t] == k + 1) rn[ej[t]] = v[t];
+    __syncthreads();
+  }
 #pragma unroll
-    for (int i = 0; i < RMAX; ++i) {
-      const double mik = __shfl_sync(0xffffffffu, col[i], k);
-      if (i < R) {
-        if (lane == k) {
-          col[i] = (i == k) ? -dinv : col[i] * dinv;
-        } else {
-          col[i] = (i == k) ? mkj * dinv : col[i] - mik * (mkj * dinv);
+  for (int t = 0; t < kSweepEPT; ++t) {
+    const int i = ei[t], j = ej[t];
+    if (i >= 0) Gm[i * RS + j] = (swept[i] && swept[j]) ? -v[t] : 0.0;
+  }
+  __syncthreads();
+  return rank;
+}
+
+
+// single-warp symmetric sweep for R <= 32 (same algorithm and reading R4(b) as cta_sweep_inverse):
+// lane owns entries e = lane + 32 t of the R x R matrix in registers; the pivot row is published
+// through a double-buffered shared row, so each pivot costs one __syncwarp (no CTA barrier).
+__device__ int warp_sweep_inverse32(double* Gm, int R, double tol, double* rowbuf /* 2*R */, int* swept /* R */) {
+  const int lane = threadIdx.x & 31, RS = R + 1;
+  constexpr int EPT = 32;  // R^2 <= 1024
+  double v[EPT];
+  int ij[EPT];
+#pragma unroll
+  for (int t = 0; t < EPT; ++t) {
+    const int e = lane + 32 * t;
+    const int i = e / R, j = e % R;
+    ij[t] = (e < R * R) ? (i << 8) | j : -1;
+    v[t] = (e < R * R) ? Gm[i * RS + j] : 0.0;
+  }
+  for (int j = lane; j < R; j += 32) {
+    rowbuf[j] = Gm[j];
+    swept[j] = 0;
+  }
+  __syncwarp();
+  int rank = 0;
+  for (int k = 0; k < R; ++k) {
+    const double* rk = rowbuf + (k & 1) * R;
+    double* rn = rowbuf + ((k + 1) & 1) * R;
+    const double d = rk[k];
+    if (d > tol) {
+      ++rank;
+      const double dinv = __drcp_rn(d);
+#pragma unroll
+      for (int t = 0; t < EPT; ++t) {
+        if (t * 32 >= R * R) break;  // warp-uniform
+        const int c = ij[t];
+        const int i = c >> 8, j = c & 255;
+        const double rki = rk[i & 31], rkj = rk[j & 31];
+        double nv = v[t] - rki * (rkj * dinv);
+        nv = (j == k) ? rki * dinv : nv;
+        nv = (i == k) ? rkj * dinv : nv;
+        nv = (i == k && j == k) ? -dinv : nv;
+        v[t] = (c >= 0) ? nv : v[t];
+      }
+      if (lane == 0) swept[k] = 1;
+    }
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) {
+      if (t * 32 >= R * R) break;
+      const int c = ij[t];
+      if (c >= 0 && (c >> 8) == k + 1) rn[c & 255] = v[t];
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int t = 0; t < EPT; ++t) {
+    if (t * 32 >= R * R) break;
+    const int c = ij[t];
+    if (c >= 0) {
+      const int i = c >> 8, j = c & 255;
+      Gm[i * RS + j] = (swept[i] && swept[j]) ? -v[t] : 0.0;
+    }
+  }
+  __syncwarp();
+  return rank;
+}
+
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  using type = float4;
+  static constexpr int W = 4;
+};
+template <>
+struct Vec<double> {
+  using type = double2;
+  static constexpr int W = 2;
+};
+
+// fiber gather + contraction for ROWS rows per thread and RV vector groups of columns:
+// acc[u][g] += x(row u) * zw[lb][g]; zw rows padded to RV * W with zeros (stride RP).
+template <typename T, int ROWS, int RV>
+__device__ __forceinline__ void gather_contract(const T* __restrict__ Xn, int64_t es, int64_t In, const int64_t* fb,
+                                                const T* zw, int RP, int BPC, T* Mp, int R) {
+  using V = typename Vec<T>::type;
+  constexpr int W = Vec<T>::W;
+  const int tid = threadIdx.x;
+  V acc[ROWS][RV];
+#pragma unroll
+  for (int u = 0; u < ROWS; ++u)
+#pragma unroll
+    for (int g = 0; g < RV; ++g) {
+      T* a = reinterpret_cast<T*>(&acc[u][g]);
+#pragma unroll
+      for (int c = 0; c < W; ++c) a[c] = T(0);
+    }
+  constexpr int CH = 16;
+  for (int c0 = 0; c0 < BPC; c0 += CH) {
+    T xv[CH][ROWS];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int lb = c0 + c;
+      const int64_t f = (lb < BPC) ? fb[lb] : -1;
+#pragma unroll
+      for (int u = 0; u < ROWS; ++u) {
+        const int64_t i = tid + (int64_t)u * kFThreads;
+        xv[c][u] = (f >= 0 && i < In) ? __ldg(Xn + f + i * es) : T(0);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int lb = c0 + c;
+      if (lb >= BPC) break;
+      const V* z = reinterpret_cast<const V*>(zw + lb * RP);
+#pragma unroll
+      for (int g = 0; g < RV; ++g) {
+        const V zg = z[g];
+        const T* zt = reinterpret_cast<const T*>(&zg);
+#pragma unroll
+        for (int u = 0; u < ROWS; ++u) {
+          T* a = reinterpret_cast<T*>(&acc[u][g]);
+#pragma unroll
+          for (int cc = 0; cc < W; ++cc) a[cc] += xv[c][u] * zt[cc];
         }
       }
     }
-    if (lane == k) swept = true;
   }
-  // W = -M on S x S
-  const unsigned sm = __ballot_sync(0xffffffffu, swept);
 #pragma unroll
-  for (int i = 0; i < RMAX; ++i)
-    if (lane < R && i < R) Gm[i * RS + lane] = (swept && ((sm >> i) & 1u)) ? -col[i] : 0.0;
-  __syncwarp();
-  return rank;
+  for (int u = 0; u < ROWS; ++u) {
+    const int64_t i = tid + (int64_t)u * kFThreads;
+    if (i < In) {
+#pragma unroll
+      for (int g = 0; g < RV; ++g) {
+        const T* a = reinterpret_cast<const T*>(&acc[u][g]);
+#pragma unroll
+        for (int cc = 0; cc < W; ++cc) {
+          const int j = g * W + cc;
+          if (j < R) Mp[i * R + j] = a[cc];
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int ROWS>
+__device__ __forceinline__ void gather_dispatch(const T* Xn, int64_t es, int64_t In, const int64_t* fb, const T* zw,
+                                                int RP, int BPC, T* Mp, int R) {
+  switch (RP / Vec<T>::W) {
+    case 1: gather_contract<T, ROWS, 1>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
+    case 2: gather_contract<T, ROWS, 2>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
+    case 3: gather_contract<T, ROWS, 3>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
+    case 4: gather_contract<T, ROWS, 4>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
+    case 5: gather_contract<T, ROWS, 5>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
+    case 6: gather_contract<T, ROWS, 6>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
+    case 7: gather_contract<T, ROWS, 7>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
+    default: gather_contract<T, ROWS, 8>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
+  }
 }
 
 // ------------------------------------------------------------------------------------------
 // the kernel
 // ------------------------------------------------------------------------------------------
-template <typename T, int RMAX, int ROWS>
+#define F_MARK(slot)                                                          \
+  do {                                                                        \
+    if (p.dbg && q == 0 && tid == 0 && s == 1) p.dbg[slot] = clock64();       \
+  } while (0)
+
+template <typename T, int ROWS>
 __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const int CU = p.CU;
   const int q = (int)cluster.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int N = p.N, R = p.R, RS = R + 1;
+  const int N = p.N, R = p.R, RS = R + 1, NP = N - 1;
+  const int RP = fused_rp(R, sizeof(T));
   extern __shared__ __align__(16) unsigned char f_sm[];
   int64_t cdf_elems = 0;
-  {
-    int64_t mx = 0;
+  if (p.strategy != 0)
     for (int n = 0; n < N; ++n) {
-      int64_t s = 0;
+      int64_t c = 0;
       for (int k = 0; k < N; ++k)
-        if (k != n) s += p.dims[k];
-      mx = max(mx, s);
+        if (k != n) c += p.dims[k];
+      cdf_elems = max(cdf_elems, c);
     }
-    cdf_elems = (p.strategy == 0) ? 0 : mx;
-  }
   const FusedLayout L = fused_layout(N, R, p.BPC, p.RPC, p.Imax, cdf_elems, sizeof(T));
   T* zw = reinterpret_cast<T*>(f_sm + L.zw);
   T* zu = reinterpret_cast<T*>(f_sm + L.zu);
   int64_t* fb = reinterpret_cast<int64_t*>(f_sm + L.fb);
   double* wt = reinterpret_cast<double*>(f_sm + L.wt);
   int32_t* ix = reinterpret_cast<int32_t*>(f_sm + L.ix);
+  double* ptm = reinterpret_cast<double*>(f_sm + L.pt);
   T* Mp = reinterpret_cast<T*>(f_sm + L.mp);
   T* Gp = reinterpret_cast<T*>(f_sm + L.gp);
   T* Gam = reinterpret_cast<T*>(f_sm + L.gam);
@@ -173,102 +362,106 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
   double* gpart = reinterpret_cast<double*>(f_sm + L.gpart);
   double* Gm = reinterpret_cast<double*>(f_sm + L.gm);
   double* prow = reinterpret_cast<double*>(f_sm + L.prow);
-  unsigned long long* qrow = reinterpret_cast<unsigned long long*>(f_sm + L.qrow);
+  double* sc = reinterpret_cast<double*>(f_sm + L.sc);
+  double* rowbuf = reinterpret_cast<double*>(f_sm + L.rowbuf);
+  int* swept = reinterpret_cast<int*>(f_sm + L.swept);
   unsigned long long* qtot = reinterpret_cast<unsigned long long*>(f_sm + L.qtot);
   uint64_t* cdfs = reinterpret_cast<uint64_t*>(f_sm + L.cdfs);
-  __shared__ int64_t s_beff;
   __shared__ int s_bad;
   __shared__ double s_red[kFThreads / 32];
   __shared__ unsigned long long s_wtot[kFThreads / 32];
   __shared__ const uint64_t* s_cp[kMaxOrder];
+  __shared__ int32_t s_start[kMaxOrder], s_len[kMaxOrder];
+  __shared__ double s_wblk;
+  __shared__ int64_t s_beff;
   if (tid == 0) s_bad = 0;
 
   uint64_t r = *p.iter;
   const bool block = (p.strategy == 3 || p.strategy == 4);
-  auto mode_of = [&](uint64_t it, int s) -> int {
-    return p.order == 1 ? random_mode(p.seed, it, N) : (p.first_mode + s) % N;
+  auto mode_of = [&](uint64_t it, int st) -> int {
+    return p.order == 1 ? random_mode(p.seed, it, N) : (p.first_mode + st) % N;
   };
 
-  // ---- sample this CTA's fibers of the batch of mode n at iteration it (contract §8c.2) ----
+  // ---- this CTA's fibers [q*BPC, (q+1)*BPC) of the batch of mode n at iteration it (contract §8c.2)
   auto sample_own = [&](int n, uint64_t it) {
-    // stage the CDFs of the modes k != n
     int64_t off = 0;
     if (tid < kMaxOrder) s_cp[tid] = nullptr;
     __syncthreads();
-    for (int k = 0; k < N; ++k) {
+    for (int k = 0; k < N; ++k) {  // stage the CDFs of the modes k != n
       if (k == n || p.strategy == 0) continue;
       for (int64_t i = tid; i < p.dims[k]; i += kFThreads) cdfs[off + i] = p.cdf[k][i];
       if (tid == 0) s_cp[k] = cdfs + off;
       off += p.dims[k];
     }
-    __syncthreads();
-    const int64_t bmax = p.bmax[n];
-    const int64_t b0 = (int64_t)q * p.BPC;
-    // block strategies: the window draws are common to the whole batch
-    int32_t start[kMaxOrder], len[kMaxOrder];
-    double wblk = 0.0;
-    int64_t beff = p.B;
-    if (block) {
+    if (block && tid == 0) {  // window draws (eq:bik, R2): common to the whole batch
       double prod = 1.0;
-      beff = 1;
+      int64_t beff = 1;
       int pos = 0;
       for (int k = 0; k < N; ++k) {
         if (k == n) continue;
         const int64_t bk = p.window[n][pos];
         const uint64_t Tk = p.Ttot[k];
         const uint64_t rr = scale_draw(draw_word(p.seed, it, 0u, kPurposeWindow, (uint32_t)pos), Tk);
-        const uint64_t* c = s_cp[k];
+        const uint64_t* c = p.cdf[k];
         const int64_t istar = upper_bound_u64(c, p.dims[k], rr);
         const int64_t s0 = (istar / bk) * bk, e0 = min(s0 + bk, p.dims[k]);
         const uint64_t Q = c[e0 - 1] - (s0 > 0 ? c[s0 - 1] : 0ull);
-        start[pos] = (int32_t)s0;
-        len[pos] = (int32_t)(e0 - s0);
+        s_start[pos] = (int32_t)s0;
+        s_len[pos] = (int32_t)(e0 - s0);
         const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * Q), (double)Tk);
         prod = (pos == 0) ? pt : __dmul_rn(prod, pt);
         beff *= (e0 - s0);
         ++pos;
       }
-      wblk = __ddiv_rn(1.0, prod);
+      s_wblk = __ddiv_rn(1.0, prod);
+      s_beff = beff;
+    } else if (tid == 0) {
+      s_beff = p.B;
     }
-    if (tid == 0) s_beff = beff;
+    __syncthreads();
+    const int64_t bmax = p.bmax[n], b0 = (int64_t)q * p.BPC, beff = s_beff;
+    if (!block) {  // one thread per (fiber, position) draw (eq:ik)
+      for (int e = tid; e < p.BPC * NP; e += kFThreads) {
+        const int lb = e / NP, pos = e % NP;
+        const int64_t b = b0 + lb;
+        if (b >= bmax) continue;
+        int k = pos < n ? pos : pos + 1;
+        const uint64_t Tk = (p.strategy == 0) ? (uint64_t)p.dims[k] : p.Ttot[k];
+        const uint64_t rr = scale_draw(draw_word(p.seed, it, (uint32_t)b, kPurposeRow, (uint32_t)pos), Tk);
+        int64_t i;
+        uint64_t qk;
+        if (p.strategy == 0) {
+          i = (int64_t)rr;
+          qk = 1;
+        } else {
+          const uint64_t* c = s_cp[k];
+          i = upper_bound_u64(c, p.dims[k], rr);
+          qk = c[i] - (i > 0 ? c[i - 1] : 0ull);
+        }
+        ix[e] = (int32_t)i;
+        ptm[e] = __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);
+      }
+      __syncthreads();
+    }
     for (int lb = tid; lb < p.BPC; lb += kFThreads) {
       const int64_t b = b0 + lb;
-      int32_t* ib = ix + lb * (N - 1);
+      int32_t* ib = ix + lb * NP;
       if (b >= bmax || b >= beff) {
         fb[lb] = -1;
         wt[lb] = 0.0;
         continue;
       }
       if (!block) {
-        double prod = 1.0;
-        int pos = 0;
-        for (int k = 0; k < N; ++k) {
-          if (k == n) continue;
-          const uint64_t Tk = (p.strategy == 0) ? (uint64_t)p.dims[k] : p.Ttot[k];
-          const uint64_t rr = scale_draw(draw_word(p.seed, it, (uint32_t)b, kPurposeRow, (uint32_t)pos), Tk);
-          int64_t i;
-          uint64_t qk;
-          if (p.strategy == 0) {
-            i = (int64_t)rr;
-            qk = 1;
-          } else {
-            const uint64_t* c = s_cp[k];
-            i = upper_bound_u64(c, p.dims[k], rr);
-            qk = c[i] - (i > 0 ? c[i - 1] : 0ull);
-          }
-          ib[pos] = (int32_t)i;
-          const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);
-          prod = (pos == 0) ? pt : __dmul_rn(prod, pt);
-          ++pos;
-        }
+        double prod = ptm[lb * NP];
+        for (int pos = 1; pos < NP; ++pos) prod = __dmul_rn(prod, ptm[lb * NP + pos]);
         wt[lb] = __ddiv_rn(1.0, __dmul_rn((double)p.B, prod));
       } else {
         int64_t rem = b;
-        for (int qq = 0; qq < N - 1; ++qq) {
-          ib[qq] = start[qq] + (int32_t)(rem % len[qq]);
-          rem /= len[qq];
+        for (int qq = 0; qq < NP; ++qq) {
+          ib[qq] = s_start[qq] + (int32_t)(rem % s_len[qq]);
+          rem /= s_len[qq];
         }
-        wt[lb] = wblk;
+        wt[lb] = s_wblk;
       }
       int64_t offn = 0, jrow = 0, jmul = 1;
       int pos = 0;
@@ -282,17 +475,17 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
       fb[lb] = p.pitch[n] ? jrow * p.pitch[n] : offn;
     }
     __syncthreads();
-    // SKR rows (Alg. 1): z = (*)_{k != n} A^(k)(i_k, :); zw = w z
-    for (int e = tid; e < p.BPC * R; e += kFThreads) {
-      const int lb = e / R, rr = e % R;
+    // SKR rows (Alg. 1): z = (*)_{k != n} A^(k)(i_k, :); zw = w z; padded to RP with zeros
+    for (int e = tid; e < p.BPC * RP; e += kFThreads) {
+      const int lb = e / RP, rr = e % RP;
       T z = T(0), zwv = T(0);
-      if (fb[lb] >= 0) {
-        const int32_t* ib = ix + lb * (N - 1);
+      if (rr < R && fb[lb] >= 0) {
+        const int32_t* ib = ix + lb * NP;
         z = T(1);
         int pos = 0;
         for (int k = 0; k < N; ++k) {
           if (k == n) continue;
-          z = z * p.factors[k][(int64_t)ib[pos++] * R + rr];
+          z = z * __ldg(p.factors[k] + (int64_t)ib[pos++] * R + rr);
         }
         zwv = (T)wt[lb] * z;
       }
@@ -308,70 +501,28 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
 
 #pragma unroll 1
   for (int s = 0; s < p.nsteps; ++s) {
+    F_MARK(0);
     const int64_t In = p.dims[n];
     const int64_t rpc = (In + CU - 1) / CU;
     const int64_t r_beg = min((int64_t)q * rpc, In), r_end = min(r_beg + rpc, In);
     const int nr = (int)(r_end - r_beg);
-    // ------------------------------------------------ (1) gather + partial contractions
-    {
-      T acc[ROWS][RMAX];
-#pragma unroll
-      for (int u = 0; u < ROWS; ++u)
-#pragma unroll
-        for (int j = 0; j < RMAX; ++j) acc[u][j] = T(0);
-      const T* Xn = p.Xg[n];
-      const int64_t es = p.estride[n];
-      for (int c0 = 0; c0 < p.BPC; c0 += kFChunk) {
-        T xv[kFChunk][ROWS];
-#pragma unroll
-        for (int c = 0; c < kFChunk; ++c) {
-          const int lb = c0 + c;
-          const int64_t f = (lb < p.BPC) ? fb[lb] : -1;
-#pragma unroll
-          for (int u = 0; u < ROWS; ++u) {
-            const int64_t i = tid + (int64_t)u * kFThreads;
-            xv[c][u] = (f >= 0 && i < In) ? __ldg(Xn + f + i * es) : T(0);
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < kFChunk; ++c) {
-          const int lb = c0 + c;
-          if (lb < p.BPC) {
-#pragma unroll
-            for (int j = 0; j < RMAX; ++j) {
-              const T z = (j < R) ? zw[lb * R + j] : T(0);
-#pragma unroll
-              for (int u = 0; u < ROWS; ++u) acc[u][j] += xv[c][u] * z;
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < ROWS; ++u) {
-        const int64_t i = tid + (int64_t)u * kFThreads;
-        if (i < In)
-#pragma unroll
-          for (int j = 0; j < RMAX; ++j)
-            if (j < R) Mp[i * R + j] = acc[u][j];
-      }
-      for (int e = tid; e < R * R; e += kFThreads) {
-        const int r1 = e / R, r2 = e % R;
-        T g = T(0);
-        for (int lb = 0; lb < p.BPC; ++lb) g += zw[lb * R + r1] * zu[lb * R + r2];
-        Gp[e] = g;
-      }
-    }
-    cluster.sync();  // #1: partials visible
-    // ------------------------------------------------ (2) cluster reduction (rank order) + update
+    // ------------------------------------------------ (1) gather (Alg. 5) + partial contractions
+    gather_dispatch<T, ROWS>(p.Xg[n], p.estride[n], In, fb, zw, RP, p.BPC, Mp, R);
     for (int e = tid; e < R * R; e += kFThreads) {
+      const int r1 = e / R, r2 = e % R;
       T g = T(0);
-      for (int qq = 0; qq < CU; ++qq) g += cluster.map_shared_rank(Gp, qq)[e];
-      Gam[e] = g;
+      for (int lb = 0; lb < p.BPC; ++lb) g += zw[lb * RP + r1] * zu[lb * RP + r2];
+      Gp[e] = g;
     }
-    for (int e = tid; e < nr * R; e += kFThreads) {
+    for (int e = tid; e < nr * R; e += kFThreads) {  // old rows of the block this CTA updates
       const int il = e / R, c = e % R;
       Aold[il * RS + c] = p.factors[n][(r_beg + il) * R + c];
     }
+    F_MARK(1);
+    cluster.sync();  // #1: partials visible
+    F_MARK(2);
+    // ------------------------------------------------ (2) cluster reduction (rank order) + update
+    for (int e = tid; e < R * R; e += kFThreads) Gam[e] = cluster_sum(cluster, Gp, e, CU);
     __syncthreads();
     if (q == 0 && s == p.nsteps - 1)
       for (int e = tid; e < R * R; e += kFThreads) p.Gam_out[e] = Gam[e];
@@ -379,8 +530,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     for (int e = tid; e < nr * R; e += kFThreads) {
       const int il = e / R, rr = e % R;
       const int64_t i = r_beg + il;
-      T m = T(0);
-      for (int qq = 0; qq < CU; ++qq) m += cluster.map_shared_rank(Mp, qq)[i * R + rr];
+      const T m = cluster_sum(cluster, Mp, (int)(i * R + rr), CU);
       T ag = T(0);
       for (int c = 0; c < R; ++c) ag += Aold[il * RS + c] * Gam[c * R + rr];
       const T g = ag - m;
@@ -404,6 +554,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
       Anew[il * RS + rr] = an;
     }
     __syncthreads();
+    F_MARK(3);
     // ------------------------------------------------ (3) importance table of the new A^(n)
     if (p.strategy != 0) {
       const bool lev = (p.strategy == 1 || p.strategy == 3);
@@ -434,13 +585,12 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
           gpart[0] = t;
         }
       }
+      F_MARK(4);
       cluster.sync();  // #2: partial Grams / norms visible
-      int rank = 1;
-      double fro = 1.0;
+      F_MARK(5);
       if (lev) {
         for (int pair = tid; pair < P; pair += kFThreads) {
-          double sum = 0.0;
-          for (int qq = 0; qq < CU; ++qq) sum += cluster.map_shared_rank(gpart, qq)[pair];
+          const double sum = cluster_sum(cluster, gpart, pair, CU);
           int r1 = 0, rem = pair;
           while (rem >= R - r1) { rem -= R - r1; ++r1; }
           const int r2 = r1 + rem;
@@ -448,6 +598,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
           Gm[r2 * RS + r1] = sum;
         }
         __syncthreads();
+        F_MARK(13);
         if (wid == 0) {
           double d0 = 0.0;
           bool fin = true;
@@ -458,37 +609,39 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
           }
           for (int o = 16; o > 0; o >>= 1) d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
           if (!__all_sync(0xffffffffu, fin) && lane == 0) s_bad |= 8;
-          const double tol = (double)(In > R ? In : R) * 2.220446049250313e-16 * d0;
-          const int rk = warp_sweep_inverse<RMAX>(Gm, R, tol);
-          if (lane == 0) s_red[0] = (double)rk;
+          if (lane == 0) s_red[0] = (double)(In > R ? In : R) * 2.220446049250313e-16 * d0;
         }
         __syncthreads();
-        rank = (int)s_red[0];
+        const int rank = cta_sweep_inverse<(32 * 32 + kFThreads - 1) / kFThreads>(Gm, R, s_red[0], rowbuf, swept);
+        F_MARK(6);
         if (tid == 0 && rank == 0) s_bad |= 2;
-        // scores: l = a^T W a, one warp per row, lanes over the R^2 products
-        for (int il = wid; il < nr; il += kFThreads / 32) {
+        // scores l = a^T W a: thread per (row, i) forms a_i * (W a)_i; rows summed in order
+        for (int e = tid; e < nr * R; e += kFThreads) {
+          const int il = e / R, i = e % R;
           const T* a = Anew + il * RS;
-          double part = 0.0;
-          for (int e = lane; e < R * R; e += 32) {
-            const int i = e / R, j = e % R;
-            part += (double)a[i] * Gm[i * RS + j] * (double)a[j];
-          }
-          for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-          if (lane == 0) prow[il] = rank > 0 ? fmax(part, 0.0) / (double)rank : 0.0;
+          double t = 0.0;
+          for (int j = 0; j < R; ++j) t += Gm[i * RS + j] * (double)a[j];
+          sc[e] = (double)a[i] * t;
+        }
+        __syncthreads();
+        for (int il = tid; il < nr; il += kFThreads) {
+          double l = 0.0;
+          for (int i = 0; i < R; ++i) l += sc[il * R + i];
+          prow[il] = rank > 0 ? fmax(l, 0.0) / (double)rank : 0.0;
         }
       } else {
         if (tid == 0) {
-          double t = 0.0;
-          for (int qq = 0; qq < CU; ++qq) t += cluster.map_shared_rank(gpart, qq)[0];
+          const double t = cluster_sum(cluster, gpart, 0, CU);
           s_red[0] = t;
           if (!(t == t) || t > 1.7e308) s_bad |= 8;
           else if (!(t > 0.0)) s_bad |= 2;
         }
         __syncthreads();
-        fro = s_red[0];
-        for (int il = tid; il < nr; il += kFThreads) prow[il] = prow[il] / fro;
+        const double fro = s_red[0];
+        for (int il = tid; il < nr; il += kFThreads) prow[il] = fro > 0.0 ? prow[il] / fro : 0.0;
       }
       __syncthreads();
+      F_MARK(7);
       // quantise + scan (thread per row; rows per CTA <= kFThreads)
       unsigned long long qv = 0;
       if (tid < nr) {
@@ -496,8 +649,8 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
         if (!(pv == pv) || pv > 2.0) {
           atomicOr(&s_bad, 8);
         } else if (pv > 0.0) {
-          const double sc = rint(pv * 4294967296.0);
-          qv = (sc < 1.0) ? 1ull : (unsigned long long)sc;
+          const double scv = rint(pv * 4294967296.0);
+          qv = (scv < 1.0) ? 1ull : (unsigned long long)scv;
         }
         p.pprob[n][r_beg + tid] = pv;
       }
@@ -511,13 +664,19 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
       unsigned long long wpre = 0;
       for (int w = 0; w < wid; ++w) wpre += s_wtot[w];
       if (tid == kFThreads - 1) qtot[0] = wpre + incl;
-      __syncthreads();
+      F_MARK(8);
       cluster.sync();  // #3: CTA totals visible
+      F_MARK(9);
       unsigned long long cpre = 0, total = 0;
-      for (int qq = 0; qq < CU; ++qq) {
-        const unsigned long long t = cluster.map_shared_rank(qtot, qq)[0];
-        if (qq < q) cpre += t;
-        total += t;
+      {
+        unsigned long long tv[16];
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) tv[qq] = qq < CU ? cluster.map_shared_rank(qtot, qq)[0] : 0ull;
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) {
+          if (qq < q) cpre += tv[qq];
+          total += tv[qq];
+        }
       }
       if (tid < nr) p.cdf[n][r_beg + tid] = cpre + wpre + incl;
       if (tid == 0) {
@@ -531,11 +690,12 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     ++r;
     n_done = n;
     const int n_next = mode_of(r, s + 1);
+    F_MARK(10);
     __threadfence();
     cluster.sync();  // #4: factors, CDF and T of mode n visible cluster-wide; peers done with our smem
-    if (s + 1 < p.nsteps) {
-      sample_own(n_next, r);
-    }
+    F_MARK(11);
+    if (s + 1 < p.nsteps) sample_own(n_next, r);
+    F_MARK(12);
     n = n_next;
   }
   if (q == 0 && tid == 0) {

@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kTableThreads) k_table(const T* __restrict__ A
     } else if (euc) {
       double rs = 0.0;
       for (int r = 0; r < R; ++r) rs += (double)A[i * R + r] * (double)A[i * R + r];
-      p = rs / fro;
+      p = fro > 0.0 ? rs / fro : 0.0;
     } else {
       p = 1.0 / (double)I;
     }
@@ -1012,7 +1012,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     }
     __syncthreads();
     const double fro = s_fro;
-    for (int il = tid; il < nr; il += kUTThreads) prow[il] = prow[il] / fro;
+    for (int il = tid; il < nr; il += kUTThreads) prow[il] = fro > 0.0 ? prow[il] / fro : 0.0;
   }
   __syncthreads();
   UT_MARK(5);

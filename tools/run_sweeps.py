@@ -32,7 +32,15 @@ h.sweep(a.sweeps)
 h.sync()
 print(f"{a.workload} {a.sampler}: {(time.perf_counter() - t) / a.sweeps * 1e6:.1f} us/sweep")
 h.close()
-if os.environ.get("CPSGD_DEBUG_TIMERS"):
+if os.environ.get("CPSGD_DEBUG_TIMERS") and os.environ.get("FUSED_TIMERS"):
+    h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=a.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta, seed=0)
+    h.sweep(1)
+    t = h.debug_timers()
+    names = ["gather", "sync1", "reduce+update", "gram-part", "sync2", "gram-sum+sweep", "scores", "scan", "sync3",
+             "cdf", "sync4", "sample"]
+    print(" | ".join(f"{names[i]}:{t[i + 1] - t[i]}" for i in range(12)), "| total", t[12] - t[0])
+    print("gram-sum", t[13] - t[5], "sweep", t[6] - t[13])
+elif os.environ.get("CPSGD_DEBUG_TIMERS"):
     h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=a.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta, seed=0,
               graphs=False)
     h.sweep(3)
