@@ -218,17 +218,27 @@ def run_ours(args, cfg):
     gather_bytes = (fibers_per_step / N) * In_avg * esz
     useful_gbs = value * (sum(cfg.dims) / N) * esz / 1e9
     roof = None
-    if "k_gather" in kern:
-        t_g = kern["k_gather"]["avg_us"] * 1e-6
-        ach = gather_bytes / t_g / 1e9
+    # algorithmic bytes per launch of the dominant kernel: the sampled fibers it gathers
+    # (B_eff x I_n x sizeof per SGD iteration), nothing else counted
+    if dominant == "k_sweep_fused":
+        per_launch = prof_sweeps * fibers_per_step * (sum(cfg.dims) / N) * esz
+    elif dominant == "k_gather":
+        per_launch = gather_bytes
+    else:
+        per_launch = None
+    if dominant is not None and per_launch is not None:
+        t_k = kern[dominant]["avg_us"] * 1e-6
+        ach = per_launch / t_k / 1e9
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tfile):
-            traffic = json.load(open(tfile)).get(f"{cfg.name}/{args.sampler}/k_gather")
-        roof = {"kernel": "k_gather", "bound": "hbm", "achieved": round(ach, 2), "peak": peaks["hbm_gbs"],
+            traffic = json.load(open(tfile)).get(f"{cfg.name}/{args.sampler}/{dominant}")
+        roof = {"kernel": dominant, "bound": "hbm", "achieved": round(ach, 2), "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "_fallback" not in peaks else "fallback",
-                "algorithmic_bytes_per_launch": gather_bytes}
+                "algorithmic_bytes_per_launch": per_launch,
+                "note": "latency-bound chain: per-step phases are serial (sample -> gather -> reduce -> update -> "
+                        "table -> sample); see DESIGN.md 'Roofline'"}
     # ---- e2e: host-buffer C-ABI call, H2D of all factors + D2H every step ----
     host = [a.detach().cpu().pin_memory() for a in Ad]
     h2d = sum(a.numel() * esz for a in host)

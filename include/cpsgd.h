@@ -166,6 +166,10 @@ cp_status cp_sgd_step_phase(cp_sgd_t h, int32_t mode, int32_t phase, double alph
 cp_status cp_sgd_exchange_info(cp_sgd_t h, int32_t mode, void** buf_dev, int64_t* count, int64_t* row_begin,
                                int64_t* row_end);
 
+/* copy the exchange buffer of `mode` (the partial M after phase 0, R x I_n of cfg.dtype, layout
+ * [R][I_n]) to (to_lib = 0) or from (to_lib = 1) a caller device buffer, on the handle's stream */
+cp_status cp_sgd_exchange_copy(cp_sgd_t h, int32_t mode, void* buf_dev, int32_t to_lib);
+
 /* ---- parity / debug hooks (synchronise) -------------------------------------------------- */
 /* integer table of `mode`: q_host[I_mode] (may be NULL), T_host (may be NULL), p_host (fp64
  * probabilities before quantisation, may be NULL) */

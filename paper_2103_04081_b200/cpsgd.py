@@ -29,7 +29,7 @@ EXPORTS = ["cp_sgd_init", "cp_sgd_destroy", "cp_sgd_last_error", "cp_sgd_sample"
            "cp_fit", "cp_sgd_sync", "cp_sgd_steps_host", "cp_sgd_step_phase", "cp_sgd_exchange_info",
            "cp_sgd_get_table", "cp_sgd_get_grad", "cp_sgd_get_accum", "cp_sgd_get_iter", "cp_sgd_set_iter",
            "cp_sgd_refresh_tables", "cp_sgd_get_launches", "cp_sgd_profile", "cp_sgd_profile_read",
-           "cp_sgd_version", "cp_sgd_batch_max", "cp_sgd_debug_timers"]
+           "cp_sgd_version", "cp_sgd_batch_max", "cp_sgd_debug_timers", "cp_sgd_exchange_copy"]
 
 
 class CPError(RuntimeError):
@@ -86,6 +86,7 @@ def load_library(path: str = LIB_PATH):
     L.cp_sgd_profile_read.argtypes = [P, i32, P, P, P, C.POINTER(C.c_int32)]
     L.cp_sgd_version.restype = C.c_char_p
     L.cp_sgd_debug_timers.argtypes = [P, P]
+    L.cp_sgd_exchange_copy.argtypes = [P, i32, P, i32]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype if name in ("cp_sgd_last_error", "cp_sgd_version") else C.c_int
     _lib = L
@@ -202,6 +203,10 @@ class CPSGD:
         buf, cnt, rb, re = C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int64()
         self._chk(self._L.cp_sgd_exchange_info(self._h, mode, C.byref(buf), C.byref(cnt), C.byref(rb), C.byref(re)))
         return buf.value, cnt.value, rb.value, re.value
+
+    def exchange_copy(self, mode: int, buf, to_lib: bool):
+        """copy the phase-0 exchange buffer (partial M, [R][I_n]) to / from a torch CUDA tensor"""
+        self._chk(self._L.cp_sgd_exchange_copy(self._h, mode, C.c_void_p(buf.data_ptr()), 1 if to_lib else 0))
 
     def sweep(self, nsweeps: int = 1, order: str = "cyclic", alphas=None):
         arr = None

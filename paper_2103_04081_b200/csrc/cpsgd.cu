@@ -1174,6 +1174,18 @@ cp_status cp_sgd_exchange_info(cp_sgd_t h, int32_t mode, void** buf_dev, int64_t
   return CP_OK;
 }
 
+cp_status cp_sgd_exchange_copy(cp_sgd_t h, int32_t mode, void* buf_dev, int32_t to_lib) {
+  cp_status st = check_mode(h, mode);
+  if (st) return st;
+  if (!buf_dev) return h->fail(CP_EINVAL, "NULL buffer");
+  const size_t bytes = h->esz * (size_t)h->R * (size_t)h->In_local[mode];
+  if (to_lib)
+    CUDA_TRY(h, cudaMemcpyAsync(h->Msum, buf_dev, bytes, cudaMemcpyDeviceToDevice, h->stream));
+  else
+    CUDA_TRY(h, cudaMemcpyAsync(buf_dev, h->Msum, bytes, cudaMemcpyDeviceToDevice, h->stream));
+  return CP_OK;
+}
+
 cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double* alpha_per_iter) {
   if (!h) return CP_EINVAL;
   if (nsweeps < 0) return h->fail(CP_EINVAL, "nsweeps < 0");

@@ -1,0 +1,96 @@
+"""Host-side plumbing of the slab-sharded path.
+
+The tensor is split along its LAST mode into contiguous slabs, one per rank.  Every rank holds
+replicated factors and tables and draws the same global batch (same Philox counters).  One SGD
+iteration of mode n is three library phases (cp_sgd_step_phase) with one exchange:
+  n <  N-1 : phase 0 (local fibers -> partial M) ; all-reduce(M) ; phase 1 (update) ; phase 2
+  n == N-1 : phase 0 (local rows of every fiber) ; phase 1 (update of the owned rows) ;
+             broadcast every rank's owned rows ; phase 2 (table refresh)
+With an internal NCCL communicator the library performs these exchanges itself (cp_sgd_step);
+`ShardedRunner` performs them through a `torch.distributed` process group instead (external-comm
+handles), which is also how the host logic is tested on CPU with the gloo backend.
+"""
+from __future__ import annotations
+
+from typing import List, Sequence, Tuple
+
+
+def slab_ranges(I_last: int, world: int) -> List[Tuple[int, int]]:
+    """contiguous, near-equal slabs [lo, hi) of the last mode's index range, rank order."""
+    if world < 1 or I_last < world:
+        raise ValueError("need 1 <= world <= I_last")
+    base, extra = divmod(I_last, world)
+    out, lo = [], 0
+    for r in range(world):
+        hi = lo + base + (1 if r < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def owned_fibers(idx_last, lo: int, hi: int):
+    """mask of sampled fibers whose last-mode index falls in this rank's slab (owner computes)."""
+    return (idx_last >= lo) & (idx_last < hi)
+
+
+class ShardedRunner:
+    """Drives one external-comm handle per rank.  `handle` needs step_phase(mode, phase, alpha),
+    exchange_copy(mode, buf, to_lib) and factor tensors; `group` is a torch.distributed group."""
+
+    def __init__(self, handle, factors: Sequence, dims: Sequence[int], rank: int, world: int, group=None,
+                 device=None):
+        import torch
+
+        self.h = handle
+        self.factors = list(factors)
+        self.dims = [int(d) for d in dims]
+        self.N = len(self.dims)
+        self.R = int(self.factors[0].shape[1])
+        self.rank, self.world, self.group = rank, world, group
+        self.slabs = slab_ranges(self.dims[-1], world)
+        self.device = device if device is not None else self.factors[0].device
+        self.dtype = self.factors[0].dtype
+        self._buf = {}
+        self.torch = torch
+
+    def _exchange_sum(self, n: int):
+        import torch.distributed as dist
+
+        I_local = self.dims[n] if n < self.N - 1 else self.slabs[self.rank][1] - self.slabs[self.rank][0]
+        key = (n, I_local)
+        if key not in self._buf:
+            self._buf[key] = self.torch.empty(self.R * I_local, dtype=self.dtype, device=self.device)
+        buf = self._buf[key]
+        self.h.exchange_copy(n, buf, False)
+        self.sync()
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+        self.h.exchange_copy(n, buf, True)
+
+    def _exchange_rows(self, n: int):
+        import torch.distributed as dist
+
+        self.sync()
+        A = self.factors[n]
+        for r, (lo, hi) in enumerate(self.slabs):
+            rows = A[lo:hi].contiguous()
+            dist.broadcast(rows, src=r, group=self.group)
+            if r != self.rank:
+                A[lo:hi].copy_(rows)
+
+    def sync(self):
+        if hasattr(self.h, "sync"):
+            self.h.sync()
+
+    def step(self, n: int, alpha: float = -1.0):
+        self.h.step_phase(n, 0, alpha)
+        if n < self.N - 1:
+            self._exchange_sum(n)
+        self.h.step_phase(n, 1, alpha)
+        if n == self.N - 1:
+            self._exchange_rows(n)
+        self.h.step_phase(n, 2, alpha)
+
+    def sweep(self, nsweeps: int, alpha: float = -1.0):
+        for _ in range(nsweeps):
+            for n in range(self.N):
+                self.step(n, alpha)
