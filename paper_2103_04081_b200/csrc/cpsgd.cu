@@ -176,6 +176,7 @@ struct cp_sgd_s {
   std::vector<ProfRec> prof_recs;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
+  std::vector<int64_t> row_ranges;  // [2*world]: slab [lo, hi) of every rank
 
   cp_status fail(cp_status st, const char* fmt, ...) {
     char buf[512];
@@ -735,19 +736,10 @@ static cp_status init_fail(cp_sgd_s* h, cp_status st) {
   return st;
 }
 
+// row ranges [lo, hi) of every rank's slab of the last mode (owned rows exchanged after phase 1)
 static std::vector<int64_t>* rr_store(cp_sgd_s* h, bool create) {
-  // row ranges live in a side table keyed by handle (keeps cp_sgd_s POD-like)
-  static thread_local std::vector<std::pair<cp_sgd_s*, std::vector<int64_t>*>> tab;
-  for (auto& e : tab)
-    if (e.first == h) return e.second;
-  if (!create) return nullptr;
-  auto* v = new std::vector<int64_t>();
-  tab.push_back({h, v});
-  return v;
-}
-static void rr_free(cp_sgd_s* h) {
-  auto* v = rr_store(h, false);
-  delete v;
+  if (h->row_ranges.empty() && !create) return nullptr;
+  return &h->row_ranges;
 }
 
 cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
@@ -1055,7 +1047,6 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   if (h->pinned) cudaFreeHost(h->pinned);
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   if (h->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm);
-  rr_free(h);
   cudaGetLastError();
   delete h;
   return CP_OK;

@@ -93,77 +93,6 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
 }
 
 
-// rank-ordered sum over the cluster of ptr[idx] in every CTA's shared memory: all remote loads are
-// issued before the (fixed-order) additions; ranks >= CU contribute exact zeros.
-template <typename T>
-__device__ __forceinline__ T cluster_sum(const cooperative_groups::cluster_group& cl, T* ptr, int idx, int CU) {
-  T v[16];
-#pragma unroll
-  for (int qq = 0; qq < 16; ++qq) v[qq] = (qq < CU) ? cl.map_shared_rank(ptr, qq)[idx] : T(0);
-  T s = v[0];
-#pragma unroll
-  for (int qq = 1; qq < 16; ++qq) s += v[qq];
-  return s;
-}
-
-// CTA-wide symmetric sweep (Gauss-Jordan on the SPD Gram in natural pivot order; a pivot whose
-// Schur diagonal is <= tol is skipped -- reading R4(b)).  Every thread keeps its fixed entries
-// of the R x R matrix in registers; the pivot row (= column, by symmetry) is published through a
-// double-buffered shared row, so each pivot costs one barrier.  On exit Gm (stride R+1) holds
-// W = (G_SS)^{-1} on the swept set S and 0 elsewhere; returns |S| (same value in every thread).
-template <int kSweepEPT>  // entries per thread: R^2 <= kSweepEPT * blockDim.x
-__device__ int cta_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /* 2*R */, int* swept /* R */) {
-  const int tid = threadIdx.x, nth = blockDim.x, RS = R + 1;
-  double v[kSweepEPT];
-  int ei[kSweepEPT], ej[kSweepEPT];
-#pragma unroll
-  for (int t = 0; t < kSweepEPT; ++t) {
-    const int e = tid + t * nth;
-    ei[t] = (e < R * R) ? e / R : -1;
-    ej[t] = (e < R * R) ? e % R : 0;
-    v[t] = (e < R * R) ? Gm[ei[t] * RS + ej[t]] : 0.0;
-  }
-  for (int j = tid; j < R; j += nth) {
-    rowbuf[j] = Gm[j];  // row 0
-    swept[j] = 0;
-  }
-  __syncthreads();
-  int rank = 0;
-  for (int k = 0; k < R; ++k) {
-    const double* rk = rowbuf + (k & 1) * R;
-    double* rn = rowbuf + ((k + 1) & 1) * R;
-    const double d = rk[k];
-    const bool piv = d > tol;
-    if (piv) {
-      ++rank;
-      const double dinv = __drcp_rn(d);
-#pragma unroll
-      for (int t = 0; t < kSweepEPT; ++t) {
-        const int i = ei[t], j = ej[t];
-        const double rki = rk[i < 0 ? 0 : i], rkj = rk[j];
-        double nv = v[t] - rki * (rkj * dinv);
-        nv = (j == k) ? rki * dinv : nv;
-        nv = (i == k) ? rkj * dinv : nv;
-        nv = (i == k && j == k) ? -dinv : nv;
-        v[t] = (i >= 0) ? nv : v[t];
-      }
-      if (tid == 0) swept[k] = 1;
-    }
-    // publish row k+1 of the (possibly updated) matrix for the next pivot
-#pragma unroll
-    for (int t = 0; t < kSweepEPT; ++t)
-      if (ei[t] == k + 1) rn[ej[t]] = v[t];
-    __syncthreads();
-  }
-#pragma unroll
-  for (int t = 0; t < kSweepEPT; ++t) {
-    const int i = ei[t], j = ej[t];
-    if (i >= 0) Gm[i * RS + j] = (swept[i] && swept[j]) ? -v[t] : 0.0;
-  }
-  __syncthreads();
-  return rank;
-}
-
 
 // single-warp symmetric sweep for R <= 32 (same algorithm and reading R4(b) as cta_sweep_inverse):
 // lane owns entries e = lane + 32 t of the R x R matrix in registers; the pivot row is published

@@ -686,6 +686,78 @@ __global__ void __launch_bounds__(kUpdThreads) k_update(UpdateParams<T> p) {
   }
 }
 
+// rank-ordered sum over the cluster of ptr[idx] in every CTA's shared memory: all remote loads are
+// issued before the (fixed-order) additions; ranks >= CU contribute exact zeros.
+template <typename T>
+__device__ __forceinline__ T cluster_sum(const cooperative_groups::cluster_group& cl, T* ptr, int idx, int CU) {
+  T v[16];
+#pragma unroll
+  for (int qq = 0; qq < 16; ++qq) v[qq] = (qq < CU) ? cl.map_shared_rank(ptr, qq)[idx] : T(0);
+  T s = v[0];
+#pragma unroll
+  for (int qq = 1; qq < 16; ++qq) s += v[qq];
+  return s;
+}
+
+// CTA-wide symmetric sweep (Gauss-Jordan on the SPD Gram in natural pivot order; a pivot whose
+// Schur diagonal is <= tol is skipped -- reading R4(b)).  Every thread keeps its fixed entries
+// of the R x R matrix in registers; the pivot row (= column, by symmetry) is published through a
+// double-buffered shared row, so each pivot costs one barrier.  On exit Gm (stride R+1) holds
+// W = (G_SS)^{-1} on the swept set S and 0 elsewhere; returns |S| (same value in every thread).
+template <int kSweepEPT>  // entries per thread: R^2 <= kSweepEPT * blockDim.x
+__device__ int cta_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /* 2*R */, int* swept /* R */) {
+  const int tid = threadIdx.x, nth = blockDim.x, RS = R + 1;
+  double v[kSweepEPT];
+  int ei[kSweepEPT], ej[kSweepEPT];
+#pragma unroll
+  for (int t = 0; t < kSweepEPT; ++t) {
+    const int e = tid + t * nth;
+    ei[t] = (e < R * R) ? e / R : -1;
+    ej[t] = (e < R * R) ? e % R : 0;
+    v[t] = (e < R * R) ? Gm[ei[t] * RS + ej[t]] : 0.0;
+  }
+  for (int j = tid; j < R; j += nth) {
+    rowbuf[j] = Gm[j];  // row 0
+    swept[j] = 0;
+  }
+  __syncthreads();
+  int rank = 0;
+  for (int k = 0; k < R; ++k) {
+    const double* rk = rowbuf + (k & 1) * R;
+    double* rn = rowbuf + ((k + 1) & 1) * R;
+    const double d = rk[k];
+    const bool piv = d > tol;
+    if (piv) {
+      ++rank;
+      const double dinv = __drcp_rn(d);
+#pragma unroll
+      for (int t = 0; t < kSweepEPT; ++t) {
+        const int i = ei[t], j = ej[t];
+        const double rki = rk[i < 0 ? 0 : i], rkj = rk[j];
+        double nv = v[t] - rki * (rkj * dinv);
+        nv = (j == k) ? rki * dinv : nv;
+        nv = (i == k) ? rkj * dinv : nv;
+        nv = (i == k && j == k) ? -dinv : nv;
+        v[t] = (i >= 0) ? nv : v[t];
+      }
+      if (tid == 0) swept[k] = 1;
+    }
+    // publish row k+1 of the (possibly updated) matrix for the next pivot
+#pragma unroll
+    for (int t = 0; t < kSweepEPT; ++t)
+      if (ei[t] == k + 1) rn[ej[t]] = v[t];
+    __syncthreads();
+  }
+#pragma unroll
+  for (int t = 0; t < kSweepEPT; ++t) {
+    const int i = ei[t], j = ej[t];
+    if (i >= 0) Gm[i * RS + j] = (swept[i] && swept[j]) ? -v[t] : 0.0;
+  }
+  __syncthreads();
+  return rank;
+}
+
+
 // ==========================================================================================
 // (a6, a7, a8, a1, a9) fused update + table refresh: ONE thread-block cluster of CU <= 16 CTAs
 // owns all rows of A^(n) (CTA q: rows [q*rows_per, ...)).
@@ -736,7 +808,9 @@ __host__ __device__ inline size_t ut_smem_bytes(int R, int64_t rows_per, size_t 
   take(esz * rows_per * (R + 1));        // Aold
   take(esz * rows_per * (R + 1));        // Anew
   take(sizeof(double) * (R * (R + 1) / 2 + 1));  // partial Gram / partial ||A||^2 (read by peers)
-  take(sizeof(double) * R * R);          // Gm (Gram -> Cholesky factor)
+  take(sizeof(double) * R * (R + 1));    // Gm (Gram -> inverse), row stride R+1
+  take(sizeof(double) * 2 * R);          // sweep row buffer
+  take(sizeof(int) * R);                 // swept flags
   take(sizeof(double) * rows_per);       // per-row p
   take(sizeof(unsigned long long) * rows_per);   // per-row q -> local inclusive scan
   take(sizeof(unsigned long long) * 2);  // CTA total (read by peers), pad
@@ -771,7 +845,9 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   T* Aold = reinterpret_cast<T*>(carve(sizeof(T) * p.rows_per * RS));
   T* Anew = reinterpret_cast<T*>(carve(sizeof(T) * p.rows_per * RS));
   double* gpart = reinterpret_cast<double*>(carve(sizeof(double) * (R * (R + 1) / 2 + 1)));
-  double* Gm = reinterpret_cast<double*>(carve(sizeof(double) * R * R));
+  double* Gm = reinterpret_cast<double*>(carve(sizeof(double) * R * (R + 1)));
+  double* rowbuf = reinterpret_cast<double*>(carve(sizeof(double) * 2 * R));
+  int* swept = reinterpret_cast<int*>(carve(sizeof(int) * R));
   double* prow = reinterpret_cast<double*>(carve(sizeof(double) * p.rows_per));
   unsigned long long* qrow = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * p.rows_per));
   unsigned long long* qtot = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * 2));
@@ -896,8 +972,8 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
       int r1 = 0, rem = pair;
       while (rem >= R - r1) { rem -= R - r1; ++r1; }
       const int r2 = r1 + rem;
-      Gm[r1 * R + r2] = sum;
-      Gm[r2 * R + r1] = sum;
+      Gm[r1 * (R + 1) + r2] = sum;
+      Gm[r2 * (R + 1) + r1] = sum;
     }
     __syncthreads();
     // Inverse of the Gram on its numerically full-rank pivot set S by the symmetric sweep
@@ -910,78 +986,21 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
       double d0 = 0.0;
       bool fin = true;
       for (int j = 0; j < R; ++j) {
-        d0 = fmax(d0, Gm[j * R + j]);
-        fin = fin && (Gm[j * R + j] == Gm[j * R + j]) && Gm[j * R + j] < 1.7e308;
+        const double dj = Gm[j * (R + 1) + j];
+        d0 = fmax(d0, dj);
+        fin = fin && (dj == dj) && dj < 1.7e308;
       }
       if (!fin) s_bad |= 8;
       s_tol = (double)(p.In > R ? p.In : R) * 2.220446049250313e-16 * d0;
     }
-    if (tid < R) piv[tid] = 0;  // 1 = swept
     __syncthreads();
-    const double tol = s_tol;
-    UT_MARK(3);
-    // this thread's fixed set of matrix entries (R^2 <= 4096 -> at most 16 per thread)
-    constexpr int EPT = (kMaxRank * kMaxRank + kUTThreads - 1) / kUTThreads;
-    int ei[EPT], ej[EPT];
-#pragma unroll
-    for (int t = 0; t < EPT; ++t) {
-      const int e = tid + t * kUTThreads;
-      ei[t] = e < R * R ? e / R : -1;
-      ej[t] = e < R * R ? e % R : -1;
-    }
-    int k = 0;
-    for (; k < R; ++k) {
-      // pivot: largest unswept diagonal, lowest index on ties (every warp computes it -> no barrier)
-      double best = -1.0;
-      int bj = -1;
-      for (int j = (tid & 31); j < R; j += 32) {
-        const double d = piv[j] ? -1.0 : Gm[j * R + j];
-        if (d > best) { best = d; bj = j; }
+    {
+      const int rk = cta_sweep_inverse<(kMaxRank * kMaxRank + kUTThreads - 1) / kUTThreads>(Gm, R, s_tol, rowbuf,
+                                                                                             swept);
+      if (tid == 0) {
+        s_rank = rk;
+        if (rk == 0) s_bad |= 2;
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-        const bool take = (ob > best) | ((ob == best) & (oj >= 0) & ((bj < 0) | (oj < bj)));
-        best = take ? ob : best;
-        bj = take ? oj : bj;
-      }
-      if (k == 1) UT_MARK(8);
-      if (!(best > tol)) break;
-      const int pk = bj;
-      const double dinv = __drcp_rn(Gm[pk * R + pk]);
-      if (k == 1) UT_MARK(9);
-      // rank-1 update of the entries off row/column pk (reads only row/col pk: no hazard)
-#pragma unroll
-      for (int t = 0; t < EPT; ++t) {
-        const int i = ei[t], j = ej[t];
-        if (i >= 0 && i != pk && j != pk) Gm[i * R + j] -= Gm[i * R + pk] * (Gm[pk * R + j] * dinv);
-      }
-      if (k == 1) UT_MARK(10);
-      __syncthreads();
-      if (k == 1) UT_MARK(11);
-      if (tid < R) {
-        if (tid != pk) {
-          Gm[tid * R + pk] *= dinv;
-          Gm[pk * R + tid] *= dinv;
-        } else {
-          Gm[pk * R + pk] = -dinv;
-          piv[pk] = 1;
-        }
-      }
-      __syncthreads();
-      if (k == 1) UT_MARK(12);
-      if (k == 2) UT_MARK(13);
-    }
-    if (tid == 0) {
-      s_rank = k;
-      if (k == 0) s_bad |= 2;
-    }
-    // W = -M on S x S, zero elsewhere (in place)
-#pragma unroll
-    for (int t = 0; t < EPT; ++t) {
-      const int i = ei[t], j = ej[t];
-      if (i >= 0) Gm[i * R + j] = (piv[i] && piv[j]) ? -Gm[i * R + j] : 0.0;
     }
     __syncthreads();
     const int rank = s_rank;
@@ -994,7 +1013,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
         double part = 0.0;
         for (int i = lane; i < R; i += 32) {
           double t = 0.0;
-          for (int j = 0; j < R; ++j) t += Gm[i * R + j] * (double)a[j];
+          for (int j = 0; j < R; ++j) t += Gm[i * (R + 1) + j] * (double)a[j];
           part += (double)a[i] * t;
         }
 #pragma unroll
