@@ -541,7 +541,9 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
           if (lane == 0) s_red[0] = (double)(In > R ? In : R) * 2.220446049250313e-16 * d0;
         }
         __syncthreads();
-        const int rank = cta_sweep_inverse<(32 * 32 + kFThreads - 1) / kFThreads>(Gm, R, s_red[0], rowbuf, swept);
+        constexpr int EPT = (32 * 32 + kFThreads - 1) / kFThreads;
+        const int rank = (In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, s_red[0], rowbuf, swept, rowbuf + R)
+                                      : cta_sweep_inverse<EPT>(Gm, R, s_red[0], rowbuf, swept);
         F_MARK(6);
         if (tid == 0 && rank == 0) s_bad |= 2;
         // scores l = a^T W a: thread per (row, i) forms a_i * (W a)_i; rows summed in order

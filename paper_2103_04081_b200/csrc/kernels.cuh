@@ -758,6 +758,72 @@ __device__ int cta_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /
 }
 
 
+// Pivoted variant (largest remaining Schur diagonal first, as a pivoted Cholesky would) for
+// factors that can be rank deficient (I_n < 2R): dependent columns are left for last, where their
+// residual Schur diagonals sit at rounding level and fall under tol.  Two barriers per pivot;
+// the argmax is one warp reduction on a 32-bit key (26 high bits of the positive double + index).
+template <int kSweepEPT>
+__device__ int cta_sweep_inverse_pivoted(double* Gm, int R, double tol, double* rowbuf /* R */,
+                                         int* swept /* R */, double* diag /* R */) {
+  const int tid = threadIdx.x, nth = blockDim.x, RS = R + 1, lane = tid & 31;
+  double v[kSweepEPT];
+  int ei[kSweepEPT], ej[kSweepEPT];
+#pragma unroll
+  for (int t = 0; t < kSweepEPT; ++t) {
+    const int e = tid + t * nth;
+    ei[t] = (e < R * R) ? e / R : -1;
+    ej[t] = (e < R * R) ? e % R : 0;
+    v[t] = (e < R * R) ? Gm[ei[t] * RS + ej[t]] : 0.0;
+  }
+  for (int j = tid; j < R; j += nth) {
+    diag[j] = Gm[j * RS + j];
+    swept[j] = 0;
+  }
+  __syncthreads();
+  int rank = 0;
+  for (int step = 0; step < R; ++step) {
+    unsigned key = 0u;
+    for (int j = lane; j < R; j += 32) {
+      const double d = diag[j];
+      if (!swept[j] && d > 0.0) {
+        const unsigned kj = ((unsigned)__double2hiint(d) & 0xFFFFFFC0u) | (unsigned)(63 - j);
+        key = kj > key ? kj : key;
+      }
+    }
+    key = __reduce_max_sync(0xffffffffu, key);
+    if (key == 0u) break;
+    const int k = 63 - (int)(key & 63u);
+    const double d = diag[k];
+    if (!(d > tol)) break;
+#pragma unroll
+    for (int t = 0; t < kSweepEPT; ++t)
+      if (ei[t] == k) rowbuf[ej[t]] = v[t];
+    __syncthreads();
+    ++rank;
+    const double dinv = __drcp_rn(d);
+#pragma unroll
+    for (int t = 0; t < kSweepEPT; ++t) {
+      const int i = ei[t], j = ej[t];
+      const double rki = rowbuf[i < 0 ? 0 : i], rkj = rowbuf[j];
+      double nv = v[t] - rki * (rkj * dinv);
+      nv = (j == k) ? rki * dinv : nv;
+      nv = (i == k) ? rkj * dinv : nv;
+      nv = (i == k && j == k) ? -dinv : nv;
+      v[t] = (i >= 0) ? nv : v[t];
+      if (i >= 0 && i == j && i != k) diag[i] = v[t];
+    }
+    if (tid == 0) swept[k] = 1;
+    __syncthreads();
+  }
+#pragma unroll
+  for (int t = 0; t < kSweepEPT; ++t) {
+    const int i = ei[t], j = ej[t];
+    if (i >= 0) Gm[i * RS + j] = (swept[i] && swept[j]) ? -v[t] : 0.0;
+  }
+  __syncthreads();
+  return rank;
+}
+
 // ==========================================================================================
 // (a6, a7, a8, a1, a9) fused update + table refresh: ONE thread-block cluster of CU <= 16 CTAs
 // owns all rows of A^(n) (CTA q: rows [q*rows_per, ...)).
@@ -995,8 +1061,9 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     }
     __syncthreads();
     {
-      const int rk = cta_sweep_inverse<(kMaxRank * kMaxRank + kUTThreads - 1) / kUTThreads>(Gm, R, s_tol, rowbuf,
-                                                                                             swept);
+      constexpr int EPT = (kMaxRank * kMaxRank + kUTThreads - 1) / kUTThreads;
+      const int rk = (p.In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, s_tol, rowbuf, swept, rowbuf + R)
+                                    : cta_sweep_inverse<EPT>(Gm, R, s_tol, rowbuf, swept);
       if (tid == 0) {
         s_rank = rk;
         if (rk == 0) s_bad |= 2;
