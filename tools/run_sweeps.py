@@ -18,11 +18,15 @@ ap.add_argument("--sweeps", type=int, default=5)
 ap.add_argument("--direct", action="store_true", help="no CUDA graph")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.workload]
-X = synth.tensor(cfg)
-A0 = synth.init_factors(cfg, X)
 dev = torch.device("cuda:0")
-Xd = torch.from_numpy(X).to(dev)
-Ad = [torch.from_numpy(x).to(dev) for x in A0]
+if cfg.numel <= 200_000_000:
+    X = synth.tensor(cfg)
+    A0 = synth.init_factors(cfg, X)
+    Xd = torch.from_numpy(X).to(dev)
+    Ad = [torch.from_numpy(x).to(dev) for x in A0]
+else:
+    Xd, _, xn = synth.tensor_torch(cfg, device=dev)
+    Ad = synth.init_factors_torch(cfg, xn, device=dev)
 h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=a.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta, seed=0,
           graphs=not a.direct)
 h.sweep(2)
