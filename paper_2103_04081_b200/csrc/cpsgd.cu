@@ -20,6 +20,7 @@
 
 #include "../../include/cpsgd.h"
 #include "fused.cuh"
+#include "gupdate.cuh"
 #include "kernels.cuh"
 
 using namespace cps;
@@ -75,7 +76,7 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
-enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kNumKernelIds };
+enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kKGatherUpdate, kKZwGamma, kNumKernelIds };
 
 struct ProfRec {
   int id;
@@ -141,6 +142,9 @@ struct cp_sgd_s {
   int64_t* fbase = nullptr;      // prefetched fiber offsets [Bmax]
   long long* dbg = nullptr;      // CPSGD_DEBUG_TIMERS: phase timestamps of k_update_table
   int* last_mode_dev = nullptr;  // written by the fused sweep kernel
+  void* zwp = nullptr;           // wide path: weighted padded SKR rows [Bmax][ceil8(R)] of the prefetched batch
+  void* gam_next = nullptr;      // wide path: Gamma of the prefetched batch [R][R]
+  int gu_ck[kMaxOrder] = {};     // wide path: cluster size (batch chunks) of k_gather_update, 0 = not eligible
   int fused_cu = 0, fused_bpc = 0, fused_rpc = 0;  // fused kernel geometry (0: not eligible)
   size_t fused_smem = 0;
   int pref_mode = -1;            // mode whose batch (at the current r) sits in idx/w/zrow/fbase
@@ -248,6 +252,7 @@ cp_status launch_table(cp_sgd_s* h, int k) {
 cp_status launch_ut(cp_sgd_s* h, int n, int do_update, int do_table, int64_t row0, int64_t In, double alpha,
                     const double* alpha_dev, bool use_sum, int next_mode);
 bool ut_fits(const cp_sgd_s* h, int64_t In);
+bool wide_mode(const cp_sgd_s* h, int n);
 
 cp_status launch_table_any(cp_sgd_s* h, int k) {
   if (h->sampler == CP_UNIFORM) return CP_OK;
@@ -420,7 +425,13 @@ cp_status launch_ut_t(cp_sgd_s* h, int n, int do_update, int do_table, int64_t r
     fill_sample_params(h, p.sp, next_mode, h->iter_dev, 0, h->idx, h->w, h->beff, true);
     const size_t cb = sample_cdf_bytes(h, next_mode);
     p.sp.stage_smem = (cb > 0 && smem + cb <= (size_t)h->sample_smem) ? 1 : 0;
-    if (p.sp.stage_smem) smem += cb;
+    size_t extra = p.sp.stage_smem ? cb : 0;
+    if (wide_mode(h, next_mode)) {  // zw rows + Gamma of the next batch (wide path)
+      p.sp.zwp = h->zwp;
+      p.sp.gam_next = h->gam_next;
+      extra = std::max(extra, zg_scratch_bytes(h->R, sizeof(T), kUTThreads));
+    }
+    smem += extra;
   }
   // one CTA per SM: the cluster's CTAs each run the serial table stages; co-residing CTAs would
   // share one SM's issue slots (claim more than half of the SM's shared memory)
@@ -508,6 +519,127 @@ cp_status launch_reduce(cp_sgd_s* h, int n) {
 }
 
 bool sharded(const cp_sgd_s* h) { return h->world_size > 1; }
+
+// ---- wide single-GPU path: k_gather_update (gather + split-K + update) and the zw / Gamma epilogue ----
+bool wide_mode(const cp_sgd_s* h, int n) { return n >= 0 && h->gu_ck[n] > 0; }
+
+template <typename T, int CPT>
+cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
+  ProfScope ps(h, kKGatherUpdate);
+  GUParams<T> p;
+  memset(&p, 0, sizeof p);
+  p.R = h->R;
+  p.In = h->dims[n];
+  if (h->Xmm[n]) {
+    p.X = (const T*)h->Xmm[n];
+    p.es = 1;
+    p.vec = 1;
+  } else {
+    p.X = (const T*)h->X;
+    p.es = h->lstride[n];
+    p.vec = (n == 0 && (h->dims[0] * (int64_t)sizeof(T)) % 16 == 0) ? 1 : 0;
+  }
+  p.fbase = h->fbase;
+  p.zwp = (const T*)h->zwp;
+  p.bmax = h->bmax[n];
+  const int CK = h->gu_ck[n];
+  p.KB = ceil_div(h->bmax[n], CK);
+  p.Gam = (const T*)h->gam_next;
+  p.A = (T*)h->factors[n];
+  p.S = (T*)h->S[n];
+  p.Gout = (T*)h->Gout;
+  p.Gam_out = (T*)h->Gam_out;
+  p.rule = h->rule;
+  p.alpha = alpha;
+  p.alpha_dev = alpha_dev;
+  p.eta = h->eta;
+  p.b = h->bpar;
+  p.eps = h->eps;
+  p.iter = h->iter_dev;
+  const size_t smem = gu_smem_bytes<T, CPT>(p.KB);
+  static bool attr_set = false;
+  if (!attr_set) {
+    allow_max_dyn_smem(k_gather_update<T, CPT>);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)ceil_div(h->dims[n], kGUTI), (unsigned)CK, 1);
+  lc.blockDim = dim3(kGUThreads, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = h->ls;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = CK;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_gather_update<T, CPT>, p);
+  h->launches++;
+  if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_gather_update launch: %s", cudaGetErrorString(e));
+  return check_launch(h, "k_gather_update");
+}
+
+template <typename T>
+cp_status launch_gu(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
+  switch ((h->R + 7) / 8) {
+    case 1: return launch_gu_t<T, 1>(h, n, alpha, alpha_dev);
+    case 2: return launch_gu_t<T, 2>(h, n, alpha, alpha_dev);
+    case 3: return launch_gu_t<T, 3>(h, n, alpha, alpha_dev);
+    case 4: return launch_gu_t<T, 4>(h, n, alpha, alpha_dev);
+    case 5: return launch_gu_t<T, 5>(h, n, alpha, alpha_dev);
+    case 6: return launch_gu_t<T, 6>(h, n, alpha, alpha_dev);
+    case 7: return launch_gu_t<T, 7>(h, n, alpha, alpha_dev);
+    default: return launch_gu_t<T, 8>(h, n, alpha, alpha_dev);
+  }
+}
+
+int zg_cluster(const cp_sgd_s* h, int n) {
+  int CU = 1;
+  while (CU < 16 && CU * 256 < h->bmax[n]) CU *= 2;
+  return CU;
+}
+
+// zw rows + Gamma of the batch in idx / w / zrow / fbase (after k_sample)
+template <typename T>
+cp_status launch_zw_gamma_t(cp_sgd_s* h, int n) {
+  ProfScope ps(h, kKZwGamma);
+  SampleParams p;
+  fill_sample_params(h, p, n, h->iter_dev, 0, h->idx, h->w, h->beff, true);
+  p.zwp = h->zwp;
+  p.gam_next = h->gam_next;
+  const int CU = zg_cluster(h, n);
+  const size_t smem = zg_scratch_bytes(h->R, sizeof(T), 256);
+  static bool attr_set = false;
+  if (!attr_set) {
+    allow_max_dyn_smem(k_zw_gamma<T>);
+    cudaFuncSetAttribute(k_zw_gamma<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(CU, 1, 1);
+  lc.blockDim = dim3(256, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = h->ls;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CU;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_zw_gamma<T>, p);
+  h->launches++;
+  if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_zw_gamma launch: %s", cudaGetErrorString(e));
+  return check_launch(h, "k_zw_gamma");
+}
+
+// the batch of mode n at the current r into the prefetch buffers (k_sample [+ k_zw_gamma])
+cp_status launch_prefetch(cp_sgd_s* h, int n) {
+  cp_status st = launch_sample(h, n, h->iter_dev, h->idx, h->w, h->beff, true);
+  if (st || !wide_mode(h, n)) return st;
+  return h->dtype == CP_F64 ? launch_zw_gamma_t<double>(h, n) : launch_zw_gamma_t<float>(h, n);
+}
 
 // ---- persistent single-cluster sweep kernel (fused.cuh) ----------------------------------------
 template <typename T, int ROWS>
@@ -630,12 +762,17 @@ void plan_fused(cp_sgd_s* h) {
 }
 
 // ---- one step, by phases ------------------------------------------------------------------------
-cp_status phase0(cp_sgd_s* h, int n) {
+cp_status phase0(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
   cp_status st = CP_OK;
   if (h->pref_mode != n) {  // no prefetched batch for this mode: sample it now
-    st = launch_sample(h, n, h->iter_dev, h->idx, h->w, h->beff, true);
+    st = launch_prefetch(h, n);
     if (st) return st;
     h->pref_mode = n;
+  }
+  if (wide_mode(h, n)) {  // gather + contraction + split-K + update in one launch
+    st = h->dtype == CP_F64 ? launch_gu<double>(h, n, alpha, alpha_dev) : launch_gu<float>(h, n, alpha, alpha_dev);
+    h->pref_mode = -1;
+    return st;
   }
   st = h->dtype == CP_F64 ? launch_gather<double>(h, n) : launch_gather<float>(h, n);
   if (st) return st;
@@ -646,6 +783,12 @@ cp_status phase0(cp_sgd_s* h, int n) {
 
 // update (+ table + next batch when the rows are all local)
 cp_status phase1(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, int next_mode) {
+  if (wide_mode(h, n)) {  // table of the updated A^(n) + the next batch (+ its zw rows and Gamma)
+    if (h->sampler == CP_UNIFORM && next_mode < 0) return CP_OK;
+    cp_status st = launch_ut(h, n, 0, 1, 0, h->dims[n], 0.0, nullptr, false, next_mode);
+    if (!st && next_mode >= 0) h->pref_mode = next_mode;
+    return st;
+  }
   const bool last_sharded = sharded(h) && n == h->N - 1;
   if (ut_fits(h, h->In_local[n])) {
     cp_status st;
@@ -662,6 +805,7 @@ cp_status phase1(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, int 
 
 // table refresh of mode n when it could not be fused into phase 1 (rows gathered first / legacy)
 cp_status phase2(cp_sgd_s* h, int n, int next_mode) {
+  if (wide_mode(h, n)) return CP_OK;
   const bool last_sharded = sharded(h) && n == h->N - 1;
   if (ut_fits(h, h->In_local[n])) {
     if (!last_sharded) return CP_OK;
@@ -711,7 +855,7 @@ namespace {
 
 cp_status do_step(cp_sgd_s* h, int n, int next_mode, double alpha, const double* alpha_dev,
                   const std::vector<int64_t>& rr) {
-  cp_status st = phase0(h, n);
+  cp_status st = phase0(h, n, alpha, alpha_dev);
   if (!st) st = exchange_after0(h, n);
   if (!st) st = phase1(h, n, alpha, alpha_dev, next_mode);
   if (!st) st = exchange_after1(h, n, rr);
@@ -943,6 +1087,29 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
     cudaGetLastError();
   }
   plan_fused(h);
+  // ---- wide single-GPU path (k_gather_update) eligibility and buffers ----
+  if (h->world_size == 1 && !(h->flags & CP_FLAG_NO_WIDE)) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    bool any = false;
+    for (int n = 0; n < h->N; ++n) {
+      const int64_t nt = ceil_div(h->dims[n], kGUTI);
+      const int CK = nt > 74 ? 2 : nt > 37 ? 4 : 8;
+      const int64_t KB = ceil_div(h->bmax[n], CK);
+      const size_t gs = h->esz == 8 ? gu_smem_bytes<double, 8>(KB) : gu_smem_bytes<float, 8>(KB);
+      const size_t us = ut_smem_bytes(h->R, ceil_div(h->dims[n], 16), h->esz) + zg_scratch_bytes(h->R, h->esz, kUTThreads);
+      if (ut_fits(h, h->dims[n]) && gs + 1024 <= (size_t)optin && us <= (size_t)h->sample_smem) {
+        h->gu_ck[n] = CK;
+        any = true;
+      }
+    }
+    if (any) {
+      ALLOC(h->zwp, h->esz * Bmax_all * zg_rp(h->R));
+      ALLOC(h->gam_next, h->esz * h->R * h->R);
+      cudaMemsetAsync(h->zwp, 0, h->esz * Bmax_all * zg_rp(h->R), h->stream);
+    }
+  }
   // ---- optional mode-major copies (n >= 1; mode 0 fibers are already contiguous) ----
   if (h->flags & CP_FLAG_MODE_MAJOR) {
     for (int n = 1; n < h->N; ++n) {
@@ -1031,6 +1198,8 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->dbg);
   cudaFree(h->zrow);
   cudaFree(h->fbase);
+  cudaFree(h->zwp);
+  cudaFree(h->gam_next);
   cudaFree(h->iter_dev);
   cudaFree(h->iter_tmp);
   cudaFree(h->status_dev);
@@ -1130,7 +1299,7 @@ cp_status cp_sgd_step_phase(cp_sgd_t h, int32_t mode, int32_t phase, double alph
   if (st) return st;
   const double a = (alpha < 0.0) ? h->alpha : alpha;
   if (phase == 0) {
-    st = phase0(h, mode);
+    st = phase0(h, mode, a, nullptr);
     if (!st && sharded(h) && !(h->flags & CP_FLAG_EXTERNAL_COMM)) st = exchange_after0(h, mode);
     return st;
   }
@@ -1245,7 +1414,7 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
   }
   for (int s = 0; s < nsweeps; ++s) {
     if (h->pref_mode != 0) {
-      cp_status st = launch_sample(h, 0, h->iter_dev, h->idx, h->w, h->beff, true);
+      cp_status st = launch_prefetch(h, 0);
       if (st) return st;
     }
     CUDA_TRY(h, cudaGraphLaunch(h->sweep_exec, h->stream));

@@ -84,7 +84,7 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
   L.gm = take(sizeof(double) * R * (R + 1));
   L.prow = take(sizeof(double) * RPC);
   L.sc = take(sizeof(double) * RPC * R);
-  L.rowbuf = take(sizeof(double) * 2 * R);
+  L.rowbuf = take(sizeof(double) * 2 * kMaxRank);
   L.swept = take(sizeof(int) * R);
   L.qtot = take(sizeof(unsigned long long) * 2);
   L.cdfs = take(sizeof(uint64_t) * cdf_elems);
@@ -93,69 +93,6 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
 }
 
 
-
-// single-warp symmetric sweep for R <= 32 (same algorithm and reading R4(b) as cta_sweep_inverse):
-// lane owns entries e = lane + 32 t of the R x R matrix in registers; the pivot row is published
-// through a double-buffered shared row, so each pivot costs one __syncwarp (no CTA barrier).
-__device__ int warp_sweep_inverse32(double* Gm, int R, double tol, double* rowbuf /* 2*R */, int* swept /* R */) {
-  const int lane = threadIdx.x & 31, RS = R + 1;
-  constexpr int EPT = 32;  // R^2 <= 1024
-  double v[EPT];
-  int ij[EPT];
-#pragma unroll
-  for (int t = 0; t < EPT; ++t) {
-    const int e = lane + 32 * t;
-    const int i = e / R, j = e % R;
-    ij[t] = (e < R * R) ? (i << 8) | j : -1;
-    v[t] = (e < R * R) ? Gm[i * RS + j] : 0.0;
-  }
-  for (int j = lane; j < R; j += 32) {
-    rowbuf[j] = Gm[j];
-    swept[j] = 0;
-  }
-  __syncwarp();
-  int rank = 0;
-  for (int k = 0; k < R; ++k) {
-    const double* rk = rowbuf + (k & 1) * R;
-    double* rn = rowbuf + ((k + 1) & 1) * R;
-    const double d = rk[k];
-    if (d > tol) {
-      ++rank;
-      const double dinv = __drcp_rn(d);
-#pragma unroll
-      for (int t = 0; t < EPT; ++t) {
-        if (t * 32 >= R * R) break;  // warp-uniform
-        const int c = ij[t];
-        const int i = c >> 8, j = c & 255;
-        const double rki = rk[i & 31], rkj = rk[j & 31];
-        double nv = v[t] - rki * (rkj * dinv);
-        nv = (j == k) ? rki * dinv : nv;
-        nv = (i == k) ? rkj * dinv : nv;
-        nv = (i == k && j == k) ? -dinv : nv;
-        v[t] = (c >= 0) ? nv : v[t];
-      }
-      if (lane == 0) swept[k] = 1;
-    }
-#pragma unroll
-    for (int t = 0; t < EPT; ++t) {
-      if (t * 32 >= R * R) break;
-      const int c = ij[t];
-      if (c >= 0 && (c >> 8) == k + 1) rn[c & 255] = v[t];
-    }
-    __syncwarp();
-  }
-#pragma unroll
-  for (int t = 0; t < EPT; ++t) {
-    if (t * 32 >= R * R) break;
-    const int c = ij[t];
-    if (c >= 0) {
-      const int i = c >> 8, j = c & 255;
-      Gm[i * RS + j] = (swept[i] && swept[j]) ? -v[t] : 0.0;
-    }
-  }
-  __syncwarp();
-  return rank;
-}
 
 template <typename T>
 struct Vec;
@@ -543,7 +480,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
         __syncthreads();
         constexpr int EPT = (32 * 32 + kFThreads - 1) / kFThreads;
         const int rank = (In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, s_red[0], rowbuf, swept, rowbuf + R)
-                                      : cta_sweep_inverse<EPT>(Gm, R, s_red[0], rowbuf, swept);
+                                      : blk_sweep_inverse(Gm, R, s_red[0], rowbuf, swept);
         F_MARK(6);
         if (tid == 0 && rank == 0) s_bad |= 2;
         // scores l = a^T W a: thread per (row, i) forms a_i * (W a)_i; rows summed in order

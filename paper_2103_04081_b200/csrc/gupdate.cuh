@@ -1,0 +1,254 @@
+// gupdate.cuh -- k_gather_update: the wide single-GPU step kernel for problems too large for one
+// cluster (C4/C5 of BASELINE.json).  ONE launch does, for every row block of A^(n):
+//
+//   (a5) TensorSamp (Alg. 5): the I-tile segment of every sampled fiber,
+//        staged HBM -> shared memory with cp.async (16-byte vectors of the mode-major copy, or
+//        scalars of the native layout), NS-stage pipeline;
+//   (a6) M_tile = X_F diag(w) Z_F restricted to the tile (eq:gradient1/2):
+//        register-blocked FFMA (4 rows x CPT columns per thread) against the weighted SKR rows
+//        zw_b = w_b z_b prepared by the sampler (Alg. 1);
+//   (a6) deterministic split-K: the CK CTAs of a cluster hold the CK batch chunks of one I-tile;
+//        partial tiles are summed through DSMEM in rank order, CTA q finishing rows
+//        [q TI/CK, (q+1) TI/CK) of the tile;
+//   (a6-a8) G = A Gamma - M for those rows (Gamma = Z_F^T diag(w) Z_F from the sampler), then the
+//        fixed (eq:proposed, :459-464) or adaptive (eq:etaada/eq:Aada, :531-537, R12) update.
+//
+// grid = (ceil(I_n / TI), CK), cluster (1, CK, 1); 256 threads: warp w = column group
+// [w CPT, (w+1) CPT), lane l = rows [4l, 4l+4) of the tile.  RP = 8 CPT >= R (zero padded).
+#pragma once
+#include <cooperative_groups.h>
+
+#include "kernels.cuh"
+
+namespace cps {
+
+constexpr int kGUThreads = 256;
+constexpr int kGUTI = 128;     // rows per I-tile
+constexpr int kGUKS = 32;      // fibers per pipeline stage
+constexpr int kGUStages = 3;
+
+template <typename T>
+struct GUParams {
+  int R;
+  int64_t In;             // rows of A^(n)
+  const T* X;             // gather base: mode-major copy of mode n (es = 1) or the native tensor
+  int64_t es;             // element stride along a fiber
+  int vec;                // 1: es == 1 and every fiber starts 16-byte aligned (16-byte cp.async)
+  const int64_t* fbase;   // [Bmax] element offset of fiber b (-1: padding row)
+  const T* zwp;           // [Bmax][RP] weighted SKR rows, zero padded (sampler)
+  int64_t bmax;           // rows of the batch buffers for this mode
+  int64_t KB;             // fibers per chunk (= per CTA)
+  const T* Gam;           // [R][R] Gamma of this batch (sampler)
+  T* A;                   // A^(n), row-major I_n x R, updated in place
+  T* S;                   // adaptive accumulator or NULL
+  T* Gout;                // G (debug hook)
+  T* Gam_out;             // Gamma (debug hook)
+  int rule;
+  double alpha;
+  const double* alpha_dev;
+  double eta, b, eps;
+  uint64_t* iter;         // r <- r + 1 (Alg. 6/7)
+};
+
+// shared memory: max(pipeline, epilogue) + Gamma + fiber offsets of the chunk
+template <typename T, int CPT>
+__host__ __device__ constexpr size_t gu_pipe_bytes() {
+  return (size_t)kGUStages * kGUKS * (kGUTI + 8 * CPT) * sizeof(T);
+}
+// epilogue: partial tile [TI][RP+1] (read by the peers) + finished rows M [TI/CK][R] + old rows of
+// A [TI/CK][R+1]; the host uses CK >= 2
+template <typename T, int CPT>
+__host__ __device__ constexpr size_t gu_epi_bytes() {
+  return ((size_t)kGUTI * (8 * CPT + 1) + (size_t)(kGUTI / 2) * (16 * CPT + 1)) * sizeof(T);
+}
+template <typename T, int CPT>
+__host__ __device__ inline size_t gu_smem_bytes(int64_t KB) {
+  constexpr size_t a = gu_pipe_bytes<T, CPT>() > gu_epi_bytes<T, CPT>() ? gu_pipe_bytes<T, CPT>()
+                                                                          : gu_epi_bytes<T, CPT>();
+  return a + (size_t)kMaxRank * kMaxRank * sizeof(T) + (size_t)KB * sizeof(int64_t) + 64;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_small(void* dst, const void* src, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src), "n"(BYTES), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename T, int CPT>
+__global__ void __launch_bounds__(kGUThreads, 1) k_gather_update(GUParams<T> p) {
+  namespace cg = cooperative_groups;
+  constexpr int RP = 8 * CPT;
+  constexpr int TI = kGUTI, KS = kGUKS, NS = kGUStages;
+  constexpr int VE = 16 / (int)sizeof(T);      // elements per 16-byte vector
+  constexpr int XV = TI / VE;                  // vectors per fiber segment
+  constexpr int ZV = RP / VE;                  // vectors per zw row (RP*sizeof(T) is a multiple of 16)
+  extern __shared__ __align__(16) unsigned char gu_sm[];
+  T* pipe = reinterpret_cast<T*>(gu_sm);
+  constexpr size_t kA = gu_pipe_bytes<T, CPT>() > gu_epi_bytes<T, CPT>() ? gu_pipe_bytes<T, CPT>()
+                                                                           : gu_epi_bytes<T, CPT>();
+  T* sGam = reinterpret_cast<T*>(gu_sm + kA);
+  int64_t* sfb = reinterpret_cast<int64_t*>(gu_sm + kA + (size_t)kMaxRank * kMaxRank * sizeof(T));
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CK = (int)cluster.dim_blocks().y;
+  const int q = (int)cluster.block_index().y;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int R = p.R;
+  const int64_t i0 = (int64_t)blockIdx.x * TI;
+  const int64_t c0 = (int64_t)blockIdx.y * p.KB;
+  const int64_t c1 = min(c0 + p.KB, p.bmax);
+  const int nfib = (int)cmax64(0, c1 - c0);
+  const int nst = (nfib + KS - 1) / KS;
+
+  for (int b = tid; b < nfib; b += kGUThreads) sfb[b] = p.fbase[c0 + b];
+  for (int e = tid; e < R * R; e += kGUThreads) sGam[e] = p.Gam[e];
+  __syncthreads();
+
+  auto xs_of = [&](int s) { return pipe + (size_t)s * KS * (TI + RP); };
+  // issue the cp.async group of pipeline stage `st` (fibers [st*KS, st*KS + KS) of the chunk)
+  auto load_stage = [&](int st) {
+    T* xs = xs_of(st % NS);
+    T* zs = xs + KS * TI;
+    const int f0 = st * KS;
+    if (p.vec) {
+      for (int e = tid; e < KS * XV; e += kGUThreads) {
+        const int kk = e / XV, v = e % XV;
+        const int lb = f0 + kk;
+        const int64_t fb = lb < nfib ? sfb[lb] : -1;
+        const int64_t r0 = i0 + (int64_t)v * VE;
+        int bytes = 0;
+        const T* src = p.X;
+        if (fb >= 0 && r0 < p.In) {
+          bytes = (int)cmin64(p.In - r0, VE) * (int)sizeof(T);
+          src = p.X + fb + r0;
+        }
+        cp_async16(xs + kk * TI + v * VE, src, bytes);
+      }
+    } else {
+      for (int e = tid; e < KS * TI; e += kGUThreads) {
+        const int kk = e / TI, il = e % TI;
+        const int lb = f0 + kk;
+        const int64_t fb = lb < nfib ? sfb[lb] : -1;
+        const int64_t r = i0 + il;
+        const bool ok = fb >= 0 && r < p.In;
+        cp_async_small<sizeof(T)>(xs + kk * TI + il, ok ? p.X + fb + r * p.es : p.X, ok ? (int)sizeof(T) : 0);
+      }
+    }
+    for (int e = tid; e < KS * ZV; e += kGUThreads) {
+      const int kk = e / ZV, v = e % ZV;
+      const int64_t b = c0 + f0 + kk;
+      const bool ok = b < c1;
+      cp_async16(zs + kk * RP + v * VE, ok ? p.zwp + b * RP + v * VE : p.zwp, ok ? 16 : 0);
+    }
+  };
+
+  T acc[4][CPT];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) acc[a][c] = T(0);
+
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) {
+    if (s < nst) load_stage(s);
+    cp_async_commit();
+  }
+  for (int st = 0; st < nst; ++st) {
+    cp_async_wait<NS - 2>();
+    __syncthreads();  // stage st landed for every thread; stage st-1's buffer is free
+    if (st + NS - 1 < nst) load_stage(st + NS - 1);
+    cp_async_commit();
+    const T* xs = xs_of(st % NS);
+    const T* zs = xs + KS * TI + wid * CPT;
+    const int kmax = min(KS, nfib - st * KS);
+#pragma unroll 4
+    for (int kk = 0; kk < kmax; ++kk) {
+      T xv[4];
+      if constexpr (sizeof(T) == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(xs + kk * TI + 4 * lane);
+        xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
+      } else {
+        const double2 v0 = *reinterpret_cast<const double2*>(xs + kk * TI + 4 * lane);
+        const double2 v1 = *reinterpret_cast<const double2*>(xs + kk * TI + 4 * lane + 2);
+        xv[0] = v0.x; xv[1] = v0.y; xv[2] = v1.x; xv[3] = v1.y;
+      }
+      T zv[CPT];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) zv[c] = zs[kk * RP + c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[a][c] = fma(xv[a], zv[c], acc[a][c]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // ---- split-K over the cluster: partial tile -> shared [TI][RP+1]; rank-ordered DSMEM sum ----
+  constexpr int MS = RP + 1;
+  T* Mt = pipe;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) Mt[(4 * lane + a) * MS + wid * CPT + c] = acc[a][c];
+  cluster.sync();
+  const int rows_q = TI / CK;
+  const int rl0 = q * rows_q;
+  // finished rows go after Mt (Mt is read by the peers until the final cluster barrier)
+  T* Mf = Mt + TI * MS;              // [rows_q][R]
+  T* Af = Mf + rows_q * R;           // [rows_q][R+1] old rows of A
+  const int nrow = (int)cmax64(0, cmin64(rows_q, p.In - (i0 + rl0)));
+  for (int e = tid; e < nrow * R; e += kGUThreads) {
+    const int rl = e / R, c = e % R;
+    T v[16];
+#pragma unroll
+    for (int qq = 0; qq < 16; ++qq)
+      v[qq] = qq < CK ? cluster.map_shared_rank(Mt, qq)[(rl0 + rl) * MS + c] : T(0);
+    T s = v[0];
+#pragma unroll
+    for (int qq = 1; qq < 16; ++qq) s += v[qq];
+    Mf[rl * R + c] = s;
+    Af[rl * (R + 1) + c] = p.A[(i0 + rl0 + rl) * R + c];
+  }
+  __syncthreads();
+  // ---- G = A Gamma - M; fixed / adaptive update of the finished rows ----
+  const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
+  for (int e = tid; e < nrow * R; e += kGUThreads) {
+    const int rl = e / R, r = e % R;
+    const int64_t gi = (i0 + rl0 + rl) * R + r;
+    T ag = T(0);
+    for (int c = 0; c < R; ++c) ag += Af[rl * (R + 1) + c] * sGam[c * R + r];
+    const T g = ag - Mf[rl * R + r];
+    p.Gout[gi] = g;
+    const T a = Af[rl * (R + 1) + r];
+    T an = a;
+    if (p.rule == 0) {
+      an = a - (T)alpha * g;
+    } else {
+      const T sv = p.S[gi] + g * g;
+      p.S[gi] = sv;
+      if (sv > T(0)) {
+        T step;
+        if (p.eps == 0.0) step = (T)p.eta / sqrt((T)p.b + sv);
+        else step = (T)p.eta / (T)pow((double)((T)p.b + sv), 0.5 + p.eps);
+        an = a - step * g;
+      }
+    }
+    p.A[gi] = an;
+  }
+  if (blockIdx.x == 0 && q == 0) {
+    for (int e = tid; e < R * R; e += kGUThreads) p.Gam_out[e] = sGam[e];
+    if (tid == 0) *p.iter += 1;  // r <- r + 1 (Alg. 6/7); nothing in this launch reads r
+  }
+  cluster.sync();  // peers may still read this CTA's partial tile
+}
+
+}  // namespace cps

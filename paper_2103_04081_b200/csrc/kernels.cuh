@@ -50,6 +50,9 @@ struct SampleParams {
   int64_t lo_last;
   int mode_major;
   int64_t pitch;
+  // wide path (k_gather_update): weighted padded SKR rows and Gamma of the batch (or NULL)
+  void* zwp;                       // T [B_max][ceil8(R)]
+  void* gam_next;                  // T [R][R]
 };
 
 template <typename T>
@@ -104,6 +107,9 @@ __device__ __forceinline__ int64_t upper_bound_u64(const uint64_t* __restrict__ 
   }
   return lo;  // #{i : cdf[i] <= r}
 }
+
+__host__ __device__ __forceinline__ int64_t cmin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t cmax64(int64_t a, int64_t b) { return a > b ? a : b; }
 
 template <typename T>
 __device__ __forceinline__ T ldg(const T* p) {
@@ -428,23 +434,154 @@ __device__ __forceinline__ void draw_rows(const SampleParams& p, const uint64_t*
 }
 
 // SKR rows (Alg. 1) of rows [b0, b1): z_b[r] = prod_{k != n, ascending} A^(k)(i_k, r)
+// Latency-friendly: each thread owns kSkrU elements and issues all their factor loads of one mode
+// before multiplying (the product order over modes stays ascending).  Plain loads: A^(n) may have
+// been written earlier in the same launch by another CTA.
+constexpr int kSkrU = 8;
 template <typename T>
 __device__ __forceinline__ void skr_rows(const SampleParams& p, int64_t b0, int64_t b1, int tid, int nthreads) {
   const int N = p.N, n = p.n, R = p.R;
   T* Z = reinterpret_cast<T*>(p.zrow);
   const int cnt = (int)(b1 - b0) * R;
-  for (int e = tid; e < cnt; e += nthreads) {
-    const int64_t b = b0 + e / R;
-    const int r = e % R;
-    const int32_t* ib = p.idx + b * (N - 1);
-    T z = T(1);
+  for (int base = 0; base < cnt; base += nthreads * kSkrU) {
+    int64_t row[kSkrU];
+    int col[kSkrU];
+    T z[kSkrU];
+#pragma unroll
+    for (int u = 0; u < kSkrU; ++u) {
+      const int e = base + u * nthreads + tid;
+      row[u] = e < cnt ? b0 + e / R : -1;
+      col[u] = e < cnt ? e % R : 0;
+      z[u] = T(1);
+    }
+    int32_t ix[kSkrU];
     int pos = 0;
     for (int k = 0; k < N; ++k) {
       if (k == n) continue;
-      z = z * __ldg(reinterpret_cast<const T*>(p.factors[k]) + (int64_t)ib[pos++] * R + r);
+      const T* F = reinterpret_cast<const T*>(p.factors[k]);
+#pragma unroll
+      for (int u = 0; u < kSkrU; ++u) ix[u] = row[u] >= 0 ? p.idx[row[u] * (N - 1) + pos] : 0;
+      T f[kSkrU];
+#pragma unroll
+      for (int u = 0; u < kSkrU; ++u) f[u] = row[u] >= 0 ? F[(int64_t)ix[u] * R + col[u]] : T(0);
+#pragma unroll
+      for (int u = 0; u < kSkrU; ++u) z[u] = z[u] * f[u];
+      ++pos;
     }
-    Z[b * R + r] = z;
+#pragma unroll
+    for (int u = 0; u < kSkrU; ++u)
+      if (row[u] >= 0) Z[row[u] * R + col[u]] = z[u];
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// (a6 prologue, moved to the sampler) for rows [b0, b1) of the batch just drawn:
+//   zw_b = w_b z_b (eq:gradient1/2 weights applied to the SKR row), zero padded to RP = ceil8(R)
+//   and zero for padding rows (fbase < 0) -> p.zwp [B_max][RP], the operand k_gather_update streams;
+//   Gamma_q = sum_b zw_b z_b^T over these rows (R x R, this CTA's share of Z_F^T diag(w) Z_F).
+// Threads own 4x4 blocks (bi <= bj) of Gamma; G fiber groups split the rows; groups are summed
+// in order.  Returns Gamma_q (R x R, row-major) in shared memory (inside `scratch`).
+// ------------------------------------------------------------------------------------------
+constexpr int kZGCh = 32;  // rows staged per chunk
+__host__ __device__ inline int zg_rp(int R) { return (R + 7) / 8 * 8; }
+__host__ __device__ inline int zg_groups(int R, int nthreads) {
+  const int nb = (R + 3) / 4, nblk = nb * (nb + 1) / 2;
+  const int g = nthreads / nblk;
+  return g < 1 ? 1 : (g > 4 ? 4 : g);
+}
+__host__ __device__ inline size_t zg_scratch_bytes(int R, size_t esz, int nthreads) {
+  return esz * (2 * (size_t)kZGCh * zg_rp(R) + (size_t)zg_groups(R, nthreads) * R * R) + 32;
+}
+
+template <typename T>
+__device__ T* zw_gamma_rows(const SampleParams& p, int64_t b0, int64_t b1, unsigned char* scratch, int tid, int nth) {
+  const int R = p.R, RP = zg_rp(R);
+  const int nb = (R + 3) / 4, nblk = nb * (nb + 1) / 2;
+  const int G = zg_groups(R, nth);
+  T* zs = reinterpret_cast<T*>(scratch);
+  T* ws = zs + kZGCh * RP;
+  T* red = ws + kZGCh * RP;  // [G][R][R]
+  const T* Z = reinterpret_cast<const T*>(p.zrow);
+  T* zwp = reinterpret_cast<T*>(p.zwp);
+  const int g = tid / nblk, blk = tid % nblk;
+  const bool act = g < G;
+  int bi = 0, bj = 0;
+  {  // upper-triangular block index -> (bi, bj), bi <= bj
+    int rem = blk;
+    while (rem >= nb - bi) { rem -= nb - bi; ++bi; }
+    bj = bi + rem;
+  }
+  T acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = T(0);
+  for (int64_t c0 = b0; c0 < b1; c0 += kZGCh) {
+    const int nch = (int)cmin64(kZGCh, b1 - c0);
+    for (int e = tid; e < kZGCh * RP; e += nth) {
+      const int kk = e / RP, r = e % RP;
+      const int64_t b = c0 + kk;
+      T z = T(0), zw = T(0);
+      if (kk < nch && r < R && p.fbase[b] >= 0) {
+        z = Z[b * R + r];
+        zw = (T)p.w[b] * z;
+      }
+      zs[e] = z;
+      ws[e] = zw;
+      if (kk < nch) zwp[b * RP + r] = zw;
+    }
+    __syncthreads();
+    if (act) {
+      for (int kk = g; kk < nch; kk += G) {
+        T x[4], y[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          x[a] = ws[kk * RP + 4 * bi + a];
+          y[a] = zs[kk * RP + 4 * bj + a];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = fma(x[a], y[c], acc[a][c]);
+      }
+    }
+    __syncthreads();
+  }
+  if (act) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int r1 = 4 * bi + a, r2 = 4 * bj + c;
+        if (r1 < R && r2 < R) {
+          red[(g * R + r1) * R + r2] = acc[a][c];
+          if (bi != bj) red[(g * R + r2) * R + r1] = acc[a][c];
+        }
+      }
+  }
+  __syncthreads();
+  for (int e = tid; e < R * R; e += nth) {
+    T s = red[e];
+    for (int gg = 1; gg < G; ++gg) s += red[gg * R * R + e];
+    red[e] = s;
+  }
+  __syncthreads();
+  return red;
+}
+
+// rank-ordered cluster sum of every CTA's Gamma_q (same shared offset in each CTA) -> out (global)
+template <typename T>
+__device__ void gamma_cluster_reduce(const cooperative_groups::cluster_group& cl, T* red, int R, T* out, int tid,
+                                     int nth) {
+  const int CU = (int)cl.num_blocks(), q = (int)cl.block_rank();
+  cl.sync();
+  const int E = R * R, per = (E + CU - 1) / CU;
+  for (int e = q * per + tid; e < min(E, (q + 1) * per); e += nth) {
+    T s = T(0);
+    for (int qq = 0; qq < CU; ++qq) s += cl.map_shared_rank(red, qq)[e];
+    out[e] = s;
+  }
+  cl.sync();  // peers done reading this CTA's shared memory
 }
 
 // (a2, a3[, a4]) standalone sampler (API calls and the first step of a call).  grid-stride rows.
@@ -466,6 +603,18 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
     __syncthreads();
     skr_rows<T>(p, b0, b1, threadIdx.x, blockDim.x);
   }
+}
+
+// wide path after k_sample: zw rows and Gamma of the whole batch, one cluster of CU CTAs
+template <typename T>
+__global__ void __launch_bounds__(256) k_zw_gamma(SampleParams p) {
+  extern __shared__ __align__(16) unsigned char zg_sm[];
+  cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+  const int CU = (int)cl.num_blocks(), q = (int)cl.block_rank();
+  const int64_t per = (p.bmax + CU - 1) / CU;
+  const int64_t b0 = min((int64_t)q * per, p.bmax), b1 = min(b0 + per, p.bmax);
+  T* red = zw_gamma_rows<T>(p, b0, b1, zg_sm, threadIdx.x, blockDim.x);
+  gamma_cluster_reduce<T>(cl, red, p.R, reinterpret_cast<T*>(p.gam_next), threadIdx.x, blockDim.x);
 }
 
 // ==========================================================================================
@@ -699,64 +848,251 @@ __device__ __forceinline__ T cluster_sum(const cooperative_groups::cluster_group
   return s;
 }
 
-// CTA-wide symmetric sweep (Gauss-Jordan on the SPD Gram in natural pivot order; a pivot whose
-// Schur diagonal is <= tol is skipped -- reading R4(b)).  Every thread keeps its fixed entries
-// of the R x R matrix in registers; the pivot row (= column, by symmetry) is published through a
-// double-buffered shared row, so each pivot costs one barrier.  On exit Gm (stride R+1) holds
-// W = (G_SS)^{-1} on the swept set S and 0 elsewhere; returns |S| (same value in every thread).
-template <int kSweepEPT>  // entries per thread: R^2 <= kSweepEPT * blockDim.x
-__device__ int cta_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /* 2*R */, int* swept /* R */) {
-  const int tid = threadIdx.x, nth = blockDim.x, RS = R + 1;
-  double v[kSweepEPT];
-  int ei[kSweepEPT], ej[kSweepEPT];
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Symmetric sweep (Gauss-Jordan on the SPD Gram in natural pivot order; a pivot whose Schur
+// diagonal is <= tol is skipped -- reading R4(b)), register-blocked: thread t < nb^2 (nb =
+// ceil(R/4)) keeps the 4x4 block (t / nb, t % nb) of the R x R matrix in registers.  Sweeping
+// pivot k maps M_ij -= M_ik (M_kj / d) (i, j != k), M_kj /= d, M_ik /= d, M_kk = -1/d (d = M_kk);
+// the pivot row (= column, by symmetry) is published through a double-buffered shared row, so a
+// pivot costs 8 shared loads, 4 DMUL, 16 DFMA and ONE named barrier over the ceil(nb^2/32)
+// participating warps (one warp for R <= 20).  Called by every thread of the CTA.  On exit Gm
+// (stride R+1) holds W = (G_SS)^{-1} on the swept set S and 0 elsewhere; returns |S|.
+__device__ int blk_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /* 2*64 */, int* swept /* R */) {
+  const int tid = threadIdx.x, RS = R + 1;
+  const int nb = (R + 3) >> 2, nact = nb * nb;
+  const int nthr = ((nact + 31) >> 5) << 5;
+  if (tid < nthr) {
+    const bool act = tid < nact;
+    const int bi = act ? tid / nb : -1, bj = act ? tid % nb : -1;
+    const int i0 = 4 * (act ? bi : 0), j0 = 4 * (act ? bj : 0);
+    double v[4][4];
 #pragma unroll
-  for (int t = 0; t < kSweepEPT; ++t) {
-    const int e = tid + t * nth;
-    ei[t] = (e < R * R) ? e / R : -1;
-    ej[t] = (e < R * R) ? e % R : 0;
-    v[t] = (e < R * R) ? Gm[ei[t] * RS + ej[t]] : 0.0;
-  }
-  for (int j = tid; j < R; j += nth) {
-    rowbuf[j] = Gm[j];  // row 0
-    swept[j] = 0;
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        v[a][c] = (act && i0 + a < R && j0 + c < R) ? Gm[(i0 + a) * RS + j0 + c] : 0.0;
+    if (bi == 0)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) rowbuf[j0 + c] = v[0][c];  // row 0 (zero past R)
+    for (int j = tid; j < R; j += nthr) swept[j] = 0;
+    named_bar_sync(1, nthr);
+    for (int k = 0; k < R; ++k) {
+      const double* rk = rowbuf + (k & 1) * 64;
+      double* rn = rowbuf + ((k + 1) & 1) * 64;
+      const double d = rk[k];
+      if (d > tol) {  // uniform across the participating threads
+        const double dinv = __drcp_rn(d);
+        const double2 ri01 = *reinterpret_cast<const double2*>(rk + i0);
+        const double2 ri23 = *reinterpret_cast<const double2*>(rk + i0 + 2);
+        const double2 rj01 = *reinterpret_cast<const double2*>(rk + j0);
+        const double2 rj23 = *reinterpret_cast<const double2*>(rk + j0 + 2);
+        const double ri[4] = {ri01.x, ri01.y, ri23.x, ri23.y};
+        const double f[4] = {rj01.x * dinv, rj01.y * dinv, rj23.x * dinv, rj23.y * dinv};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) v[a][c] = fma(-ri[a], f[c], v[a][c]);
+        const int kb = k >> 2, ks = k & 3;
+        if (bi == kb)  // row k: M_kj / d
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[a][c] = (a == ks) ? f[c] : v[a][c];
+        if (bj == kb)  // column k: M_ik / d, and M_kk = -1/d
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              v[a][c] = (c == ks) ? ((bi == kb && a == ks) ? -dinv : ri[a] * dinv) : v[a][c];
+        if (tid == 0) swept[k] = 1;
+      }
+      if (k + 1 < R && bi == ((k + 1) >> 2)) {  // publish row k+1 for the next pivot
+        const int a = (k + 1) & 3;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) rn[j0 + c] = a == 0 ? v[0][c] : a == 1 ? v[1][c] : a == 2 ? v[2][c] : v[3][c];
+      }
+      named_bar_sync(1, nthr);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = i0 + a, j = j0 + c;
+        if (act && i < R && j < R) Gm[i * RS + j] = (swept[i] && swept[j]) ? -v[a][c] : 0.0;
+      }
   }
   __syncthreads();
   int rank = 0;
-  for (int k = 0; k < R; ++k) {
-    const double* rk = rowbuf + (k & 1) * R;
-    double* rn = rowbuf + ((k + 1) & 1) * R;
-    const double d = rk[k];
-    const bool piv = d > tol;
-    if (piv) {
-      ++rank;
-      const double dinv = __drcp_rn(d);
-#pragma unroll
-      for (int t = 0; t < kSweepEPT; ++t) {
-        const int i = ei[t], j = ej[t];
-        const double rki = rk[i < 0 ? 0 : i], rkj = rk[j];
-        double nv = v[t] - rki * (rkj * dinv);
-        nv = (j == k) ? rki * dinv : nv;
-        nv = (i == k) ? rkj * dinv : nv;
-        nv = (i == k && j == k) ? -dinv : nv;
-        v[t] = (i >= 0) ? nv : v[t];
-      }
-      if (tid == 0) swept[k] = 1;
-    }
-    // publish row k+1 of the (possibly updated) matrix for the next pivot
-#pragma unroll
-    for (int t = 0; t < kSweepEPT; ++t)
-      if (ei[t] == k + 1) rn[ej[t]] = v[t];
-    __syncthreads();
-  }
-#pragma unroll
-  for (int t = 0; t < kSweepEPT; ++t) {
-    const int i = ei[t], j = ej[t];
-    if (i >= 0) Gm[i * RS + j] = (swept[i] && swept[j]) ? -v[t] : 0.0;
-  }
-  __syncthreads();
+  for (int j = 0; j < R; ++j) rank += swept[j];
   return rank;
 }
 
+
+// Same sweep, four pivots per barrier.  Sweep operators on distinct pivots commute and compose:
+// sweeping the pivot block K = {4kb..4kb+3} one pivot at a time (with the R4(b) skip rule) equals
+// one block sweep with S = swept subset of K, U = K \ S, H = (M_SS)^{-1}:
+//   M_IJ -= M_IS H M_SJ,  M_IS <- M_IS H,  M_SJ <- H M_SJ,  M_IU -= M_IS H M_SU,  M_KK <- sweep_S(M_KK).
+// The 4x4 diagonal block D = M_KK is swept sequentially (skip rule on its Schur diagonals, which
+// are exactly those of the one-at-a-time sweep) by every thread redundantly, giving D' and
+// Q = -D' with the U columns zeroed (Q_SS = H).  A thread owning block (bi, bj) then needs only
+// C_i = M_{i,K} and C_j = M_{j,K} (= M_{K,j}) of its rows/columns, published once per block step:
+//   bi, bj != kb : v -= (C_i Hm) C_j^T              (Hm = Q with the U rows zeroed)
+//   bi == kb     : v[a][c] = [a in U] v[a][c] + sum_s Q[a][s] C_j[c][s]
+//   bj == kb     : v[a][c] = [c in U] v[a][c] + sum_s C_i[a][s] Q[c][s]
+//   both         : v = D'
+// ceil(R/4) barriers instead of R; called by every thread of the CTA; returns |S|.
+__device__ int blk4_sweep_inverse(double* Gm, int R, double tol, double* colbuf /* 2*64*4 */, int* swept /* R */) {
+  const int tid = threadIdx.x, RS = R + 1;
+  const int nb = (R + 3) >> 2, nact = nb * nb;
+  const int nthr = ((nact + 31) >> 5) << 5;
+  if (tid < nthr) {
+    const bool act = tid < nact;
+    const int bi = act ? tid / nb : -1, bj = act ? tid % nb : -1;
+    const int i0 = 4 * (act ? bi : 0), j0 = 4 * (act ? bj : 0);
+    double v[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        v[a][c] = (act && i0 + a < R && j0 + c < R) ? Gm[(i0 + a) * RS + j0 + c] : 0.0;
+    // column block 0: colbuf[par][row][4]
+    if (bj == 0)
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        double2* d = reinterpret_cast<double2*>(colbuf + (i0 + a) * 4);
+        d[0] = make_double2(v[a][0], v[a][1]);
+        d[1] = make_double2(v[a][2], v[a][3]);
+      }
+    for (int j = tid; j < R; j += nthr) swept[j] = 0;
+    named_bar_sync(1, nthr);
+    for (int kb = 0; kb < nb; ++kb) {
+      const double* cb = colbuf + (kb & 1) * 256;
+      double* cn = colbuf + ((kb + 1) & 1) * 256;
+      const int k0 = 4 * kb;
+      // D = M_KK, swept one pivot at a time (every thread, identical arithmetic)
+      double D[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double2 x = *reinterpret_cast<const double2*>(cb + (k0 + a) * 4);
+        const double2 y = *reinterpret_cast<const double2*>(cb + (k0 + a) * 4 + 2);
+        D[a][0] = x.x; D[a][1] = x.y; D[a][2] = y.x; D[a][3] = y.y;
+      }
+      bool piv[4];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const double d = D[s][s];
+        piv[s] = (k0 + s < R) && d > tol;
+        if (piv[s]) {
+          const double dinv = __drcp_rn(d);
+          double col[4], row[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            col[a] = D[a][s];
+            row[a] = D[s][a] * dinv;
+          }
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              double nv = fma(-col[a], row[c], D[a][c]);
+              nv = (a == s) ? row[c] : nv;
+              nv = (c == s) ? col[a] * dinv : nv;
+              D[a][c] = (a == s && c == s) ? -dinv : nv;
+            }
+        }
+      }
+      double Q[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) Q[a][c] = piv[c] ? -D[a][c] : 0.0;
+      if (tid == 0)
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+          if (k0 + s < R) swept[k0 + s] = piv[s] ? 1 : 0;
+      if (act) {
+        double Ci[4][4], Cj[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const double2 x = *reinterpret_cast<const double2*>(cb + (i0 + a) * 4);
+          const double2 y = *reinterpret_cast<const double2*>(cb + (i0 + a) * 4 + 2);
+          Ci[a][0] = x.x; Ci[a][1] = x.y; Ci[a][2] = y.x; Ci[a][3] = y.y;
+          const double2 z = *reinterpret_cast<const double2*>(cb + (j0 + a) * 4);
+          const double2 w = *reinterpret_cast<const double2*>(cb + (j0 + a) * 4 + 2);
+          Cj[a][0] = z.x; Cj[a][1] = z.y; Cj[a][2] = w.x; Cj[a][3] = w.y;
+        }
+        if (bi != kb && bj != kb) {
+          double X[4][4];  // X = C_i Hm
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              double t = 0.0;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) t = fma(Ci[a][u], piv[u] ? Q[u][s] : 0.0, t);
+              X[a][s] = t;
+            }
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              double t = v[a][c];
+#pragma unroll
+              for (int s = 0; s < 4; ++s) t = fma(-X[a][s], Cj[c][s], t);
+              v[a][c] = t;
+            }
+        } else if (bi == kb && bj != kb) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              double t = piv[a] ? 0.0 : v[a][c];
+#pragma unroll
+              for (int s = 0; s < 4; ++s) t = fma(Q[a][s], Cj[c][s], t);
+              v[a][c] = t;
+            }
+        } else if (bj == kb && bi != kb) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              double t = piv[c] ? 0.0 : v[a][c];
+#pragma unroll
+              for (int s = 0; s < 4; ++s) t = fma(Ci[a][s], Q[c][s], t);
+              v[a][c] = t;
+            }
+        } else {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[a][c] = D[a][c];
+        }
+        if (bj == kb + 1)  // publish the next column block
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            double2* d = reinterpret_cast<double2*>(cn + (i0 + a) * 4);
+            d[0] = make_double2(v[a][0], v[a][1]);
+            d[1] = make_double2(v[a][2], v[a][3]);
+          }
+      }
+      named_bar_sync(1, nthr);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = i0 + a, j = j0 + c;
+        if (act && i < R && j < R) Gm[i * RS + j] = (swept[i] && swept[j]) ? -v[a][c] : 0.0;
+      }
+  }
+  __syncthreads();
+  int rank = 0;
+  for (int j = 0; j < R; ++j) rank += swept[j];
+  return rank;
+}
 
 // Pivoted variant (largest remaining Schur diagonal first, as a pivoted Cholesky would) for
 // factors that can be rank deficient (I_n < 2R): dependent columns are left for last, where their
@@ -866,6 +1202,19 @@ struct UTParams {
 
 constexpr int kUTThreads = 256;
 
+// fp64 blocking of the table stage: 4x4 register blocks, rows of stride RD = ceil4(R)
+__host__ __device__ inline int ut_rd(int R) { return (R + 3) / 4 * 4; }
+__host__ __device__ inline int ut_gram_groups(int R) {
+  const int nb = (R + 3) / 4, nblk = nb * (nb + 1) / 2;
+  const int g = kUTThreads / nblk;
+  return g < 1 ? 1 : (g > 2 ? 2 : g);
+}
+__host__ __device__ inline size_t ut_work_bytes(int R, int64_t rows_per) {
+  const size_t gram = sizeof(double) * (size_t)ut_gram_groups(R) * (R * (R + 1) / 2);
+  const size_t scores = sizeof(double) * ((size_t)R * ut_rd(R) + (size_t)((R + 3) / 4) * rows_per);
+  return gram > scores ? gram : scores;
+}
+
 // shared-memory carve-up of k_update_table (bytes), also used by the host to size the launch
 __host__ __device__ inline size_t ut_smem_bytes(int R, int64_t rows_per, size_t esz) {
   size_t off = 0;
@@ -875,11 +1224,13 @@ __host__ __device__ inline size_t ut_smem_bytes(int R, int64_t rows_per, size_t 
   take(esz * rows_per * (R + 1));        // Anew
   take(sizeof(double) * (R * (R + 1) / 2 + 1));  // partial Gram / partial ||A||^2 (read by peers)
   take(sizeof(double) * R * (R + 1));    // Gm (Gram -> inverse), row stride R+1
-  take(sizeof(double) * 2 * R);          // sweep row buffer
+  take(sizeof(double) * 2 * kMaxRank);   // sweep row buffer (double-buffered pivot row)
   take(sizeof(int) * R);                 // swept flags
   take(sizeof(double) * rows_per);       // per-row p
   take(sizeof(unsigned long long) * rows_per);   // per-row q -> local inclusive scan
   take(sizeof(unsigned long long) * 2);  // CTA total (read by peers), pad
+  take(sizeof(double) * rows_per * ut_rd(R));  // fp64 copy of the new rows (stride ceil4(R))
+  take(ut_work_bytes(R, rows_per));      // Gram group partials | W (stride ceil4(R)) + score partials
   return off + 16;
 }
 
@@ -912,11 +1263,14 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   T* Anew = reinterpret_cast<T*>(carve(sizeof(T) * p.rows_per * RS));
   double* gpart = reinterpret_cast<double*>(carve(sizeof(double) * (R * (R + 1) / 2 + 1)));
   double* Gm = reinterpret_cast<double*>(carve(sizeof(double) * R * (R + 1)));
-  double* rowbuf = reinterpret_cast<double*>(carve(sizeof(double) * 2 * R));
+  double* rowbuf = reinterpret_cast<double*>(carve(sizeof(double) * 2 * kMaxRank));
   int* swept = reinterpret_cast<int*>(carve(sizeof(int) * R));
   double* prow = reinterpret_cast<double*>(carve(sizeof(double) * p.rows_per));
   unsigned long long* qrow = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * p.rows_per));
   unsigned long long* qtot = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * 2));
+  const int RD = ut_rd(R);
+  double* Ad = reinterpret_cast<double*>(carve(sizeof(double) * p.rows_per * RD));
+  double* work = reinterpret_cast<double*>(carve(ut_work_bytes(R, p.rows_per)));
   __shared__ int piv[kMaxRank];
   __shared__ int s_rank, s_bad, s_stop, s_jm;
   __shared__ double s_red[kUTThreads / 32];
@@ -998,14 +1352,50 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   UT_MARK(1);
   const bool lev = (p.strategy == 1 || p.strategy == 3);
   const int P = R * (R + 1) / 2;
+  const int nb4 = (R + 3) >> 2;
   if (lev) {
+    // fp64 copy of the owned rows, zero padded to RD
+    for (int e = tid; e < nr * RD; e += kUTThreads) {
+      const int il = e / RD, c = e % RD;
+      Ad[e] = c < R ? (double)Anew[il * RS + c] : 0.0;
+    }
+    __syncthreads();
+    // partial Gram sum_il a_il a_il^T: thread = (row group g, 4x4 block bi <= bj); groups summed in order
+    const int nblk = nb4 * (nb4 + 1) / 2, GG = ut_gram_groups(R);
+    const int g = tid / nblk, blk = tid % nblk;
+    if (g < GG) {
+      int bi = 0, rem = blk;
+      while (rem >= nb4 - bi) { rem -= nb4 - bi; ++bi; }
+      const int bj = bi + rem;
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+      for (int il = g; il < nr; il += GG) {
+        const double2 x0 = *reinterpret_cast<const double2*>(Ad + il * RD + 4 * bi);
+        const double2 x1 = *reinterpret_cast<const double2*>(Ad + il * RD + 4 * bi + 2);
+        const double2 y0 = *reinterpret_cast<const double2*>(Ad + il * RD + 4 * bj);
+        const double2 y1 = *reinterpret_cast<const double2*>(Ad + il * RD + 4 * bj + 2);
+        const double x[4] = {x0.x, x0.y, x1.x, x1.y}, y[4] = {y0.x, y0.y, y1.x, y1.y};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = fma(x[a], y[c], acc[a][c]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int r1 = 4 * bi + a, r2 = 4 * bj + c;
+          if (r1 < R && r2 < R && r1 <= r2) work[g * P + r1 * R - r1 * (r1 - 1) / 2 + (r2 - r1)] = acc[a][c];
+        }
+    }
+    __syncthreads();
     for (int pair = tid; pair < P; pair += kUTThreads) {
-      int r1 = 0, rem = pair;
-      while (rem >= R - r1) { rem -= R - r1; ++r1; }
-      const int r2 = r1 + rem;
-      double acc = 0.0;
-      for (int il = 0; il < nr; ++il) acc += (double)Anew[il * RS + r1] * (double)Anew[il * RS + r2];
-      gpart[pair] = acc;
+      double s = work[pair];
+      for (int gg = 1; gg < GG; ++gg) s += work[gg * P + pair];
+      gpart[pair] = s;
     }
   } else {
     double acc = 0.0;
@@ -1063,7 +1453,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     {
       constexpr int EPT = (kMaxRank * kMaxRank + kUTThreads - 1) / kUTThreads;
       const int rk = (p.In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, s_tol, rowbuf, swept, rowbuf + R)
-                                    : cta_sweep_inverse<EPT>(Gm, R, s_tol, rowbuf, swept);
+                                    : blk_sweep_inverse(Gm, R, s_tol, rowbuf, swept);
       if (tid == 0) {
         s_rank = rk;
         if (rk == 0) s_bad |= 2;
@@ -1072,20 +1462,58 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     __syncthreads();
     const int rank = s_rank;
     UT_MARK(4);
-    // scores of the owned rows: l = a^T W a; one warp per row, lanes over i, butterfly sum
+    // scores of the owned rows: l_i = sum_c (A W)_ic a_ic.  W -> stride RD (zero padded); thread
+    // task = 4 rows x 4 columns of A W (k in pairs: 8 LDS.128 per 32 DFMA); per-column-group partials
+    // summed in order.
     {
-      const int lane = tid & 31, wid = tid >> 5;
-      for (int il = wid; il < nr; il += kUTThreads / 32) {
-        const T* a = Anew + il * RS;
-        double part = 0.0;
-        for (int i = lane; i < R; i += 32) {
-          double t = 0.0;
-          for (int j = 0; j < R; ++j) t += Gm[i * (R + 1) + j] * (double)a[j];
-          part += (double)a[i] * t;
+      double* Wd = work;
+      double* sc = work + R * RD;  // [nb4][rows_per]
+      for (int e = tid; e < R * RD; e += kUTThreads) {
+        const int r1 = e / RD, c = e % RD;
+        Wd[e] = c < R ? Gm[r1 * (R + 1) + c] : 0.0;
+      }
+      __syncthreads();
+      const int nrg = (nr + 3) >> 2, ntask = nrg * nb4;
+      for (int t = tid; t < ntask; t += kUTThreads) {
+        const int rg = t / nb4, cg = t % nb4;
+        const int il0 = 4 * rg;
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+        const double* arow[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) arow[a] = Ad + (il0 + a < nr ? il0 + a : il0) * RD;
+        for (int kk = 0; kk < R; kk += 2) {  // RD is a multiple of 4: the pair (kk, kk+1) is in range
+          double2 av[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) av[a] = *reinterpret_cast<const double2*>(arow[a] + kk);
+          const double2 w00 = *reinterpret_cast<const double2*>(Wd + kk * RD + 4 * cg);
+          const double2 w01 = *reinterpret_cast<const double2*>(Wd + kk * RD + 4 * cg + 2);
+          const double2 w10 = *reinterpret_cast<const double2*>(Wd + (kk + 1 < R ? kk + 1 : kk) * RD + 4 * cg);
+          const double2 w11 = *reinterpret_cast<const double2*>(Wd + (kk + 1 < R ? kk + 1 : kk) * RD + 4 * cg + 2);
+          const double wk0[4] = {w00.x, w00.y, w01.x, w01.y};
+          const double wk1[4] = {kk + 1 < R ? w10.x : 0.0, kk + 1 < R ? w10.y : 0.0, kk + 1 < R ? w11.x : 0.0,
+                                 kk + 1 < R ? w11.y : 0.0};
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[a][c] = fma(av[a].y, wk1[c], fma(av[a].x, wk0[c], acc[a][c]));
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == 0) prow[il] = rank > 0 ? fmax(part, 0.0) / (double)rank : 0.0;
+        for (int a = 0; a < 4; ++a) {
+          if (il0 + a >= nr) continue;
+          const double2 x0 = *reinterpret_cast<const double2*>(arow[a] + 4 * cg);
+          const double2 x1 = *reinterpret_cast<const double2*>(arow[a] + 4 * cg + 2);
+          sc[cg * p.rows_per + il0 + a] = acc[a][0] * x0.x + acc[a][1] * x0.y + acc[a][2] * x1.x + acc[a][3] * x1.y;
+        }
+      }
+      __syncthreads();
+      for (int il = tid; il < nr; il += kUTThreads) {
+        double l = 0.0;
+        for (int cg = 0; cg < nb4; ++cg) l += sc[cg * p.rows_per + il];
+        prow[il] = rank > 0 ? fmax(l, 0.0) / (double)rank : 0.0;
       }
     }
   } else {
@@ -1174,6 +1602,12 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     draw_rows(p.sp, cp, r_now + (p.do_update ? 1 : 0), b0, b1, tid, kUTThreads);
     __syncthreads();
     skr_rows<T>(p.sp, b0, b1, tid, kUTThreads);
+    if (p.sp.zwp) {  // wide path: zw rows + Gamma of the next batch (the CDF staging area is free now)
+      __syncthreads();
+      T* red = zw_gamma_rows<T>(p.sp, b0, b1, reinterpret_cast<unsigned char*>(s_cdf), tid, kUTThreads);
+      gamma_cluster_reduce<T>(cluster, red, p.sp.R, reinterpret_cast<T*>(p.sp.gam_next), tid, kUTThreads);
+      synced = true;
+    }
     UT_MARK(7);
   }
   if (p.do_update) {

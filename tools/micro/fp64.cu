@@ -42,6 +42,20 @@ __global__ void divs(double* out, double a, int n, long long* cyc) {
   out[threadIdx.x] = x;
   if (threadIdx.x == 0) cyc[0] = t1 - t0;
 }
+__global__ void rcps(double* out, double a, int n, long long* cyc) {
+  double x = a;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) x = __drcp_rn(x + 1.0);
+  long long t1 = clock64();
+  out[threadIdx.x] = x;
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+__global__ void barw(int n, long long* cyc) {
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) asm volatile("bar.sync 1, 32;");
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
 int main() {
   double* d; float* f; long long* c; long long h;
   cudaMalloc(&d, 1 << 24); cudaMalloc(&f, 1 << 20); cudaMalloc(&c, 64);
@@ -58,6 +72,10 @@ int main() {
   printf("__syncthreads 256 thr: %.2f cyc\n", (double)h / n);
   divs<<<1, 32>>>(d, 1.0, 1000, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
   printf("fp64 1/x dependent: %.2f cyc\n", (double)h / 1000);
+  rcps<<<1, 32>>>(d, 1.0, 1000, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("__drcp_rn dependent: %.2f cyc\n", (double)h / 1000);
+  barw<<<1, 32>>>(n, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("bar.sync 1,32 (1 warp): %.2f cyc\n", (double)h / n);
   cudaDeviceSynchronize();
   return 0;
 }

@@ -16,6 +16,8 @@ ap.add_argument("--workload", default="C2")
 ap.add_argument("--sampler", default="leverage")
 ap.add_argument("--sweeps", type=int, default=5)
 ap.add_argument("--direct", action="store_true", help="no CUDA graph")
+ap.add_argument("--wide", type=int, default=1, help="0: legacy split path (gather partials + update/table)")
+ap.add_argument("--fused", type=int, default=1)
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.workload]
 dev = torch.device("cuda:0")
@@ -28,13 +30,19 @@ else:
     Xd, _, xn = synth.tensor_torch(cfg, device=dev)
     Ad = synth.init_factors_torch(cfg, xn, device=dev)
 h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=a.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta, seed=0,
-          graphs=not a.direct)
+          graphs=not a.direct, wide=bool(a.wide), fused=bool(a.fused))
 h.sweep(2)
 h.sync()
 t = time.perf_counter()
 h.sweep(a.sweeps)
 h.sync()
 print(f"{a.workload} {a.sampler}: {(time.perf_counter() - t) / a.sweeps * 1e6:.1f} us/sweep")
+if a.direct:
+    h.profile(True)
+    h.sweep(a.sweeps)
+    prof = h.profile_read()
+    h.profile(False)
+    print("  per launch (CUDA events): " + ", ".join(f"{k} {v[0] / v[1] * 1e3:.1f} us x{v[1]}" for k, v in prof.items()))
 h.close()
 if os.environ.get("CPSGD_DEBUG_TIMERS") and os.environ.get("FUSED_TIMERS"):
     h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=a.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta, seed=0)
