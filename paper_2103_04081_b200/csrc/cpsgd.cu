@@ -21,6 +21,7 @@
 #include "../../include/cpsgd.h"
 #include "fused.cuh"
 #include "gupdate.cuh"
+#include "tsample.cuh"
 #include "kernels.cuh"
 
 using namespace cps;
@@ -425,13 +426,7 @@ cp_status launch_ut_t(cp_sgd_s* h, int n, int do_update, int do_table, int64_t r
     fill_sample_params(h, p.sp, next_mode, h->iter_dev, 0, h->idx, h->w, h->beff, true);
     const size_t cb = sample_cdf_bytes(h, next_mode);
     p.sp.stage_smem = (cb > 0 && smem + cb <= (size_t)h->sample_smem) ? 1 : 0;
-    size_t extra = p.sp.stage_smem ? cb : 0;
-    if (wide_mode(h, next_mode)) {  // zw rows + Gamma of the next batch (wide path)
-      p.sp.zwp = h->zwp;
-      p.sp.gam_next = h->gam_next;
-      extra = std::max(extra, zg_scratch_bytes(h->R, sizeof(T), kUTThreads));
-    }
-    smem += extra;
+    if (p.sp.stage_smem) smem += cb;
   }
   // one CTA per SM: the cluster's CTAs each run the serial table stages; co-residing CTAs would
   // share one SM's issue slots (claim more than half of the SM's shared memory)
@@ -634,6 +629,70 @@ cp_status launch_zw_gamma_t(cp_sgd_s* h, int n) {
   return check_launch(h, "k_zw_gamma");
 }
 
+int ut_cluster(int64_t In) {
+  int CU = 1;
+  while (CU < 16 && CU * 32 < In) CU *= 2;
+  return CU;
+}
+
+int64_t ts_cdf_elems(const cp_sgd_s* h, int next_mode) {
+  if (next_mode < 0 || h->sampler == CP_UNIFORM) return 0;
+  int64_t c = 0;
+  for (int k = 0; k < h->N; ++k)
+    if (k != next_mode) c += h->dims[k];
+  return c;
+}
+
+// table of the updated A^(n) + the next batch (mode next_mode) with its zw rows and Gamma
+template <typename T>
+cp_status launch_ts_t(cp_sgd_s* h, int n, int next_mode) {
+  ProfScope ps(h, kKTable);
+  TSParams<T> p;
+  memset(&p, 0, sizeof p);
+  const int CU = ut_cluster(h->dims[n]);
+  p.R = h->R;
+  p.strategy = h->sampler;
+  p.In = h->dims[n];
+  p.rows_per = ceil_div(h->dims[n], CU);
+  p.A = (const T*)h->factors[n];
+  p.p_out = h->pprob[n];
+  p.cdf = h->cdf[n];
+  p.Tout = h->Ttot + n;
+  p.status = h->status_dev;
+  p.dbg = h->dbg;
+  if (next_mode >= 0) {
+    p.sample_next = 1;
+    fill_sample_params(h, p.sp, next_mode, h->iter_dev, 0, h->idx, h->w, h->beff, true);
+    p.sp.zwp = h->zwp;
+    p.sp.gam_next = h->gam_next;
+    p.fpc = ceil_div(h->bmax[next_mode], CU);
+  }
+  const size_t smem = ts_layout(h->N, h->R, p.rows_per, p.fpc, ts_cdf_elems(h, next_mode), sizeof(T)).total;
+  static bool attr_set = false;
+  if (!attr_set) {
+    allow_max_dyn_smem(k_table_sample<T>);
+    cudaFuncSetAttribute(k_table_sample<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(CU, 1, 1);
+  lc.blockDim = dim3(kTSThreads, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = h->ls;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CU;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_table_sample<T>, p);
+  h->launches++;
+  if (e != cudaSuccess)
+    return h->fail(CP_ECUDA, "k_table_sample launch (cluster %d, smem %zu): %s", CU, smem, cudaGetErrorString(e));
+  return check_launch(h, "k_table_sample");
+}
+
 // the batch of mode n at the current r into the prefetch buffers (k_sample [+ k_zw_gamma])
 cp_status launch_prefetch(cp_sgd_s* h, int n) {
   cp_status st = launch_sample(h, n, h->iter_dev, h->idx, h->w, h->beff, true);
@@ -785,7 +844,7 @@ cp_status phase0(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
 cp_status phase1(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, int next_mode) {
   if (wide_mode(h, n)) {  // table of the updated A^(n) + the next batch (+ its zw rows and Gamma)
     if (h->sampler == CP_UNIFORM && next_mode < 0) return CP_OK;
-    cp_status st = launch_ut(h, n, 0, 1, 0, h->dims[n], 0.0, nullptr, false, next_mode);
+    cp_status st = h->dtype == CP_F64 ? launch_ts_t<double>(h, n, next_mode) : launch_ts_t<float>(h, n, next_mode);
     if (!st && next_mode >= 0) h->pref_mode = next_mode;
     return st;
   }
@@ -1098,8 +1157,15 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       const int CK = nt > 74 ? 2 : nt > 37 ? 4 : 8;
       const int64_t KB = ceil_div(h->bmax[n], CK);
       const size_t gs = h->esz == 8 ? gu_smem_bytes<double, 8>(KB) : gu_smem_bytes<float, 8>(KB);
-      const size_t us = ut_smem_bytes(h->R, ceil_div(h->dims[n], 16), h->esz) + zg_scratch_bytes(h->R, h->esz, kUTThreads);
-      if (ut_fits(h, h->dims[n]) && gs + 1024 <= (size_t)optin && us <= (size_t)h->sample_smem) {
+      int64_t bmx = 0, cdfmax = 0;
+      for (int k = 0; k < h->N; ++k) {
+        bmx = std::max(bmx, h->bmax[k]);
+        cdfmax = std::max(cdfmax, ts_cdf_elems(h, k));
+      }
+      const int CU = ut_cluster(h->dims[n]);
+      const size_t us = ts_layout(h->N, h->R, ceil_div(h->dims[n], CU), ceil_div(bmx, CU), cdfmax, h->esz).total;
+      const size_t zs = zg_scratch_bytes(h->R, h->esz, 256);
+      if (gs + 1024 <= (size_t)optin && us <= (size_t)h->sample_smem && zs <= (size_t)h->sample_smem) {
         h->gu_ck[n] = CK;
         any = true;
       }

@@ -255,10 +255,11 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     __syncthreads();
     for (int k = 0; k < N; ++k) {  // stage the CDFs of the modes k != n
       if (k == n || p.strategy == 0) continue;
-      for (int64_t i = tid; i < p.dims[k]; i += kFThreads) cdfs[off + i] = p.cdf[k][i];
+      cp_async_u64(cdfs + off, p.cdf[k], p.dims[k], tid, kFThreads);
       if (tid == 0) s_cp[k] = cdfs + off;
       off += p.dims[k];
     }
+    cp_async_wait<0>();
     if (block && tid == 0) {  // window draws (eq:bik, R2): common to the whole batch
       double prod = 1.0;
       int64_t beff = 1;
@@ -380,6 +381,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
       for (int lb = 0; lb < p.BPC; ++lb) g += zw[lb * RP + r1] * zu[lb * RP + r2];
       Gp[e] = g;
     }
+#pragma unroll 8
     for (int e = tid; e < nr * R; e += kFThreads) {  // old rows of the block this CTA updates
       const int il = e / R, c = e % R;
       Aold[il * RS + c] = p.factors[n][(r_beg + il) * R + c];
@@ -480,7 +482,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
         __syncthreads();
         constexpr int EPT = (32 * 32 + kFThreads - 1) / kFThreads;
         const int rank = (In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, s_red[0], rowbuf, swept, rowbuf + R)
-                                      : blk_sweep_inverse(Gm, R, s_red[0], rowbuf, swept);
+                                      : lc_sweep_dispatch<32>(Gm, R, s_red[0], rowbuf, swept);
         F_MARK(6);
         if (tid == 0 && rank == 0) s_bad |= 2;
         // scores l = a^T W a: thread per (row, i) forms a_i * (W a)_i; rows summed in order

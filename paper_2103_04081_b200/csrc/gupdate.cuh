@@ -68,20 +68,6 @@ __host__ __device__ inline size_t gu_smem_bytes(int64_t KB) {
   return a + (size_t)kMaxRank * kMaxRank * sizeof(T) + (size_t)KB * sizeof(int64_t) + 64;
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
-}
-template <int BYTES>
-__device__ __forceinline__ void cp_async_small(void* dst, const void* src, int src_bytes) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src), "n"(BYTES), "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
 template <typename T, int CPT>
 __global__ void __launch_bounds__(kGUThreads, 1) k_gather_update(GUParams<T> p) {
   namespace cg = cooperative_groups;
@@ -108,8 +94,11 @@ __global__ void __launch_bounds__(kGUThreads, 1) k_gather_update(GUParams<T> p) 
   const int nfib = (int)cmax64(0, c1 - c0);
   const int nst = (nfib + KS - 1) / KS;
 
-  for (int b = tid; b < nfib; b += kGUThreads) sfb[b] = p.fbase[c0 + b];
+  cp_async_u64(reinterpret_cast<uint64_t*>(sfb), reinterpret_cast<const uint64_t*>(p.fbase + c0), nfib, tid,
+               kGUThreads);
+#pragma unroll 8
   for (int e = tid; e < R * R; e += kGUThreads) sGam[e] = p.Gam[e];
+  cp_async_wait<0>();
   __syncthreads();
 
   auto xs_of = [&](int s) { return pipe + (size_t)s * KS * (TI + RP); };
@@ -206,6 +195,7 @@ __global__ void __launch_bounds__(kGUThreads, 1) k_gather_update(GUParams<T> p) 
   T* Mf = Mt + TI * MS;              // [rows_q][R]
   T* Af = Mf + rows_q * R;           // [rows_q][R+1] old rows of A
   const int nrow = (int)cmax64(0, cmin64(rows_q, p.In - (i0 + rl0)));
+#pragma unroll 4
   for (int e = tid; e < nrow * R; e += kGUThreads) {
     const int rl = e / R, c = e % R;
     T v[16];

@@ -116,6 +116,27 @@ __device__ __forceinline__ T ldg(const T* p) {
   return __ldg(p);
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_small(void* dst, const void* src, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src), "n"(BYTES), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// global -> shared copy of n 8-byte elements, every request in flight at once (one commit group);
+// the caller waits (cp_async_wait<0>) and synchronises
+__device__ __forceinline__ void cp_async_u64(uint64_t* dst, const uint64_t* src, int64_t n, int tid, int nth) {
+  for (int64_t i = tid; i < n; i += nth) cp_async_small<8>(dst + i, src + i, 8);
+  cp_async_commit();
+}
+
 // ==========================================================================================
 // (a1) importance table of one mode -- single CTA of 1024 threads.
 //   leverage : l_i = ||L^{-1} a_{i,piv}||^2 with A_piv^T A_piv = L L^T (pivoted Cholesky of the
@@ -336,15 +357,18 @@ __device__ __forceinline__ void stage_cdfs(const SampleParams& p, uint64_t* s_cd
   for (int k = 0; k < p.N; ++k) {
     cdfp[k] = p.cdf[k];
     if (k == p.n || !p.stage_smem || p.strategy == 0) continue;
-    for (int64_t i = tid; i < p.dims[k]; i += nthreads) s_cdf[off + i] = p.cdf[k][i];
+    cp_async_u64(s_cdf + off, p.cdf[k], p.dims[k], tid, nthreads);
     cdfp[k] = s_cdf + off;
     off += p.dims[k];
   }
+  cp_async_wait<0>();
 }
 
 // rows [b0, b1) of the batch of mode p.n at iteration r: indices, exact weights, fiber offsets.
 __device__ __forceinline__ void draw_rows(const SampleParams& p, const uint64_t* const* cdfp, uint64_t r_it,
-                                          int64_t b0, int64_t b1, int tid, int nthreads) {
+                                          int64_t b0, int64_t b1, int tid, int nthreads,
+                                          int32_t* sidx = nullptr /* shared [b1-b0][N-1] copy */,
+                                          double* sw = nullptr /* shared [b1-b0] copy */) {
   const int N = p.N, n = p.n;
   const bool block = (p.strategy == 3 || p.strategy == 4);
   int32_t start[kMaxOrder], len[kMaxOrder];
@@ -378,6 +402,9 @@ __device__ __forceinline__ void draw_rows(const SampleParams& p, const uint64_t*
   for (int64_t b = b0 + tid; b < b1; b += nthreads) {
     if (b >= beff) {
       if (p.fbase) p.fbase[b] = -1;
+      if (sw) sw[b - b0] = 0.0;
+      if (sidx)
+        for (int q = 0; q < N - 1; ++q) sidx[(b - b0) * (N - 1) + q] = 0;
       continue;
     }
     int32_t* ib = p.idx + b * (N - 1);
@@ -405,6 +432,7 @@ __device__ __forceinline__ void draw_rows(const SampleParams& p, const uint64_t*
         ++pos;
       }
       p.w[b] = __ddiv_rn(1.0, __dmul_rn((double)p.B, prod));
+      if (sw) sw[b - b0] = __ddiv_rn(1.0, __dmul_rn((double)p.B, prod));
     } else {
       int64_t rem = b;
       for (int q = 0; q < N - 1; ++q) {
@@ -412,7 +440,10 @@ __device__ __forceinline__ void draw_rows(const SampleParams& p, const uint64_t*
         rem /= len[q];
       }
       p.w[b] = wblk;
+      if (sw) sw[b - b0] = wblk;
     }
+    if (sidx)
+      for (int q = 0; q < N - 1; ++q) sidx[(b - b0) * (N - 1) + q] = ib[q];
     if (p.fbase) {  // fiber offset in the gather's layout (mode-major row, or native base)
       int64_t off = 0, jrow = 0, jmul = 1;
       bool own = true;
@@ -931,6 +962,89 @@ __device__ int blk_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /
 }
 
 
+// Same sweep, lane per column: thread c < RMAX (RMAX = ceil8(R) <= 64, warps 0..RMAX/32) keeps
+// column c of the RMAX x RMAX matrix (identity past R) in registers, rows in ROTATED order: before
+// pivot k slot t holds row (k + t) mod RMAX, so the pivot row is always slot 0 and every register
+// index is static.  Pivot k:
+//   publish  thread c stores v[0] (= M_kc = M_ck by symmetry) at cb[(c - k) mod RMAX], so slot t
+//            of every column reads c_t = M_{row(t),k} = cb[t] (broadcast loads);
+//   d = c_0 > tol:  f = (c == k) ? -1/d : v[0]/d;  slot t-1 <- [c != k] v[t] - c_t f (t >= 1);
+//                   slot RMAX-1 <- f (the new row k);      otherwise rotate only.
+// One named barrier (or __syncwarp) per pivot; one DFMA + two selects per held entry.  After R
+// pivots slot t holds row (R + t) mod RMAX.  Called by every thread of the CTA; returns |S|.
+template <int RMAX>
+__device__ int lc_sweep_inverse(double* Gm, int R, double tol, double* colbuf /* 2*RMAX */, int* swept /* R */) {
+  constexpr int NT = (RMAX + 31) / 32 * 32;
+  const int tid = threadIdx.x, RS = R + 1;
+  if (tid < NT) {
+    const int c = tid;
+    double v[RMAX];
+#pragma unroll
+    for (int t = 0; t < RMAX; ++t) v[t] = (t < R && c < R) ? Gm[t * RS + c] : (t == c ? 1.0 : 0.0);
+    for (int j = tid; j < R; j += NT) swept[j] = 0;
+#pragma unroll 1
+    for (int k = 0; k < R; ++k) {
+      double* cb = colbuf + (k & 1) * RMAX;
+      if (c < RMAX) cb[c >= k ? c - k : c - k + RMAX] = v[0];
+      if (NT == 32) __syncwarp();
+      else named_bar_sync(1, NT);
+      const double d = cb[0];
+      if (d > tol) {  // uniform
+        const double dinv = __drcp_rn(d);
+        const bool isk = (c == k);
+        const double f = isk ? -dinv : v[0] * dinv;
+#pragma unroll
+        for (int u = 0; u < RMAX; u += 2) {  // (c_u, c_{u+1}) per broadcast load
+          const double2 cc = *reinterpret_cast<const double2*>(cb + u);
+          if (u >= 1) v[u - 1] = fma(-cc.x, f, isk ? 0.0 : v[u]);
+          v[u] = fma(-cc.y, f, isk ? 0.0 : v[u + 1]);
+        }
+        v[RMAX - 1] = f;
+        if (tid == 0) swept[k] = 1;
+      } else {
+        const double v0 = v[0];
+#pragma unroll
+        for (int t = 1; t < RMAX; ++t) v[t - 1] = v[t];
+        v[RMAX - 1] = v0;
+      }
+    }
+    if (NT == 32) __syncwarp();
+    else named_bar_sync(1, NT);
+    if (c < R) {
+#pragma unroll
+      for (int t = 0; t < RMAX; ++t) {
+        const int i = t - (RMAX - R);  // slot t holds row (R + t) mod RMAX
+        if (i >= 0) Gm[i * RS + c] = (swept[i] && swept[c]) ? -v[t] : 0.0;
+      }
+    }
+  }
+  __syncthreads();
+  int rank = 0;
+  for (int j = 0; j < R; ++j) rank += swept[j];
+  return rank;
+}
+
+// MAXR: largest rank the calling kernel supports (instantiates only RMAX <= MAXR)
+template <int MAXR = kMaxRank>
+__device__ inline int lc_sweep_dispatch(double* Gm, int R, double tol, double* colbuf, int* swept) {
+  switch ((R + 7) / 8) {
+    case 1: return lc_sweep_inverse<8>(Gm, R, tol, colbuf, swept);
+    case 2: return lc_sweep_inverse<16>(Gm, R, tol, colbuf, swept);
+    case 3: return lc_sweep_inverse<24>(Gm, R, tol, colbuf, swept);
+    case 4: return lc_sweep_inverse<32>(Gm, R, tol, colbuf, swept);
+    default: break;
+  }
+  if constexpr (MAXR > 32) {
+    switch ((R + 7) / 8) {
+      case 5: return lc_sweep_inverse<40>(Gm, R, tol, colbuf, swept);
+      case 6: return lc_sweep_inverse<48>(Gm, R, tol, colbuf, swept);
+      case 7: return lc_sweep_inverse<56>(Gm, R, tol, colbuf, swept);
+      default: return lc_sweep_inverse<64>(Gm, R, tol, colbuf, swept);
+    }
+  }
+  return 0;
+}
+
 // Same sweep, four pivots per barrier.  Sweep operators on distinct pivots commute and compose:
 // sweeping the pivot block K = {4kb..4kb+3} one pivot at a time (with the R4(b) skip rule) equals
 // one block sweep with S = swept subset of K, U = K \ S, H = (M_SS)^{-1}:
@@ -1286,6 +1400,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   }
 
   // ---------------- stage A: update ----------------
+#pragma unroll 8
   for (int e = tid; e < nr * R; e += kUTThreads) {
     const int il = e / R, c = e % R;
     Aold[il * RS + c] = p.A[(r_beg + il) * R + c];
@@ -1355,6 +1470,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   const int nb4 = (R + 3) >> 2;
   if (lev) {
     // fp64 copy of the owned rows, zero padded to RD
+#pragma unroll 8
     for (int e = tid; e < nr * RD; e += kUTThreads) {
       const int il = e / RD, c = e % RD;
       Ad[e] = c < R ? (double)Anew[il * RS + c] : 0.0;
@@ -1453,7 +1569,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     {
       constexpr int EPT = (kMaxRank * kMaxRank + kUTThreads - 1) / kUTThreads;
       const int rk = (p.In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, s_tol, rowbuf, swept, rowbuf + R)
-                                    : blk_sweep_inverse(Gm, R, s_tol, rowbuf, swept);
+                                    : lc_sweep_dispatch(Gm, R, s_tol, rowbuf, swept);
       if (tid == 0) {
         s_rank = rk;
         if (rk == 0) s_bad |= 2;
@@ -1602,12 +1718,6 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     draw_rows(p.sp, cp, r_now + (p.do_update ? 1 : 0), b0, b1, tid, kUTThreads);
     __syncthreads();
     skr_rows<T>(p.sp, b0, b1, tid, kUTThreads);
-    if (p.sp.zwp) {  // wide path: zw rows + Gamma of the next batch (the CDF staging area is free now)
-      __syncthreads();
-      T* red = zw_gamma_rows<T>(p.sp, b0, b1, reinterpret_cast<unsigned char*>(s_cdf), tid, kUTThreads);
-      gamma_cluster_reduce<T>(cluster, red, p.sp.R, reinterpret_cast<T*>(p.sp.gam_next), tid, kUTThreads);
-      synced = true;
-    }
     UT_MARK(7);
   }
   if (p.do_update) {

@@ -54,11 +54,13 @@ if os.environ.get("CPSGD_DEBUG_TIMERS") and os.environ.get("FUSED_TIMERS"):
     print("gram-sum", t[13] - t[5], "sweep", t[6] - t[13])
 elif os.environ.get("CPSGD_DEBUG_TIMERS"):
     h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=a.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta, seed=0,
-              graphs=False)
+              graphs=False, wide=bool(a.wide), fused=bool(a.fused))
     h.sweep(3)
     t = h.debug_timers()
-    names = ["start", "stageB", "gram-synced", "sweep-start", "sweep-done", "scores-done", "cdf-synced", "sampled"]
-    print(" ".join(f"{names[i]}:{t[i] - t[0]}" for i in range(8)))
-    print("iter1: pivot->rcp", t[9] - t[8], "update", t[10] - t[9], "sync", t[11] - t[10], "rowcol+sync", t[12] - t[11],
-          "full iter", t[13] - t[8])
-    print("smids", t[16:32])
+    if a.wide:  # k_table_sample marks
+        names = ["gram+sync", "sweep", "scores", "scan+cdf", "draw", "skr+zw+gamma"]
+        print("k_table_sample cycles: " + " | ".join(f"{names[i]} {t[i + 1] - t[i]}" for i in range(6)),
+              "| total", t[6] - t[0])
+    else:
+        names = ["start", "stageB", "gram-synced", "sweep-start", "sweep-done", "scores-done", "cdf-synced", "sampled"]
+        print(" ".join(f"{names[i]}:{t[i] - t[0]}" for i in range(8)))
