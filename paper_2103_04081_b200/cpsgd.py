@@ -19,9 +19,10 @@ LIB_PATH = os.path.join(_HERE, "libcpsgd.so")
 SAMPLERS = {"uniform": 0, "leverage": 1, "euclidean": 2, "block_leverage": 3, "block_euclidean": 4}
 RULES = {"fixed": 0, "adaptive": 1}
 ORDERS = {"cyclic": 0, "random": 1}
-FLAG_MODE_MAJOR, FLAG_NO_GRAPH, FLAG_EXTERNAL_COMM, FLAG_NO_FUSED, FLAG_NO_WIDE = 0x1, 0x2, 0x4, 0x8, 0x10
+FLAG_MODE_MAJOR, FLAG_NO_GRAPH, FLAG_EXTERNAL_COMM, FLAG_NO_FUSED, FLAG_NO_WIDE, FLAG_NO_TC = \
+    0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 KERNEL_NAMES = ["k_sample", "k_gather", "k_update_table", "k_table", "k_reduce_partials", "nccl", "k_fit",
-                "k_sweep_fused", "k_gather_update", "k_zw_gamma"]
+                "k_sweep_fused", "k_gather_update", "k_zw_gamma", "k_gather_update_tc"]
 STATUS = {0: "CP_OK", -1: "CP_EINVAL", -2: "CP_ERANGE", -3: "CP_EDEGENERATE", -4: "CP_ENOMEM", -5: "CP_ECUDA",
           -6: "CP_ENCCL", -7: "CP_ESTATE", -8: "CP_ENONFINITE"}
 
@@ -115,7 +116,8 @@ class CPSGD:
                  rule: str = "fixed", alpha: float = 0.01, eta: float = 0.05, b: float = 0.0, eps: float = 0.0,
                  seed: int = 0, stream=None, world_rank: int = 0, world_size: int = 1, nccl_id: bytes = None,
                  slab=None, mode_major: bool = True, block_window=None, graphs: bool = True,
-                 external_comm: bool = False, fused: bool = True, wide: bool = True):
+                 external_comm: bool = False, fused: bool = True, wide: bool = True,
+                 tc: bool = True):
         import torch
 
         L = load_library()
@@ -140,7 +142,7 @@ class CPSGD:
         self._nccl_id = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
         flags = (FLAG_MODE_MAJOR if mode_major else 0) | (0 if graphs else FLAG_NO_GRAPH) | \
                 (FLAG_EXTERNAL_COMM if external_comm else 0) | (0 if fused else FLAG_NO_FUSED) | \
-                (0 if wide else FLAG_NO_WIDE)
+                (0 if wide else FLAG_NO_WIDE) | (0 if tc else FLAG_NO_TC)
         lo, hi = (0, self.dims[-1]) if slab is None else (int(slab[0]), int(slab[1]))
         cfg = Config(self.N, self._dims_arr, self.R, self.dtype, X.data_ptr(), self._fac_arr, int(batch),
                      self._win_arr, SAMPLERS[sampler], RULES[rule], float(alpha), float(eta), float(b), float(eps),
@@ -279,7 +281,7 @@ class CPSGD:
         return int(n.value)
 
     def debug_timers(self):
-        out = (C.c_longlong * 64)()
+        out = (C.c_longlong * 4096)()
         self._chk(self._L.cp_sgd_debug_timers(self._h, out))
         return list(out)
 

@@ -21,6 +21,7 @@
 #include "../../include/cpsgd.h"
 #include "fused.cuh"
 #include "gupdate.cuh"
+#include "gupdate_tc.cuh"
 #include "tsample.cuh"
 #include "kernels.cuh"
 
@@ -77,7 +78,7 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
-enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kKGatherUpdate, kKZwGamma, kNumKernelIds };
+enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kKGatherUpdate, kKZwGamma, kKGatherUpdateTC, kNumKernelIds };
 
 struct ProfRec {
   int id;
@@ -145,7 +146,13 @@ struct cp_sgd_s {
   int* last_mode_dev = nullptr;  // written by the fused sweep kernel
   void* zwp = nullptr;           // wide path: weighted padded SKR rows [Bmax][ceil8(R)] of the prefetched batch
   void* gam_next = nullptr;      // wide path: Gamma of the prefetched batch [R][R]
-  int gu_ck[kMaxOrder] = {};     // wide path: cluster size (batch chunks) of k_gather_update, 0 = not eligible
+  int gu_ck[kMaxOrder] = {};     // wide path: batch chunks (CTAs per I-tile) of k_gather_update, 0 = not eligible
+  int64_t gu_kb[kMaxOrder] = {};  // wide path: fibers per chunk
+  void* Mpart = nullptr;         // wide path: split-K partial tiles [tiles][chunks][128][R]
+  unsigned* gu_cnt = nullptr;    // wide path: per-tile arrival counters
+  int tc_nb8 = 0;                // fp32 wide path on tcgen05: UMMA N = 8 tc_nb8 = ceil8(R), 0 = FFMA mainloop
+  float* zhi = nullptr;          // tcgen05 path: 3xTF32 B-operand images of the prefetched batch
+  float* zlo = nullptr;
   int fused_cu = 0, fused_bpc = 0, fused_rpc = 0;  // fused kernel geometry (0: not eligible)
   size_t fused_smem = 0;
   int pref_mode = -1;            // mode whose batch (at the current r) sits in idx/w/zrow/fbase
@@ -291,6 +298,9 @@ void fill_sample_params(cp_sgd_s* h, SampleParams& p, int n, const uint64_t* ite
   if (prefetch) {
     p.zrow = h->zrow;
     p.fbase = h->fbase;
+    p.zhi = h->zhi;
+    p.zlo = h->zlo;
+    p.nb8 = h->tc_nb8;
   }
 }
 
@@ -538,7 +548,9 @@ cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   p.zwp = (const T*)h->zwp;
   p.bmax = h->bmax[n];
   const int CK = h->gu_ck[n];
-  p.KB = ceil_div(h->bmax[n], CK);
+  p.KB = h->gu_kb[n];
+  p.Mpart = (T*)h->Mpart;
+  p.cnt = h->gu_cnt;
   p.Gam = (const T*)h->gam_next;
   p.A = (T*)h->factors[n];
   p.S = (T*)h->S[n];
@@ -555,6 +567,7 @@ cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   static bool attr_set = false;
   if (!attr_set) {
     allow_max_dyn_smem(k_gather_update<T, CPT>);
+    cudaFuncSetAttribute(k_gather_update<T, CPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
@@ -562,21 +575,80 @@ cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   lc.blockDim = dim3(kGUThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 1;
-  at[0].val.clusterDim.y = CK;
-  at[0].val.clusterDim.z = 1;
-  lc.attrs = at;
-  lc.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&lc, k_gather_update<T, CPT>, p);
   h->launches++;
   if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_gather_update launch: %s", cudaGetErrorString(e));
   return check_launch(h, "k_gather_update");
 }
 
+template <int NB8>
+cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
+  ProfScope ps(h, kKGatherUpdateTC);
+  GUParams<float> p;
+  memset(&p, 0, sizeof p);
+  p.R = h->R;
+  p.In = h->dims[n];
+  p.X = h->Xmm[n] ? (const float*)h->Xmm[n] : (const float*)h->X;
+  p.es = 1;
+  p.vec = 1;
+  p.rowlen = h->Xmm[n] ? h->pitch[n] : h->dims[n];
+  p.fbase = h->fbase;
+  p.zwp = (const float*)h->zwp;
+  p.zhi = h->zhi;
+  p.zlo = h->zlo;
+  p.bmax = h->bmax[n];
+  const int CK = h->gu_ck[n];
+  p.KB = h->gu_kb[n];
+  p.Mpart = (float*)h->Mpart;
+  p.cnt = h->gu_cnt;
+  p.Gam = (const float*)h->gam_next;
+  p.A = (float*)h->factors[n];
+  p.S = (float*)h->S[n];
+  p.Gout = (float*)h->Gout;
+  p.Gam_out = (float*)h->Gam_out;
+  p.rule = h->rule;
+  p.alpha = alpha;
+  p.alpha_dev = alpha_dev;
+  p.eta = h->eta;
+  p.b = h->bpar;
+  p.eps = h->eps;
+  p.iter = h->iter_dev;
+  p.dbg = h->dbg;
+  const size_t smem = tc_smem_bytes<NB8>(h->R, p.KB);
+  static bool attr_set = false;
+  if (!attr_set) {
+    allow_max_dyn_smem(k_gather_update_tc<NB8>);
+    cudaFuncSetAttribute(k_gather_update_tc<NB8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)ceil_div(h->dims[n], kGUTI), (unsigned)CK, 1);
+  lc.blockDim = dim3(kTCThreads, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = h->ls;
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_gather_update_tc<NB8>, p);
+  h->launches++;
+  if (e != cudaSuccess)
+    return h->fail(CP_ECUDA, "k_gather_update_tc launch (cluster %d, smem %zu): %s", CK, smem, cudaGetErrorString(e));
+  return check_launch(h, "k_gather_update_tc");
+}
+
 template <typename T>
 cp_status launch_gu(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
+  // tensor-core mainloop needs fiber-contiguous, 16-byte aligned fibers (mode-major copy, or mode 0)
+  const bool tc_ok = sizeof(T) == 4 && h->tc_nb8 && (h->Xmm[n] || (n == 0 && h->dims[0] % 4 == 0));
+  if (tc_ok) {
+    switch (h->tc_nb8) {
+      case 1: return launch_gu_tc<1>(h, n, alpha, alpha_dev);
+      case 2: return launch_gu_tc<2>(h, n, alpha, alpha_dev);
+      case 3: return launch_gu_tc<3>(h, n, alpha, alpha_dev);
+      case 4: return launch_gu_tc<4>(h, n, alpha, alpha_dev);
+      case 5: return launch_gu_tc<5>(h, n, alpha, alpha_dev);
+      case 6: return launch_gu_tc<6>(h, n, alpha, alpha_dev);
+      case 7: return launch_gu_tc<7>(h, n, alpha, alpha_dev);
+      default: return launch_gu_tc<8>(h, n, alpha, alpha_dev);
+    }
+  }
   switch ((h->R + 7) / 8) {
     case 1: return launch_gu_t<T, 1>(h, n, alpha, alpha_dev);
     case 2: return launch_gu_t<T, 2>(h, n, alpha, alpha_dev);
@@ -645,7 +717,7 @@ int64_t ts_cdf_elems(const cp_sgd_s* h, int next_mode) {
 
 // table of the updated A^(n) + the next batch (mode next_mode) with its zw rows and Gamma
 template <typename T>
-cp_status launch_ts_t(cp_sgd_s* h, int n, int next_mode) {
+cp_status launch_ts_t(cp_sgd_s* h, int n, int next_mode, double alpha, const double* alpha_dev) {
   ProfScope ps(h, kKTable);
   TSParams<T> p;
   memset(&p, 0, sizeof p);
@@ -653,7 +725,20 @@ cp_status launch_ts_t(cp_sgd_s* h, int n, int next_mode) {
   p.R = h->R;
   p.strategy = h->sampler;
   p.In = h->dims[n];
-  p.rows_per = ceil_div(h->dims[n], CU);
+  p.rows_per = ceil_div(ceil_div(h->dims[n], CU), 4) * 4;  // multiple of 4: 16-byte partial reads
+  // stage U: finish the step of k_gather_update (sum of the chunk partials, G = A Gamma - M, update)
+  p.Mpart = (const T*)h->Mpart;
+  p.CK = h->gu_ck[n];
+  p.Gam = (const T*)h->gam_next;
+  p.Aw = (T*)h->factors[n];
+  p.S = (T*)h->S[n];
+  p.Gout = (T*)h->Gout;
+  p.rule = h->rule;
+  p.alpha = alpha;
+  p.alpha_dev = alpha_dev;
+  p.eta = h->eta;
+  p.b = h->bpar;
+  p.eps = h->eps;
   p.A = (const T*)h->factors[n];
   p.p_out = h->pprob[n];
   p.cdf = h->cdf[n];
@@ -843,8 +928,8 @@ cp_status phase0(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
 // update (+ table + next batch when the rows are all local)
 cp_status phase1(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, int next_mode) {
   if (wide_mode(h, n)) {  // table of the updated A^(n) + the next batch (+ its zw rows and Gamma)
-    if (h->sampler == CP_UNIFORM && next_mode < 0) return CP_OK;
-    cp_status st = h->dtype == CP_F64 ? launch_ts_t<double>(h, n, next_mode) : launch_ts_t<float>(h, n, next_mode);
+    cp_status st = h->dtype == CP_F64 ? launch_ts_t<double>(h, n, next_mode, alpha, alpha_dev)
+                                      : launch_ts_t<float>(h, n, next_mode, alpha, alpha_dev);
     if (!st && next_mode >= 0) h->pref_mode = next_mode;
     return st;
   }
@@ -1090,8 +1175,8 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
   ALLOC(h->beff_api, sizeof(int64_t));
   ALLOC(h->last_mode_dev, sizeof(int));
   if (getenv("CPSGD_DEBUG_TIMERS")) {
-    ALLOC(h->dbg, sizeof(long long) * 64);
-    cudaMemsetAsync(h->dbg, 0, sizeof(long long) * 64, h->stream);
+    ALLOC(h->dbg, sizeof(long long) * 4096);
+    cudaMemsetAsync(h->dbg, 0, sizeof(long long) * 4096, h->stream);
   }
   ALLOC(h->zrow, h->esz * Bmax_all * h->R);
   ALLOC(h->fbase, sizeof(int64_t) * Bmax_all);
@@ -1152,28 +1237,54 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     bool any = false;
+    const bool tc = h->dtype == CP_F32 && !(h->flags & CP_FLAG_NO_TC);
+    if (tc) h->tc_nb8 = (h->R + 7) / 8;
+    int64_t mpart = 0;
     for (int n = 0; n < h->N; ++n) {
       const int64_t nt = ceil_div(h->dims[n], kGUTI);
-      const int CK = nt > 74 ? 2 : nt > 37 ? 4 : 8;
-      const int64_t KB = ceil_div(h->bmax[n], CK);
-      const size_t gs = h->esz == 8 ? gu_smem_bytes<double, 8>(KB) : gu_smem_bytes<float, 8>(KB);
+      // chunks per I-tile: one wave of CTAs (tcgen05 kernel: one CTA per SM; FFMA kernel: two)
+      const int64_t slots = tc ? 148 : 296;
+      int64_t CK = std::max<int64_t>(1, std::min<int64_t>(slots / nt, 64));
+      const int64_t gran = tc ? kTCKS : 8;
+      int64_t KB = ceil_div(ceil_div(h->bmax[n], CK), gran) * gran;
+      CK = ceil_div(h->bmax[n], KB);  // no empty chunk
+      size_t gs = h->esz == 8 ? gu_smem_bytes<double, 8>(KB) : gu_smem_bytes<float, 8>(KB);
+      if (tc) gs = std::max(gs, tc_smem_bytes<8>(h->R, KB));
       int64_t bmx = 0, cdfmax = 0;
       for (int k = 0; k < h->N; ++k) {
         bmx = std::max(bmx, h->bmax[k]);
         cdfmax = std::max(cdfmax, ts_cdf_elems(h, k));
       }
       const int CU = ut_cluster(h->dims[n]);
-      const size_t us = ts_layout(h->N, h->R, ceil_div(h->dims[n], CU), ceil_div(bmx, CU), cdfmax, h->esz).total;
+      const size_t us = ts_layout(h->N, h->R, ceil_div(ceil_div(h->dims[n], CU), 4) * 4, ceil_div(bmx, CU), cdfmax,
+                                  h->esz).total;
       const size_t zs = zg_scratch_bytes(h->R, h->esz, 256);
       if (gs + 1024 <= (size_t)optin && us <= (size_t)h->sample_smem && zs <= (size_t)h->sample_smem) {
-        h->gu_ck[n] = CK;
+        h->gu_ck[n] = (int)CK;
+        h->gu_kb[n] = KB;
+        mpart = std::max(mpart, nt * CK * kGUTI * h->R);
         any = true;
       }
     }
     if (any) {
+      ALLOC(h->Mpart, h->esz * mpart);
+      ALLOC(h->gu_cnt, sizeof(unsigned) * ceil_div(Imax, kGUTI));
+      cudaMemsetAsync(h->gu_cnt, 0, sizeof(unsigned) * ceil_div(Imax, kGUTI), h->stream);
       ALLOC(h->zwp, h->esz * Bmax_all * zg_rp(h->R));
       ALLOC(h->gam_next, h->esz * h->R * h->R);
       cudaMemsetAsync(h->zwp, 0, h->esz * Bmax_all * zg_rp(h->R), h->stream);
+      if (h->tc_nb8) {  // B images: every chunk rounded up to whole stages; rows past B_max stay zero
+        int64_t rows = 0;
+        for (int n = 0; n < h->N; ++n)
+          if (h->gu_ck[n]) rows = std::max(rows, (int64_t)h->gu_ck[n] * h->gu_kb[n]);
+        const size_t bytes = sizeof(float) * (size_t)rows * 8 * h->tc_nb8;
+        ALLOC(h->zhi, bytes);
+        ALLOC(h->zlo, bytes);
+        cudaMemsetAsync(h->zhi, 0, bytes, h->stream);
+        cudaMemsetAsync(h->zlo, 0, bytes, h->stream);
+      }
+    } else {
+      h->tc_nb8 = 0;
     }
   }
   // ---- optional mode-major copies (n >= 1; mode 0 fibers are already contiguous) ----
@@ -1266,6 +1377,10 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->fbase);
   cudaFree(h->zwp);
   cudaFree(h->gam_next);
+  cudaFree(h->zhi);
+  cudaFree(h->zlo);
+  cudaFree(h->Mpart);
+  cudaFree(h->gu_cnt);
   cudaFree(h->iter_dev);
   cudaFree(h->iter_tmp);
   cudaFree(h->status_dev);
@@ -1626,7 +1741,7 @@ cp_status cp_sgd_debug_timers(cp_sgd_t h, long long* out16) {
   if (!h || !out16) return CP_EINVAL;
   if (!h->dbg) return h->fail(CP_ESTATE, "CPSGD_DEBUG_TIMERS was not set at init");
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-  CUDA_TRY(h, cudaMemcpy(out16, h->dbg, sizeof(long long) * 64, cudaMemcpyDeviceToHost));
+  CUDA_TRY(h, cudaMemcpy(out16, h->dbg, sizeof(long long) * 4096, cudaMemcpyDeviceToHost));
   return CP_OK;
 }
 

@@ -94,19 +94,6 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
 
 
 
-template <typename T>
-struct Vec;
-template <>
-struct Vec<float> {
-  using type = float4;
-  static constexpr int W = 4;
-};
-template <>
-struct Vec<double> {
-  using type = double2;
-  static constexpr int W = 2;
-};
-
 // fiber gather + contraction for ROWS rows per thread and RV vector groups of columns:
 // acc[u][g] += x(row u) * zw[lb][g]; zw rows padded to RV * W with zeros (stride RP).
 template <typename T, int ROWS, int RV>

@@ -1,4 +1,4 @@
-// gupdate.cuh -- k_gather_update: the wide single-GPU step kernel for problems too large for one
+// gupdate.cuh -- k_gather_update: the wide single-GPU gather kernel for problems too large for one
 // cluster (C4/C5 of BASELINE.json).  ONE launch does, for every row block of A^(n):
 //
 //   (a5) TensorSamp (Alg. 5): the I-tile segment of every sampled fiber,
@@ -7,13 +7,11 @@
 //   (a6) M_tile = X_F diag(w) Z_F restricted to the tile (eq:gradient1/2):
 //        register-blocked FFMA (4 rows x CPT columns per thread) against the weighted SKR rows
 //        zw_b = w_b z_b prepared by the sampler (Alg. 1);
-//   (a6) deterministic split-K: the CK CTAs of a cluster hold the CK batch chunks of one I-tile;
-//        partial tiles are summed through DSMEM in rank order, CTA q finishing rows
-//        [q TI/CK, (q+1) TI/CK) of the tile;
-//   (a6-a8) G = A Gamma - M for those rows (Gamma = Z_F^T diag(w) Z_F from the sampler), then the
-//        fixed (eq:proposed, :459-464) or adaptive (eq:etaada/eq:Aada, :531-537, R12) update.
+//   (a6) deterministic split-K: the CK CTAs of an I-tile hold its CK batch chunks; their partial
+//        tiles go to a global workspace, summed in chunk order by k_table_sample, which also forms
+//        G = A Gamma - M and applies the update (a7, a8) before rebuilding the table.
 //
-// grid = (ceil(I_n / TI), CK), cluster (1, CK, 1); 256 threads: warp w = column group
+// grid = (ceil(I_n / TI), CK); 256 threads: warp w = column group
 // [w CPT, (w+1) CPT), lane l = rows [4l, 4l+4) of the tile.  RP = 8 CPT >= R (zero padded).
 #pragma once
 #include <cooperative_groups.h>
@@ -34,8 +32,11 @@ struct GUParams {
   const T* X;             // gather base: mode-major copy of mode n (es = 1) or the native tensor
   int64_t es;             // element stride along a fiber
   int vec;                // 1: es == 1 and every fiber starts 16-byte aligned (16-byte cp.async)
+  int64_t rowlen;         // tcgen05 path: readable elements per fiber row (pitch of the mode-major copy)
   const int64_t* fbase;   // [Bmax] element offset of fiber b (-1: padding row)
   const T* zwp;           // [Bmax][RP] weighted SKR rows, zero padded (sampler)
+  const float* zhi;       // tcgen05 path: 3xTF32 split of zw (hi / lo) as UMMA B-operand images
+  const float* zlo;       //   [B_pad/8][NB/32][8][32] (MN-major, 128-byte swizzle), see gupdate_tc.cuh
   int64_t bmax;           // rows of the batch buffers for this mode
   int64_t KB;             // fibers per chunk (= per CTA)
   const T* Gam;           // [R][R] Gamma of this batch (sampler)
@@ -48,6 +49,9 @@ struct GUParams {
   const double* alpha_dev;
   double eta, b, eps;
   uint64_t* iter;         // r <- r + 1 (Alg. 6/7)
+  T* Mpart;               // [tiles][chunks][TI][R] partial tiles (split-K workspace)
+  unsigned* cnt;          // [tiles] arrival counters (zero between launches)
+  long long* dbg;         // optional phase timestamps (CTA (0,0), thread 0)
 };
 
 // shared memory: max(pipeline, epilogue) + Gamma + fiber offsets of the chunk
@@ -55,11 +59,10 @@ template <typename T, int CPT>
 __host__ __device__ constexpr size_t gu_pipe_bytes() {
   return (size_t)kGUStages * kGUKS * (kGUTI + 8 * CPT) * sizeof(T);
 }
-// epilogue: partial tile [TI][RP+1] (read by the peers) + finished rows M [TI/CK][R] + old rows of
-// A [TI/CK][R+1]; the host uses CK >= 2
+// epilogue: partial tile [TI][RP+1]
 template <typename T, int CPT>
 __host__ __device__ constexpr size_t gu_epi_bytes() {
-  return ((size_t)kGUTI * (8 * CPT + 1) + (size_t)(kGUTI / 2) * (16 * CPT + 1)) * sizeof(T);
+  return (size_t)kGUTI * (8 * CPT + 1) * sizeof(T);
 }
 template <typename T, int CPT>
 __host__ __device__ inline size_t gu_smem_bytes(int64_t KB) {
@@ -68,9 +71,26 @@ __host__ __device__ inline size_t gu_smem_bytes(int64_t KB) {
   return a + (size_t)kMaxRank * kMaxRank * sizeof(T) + (size_t)KB * sizeof(int64_t) + 64;
 }
 
+// Epilogue shared by both mainloops: this CTA's partial tile M_c (shared, [TI][MS]) -> the split-K
+// workspace p.Mpart[tile][chunk][R][TI] (row-contiguous, coalesced).  The chunk partials are summed
+// in chunk order, and G = A Gamma - M and the update applied, by k_table_sample (the next launch).
+template <typename T>
+__device__ __forceinline__ void gu_finish(const GUParams<T>& p, const T* Mt, int MS, int64_t i0, int tid, int nth) {
+  const int R = p.R, TI = kGUTI;
+  const int nrow = (int)cmax64(0, cmin64(TI, p.In - i0));
+  T* part = p.Mpart + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * R * TI;
+  for (int e = tid; e < R * TI; e += nth) {
+    const int r = e / TI, rl = e % TI;
+    if (rl < nrow) part[e] = Mt[rl * MS + r];
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0) {
+    for (int e = tid; e < R * R; e += nth) p.Gam_out[e] = p.Gam[e];
+    if (tid == 0) *p.iter += 1;  // r <- r + 1 (Alg. 6/7); nothing in this launch reads r
+  }
+}
+
 template <typename T, int CPT>
 __global__ void __launch_bounds__(kGUThreads, 1) k_gather_update(GUParams<T> p) {
-  namespace cg = cooperative_groups;
   constexpr int RP = 8 * CPT;
   constexpr int TI = kGUTI, KS = kGUKS, NS = kGUStages;
   constexpr int VE = 16 / (int)sizeof(T);      // elements per 16-byte vector
@@ -83,9 +103,6 @@ __global__ void __launch_bounds__(kGUThreads, 1) k_gather_update(GUParams<T> p) 
   T* sGam = reinterpret_cast<T*>(gu_sm + kA);
   int64_t* sfb = reinterpret_cast<int64_t*>(gu_sm + kA + (size_t)kMaxRank * kMaxRank * sizeof(T));
 
-  cg::cluster_group cluster = cg::this_cluster();
-  const int CK = (int)cluster.dim_blocks().y;
-  const int q = (int)cluster.block_index().y;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int R = p.R;
   const int64_t i0 = (int64_t)blockIdx.x * TI;
@@ -96,8 +113,6 @@ __global__ void __launch_bounds__(kGUThreads, 1) k_gather_update(GUParams<T> p) 
 
   cp_async_u64(reinterpret_cast<uint64_t*>(sfb), reinterpret_cast<const uint64_t*>(p.fbase + c0), nfib, tid,
                kGUThreads);
-#pragma unroll 8
-  for (int e = tid; e < R * R; e += kGUThreads) sGam[e] = p.Gam[e];
   cp_async_wait<0>();
   __syncthreads();
 
@@ -181,64 +196,15 @@ __global__ void __launch_bounds__(kGUThreads, 1) k_gather_update(GUParams<T> p) 
   cp_async_wait<0>();
   __syncthreads();
 
-  // ---- split-K over the cluster: partial tile -> shared [TI][RP+1]; rank-ordered DSMEM sum ----
+  // ---- split-K: partial tile -> shared [TI][RP+1] -> gu_finish ----
   constexpr int MS = RP + 1;
   T* Mt = pipe;
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int c = 0; c < CPT; ++c) Mt[(4 * lane + a) * MS + wid * CPT + c] = acc[a][c];
-  cluster.sync();
-  const int rows_q = TI / CK;
-  const int rl0 = q * rows_q;
-  // finished rows go after Mt (Mt is read by the peers until the final cluster barrier)
-  T* Mf = Mt + TI * MS;              // [rows_q][R]
-  T* Af = Mf + rows_q * R;           // [rows_q][R+1] old rows of A
-  const int nrow = (int)cmax64(0, cmin64(rows_q, p.In - (i0 + rl0)));
-#pragma unroll 4
-  for (int e = tid; e < nrow * R; e += kGUThreads) {
-    const int rl = e / R, c = e % R;
-    T v[16];
-#pragma unroll
-    for (int qq = 0; qq < 16; ++qq)
-      v[qq] = qq < CK ? cluster.map_shared_rank(Mt, qq)[(rl0 + rl) * MS + c] : T(0);
-    T s = v[0];
-#pragma unroll
-    for (int qq = 1; qq < 16; ++qq) s += v[qq];
-    Mf[rl * R + c] = s;
-    Af[rl * (R + 1) + c] = p.A[(i0 + rl0 + rl) * R + c];
-  }
   __syncthreads();
-  // ---- G = A Gamma - M; fixed / adaptive update of the finished rows ----
-  const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
-  for (int e = tid; e < nrow * R; e += kGUThreads) {
-    const int rl = e / R, r = e % R;
-    const int64_t gi = (i0 + rl0 + rl) * R + r;
-    T ag = T(0);
-    for (int c = 0; c < R; ++c) ag += Af[rl * (R + 1) + c] * sGam[c * R + r];
-    const T g = ag - Mf[rl * R + r];
-    p.Gout[gi] = g;
-    const T a = Af[rl * (R + 1) + r];
-    T an = a;
-    if (p.rule == 0) {
-      an = a - (T)alpha * g;
-    } else {
-      const T sv = p.S[gi] + g * g;
-      p.S[gi] = sv;
-      if (sv > T(0)) {
-        T step;
-        if (p.eps == 0.0) step = (T)p.eta / sqrt((T)p.b + sv);
-        else step = (T)p.eta / (T)pow((double)((T)p.b + sv), 0.5 + p.eps);
-        an = a - step * g;
-      }
-    }
-    p.A[gi] = an;
-  }
-  if (blockIdx.x == 0 && q == 0) {
-    for (int e = tid; e < R * R; e += kGUThreads) p.Gam_out[e] = sGam[e];
-    if (tid == 0) *p.iter += 1;  // r <- r + 1 (Alg. 6/7); nothing in this launch reads r
-  }
-  cluster.sync();  // peers may still read this CTA's partial tile
+  gu_finish<T>(p, Mt, MS, i0, tid, kGUThreads);
 }
 
 }  // namespace cps

@@ -53,7 +53,23 @@ struct SampleParams {
   // wide path (k_gather_update): weighted padded SKR rows and Gamma of the batch (or NULL)
   void* zwp;                       // T [B_max][ceil8(R)]
   void* gam_next;                  // T [R][R]
+  float* zhi;                      // tcgen05 path: 3xTF32 split of zw as UMMA B images (or NULL)
+  float* zlo;
+  int nb8;                         //   UMMA N = 8 nb8 (= ceil8(R)) rows of the B images
 };
+
+// byte offset of (fiber b, column r) in the UMMA B-operand images of gupdate_tc.cuh: per stage of 32
+// fibers, NB = 8 nb8 rows (columns r) of 128 B, K-major with the 128-byte swizzle
+__host__ __device__ __forceinline__ uint32_t zimg_off(int64_t b, int r, int nb8) {
+  const int kk = (int)(b & 31), rr = r & 7, c = (kk >> 2) & 7;
+  return (uint32_t)((b >> 5) * (8 * nb8 * 128) + (r >> 3) * 1024 + rr * 128 + ((c ^ rr) << 4) + ((kk & 3) << 2));
+}
+__device__ __forceinline__ void write_zw_images(const SampleParams& p, int64_t b, int r, float zw) {
+  const float h = __uint_as_float(__float_as_uint(zw) & 0xFFFFE000u);
+  const uint32_t o = zimg_off(b, r, p.nb8) >> 2;
+  p.zhi[o] = h;
+  p.zlo[o] = zw - h;
+}
 
 template <typename T>
 struct GatherParams {
@@ -107,6 +123,19 @@ __device__ __forceinline__ int64_t upper_bound_u64(const uint64_t* __restrict__ 
   }
   return lo;  // #{i : cdf[i] <= r}
 }
+
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  using type = float4;
+  static constexpr int W = 4;
+};
+template <>
+struct Vec<double> {
+  using type = double2;
+  static constexpr int W = 2;
+};
 
 __host__ __device__ __forceinline__ int64_t cmin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t cmax64(int64_t a, int64_t b) { return a > b ? a : b; }
@@ -560,6 +589,9 @@ __device__ T* zw_gamma_rows(const SampleParams& p, int64_t b0, int64_t b1, unsig
       zs[e] = z;
       ws[e] = zw;
       if (kk < nch) zwp[b * RP + r] = zw;
+      if constexpr (sizeof(T) == 4) {
+        if (p.zhi && kk < nch && r < R) write_zw_images(p, b, r, (float)zw);
+      }
     }
     __syncthreads();
     if (act) {

@@ -37,10 +37,22 @@ struct TSParams {
   int sample_next;
   int64_t fpc;          // fibers of the next batch per CTA
   SampleParams sp;      // next batch (mode sp.n); sp.zwp / sp.gam_next set
+  // stage U (wide path, p.Mpart != NULL): finish the step k_gather_update started
+  const T* Mpart;       // [tiles][CK][R][128] chunk partials of M = X_F diag(w) Z_F
+  int CK;
+  const T* Gam;         // Gamma of this step's batch (R x R)
+  T* Aw;                // A^(n), updated in place (== A)
+  T* S;                 // adaptive accumulator of mode n, or NULL
+  T* Gout;              // G (debug hook)
+  int rule;
+  double alpha;
+  const double* alpha_dev;
+  double eta, b, eps;
   long long* dbg;
 };
 
 struct TSLayout {
+  size_t us, uss, ug, um;                                               // update phase (rows: stride R+1)
   size_t ad, work, gpart, gm, colbuf, swept, prow, qrow, qtot, tbytes;   // table phase
   size_t cdfs, sidx, sw, zs, red, sbytes;                               // sample phase (aliases)
   size_t total;
@@ -57,7 +69,9 @@ __host__ __device__ inline TSLayout ts_layout(int N, int R, int64_t rows_per, in
     return at;
   };
   const int RD = ut_rd(R);
+  // table phase
   L.ad = take(sizeof(double) * rows_per * RD);
+  const size_t ad_end = off;
   L.work = take(ut_work_bytes(R, rows_per));
   L.gpart = take(sizeof(double) * (R * (R + 1) / 2 + 1));
   L.gm = take(sizeof(double) * R * (R + 1));
@@ -67,6 +81,16 @@ __host__ __device__ inline TSLayout ts_layout(int N, int R, int64_t rows_per, in
   L.qrow = take(sizeof(unsigned long long) * rows_per);
   L.qtot = take(sizeof(unsigned long long) * 2);
   L.tbytes = off;
+  // update phase (before the table; everything but `us` is dead once the rows are updated, and `us`
+  // only until the fp64 copy `ad` is filled, so `us` must not overlap `ad`)
+  off = 0;
+  L.uss = take(esz * rows_per * (R + 1));    // S rows
+  L.ug = take(esz * R * R);                  // Gamma
+  L.um = take(esz * rows_per * (R + 1));     // M rows -> G rows
+  if (off < ad_end) off = ad_end;
+  L.us = take(esz * rows_per * (R + 1));     // rows of A^(n), updated
+  const size_t ubytes = off;
+  // sample phase
   off = 0;
   const int RP = zg_rp(R);
   L.cdfs = take(sizeof(uint64_t) * cdf_elems);
@@ -75,7 +99,8 @@ __host__ __device__ inline TSLayout ts_layout(int N, int R, int64_t rows_per, in
   L.zs = take(esz * fpc * RP);
   L.red = take(esz * (size_t)zg_groups(R, kTSThreads) * R * R);
   L.sbytes = off;
-  L.total = (L.tbytes > L.sbytes ? L.tbytes : L.sbytes) + 16;
+  size_t tot = L.tbytes > L.sbytes ? L.tbytes : L.sbytes;
+  L.total = (tot > ubytes ? tot : ubytes) + 16;
   return L;
 }
 
@@ -114,6 +139,126 @@ __global__ void __launch_bounds__(kTSThreads, 1) k_table_sample(TSParams<T> p) {
   __shared__ double s_tol, s_fro;
   if (tid == 0) s_bad = 0;
   TS_MARK(0);
+  T* As = reinterpret_cast<T*>(ts_sm + L.us);  // rows of A^(n) owned by this CTA (stride R+1)
+  if (p.Mpart) {
+    // ======================= (a6-a8) finish the step: G = A Gamma - sum_c M_c, update =======================
+    T* Ss = reinterpret_cast<T*>(ts_sm + L.uss);
+    T* sG = reinterpret_cast<T*>(ts_sm + L.ug);
+    T* Mf = reinterpret_cast<T*>(ts_sm + L.um);
+    for (int e = tid; e < nr * R; e += kTSThreads) {
+      const int il = e / R, c = e % R;
+      cp_async_small<sizeof(T)>(As + il * RS + c, p.Aw + (r_beg + il) * R + c, sizeof(T));
+      if (p.rule != 0) cp_async_small<sizeof(T)>(Ss + il * RS + c, p.S + (r_beg + il) * R + c, sizeof(T));
+    }
+    for (int e = tid; e < R * R; e += kTSThreads) cp_async_small<sizeof(T)>(sG + e, p.Gam + e, sizeof(T));
+    cp_async_commit();
+    // M rows: partials [tile][c][r][128 rows], 16-byte vectors of VW rows, chunks summed in order
+    {
+      constexpr int VW = 16 / (int)sizeof(T);
+      using V = typename Vec<T>::type;
+      const int ng = (nr + VW - 1) / VW;  // rows_per and r_beg are multiples of 4 (host)
+      const int ntask = R * ng;
+      constexpr int TU = 2;
+      for (int t0 = tid; t0 < ntask; t0 += TU * kTSThreads) {
+        T acc[TU][VW];
+        int64_t off[TU];
+#pragma unroll
+        for (int u = 0; u < TU; ++u) {
+          const int t = t0 + u * kTSThreads;
+          const int r = t / ng, gq = t % ng;
+          const int64_t row = r_beg + (int64_t)gq * VW;
+          off[u] = t < ntask ? ((row / kGUTI) * p.CK * R + r) * kGUTI + (row % kGUTI) : -1;
+#pragma unroll
+          for (int w = 0; w < VW; ++w) acc[u][w] = T(0);
+        }
+        for (int c0 = 0; c0 < p.CK; c0 += 8) {
+          V ld[TU][8];
+#pragma unroll
+          for (int u = 0; u < TU; ++u)
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (off[u] >= 0 && c0 + k < p.CK)
+                ld[u][k] = __ldcg(reinterpret_cast<const V*>(p.Mpart + off[u] + (int64_t)(c0 + k) * R * kGUTI));
+#pragma unroll
+          for (int u = 0; u < TU; ++u)
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (off[u] >= 0 && c0 + k < p.CK) {
+                const T* x = reinterpret_cast<const T*>(&ld[u][k]);
+#pragma unroll
+                for (int w = 0; w < VW; ++w) acc[u][w] += x[w];
+              }
+        }
+#pragma unroll
+        for (int u = 0; u < TU; ++u) {
+          const int t = t0 + u * kTSThreads;
+          if (t >= ntask) continue;
+          const int r = t / ng, gq = t % ng;
+#pragma unroll
+          for (int w = 0; w < VW; ++w)
+            if (gq * VW + w < nr) Mf[(gq * VW + w) * RS + r] = acc[u][w];
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    // G = A Gamma - M (4 rows x 4 columns per task), then the fixed / adaptive update in place
+    T* Gf = Mf;
+    {
+      const int ntask = ((nr + 3) >> 2) * nb4;
+      for (int t = tid; t < ntask; t += kTSThreads) {
+        const int r0 = 4 * (t / nb4), q0 = 4 * (t % nb4);
+        T acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = T(0);
+        for (int k = 0; k < R; ++k) {
+          T x[4], y[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) x[a] = (r0 + a < nr) ? As[(r0 + a) * RS + k] : T(0);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) y[c] = (q0 + c < R) ? sG[k * R + q0 + c] : T(0);
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[a][c] = fma(x[a], y[c], acc[a][c]);
+        }
+        // each task reads and writes only its own 4x4 block of M -> G in place
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (r0 + a < nr && q0 + c < R) Gf[(r0 + a) * RS + q0 + c] = acc[a][c] - Mf[(r0 + a) * RS + q0 + c];
+      }
+    }
+    __syncthreads();
+    const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
+    for (int e = tid; e < nr * R; e += kTSThreads) {
+      const int il = e / R, r = e % R;
+      const int64_t gi = (r_beg + il) * R + r;
+      const T g = Gf[il * RS + r];
+      p.Gout[gi] = g;
+      const T a = As[il * RS + r];
+      T an = a;
+      if (p.rule == 0) {
+        an = a - (T)alpha * g;
+      } else {
+        const T sv = Ss[il * RS + r] + g * g;
+        p.S[gi] = sv;
+        if (sv > T(0)) {
+          T step;
+          if (p.eps == 0.0) step = (T)p.eta / sqrt((T)p.b + sv);
+          else step = (T)p.eta / (T)pow((double)((T)p.b + sv), 0.5 + p.eps);
+          an = a - step * g;
+        }
+      }
+      p.Aw[gi] = an;
+      As[il * RS + r] = an;
+    }
+    __syncthreads();
+    TS_MARK(7);
+  }
 
   if (p.strategy != 0) {
     // ======================= (a1) table of the updated A^(n) =======================
@@ -121,7 +266,7 @@ __global__ void __launch_bounds__(kTSThreads, 1) k_table_sample(TSParams<T> p) {
 #pragma unroll 8
     for (int e = tid; e < nr * RD; e += kTSThreads) {  // fp64 copy of the owned rows, zero padded to RD
       const int il = e / RD, c = e % RD;
-      Ad[e] = c < R ? (double)p.A[(r_beg + il) * R + c] : 0.0;
+      Ad[e] = c < R ? (double)(p.Mpart ? As[il * RS + c] : p.A[(r_beg + il) * R + c]) : 0.0;
     }
     __syncthreads();
     if (lev) {
@@ -399,8 +544,12 @@ __global__ void __launch_bounds__(kTSThreads, 1) k_table_sample(TSParams<T> p) {
   {
     T* zwp = reinterpret_cast<T*>(sp.zwp);
     for (int e = tid; e < nf * RP; e += kTSThreads) {
-      const int lb = e / RP;
-      zwp[(b0 + lb) * RP + (e % RP)] = (T)sw[lb] * zs[e];
+      const int lb = e / RP, r = e % RP;
+      const T zw = (T)sw[lb] * zs[e];
+      zwp[(b0 + lb) * RP + r] = zw;
+      if constexpr (sizeof(T) == 4) {
+        if (sp.zhi && r < R) write_zw_images(sp, b0 + lb, r, (float)zw);
+      }
     }
     const int nblk = nb4 * (nb4 + 1) / 2, G = zg_groups(R, kTSThreads);
     const int g = tid / nblk, blk = tid % nblk;

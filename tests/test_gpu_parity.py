@@ -120,6 +120,7 @@ STEP_CASES = [
 PATHS = {"fused": dict(fused=True, mode_major=True),            # persistent single-cluster kernel
          "split_mm": dict(fused=False, mode_major=True),        # gather+update kernel, then table/sample kernel
          "split_native": dict(fused=False, mode_major=False),   # same, strided fibers in the native layout
+         "split_ffma": dict(fused=False, tc=False, mode_major=True),  # wide path, FFMA mainloop (no tcgen05)
          "legacy_mm": dict(fused=False, wide=False, mode_major=True)}  # gather partials + update/table/sample
 
 

@@ -57,6 +57,20 @@ elif os.environ.get("CPSGD_DEBUG_TIMERS"):
               graphs=False, wide=bool(a.wide), fused=bool(a.fused))
     h.sweep(3)
     t = h.debug_timers()
+    if t[36]:
+        print("k_gather_update_tc cycles: prologue", t[33] - t[32], "mainloop", t[34] - t[33], "tmem->smem", t[35] - t[34],
+              "finish", t[36] - t[35])
+        import numpy as np
+        g0 = np.array(t[1024:3072:2]); g1 = np.array(t[1025:3072:2]); m = g0 > 0
+        g0, g1 = g0[m], g1[m]
+        base = g0.min()
+        print(f"  CTAs {m.sum()}: start spread {(g0.max() - base) / 1e3:.1f} us, end min {(g1.min() - base) / 1e3:.1f} "
+              f"max {(g1.max() - base) / 1e3:.1f} us, duration median {np.median(g1 - g0) / 1e3:.1f} us; "
+              f"distinct SMs {len(set(t[3072:3072 + m.sum()]))}")
+        print("  finish(tile 0): chunk0 A-load", t[38] - t[37], "AGamma", t[39] - t[38], "part+fence+atomic", t[40] - t[39],
+              "| last CTA = chunk", t[60], ": reduce", t[41] - (t[40] if t[60] == 0 else t[48]), "update", t[42] - t[41])
+        print("  stage 8: load issue->data", t[18] - t[23], "wait xh/xl", t[19] - t[18], "split", t[20] - t[19],
+              "split->mma start", t[21] - t[20], "mma issue", t[22] - t[21])
     if a.wide:  # k_table_sample marks
         names = ["gram+sync", "sweep", "scores", "scan+cdf", "draw", "skr+zw+gamma"]
         print("k_table_sample cycles: " + " | ".join(f"{names[i]} {t[i + 1] - t[i]}" for i in range(6)),
