@@ -78,7 +78,7 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
-enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kKGatherUpdate, kKZwGamma, kKGatherUpdateTC, kNumKernelIds };
+enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kKGatherUpdate, kKZwGamma, kKGatherUpdateTC, kKTableSample, kNumKernelIds };
 
 struct ProfRec {
   int id;
@@ -718,7 +718,7 @@ int64_t ts_cdf_elems(const cp_sgd_s* h, int next_mode) {
 // table of the updated A^(n) + the next batch (mode next_mode) with its zw rows and Gamma
 template <typename T>
 cp_status launch_ts_t(cp_sgd_s* h, int n, int next_mode, double alpha, const double* alpha_dev) {
-  ProfScope ps(h, kKTable);
+  ProfScope ps(h, kKTableSample);
   TSParams<T> p;
   memset(&p, 0, sizeof p);
   const int CU = ut_cluster(h->dims[n]);
