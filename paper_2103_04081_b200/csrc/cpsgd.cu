@@ -22,7 +22,7 @@
 #include "fused.cuh"
 #include "gupdate.cuh"
 #include "gupdate_tc.cuh"
-#include "tsample.cuh"
+#include "wide.cuh"
 #include "kernels.cuh"
 
 using namespace cps;
@@ -78,7 +78,7 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
-enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kKGatherUpdate, kKZwGamma, kKGatherUpdateTC, kKTableSample, kNumKernelIds };
+enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kKGatherUpdate, kKZwGamma, kKGatherUpdateTC, kKTableSample, kKUpdateWide, kKTableWide, kKSampleWide, kNumKernelIds };
 
 struct ProfRec {
   int id;
@@ -149,7 +149,11 @@ struct cp_sgd_s {
   int gu_ck[kMaxOrder] = {};     // wide path: batch chunks (CTAs per I-tile) of k_gather_update, 0 = not eligible
   int64_t gu_kb[kMaxOrder] = {};  // wide path: fibers per chunk
   void* Mpart = nullptr;         // wide path: split-K partial tiles [tiles][chunks][128][R]
-  unsigned* gu_cnt = nullptr;    // wide path: per-tile arrival counters
+  unsigned* gu_cnt = nullptr;    // wide path: per-tile arrival counters (unused)
+  double* uw_gpart = nullptr;    // wide path: k_update_wide table partials [CTAs][R(R+1)/2]
+  double* uw_rownorm = nullptr;  // wide path: Euclidean row norms [I_max]
+  void* sw_gcl = nullptr;        // wide path: k_sample_wide cluster partials of Gamma
+  unsigned* sw_cnt = nullptr;    // wide path: k_sample_wide arrival counter
   int tc_nb8 = 0;                // fp32 wide path on tcgen05: UMMA N = 8 tc_nb8 = ceil8(R), 0 = FFMA mainloop
   float* zhi = nullptr;          // tcgen05 path: 3xTF32 B-operand images of the prefetched batch
   float* zlo = nullptr;
@@ -661,46 +665,6 @@ cp_status launch_gu(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
   }
 }
 
-int zg_cluster(const cp_sgd_s* h, int n) {
-  int CU = 1;
-  while (CU < 16 && CU * 256 < h->bmax[n]) CU *= 2;
-  return CU;
-}
-
-// zw rows + Gamma of the batch in idx / w / zrow / fbase (after k_sample)
-template <typename T>
-cp_status launch_zw_gamma_t(cp_sgd_s* h, int n) {
-  ProfScope ps(h, kKZwGamma);
-  SampleParams p;
-  fill_sample_params(h, p, n, h->iter_dev, 0, h->idx, h->w, h->beff, true);
-  p.zwp = h->zwp;
-  p.gam_next = h->gam_next;
-  const int CU = zg_cluster(h, n);
-  const size_t smem = zg_scratch_bytes(h->R, sizeof(T), 256);
-  static bool attr_set = false;
-  if (!attr_set) {
-    allow_max_dyn_smem(k_zw_gamma<T>);
-    cudaFuncSetAttribute(k_zw_gamma<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr_set = true;
-  }
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(CU, 1, 1);
-  lc.blockDim = dim3(256, 1, 1);
-  lc.dynamicSmemBytes = smem;
-  lc.stream = h->ls;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CU;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  lc.attrs = at;
-  lc.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&lc, k_zw_gamma<T>, p);
-  h->launches++;
-  if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_zw_gamma launch: %s", cudaGetErrorString(e));
-  return check_launch(h, "k_zw_gamma");
-}
-
 int ut_cluster(int64_t In) {
   int CU = 1;
   while (CU < 16 && CU * 32 < In) CU *= 2;
@@ -715,53 +679,72 @@ int64_t ts_cdf_elems(const cp_sgd_s* h, int next_mode) {
   return c;
 }
 
-// table of the updated A^(n) + the next batch (mode next_mode) with its zw rows and Gamma
+// ---- wide path: k_update_wide -> k_table_wide -> k_sample_wide (wide.cuh) ----
 template <typename T>
-cp_status launch_ts_t(cp_sgd_s* h, int n, int next_mode, double alpha, const double* alpha_dev) {
-  ProfScope ps(h, kKTableSample);
-  TSParams<T> p;
+cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
+  ProfScope ps(h, kKUpdateWide);
+  UWParams<T> p;
   memset(&p, 0, sizeof p);
-  const int CU = ut_cluster(h->dims[n]);
   p.R = h->R;
   p.strategy = h->sampler;
+  p.rule = h->rule;
   p.In = h->dims[n];
-  p.rows_per = ceil_div(ceil_div(h->dims[n], CU), 4) * 4;  // multiple of 4: 16-byte partial reads
-  // stage U: finish the step of k_gather_update (sum of the chunk partials, G = A Gamma - M, update)
   p.Mpart = (const T*)h->Mpart;
   p.CK = h->gu_ck[n];
   p.Gam = (const T*)h->gam_next;
-  p.Aw = (T*)h->factors[n];
+  p.A = (T*)h->factors[n];
   p.S = (T*)h->S[n];
   p.Gout = (T*)h->Gout;
-  p.rule = h->rule;
+  p.Gam_out = (T*)h->Gam_out;
   p.alpha = alpha;
   p.alpha_dev = alpha_dev;
   p.eta = h->eta;
   p.b = h->bpar;
   p.eps = h->eps;
-  p.A = (const T*)h->factors[n];
+  p.gpart = h->uw_gpart;
+  p.rownorm = h->uw_rownorm;
+  const size_t smem = uw_smem_bytes(h->R, sizeof(T));
+  static bool attr_set = false;
+  if (!attr_set) {
+    allow_max_dyn_smem(k_update_wide<T>);
+    attr_set = true;
+  }
+  k_update_wide<T><<<(unsigned)ceil_div(h->dims[n], kUWRows), kWThreads, smem, h->ls>>>(p);
+  h->launches++;
+  return check_launch(h, "k_update_wide");
+}
+
+template <typename T>
+cp_status launch_tw_t(cp_sgd_s* h, int n) {
+  if (h->sampler == CP_UNIFORM) return CP_OK;  // uniform tables are constant
+  ProfScope ps(h, kKTableWide);
+  TWParams p;
+  memset(&p, 0, sizeof p);
+  const int CU = ut_cluster(h->dims[n]);
+  p.R = h->R;
+  p.strategy = h->sampler;
+  p.In = h->dims[n];
+  p.rows_per = ceil_div(h->dims[n], CU);
+  p.nparts = (int)ceil_div(h->dims[n], kUWRows);
+  p.gpart = h->uw_gpart;
+  p.rownorm = h->uw_rownorm;
+  p.A = h->factors[n];
+  p.esz = (int)sizeof(T);
   p.p_out = h->pprob[n];
   p.cdf = h->cdf[n];
   p.Tout = h->Ttot + n;
   p.status = h->status_dev;
   p.dbg = h->dbg;
-  if (next_mode >= 0) {
-    p.sample_next = 1;
-    fill_sample_params(h, p.sp, next_mode, h->iter_dev, 0, h->idx, h->w, h->beff, true);
-    p.sp.zwp = h->zwp;
-    p.sp.gam_next = h->gam_next;
-    p.fpc = ceil_div(h->bmax[next_mode], CU);
-  }
-  const size_t smem = ts_layout(h->N, h->R, p.rows_per, p.fpc, ts_cdf_elems(h, next_mode), sizeof(T)).total;
+  const size_t smem = tw_smem_bytes(h->R, p.rows_per);
   static bool attr_set = false;
   if (!attr_set) {
-    allow_max_dyn_smem(k_table_sample<T>);
-    cudaFuncSetAttribute(k_table_sample<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    allow_max_dyn_smem(k_table_wide<T>);
+    cudaFuncSetAttribute(k_table_wide<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(CU, 1, 1);
-  lc.blockDim = dim3(kTSThreads, 1, 1);
+  lc.blockDim = dim3(kWThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
   cudaLaunchAttribute at[1];
@@ -771,18 +754,53 @@ cp_status launch_ts_t(cp_sgd_s* h, int n, int next_mode, double alpha, const dou
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&lc, k_table_sample<T>, p);
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_table_wide<T>, p);
   h->launches++;
-  if (e != cudaSuccess)
-    return h->fail(CP_ECUDA, "k_table_sample launch (cluster %d, smem %zu): %s", CU, smem, cudaGetErrorString(e));
-  return check_launch(h, "k_table_sample");
+  if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_table_wide launch (cluster %d, smem %zu): %s", CU, smem, cudaGetErrorString(e));
+  return check_launch(h, "k_table_wide");
+}
+
+template <typename T>
+cp_status launch_sw_t(cp_sgd_s* h, int n) {
+  ProfScope ps(h, kKSampleWide);
+  SWParams p;
+  memset(&p, 0, sizeof p);
+  fill_sample_params(h, p.sp, n, h->iter_dev, 0, h->idx, h->w, h->beff, true);
+  p.sp.zwp = h->zwp;
+  p.sp.gam_next = h->gam_next;
+  p.gcl = h->sw_gcl;
+  p.cnt = h->sw_cnt;
+  p.dbg = h->dbg;
+  p.cdf_elems = ts_cdf_elems(h, n);
+  const size_t smem = sw_smem_bytes(h->N, h->R, p.cdf_elems, sizeof(T));
+  static bool attr_set = false;
+  if (!attr_set) {
+    allow_max_dyn_smem(k_sample_wide<T>);
+    attr_set = true;
+  }
+  const int64_t ctas = ceil_div(ceil_div(h->bmax[n], kSWFibers), kSWCluster) * kSWCluster;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)ctas, 1, 1);
+  lc.blockDim = dim3(kWThreads, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = h->ls;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kSWCluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_sample_wide<T>, p);
+  h->launches++;
+  if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_sample_wide launch (smem %zu): %s", smem, cudaGetErrorString(e));
+  return check_launch(h, "k_sample_wide");
 }
 
 // the batch of mode n at the current r into the prefetch buffers (k_sample [+ k_zw_gamma])
 cp_status launch_prefetch(cp_sgd_s* h, int n) {
-  cp_status st = launch_sample(h, n, h->iter_dev, h->idx, h->w, h->beff, true);
-  if (st || !wide_mode(h, n)) return st;
-  return h->dtype == CP_F64 ? launch_zw_gamma_t<double>(h, n) : launch_zw_gamma_t<float>(h, n);
+  if (wide_mode(h, n)) return h->dtype == CP_F64 ? launch_sw_t<double>(h, n) : launch_sw_t<float>(h, n);
+  return launch_sample(h, n, h->iter_dev, h->idx, h->w, h->beff, true);
 }
 
 // ---- persistent single-cluster sweep kernel (fused.cuh) ----------------------------------------
@@ -927,10 +945,14 @@ cp_status phase0(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
 
 // update (+ table + next batch when the rows are all local)
 cp_status phase1(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, int next_mode) {
-  if (wide_mode(h, n)) {  // table of the updated A^(n) + the next batch (+ its zw rows and Gamma)
-    cp_status st = h->dtype == CP_F64 ? launch_ts_t<double>(h, n, next_mode, alpha, alpha_dev)
-                                      : launch_ts_t<float>(h, n, next_mode, alpha, alpha_dev);
-    if (!st && next_mode >= 0) h->pref_mode = next_mode;
+  if (wide_mode(h, n)) {  // update, table of the updated A^(n), the next batch (+ its zw rows and Gamma)
+    const bool f64 = h->dtype == CP_F64;
+    cp_status st = f64 ? launch_uw_t<double>(h, n, alpha, alpha_dev) : launch_uw_t<float>(h, n, alpha, alpha_dev);
+    if (!st) st = f64 ? launch_tw_t<double>(h, n) : launch_tw_t<float>(h, n);
+    if (!st && next_mode >= 0) {
+      st = launch_prefetch(h, next_mode);
+      if (!st) h->pref_mode = next_mode;
+    }
     return st;
   }
   const bool last_sharded = sharded(h) && n == h->N - 1;
@@ -1256,10 +1278,9 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
         cdfmax = std::max(cdfmax, ts_cdf_elems(h, k));
       }
       const int CU = ut_cluster(h->dims[n]);
-      const size_t us = ts_layout(h->N, h->R, ceil_div(ceil_div(h->dims[n], CU), 4) * 4, ceil_div(bmx, CU), cdfmax,
-                                  h->esz).total;
-      const size_t zs = zg_scratch_bytes(h->R, h->esz, 256);
-      if (gs + 1024 <= (size_t)optin && us <= (size_t)h->sample_smem && zs <= (size_t)h->sample_smem) {
+      const size_t us = std::max(tw_smem_bytes(h->R, ceil_div(h->dims[n], CU)),
+                                 sw_smem_bytes(h->N, h->R, cdfmax, h->esz));
+      if (gs + 1024 <= (size_t)optin && us <= (size_t)h->sample_smem) {
         h->gu_ck[n] = (int)CK;
         h->gu_kb[n] = KB;
         mpart = std::max(mpart, nt * CK * kGUTI * h->R);
@@ -1267,6 +1288,14 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       }
     }
     if (any) {
+      const int P = h->R * (h->R + 1) / 2;
+      ALLOC(h->uw_gpart, sizeof(double) * ceil_div(Imax, kUWRows) * P);
+      ALLOC(h->uw_rownorm, sizeof(double) * Imax);
+      int64_t ncl = 0;
+      for (int n = 0; n < h->N; ++n) ncl = std::max(ncl, ceil_div(ceil_div(h->bmax[n], kSWFibers), kSWCluster));
+      ALLOC(h->sw_gcl, h->esz * ncl * h->R * h->R);
+      ALLOC(h->sw_cnt, sizeof(unsigned));
+      cudaMemsetAsync(h->sw_cnt, 0, sizeof(unsigned), h->stream);
       ALLOC(h->Mpart, h->esz * mpart);
       ALLOC(h->gu_cnt, sizeof(unsigned) * ceil_div(Imax, kGUTI));
       cudaMemsetAsync(h->gu_cnt, 0, sizeof(unsigned) * ceil_div(Imax, kGUTI), h->stream);
@@ -1381,6 +1410,10 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->zlo);
   cudaFree(h->Mpart);
   cudaFree(h->gu_cnt);
+  cudaFree(h->uw_gpart);
+  cudaFree(h->uw_rownorm);
+  cudaFree(h->sw_gcl);
+  cudaFree(h->sw_cnt);
   cudaFree(h->iter_dev);
   cudaFree(h->iter_tmp);
   cudaFree(h->status_dev);

@@ -534,117 +534,13 @@ __device__ __forceinline__ void skr_rows(const SampleParams& p, int64_t b0, int6
   }
 }
 
-// ------------------------------------------------------------------------------------------
-// (a6 prologue, moved to the sampler) for rows [b0, b1) of the batch just drawn:
-//   zw_b = w_b z_b (eq:gradient1/2 weights applied to the SKR row), zero padded to RP = ceil8(R)
-//   and zero for padding rows (fbase < 0) -> p.zwp [B_max][RP], the operand k_gather_update streams;
-//   Gamma_q = sum_b zw_b z_b^T over these rows (R x R, this CTA's share of Z_F^T diag(w) Z_F).
-// Threads own 4x4 blocks (bi <= bj) of Gamma; G fiber groups split the rows; groups are summed
-// in order.  Returns Gamma_q (R x R, row-major) in shared memory (inside `scratch`).
-// ------------------------------------------------------------------------------------------
-constexpr int kZGCh = 32;  // rows staged per chunk
+// weighted SKR rows zw_b = w_b z_b are stored padded to RP = ceil8(R) columns (zero past R and for
+// padding rows); Gamma partials use 4x4 blocks (bi <= bj) with up to 4 fiber groups summed in order
 __host__ __device__ inline int zg_rp(int R) { return (R + 7) / 8 * 8; }
 __host__ __device__ inline int zg_groups(int R, int nthreads) {
   const int nb = (R + 3) / 4, nblk = nb * (nb + 1) / 2;
   const int g = nthreads / nblk;
   return g < 1 ? 1 : (g > 4 ? 4 : g);
-}
-__host__ __device__ inline size_t zg_scratch_bytes(int R, size_t esz, int nthreads) {
-  return esz * (2 * (size_t)kZGCh * zg_rp(R) + (size_t)zg_groups(R, nthreads) * R * R) + 32;
-}
-
-template <typename T>
-__device__ T* zw_gamma_rows(const SampleParams& p, int64_t b0, int64_t b1, unsigned char* scratch, int tid, int nth) {
-  const int R = p.R, RP = zg_rp(R);
-  const int nb = (R + 3) / 4, nblk = nb * (nb + 1) / 2;
-  const int G = zg_groups(R, nth);
-  T* zs = reinterpret_cast<T*>(scratch);
-  T* ws = zs + kZGCh * RP;
-  T* red = ws + kZGCh * RP;  // [G][R][R]
-  const T* Z = reinterpret_cast<const T*>(p.zrow);
-  T* zwp = reinterpret_cast<T*>(p.zwp);
-  const int g = tid / nblk, blk = tid % nblk;
-  const bool act = g < G;
-  int bi = 0, bj = 0;
-  {  // upper-triangular block index -> (bi, bj), bi <= bj
-    int rem = blk;
-    while (rem >= nb - bi) { rem -= nb - bi; ++bi; }
-    bj = bi + rem;
-  }
-  T acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[a][c] = T(0);
-  for (int64_t c0 = b0; c0 < b1; c0 += kZGCh) {
-    const int nch = (int)cmin64(kZGCh, b1 - c0);
-    for (int e = tid; e < kZGCh * RP; e += nth) {
-      const int kk = e / RP, r = e % RP;
-      const int64_t b = c0 + kk;
-      T z = T(0), zw = T(0);
-      if (kk < nch && r < R && p.fbase[b] >= 0) {
-        z = Z[b * R + r];
-        zw = (T)p.w[b] * z;
-      }
-      zs[e] = z;
-      ws[e] = zw;
-      if (kk < nch) zwp[b * RP + r] = zw;
-      if constexpr (sizeof(T) == 4) {
-        if (p.zhi && kk < nch && r < R) write_zw_images(p, b, r, (float)zw);
-      }
-    }
-    __syncthreads();
-    if (act) {
-      for (int kk = g; kk < nch; kk += G) {
-        T x[4], y[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          x[a] = ws[kk * RP + 4 * bi + a];
-          y[a] = zs[kk * RP + 4 * bj + a];
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) acc[a][c] = fma(x[a], y[c], acc[a][c]);
-      }
-    }
-    __syncthreads();
-  }
-  if (act) {
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int r1 = 4 * bi + a, r2 = 4 * bj + c;
-        if (r1 < R && r2 < R) {
-          red[(g * R + r1) * R + r2] = acc[a][c];
-          if (bi != bj) red[(g * R + r2) * R + r1] = acc[a][c];
-        }
-      }
-  }
-  __syncthreads();
-  for (int e = tid; e < R * R; e += nth) {
-    T s = red[e];
-    for (int gg = 1; gg < G; ++gg) s += red[gg * R * R + e];
-    red[e] = s;
-  }
-  __syncthreads();
-  return red;
-}
-
-// rank-ordered cluster sum of every CTA's Gamma_q (same shared offset in each CTA) -> out (global)
-template <typename T>
-__device__ void gamma_cluster_reduce(const cooperative_groups::cluster_group& cl, T* red, int R, T* out, int tid,
-                                     int nth) {
-  const int CU = (int)cl.num_blocks(), q = (int)cl.block_rank();
-  cl.sync();
-  const int E = R * R, per = (E + CU - 1) / CU;
-  for (int e = q * per + tid; e < min(E, (q + 1) * per); e += nth) {
-    T s = T(0);
-    for (int qq = 0; qq < CU; ++qq) s += cl.map_shared_rank(red, qq)[e];
-    out[e] = s;
-  }
-  cl.sync();  // peers done reading this CTA's shared memory
 }
 
 // (a2, a3[, a4]) standalone sampler (API calls and the first step of a call).  grid-stride rows.
@@ -666,18 +562,6 @@ __global__ void __launch_bounds__(256) k_sample(SampleParams p) {
     __syncthreads();
     skr_rows<T>(p, b0, b1, threadIdx.x, blockDim.x);
   }
-}
-
-// wide path after k_sample: zw rows and Gamma of the whole batch, one cluster of CU CTAs
-template <typename T>
-__global__ void __launch_bounds__(256) k_zw_gamma(SampleParams p) {
-  extern __shared__ __align__(16) unsigned char zg_sm[];
-  cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
-  const int CU = (int)cl.num_blocks(), q = (int)cl.block_rank();
-  const int64_t per = (p.bmax + CU - 1) / CU;
-  const int64_t b0 = min((int64_t)q * per, p.bmax), b1 = min(b0 + per, p.bmax);
-  T* red = zw_gamma_rows<T>(p, b0, b1, zg_sm, threadIdx.x, blockDim.x);
-  gamma_cluster_reduce<T>(cl, red, p.R, reinterpret_cast<T*>(p.gam_next), threadIdx.x, blockDim.x);
 }
 
 // ==========================================================================================
@@ -915,86 +799,12 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Symmetric sweep (Gauss-Jordan on the SPD Gram in natural pivot order; a pivot whose Schur
-// diagonal is <= tol is skipped -- reading R4(b)), register-blocked: thread t < nb^2 (nb =
-// ceil(R/4)) keeps the 4x4 block (t / nb, t % nb) of the R x R matrix in registers.  Sweeping
-// pivot k maps M_ij -= M_ik (M_kj / d) (i, j != k), M_kj /= d, M_ik /= d, M_kk = -1/d (d = M_kk);
-// the pivot row (= column, by symmetry) is published through a double-buffered shared row, so a
-// pivot costs 8 shared loads, 4 DMUL, 16 DFMA and ONE named barrier over the ceil(nb^2/32)
-// participating warps (one warp for R <= 20).  Called by every thread of the CTA.  On exit Gm
-// (stride R+1) holds W = (G_SS)^{-1} on the swept set S and 0 elsewhere; returns |S|.
-__device__ int blk_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /* 2*64 */, int* swept /* R */) {
-  const int tid = threadIdx.x, RS = R + 1;
-  const int nb = (R + 3) >> 2, nact = nb * nb;
-  const int nthr = ((nact + 31) >> 5) << 5;
-  if (tid < nthr) {
-    const bool act = tid < nact;
-    const int bi = act ? tid / nb : -1, bj = act ? tid % nb : -1;
-    const int i0 = 4 * (act ? bi : 0), j0 = 4 * (act ? bj : 0);
-    double v[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        v[a][c] = (act && i0 + a < R && j0 + c < R) ? Gm[(i0 + a) * RS + j0 + c] : 0.0;
-    if (bi == 0)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) rowbuf[j0 + c] = v[0][c];  // row 0 (zero past R)
-    for (int j = tid; j < R; j += nthr) swept[j] = 0;
-    named_bar_sync(1, nthr);
-    for (int k = 0; k < R; ++k) {
-      const double* rk = rowbuf + (k & 1) * 64;
-      double* rn = rowbuf + ((k + 1) & 1) * 64;
-      const double d = rk[k];
-      if (d > tol) {  // uniform across the participating threads
-        const double dinv = __drcp_rn(d);
-        const double2 ri01 = *reinterpret_cast<const double2*>(rk + i0);
-        const double2 ri23 = *reinterpret_cast<const double2*>(rk + i0 + 2);
-        const double2 rj01 = *reinterpret_cast<const double2*>(rk + j0);
-        const double2 rj23 = *reinterpret_cast<const double2*>(rk + j0 + 2);
-        const double ri[4] = {ri01.x, ri01.y, ri23.x, ri23.y};
-        const double f[4] = {rj01.x * dinv, rj01.y * dinv, rj23.x * dinv, rj23.y * dinv};
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) v[a][c] = fma(-ri[a], f[c], v[a][c]);
-        const int kb = k >> 2, ks = k & 3;
-        if (bi == kb)  // row k: M_kj / d
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) v[a][c] = (a == ks) ? f[c] : v[a][c];
-        if (bj == kb)  // column k: M_ik / d, and M_kk = -1/d
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-              v[a][c] = (c == ks) ? ((bi == kb && a == ks) ? -dinv : ri[a] * dinv) : v[a][c];
-        if (tid == 0) swept[k] = 1;
-      }
-      if (k + 1 < R && bi == ((k + 1) >> 2)) {  // publish row k+1 for the next pivot
-        const int a = (k + 1) & 3;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) rn[j0 + c] = a == 0 ? v[0][c] : a == 1 ? v[1][c] : a == 2 ? v[2][c] : v[3][c];
-      }
-      named_bar_sync(1, nthr);
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int i = i0 + a, j = j0 + c;
-        if (act && i < R && j < R) Gm[i * RS + j] = (swept[i] && swept[j]) ? -v[a][c] : 0.0;
-      }
-  }
-  __syncthreads();
-  int rank = 0;
-  for (int j = 0; j < R; ++j) rank += swept[j];
-  return rank;
-}
-
-
-// Same sweep, lane per column: thread c < RMAX (RMAX = ceil8(R) <= 64, warps 0..RMAX/32) keeps
+// Inverse of the fp64 Gram on its numerically full-rank pivot set S by the symmetric sweep
+// operator (Gauss-Jordan with diagonal pivoting in natural order, Goodnight 1979): sweeping pivot k
+// maps M_ij -= M_ik M_kj / d (i, j != k), M_ik, M_kj /= d, M_kk = -1/d (d = M_kk).  The unswept
+// diagonal is the Schur-complement diagonal, so a pivot whose value is <= tol is skipped (reading
+// R4(b), the rank rule of a pivoted Cholesky); after sweeping S, M_SS = -(G_SS)^{-1}.
+// Lane per column: thread c < RMAX (RMAX = ceil8(R) <= 64, warps 0..RMAX/32) keeps
 // column c of the RMAX x RMAX matrix (identity past R) in registers, rows in ROTATED order: before
 // pivot k slot t holds row (k + t) mod RMAX, so the pivot row is always slot 0 and every register
 // index is static.  Pivot k:
@@ -1075,169 +885,6 @@ __device__ inline int lc_sweep_dispatch(double* Gm, int R, double tol, double* c
     }
   }
   return 0;
-}
-
-// Same sweep, four pivots per barrier.  Sweep operators on distinct pivots commute and compose:
-// sweeping the pivot block K = {4kb..4kb+3} one pivot at a time (with the R4(b) skip rule) equals
-// one block sweep with S = swept subset of K, U = K \ S, H = (M_SS)^{-1}:
-//   M_IJ -= M_IS H M_SJ,  M_IS <- M_IS H,  M_SJ <- H M_SJ,  M_IU -= M_IS H M_SU,  M_KK <- sweep_S(M_KK).
-// The 4x4 diagonal block D = M_KK is swept sequentially (skip rule on its Schur diagonals, which
-// are exactly those of the one-at-a-time sweep) by every thread redundantly, giving D' and
-// Q = -D' with the U columns zeroed (Q_SS = H).  A thread owning block (bi, bj) then needs only
-// C_i = M_{i,K} and C_j = M_{j,K} (= M_{K,j}) of its rows/columns, published once per block step:
-//   bi, bj != kb : v -= (C_i Hm) C_j^T              (Hm = Q with the U rows zeroed)
-//   bi == kb     : v[a][c] = [a in U] v[a][c] + sum_s Q[a][s] C_j[c][s]
-//   bj == kb     : v[a][c] = [c in U] v[a][c] + sum_s C_i[a][s] Q[c][s]
-//   both         : v = D'
-// ceil(R/4) barriers instead of R; called by every thread of the CTA; returns |S|.
-__device__ int blk4_sweep_inverse(double* Gm, int R, double tol, double* colbuf /* 2*64*4 */, int* swept /* R */) {
-  const int tid = threadIdx.x, RS = R + 1;
-  const int nb = (R + 3) >> 2, nact = nb * nb;
-  const int nthr = ((nact + 31) >> 5) << 5;
-  if (tid < nthr) {
-    const bool act = tid < nact;
-    const int bi = act ? tid / nb : -1, bj = act ? tid % nb : -1;
-    const int i0 = 4 * (act ? bi : 0), j0 = 4 * (act ? bj : 0);
-    double v[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        v[a][c] = (act && i0 + a < R && j0 + c < R) ? Gm[(i0 + a) * RS + j0 + c] : 0.0;
-    // column block 0: colbuf[par][row][4]
-    if (bj == 0)
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        double2* d = reinterpret_cast<double2*>(colbuf + (i0 + a) * 4);
-        d[0] = make_double2(v[a][0], v[a][1]);
-        d[1] = make_double2(v[a][2], v[a][3]);
-      }
-    for (int j = tid; j < R; j += nthr) swept[j] = 0;
-    named_bar_sync(1, nthr);
-    for (int kb = 0; kb < nb; ++kb) {
-      const double* cb = colbuf + (kb & 1) * 256;
-      double* cn = colbuf + ((kb + 1) & 1) * 256;
-      const int k0 = 4 * kb;
-      // D = M_KK, swept one pivot at a time (every thread, identical arithmetic)
-      double D[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const double2 x = *reinterpret_cast<const double2*>(cb + (k0 + a) * 4);
-        const double2 y = *reinterpret_cast<const double2*>(cb + (k0 + a) * 4 + 2);
-        D[a][0] = x.x; D[a][1] = x.y; D[a][2] = y.x; D[a][3] = y.y;
-      }
-      bool piv[4];
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const double d = D[s][s];
-        piv[s] = (k0 + s < R) && d > tol;
-        if (piv[s]) {
-          const double dinv = __drcp_rn(d);
-          double col[4], row[4];
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            col[a] = D[a][s];
-            row[a] = D[s][a] * dinv;
-          }
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              double nv = fma(-col[a], row[c], D[a][c]);
-              nv = (a == s) ? row[c] : nv;
-              nv = (c == s) ? col[a] * dinv : nv;
-              D[a][c] = (a == s && c == s) ? -dinv : nv;
-            }
-        }
-      }
-      double Q[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) Q[a][c] = piv[c] ? -D[a][c] : 0.0;
-      if (tid == 0)
-#pragma unroll
-        for (int s = 0; s < 4; ++s)
-          if (k0 + s < R) swept[k0 + s] = piv[s] ? 1 : 0;
-      if (act) {
-        double Ci[4][4], Cj[4][4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const double2 x = *reinterpret_cast<const double2*>(cb + (i0 + a) * 4);
-          const double2 y = *reinterpret_cast<const double2*>(cb + (i0 + a) * 4 + 2);
-          Ci[a][0] = x.x; Ci[a][1] = x.y; Ci[a][2] = y.x; Ci[a][3] = y.y;
-          const double2 z = *reinterpret_cast<const double2*>(cb + (j0 + a) * 4);
-          const double2 w = *reinterpret_cast<const double2*>(cb + (j0 + a) * 4 + 2);
-          Cj[a][0] = z.x; Cj[a][1] = z.y; Cj[a][2] = w.x; Cj[a][3] = w.y;
-        }
-        if (bi != kb && bj != kb) {
-          double X[4][4];  // X = C_i Hm
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-              double t = 0.0;
-#pragma unroll
-              for (int u = 0; u < 4; ++u) t = fma(Ci[a][u], piv[u] ? Q[u][s] : 0.0, t);
-              X[a][s] = t;
-            }
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              double t = v[a][c];
-#pragma unroll
-              for (int s = 0; s < 4; ++s) t = fma(-X[a][s], Cj[c][s], t);
-              v[a][c] = t;
-            }
-        } else if (bi == kb && bj != kb) {
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              double t = piv[a] ? 0.0 : v[a][c];
-#pragma unroll
-              for (int s = 0; s < 4; ++s) t = fma(Q[a][s], Cj[c][s], t);
-              v[a][c] = t;
-            }
-        } else if (bj == kb && bi != kb) {
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              double t = piv[c] ? 0.0 : v[a][c];
-#pragma unroll
-              for (int s = 0; s < 4; ++s) t = fma(Ci[a][s], Q[c][s], t);
-              v[a][c] = t;
-            }
-        } else {
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) v[a][c] = D[a][c];
-        }
-        if (bj == kb + 1)  // publish the next column block
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            double2* d = reinterpret_cast<double2*>(cn + (i0 + a) * 4);
-            d[0] = make_double2(v[a][0], v[a][1]);
-            d[1] = make_double2(v[a][2], v[a][3]);
-          }
-      }
-      named_bar_sync(1, nthr);
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int i = i0 + a, j = j0 + c;
-        if (act && i < R && j < R) Gm[i * RS + j] = (swept[i] && swept[j]) ? -v[a][c] : 0.0;
-      }
-  }
-  __syncthreads();
-  int rank = 0;
-  for (int j = 0; j < R; ++j) rank += swept[j];
-  return rank;
 }
 
 // Pivoted variant (largest remaining Schur diagonal first, as a pivoted Cholesky would) for

@@ -71,7 +71,11 @@ elif os.environ.get("CPSGD_DEBUG_TIMERS"):
               "| last CTA = chunk", t[60], ": reduce", t[41] - (t[40] if t[60] == 0 else t[48]), "update", t[42] - t[41])
         print("  stage 8: load issue->data", t[18] - t[23], "wait xh/xl", t[19] - t[18], "split", t[20] - t[19],
               "split->mma start", t[21] - t[20], "mma issue", t[22] - t[21])
-    if a.wide:  # k_table_sample marks
+    if t[107]:
+        nm = ["cdf stage", "draw", "skr", "zw/img", "gamma", "cluster+fence", "last"]
+        print("k_sample_wide (CTA 0) cycles: " + " | ".join(f"{nm[i]} {t[101 + i] - t[100 + i]}" for i in range(7)))
+        print("k_table_wide cycles: gram-sum", t[1] - t[0], "sweep", t[2] - t[1], "scores", t[3] - t[2], "scan", t[4] - t[3])
+    if a.wide and not t[107]:  # k_table_sample marks
         names = ["gram+sync", "sweep", "scores", "scan+cdf", "draw", "skr+zw+gamma"]
         print("k_table_sample cycles: " + " | ".join(f"{names[i]} {t[i + 1] - t[i]}" for i in range(6)),
               "| total", t[6] - t[0])
