@@ -709,8 +709,21 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
     allow_max_dyn_smem(k_update_wide<T>);
     attr_set = true;
   }
-  k_update_wide<T><<<(unsigned)ceil_div(h->dims[n], kUWRows), kWThreads, smem, h->ls>>>(p);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(ceil_div(ceil_div(h->dims[n], kUWRows), kUWCluster) * kUWCluster), 1, 1);
+  lc.blockDim = dim3(kWThreads, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = h->ls;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kUWCluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_update_wide<T>, p);
   h->launches++;
+  if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_update_wide launch: %s", cudaGetErrorString(e));
   return check_launch(h, "k_update_wide");
 }
 
@@ -725,7 +738,7 @@ cp_status launch_tw_t(cp_sgd_s* h, int n) {
   p.strategy = h->sampler;
   p.In = h->dims[n];
   p.rows_per = ceil_div(h->dims[n], CU);
-  p.nparts = (int)ceil_div(h->dims[n], kUWRows);
+  p.nparts = (int)ceil_div(ceil_div(h->dims[n], kUWRows), kUWCluster);  // k_update_wide clusters
   p.gpart = h->uw_gpart;
   p.rownorm = h->uw_rownorm;
   p.A = h->factors[n];
@@ -744,7 +757,7 @@ cp_status launch_tw_t(cp_sgd_s* h, int n) {
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(CU, 1, 1);
-  lc.blockDim = dim3(kWThreads, 1, 1);
+  lc.blockDim = dim3(kTWThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
   cudaLaunchAttribute at[1];

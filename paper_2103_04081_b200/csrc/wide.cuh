@@ -20,8 +20,10 @@ namespace cps {
 
 constexpr int kUWRows = 16;     // rows of A^(n) per k_update_wide CTA (divides the 128-row tiles)
 constexpr int kWThreads = 256;
+constexpr int kTWThreads = 256;  // k_table_wide (512 would cap registers at 128 and spill the sweep)
 constexpr int kSWFibers = 32;   // fibers per k_sample_wide CTA
 constexpr int kSWCluster = 8;
+constexpr int kUWCluster = 8;   // k_update_wide CTAs per cluster (table partials summed over DSMEM)
 
 template <typename T>
 struct UWParams {
@@ -37,26 +39,29 @@ struct UWParams {
   double alpha;
   const double* alpha_dev;
   double eta, b, eps;
-  double* gpart;      // [CTAs][R(R+1)/2] (leverage) or [CTAs][1] (Euclidean)
+  double* gpart;      // [clusters][R(R+1)/2] (leverage) or [clusters] (Euclidean)
   double* rownorm;    // [I_n] (Euclidean)
 };
 
 // (a6-a8) + the parallel half of (a1): grid = ceil(I_n / kUWRows); dynamic shared memory
 __host__ __device__ inline size_t uw_smem_bytes(int R, size_t esz) {
-  return esz * (3 * (size_t)kUWRows * (R + 1) + (size_t)R * R) + 16;
+  return (esz * (3 * (size_t)kUWRows * (R + 1) + (size_t)R * R) + 15) / 16 * 16 +
+         sizeof(double) * (size_t)(R * (R + 1) / 2) + 16;
 }
 template <typename T>
 __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
   constexpr int UR = kUWRows, TI = 128;
   const int R = p.R, RS = R + 1, tid = threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.x * UR;
-  const int nr = (int)cmin64(UR, p.In - r0);
+  const int nr = (int)cmax64(0, cmin64(UR, p.In - r0));  // 0 for the CTAs rounding the grid up
   extern __shared__ __align__(16) unsigned char uw_sm[];
   T* sA = reinterpret_cast<T*>(uw_sm);  // [UR][R+1] each
   T* sS = sA + UR * RS;
   T* sM = sS + UR * RS;
   T* sG = sM + UR * RS;                 // [R][R]
+  double* sgp = reinterpret_cast<double*>(uw_sm + ((sizeof(T) * (3 * UR * RS + R * R) + 15) / 16) * 16);  // [P]
   __shared__ double sred[kWThreads / 32];
+  cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
   // rows of A and S, Gamma: every request in flight at once
   for (int e = tid; e < nr * R; e += kWThreads) {
     const int il = e / R, c = e % R;
@@ -182,9 +187,22 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
         for (int c = 0; c < 4; ++c) {
           const int r1 = 4 * bi + a, r2 = 4 * bj + c;
           if (r1 < R && r2 < R && r1 <= r2)
-            p.gpart[(int64_t)blockIdx.x * P + r1 * R - r1 * (r1 - 1) / 2 + (r2 - r1)] = acc[a][c];
+            sgp[r1 * R - r1 * (r1 - 1) / 2 + (r2 - r1)] = acc[a][c];
         }
     }
+    // cluster sum (rank order) of the CTA partials -> one partial per cluster of kUWCluster CTAs
+    cluster.sync();
+    const int CU = (int)cluster.num_blocks(), q = (int)cluster.block_rank();
+    const int per = (P + CU - 1) / CU;
+    for (int pair = q * per + tid; pair < min(P, (q + 1) * per); pair += kWThreads) {
+      double v[kUWCluster], s = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < kUWCluster; ++qq) v[qq] = qq < CU ? cluster.map_shared_rank(sgp, qq)[pair] : 0.0;
+#pragma unroll
+      for (int qq = 0; qq < kUWCluster; ++qq) s += v[qq];
+      p.gpart[(int64_t)(blockIdx.x / CU) * P + pair] = s;
+    }
+    cluster.sync();
   } else if (p.strategy == 2 || p.strategy == 4) {  // Euclidean: row norms + the CTA's partial ||A||^2
     double acc = 0.0;
     for (int il = tid; il < nr; il += kWThreads) {
@@ -200,8 +218,15 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
     if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < kWThreads / 32; ++w) t += sred[w];
-      p.gpart[blockIdx.x] = t;
+      sgp[0] = t;
     }
+    cluster.sync();
+    if (cluster.block_rank() == 0 && tid == 0) {
+      double t = 0.0;
+      for (int qq = 0; qq < (int)cluster.num_blocks(); ++qq) t += cluster.map_shared_rank(sgp, qq)[0];
+      p.gpart[blockIdx.x / cluster.num_blocks()] = t;
+    }
+    cluster.sync();
   }
 }
 
@@ -231,7 +256,8 @@ __host__ __device__ inline size_t tw_smem_bytes(int R, int64_t rows_per) {
   };
   const int RD = ut_rd(R), P = R * (R + 1) / 2;
   take(sizeof(double) * rows_per * RD);      // Ad
-  take(ut_work_bytes(R, rows_per));          // W + score partials
+  const size_t wk = ut_work_bytes(R, rows_per), st = sizeof(double) * rows_per * R;
+  take(wk > st ? wk : st);                   // W + score partials | staged rows of A
   take(sizeof(double) * P);                  // this CTA's slice sums (read by peers)
   take(sizeof(double) * R * (R + 1));        // Gm
   take(sizeof(double) * 4 * kMaxRank);       // sweep buffers
@@ -260,7 +286,9 @@ __device__ void table_wide_body(const TWParams& p) {
     return ptr;
   };
   double* Ad = reinterpret_cast<double*>(carve(sizeof(double) * p.rows_per * RD));
-  double* work = reinterpret_cast<double*>(carve(ut_work_bytes(R, p.rows_per)));
+  double* work = reinterpret_cast<double*>(
+      carve(ut_work_bytes(R, p.rows_per) > sizeof(double) * p.rows_per * R ? ut_work_bytes(R, p.rows_per)
+                                                                             : sizeof(double) * p.rows_per * R));
   double* slice = reinterpret_cast<double*>(carve(sizeof(double) * P));
   double* Gm = reinterpret_cast<double*>(carve(sizeof(double) * R * (R + 1)));
   double* colbuf = reinterpret_cast<double*>(carve(sizeof(double) * 4 * kMaxRank));
@@ -269,23 +297,22 @@ __device__ void table_wide_body(const TWParams& p) {
   unsigned long long* qrow = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * p.rows_per));
   unsigned long long* qtot = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * 2));
   __shared__ int s_bad;
-  __shared__ double s_red[kWThreads / 32];
-  __shared__ unsigned long long s_wtot[kWThreads / 32];
+  __shared__ double s_red[kTWThreads / 32];
+  __shared__ unsigned long long s_wtot[kTWThreads / 32];
   __shared__ double s_tol, s_fro;
   if (tid == 0) s_bad = 0;
   const bool lev = (p.strategy == 1 || p.strategy == 3);
   const T* A = reinterpret_cast<const T*>(p.A);
   if (p.dbg && q == 0 && tid == 0) p.dbg[0] = clock64();
   if (lev) {
-    // rows of the new A^(n) for the scores (fp64, zero padded to RD)
-#pragma unroll 8
-    for (int e = tid; e < nr * RD; e += kWThreads) {
-      const int il = e / RD, c = e % RD;
-      Ad[e] = c < R ? (double)A[(r_beg + il) * R + c] : 0.0;
-    }
+    // rows of the new A^(n) for the scores: cp.async into the work area (all requests in flight,
+    // overlapped with the slice sums), then fp64 (zero padded to RD)
+    T* Ast = reinterpret_cast<T*>(work);
+    for (int e = tid; e < nr * R; e += kTWThreads) cp_async_small<sizeof(T)>(Ast + e, A + r_beg * R + e, sizeof(T));
+    cp_async_commit();
     // pair slice of this CTA: sum of the k_update_wide partials in CTA order
     const int per = (P + CU - 1) / CU, pb = q * per, pe = min(P, pb + per);
-    for (int pair = pb + tid; pair < pe; pair += kWThreads) {
+    for (int pair = pb + tid; pair < pe; pair += kTWThreads) {
       double v[8], s = 0.0;
       for (int c0 = 0; c0 < p.nparts; c0 += 8) {
 #pragma unroll
@@ -295,8 +322,14 @@ __device__ void table_wide_body(const TWParams& p) {
       }
       slice[pair - pb] = s;
     }
-    cluster.sync();  // #1 slices visible
-    for (int pair = tid; pair < P; pair += kWThreads) {
+    cp_async_wait<0>();
+    __syncthreads();
+    for (int e = tid; e < nr * RD; e += kTWThreads) {
+      const int il = e / RD, c = e % RD;
+      Ad[e] = c < R ? (double)Ast[il * R + c] : 0.0;
+    }
+    cluster.sync();  // #1 slices visible (and Ad complete; the work area is free again)
+    for (int pair = tid; pair < P; pair += kTWThreads) {
       const int owner = pair / per;
       const double sum = cluster.map_shared_rank(slice, owner)[pair - owner * per];
       int r1 = 0, rem = pair;
@@ -321,7 +354,7 @@ __device__ void table_wide_body(const TWParams& p) {
     }
     __syncthreads();
     if (p.dbg && q == 0 && tid == 0) p.dbg[1] = clock64();
-    constexpr int EPT = (kMaxRank * kMaxRank + kWThreads - 1) / kWThreads;
+    constexpr int EPT = (kMaxRank * kMaxRank + kTWThreads - 1) / kTWThreads;
     const int rank = (p.In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, s_tol, colbuf, swept, colbuf + R)
                                     : lc_sweep_dispatch(Gm, R, s_tol, colbuf, swept);
     if (tid == 0 && rank == 0) s_bad |= 2;
@@ -329,13 +362,13 @@ __device__ void table_wide_body(const TWParams& p) {
     // scores l_i = sum_c (A W)_ic a_ic (4 rows x 4 columns per task; k in pairs)
     double* Wd = work;
     double* sc = work + R * RD;  // [nb4][rows_per]
-    for (int e = tid; e < R * RD; e += kWThreads) {
+    for (int e = tid; e < R * RD; e += kTWThreads) {
       const int r1 = e / RD, c = e % RD;
       Wd[e] = c < R ? Gm[r1 * RS + c] : 0.0;
     }
     __syncthreads();
     const int nrg = (nr + 3) >> 2, ntask = nrg * nb4;
-    for (int t = tid; t < ntask; t += kWThreads) {
+    for (int t = tid; t < ntask; t += kTWThreads) {
       const int rg = t / nb4, cg2 = t % nb4;
       const int il0 = 4 * rg;
       double acc[4][4];
@@ -371,7 +404,7 @@ __device__ void table_wide_body(const TWParams& p) {
       }
     }
     __syncthreads();
-    for (int il = tid; il < nr; il += kWThreads) {
+    for (int il = tid; il < nr; il += kTWThreads) {
       double l = 0.0;
       for (int cg2 = 0; cg2 < nb4; ++cg2) l += sc[cg2 * p.rows_per + il];
       prow[il] = rank > 0 ? fmax(l, 0.0) / (double)rank : 0.0;
@@ -386,13 +419,13 @@ __device__ void table_wide_body(const TWParams& p) {
     }
     __syncthreads();
     const double fro = s_fro;
-    for (int il = tid; il < nr; il += kWThreads) prow[il] = fro > 0.0 ? __ldcg(p.rownorm + r_beg + il) / fro : 0.0;
+    for (int il = tid; il < nr; il += kTWThreads) prow[il] = fro > 0.0 ? __ldcg(p.rownorm + r_beg + il) / fro : 0.0;
     cluster.sync();  // #1 (matches the leverage branch)
   }
   __syncthreads();
   if (p.dbg && q == 0 && tid == 0) p.dbg[3] = clock64();
   // quantise + CTA scan (contiguous segment per thread) + DSMEM prefix of the lower ranks
-  const int seg = (nr + kWThreads - 1) / kWThreads;
+  const int seg = (nr + kTWThreads - 1) / kTWThreads;
   const int a0 = min(tid * seg, nr), a1 = min(a0 + seg, nr);
   unsigned long long local = 0;
   int bad = 0;
@@ -421,7 +454,7 @@ __device__ void table_wide_body(const TWParams& p) {
   unsigned long long wpre = 0;
   for (int w = 0; w < wid; ++w) wpre += s_wtot[w];
   const unsigned long long seg_pre = wpre + incl - local;
-  if (tid == kWThreads - 1) qtot[0] = seg_pre + local;
+  if (tid == kTWThreads - 1) qtot[0] = seg_pre + local;
   cluster.sync();  // #2 CTA totals visible
   unsigned long long cta_pre = 0, total = 0;
   for (int qq = 0; qq < CU; ++qq) {
@@ -442,7 +475,7 @@ __device__ void table_wide_body(const TWParams& p) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kWThreads, 1) k_table_wide(TWParams p) {
+__global__ void __launch_bounds__(kTWThreads, 1) k_table_wide(TWParams p) {
   table_wide_body<T>(p);
 }
 
@@ -498,6 +531,8 @@ __global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
   __shared__ const uint64_t* s_cp[kMaxOrder];
   __shared__ int s_last;
   SWM(0);
+  long long gt0 = 0;
+  if (P.dbg && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
   {
     int64_t o = 0;
     for (int k = 0; k < N; ++k) {
@@ -516,7 +551,53 @@ __global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
 
   const int64_t b0 = cmin64((int64_t)blockIdx.x * kSWFibers, sp.bmax), b1 = cmin64(b0 + kSWFibers, sp.bmax);
   const int nf = (int)(b1 - b0);
-  draw_rows(sp, s_cp, r_now, b0, b1, tid, kWThreads, sidx, sw);
+  if (sp.strategy == 3 || sp.strategy == 4) {
+    draw_rows(sp, s_cp, r_now, b0, b1, tid, kWThreads, sidx, sw);
+  } else {
+    // row-wise draws (eq:ik, R8): one thread per (fiber, position) -- the N-1 draws of a fiber run
+    // in parallel -- then per fiber the exact weight (DESIGN.md section 4 order) and the offset
+    double* spt = reinterpret_cast<double*>(zs);  // [kSWFibers][N-1] realised probabilities (scratch)
+    for (int e = tid; e < nf * NP; e += kWThreads) {
+      const int lb = e / NP, pos = e % NP;
+      const int k = pos < sp.n ? pos : pos + 1;
+      const uint64_t Tk = sp.strategy == 0 ? (uint64_t)sp.dims[k] : sp.Ttot[k];
+      const uint64_t rr = scale_draw(draw_word(sp.seed, r_now, (uint32_t)(b0 + lb), kPurposeRow, (uint32_t)pos), Tk);
+      int64_t i;
+      uint64_t qk;
+      if (sp.strategy == 0) {
+        i = (int64_t)rr;
+        qk = 1;
+      } else {
+        const uint64_t* c = s_cp[k];
+        i = upper_bound_u64(c, sp.dims[k], rr);
+        qk = c[i] - (i > 0 ? c[i - 1] : 0ull);
+      }
+      sidx[e] = (int32_t)i;
+      spt[e] = __ddiv_rn((double)((uint64_t)sp.dims[k] * qk), (double)Tk);
+    }
+    __syncthreads();
+    if (b0 == 0 && tid == 0) *sp.beff = sp.B;
+    for (int lb = tid; lb < nf; lb += kWThreads) {
+      const int64_t b = b0 + lb;
+      double prod = spt[lb * NP];
+      for (int pos = 1; pos < NP; ++pos) prod = __dmul_rn(prod, spt[lb * NP + pos]);
+      const double wv = __ddiv_rn(1.0, __dmul_rn((double)sp.B, prod));
+      sw[lb] = wv;
+      sp.w[b] = wv;
+      int64_t offn = 0, jrow = 0, jmul = 1;
+      int pos = 0;
+      for (int k = 0; k < N; ++k) {
+        if (k == sp.n) continue;
+        const int64_t ik = sidx[lb * NP + pos];
+        sp.idx[b * NP + pos] = (int32_t)ik;
+        ++pos;
+        offn += ik * sp.lstride[k];
+        jrow += ik * jmul;
+        jmul *= sp.ldims[k];
+      }
+      sp.fbase[b] = sp.mode_major ? jrow * sp.pitch : offn;
+    }
+  }
   __syncthreads();
   SWM(2);
   // SKR rows (Alg. 1): z[lb][r] = prod_{k != n, ascending} A^(k)(i_k, r); every
@@ -550,16 +631,20 @@ __global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
   }
   __syncthreads();
   SWM(3);
-  // weighted rows for the gather kernel; tcgen05 B images
+  // weighted rows for the FFMA gather kernel (row-contiguous) and the tcgen05 B images (per column
+  // r one 128-byte row of the 32 fibers: lanes run over fibers, coalesced)
   {
     T* zwp = reinterpret_cast<T*>(sp.zwp);
     for (int e = tid; e < nf * RP; e += kWThreads) {
       const int lb = e / RP, r = e % RP;
-      const T zw = (T)sw[lb] * zs[e];
-      zwp[(b0 + lb) * RP + r] = zw;
-      if constexpr (sizeof(T) == 4) {
-        if (sp.zhi && r < R) write_zw_images(sp, b0 + lb, r, (float)zw);
-      }
+      zwp[(b0 + lb) * RP + r] = (T)sw[lb] * zs[e];
+    }
+    if constexpr (sizeof(T) == 4) {
+      if (sp.zhi)
+        for (int e = tid; e < R * kSWFibers; e += kWThreads) {
+          const int r = e / kSWFibers, lb = e % kSWFibers;
+          if (lb < nf) write_zw_images(sp, b0 + lb, r, (float)((T)sw[lb] * zs[lb * RP + r]));
+        }
     }
   }
   SWM(4);
@@ -623,28 +708,33 @@ __global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
   }
   SWM(6);
   __threadfence();
-  cluster.sync();  // the whole cluster partial is written (and peers are done with our shared memory)
-  if (q == 0) {
-    if (tid == 0) s_last = (atomicAdd(P.cnt, 1u) == (unsigned)(ncl - 1));
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      T* out = reinterpret_cast<T*>(sp.gam_next);
-      const int E = R * R;
-      for (int e = tid; e < E; e += kWThreads) {
-        T v[8], s = T(0);
-        for (int c0 = 0; c0 < ncl; c0 += 8) {
+  cluster.sync();  // the whole cluster partial is written
+  if (q == 0 && tid == 0) s_last = (atomicAdd(P.cnt, 1u) == (unsigned)(ncl - 1));
+  cluster.sync();
+  if (*cluster.map_shared_rank(&s_last, 0)) {  // this cluster arrived last: its CTAs sum all partials
+    __threadfence();
+    T* out = reinterpret_cast<T*>(sp.gam_next);
+    const int E = R * R, per = (E + CU - 1) / CU;
+    for (int e = q * per + tid; e < min(E, (q + 1) * per); e += kWThreads) {
+      T v[16], s = T(0);
+      for (int c0 = 0; c0 < ncl; c0 += 16) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) v[k] = (c0 + k < ncl) ? __ldcg(gcl + (int64_t)(c0 + k) * E + e) : T(0);
+        for (int k = 0; k < 16; ++k) v[k] = (c0 + k < ncl) ? __ldcg(gcl + (int64_t)(c0 + k) * E + e) : T(0);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) s += v[k];
-        }
-        out[e] = s;
+        for (int k = 0; k < 16; ++k) s += v[k];  // cluster order; zeros past ncl are exact
       }
-      if (tid == 0) *P.cnt = 0u;
+      out[e] = s;
     }
+    if (q == 0 && tid == 0) *P.cnt = 0u;
   }
+  cluster.sync();  // rank 0's s_last read by the peers before it exits
   SWM(7);
+  if (P.dbg && tid == 0 && blockIdx.x < 480) {
+    long long gt1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+    P.dbg[2048 + 2 * blockIdx.x] = gt0;
+    P.dbg[2049 + 2 * blockIdx.x] = gt1;
+  }
 }
 
 }  // namespace cps

@@ -74,6 +74,12 @@ elif os.environ.get("CPSGD_DEBUG_TIMERS"):
     if t[107]:
         nm = ["cdf stage", "draw", "skr", "zw/img", "gamma", "cluster+fence", "last"]
         print("k_sample_wide (CTA 0) cycles: " + " | ".join(f"{nm[i]} {t[101 + i] - t[100 + i]}" for i in range(7)))
+        import numpy as np
+        g0 = np.array(t[2048:3008:2]); g1 = np.array(t[2049:3008:2]); m = g0 > 0
+        g0, g1 = g0[m], g1[m]
+        base = g0.min()
+        print(f"  k_sample_wide CTAs {m.sum()}: start spread {(g0.max() - base) / 1e3:.1f} us, end min "
+              f"{(g1.min() - base) / 1e3:.1f} max {(g1.max() - base) / 1e3:.1f} us, median dur {np.median(g1 - g0) / 1e3:.1f} us")
         print("k_table_wide cycles: gram-sum", t[1] - t[0], "sweep", t[2] - t[1], "scores", t[3] - t[2], "scan", t[4] - t[3])
     if a.wide and not t[107]:  # k_table_sample marks
         names = ["gram+sync", "sweep", "scores", "scan+cdf", "draw", "skr+zw+gamma"]
