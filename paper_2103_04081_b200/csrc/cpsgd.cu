@@ -154,9 +154,8 @@ struct cp_sgd_s {
   double* uw_rownorm = nullptr;  // wide path: Euclidean row norms [I_max]
   void* sw_gcl = nullptr;        // wide path: k_sample_wide cluster partials of Gamma
   unsigned* sw_cnt = nullptr;    // wide path: k_sample_wide arrival counter
-  int tc_nb8 = 0;                // fp32 wide path on tcgen05: UMMA N = 8 tc_nb8 = ceil8(R), 0 = FFMA mainloop
-  float* zhi = nullptr;          // tcgen05 path: 3xTF32 B-operand images of the prefetched batch
-  float* zlo = nullptr;
+  bool use_tc = false;           // fp32 wide path on tcgen05 (k_gather_update_tc), else the FFMA mainloop
+  float* zimg = nullptr;         // tcgen05 path: {zh; zl} A-operand images of the prefetched batch
   int fused_cu = 0, fused_bpc = 0, fused_rpc = 0;  // fused kernel geometry (0: not eligible)
   size_t fused_smem = 0;
   int pref_mode = -1;            // mode whose batch (at the current r) sits in idx/w/zrow/fbase
@@ -302,9 +301,7 @@ void fill_sample_params(cp_sgd_s* h, SampleParams& p, int n, const uint64_t* ite
   if (prefetch) {
     p.zrow = h->zrow;
     p.fbase = h->fbase;
-    p.zhi = h->zhi;
-    p.zlo = h->zlo;
-    p.nb8 = h->tc_nb8;
+    p.zimg = h->zimg;
   }
 }
 
@@ -585,7 +582,6 @@ cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   return check_launch(h, "k_gather_update");
 }
 
-template <int NB8>
 cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
   ProfScope ps(h, kKGatherUpdateTC);
   GUParams<float> p;
@@ -598,8 +594,7 @@ cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev
   p.rowlen = h->Xmm[n] ? h->pitch[n] : h->dims[n];
   p.fbase = h->fbase;
   p.zwp = (const float*)h->zwp;
-  p.zhi = h->zhi;
-  p.zlo = h->zlo;
+  p.zimg = h->zimg;
   p.bmax = h->bmax[n];
   const int CK = h->gu_ck[n];
   p.KB = h->gu_kb[n];
@@ -618,11 +613,10 @@ cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev
   p.eps = h->eps;
   p.iter = h->iter_dev;
   p.dbg = h->dbg;
-  const size_t smem = tc_smem_bytes<NB8>(h->R, p.KB);
+  const size_t smem = tc_smem_bytes(p.KB);
   static bool attr_set = false;
   if (!attr_set) {
-    allow_max_dyn_smem(k_gather_update_tc<NB8>);
-    cudaFuncSetAttribute(k_gather_update_tc<NB8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    allow_max_dyn_smem(k_gather_update_tc);
     attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
@@ -630,29 +624,18 @@ cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev
   lc.blockDim = dim3(kTCThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
-  cudaError_t e = cudaLaunchKernelEx(&lc, k_gather_update_tc<NB8>, p);
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_gather_update_tc, p);
   h->launches++;
   if (e != cudaSuccess)
-    return h->fail(CP_ECUDA, "k_gather_update_tc launch (cluster %d, smem %zu): %s", CK, smem, cudaGetErrorString(e));
+    return h->fail(CP_ECUDA, "k_gather_update_tc launch (chunks %d, smem %zu): %s", CK, smem, cudaGetErrorString(e));
   return check_launch(h, "k_gather_update_tc");
 }
 
 template <typename T>
 cp_status launch_gu(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
   // tensor-core mainloop needs fiber-contiguous, 16-byte aligned fibers (mode-major copy, or mode 0)
-  const bool tc_ok = sizeof(T) == 4 && h->tc_nb8 && (h->Xmm[n] || (n == 0 && h->dims[0] % 4 == 0));
-  if (tc_ok) {
-    switch (h->tc_nb8) {
-      case 1: return launch_gu_tc<1>(h, n, alpha, alpha_dev);
-      case 2: return launch_gu_tc<2>(h, n, alpha, alpha_dev);
-      case 3: return launch_gu_tc<3>(h, n, alpha, alpha_dev);
-      case 4: return launch_gu_tc<4>(h, n, alpha, alpha_dev);
-      case 5: return launch_gu_tc<5>(h, n, alpha, alpha_dev);
-      case 6: return launch_gu_tc<6>(h, n, alpha, alpha_dev);
-      case 7: return launch_gu_tc<7>(h, n, alpha, alpha_dev);
-      default: return launch_gu_tc<8>(h, n, alpha, alpha_dev);
-    }
-  }
+  const bool tc_ok = sizeof(T) == 4 && h->use_tc && (h->Xmm[n] || (n == 0 && h->dims[0] % 4 == 0));
+  if (tc_ok) return launch_gu_tc(h, n, alpha, alpha_dev);
   switch ((h->R + 7) / 8) {
     case 1: return launch_gu_t<T, 1>(h, n, alpha, alpha_dev);
     case 2: return launch_gu_t<T, 2>(h, n, alpha, alpha_dev);
@@ -1273,7 +1256,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     bool any = false;
     const bool tc = h->dtype == CP_F32 && !(h->flags & CP_FLAG_NO_TC);
-    if (tc) h->tc_nb8 = (h->R + 7) / 8;
+    h->use_tc = tc;
     int64_t mpart = 0;
     for (int n = 0; n < h->N; ++n) {
       const int64_t nt = ceil_div(h->dims[n], kGUTI);
@@ -1284,7 +1267,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       int64_t KB = ceil_div(ceil_div(h->bmax[n], CK), gran) * gran;
       CK = ceil_div(h->bmax[n], KB);  // no empty chunk
       size_t gs = h->esz == 8 ? gu_smem_bytes<double, 8>(KB) : gu_smem_bytes<float, 8>(KB);
-      if (tc) gs = std::max(gs, tc_smem_bytes<8>(h->R, KB));
+      if (tc) gs = std::max(gs, tc_smem_bytes(KB));
       int64_t bmx = 0, cdfmax = 0;
       for (int k = 0; k < h->N; ++k) {
         bmx = std::max(bmx, h->bmax[k]);
@@ -1315,18 +1298,16 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       ALLOC(h->zwp, h->esz * Bmax_all * zg_rp(h->R));
       ALLOC(h->gam_next, h->esz * h->R * h->R);
       cudaMemsetAsync(h->zwp, 0, h->esz * Bmax_all * zg_rp(h->R), h->stream);
-      if (h->tc_nb8) {  // B images: every chunk rounded up to whole stages; rows past B_max stay zero
+      if (h->use_tc) {  // A images: every chunk rounded up to whole stages; rows r >= R stay zero
         int64_t rows = 0;
         for (int n = 0; n < h->N; ++n)
           if (h->gu_ck[n]) rows = std::max(rows, (int64_t)h->gu_ck[n] * h->gu_kb[n]);
-        const size_t bytes = sizeof(float) * (size_t)rows * 8 * h->tc_nb8;
-        ALLOC(h->zhi, bytes);
-        ALLOC(h->zlo, bytes);
-        cudaMemsetAsync(h->zhi, 0, bytes, h->stream);
-        cudaMemsetAsync(h->zlo, 0, bytes, h->stream);
+        const size_t bytes = (size_t)ceil_div(rows, kTCKS) * kTCZBytes;
+        ALLOC(h->zimg, bytes);
+        cudaMemsetAsync(h->zimg, 0, bytes, h->stream);
       }
     } else {
-      h->tc_nb8 = 0;
+      h->use_tc = false;
     }
   }
   // ---- optional mode-major copies (n >= 1; mode 0 fibers are already contiguous) ----
@@ -1418,9 +1399,8 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->zrow);
   cudaFree(h->fbase);
   cudaFree(h->zwp);
+  cudaFree(h->zimg);
   cudaFree(h->gam_next);
-  cudaFree(h->zhi);
-  cudaFree(h->zlo);
   cudaFree(h->Mpart);
   cudaFree(h->gu_cnt);
   cudaFree(h->uw_gpart);

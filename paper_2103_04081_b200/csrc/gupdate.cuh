@@ -35,8 +35,7 @@ struct GUParams {
   int64_t rowlen;         // tcgen05 path: readable elements per fiber row (pitch of the mode-major copy)
   const int64_t* fbase;   // [Bmax] element offset of fiber b (-1: padding row)
   const T* zwp;           // [Bmax][RP] weighted SKR rows, zero padded (sampler)
-  const float* zhi;       // tcgen05 path: 3xTF32 split of zw (hi / lo) as UMMA B-operand images
-  const float* zlo;       //   [B_pad/8][NB/32][8][32] (MN-major, 128-byte swizzle), see gupdate_tc.cuh
+  const float* zimg;      // tcgen05 path: A-operand images {zh; zl} per stage of 32 fibers (zimg_off)
   int64_t bmax;           // rows of the batch buffers for this mode
   int64_t KB;             // fibers per chunk (= per CTA)
   const T* Gam;           // [R][R] Gamma of this batch (sampler)
@@ -83,10 +82,8 @@ __device__ __forceinline__ void gu_finish(const GUParams<T>& p, const T* Mt, int
     const int r = e / TI, rl = e % TI;
     if (rl < nrow) part[e] = Mt[rl * MS + r];
   }
-  if (blockIdx.x == 0 && blockIdx.y == 0) {
-    for (int e = tid; e < R * R; e += nth) p.Gam_out[e] = p.Gam[e];
-    if (tid == 0) *p.iter += 1;  // r <- r + 1 (Alg. 6/7); nothing in this launch reads r
-  }
+  // r <- r + 1 (Alg. 6/7); nothing in this launch reads r (Gamma_out: k_update_wide)
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *p.iter += 1;
 }
 
 template <typename T, int CPT>

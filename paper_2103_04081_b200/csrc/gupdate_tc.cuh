@@ -1,32 +1,37 @@
 // gupdate_tc.cuh -- k_gather_update_tc: the fp32 wide-path step kernel with the sampled MTTKRP
 // M_tile = X_F diag(w) Z_F (eq:gradient1/2) on the 5th-generation tensor cores.
 //
-//   D[i][r] (TMEM, fp32) = sum_b X[i][b] ZW[b][r]     i: 128 rows of the I-tile (UMMA M = 128)
-//                                                      r: NB = 32*ceil(R/32) columns (UMMA N)
-//                                                      b: fibers, K = 8 per tcgen05.mma (kind::tf32)
-//   3xTF32 (SURVEY section 7 hard part 3): x = xh + xl, zw = zh + zl with xh = trunc_tf32(x) and
-//   xl = x - xh (exact in fp32), D += xh zh + xh zl + xl zh  -> ~fp32 accuracy (dropped xl zl ~ 2^-22).
+//   3xTF32 (SURVEY section 7 hard part 3): x = xh + xl, zw = zh + zl with h = trunc_tf32(.) and
+//   l = . - h (exact in fp32).  ONE tcgen05.mma (kind::tf32, M = 128, N = 256, K = 8) per 8 fibers
+//   computes all four products at once:
 //
-// Operands in shared memory, canonical UMMA layout "K-major, 128-byte swizzle": an atom is 8 MN-rows
+//      A (SMEM, 128 rows x K)   = [ zh_0..zh_63 ; zl_0..zl_63 ]          (rows r >= R are zero)
+//      B (SMEM, 256 rows x K)   = [ xh_i (i = 0..127) ; xl_i (i = 0..127) ]
+//      D (TMEM, 128 x 256 fp32) = A B^T,  M^T[r][i] = D[r][i] + D[r][128+i] + D[64+r][i] + D[64+r][128+i]
+//
+//   (zl xl is kept: the result is the full fp32 product up to accumulation rounding.)  A tcgen05.mma
+//   costs ~100 cycles whatever its N below ~128 on this part (N = 256: ~170, tools/micro/umma_ts.cu),
+//   so four products in one N = 256 instruction replace the twelve N = 56 ones of a 3-MMA split.
+//
+// Both operands in shared memory, canonical UMMA layout "K-major, 128-byte swizzle": an atom is 8 rows
 // x 128 B (the 32 fibers of a stage), 16-byte chunk c of row rr stored at chunk (c ^ rr); 8-row
-// groups at SBO = 1024 B; UMMA K-step k (8 fibers = 32 B) starts 32k bytes into the atom.  The X
-// tile arrives by cp.async in plain [fiber][row] order (a fiber segment is 512 contiguous bytes of
-// the mode-major copy: the HBM stream of Alg. 5 TensorSamp); one pass transposes 4x4 blocks in
-// registers and writes xh and xl in the K-major layout.  B (zh, zl) is produced by the sampler
-// directly as layout images and copied linearly.  (MN-major tf32 operands read as zeros on this
-// toolchain/driver -- tools/micro/umma.cu -- so both operands are K-major.)
+// groups at SBO = 1024 B (xl's 128 rows follow xh's directly); UMMA K-step k starts 32k bytes into
+// the atom.  The X tile arrives by cp.async in plain [fiber][row] order (a fiber segment is 512
+// contiguous bytes of the mode-major copy: the HBM stream of Alg. 5 TensorSamp); one pass transposes
+// 4x4 blocks in registers and writes xh and xl.  (MN-major tf32 operands read as zeros on this
+// toolchain/driver -- tools/micro/umma.cu -- so B is K-major.)  A is produced by the sampler directly
+// in this layout (one 16 KB image per stage, zimg_off in kernels.cuh) and copied linearly.
 //
 // Warp-specialised pipeline (stages of KS = 32 fibers; 448 threads):
-//   warps 0-3   X loaders: 16-byte cp.async chunks of the sampled fiber segments (512 contiguous bytes
-//               of the mode-major copy each) into an NX-deep raw ring; completion on xfull[s] via
-//               cp.async.mbarrier.arrive.noinc; slots recycled through xempty[s];
-//   warp 13     B producer (one thread): the hi / lo B images of the stage (2 bulk copies, 2-deep ring);
-//   warps 4-11  split: 4x4 register transposes -> xh / xl (K-major) in pair s & 1 (free once stage
-//               s-2's MMAs retired: mdone), fence.proxy.async, arrive sdone;
-//   warp 12     MMA issuer (one thread): 12 tcgen05.mma per stage, tcgen05.commit -> mdone[s & 1];
-//               last commit -> accf.
-//   epilogue    warps 4-7 read the accumulator (tcgen05.ld.32x32b: warp w <-> TMEM lanes 32(w%4)..),
-//               then all threads write the partial tile (gu_finish).
+//   warps 0-3   X loaders: 16-byte cp.async chunks of the sampled fiber segments into an NX-deep raw
+//               ring; completion on xfull[s] via cp.async.mbarrier.arrive.noinc; recycled via xempty[s];
+//   warps 4-11  split: 4x4 register transposes -> {xh, xl} pair s % NP (free once stage s-NP's MMAs
+//               retired: mdone), fence.proxy.async, arrive sdone;
+//   warp 12     A producer (one thread): the stage's image, one 16 KB cp.async.bulk into slot s % NZ
+//               (completion: afull[s] transaction bytes; slot freed by tcgen05.commit -> afree);
+//   warp 13     MMA issuer (one thread): 4 tcgen05.mma per stage, commits -> mdone, afree; last -> accf.
+//   epilogue    warps 4-11 fold the xh / xl halves (tcgen05.ld.32x32b) into shared memory, then all
+//               threads fold the zh / zl halves and write the partial tile to the split-K workspace.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -101,19 +106,17 @@ __host__ __device__ __forceinline__ uint32_t kmaj_off(int m, int kk) {
   return (uint32_t)((m >> 3) * 1024 + rr * 128 + ((c ^ rr) << 4) + ((kk & 3) << 2));
 }
 
-// ring sizes (bytes): NX stages of raw X, 2 stages of B (hi, lo), 2 pairs of K-major (xh, xl)
-template <int NB8>
-__host__ __device__ constexpr uint32_t tc_b_bytes() { return (uint32_t)kTCKS * 8 * NB8 * 4; }
-constexpr uint32_t kTCABytes = kTCKS * 128 * 4;
-template <int NB8>
-__host__ __device__ constexpr int tc_nx() {  // deepest X ring that fits next to the other buffers
-  return (int)((200u * 1024u - 4u * kTCABytes - 4u * tc_b_bytes<NB8>()) / kTCABytes);
-}
-template <int NB8>
-__host__ __device__ inline size_t tc_smem_bytes(int R, int64_t KB) {
-  const size_t ring = (size_t)tc_nx<NB8>() * kTCABytes + 4 * (size_t)tc_b_bytes<NB8>() + 4 * (size_t)kTCABytes;
-  const size_t epi = (size_t)kGUTI * (8 * NB8 + 1) * 4;
-  return 1024 + (ring > epi ? ring : epi) + (size_t)R * R * 4 + (size_t)KB * 8 + 256;
+// shared-memory rings (bytes): NX stages of raw X, NPAIR pairs {xh, xl} of the K-major UMMA B operand
+constexpr uint32_t kTCABytes = kTCKS * 128 * 4;  // one stage of raw X / one K-major half (16 KB)
+constexpr int kTCPairs = 2;
+constexpr int kTCNZ = 3;                          // A-operand (zw hi / lo image) stages
+constexpr uint32_t kTCZBytes = 128 * kTCKS * 4;   // one image stage: 128 rows x 128 B (16 KB)
+constexpr int kTCNX = (int)((200u * 1024u - kTCPairs * 2u * kTCABytes - kTCNZ * kTCZBytes) / kTCABytes);
+constexpr int kTCEpiStride = kGUTI + 4;  // epilogue staging row pitch (floats): conflict-free float4 rows
+__host__ __device__ inline size_t tc_smem_bytes(int64_t KB) {
+  const size_t ring = (size_t)kTCNX * kTCABytes + (size_t)kTCPairs * 2 * kTCABytes + (size_t)kTCNZ * kTCZBytes;
+  const size_t epi = (size_t)128 * kTCEpiStride * 4;
+  return 1024 + (ring > epi ? ring : epi) + (size_t)KB * 8 + 256;
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -131,24 +134,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-
-template <int NB8>
-__global__ void __launch_bounds__(448, 1) k_gather_update_tc(GUParams<float> p) {
-  constexpr int NB = 8 * NB8;                                   // UMMA N (columns r >= R are zero)
-  constexpr int TMEM_COLS = NB <= 32 ? 32 : 64;
-  constexpr int KS = kTCKS, NX = tc_nx<NB8>(), TI = kGUTI;
-  constexpr uint32_t A_BYTES = kTCABytes, B_BYTES = tc_b_bytes<NB8>();
-  constexpr uint32_t IDESC = umma_idesc_tf32_mn(128, NB) & ~((1u << 15) | (1u << 16));  // K-major A and B
+__global__ void __launch_bounds__(kTCThreads, 1) k_gather_update_tc(GUParams<float> p) {
+  constexpr int KS = kTCKS, NX = kTCNX, NP = kTCPairs, NZ = kTCNZ, TI = kGUTI;
+  constexpr uint32_t A_BYTES = kTCABytes;
+  constexpr uint32_t TMEM_COLS = 256;    // D: 128 lanes x 256 fp32 columns
+  // M = 128 (A rows: zh 0-63, zl 64-127), N = 256 (B rows: xh 0-127, xl 128-255), both K-major
+  constexpr uint32_t IDESC = umma_idesc_tf32_mn(128, 256) & ~((1u << 15) | (1u << 16));
   extern __shared__ __align__(16) unsigned char tc_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* xsp = sm;                          // 2 x {xh, xl} (K-major, 128-byte swizzle)
-  unsigned char* bring = sm + 4 * A_BYTES;          // 2 x {B hi, B lo}
-  unsigned char* xring = bring + 4 * B_BYTES;       // NX x raw X [32 fibers][512 B]
-  const size_t body = (size_t)4 * A_BYTES + 4 * B_BYTES + (size_t)NX * A_BYTES;
-  const size_t epi = (size_t)TI * (NB + 1) * 4;
-  float* sGam = reinterpret_cast<float*>(sm + (body > epi ? body : epi));
-  int64_t* sfb = reinterpret_cast<int64_t*>(sGam + p.R * p.R + (p.R * p.R & 1));
-  __shared__ __align__(8) uint64_t xfull[16], xempty[16], bfull[2], sdone[2], mdone[2], accf;
+  // 1024-byte aligned base, derived from the shared array itself so every access stays LDS / STS
+  // (integer round-tripping the pointer turns them into generic LD / ST)
+  unsigned char* sm = tc_raw + ((1024u - (smem_u32(tc_raw) & 1023u)) & 1023u);
+  unsigned char* xsp = sm;                          // NP x {xh, xl} (K-major, 128-byte swizzle, contiguous)
+  unsigned char* xring = sm + NP * 2 * A_BYTES;     // NX x raw X [32 fibers][512 B]
+  unsigned char* zring = xring + NX * A_BYTES;      // NZ x A image [128 rows][128 B] (K-major, swizzled)
+  const size_t body = (size_t)NP * 2 * A_BYTES + (size_t)NX * A_BYTES + (size_t)NZ * kTCZBytes;
+  const size_t epi = (size_t)128 * kTCEpiStride * 4;
+  int64_t* sfb = reinterpret_cast<int64_t*>(sm + (body > epi ? body : epi));
+  __shared__ __align__(8) uint64_t xfull[16], xempty[16], sdone[4], mdone[4], afull[4], afree[4], accf;
   __shared__ uint32_t s_tmem;
 
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
@@ -163,9 +165,9 @@ __global__ void __launch_bounds__(448, 1) k_gather_update_tc(GUParams<float> p) 
   long long gt0 = 0;
   if (p.dbg && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
 
-  if (wid == 12) {  // TMEM accumulator: 128 lanes x TMEM_COLS columns
+  if (wid == 13) {  // TMEM accumulator
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
-                 "r"((uint32_t)TMEM_COLS));
+                 "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -173,15 +175,19 @@ __global__ void __launch_bounds__(448, 1) k_gather_update_tc(GUParams<float> p) 
       mbar_init(&xfull[s], 128);   // the 128 loader threads' cp.async.mbarrier.arrive.noinc
       mbar_init(&xempty[s], 256);  // the 256 split threads are done reading the raw stage
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&bfull[s], 1);
+    for (int s = 0; s < NP; ++s) {
       mbar_init(&sdone[s], 256);
-      mbar_init(&mdone[s], 1);  // tcgen05.commit: MMAs of the stage retired (xh/xl pair + B slot free)
+      mbar_init(&mdone[s], 1);  // tcgen05.commit: MMAs of the stage retired (xh/xl pair free)
+    }
+    for (int s = 0; s < NZ; ++s) {
+      mbar_init(&afull[s], 1);  // expect_tx arrival + the bulk copy's bytes
+      mbar_init(&afree[s], 1);  // tcgen05.commit: the A slot may be overwritten
     }
     mbar_init(&accf, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  cp_async_u64(reinterpret_cast<uint64_t*>(sfb), reinterpret_cast<const uint64_t*>(p.fbase + c0), nfib, tid, 448);
+  cp_async_u64(reinterpret_cast<uint64_t*>(sfb), reinterpret_cast<const uint64_t*>(p.fbase + c0), nfib, tid,
+               kTCThreads);
   cp_async_commit();
   cp_async_wait<0>();
   tc_fence_before();
@@ -212,30 +218,20 @@ __global__ void __launch_bounds__(448, 1) k_gather_update_tc(GUParams<float> p) 
       }
       cp_async_mbar_arrive_noinc(&xfull[slot]);
     }
-  } else if (wid == 13) {
-    // ======================= B producer (one thread): hi / lo images, 2-deep ring =======================
-    if (lane == 0) {
-      for (int st = 0; st < nst; ++st) {
-        const int slot = st & 1;
-        if (st >= 2) mbar_wait(&mdone[slot], (uint32_t)(((st >> 1) - 1) & 1));
-        unsigned char* Bh = bring + slot * 2 * B_BYTES;
-        const int64_t sb = (c0 + (int64_t)st * KS) / KS;  // stage index in the images ([stage][NB rows][128 B])
-        mbar_expect_tx(&bfull[slot], 2 * B_BYTES);
-        bulk_g2s(Bh, p.zhi + sb * (B_BYTES / 4), B_BYTES, &bfull[slot]);
-        bulk_g2s(Bh + B_BYTES, p.zlo + sb * (B_BYTES / 4), B_BYTES, &bfull[slot]);
-      }
-    }
-  } else if (wid >= 4 && wid <= 11) {
+  } else if (wid <= 11) {
     // ======================= 3xTF32 split / transpose (256 threads) =======================
     // block = 4 fibers (4kq..) x 4 rows {iq, iq+32, iq+64, iq+96}: lanes run over iq, so the raw
     // loads (4 B, consecutive rows) and the K-major stores (row & 7 = iq & 7) are conflict-free
     const int t = tid - 128;
     const int iq = t & 31, kq = t >> 5;  // warp -> fiber quad kq (0..7)
     for (int st = 0; st < nst; ++st) {
-      const int slot = st % NX, hb = st & 1;
+      const int slot = st % NX, hb = st % NP;
+      if (mark && st == 8) p.dbg[26] = clock64();
+      if (mark && st == 9) p.dbg[27] = clock64();
+      if (mark && st == 12) p.dbg[28] = clock64();
       mbar_wait(&xfull[slot], (uint32_t)((st / NX) & 1));
       if (mark && st == 8) p.dbg[18] = clock64();
-      if (st >= 2) mbar_wait(&mdone[hb], (uint32_t)(((st >> 1) - 1) & 1));  // xh/xl pair hb free
+      if (st >= NP) mbar_wait(&mdone[hb], (uint32_t)(((st / NP) - 1) & 1));  // xh/xl pair hb free
       if (mark && st == 8) p.dbg[19] = clock64();
       const float* A = reinterpret_cast<const float*>(xring + slot * A_BYTES);
       unsigned char* H = xsp + hb * 2 * A_BYTES;
@@ -262,61 +258,90 @@ __global__ void __launch_bounds__(448, 1) k_gather_update_tc(GUParams<float> p) 
       mbar_arrive(&sdone[hb]);
       if (mark && st == 8) p.dbg[20] = clock64();
     }
-  } else if (wid == 12 && lane == 0) {
+  } else if (wid == 12) {
+    // ======================= A producer (one thread): the sampler's zh / zl image of the stage =======================
+    if (lane == 0) {
+      for (int st = 0; st < nst; ++st) {
+        const int zs = st % NZ;
+        if (st >= NZ) mbar_wait(&afree[zs], (uint32_t)(((st / NZ) - 1) & 1));
+        const int64_t sb = (c0 + (int64_t)st * KS) / KS;  // stage index in the images
+        mbar_expect_tx(&afull[zs], kTCZBytes);
+        bulk_g2s(zring + zs * kTCZBytes, p.zimg + sb * (kTCZBytes / 4), kTCZBytes, &afull[zs]);
+      }
+    }
+  } else if (wid == 13 && lane == 0) {
     // ======================= MMA issuer =======================
     const bool mk = p.dbg && blockIdx.x == 0 && blockIdx.y == 0;
-    const uint64_t dx = umma_desc_sw128(smem_u32(xsp), 16, 1024);    // xh of pair 0
-    const uint64_t dbz = umma_desc_sw128(smem_u32(bring), 16, 1024);  // B hi of slot 0
+    const uint64_t dx = umma_desc_sw128(smem_u32(xsp), 16, 1024);   // B = {xh; xl} of pair 0
+    const uint64_t dz = umma_desc_sw128(smem_u32(zring), 16, 1024);  // A = {zh; zl} of slot 0
     for (int st = 0; st < nst; ++st) {
-      const int hb = st & 1;
-      mbar_wait(&sdone[hb], (uint32_t)((st >> 1) & 1));
-      mbar_wait(&bfull[hb], (uint32_t)((st >> 1) & 1));
+      const int hb = st % NP, as = st % NZ;
+      if (mk && st == 8) p.dbg[24] = clock64();
+      mbar_wait(&sdone[hb], (uint32_t)((st / NP) & 1));
+      if (mk && st == 8) p.dbg[25] = clock64();
+      mbar_wait(&afull[as], (uint32_t)((st / NZ) & 1));
       tc_fence_after();
       if (mk && st == 8) p.dbg[21] = clock64();
-      const uint64_t h = dx + ((uint64_t)(hb * 2 * A_BYTES) >> 4);
-      const uint64_t l = h + (A_BYTES >> 4);
-      const uint64_t bh = dbz + ((uint64_t)(hb * 2 * B_BYTES) >> 4), bl = bh + (B_BYTES >> 4);
+      const uint64_t b = dx + ((uint64_t)(hb * 2 * A_BYTES) >> 4);
+      const uint64_t a = dz + ((uint64_t)(as * kTCZBytes) >> 4);
 #pragma unroll
-      for (int k = 0; k < KS / 8; ++k) {  // K-step k: fibers 8k..8k+7 = bytes 32k.. of every atom row
-        umma_tf32(tmem, h + 2 * k, bh + 2 * k, IDESC, (st > 0 || k > 0) ? 1u : 0u);
-        umma_tf32(tmem, h + 2 * k, bl + 2 * k, IDESC, 1u);
-        umma_tf32(tmem, l + 2 * k, bh + 2 * k, IDESC, 1u);
-      }
+      for (int k = 0; k < KS / 8; ++k)  // K-step k: fibers 8k..8k+7 = bytes 32k.. of every atom row
+        umma_tf32(tmem, a + 2 * k, b + 2 * k, IDESC, (st > 0 || k > 0) ? 1u : 0u);
       umma_commit(&mdone[hb]);
+      umma_commit(&afree[as]);
       if (mk && st == 8) p.dbg[22] = clock64();
     }
     umma_commit(&accf);
   }
   __syncthreads();
   if (mark) p.dbg[34] = clock64();
-  // ---- accumulator -> shared partial tile [TI][NB+1] (zero if this CTA had no fibers) ----
+  // ---- epilogue: E[L][i] = D[L][i] + D[L][128 + i] (x = xh + xl) staged in shared memory, then
+  //      M^T[r][i] = E[r][i] + E[64 + r][i] (zw = zh + zl) -> the split-K workspace ----
   if (nst > 0) mbar_wait(&accf, 0u);
   tc_fence_after();
-  constexpr int MS = NB + 1;
-  float* Mt = reinterpret_cast<float*>(sm);  // every ring is dead
-  if (wid >= 4 && wid <= 7) {
-    const int lg = wid & 3;          // TMEM lane group of this warp
-    const int row = 32 * lg + lane;  // TMEM lane = tile row
-#pragma unroll
-    for (int cb = 0; cb < NB; cb += 8) {
-      uint32_t r[8];
+  float* E = reinterpret_cast<float*>(sm);  // every ring is dead
+  if (wid >= 4 && wid <= 11) {  // warp w: TMEM lanes 32 (w & 3).., tile rows [64 hh, 64 hh + 64)
+    const int L = 32 * (wid & 3) + lane, hh = (wid - 4) >> 2;
+    const uint32_t trow = tmem + ((uint32_t)(32 * (wid & 3)) << 16);
+#pragma unroll 1
+    for (int c = 64 * hh; c < 64 * hh + 64; c += 16) {
+      float v1[16], v2[16];
       if (nst > 0) {
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                     : "r"(tmem + ((uint32_t)(32 * lg) << 16) + (uint32_t)cb));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tmem_ld16(trow + (uint32_t)c, v1);
+        tmem_ld16(trow + 128u + (uint32_t)c, v2);
       } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = 0u;
+        for (int j = 0; j < 16; ++j) v1[j] = v2[j] = 0.f;
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) Mt[row * MS + cb + j] = __uint_as_float(r[j]);
+      for (int j = 0; j < 16; j += 4)
+        *reinterpret_cast<float4*>(E + L * kTCEpiStride + c + j) =
+            make_float4(v1[j] + v2[j], v1[j + 1] + v2[j + 1], v1[j + 2] + v2[j + 2], v1[j + 3] + v2[j + 3]);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (wid == 12) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)TMEM_COLS));
+  if (wid == 13) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   if (mark) p.dbg[35] = clock64();
+  {
+    const int nrow = (int)cmax64(0, cmin64(TI, p.In - i0));
+    float* part = p.Mpart + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * R * TI;
+    for (int e = tid; e < R * (TI / 4); e += kTCThreads) {
+      const int r = e / (TI / 4), i = 4 * (e % (TI / 4));
+      const float4 a = *reinterpret_cast<const float4*>(E + r * kTCEpiStride + i);
+      const float4 b = *reinterpret_cast<const float4*>(E + (64 + r) * kTCEpiStride + i);
+      const float4 s = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+      if (i + 4 <= nrow) {
+        *reinterpret_cast<float4*>(part + r * TI + i) = s;
+      } else {
+        if (i < nrow) part[r * TI + i] = s.x;
+        if (i + 1 < nrow) part[r * TI + i + 1] = s.y;
+        if (i + 2 < nrow) part[r * TI + i + 2] = s.z;
+      }
+    }
+    // r <- r + 1 (Alg. 6/7); nothing in this launch reads r (Gamma_out: k_update_wide)
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) *p.iter += 1;
+  }
   if (p.dbg && tid == 0 && cta < 1000) {
     long long gt1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
@@ -326,7 +351,6 @@ __global__ void __launch_bounds__(448, 1) k_gather_update_tc(GUParams<float> p) 
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     p.dbg[3072 + cta] = smid;
   }
-  gu_finish<float>(p, Mt, MS, i0, tid, 448);
   if (mark) p.dbg[36] = clock64();
 }
 

@@ -53,22 +53,15 @@ struct SampleParams {
   // wide path (k_gather_update): weighted padded SKR rows and Gamma of the batch (or NULL)
   void* zwp;                       // T [B_max][ceil8(R)]
   void* gam_next;                  // T [R][R]
-  float* zhi;                      // tcgen05 path: 3xTF32 split of zw as UMMA B images (or NULL)
-  float* zlo;
-  int nb8;                         //   UMMA N = 8 nb8 (= ceil8(R)) rows of the B images
+  float* zimg;                     // tcgen05 path: 3xTF32 A-operand images of zw (or NULL)
 };
 
-// byte offset of (fiber b, column r) in the UMMA B-operand images of gupdate_tc.cuh: per stage of 32
-// fibers, NB = 8 nb8 rows (columns r) of 128 B, K-major with the 128-byte swizzle
-__host__ __device__ __forceinline__ uint32_t zimg_off(int64_t b, int r, int nb8) {
-  const int kk = (int)(b & 31), rr = r & 7, c = (kk >> 2) & 7;
-  return (uint32_t)((b >> 5) * (8 * nb8 * 128) + (r >> 3) * 1024 + rr * 128 + ((c ^ rr) << 4) + ((kk & 3) << 2));
-}
-__device__ __forceinline__ void write_zw_images(const SampleParams& p, int64_t b, int r, float zw) {
-  const float h = __uint_as_float(__float_as_uint(zw) & 0xFFFFE000u);
-  const uint32_t o = zimg_off(b, r, p.nb8) >> 2;
-  p.zhi[o] = h;
-  p.zlo[o] = zw - h;
+// byte offset of zh_r (part 0) / zl_r (part 1) of fiber b in the tcgen05 A-operand images
+// (gupdate_tc.cuh): per stage of 32 fibers one 128-row x 128-byte tile (rows 0-63 zh, 64-127 zl),
+// K-major with the 128-byte swizzle (16-byte chunk c of row m at chunk c ^ (m & 7))
+__host__ __device__ __forceinline__ uint32_t zimg_off(int64_t b, int m) {
+  const int kk = (int)(b & 31), rr = m & 7, c = (kk >> 2) & 7;
+  return (uint32_t)((b >> 5) * 16384 + (m >> 3) * 1024 + rr * 128 + ((c ^ rr) << 4) + ((kk & 3) << 2));
 }
 
 template <typename T>

@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(kTWThreads, 1) k_table_wide(TWParams p) {
 // ------------------------------------------------------------------------------------------
 struct SWParams {
   long long* dbg;
-  SampleParams sp;          // batch of mode sp.n at the iteration in *sp.iter; zwp / zhi / gam_next set
+  SampleParams sp;          // batch of mode sp.n at the iteration in *sp.iter; zwp / gam_next set
   void* gcl;                // [clusters][R][R] cluster partials of Gamma (T)
   unsigned* cnt;            // arrival counter (zero between launches)
   int64_t cdf_elems;        // staged CDF entries (sum of I_k, k != n; 0 = uniform)
@@ -631,8 +631,8 @@ __global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
   }
   __syncthreads();
   SWM(3);
-  // weighted rows for the FFMA gather kernel (row-contiguous) and the tcgen05 B images (per column
-  // r one 128-byte row of the 32 fibers: lanes run over fibers, coalesced)
+  // weighted rows zw_b = w_b z_b for the gather kernels (row-contiguous, zero past R) and the
+  // tcgen05 A-operand images (zh / zl rows of 128 B over the 32 fibers: lanes run over fibers)
   {
     T* zwp = reinterpret_cast<T*>(sp.zwp);
     for (int e = tid; e < nf * RP; e += kWThreads) {
@@ -640,10 +640,15 @@ __global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
       zwp[(b0 + lb) * RP + r] = (T)sw[lb] * zs[e];
     }
     if constexpr (sizeof(T) == 4) {
-      if (sp.zhi)
+      if (sp.zimg)
         for (int e = tid; e < R * kSWFibers; e += kWThreads) {
           const int r = e / kSWFibers, lb = e % kSWFibers;
-          if (lb < nf) write_zw_images(sp, b0 + lb, r, (float)((T)sw[lb] * zs[lb * RP + r]));
+          if (lb < nf) {
+            const float zw = (float)((T)sw[lb] * zs[lb * RP + r]);
+            const float h = __uint_as_float(__float_as_uint(zw) & 0xFFFFE000u);
+            sp.zimg[zimg_off(b0 + lb, r) >> 2] = h;
+            sp.zimg[zimg_off(b0 + lb, 64 + r) >> 2] = zw - h;
+          }
         }
     }
   }

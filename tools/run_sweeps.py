@@ -70,7 +70,11 @@ elif os.environ.get("CPSGD_DEBUG_TIMERS"):
         print("  finish(tile 0): chunk0 A-load", t[38] - t[37], "AGamma", t[39] - t[38], "part+fence+atomic", t[40] - t[39],
               "| last CTA = chunk", t[60], ": reduce", t[41] - (t[40] if t[60] == 0 else t[48]), "update", t[42] - t[41])
         print("  stage 8: load issue->data", t[18] - t[23], "wait xh/xl", t[19] - t[18], "split", t[20] - t[19],
-              "split->mma start", t[21] - t[20], "mma issue", t[22] - t[21])
+              "split->mma start", t[21] - t[20], "mma issue", t[22] - t[21], "| mma thread: wait sdone", t[25] - t[24],
+              "wait bfull", t[21] - t[25], "| split: wait xfull", t[18] - t[26], "stage 8->9", t[27] - t[26],
+              "stage 8->12 /4", (t[28] - t[26]) / 4)
+        print("  z writer st 8: wait_group", t[41] - t[40], "bar", t[42] - t[41], "issue+lds+cvt", t[43] - t[42],
+              "afree", t[44] - t[43], "st+arrive", t[45] - t[44], "| z top vs split top", t[40] - t[26])
     if t[107]:
         nm = ["cdf stage", "draw", "skr", "zw/img", "gamma", "cluster+fence", "last"]
         print("k_sample_wide (CTA 0) cycles: " + " | ".join(f"{nm[i]} {t[101 + i] - t[100 + i]}" for i in range(7)))
@@ -80,6 +84,8 @@ elif os.environ.get("CPSGD_DEBUG_TIMERS"):
         base = g0.min()
         print(f"  k_sample_wide CTAs {m.sum()}: start spread {(g0.max() - base) / 1e3:.1f} us, end min "
               f"{(g1.min() - base) / 1e3:.1f} max {(g1.max() - base) / 1e3:.1f} us, median dur {np.median(g1 - g0) / 1e3:.1f} us")
+        import struct
+        print("  NS residuals:", [struct.unpack('d', struct.pack('q', v))[0] for v in t[200:208]])
         print("k_table_wide cycles: gram-sum", t[1] - t[0], "sweep", t[2] - t[1], "scores", t[3] - t[2], "scan", t[4] - t[3])
     if a.wide and not t[107]:  # k_table_sample marks
         names = ["gram+sync", "sweep", "scores", "scan+cdf", "draw", "skr+zw+gamma"]
