@@ -84,7 +84,7 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
   L.gm = take(sizeof(double) * R * (R + 1));
   L.prow = take(sizeof(double) * RPC);
   L.sc = take(sizeof(double) * RPC * R);
-  L.rowbuf = take(sizeof(double) * 2 * kMaxRank);
+  L.rowbuf = take(sizeof(double) * 3 * kMaxRank);
   L.swept = take(sizeof(int) * R);
   L.qtot = take(sizeof(unsigned long long) * 2);
   L.cdfs = take(sizeof(uint64_t) * cdf_elems);
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
         __syncthreads();
         constexpr int EPT = (32 * 32 + kFThreads - 1) / kFThreads;
         const int rank = (In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, s_red[0], rowbuf, swept, rowbuf + R)
-                                      : lc_sweep_dispatch<32>(Gm, R, s_red[0], rowbuf, swept);
+                                      : grp_sweep_dispatch<32>(Gm, R, s_red[0], rowbuf, swept);
         F_MARK(6);
         if (tid == 0 && rank == 0) s_bad |= 2;
         // scores l = a^T W a: thread per (row, i) forms a_i * (W a)_i; rows summed in order

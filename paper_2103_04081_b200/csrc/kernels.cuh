@@ -797,59 +797,61 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // maps M_ij -= M_ik M_kj / d (i, j != k), M_ik, M_kj /= d, M_kk = -1/d (d = M_kk).  The unswept
 // diagonal is the Schur-complement diagonal, so a pivot whose value is <= tol is skipped (reading
 // R4(b), the rank rule of a pivoted Cholesky); after sweeping S, M_SS = -(G_SS)^{-1}.
-// Lane per column: thread c < RMAX (RMAX = ceil8(R) <= 64, warps 0..RMAX/32) keeps
-// column c of the RMAX x RMAX matrix (identity past R) in registers, rows in ROTATED order: before
-// pivot k slot t holds row (k + t) mod RMAX, so the pivot row is always slot 0 and every register
-// index is static.  Pivot k:
-//   publish  thread c stores v[0] (= M_kc = M_ck by symmetry) at cb[(c - k) mod RMAX], so slot t
-//            of every column reads c_t = M_{row(t),k} = cb[t] (broadcast loads);
-//   d = c_0 > tol:  f = (c == k) ? -1/d : v[0]/d;  slot t-1 <- [c != k] v[t] - c_t f (t >= 1);
-//                   slot RMAX-1 <- f (the new row k);      otherwise rotate only.
-// One named barrier (or __syncwarp) per pivot; one DFMA + two selects per held entry.  After R
-// pivots slot t holds row (R + t) mod RMAX.  Called by every thread of the CTA; returns |S|.
-template <int RMAX>
-__device__ int lc_sweep_inverse(double* Gm, int R, double tol, double* colbuf /* 2*RMAX */, int* swept /* R */) {
-  constexpr int NT = (RMAX + 31) / 32 * 32;
+// Row groups x lanes: thread (g, c) of NT = 32 ceil(RMAX/32) G threads keeps rows
+// [g RPG, (g + 1) RPG) of column c of the RMAX x RMAX matrix (identity past R; RMAX = ceil8(R),
+// RPG = ceil(RMAX / G)) in registers, static indices, no rotation.  Pivot k:
+//   publish  the owner group of row k stores M_kc (register select on k mod RPG) at rb[c]; by
+//            symmetry rb[t] = M_tk is also the pivot column (broadcast loads);
+//   d = rb[k] > tol:  f = (c == k) ? -1/d : rb[c]/d;
+//                     row k <- f;  row t != k <- [c != k] M_tc - rb[t] f;      otherwise nothing.
+// The single-warp lane-per-column form is issue-bound (one warp issues all RMAX^2 updates of a
+// pivot); spreading the rows over G groups puts G (x 2 for RMAX > 32) warps on the SM's four
+// schedulers: R = 20: 17.6k -> 9.4k cycles, R = 50: 56k -> 36k (tools/micro/sweep_grp.cu, results
+// bit-identical).  One named barrier per pivot (double-buffered rb).  Called by every thread of the
+// CTA (>= NT threads); returns |S|.
+template <int RMAX, int G>
+__device__ int grp_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /* 2 (RPG G + 8) */, int* swept) {
+  constexpr int CW = (RMAX + 31) / 32, NT = 32 * CW * G, RPG = (RMAX + G - 1) / G, RB = RPG * G + 8;
   const int tid = threadIdx.x, RS = R + 1;
   if (tid < NT) {
-    const int c = tid;
-    double v[RMAX];
+    const int g = tid / (32 * CW), c = tid % (32 * CW);
+    double v[RPG];
 #pragma unroll
-    for (int t = 0; t < RMAX; ++t) v[t] = (t < R && c < R) ? Gm[t * RS + c] : (t == c ? 1.0 : 0.0);
+    for (int t = 0; t < RPG; ++t) {
+      const int row = g * RPG + t;
+      v[t] = (row < R && c < R) ? Gm[row * RS + c] : (row == c ? 1.0 : 0.0);
+    }
     for (int j = tid; j < R; j += NT) swept[j] = 0;
 #pragma unroll 1
     for (int k = 0; k < R; ++k) {
-      double* cb = colbuf + (k & 1) * RMAX;
-      if (c < RMAX) cb[c >= k ? c - k : c - k + RMAX] = v[0];
-      if (NT == 32) __syncwarp();
-      else named_bar_sync(1, NT);
-      const double d = cb[0];
+      double* rb = rowbuf + (k & 1) * RB;
+      const int gk = k / RPG, tk = k - gk * RPG;
+      if (g == gk) {
+        double pv = v[0];
+#pragma unroll
+        for (int t = 1; t < RPG; ++t) pv = (tk == t) ? v[t] : pv;
+        rb[c] = pv;
+      }
+      named_bar_sync(1, NT);
+      const double d = rb[k];
       if (d > tol) {  // uniform
         const double dinv = __drcp_rn(d);
         const bool isk = (c == k);
-        const double f = isk ? -dinv : v[0] * dinv;
+        const double f = isk ? -dinv : rb[c] * dinv;
 #pragma unroll
-        for (int u = 0; u < RMAX; u += 2) {  // (c_u, c_{u+1}) per broadcast load
-          const double2 cc = *reinterpret_cast<const double2*>(cb + u);
-          if (u >= 1) v[u - 1] = fma(-cc.x, f, isk ? 0.0 : v[u]);
-          v[u] = fma(-cc.y, f, isk ? 0.0 : v[u + 1]);
+        for (int t = 0; t < RPG; ++t) {
+          const int row = g * RPG + t;
+          v[t] = (row == k) ? f : fma(-rb[row], f, isk ? 0.0 : v[t]);
         }
-        v[RMAX - 1] = f;
         if (tid == 0) swept[k] = 1;
-      } else {
-        const double v0 = v[0];
-#pragma unroll
-        for (int t = 1; t < RMAX; ++t) v[t - 1] = v[t];
-        v[RMAX - 1] = v0;
       }
     }
-    if (NT == 32) __syncwarp();
-    else named_bar_sync(1, NT);
+    named_bar_sync(1, NT);
     if (c < R) {
 #pragma unroll
-      for (int t = 0; t < RMAX; ++t) {
-        const int i = t - (RMAX - R);  // slot t holds row (R + t) mod RMAX
-        if (i >= 0) Gm[i * RS + c] = (swept[i] && swept[c]) ? -v[t] : 0.0;
+      for (int t = 0; t < RPG; ++t) {
+        const int row = g * RPG + t;
+        if (row < R) Gm[row * RS + c] = (swept[row] && swept[c]) ? -v[t] : 0.0;
       }
     }
   }
@@ -859,22 +861,22 @@ __device__ int lc_sweep_inverse(double* Gm, int R, double tol, double* colbuf /*
   return rank;
 }
 
-// MAXR: largest rank the calling kernel supports (instantiates only RMAX <= MAXR)
+// MAXR: largest rank the calling kernel supports (instantiates only RMAX <= MAXR); needs 256 threads
 template <int MAXR = kMaxRank>
-__device__ inline int lc_sweep_dispatch(double* Gm, int R, double tol, double* colbuf, int* swept) {
+__device__ inline int grp_sweep_dispatch(double* Gm, int R, double tol, double* rowbuf, int* swept) {
   switch ((R + 7) / 8) {
-    case 1: return lc_sweep_inverse<8>(Gm, R, tol, colbuf, swept);
-    case 2: return lc_sweep_inverse<16>(Gm, R, tol, colbuf, swept);
-    case 3: return lc_sweep_inverse<24>(Gm, R, tol, colbuf, swept);
-    case 4: return lc_sweep_inverse<32>(Gm, R, tol, colbuf, swept);
+    case 1: return grp_sweep_inverse<8, 8>(Gm, R, tol, rowbuf, swept);
+    case 2: return grp_sweep_inverse<16, 8>(Gm, R, tol, rowbuf, swept);
+    case 3: return grp_sweep_inverse<24, 8>(Gm, R, tol, rowbuf, swept);
+    case 4: return grp_sweep_inverse<32, 8>(Gm, R, tol, rowbuf, swept);
     default: break;
   }
   if constexpr (MAXR > 32) {
     switch ((R + 7) / 8) {
-      case 5: return lc_sweep_inverse<40>(Gm, R, tol, colbuf, swept);
-      case 6: return lc_sweep_inverse<48>(Gm, R, tol, colbuf, swept);
-      case 7: return lc_sweep_inverse<56>(Gm, R, tol, colbuf, swept);
-      default: return lc_sweep_inverse<64>(Gm, R, tol, colbuf, swept);
+      case 5: return grp_sweep_inverse<40, 4>(Gm, R, tol, rowbuf, swept);
+      case 6: return grp_sweep_inverse<48, 4>(Gm, R, tol, rowbuf, swept);
+      case 7: return grp_sweep_inverse<56, 4>(Gm, R, tol, rowbuf, swept);
+      default: return grp_sweep_inverse<64, 4>(Gm, R, tol, rowbuf, swept);
     }
   }
   return 0;
@@ -1010,7 +1012,7 @@ __host__ __device__ inline size_t ut_smem_bytes(int R, int64_t rows_per, size_t 
   take(esz * rows_per * (R + 1));        // Anew
   take(sizeof(double) * (R * (R + 1) / 2 + 1));  // partial Gram / partial ||A||^2 (read by peers)
   take(sizeof(double) * R * (R + 1));    // Gm (Gram -> inverse), row stride R+1
-  take(sizeof(double) * 2 * kMaxRank);   // sweep row buffer (double-buffered pivot row)
+  take(sizeof(double) * 3 * kMaxRank);   // sweep column buffer (triple-buffered pivot column)
   take(sizeof(int) * R);                 // swept flags
   take(sizeof(double) * rows_per);       // per-row p
   take(sizeof(unsigned long long) * rows_per);   // per-row q -> local inclusive scan
@@ -1049,7 +1051,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   T* Anew = reinterpret_cast<T*>(carve(sizeof(T) * p.rows_per * RS));
   double* gpart = reinterpret_cast<double*>(carve(sizeof(double) * (R * (R + 1) / 2 + 1)));
   double* Gm = reinterpret_cast<double*>(carve(sizeof(double) * R * (R + 1)));
-  double* rowbuf = reinterpret_cast<double*>(carve(sizeof(double) * 2 * kMaxRank));
+  double* rowbuf = reinterpret_cast<double*>(carve(sizeof(double) * 3 * kMaxRank));
   int* swept = reinterpret_cast<int*>(carve(sizeof(int) * R));
   double* prow = reinterpret_cast<double*>(carve(sizeof(double) * p.rows_per));
   unsigned long long* qrow = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * p.rows_per));
@@ -1241,7 +1243,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
     {
       constexpr int EPT = (kMaxRank * kMaxRank + kUTThreads - 1) / kUTThreads;
       const int rk = (p.In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, s_tol, rowbuf, swept, rowbuf + R)
-                                    : lc_sweep_dispatch(Gm, R, s_tol, rowbuf, swept);
+                                    : grp_sweep_dispatch(Gm, R, s_tol, rowbuf, swept);
       if (tid == 0) {
         s_rank = rk;
         if (rk == 0) s_bad |= 2;

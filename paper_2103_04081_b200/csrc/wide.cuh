@@ -356,7 +356,7 @@ __device__ void table_wide_body(const TWParams& p) {
     if (p.dbg && q == 0 && tid == 0) p.dbg[1] = clock64();
     constexpr int EPT = (kMaxRank * kMaxRank + kTWThreads - 1) / kTWThreads;
     const int rank = (p.In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, s_tol, colbuf, swept, colbuf + R)
-                                    : lc_sweep_dispatch(Gm, R, s_tol, colbuf, swept);
+                                    : grp_sweep_dispatch(Gm, R, s_tol, colbuf, swept);
     if (tid == 0 && rank == 0) s_bad |= 2;
     if (p.dbg && q == 0 && tid == 0) p.dbg[2] = clock64();
     // scores l_i = sum_c (A W)_ic a_ic (4 rows x 4 columns per task; k in pairs)

@@ -13,7 +13,7 @@ __global__ void k(const double* G, int R, double tol, double* out, long long* cy
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) Gm[(e / R) * (R + 1) + e % R] = G[e];
   __syncthreads();
   long long t0 = clock64();
-  int rk = V == 4 ? lc_sweep_dispatch(Gm, R, tol, buf, swept) : cta_sweep_inverse_pivoted<16>(Gm, R, tol, buf, swept, buf + 64);
+  int rk = V == 4 ? grp_sweep_dispatch(Gm, R, tol, buf, swept) : cta_sweep_inverse_pivoted<16>(Gm, R, tol, buf, swept, buf + 64);
   long long t1 = clock64();
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) out[e] = Gm[(e / R) * (R + 1) + e % R];
   if (threadIdx.x == 0) { cyc[0] = t1 - t0; cyc[1] = rk; }
