@@ -52,8 +52,13 @@ struct FusedParams {
 
 // shared memory layout (bytes) -- mirrored by the host
 struct FusedLayout {
-  size_t zw, zu, fb, wt, ix, pt, mp, gp, gam, aold, anew, gpart, gm, prow, sc, rowbuf, swept, qtot, cdfs, total;
+  size_t zw, zu, fb, wt, ix, pt, mp, gp, gam, aold, anew, gpart, gm, prow, sc, rowbuf, swept, qtot, cdfs, xs, total;
 };
+// row pitch (elements) of the staged fiber segments: I_max rounded up to a 16-byte multiple
+__host__ __device__ inline int64_t fused_xpitch(int64_t Imax, size_t esz) {
+  const int64_t VE = 16 / (int64_t)esz;
+  return (Imax + VE - 1) / VE * VE;
+}
 __host__ __device__ inline int fused_rp(int R, size_t esz) {
   const int W = esz == 8 ? 2 : 4;
   return (R + W - 1) / W * W;
@@ -88,6 +93,7 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
   L.swept = take(sizeof(int) * R);
   L.qtot = take(sizeof(unsigned long long) * 2);
   L.cdfs = take(sizeof(uint64_t) * cdf_elems);
+  L.xs = take(esz * (size_t)BPC * fused_xpitch(Imax, esz));
   L.total = off + 16;
   return L;
 }
@@ -97,8 +103,8 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
 // fiber gather + contraction for ROWS rows per thread and RV vector groups of columns:
 // acc[u][g] += x(row u) * zw[lb][g]; zw rows padded to RV * W with zeros (stride RP).
 template <typename T, int ROWS, int RV>
-__device__ __forceinline__ void gather_contract(const T* __restrict__ Xn, int64_t es, int64_t In, const int64_t* fb,
-                                                const T* zw, int RP, int BPC, T* Mp, int R) {
+__device__ __forceinline__ void gather_contract(const T* xs, int64_t Ip, int64_t In, const int64_t* fb,
+                                                const T* zw, int RP, int BPC, T* Mp, int R, long long* dbg = nullptr) {
   using V = typename Vec<T>::type;
   constexpr int W = Vec<T>::W;
   const int tid = threadIdx.x;
@@ -112,34 +118,61 @@ __device__ __forceinline__ void gather_contract(const T* __restrict__ Xn, int64_
       for (int c = 0; c < W; ++c) a[c] = T(0);
     }
   constexpr int CH = 16;
+  if (dbg) dbg[16] = clock64();
   for (int c0 = 0; c0 < BPC; c0 += CH) {
     T xv[CH][ROWS];
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       const int lb = c0 + c;
-      const int64_t f = (lb < BPC) ? fb[lb] : -1;
 #pragma unroll
       for (int u = 0; u < ROWS; ++u) {
-        const int64_t i = tid + (int64_t)u * kFThreads;
-        xv[c][u] = (f >= 0 && i < In) ? __ldg(Xn + f + i * es) : T(0);
+        const int i = tid + u * kFThreads;
+        xv[c][u] = (lb < BPC && i < In) ? xs[lb * Ip + i] : T(0);  // padding fibers are staged as zeros
       }
+    }
+    if (dbg && c0 < 2 * CH) {
+      if (xv[CH - 1][ROWS - 1] == T(-12345)) xv[0][0] = T(0);
+      dbg[17 + 2 * (c0 / CH)] = clock64();
     }
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       const int lb = c0 + c;
       if (lb >= BPC) break;
       const V* z = reinterpret_cast<const V*>(zw + lb * RP);
+      if constexpr (sizeof(T) == 4) {
+        // packed fp32x2 FMA (FFMA2): two independent round-to-nearest FMAs per instruction, the same
+        // values as the scalar form with half the issue slots
+        uint64_t xx[ROWS];
 #pragma unroll
-      for (int g = 0; g < RV; ++g) {
-        const V zg = z[g];
-        const T* zt = reinterpret_cast<const T*>(&zg);
+        for (int u = 0; u < ROWS; ++u) asm("mov.b64 %0, {%1, %1};" : "=l"(xx[u]) : "f"((float)xv[c][u]));
 #pragma unroll
-        for (int u = 0; u < ROWS; ++u) {
-          T* a = reinterpret_cast<T*>(&acc[u][g]);
+        for (int g = 0; g < RV; ++g) {
+          const V zg = z[g];
+          const uint64_t* z2 = reinterpret_cast<const uint64_t*>(&zg);
 #pragma unroll
-          for (int cc = 0; cc < W; ++cc) a[cc] += xv[c][u] * zt[cc];
+          for (int u = 0; u < ROWS; ++u) {
+            uint64_t* a2 = reinterpret_cast<uint64_t*>(&acc[u][g]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a2[h]) : "l"(xx[u]), "l"(z2[h]));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < RV; ++g) {
+          const V zg = z[g];
+          const T* zt = reinterpret_cast<const T*>(&zg);
+#pragma unroll
+          for (int u = 0; u < ROWS; ++u) {
+            T* a = reinterpret_cast<T*>(&acc[u][g]);
+#pragma unroll
+            for (int cc = 0; cc < W; ++cc) a[cc] += xv[c][u] * zt[cc];
+          }
         }
       }
+    }
+    if (dbg && c0 < 2 * CH) {
+      if (reinterpret_cast<T*>(&acc[ROWS - 1][RV - 1])[W - 1] == T(-12345)) xv[0][0] = T(1);
+      dbg[18 + 2 * (c0 / CH)] = clock64();
     }
   }
 #pragma unroll
@@ -160,17 +193,17 @@ __device__ __forceinline__ void gather_contract(const T* __restrict__ Xn, int64_
 }
 
 template <typename T, int ROWS>
-__device__ __forceinline__ void gather_dispatch(const T* Xn, int64_t es, int64_t In, const int64_t* fb, const T* zw,
-                                                int RP, int BPC, T* Mp, int R) {
+__device__ __forceinline__ void gather_dispatch(const T* xs, int64_t Ip, int64_t In, const int64_t* fb, const T* zw,
+                                                int RP, int BPC, T* Mp, int R, long long* dbg = nullptr) {
   switch (RP / Vec<T>::W) {
-    case 1: gather_contract<T, ROWS, 1>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
-    case 2: gather_contract<T, ROWS, 2>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
-    case 3: gather_contract<T, ROWS, 3>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
-    case 4: gather_contract<T, ROWS, 4>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
-    case 5: gather_contract<T, ROWS, 5>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
-    case 6: gather_contract<T, ROWS, 6>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
-    case 7: gather_contract<T, ROWS, 7>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
-    default: gather_contract<T, ROWS, 8>(Xn, es, In, fb, zw, RP, BPC, Mp, R); break;
+    case 1: gather_contract<T, ROWS, 1>(xs, Ip, In, fb, zw, RP, BPC, Mp, R, dbg); break;
+    case 2: gather_contract<T, ROWS, 2>(xs, Ip, In, fb, zw, RP, BPC, Mp, R, dbg); break;
+    case 3: gather_contract<T, ROWS, 3>(xs, Ip, In, fb, zw, RP, BPC, Mp, R, dbg); break;
+    case 4: gather_contract<T, ROWS, 4>(xs, Ip, In, fb, zw, RP, BPC, Mp, R, dbg); break;
+    case 5: gather_contract<T, ROWS, 5>(xs, Ip, In, fb, zw, RP, BPC, Mp, R, dbg); break;
+    case 6: gather_contract<T, ROWS, 6>(xs, Ip, In, fb, zw, RP, BPC, Mp, R, dbg); break;
+    case 7: gather_contract<T, ROWS, 7>(xs, Ip, In, fb, zw, RP, BPC, Mp, R, dbg); break;
+    default: gather_contract<T, ROWS, 8>(xs, Ip, In, fb, zw, RP, BPC, Mp, R, dbg); break;
   }
 }
 
@@ -220,6 +253,8 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
   int* swept = reinterpret_cast<int*>(f_sm + L.swept);
   unsigned long long* qtot = reinterpret_cast<unsigned long long*>(f_sm + L.qtot);
   uint64_t* cdfs = reinterpret_cast<uint64_t*>(f_sm + L.cdfs);
+  T* xs = reinterpret_cast<T*>(f_sm + L.xs);
+  const int64_t Ip = fused_xpitch(p.Imax, sizeof(T));
   __shared__ int s_bad;
   __shared__ double s_red[kFThreads / 32];
   __shared__ unsigned long long s_wtot[kFThreads / 32];
@@ -329,6 +364,33 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
       fb[lb] = p.pitch[n] ? jrow * p.pitch[n] : offn;
     }
     __syncthreads();
+    // TensorSamp (Alg. 5) issue: this CTA's fiber segments -> shared memory (xs[lb][i], pitch Ip) by
+    // cp.async, completed at the gather.  The copies overlap the SKR rows and, for the next step's
+    // batch, the whole tail of the current step.  (Direct loads at the gather were bound by the
+    // SM's outstanding-miss limit: ~4.6k cycles per 16-fiber round, tools/micro/gat_lat.cu.)
+    {
+      const T* Xn = p.Xg[n];
+      const int64_t In = p.dims[n], es = p.estride[n];
+      constexpr int VE = 16 / (int)sizeof(T);
+      const int nv = (int)((In + VE - 1) / VE);
+      for (int e = tid; e < p.BPC * nv; e += kFThreads) {
+        const int lb = e / nv, v = e % nv;
+        const int64_t f = fb[lb];
+        const int64_t i0 = (int64_t)v * VE;
+        T* dst = xs + lb * Ip + i0;
+        if (f < 0) {  // padding fiber: zeros, so the contraction needs no per-fiber test
+#pragma unroll
+          for (int j = 0; j < VE; ++j) dst[j] = T(0);
+        } else if (es == 1 && (f % VE) == 0) {
+          cp_async16(dst, Xn + f + i0, (int)(cmin64(VE, In - i0) * (int64_t)sizeof(T)));
+        } else {
+#pragma unroll
+          for (int j = 0; j < VE; ++j)
+            if (i0 + j < In) cp_async_small<sizeof(T)>(dst + j, Xn + f + (i0 + j) * es, (int)sizeof(T));
+        }
+      }
+      cp_async_commit();
+    }
     // SKR rows (Alg. 1): z = (*)_{k != n} A^(k)(i_k, :); zw = w z; padded to RP with zeros
     for (int e = tid; e < p.BPC * RP; e += kFThreads) {
       const int lb = e / RP, rr = e % RP;
@@ -361,13 +423,18 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     const int64_t r_beg = min((int64_t)q * rpc, In), r_end = min(r_beg + rpc, In);
     const int nr = (int)(r_end - r_beg);
     // ------------------------------------------------ (1) gather (Alg. 5) + partial contractions
-    gather_dispatch<T, ROWS>(p.Xg[n], p.estride[n], In, fb, zw, RP, p.BPC, Mp, R);
+    cp_async_wait<0>();  // this batch's fiber segments (issued by sample_own)
+    __syncthreads();
+    gather_dispatch<T, ROWS>(xs, Ip, In, fb, zw, RP, p.BPC, Mp, R,
+                             (p.dbg && q == 0 && tid == 0 && s == 1) ? p.dbg : nullptr);
+    F_MARK(14);
     for (int e = tid; e < R * R; e += kFThreads) {
       const int r1 = e / R, r2 = e % R;
       T g = T(0);
       for (int lb = 0; lb < p.BPC; ++lb) g += zw[lb * RP + r1] * zu[lb * RP + r2];
       Gp[e] = g;
     }
+    F_MARK(15);
 #pragma unroll 8
     for (int e = tid; e < nr * R; e += kFThreads) {  // old rows of the block this CTA updates
       const int il = e / R, c = e % R;

@@ -51,7 +51,9 @@ if os.environ.get("CPSGD_DEBUG_TIMERS") and os.environ.get("FUSED_TIMERS"):
     names = ["gather", "sync1", "reduce+update", "gram-part", "sync2", "gram-sum+sweep", "scores", "scan", "sync3",
              "cdf", "sync4", "sample"]
     print(" | ".join(f"{names[i]}:{t[i + 1] - t[i]}" for i in range(12)), "| total", t[12] - t[0])
-    print("gram-sum", t[13] - t[5], "sweep", t[6] - t[13])
+    print("gram-sum", t[13] - t[5], "sweep", t[6] - t[13], "| gather: contract", t[14] - t[0], "Gamma part", t[15] - t[14],
+          "Aold", t[1] - t[15])
+    print("  contract: ld0", t[17] - t[16], "fma0", t[18] - t[17], "ld1", t[19] - t[18], "fma1", t[20] - t[19], "store", t[14] - t[20])
 elif os.environ.get("CPSGD_DEBUG_TIMERS"):
     h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=a.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta, seed=0,
               graphs=False, wide=bool(a.wide), fused=bool(a.fused))
@@ -67,14 +69,10 @@ elif os.environ.get("CPSGD_DEBUG_TIMERS"):
         print(f"  CTAs {m.sum()}: start spread {(g0.max() - base) / 1e3:.1f} us, end min {(g1.min() - base) / 1e3:.1f} "
               f"max {(g1.max() - base) / 1e3:.1f} us, duration median {np.median(g1 - g0) / 1e3:.1f} us; "
               f"distinct SMs {len(set(t[3072:3072 + m.sum()]))}")
-        print("  finish(tile 0): chunk0 A-load", t[38] - t[37], "AGamma", t[39] - t[38], "part+fence+atomic", t[40] - t[39],
-              "| last CTA = chunk", t[60], ": reduce", t[41] - (t[40] if t[60] == 0 else t[48]), "update", t[42] - t[41])
         print("  stage 8: load issue->data", t[18] - t[23], "wait xh/xl", t[19] - t[18], "split", t[20] - t[19],
               "split->mma start", t[21] - t[20], "mma issue", t[22] - t[21], "| mma thread: wait sdone", t[25] - t[24],
-              "wait bfull", t[21] - t[25], "| split: wait xfull", t[18] - t[26], "stage 8->9", t[27] - t[26],
+              "wait A image", t[21] - t[25], "| split: wait xfull", t[18] - t[26], "stage 8->9", t[27] - t[26],
               "stage 8->12 /4", (t[28] - t[26]) / 4)
-        print("  z writer st 8: wait_group", t[41] - t[40], "bar", t[42] - t[41], "issue+lds+cvt", t[43] - t[42],
-              "afree", t[44] - t[43], "st+arrive", t[45] - t[44], "| z top vs split top", t[40] - t[26])
     if t[107]:
         nm = ["cdf stage", "draw", "skr", "zw/img", "gamma", "cluster+fence", "last"]
         print("k_sample_wide (CTA 0) cycles: " + " | ".join(f"{nm[i]} {t[101 + i] - t[100 + i]}" for i in range(7)))
@@ -84,13 +82,7 @@ elif os.environ.get("CPSGD_DEBUG_TIMERS"):
         base = g0.min()
         print(f"  k_sample_wide CTAs {m.sum()}: start spread {(g0.max() - base) / 1e3:.1f} us, end min "
               f"{(g1.min() - base) / 1e3:.1f} max {(g1.max() - base) / 1e3:.1f} us, median dur {np.median(g1 - g0) / 1e3:.1f} us")
-        import struct
-        print("  NS residuals:", [struct.unpack('d', struct.pack('q', v))[0] for v in t[200:208]])
         print("k_table_wide cycles: gram-sum", t[1] - t[0], "sweep", t[2] - t[1], "scores", t[3] - t[2], "scan", t[4] - t[3])
-    if a.wide and not t[107]:  # k_table_sample marks
-        names = ["gram+sync", "sweep", "scores", "scan+cdf", "draw", "skr+zw+gamma"]
-        print("k_table_sample cycles: " + " | ".join(f"{names[i]} {t[i + 1] - t[i]}" for i in range(6)),
-              "| total", t[6] - t[0])
-    else:
+    if not a.wide:
         names = ["start", "stageB", "gram-synced", "sweep-start", "sweep-done", "scores-done", "cdf-synced", "sampled"]
         print(" ".join(f"{names[i]}:{t[i] - t[0]}" for i in range(8)))
