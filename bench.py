@@ -231,10 +231,14 @@ def run_ours(args, cfg):
             return None
         t_k = kern[name]["avg_us"] * 1e-6
         ach = per_launch / t_k / 1e9
+        # DRAM bytes (read + write) of this kernel from one ncu --set full capture (profiles/traffic.json,
+        # written by tools/ncu_summary.py traffic): per launch, or per sweep for the fused kernel
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tfile):
-            traffic = json.load(open(tfile)).get(f"{cfg.name}/{args.sampler}/{name}")
+            ent = json.load(open(tfile)).get(f"{cfg.name}/{args.sampler}/{name}")
+            if ent:
+                traffic = ent["bytes"] / ent.get("sweeps", 1) * (prof_sweeps if "sweeps" in ent else 1)
         return {"kernel": name, "bound": "hbm", "achieved": round(ach, 2), "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "_fallback" not in peaks else "fallback",

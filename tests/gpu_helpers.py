@@ -67,3 +67,40 @@ def near_boundary(p, tol_abs):
     """entries whose fixed-point value p 2^32 lies within tol_abs of a rounding boundary (x.5)"""
     s = np.asarray(p, np.float64) * 2.0 ** 32
     return np.abs(s - np.floor(s) - 0.5) <= tol_abs
+
+
+def gather_fibers_torch(Xd, dims, n, idx):
+    """X_(n)(:, F) as a (B, I_n) fp64 array read from the seeded input tensor on the device (input
+    data from synth, first-index-fastest layout -- not an output of the CUDA path)."""
+    import torch
+
+    strides = np.cumprod([1] + list(dims[:-1])).astype(np.int64)
+    base = np.zeros(idx.shape[0], np.int64)
+    pos = 0
+    for k in range(len(dims)):
+        if k == n:
+            continue
+        base += idx[:, pos].astype(np.int64) * strides[k]
+        pos += 1
+    off = (torch.from_numpy(base).to(Xd.device)[:, None]
+           + torch.arange(dims[n], device=Xd.device, dtype=torch.int64)[None, :] * int(strides[n]))
+    return Xd[off].double().cpu().numpy()
+
+
+def oracle_gradient_from_fibers(XF, dims, factors, n, strategy, B, idx, pj):
+    """eq:gradient1/2 for row-wise strategies from pre-gathered fibers XF (B, I_n):
+    the oracle's SKR rows (oracle.skr), D = diag(1/p_j) and the 1/(B J_n) scale of oracle.gradient,
+    for problems whose full tensor does not fit the oracle.  Pinned against oracle.gradient in
+    tests/test_oracle_pins.py::test_gradient_from_fibers_matches_oracle."""
+    assert strategy in ("uniform", "leverage", "euclidean")
+    fs = [np.asarray(A, np.float64) for A in factors]
+    Z = oracle.skr(fs, n, idx)
+    Jn = float(np.prod([d for k, d in enumerate(dims) if k != n]))
+    scale = 1.0 / (float(B) * Jn)
+    d = 1.0 / np.asarray(pj, np.float64)
+    C1 = Z.T @ (d[:, None] * Z)
+    C2 = np.asarray(XF, np.float64).T @ (d[:, None] * Z)
+    Gam = scale * C1
+    M = scale * C2
+    G = scale * (fs[n] @ C1 - C2)
+    return G, Gam, M

@@ -13,7 +13,8 @@ import pytest
 
 import oracle
 import synth
-from gpu_helpers import S, TOL, handle, make_problem, near_boundary, oracle_step, oracle_tables, rel_err, to_dev
+from gpu_helpers import (S, TOL, gather_fibers_torch, handle, make_problem, near_boundary, oracle_gradient_from_fibers,
+                         oracle_step, oracle_tables, rel_err, to_dev)
 
 pytestmark = pytest.mark.gpu
 
@@ -259,6 +260,38 @@ def test_c2_full_size_step_and_fit(path):
         assert rel_err(G_g, G_o, scale) <= 1e-4
         h.close()
         del Xd
+
+
+def test_c4_full_size_tcgen05_step():
+    """C4 at full size (2000^3 fp32 = 32 GB, R50, B4096, leverage) through the wide tcgen05 path in
+    the launch configuration bench.py --workload C4 times: sampled indices and weights bit-exact,
+    G and Gamma within 1e-4 of the oracle from the same seeded input (the oracle reads the sampled
+    fibers of the seeded tensor; its SKR rows, weights and scale are its own)."""
+    cfg = synth.CONFIGS["C4"]
+    dev = torch.device("cuda:0")
+    Xd, _, xn = synth.tensor_torch(cfg, device=dev)
+    Ad0 = synth.init_factors_torch(cfg, xn, device=dev)
+    A0 = [a.cpu().numpy() for a in Ad0]
+    tabs = oracle_tables("leverage", A0)
+    tq = [(t[1], t[2]) for t in tabs]
+    for n in range(3):
+        Ad = [a.clone() for a in Ad0]
+        h = handle(cfg, Xd, Ad, "leverage", seed=0, fused=False, mode_major=True)
+        h.iter = n
+        idx_o, w_o, pj = oracle.sample(cfg.dims, n, oracle.STRATEGIES["leverage"], cfg.batch, tq, 0, n)
+        idx_g, w_g = h.sample(n, n)
+        assert np.array_equal(idx_g.cpu().numpy(), idx_o) and np.array_equal(w_g.cpu().numpy(), w_o)
+        h.step(n)
+        G_g, m, Gam_g = h.get_grad()
+        assert m == n
+        XF = gather_fibers_torch(Xd, cfg.dims, n, idx_o)
+        G_o, Gam_o, M_o = oracle_gradient_from_fibers(XF, cfg.dims, A0, n, "leverage", cfg.batch, idx_o, pj)
+        scale = np.linalg.norm(np.asarray(A0[n], np.float64) @ Gam_o) + np.linalg.norm(M_o)
+        assert rel_err(G_g, G_o, scale) <= 1e-4
+        assert rel_err(Gam_g, Gam_o, np.linalg.norm(Gam_o)) <= 1e-4
+        h.close()
+        del Ad
+        torch.cuda.empty_cache()
 
 
 # ------------------------------------------------------------------------------------------ e2e host path

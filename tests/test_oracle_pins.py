@@ -527,3 +527,28 @@ def test_recovers_noiseless_exact_rank(orc, strategy):
     fs, _, _ = orc.run(X, A0, orc.STRATEGIES[strategy], orc.STEP_ADAPTIVE, 36, 3 * 3000, window=[6, 6],
                        eta=0.3, seed=0)
     assert orc.fit(X, fs) >= 0.99
+
+
+# ---------------------------------------------------------------------------------------- test helpers
+@pytest.mark.parametrize("strategy", ROWWISE)
+def test_gradient_from_fibers_matches_oracle(orc, strategy):
+    """The full-size GPU test's reference (gpu_helpers.oracle_gradient_from_fibers over fibers read
+    by gpu_helpers.gather_fibers_torch from the flat first-index-fastest tensor) equals
+    oracle.tensor_samp / oracle.gradient on a small problem with a ragged mode."""
+    torch = pytest.importorskip("torch")
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from gpu_helpers import gather_fibers_torch, oracle_gradient_from_fibers
+
+    dims, R, B = (7, 5, 6), 3, 40
+    fs = rand_factors(dims, R, seed=4)
+    X = rand_tensor(dims, seed=5)
+    tabs = tables_for(orc, strategy, fs)
+    for n in range(3):
+        idx, w, pj = orc.sample(dims, n, orc.STRATEGIES[strategy], B, tabs, 9, 2 + n)
+        XF = gather_fibers_torch(torch.from_numpy(X), dims, n, idx)
+        assert np.array_equal(XF, orc.tensor_samp(X, dims, n, idx).T)
+        G, Gam, M = oracle_gradient_from_fibers(XF, dims, fs, n, strategy, B, idx, pj)
+        G_o, Gam_o, M_o = orc.gradient(X, dims, fs, n, orc.STRATEGIES[strategy], B, idx, pj)
+        for a, b in ((G, G_o), (Gam, Gam_o), (M, M_o)):
+            assert np.allclose(a, b, rtol=1e-12, atol=1e-12 * np.abs(b).max())

@@ -2,6 +2,9 @@
 
     python tools/ncu_summary.py full  <report.ncu-rep> [--bytes-per-launch KERNEL=BYTES ...]
     python tools/ncu_summary.py launches <launches.csv>
+    python tools/ncu_summary.py traffic <report.ncu-rep> <workload/sampler> [sweeps=S]
+        -> merges {"<workload/sampler>/<kernel>": {"bytes": dram read+write of its first captured
+           launch[, "sweeps": S]}} into profiles/traffic.json (bench.py's roofline "traffic")
 
 Reads the report with ``ncu -i ... --page raw --csv`` (no GPU needed) and prints, per profiled
 launch: duration, DRAM bytes read/written (the roofline ``traffic``), DRAM / SM throughput, pipe
@@ -86,7 +89,7 @@ def full(report: str, bpl: dict) -> str:
     return "\n".join(lines)
 
 
-def launches(path: str) -> str:
+def launches(path: str, only: str = "") -> str:
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr = rows[0]
     ix = {h: i for i, h in enumerate(hdr)}
@@ -95,6 +98,8 @@ def launches(path: str) -> str:
         if r[ix["Metric Name"]] != "gpu__time_duration.sum":
             continue
         name = r[ix["Kernel Name"]].split("(")[0].replace("void ", "")
+        if only and not name.startswith(only):
+            continue
         t = float(r[ix["Metric Value"]]) * {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(r[ix["Metric Unit"]], 1.0)
         agg.setdefault(name, []).append(t)
     tot = sum(sum(v) for v in agg.values()) or 1.0
@@ -105,11 +110,40 @@ def launches(path: str) -> str:
     return "\n".join(lines) + "\n"
 
 
+def traffic(report: str, key: str, sweeps: int | None) -> str:
+    import json
+    import os
+    hdr, units, rows = _raw(report)
+    ix = {h: i for i, h in enumerate(hdr)}
+    tfile = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "traffic.json")
+    data = json.load(open(tfile)) if os.path.exists(tfile) else {}
+    seen = set()
+    for r in rows:
+        name = r[ix["Kernel Name"]].split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
+        if name in seen:
+            continue
+        seen.add(name)
+        b = sum(_to_bytes(r[ix[k]], units[ix[k]]) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        ent = {"bytes": b}
+        if sweeps and name == "k_sweep_fused":
+            ent["sweeps"] = sweeps
+        data[f"{key}/{name}"] = ent
+    json.dump(data, open(tfile, "w"), indent=1, sort_keys=True)
+    return json.dumps(data, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
+    if mode == "traffic":
+        sw = [int(a.split("=")[1]) for a in sys.argv[4:] if a.startswith("sweeps=")]
+        print(traffic(path, sys.argv[3], sw[0] if sw else None))
+        sys.exit(0)
     bpl = {}
     for a in sys.argv[3:]:
         if "=" in a:
             k, v = a.split("=", 1)
             bpl[k] = float(v)
-    print(full(path, bpl) if mode == "full" else launches(path))
+    if mode == "full":
+        print(full(path, bpl))
+    else:
+        print(launches(path, sys.argv[3] if len(sys.argv) > 3 else ""))
