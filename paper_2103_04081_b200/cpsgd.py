@@ -23,7 +23,7 @@ FLAG_MODE_MAJOR, FLAG_NO_GRAPH, FLAG_EXTERNAL_COMM, FLAG_NO_FUSED, FLAG_NO_WIDE,
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 KERNEL_NAMES = ["k_sample", "k_gather", "k_update_table", "k_table", "k_reduce_partials", "nccl", "k_fit",
                 "k_sweep_fused", "k_gather_update", "k_zw_gamma", "k_gather_update_tc", "k_table_sample",
-                "k_update_wide", "k_table_wide", "k_sample_wide"]
+                "k_update_wide", "k_scores_wide", "k_sample_wide"]
 STATUS = {0: "CP_OK", -1: "CP_EINVAL", -2: "CP_ERANGE", -3: "CP_EDEGENERATE", -4: "CP_ENOMEM", -5: "CP_ECUDA",
           -6: "CP_ENCCL", -7: "CP_ESTATE", -8: "CP_ENONFINITE"}
 

@@ -78,7 +78,7 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
-enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kKGatherUpdate, kKZwGamma, kKGatherUpdateTC, kKTableSample, kKUpdateWide, kKTableWide, kKSampleWide, kNumKernelIds };
+enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kKGatherUpdate, kKZwGamma, kKGatherUpdateTC, kKTableSample, kKUpdateWide, kKScoresWide, kKSampleWide, kNumKernelIds };
 
 struct ProfRec {
   int id;
@@ -152,6 +152,12 @@ struct cp_sgd_s {
   unsigned* gu_cnt = nullptr;    // wide path: per-tile arrival counters (unused)
   double* uw_gpart = nullptr;    // wide path: k_update_wide table partials [CTAs][R(R+1)/2]
   double* uw_rownorm = nullptr;  // wide path: Euclidean row norms [I_max]
+  unsigned* uw_cnt = nullptr;    // wide path: k_update_wide CTA arrival counter
+  double* tw_W = nullptr;        // wide path: W = swept Gram inverse [R][R] (or ||A||_F^2)
+  int* tw_stat = nullptr;        // wide path: rank, bad bits of the table being built
+  unsigned long long* sc_q = nullptr;  // wide path: quantised weights of the table being built [I_max]
+  unsigned* sc_cnt = nullptr;    // wide path: k_update_wide score-phase CTA arrival counter
+  unsigned* uw_flag = nullptr;   // wide path: W-ready epoch (monotonic)
   void* sw_gcl = nullptr;        // wide path: k_sample_wide cluster partials of Gamma
   unsigned* sw_cnt = nullptr;    // wide path: k_sample_wide arrival counter
   bool use_tc = false;           // fp32 wide path on tcgen05 (k_gather_update_tc), else the FFMA mainloop
@@ -648,12 +654,6 @@ cp_status launch_gu(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
   }
 }
 
-int ut_cluster(int64_t In) {
-  int CU = 1;
-  while (CU < 16 && CU * 32 < In) CU *= 2;
-  return CU;
-}
-
 int64_t ts_cdf_elems(const cp_sgd_s* h, int next_mode) {
   if (next_mode < 0 || h->sampler == CP_UNIFORM) return 0;
   int64_t c = 0;
@@ -662,7 +662,7 @@ int64_t ts_cdf_elems(const cp_sgd_s* h, int next_mode) {
   return c;
 }
 
-// ---- wide path: k_update_wide -> k_table_wide -> k_sample_wide (wide.cuh) ----
+// ---- wide path: k_update_wide (+ the Gram inverse in its last cluster, the scores, the scan) -> k_sample_wide (wide.cuh) ----
 template <typename T>
 cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
   ProfScope ps(h, kKUpdateWide);
@@ -686,7 +686,19 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   p.eps = h->eps;
   p.gpart = h->uw_gpart;
   p.rownorm = h->uw_rownorm;
-  const size_t smem = uw_smem_bytes(h->R, sizeof(T));
+  p.W = h->tw_W;
+  p.tstat = h->tw_stat;
+  p.cnt = h->uw_cnt;
+  p.flag = h->uw_flag;
+  p.cnt2 = h->sc_cnt;
+  p.qbuf = h->sc_q;
+  p.p_out = h->pprob[n];
+  p.cdf = h->cdf[n];
+  p.Tout = h->Ttot + n;
+  p.status = h->status_dev;
+  p.qch = std::min<int64_t>(h->dims[n], 4096);
+  p.dbg = h->dbg;
+  const size_t smem = uw_smem_bytes(h->R, sizeof(T), p.qch);
   static bool attr_set = false;
   if (!attr_set) {
     allow_max_dyn_smem(k_update_wide<T>);
@@ -697,63 +709,20 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   lc.blockDim = dim3(kWThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = kUWCluster;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  // every CTA waits for the Gram inverse of the last cluster: the grid must be co-resident
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
   lc.attrs = at;
-  lc.numAttrs = 1;
+  lc.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&lc, k_update_wide<T>, p);
   h->launches++;
   if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_update_wide launch: %s", cudaGetErrorString(e));
   return check_launch(h, "k_update_wide");
-}
-
-template <typename T>
-cp_status launch_tw_t(cp_sgd_s* h, int n) {
-  if (h->sampler == CP_UNIFORM) return CP_OK;  // uniform tables are constant
-  ProfScope ps(h, kKTableWide);
-  TWParams p;
-  memset(&p, 0, sizeof p);
-  const int CU = ut_cluster(h->dims[n]);
-  p.R = h->R;
-  p.strategy = h->sampler;
-  p.In = h->dims[n];
-  p.rows_per = ceil_div(h->dims[n], CU);
-  p.nparts = (int)ceil_div(ceil_div(h->dims[n], kUWRows), kUWCluster);  // k_update_wide clusters
-  p.gpart = h->uw_gpart;
-  p.rownorm = h->uw_rownorm;
-  p.A = h->factors[n];
-  p.esz = (int)sizeof(T);
-  p.p_out = h->pprob[n];
-  p.cdf = h->cdf[n];
-  p.Tout = h->Ttot + n;
-  p.status = h->status_dev;
-  p.dbg = h->dbg;
-  const size_t smem = tw_smem_bytes(h->R, p.rows_per);
-  static bool attr_set = false;
-  if (!attr_set) {
-    allow_max_dyn_smem(k_table_wide<T>);
-    cudaFuncSetAttribute(k_table_wide<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr_set = true;
-  }
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(CU, 1, 1);
-  lc.blockDim = dim3(kTWThreads, 1, 1);
-  lc.dynamicSmemBytes = smem;
-  lc.stream = h->ls;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CU;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  lc.attrs = at;
-  lc.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&lc, k_table_wide<T>, p);
-  h->launches++;
-  if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_table_wide launch (cluster %d, smem %zu): %s", CU, smem, cudaGetErrorString(e));
-  return check_launch(h, "k_table_wide");
 }
 
 template <typename T>
@@ -944,7 +913,6 @@ cp_status phase1(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, int 
   if (wide_mode(h, n)) {  // update, table of the updated A^(n), the next batch (+ its zw rows and Gamma)
     const bool f64 = h->dtype == CP_F64;
     cp_status st = f64 ? launch_uw_t<double>(h, n, alpha, alpha_dev) : launch_uw_t<float>(h, n, alpha, alpha_dev);
-    if (!st) st = f64 ? launch_tw_t<double>(h, n) : launch_tw_t<float>(h, n);
     if (!st && next_mode >= 0) {
       st = launch_prefetch(h, next_mode);
       if (!st) h->pref_mode = next_mode;
@@ -1273,8 +1241,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
         bmx = std::max(bmx, h->bmax[k]);
         cdfmax = std::max(cdfmax, ts_cdf_elems(h, k));
       }
-      const int CU = ut_cluster(h->dims[n]);
-      const size_t us = std::max(tw_smem_bytes(h->R, ceil_div(h->dims[n], CU)),
+      const size_t us = std::max(uw_smem_bytes(h->R, h->esz, std::min<int64_t>(h->dims[n], 4096)),
                                  sw_smem_bytes(h->N, h->R, cdfmax, h->esz));
       if (gs + 1024 <= (size_t)optin && us <= (size_t)h->sample_smem) {
         h->gu_ck[n] = (int)CK;
@@ -1287,6 +1254,15 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       const int P = h->R * (h->R + 1) / 2;
       ALLOC(h->uw_gpart, sizeof(double) * ceil_div(Imax, kUWRows) * P);
       ALLOC(h->uw_rownorm, sizeof(double) * Imax);
+      ALLOC(h->uw_cnt, sizeof(unsigned));
+      ALLOC(h->sc_cnt, sizeof(unsigned));
+      cudaMemsetAsync(h->uw_cnt, 0, sizeof(unsigned), h->stream);
+      cudaMemsetAsync(h->sc_cnt, 0, sizeof(unsigned), h->stream);
+      ALLOC(h->uw_flag, sizeof(unsigned));
+      cudaMemsetAsync(h->uw_flag, 0, sizeof(unsigned), h->stream);
+      ALLOC(h->tw_W, sizeof(double) * h->R * h->R);
+      ALLOC(h->tw_stat, sizeof(int) * 2);
+      ALLOC(h->sc_q, sizeof(unsigned long long) * Imax);
       int64_t ncl = 0;
       for (int n = 0; n < h->N; ++n) ncl = std::max(ncl, ceil_div(ceil_div(h->bmax[n], kSWFibers), kSWCluster));
       ALLOC(h->sw_gcl, h->esz * ncl * h->R * h->R);
@@ -1405,6 +1381,12 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->gu_cnt);
   cudaFree(h->uw_gpart);
   cudaFree(h->uw_rownorm);
+  cudaFree(h->uw_cnt);
+  cudaFree(h->sc_cnt);
+  cudaFree(h->uw_flag);
+  cudaFree(h->tw_W);
+  cudaFree(h->tw_stat);
+  cudaFree(h->sc_q);
   cudaFree(h->sw_gcl);
   cudaFree(h->sw_cnt);
   cudaFree(h->iter_dev);

@@ -2,11 +2,13 @@
 //
 //   k_gather_update[_tc]  (a4-a6)  chunk partials of M = X_F diag(w) Z_F            (all SMs)
 //   k_update_wide         (a6-a8)  M = sum_c M_c (chunk order), G = A Gamma - M, fixed / adaptive
-//                                  update; partial fp64 Grams (leverage) or row norms (Euclidean)
-//                                  of the new rows -> the table kernel               (all SMs)
-//   k_table_wide          (a1)     Gram -> symmetric-sweep inverse -> leverage scores, or the
-//                                  Euclidean ratios; fixed-point quantisation; integer scan -> CDF
-//                                  (one cluster: the R-pivot chain is inherently serial)
+//                    + (a1)        update; partial fp64 Grams (leverage) or row norms (Euclidean) of
+//                                  the new rows; the LAST cluster sums the cluster partials and its
+//                                  rank 0 inverts the Gram by the symmetric sweep -> W, |S| (the
+//                                  R-pivot chain is inherently serial: one CTA) while every other CTA
+//                                  waits (one resident wave, cooperative launch); then every CTA
+//                                  scores and quantises its own rows, the LAST CTA scans -> CDF, T
+//                                                                                     (all SMs)
 //   k_sample_wide         (a2-a4)  the next batch: draws, SKR rows, weighted rows / tcgen05 images,
 //                                  Gamma = Z_F^T diag(w) Z_F (clusters of 8, last cluster sums)  (all SMs)
 //
@@ -18,9 +20,18 @@
 
 namespace cps {
 
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define WMARK(cond, slot)                                   \
+  do {                                                      \
+    if (p.dbg && (cond) && threadIdx.x == 0) p.dbg[slot] = gtimer(); \
+  } while (0)
+
 constexpr int kUWRows = 16;     // rows of A^(n) per k_update_wide CTA (divides the 128-row tiles)
 constexpr int kWThreads = 256;
-constexpr int kTWThreads = 256;  // k_table_wide (512 would cap registers at 128 and spill the sweep)
 constexpr int kSWFibers = 32;   // fibers per k_sample_wide CTA
 constexpr int kSWCluster = 8;
 constexpr int kUWCluster = 8;   // k_update_wide CTAs per cluster (table partials summed over DSMEM)
@@ -41,19 +52,270 @@ struct UWParams {
   double eta, b, eps;
   double* gpart;      // [clusters][R(R+1)/2] (leverage) or [clusters] (Euclidean)
   double* rownorm;    // [I_n] (Euclidean)
+  double* W;          // out (last CTA): leverage: the swept inverse W [R][R]; Euclidean: W[0] = ||A||_F^2
+  int* tstat;         // out (last CTA): [0] rank |S| (leverage), [1] bad bits (2 degenerate, 8 non-finite)
+  unsigned* cnt;      // cluster arrival counter (zero between launches)
+  unsigned* flag;     // W-ready epoch: incremented once per launch by the sweeping CTA (never reset)
+  unsigned* cnt2;     // CTA arrival counter of the scores (zero between launches)
+  unsigned long long* qbuf;  // [I_n] quantised weights
+  double* p_out;      // table: probabilities, CDF, T, status
+  uint64_t* cdf;
+  uint64_t* Tout;
+  int* status;
+  int64_t qch;        // last CTA's scan: q entries staged per round
+  long long* dbg;
 };
 
-// (a6-a8) + the parallel half of (a1): grid = ceil(I_n / kUWRows); dynamic shared memory
-__host__ __device__ inline size_t uw_smem_bytes(int R, size_t esz) {
-  return (esz * (3 * (size_t)kUWRows * (R + 1) + (size_t)R * R) + 15) / 16 * 16 +
-         sizeof(double) * (size_t)(R * (R + 1) / 2) + 16;
+// (a6-a8) + (a1) up to the inverse: grid = ceil(I_n / kUWRows); dynamic shared memory = the step's
+// working set, or the last CTA's sweep workspace (Gram, sweep buffers), whichever is larger
+__host__ __device__ inline size_t uw_sweep_ws_bytes(int R) {  // Gram + sweep buffers + swept flags
+  return sizeof(double) * ((size_t)R * (R + 1) + 3 * kMaxRank + kMaxRank) + sizeof(int) * kMaxRank + 64;
 }
+// dynamic shared memory: [step area: A, S, M rows, Gamma, Gram partial] [ext area: the last
+// cluster's Gram slice + sweep workspace | W + score partials | the scan's q staging]
+__host__ __device__ inline size_t uw_step_bytes(int R, size_t esz) {
+  return ((esz * (3 * (size_t)kUWRows * (R + 1) + (size_t)R * R) + 15) / 16) * 16 +
+         (sizeof(double) * (size_t)(R * (R + 1) / 2) + 15) / 16 * 16;
+}
+__host__ __device__ inline size_t uw_ext_bytes(int R, int64_t qch) {
+  const size_t tail = (uw_sweep_ws_bytes(R) + 15) / 16 * 16 +
+                      sizeof(double) * (size_t)((R * (R + 1) / 2 + kUWCluster - 1) / kUWCluster);
+  const size_t sc = sizeof(double) * ((size_t)R * ut_rd(R) + (size_t)kUWRows * ut_rd(R) + (size_t)kUWRows * ((R + 3) / 4)) + 64;
+  const size_t qs = sizeof(unsigned long long) * (size_t)qch;
+  size_t m = tail > sc ? tail : sc;
+  return m > qs ? m : qs;
+}
+__host__ __device__ inline size_t uw_smem_bytes(int R, size_t esz, int64_t qch) {
+  return uw_step_bytes(R, esz) + uw_ext_bytes(R, qch);
+}
+
+// The last k_update_wide cluster to finish: the Gram of the new A^(n) as the cluster-ordered sum of
+// the cluster partials (each CTA sums a slice of the pairs, every load of a pair in flight at
+// once; rank 0 gathers the slices over DSMEM), then rank 0 inverts it by the symmetric sweep on the
+// numerically full-rank pivot set (R4(b)) -> W, |S| in global memory.  Euclidean: ||A||_F^2.
+// (Def. 2.3 / eq:lev, reading R4.)
+template <typename T>
+__device__ void uw_table_tail(const UWParams<T>& p, unsigned char* sm, const cooperative_groups::cluster_group& cluster) {
+  const int tid = threadIdx.x, lane = tid & 31, R = p.R, RS = R + 1, P = R * (R + 1) / 2;
+  const int CU = (int)cluster.num_blocks(), q = (int)cluster.block_rank(), ncl = (int)(gridDim.x / CU);
+  __shared__ int s_bad;
+  __shared__ double s_tol;
+  if (p.strategy == 1 || p.strategy == 3) {
+    double* Gm = reinterpret_cast<double*>(sm);
+    double* rowbuf = Gm + R * RS;
+    double* diag = rowbuf + 3 * kMaxRank;
+    int* swept = reinterpret_cast<int*>(diag + kMaxRank);
+    double* slice = reinterpret_cast<double*>(sm + (uw_sweep_ws_bytes(R) + 15) / 16 * 16);
+    const int per = (P + CU - 1) / CU;
+    for (int pair = q * per + tid; pair < min(P, (q + 1) * per); pair += kWThreads) {
+      double v[16], s = 0.0;
+      for (int c0 = 0; c0 < ncl; c0 += 16) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = (c0 + k < ncl) ? __ldcg(p.gpart + (int64_t)(c0 + k) * P + pair) : 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) s += v[k];  // cluster order; zeros past ncl are exact
+      }
+      slice[pair - q * per] = s;
+    }
+    cluster.sync();  // slices complete
+    if (q == 0) {
+      for (int pair = tid; pair < P; pair += kWThreads) {
+        const int owner = pair / per;
+        const double s = cluster.map_shared_rank(slice, owner)[pair - owner * per];
+        int r1 = 0, rem = pair;
+        while (rem >= R - r1) { rem -= R - r1; ++r1; }
+        Gm[r1 * RS + r1 + rem] = s;
+        Gm[(r1 + rem) * RS + r1] = s;
+      }
+    }
+    cluster.sync();  // rank 0 done reading the peers' slices
+    if (q != 0) return;
+    if (tid == 0) s_bad = 0;
+    WMARK(true, 313);
+    if (tid < 32) {
+      double d0 = 0.0;
+      bool fin = true;
+      for (int j = lane; j < R; j += 32) {
+        const double d = Gm[j * RS + j];
+        d0 = fmax(d0, d);
+        fin = fin && (d == d) && d < 1.7e308;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
+      if (lane == 0) {
+        s_bad = __all_sync(0xffffffffu, fin) ? 0 : 8;
+        s_tol = (double)(p.In > R ? p.In : R) * 2.220446049250313e-16 * d0;
+      }
+      if (lane != 0) __all_sync(0xffffffffu, fin);
+    }
+    __syncthreads();
+    constexpr int EPT = (kMaxRank * kMaxRank + kWThreads - 1) / kWThreads;
+    const int rank = (p.In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, s_tol, rowbuf, swept, diag)
+                                    : grp_sweep_dispatch(Gm, R, s_tol, rowbuf, swept);
+    WMARK(true, 314);
+    for (int e = tid; e < R * R; e += kWThreads) p.W[e] = Gm[(e / R) * RS + e % R];
+    if (tid == 0) {
+      p.tstat[0] = rank;
+      p.tstat[1] = s_bad | (rank == 0 ? 2 : 0);
+      *p.cnt = 0u;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(p.flag, 1u);  // W ready (release: the fence above)
+  } else {  // Euclidean
+    if (q == 0 && tid == 0) {
+      double fro = 0.0;
+      for (int c = 0; c < ncl; ++c) fro += __ldcg(p.gpart + c);
+      int bad = 0;
+      if (!(fro == fro) || fro > 1.7e308) bad = 8;
+      else if (!(fro > 0.0)) bad = 2;
+      p.W[0] = fro;
+      p.tstat[0] = 0;
+      p.tstat[1] = bad;
+      *p.cnt = 0u;
+      __threadfence();
+      atomicAdd(p.flag, 1u);
+    }
+  }
+}
+
+// (a1) the rows [r0, r0 + nr) of the new table: l_i = a_i^T W a_i / |S| (leverage) or
+// ||a_i||^2 / ||A||_F^2 (Euclidean), quantised to the sampling contract's 2^-32 fixed point
+// (Def. 2.3); then the last CTA to finish scans q -> CDF, T, status.
+// Task (row il, column group cg) accumulates (A W)_{i, 4cg..4cg+3} over k in order and dots it
+// with a_{i, 4cg..}; the nb4 partials of a row are summed in cg order.
+template <typename T>
+__device__ void uw_scores(const UWParams<T>& p, const T* sA, unsigned char* ext, int64_t r0, int nr) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int R = p.R, RS = R + 1, RD = ut_rd(R), nb4 = (R + 3) >> 2;
+  const bool lev = (p.strategy == 1 || p.strategy == 3);
+  __shared__ double s_p[kUWRows];
+  __shared__ int s_last;
+  __shared__ unsigned long long s_wtot[kWThreads / 32];
+  __shared__ unsigned long long s_carry;
+  if (lev) {
+    double* Wd = reinterpret_cast<double*>(ext);  // [R][RD]
+    double* Ad = Wd + R * RD;                     // [kUWRows][RD] fp64 copy of the new rows
+    double* part = Ad + kUWRows * RD;             // [kUWRows][nb4]
+    for (int e = tid; e < R * R; e += kWThreads) cp_async_small<8>(Wd + (e / R) * RD + e % R, p.W + e, 8);
+    cp_async_commit();
+    for (int e = tid; e < R * (RD - R); e += kWThreads) Wd[(e / (RD - R)) * RD + R + e % (RD - R)] = 0.0;
+    for (int e = tid; e < kUWRows * RD; e += kWThreads) {
+      const int il = e / RD, c = e % RD;
+      Ad[e] = (il < nr && c < R) ? (double)sA[il * RS + c] : 0.0;
+    }
+    const int rank = __ldcg(p.tstat);
+    cp_async_wait<0>();
+    __syncthreads();
+    // task = 2 rows x 4 columns: per k two row values, two 16-byte W loads, eight DFMA
+    const int nrp = (nr + 1) >> 1;
+    for (int t = tid; t < nrp * nb4; t += kWThreads) {
+      const int il = 2 * (t / nb4), cg = t % nb4;
+      const double* a0 = Ad + il * RD;
+      const double* a1 = a0 + RD;  // row il + 1 (zeros past nr)
+      double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+      for (int k = 0; k < R; ++k) {
+        const double x0 = a0[k], x1 = a1[k];
+        const double2 w0 = *reinterpret_cast<const double2*>(Wd + k * RD + 4 * cg);
+        const double2 w1 = *reinterpret_cast<const double2*>(Wd + k * RD + 4 * cg + 2);
+        acc0[0] = fma(x0, w0.x, acc0[0]);
+        acc0[1] = fma(x0, w0.y, acc0[1]);
+        acc0[2] = fma(x0, w1.x, acc0[2]);
+        acc0[3] = fma(x0, w1.y, acc0[3]);
+        acc1[0] = fma(x1, w0.x, acc1[0]);
+        acc1[1] = fma(x1, w0.y, acc1[1]);
+        acc1[2] = fma(x1, w1.x, acc1[2]);
+        acc1[3] = fma(x1, w1.y, acc1[3]);
+      }
+      part[il * nb4 + cg] = acc0[0] * a0[4 * cg] + acc0[1] * a0[4 * cg + 1] + acc0[2] * a0[4 * cg + 2] + acc0[3] * a0[4 * cg + 3];
+      if (il + 1 < kUWRows)
+        part[(il + 1) * nb4 + cg] =
+            acc1[0] * a1[4 * cg] + acc1[1] * a1[4 * cg + 1] + acc1[2] * a1[4 * cg + 2] + acc1[3] * a1[4 * cg + 3];
+    }
+    __syncthreads();
+    if (tid < nr) {
+      double l = 0.0;
+      for (int cg = 0; cg < nb4; ++cg) l += part[tid * nb4 + cg];
+      s_p[tid] = rank > 0 ? fmax(l, 0.0) / (double)rank : 0.0;
+    }
+  } else if (tid < nr) {
+    const double fro = __ldcg(p.W);
+    s_p[tid] = fro > 0.0 ? __ldcg(p.rownorm + r0 + tid) / fro : 0.0;
+  }
+  __syncthreads();
+  if (tid < nr) {
+    const double pv = s_p[tid];
+    unsigned long long qv = 0;
+    if (!(pv == pv) || pv > 2.0) {
+      atomicOr(p.tstat + 1, 8);
+    } else if (pv > 0.0) {
+      const double s = rint(pv * 4294967296.0);
+      qv = (s < 1.0) ? 1ull : (unsigned long long)s;
+    }
+    p.p_out[r0 + tid] = pv;
+    p.qbuf[r0 + tid] = qv;
+  }
+  // the last CTA: CDF = inclusive integer prefix of q over all rows (exact in any order), T, status
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(p.cnt2, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int64_t In = p.In;
+  unsigned long long* qs = reinterpret_cast<unsigned long long*>(ext);
+  if (tid == 0) s_carry = 0;
+  for (int64_t c0 = 0; c0 < In; c0 += p.qch) {
+    const int64_t n = cmin64(p.qch, In - c0);
+    __syncthreads();
+    for (int64_t i = tid; i < n; i += kWThreads) cp_async_small<8>(qs + i, p.qbuf + c0 + i, 8);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    const int64_t seg = (n + kWThreads - 1) / kWThreads;
+    const int64_t a0 = cmin64((int64_t)tid * seg, n), a1 = cmin64(a0 + seg, n);
+    unsigned long long local = 0;
+    for (int64_t i = a0; i < a1; ++i) local += qs[i];
+    unsigned long long incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_wtot[wid] = incl;
+    __syncthreads();
+    unsigned long long pre = s_carry + incl - local;
+    for (int w = 0; w < wid; ++w) pre += s_wtot[w];
+    for (int64_t i = a0; i < a1; ++i) {
+      pre += qs[i];
+      p.cdf[c0 + i] = pre;
+    }
+    __syncthreads();
+    if (tid == kWThreads - 1) s_carry = pre;  // the last thread's inclusive prefix = the running total
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const unsigned long long total = s_carry;
+    *p.Tout = total;
+    const int bad = __ldcg(p.tstat + 1);
+    int st = 0;
+    if (bad & 8) st = -8;
+    else if ((bad & 2) || total == 0) st = -3;
+    if (st != 0) atomicCAS(p.status, 0, st);
+    *p.cnt2 = 0u;
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
   constexpr int UR = kUWRows, TI = 128;
   const int R = p.R, RS = R + 1, tid = threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.x * UR;
   const int nr = (int)cmax64(0, cmin64(UR, p.In - r0));  // 0 for the CTAs rounding the grid up
+  WMARK(blockIdx.x == 0, 310);
+  __shared__ unsigned s_epoch0;
+  if (tid == 0) s_epoch0 = *reinterpret_cast<volatile unsigned*>(p.flag);  // before any arrival below
   extern __shared__ __align__(16) unsigned char uw_sm[];
   T* sA = reinterpret_cast<T*>(uw_sm);  // [UR][R+1] each
   T* sS = sA + UR * RS;
@@ -202,6 +464,7 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
       for (int qq = 0; qq < kUWCluster; ++qq) s += v[qq];
       p.gpart[(int64_t)(blockIdx.x / CU) * P + pair] = s;
     }
+    __threadfence();
     cluster.sync();
   } else if (p.strategy == 2 || p.strategy == 4) {  // Euclidean: row norms + the CTA's partial ||A||^2
     double acc = 0.0;
@@ -225,258 +488,39 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
       double t = 0.0;
       for (int qq = 0; qq < (int)cluster.num_blocks(); ++qq) t += cluster.map_shared_rank(sgp, qq)[0];
       p.gpart[blockIdx.x / cluster.num_blocks()] = t;
+      __threadfence();
     }
     cluster.sync();
   }
-}
-
-// ------------------------------------------------------------------------------------------
-// (a1) the table of the updated A^(n): one cluster of CU CTAs (CTA q owns rows [q rows_per, ...))
-// ------------------------------------------------------------------------------------------
-struct TWParams {
-  int R, strategy;
-  int64_t In, rows_per;
-  int nparts;               // k_update_wide CTAs
-  const double* gpart;      // their partials
-  const double* rownorm;    // Euclidean row norms (k_update_wide)
-  const void* A;            // A^(n) (updated), T = float or double
-  int esz;
-  double* p_out;
-  uint64_t* cdf;
-  uint64_t* Tout;
-  int* status;
-  long long* dbg;
-};
-
-__host__ __device__ inline size_t tw_smem_bytes(int R, int64_t rows_per) {
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    off = (off + 15) / 16 * 16;
-    off += bytes;
-  };
-  const int RD = ut_rd(R), P = R * (R + 1) / 2;
-  take(sizeof(double) * rows_per * RD);      // Ad
-  const size_t wk = ut_work_bytes(R, rows_per), st = sizeof(double) * rows_per * R;
-  take(wk > st ? wk : st);                   // W + score partials | staged rows of A
-  take(sizeof(double) * P);                  // this CTA's slice sums (read by peers)
-  take(sizeof(double) * R * (R + 1));        // Gm
-  take(sizeof(double) * 4 * kMaxRank);       // sweep buffers
-  take(sizeof(int) * kMaxRank);              // swept
-  take(sizeof(double) * rows_per);           // prow
-  take(sizeof(unsigned long long) * rows_per);
-  take(sizeof(unsigned long long) * 2);
-  return off + 16;
-}
-
-template <typename T>
-__device__ void table_wide_body(const TWParams& p) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int CU = (int)cluster.num_blocks(), q = (int)cluster.block_rank();
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int R = p.R, RD = ut_rd(R), nb4 = (R + 3) >> 2, P = R * (R + 1) / 2, RS = R + 1;
-  const int64_t r_beg = cmin64((int64_t)q * p.rows_per, p.In), r_end = cmin64(r_beg + p.rows_per, p.In);
-  const int nr = (int)(r_end - r_beg);
-  extern __shared__ __align__(16) unsigned char tw_sm[];
-  size_t off = 0;
-  auto carve = [&](size_t bytes) {
-    off = (off + 15) / 16 * 16;
-    unsigned char* ptr = tw_sm + off;
-    off += bytes;
-    return ptr;
-  };
-  double* Ad = reinterpret_cast<double*>(carve(sizeof(double) * p.rows_per * RD));
-  double* work = reinterpret_cast<double*>(
-      carve(ut_work_bytes(R, p.rows_per) > sizeof(double) * p.rows_per * R ? ut_work_bytes(R, p.rows_per)
-                                                                             : sizeof(double) * p.rows_per * R));
-  double* slice = reinterpret_cast<double*>(carve(sizeof(double) * P));
-  double* Gm = reinterpret_cast<double*>(carve(sizeof(double) * R * (R + 1)));
-  double* colbuf = reinterpret_cast<double*>(carve(sizeof(double) * 4 * kMaxRank));
-  int* swept = reinterpret_cast<int*>(carve(sizeof(int) * kMaxRank));
-  double* prow = reinterpret_cast<double*>(carve(sizeof(double) * p.rows_per));
-  unsigned long long* qrow = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * p.rows_per));
-  unsigned long long* qtot = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * 2));
-  __shared__ int s_bad;
-  __shared__ double s_red[kTWThreads / 32];
-  __shared__ unsigned long long s_wtot[kTWThreads / 32];
-  __shared__ double s_tol, s_fro;
-  if (tid == 0) s_bad = 0;
-  const bool lev = (p.strategy == 1 || p.strategy == 3);
-  const T* A = reinterpret_cast<const T*>(p.A);
-  if (p.dbg && q == 0 && tid == 0) p.dbg[0] = clock64();
-  if (lev) {
-    // rows of the new A^(n) for the scores: cp.async into the work area (all requests in flight,
-    // overlapped with the slice sums), then fp64 (zero padded to RD)
-    T* Ast = reinterpret_cast<T*>(work);
-    for (int e = tid; e < nr * R; e += kTWThreads) cp_async_small<sizeof(T)>(Ast + e, A + r_beg * R + e, sizeof(T));
-    cp_async_commit();
-    // pair slice of this CTA: sum of the k_update_wide partials in CTA order
-    const int per = (P + CU - 1) / CU, pb = q * per, pe = min(P, pb + per);
-    for (int pair = pb + tid; pair < pe; pair += kTWThreads) {
-      double v[8], s = 0.0;
-      for (int c0 = 0; c0 < p.nparts; c0 += 8) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = (c0 + k < p.nparts) ? __ldcg(p.gpart + (int64_t)(c0 + k) * P + pair) : 0.0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) s += v[k];  // zeros past nparts are exact
-      }
-      slice[pair - pb] = s;
+  WMARK(blockIdx.x == 0, 311);
+  if (p.strategy == 0) return;  // uniform tables are constant
+  unsigned char* ext = uw_sm + uw_step_bytes(R, sizeof(T));
+  {  // the last cluster: the inverse (leverage) / the Frobenius norm (Euclidean)
+    __shared__ int s_last;
+    const int ncl = (int)(gridDim.x / cluster.num_blocks());
+    if (cluster.block_rank() == 0 && tid == 0) s_last = (atomicAdd(p.cnt, 1u) == (unsigned)(ncl - 1));
+    cluster.sync();
+    const bool last = *cluster.map_shared_rank(&s_last, 0) != 0;
+    cluster.sync();  // rank 0's flag read by every peer
+    if (last) {
+      __threadfence();
+      WMARK(cluster.block_rank() == 0, 312);
+      uw_table_tail<T>(p, ext, cluster);
+      WMARK(cluster.block_rank() == 0, 315);
     }
-    cp_async_wait<0>();
-    __syncthreads();
-    for (int e = tid; e < nr * RD; e += kTWThreads) {
-      const int il = e / RD, c = e % RD;
-      Ad[e] = c < R ? (double)Ast[il * R + c] : 0.0;
-    }
-    cluster.sync();  // #1 slices visible (and Ad complete; the work area is free again)
-    for (int pair = tid; pair < P; pair += kTWThreads) {
-      const int owner = pair / per;
-      const double sum = cluster.map_shared_rank(slice, owner)[pair - owner * per];
-      int r1 = 0, rem = pair;
-      while (rem >= R - r1) { rem -= R - r1; ++r1; }
-      const int r2 = r1 + rem;
-      Gm[r1 * RS + r2] = sum;
-      Gm[r2 * RS + r1] = sum;
-    }
-    __syncthreads();
-    if (wid == 0) {
-      double d0 = 0.0;
-      bool fin = true;
-      for (int j = lane; j < R; j += 32) {
-        const double d = Gm[j * RS + j];
-        d0 = fmax(d0, d);
-        fin = fin && (d == d) && d < 1.7e308;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
-      if (!__all_sync(0xffffffffu, fin) && lane == 0) s_bad |= 8;
-      if (lane == 0) s_tol = (double)(p.In > R ? p.In : R) * 2.220446049250313e-16 * d0;
-    }
-    __syncthreads();
-    if (p.dbg && q == 0 && tid == 0) p.dbg[1] = clock64();
-    constexpr int EPT = (kMaxRank * kMaxRank + kTWThreads - 1) / kTWThreads;
-    const int rank = (p.In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, s_tol, colbuf, swept, colbuf + R)
-                                    : grp_sweep_dispatch(Gm, R, s_tol, colbuf, swept);
-    if (tid == 0 && rank == 0) s_bad |= 2;
-    if (p.dbg && q == 0 && tid == 0) p.dbg[2] = clock64();
-    // scores l_i = sum_c (A W)_ic a_ic (4 rows x 4 columns per task; k in pairs)
-    double* Wd = work;
-    double* sc = work + R * RD;  // [nb4][rows_per]
-    for (int e = tid; e < R * RD; e += kTWThreads) {
-      const int r1 = e / RD, c = e % RD;
-      Wd[e] = c < R ? Gm[r1 * RS + c] : 0.0;
-    }
-    __syncthreads();
-    const int nrg = (nr + 3) >> 2, ntask = nrg * nb4;
-    for (int t = tid; t < ntask; t += kTWThreads) {
-      const int rg = t / nb4, cg2 = t % nb4;
-      const int il0 = 4 * rg;
-      double acc[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
-      const double* arow[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) arow[a] = Ad + (il0 + a < nr ? il0 + a : il0) * RD;
-      for (int kk = 0; kk < R; kk += 2) {
-        double2 av[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) av[a] = *reinterpret_cast<const double2*>(arow[a] + kk);
-        const int k1 = kk + 1 < R ? kk + 1 : kk;
-        const double2 w00 = *reinterpret_cast<const double2*>(Wd + kk * RD + 4 * cg2);
-        const double2 w01 = *reinterpret_cast<const double2*>(Wd + kk * RD + 4 * cg2 + 2);
-        const double2 w10 = *reinterpret_cast<const double2*>(Wd + k1 * RD + 4 * cg2);
-        const double2 w11 = *reinterpret_cast<const double2*>(Wd + k1 * RD + 4 * cg2 + 2);
-        const double wk0[4] = {w00.x, w00.y, w01.x, w01.y};
-        const double wk1[4] = {w10.x, w10.y, w11.x, w11.y};
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) acc[a][c] = fma(av[a].y, wk1[c], fma(av[a].x, wk0[c], acc[a][c]));
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        if (il0 + a >= nr) continue;
-        const double2 x0 = *reinterpret_cast<const double2*>(arow[a] + 4 * cg2);
-        const double2 x1 = *reinterpret_cast<const double2*>(arow[a] + 4 * cg2 + 2);
-        sc[cg2 * p.rows_per + il0 + a] = acc[a][0] * x0.x + acc[a][1] * x0.y + acc[a][2] * x1.x + acc[a][3] * x1.y;
-      }
-    }
-    __syncthreads();
-    for (int il = tid; il < nr; il += kTWThreads) {
-      double l = 0.0;
-      for (int cg2 = 0; cg2 < nb4; ++cg2) l += sc[cg2 * p.rows_per + il];
-      prow[il] = rank > 0 ? fmax(l, 0.0) / (double)rank : 0.0;
-    }
-  } else {
-    if (tid == 0) {
-      double fro = 0.0;
-      for (int c = 0; c < p.nparts; ++c) fro += __ldcg(p.gpart + c);
-      s_fro = fro;
-      if (!(fro == fro) || fro > 1.7e308) s_bad |= 8;
-      else if (!(fro > 0.0)) s_bad |= 2;
-    }
-    __syncthreads();
-    const double fro = s_fro;
-    for (int il = tid; il < nr; il += kTWThreads) prow[il] = fro > 0.0 ? __ldcg(p.rownorm + r_beg + il) / fro : 0.0;
-    cluster.sync();  // #1 (matches the leverage branch)
   }
-  __syncthreads();
-  if (p.dbg && q == 0 && tid == 0) p.dbg[3] = clock64();
-  // quantise + CTA scan (contiguous segment per thread) + DSMEM prefix of the lower ranks
-  const int seg = (nr + kTWThreads - 1) / kTWThreads;
-  const int a0 = min(tid * seg, nr), a1 = min(a0 + seg, nr);
-  unsigned long long local = 0;
-  int bad = 0;
-  for (int il = a0; il < a1; ++il) {
-    const double pv = prow[il];
-    unsigned long long qv = 0;
-    if (!(pv == pv) || pv > 2.0) {
-      bad = 1;
-    } else if (pv > 0.0) {
-      const double s = rint(pv * 4294967296.0);
-      qv = (s < 1.0) ? 1ull : (unsigned long long)s;
-    }
-    p.p_out[r_beg + il] = pv;
-    local += qv;
-    qrow[il] = local;
-  }
-  if (bad) atomicOr(&s_bad, 8);
-  unsigned long long incl = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) s_wtot[wid] = incl;
-  __syncthreads();
-  unsigned long long wpre = 0;
-  for (int w = 0; w < wid; ++w) wpre += s_wtot[w];
-  const unsigned long long seg_pre = wpre + incl - local;
-  if (tid == kTWThreads - 1) qtot[0] = seg_pre + local;
-  cluster.sync();  // #2 CTA totals visible
-  unsigned long long cta_pre = 0, total = 0;
-  for (int qq = 0; qq < CU; ++qq) {
-    const unsigned long long t = cluster.map_shared_rank(qtot, qq)[0];
-    if (qq < q) cta_pre += t;
-    total += t;
-  }
-  for (int il = a0; il < a1; ++il) p.cdf[r_beg + il] = cta_pre + seg_pre + qrow[il];
+  // every CTA (all resident: one wave, cooperative launch) waits for W, then scores its own rows
   if (tid == 0) {
-    if (q == 0) *p.Tout = total;
-    int st = 0;
-    if (s_bad & 8) st = -8;
-    else if ((s_bad & 2) || (q == 0 && total == 0)) st = -3;
-    if (st != 0) atomicCAS(p.status, 0, st);
+    unsigned f;
+    do {
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(f) : "l"(p.flag) : "memory");
+      if (f == s_epoch0) __nanosleep(128);
+    } while (f == s_epoch0);
   }
-  cluster.sync();  // #3 peers done with this CTA's shared memory
-  if (p.dbg && q == 0 && tid == 0) p.dbg[4] = clock64();
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kTWThreads, 1) k_table_wide(TWParams p) {
-  table_wide_body<T>(p);
+  __syncthreads();
+  WMARK(blockIdx.x == 0, 316);
+  uw_scores<T>(p, sA, ext, r0, nr);
+  WMARK(blockIdx.x == 0, 317);
 }
 
 // ------------------------------------------------------------------------------------------

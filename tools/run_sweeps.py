@@ -82,7 +82,10 @@ elif os.environ.get("CPSGD_DEBUG_TIMERS"):
         base = g0.min()
         print(f"  k_sample_wide CTAs {m.sum()}: start spread {(g0.max() - base) / 1e3:.1f} us, end min "
               f"{(g1.min() - base) / 1e3:.1f} max {(g1.max() - base) / 1e3:.1f} us, median dur {np.median(g1 - g0) / 1e3:.1f} us")
-        print("k_table_wide cycles: gram-sum", t[1] - t[0], "sweep", t[2] - t[1], "scores", t[3] - t[2], "scan", t[4] - t[3])
+    if t[317]:
+        print("k_update_wide (ns, globaltimer): CTA0 body", t[311] - t[310], "| last CTA: starts", t[312] - t[310],
+              "Gram gather", t[313] - t[312], "sweep", t[314] - t[313], "W write", t[315] - t[314])
+        print("  CTA0: W wait ends", t[316] - t[310], "scores+scan", t[317] - t[316])
     if not a.wide:
         names = ["start", "stageB", "gram-synced", "sweep-start", "sweep-done", "scores-done", "cdf-synced", "sampled"]
         print(" ".join(f"{names[i]}:{t[i] - t[0]}" for i in range(8)))
