@@ -143,6 +143,8 @@ struct cp_sgd_s {
   void* zrow = nullptr;          // prefetched unweighted SKR rows [Bmax][R]
   int64_t* fbase = nullptr;      // prefetched fiber offsets [Bmax]
   long long* dbg = nullptr;      // CPSGD_DEBUG_TIMERS: phase timestamps of k_update_table
+  bool pdl = false;              // programmatic dependent launch in the wide path (CPSGD_PDL=1; measured
+                                 // slower at C4: 272 vs 265 us/sweep, so off by default)
   int* last_mode_dev = nullptr;  // written by the fused sweep kernel
   void* zwp = nullptr;           // wide path: weighted padded SKR rows [Bmax][ceil8(R)] of the prefetched batch
   void* gam_next = nullptr;      // wide path: Gamma of the prefetched batch [R][R]
@@ -582,6 +584,11 @@ cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   lc.blockDim = dim3(kGUThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+  lc.attrs = at;
+  lc.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&lc, k_gather_update<T, CPT>, p);
   h->launches++;
   if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_gather_update launch: %s", cudaGetErrorString(e));
@@ -630,6 +637,11 @@ cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev
   lc.blockDim = dim3(kTCThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+  lc.attrs = at;
+  lc.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&lc, k_gather_update_tc, p);
   h->launches++;
   if (e != cudaSuccess)
@@ -709,7 +721,7 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   lc.blockDim = dim3(kWThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = kUWCluster;
   at[0].val.clusterDim.y = 1;
@@ -717,8 +729,10 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   // every CTA waits for the Gram inverse of the last cluster: the grid must be co-resident
   at[1].id = cudaLaunchAttributeCooperative;
   at[1].val.cooperative = 1;
+  at[2].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[2].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
   lc.attrs = at;
-  lc.numAttrs = 2;
+  lc.numAttrs = 3;
   cudaError_t e = cudaLaunchKernelEx(&lc, k_update_wide<T>, p);
   h->launches++;
   if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_update_wide launch: %s", cudaGetErrorString(e));
@@ -749,13 +763,15 @@ cp_status launch_sw_t(cp_sgd_s* h, int n) {
   lc.blockDim = dim3(kWThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = kSWCluster;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
   lc.attrs = at;
-  lc.numAttrs = 1;
+  lc.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&lc, k_sample_wide<T>, p);
   h->launches++;
   if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_sample_wide launch (smem %zu): %s", smem, cudaGetErrorString(e));
@@ -1160,6 +1176,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
   ALLOC(h->beff, sizeof(int64_t));
   ALLOC(h->beff_api, sizeof(int64_t));
   ALLOC(h->last_mode_dev, sizeof(int));
+  if (getenv("CPSGD_PDL")) h->pdl = true;
   if (getenv("CPSGD_DEBUG_TIMERS")) {
     ALLOC(h->dbg, sizeof(long long) * 4096);
     cudaMemsetAsync(h->dbg, 0, sizeof(long long) * 4096, h->stream);

@@ -108,6 +108,8 @@ __global__ void __launch_bounds__(kGUThreads, 1) k_gather_update(GUParams<T> p) 
   const int nfib = (int)cmax64(0, c1 - c0);
   const int nst = (nfib + KS - 1) / KS;
 
+  pdl_trigger();
+  pdl_wait();  // the batch comes from the previous kernel
   cp_async_u64(reinterpret_cast<uint64_t*>(sfb), reinterpret_cast<const uint64_t*>(p.fbase + c0), nfib, tid,
                kGUThreads);
   cp_async_wait<0>();

@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(kTCThreads, 1) k_gather_update_tc(GUParams<flo
     mbar_init(&accf, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();  // the batch (fiber offsets, A images) comes from the previous kernel
   cp_async_u64(reinterpret_cast<uint64_t*>(sfb), reinterpret_cast<const uint64_t*>(p.fbase + c0), nfib, tid,
                kTCThreads);
   cp_async_commit();
@@ -294,6 +295,7 @@ __global__ void __launch_bounds__(kTCThreads, 1) k_gather_update_tc(GUParams<flo
     umma_commit(&accf);
   }
   __syncthreads();
+  pdl_trigger();  // mainloop done: the next kernel may start its launch
   if (mark) p.dbg[34] = clock64();
   // ---- epilogue: E[L][i] = D[L][i] + D[L][128 + i] (x = xh + xl) staged in shared memory, then
   //      M^T[r][i] = E[r][i] + E[64 + r][i] (zw = zh + zl) -> the split-K workspace ----

@@ -788,6 +788,12 @@ __device__ __forceinline__ T cluster_sum(const cooperative_groups::cluster_group
   return s;
 }
 
+// programmatic dependent launch (no-ops unless the launch carries the PDL attribute): the wide
+// path's kernels let the next kernel of the chain be scheduled as soon as every CTA has started,
+// and wait for the previous kernel's completion before touching its outputs
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

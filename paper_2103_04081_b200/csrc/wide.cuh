@@ -314,6 +314,7 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
   const int64_t r0 = (int64_t)blockIdx.x * UR;
   const int nr = (int)cmax64(0, cmin64(UR, p.In - r0));  // 0 for the CTAs rounding the grid up
   WMARK(blockIdx.x == 0, 310);
+  pdl_wait();  // partial tiles and Gamma come from the previous kernels
   __shared__ unsigned s_epoch0;
   if (tid == 0) s_epoch0 = *reinterpret_cast<volatile unsigned*>(p.flag);  // before any arrival below
   extern __shared__ __align__(16) unsigned char uw_sm[];
@@ -518,6 +519,7 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
     } while (f == s_epoch0);
   }
   __syncthreads();
+  pdl_trigger();  // W is ready: the sampler may start its launch
   WMARK(blockIdx.x == 0, 316);
   uw_scores<T>(p, sA, ext, r0, nr);
   WMARK(blockIdx.x == 0, 317);
@@ -554,6 +556,7 @@ __host__ __device__ inline size_t sw_smem_bytes(int N, int R, int64_t cdf_elems,
   } while (0)
 template <typename T>
 __global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
+  pdl_wait();  // the tables and factors come from the previous kernel
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const SampleParams& sp = P.sp;
@@ -756,6 +759,7 @@ __global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
     }
   }
   SWM(6);
+  pdl_trigger();  // the batch is written: the gather may start its launch
   __threadfence();
   cluster.sync();  // the whole cluster partial is written
   if (q == 0 && tid == 0) s_last = (atomicAdd(P.cnt, 1u) == (unsigned)(ncl - 1));
