@@ -52,7 +52,7 @@ struct FusedParams {
 
 // shared memory layout (bytes) -- mirrored by the host
 struct FusedLayout {
-  size_t zw, zu, fb, wt, ix, pt, mp, gp, gam, aold, anew, gpart, gm, prow, sc, rowbuf, swept, qtot, cdfs, xs, total;
+  size_t zw, zu, fb, wt, ix, pt, mp, gp, gam, aold, anew, sold, gpart, gm, prow, sc, rowbuf, swept, qtot, cdfs, xs, total;
 };
 // row pitch (elements) of the staged fiber segments: I_max rounded up to a 16-byte multiple
 __host__ __device__ inline int64_t fused_xpitch(int64_t Imax, size_t esz) {
@@ -85,6 +85,7 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
   L.gam = take(esz * R * R);
   L.aold = take(esz * RPC * (R + 1));
   L.anew = take(esz * RPC * (R + 1));
+  L.sold = take(esz * RPC * (R + 1));
   L.gpart = take(sizeof(double) * (R * (R + 1) / 2 + 2));
   L.gm = take(sizeof(double) * R * (R + 1));
   L.prow = take(sizeof(double) * RPC);
@@ -244,6 +245,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
   T* Gp = reinterpret_cast<T*>(f_sm + L.gp);
   T* Gam = reinterpret_cast<T*>(f_sm + L.gam);
   T* Aold = reinterpret_cast<T*>(f_sm + L.aold);
+  T* Sold = reinterpret_cast<T*>(f_sm + L.sold);
   T* Anew = reinterpret_cast<T*>(f_sm + L.anew);
   double* gpart = reinterpret_cast<double*>(f_sm + L.gpart);
   double* Gm = reinterpret_cast<double*>(f_sm + L.gm);
@@ -425,21 +427,38 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     // ------------------------------------------------ (1) gather (Alg. 5) + partial contractions
     cp_async_wait<0>();  // this batch's fiber segments (issued by sample_own)
     __syncthreads();
+    // old rows (and adaptive accumulators) of the block this CTA updates: in flight during the gather
+    for (int e = tid; e < nr * R; e += kFThreads) {
+      const int il = e / R, c = e % R;
+      cp_async_small<sizeof(T)>(Aold + il * RS + c, p.factors[n] + (r_beg + il) * R + c, sizeof(T));
+      if (p.rule != 0) cp_async_small<sizeof(T)>(Sold + il * RS + c, p.S[n] + (r_beg + il) * R + c, sizeof(T));
+    }
+    cp_async_commit();
+    const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
     gather_dispatch<T, ROWS>(xs, Ip, In, fb, zw, RP, p.BPC, Mp, R,
                              (p.dbg && q == 0 && tid == 0 && s == 1) ? p.dbg : nullptr);
     F_MARK(14);
-    for (int e = tid; e < R * R; e += kFThreads) {
-      const int r1 = e / R, r2 = e % R;
-      T g = T(0);
-      for (int lb = 0; lb < p.BPC; ++lb) g += zw[lb * RP + r1] * zu[lb * RP + r2];
-      Gp[e] = g;
+    {  // Gamma partial: 2 x 2 blocks (each entry still summed over the CTA's fibers in order)
+      const int h2 = (R + 1) >> 1;
+      for (int e = tid; e < h2 * h2; e += kFThreads) {
+        const int r1 = 2 * (e / h2), r2 = 2 * (e % h2);
+        const int r1b = r1 + 1 < R ? r1 + 1 : r1, r2b = r2 + 1 < R ? r2 + 1 : r2;
+        T g00 = T(0), g01 = T(0), g10 = T(0), g11 = T(0);
+        for (int lb = 0; lb < p.BPC; ++lb) {
+          const T w0 = zw[lb * RP + r1], w1 = zw[lb * RP + r1b], u0 = zu[lb * RP + r2], u1 = zu[lb * RP + r2b];
+          g00 += w0 * u0;
+          g01 += w0 * u1;
+          g10 += w1 * u0;
+          g11 += w1 * u1;
+        }
+        Gp[r1 * R + r2] = g00;
+        if (r2 + 1 < R) Gp[r1 * R + r2 + 1] = g01;
+        if (r1 + 1 < R) Gp[(r1 + 1) * R + r2] = g10;
+        if (r1 + 1 < R && r2 + 1 < R) Gp[(r1 + 1) * R + r2 + 1] = g11;
+      }
     }
     F_MARK(15);
-#pragma unroll 8
-    for (int e = tid; e < nr * R; e += kFThreads) {  // old rows of the block this CTA updates
-      const int il = e / R, c = e % R;
-      Aold[il * RS + c] = p.factors[n][(r_beg + il) * R + c];
-    }
+    cp_async_wait<0>();  // old rows / accumulators
     F_MARK(1);
     cluster.sync();  // #1: partials visible
     F_MARK(2);
@@ -448,7 +467,6 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     __syncthreads();
     if (q == 0 && s == p.nsteps - 1)
       for (int e = tid; e < R * R; e += kFThreads) p.Gam_out[e] = Gam[e];
-    const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
     for (int e = tid; e < nr * R; e += kFThreads) {
       const int il = e / R, rr = e % R;
       const int64_t i = r_beg + il;
@@ -463,7 +481,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
       if (p.rule == 0) {
         an = a - (T)alpha * g;
       } else {
-        const T sv = p.S[n][gi] + g * g;
+        const T sv = Sold[il * RS + rr] + g * g;
         p.S[n][gi] = sv;
         if (sv > T(0)) {
           T step;
