@@ -882,14 +882,11 @@ void plan_fused(cp_sgd_s* h) {
   h->fused_cu = 0;
   if (h->world_size > 1 || (h->flags & CP_FLAG_NO_FUSED)) return;
   if (fused_rp(h->R, h->esz) / (h->esz == 8 ? 2 : 4) > 8) return;  // gather_contract supports <= 8 vector groups
-  int64_t imax = 0, bmx = 0, cdfmax = 0;
+  int64_t imax = 0, bmx = 0, cdfmax = 0;  // cdfmax: the resident CDFs of every mode
   for (int n = 0; n < h->N; ++n) {
     imax = std::max(imax, h->dims[n]);
     bmx = std::max(bmx, h->bmax[n]);
-    int64_t c = 0;
-    for (int k = 0; k < h->N; ++k)
-      if (k != n) c += h->dims[k];
-    cdfmax = std::max(cdfmax, c);
+    cdfmax += h->dims[n];
   }
   if (imax > 2 * kFThreads) return;
   const int CU = 16;

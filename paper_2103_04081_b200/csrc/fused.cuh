@@ -52,7 +52,7 @@ struct FusedParams {
 
 // shared memory layout (bytes) -- mirrored by the host
 struct FusedLayout {
-  size_t zw, zu, fb, wt, ix, pt, mp, gp, gam, aold, anew, sold, gpart, gm, prow, sc, rowbuf, swept, qtot, cdfs, xs, total;
+  size_t zw, zu, fb, wt, ix, pt, mp, gp, gam, aold, anew, sold, gpart, gm, prow, sc, rowbuf, swept, qtot, qpre, cdfs, xs, total;
 };
 // row pitch (elements) of the staged fiber segments: I_max rounded up to a 16-byte multiple
 __host__ __device__ inline int64_t fused_xpitch(int64_t Imax, size_t esz) {
@@ -93,6 +93,7 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
   L.rowbuf = take(sizeof(double) * 3 * kMaxRank);
   L.swept = take(sizeof(int) * R);
   L.qtot = take(sizeof(unsigned long long) * 2);
+  L.qpre = take(sizeof(unsigned long long) * RPC);
   L.cdfs = take(sizeof(uint64_t) * cdf_elems);
   L.xs = take(esz * (size_t)BPC * fused_xpitch(Imax, esz));
   L.total = off + 16;
@@ -226,14 +227,9 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
   const int N = p.N, R = p.R, RS = R + 1, NP = N - 1;
   const int RP = fused_rp(R, sizeof(T));
   extern __shared__ __align__(16) unsigned char f_sm[];
-  int64_t cdf_elems = 0;
+  int64_t cdf_elems = 0;  // resident CDFs of every mode
   if (p.strategy != 0)
-    for (int n = 0; n < N; ++n) {
-      int64_t c = 0;
-      for (int k = 0; k < N; ++k)
-        if (k != n) c += p.dims[k];
-      cdf_elems = max(cdf_elems, c);
-    }
+    for (int k = 0; k < N; ++k) cdf_elems += p.dims[k];
   const FusedLayout L = fused_layout(N, R, p.BPC, p.RPC, p.Imax, cdf_elems, sizeof(T));
   T* zw = reinterpret_cast<T*>(f_sm + L.zw);
   T* zu = reinterpret_cast<T*>(f_sm + L.zu);
@@ -254,13 +250,16 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
   double* rowbuf = reinterpret_cast<double*>(f_sm + L.rowbuf);
   int* swept = reinterpret_cast<int*>(f_sm + L.swept);
   unsigned long long* qtot = reinterpret_cast<unsigned long long*>(f_sm + L.qtot);
-  uint64_t* cdfs = reinterpret_cast<uint64_t*>(f_sm + L.cdfs);
+  uint64_t* cdfs = reinterpret_cast<uint64_t*>(f_sm + L.cdfs);  // resident CDFs, mode k at cdf_off[k]
+  unsigned long long* qpre = reinterpret_cast<unsigned long long*>(f_sm + L.qpre);  // CTA-inclusive prefix of q
   T* xs = reinterpret_cast<T*>(f_sm + L.xs);
   const int64_t Ip = fused_xpitch(p.Imax, sizeof(T));
   __shared__ int s_bad;
   __shared__ double s_red[kFThreads / 32];
   __shared__ unsigned long long s_wtot[kFThreads / 32];
   __shared__ const uint64_t* s_cp[kMaxOrder];
+  __shared__ uint64_t s_T[kMaxOrder];
+  __shared__ unsigned long long s_off[17];
   __shared__ int32_t s_start[kMaxOrder], s_len[kMaxOrder];
   __shared__ double s_wblk;
   __shared__ int64_t s_beff;
@@ -273,17 +272,26 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
   };
 
   // ---- this CTA's fibers [q*BPC, (q+1)*BPC) of the batch of mode n at iteration it (contract §8c.2)
-  auto sample_own = [&](int n, uint64_t it) {
+  // the CDFs of every mode stay resident in shared memory: staged once here, then each table
+  // rebuild assembles the new CDF of its mode from the cluster's CTA prefixes over DSMEM
+  if (tid < kMaxOrder) s_cp[tid] = nullptr;
+  __syncthreads();
+  if (p.strategy != 0) {
     int64_t off = 0;
-    if (tid < kMaxOrder) s_cp[tid] = nullptr;
-    __syncthreads();
-    for (int k = 0; k < N; ++k) {  // stage the CDFs of the modes k != n
-      if (k == n || p.strategy == 0) continue;
+    for (int k = 0; k < N; ++k) {
       cp_async_u64(cdfs + off, p.cdf[k], p.dims[k], tid, kFThreads);
-      if (tid == 0) s_cp[k] = cdfs + off;
+      if (tid == 0) {
+        s_cp[k] = cdfs + off;
+        s_T[k] = p.Ttot[k];
+      }
       off += p.dims[k];
     }
+    cp_async_commit();
     cp_async_wait<0>();
+  }
+  __syncthreads();
+
+  auto sample_own = [&](int n, uint64_t it) {
     if (block && tid == 0) {  // window draws (eq:bik, R2): common to the whole batch
       double prod = 1.0;
       int64_t beff = 1;
@@ -291,9 +299,9 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
       for (int k = 0; k < N; ++k) {
         if (k == n) continue;
         const int64_t bk = p.window[n][pos];
-        const uint64_t Tk = p.Ttot[k];
+        const uint64_t Tk = s_T[k];
         const uint64_t rr = scale_draw(draw_word(p.seed, it, 0u, kPurposeWindow, (uint32_t)pos), Tk);
-        const uint64_t* c = p.cdf[k];
+        const uint64_t* c = s_cp[k];
         const int64_t istar = upper_bound_u64(c, p.dims[k], rr);
         const int64_t s0 = (istar / bk) * bk, e0 = min(s0 + bk, p.dims[k]);
         const uint64_t Q = c[e0 - 1] - (s0 > 0 ? c[s0 - 1] : 0ull);
@@ -317,7 +325,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
         const int64_t b = b0 + lb;
         if (b >= bmax) continue;
         int k = pos < n ? pos : pos + 1;
-        const uint64_t Tk = (p.strategy == 0) ? (uint64_t)p.dims[k] : p.Ttot[k];
+        const uint64_t Tk = (p.strategy == 0) ? (uint64_t)p.dims[k] : s_T[k];
         const uint64_t rr = scale_draw(draw_word(p.seed, it, (uint32_t)b, kPurposeRow, (uint32_t)pos), Tk);
         int64_t i;
         uint64_t qk;
@@ -605,23 +613,44 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
       __syncthreads();
       unsigned long long wpre = 0;
       for (int w = 0; w < wid; ++w) wpre += s_wtot[w];
+      if (tid < nr) qpre[tid] = wpre + incl;
       if (tid == kFThreads - 1) qtot[0] = wpre + incl;
       F_MARK(8);
       cluster.sync();  // #3: CTA totals visible
       F_MARK(9);
-      unsigned long long cpre = 0, total = 0;
-      {
-        unsigned long long tv[16];
-#pragma unroll
-        for (int qq = 0; qq < 16; ++qq) tv[qq] = qq < CU ? cluster.map_shared_rank(qtot, qq)[0] : 0ull;
-#pragma unroll
+      // CTA totals -> exclusive offsets (16 DSMEM loads, once per CTA)
+      if (tid < 16) s_off[tid] = tid < CU ? cluster.map_shared_rank(qtot, tid)[0] : 0ull;
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long acc = 0;
         for (int qq = 0; qq < 16; ++qq) {
-          if (qq < q) cpre += tv[qq];
-          total += tv[qq];
+          const unsigned long long v = s_off[qq];
+          s_off[qq] = acc;
+          acc += v;
+        }
+        s_off[16] = acc;
+      }
+      __syncthreads();
+      const unsigned long long cpre = s_off[q], total = s_off[16];
+      if (tid < nr) p.cdf[n][r_beg + tid] = cpre + wpre + incl;  // for the host / later launches
+      {  // the new CDF of mode n in every CTA's resident copy: the peers' prefixes over DSMEM
+        uint64_t* cn = const_cast<uint64_t*>(s_cp[n]);
+        constexpr int U = 2;  // rows per thread per round, loads issued together
+        for (int64_t r0 = tid; r0 < In; r0 += U * kFThreads) {
+          unsigned long long v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t row = r0 + u * kFThreads;
+            const int owner = row < In ? (int)(row / rpc) : 0;
+            v[u] = row < In ? cluster.map_shared_rank(qpre, owner)[row - owner * rpc] + s_off[owner] : 0ull;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (r0 + u * kFThreads < In) cn[r0 + u * kFThreads] = v[u];
         }
       }
-      if (tid < nr) p.cdf[n][r_beg + tid] = cpre + wpre + incl;
       if (tid == 0) {
+        s_T[n] = total;
         if (q == 0) p.Ttot[n] = total;
         int st = 0;
         if (s_bad & 8) st = -8;
@@ -633,8 +662,9 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     n_done = n;
     const int n_next = mode_of(r, s + 1);
     F_MARK(10);
-    __threadfence();
-    cluster.sync();  // #4: factors, CDF and T of mode n visible cluster-wide; peers done with our smem
+    __syncthreads();  // the resident CDF / T of mode n are complete (the peers' prefixes and totals are
+                      // not rewritten before the next step's barrier #1; the new factor rows are
+                      // visible cluster-wide since barrier #2)
     F_MARK(11);
     if (s + 1 < p.nsteps) sample_own(n_next, r);
     F_MARK(12);
