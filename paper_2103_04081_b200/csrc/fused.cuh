@@ -80,7 +80,7 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
   L.wt = take(sizeof(double) * BPC);
   L.ix = take(sizeof(int32_t) * BPC * (N - 1));
   L.pt = take(sizeof(double) * BPC * (N - 1));
-  L.mp = take(esz * Imax * R);
+  L.mp = take(esz * Imax * (R + 1));
   L.gp = take(esz * R * R);
   L.gam = take(esz * R * R);
   L.aold = take(esz * RPC * (R + 1));
@@ -187,7 +187,7 @@ __device__ __forceinline__ void gather_contract(const T* xs, int64_t Ip, int64_t
 #pragma unroll
         for (int cc = 0; cc < W; ++cc) {
           const int j = g * W + cc;
-          if (j < R) Mp[i * R + j] = a[cc];
+          if (j < R) Mp[i * (R + 1) + j] = a[cc];  // row pitch R + 1: conflict-free across lanes
         }
       }
     }
@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     for (int e = tid; e < nr * R; e += kFThreads) {
       const int il = e / R, rr = e % R;
       const int64_t i = r_beg + il;
-      const T m = cluster_sum(cluster, Mp, (int)(i * R + rr), CU);
+      const T m = cluster_sum(cluster, Mp, (int)(i * (R + 1) + rr), CU);
       T ag = T(0);
       for (int c = 0; c < R; ++c) ag += Aold[il * RS + c] * Gam[c * R + rr];
       const T g = ag - m;
@@ -662,9 +662,13 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     n_done = n;
     const int n_next = mode_of(r, s + 1);
     F_MARK(10);
-    __syncthreads();  // the resident CDF / T of mode n are complete (the peers' prefixes and totals are
-                      // not rewritten before the next step's barrier #1; the new factor rows are
-                      // visible cluster-wide since barrier #2)
+    // the resident CDF / T of mode n are complete; the peers' prefixes and totals are not rewritten
+    // before the next step's barrier #1, and the new factor rows are visible cluster-wide since
+    // barrier #2.  Uniform sampling has no table (no barriers #2, #3): a cluster barrier orders the
+    // peers' reads of this CTA's partials before the next step's gather rewrites them, and makes the
+    // new factor rows visible to the next batch's SKR rows.
+    if (p.strategy == 0) cluster.sync();
+    else __syncthreads();
     F_MARK(11);
     if (s + 1 < p.nsteps) sample_own(n_next, r);
     F_MARK(12);
