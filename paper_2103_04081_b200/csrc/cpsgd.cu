@@ -675,6 +675,34 @@ int64_t ts_cdf_elems(const cp_sgd_s* h, int next_mode) {
 }
 
 // ---- wide path: k_update_wide (+ the Gram inverse in its last cluster, the scores, the scan) -> k_sample_wide (wide.cuh) ----
+// k_update_wide's CTAs wait for one another (the Gram inverse of its last cluster): every cluster
+// of the grid must be resident at once.  True when the occupancy calculator says so for the
+// launch's configuration (clusters of kUWCluster, its dynamic shared memory).
+template <typename T>
+bool uw_coresident(int R, int64_t In) {
+  const int64_t ncl = ceil_div(ceil_div(In, kUWRows), kUWCluster);
+  const size_t smem = uw_smem_bytes(R, sizeof(T), std::min<int64_t>(In, 4096));
+  if (cudaFuncSetAttribute(k_update_wide<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return false;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(ncl * kUWCluster), 1, 1);
+  lc.blockDim = dim3(kWThreads, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kUWCluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int act = 0;
+  if (cudaOccupancyMaxActiveClusters(&act, k_update_wide<T>, &lc) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return (int64_t)act >= ncl;
+}
+
 template <typename T>
 cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
   ProfScope ps(h, kKUpdateWide);
@@ -721,18 +749,18 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   lc.blockDim = dim3(kWThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
-  cudaLaunchAttribute at[3];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = kUWCluster;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
-  // every CTA waits for the Gram inverse of the last cluster: the grid must be co-resident
-  at[1].id = cudaLaunchAttributeCooperative;
-  at[1].val.cooperative = 1;
-  at[2].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[2].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+  // every CTA waits for the Gram inverse of the last cluster: the grid must be co-resident, which
+  // init checked (uw_coresident; a cooperative launch attribute would say the same but is not
+  // replayable by ncu)
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
   lc.attrs = at;
-  lc.numAttrs = 3;
+  lc.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&lc, k_update_wide<T>, p);
   h->launches++;
   if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_update_wide launch: %s", cudaGetErrorString(e));
@@ -1257,7 +1285,8 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       }
       const size_t us = std::max(uw_smem_bytes(h->R, h->esz, std::min<int64_t>(h->dims[n], 4096)),
                                  sw_smem_bytes(h->N, h->R, cdfmax, h->esz));
-      if (gs + 1024 <= (size_t)optin && us <= (size_t)h->sample_smem) {
+      const bool cores = h->esz == 8 ? uw_coresident<double>(h->R, h->dims[n]) : uw_coresident<float>(h->R, h->dims[n]);
+      if (gs + 1024 <= (size_t)optin && us <= (size_t)h->sample_smem && cores) {
         h->gu_ck[n] = (int)CK;
         h->gu_kb[n] = KB;
         mpart = std::max(mpart, nt * CK * kGUTI * h->R);
