@@ -120,6 +120,7 @@ struct cp_sgd_s {
   uint32_t flags = 0;
   const void* X = nullptr;
   void* factors[kMaxOrder] = {};
+  void* fstage[kMaxOrder] = {};    // cp_sgd_steps_host staging of the host factors (fused path)
   size_t esz = 4;
   // layout
   void* Xmm[kMaxOrder] = {};
@@ -814,7 +815,8 @@ cp_status launch_prefetch(cp_sgd_s* h, int n) {
 
 // ---- persistent single-cluster sweep kernel (fused.cuh) ----------------------------------------
 template <typename T, int ROWS>
-cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev) {
+cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev,
+                         int rebuild) {
   ProfScope ps(h, kKFused);
   FusedParams<T> p;
   memset(&p, 0, sizeof p);
@@ -855,6 +857,8 @@ cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, dou
   p.nsteps = nsteps;
   p.first_mode = first_mode;
   p.order = order;
+  p.rebuild = rebuild;
+  for (int k = 0; k < h->N; ++k) p.fstage[k] = (const T*)h->fstage[k];
   p.Gout = (T*)h->Gout;
   p.Gam_out = (T*)h->Gam_out;
   p.last_mode = h->last_mode_dev;
@@ -891,16 +895,18 @@ cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, dou
 }
 
 template <typename T>
-cp_status launch_fused_r(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev) {
+cp_status launch_fused_r(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev,
+                         int rebuild) {
   int64_t imax = 0;
   for (int k = 0; k < h->N; ++k) imax = std::max(imax, h->dims[k]);
-  return imax > kFThreads ? launch_fused_t<T, 2>(h, nsteps, first_mode, order, alpha, alpha_dev)
-                          : launch_fused_t<T, 1>(h, nsteps, first_mode, order, alpha, alpha_dev);
+  return imax > kFThreads ? launch_fused_t<T, 2>(h, nsteps, first_mode, order, alpha, alpha_dev, rebuild)
+                          : launch_fused_t<T, 1>(h, nsteps, first_mode, order, alpha, alpha_dev, rebuild);
 }
 
-cp_status launch_fused(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev) {
-  cp_status st = h->dtype == CP_F64 ? launch_fused_r<double>(h, nsteps, first_mode, order, alpha, alpha_dev)
-                                    : launch_fused_r<float>(h, nsteps, first_mode, order, alpha, alpha_dev);
+cp_status launch_fused(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev,
+                       int rebuild = 0) {
+  cp_status st = h->dtype == CP_F64 ? launch_fused_r<double>(h, nsteps, first_mode, order, alpha, alpha_dev, rebuild)
+                                    : launch_fused_r<float>(h, nsteps, first_mode, order, alpha, alpha_dev, rebuild);
   h->pref_mode = -1;
   return st;
 }
@@ -1418,6 +1424,7 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->zrow);
   cudaFree(h->fbase);
   cudaFree(h->zwp);
+  for (int k = 0; k < kMaxOrder; ++k) cudaFree(h->fstage[k]);
   cudaFree(h->zimg);
   cudaFree(h->gam_next);
   cudaFree(h->Mpart);
@@ -1663,18 +1670,29 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
   cp_status st = check_mode(h, first_mode);
   if (st) return st;
   if (!factors_host) return h->fail(CP_EINVAL, "NULL factors_host");
-  for (int k = 0; k < h->N; ++k)
-    CUDA_TRY(h, cudaMemcpyAsync(h->factors[k], factors_host[k], h->esz * h->dims[k] * h->R, cudaMemcpyHostToDevice,
-                                h->stream));
-  h->pref_mode = -1;
-  // the host factors may differ from the device ones: rebuild every table first
+  const bool fused = h->fused_cu && nsteps > 0;
   for (int k = 0; k < h->N; ++k) {
-    st = launch_table_any(h, k);
-    if (st) return st;
+    const size_t bytes = h->esz * h->dims[k] * h->R;
+    if (fused && !h->fstage[k]) CUDA_TRY(h, cudaMalloc(&h->fstage[k], bytes));
+    CUDA_TRY(h, cudaMemcpyAsync(fused ? h->fstage[k] : h->factors[k], factors_host[k], bytes, cudaMemcpyHostToDevice,
+                                h->stream));
   }
-  for (int s = 0; s < nsteps; ++s) {
-    st = cp_sgd_step(h, (first_mode + s) % h->N, alpha);
+  h->pref_mode = -1;
+  // the host factors may differ from the device ones: rebuild the tables
+  if (fused) {  // one persistent launch: changed factors taken over + their tables rebuilt, then the steps
+    st = launch_fused(h, nsteps, first_mode, CP_ORDER_CYCLIC, (alpha < 0.0) ? h->alpha : alpha, nullptr, 1);
     if (st) return st;
+    h->iter_host += nsteps;
+    h->last_mode = (first_mode + nsteps - 1) % h->N;
+  } else {
+    for (int k = 0; k < h->N; ++k) {
+      st = launch_table_any(h, k);
+      if (st) return st;
+    }
+    for (int s = 0; s < nsteps; ++s) {
+      st = cp_sgd_step(h, (first_mode + s) % h->N, alpha);
+      if (st) return st;
+    }
   }
   for (int k = 0; k < h->N; ++k)
     CUDA_TRY(h, cudaMemcpyAsync(factors_host[k], h->factors[k], h->esz * h->dims[k] * h->R, cudaMemcpyDeviceToHost,

@@ -41,6 +41,9 @@ struct FusedParams {
   double alpha, eta, b, eps;
   const double* alpha_dev;
   int nsteps, first_mode, order;   // order: 0 cyclic, 1 random
+  int rebuild;                     // 1: factors staged in fstage (host input): every mode whose factor differs
+                                   // from the device copy is replaced and its table rebuilt before step 0
+  const T* fstage[kMaxOrder];
   T* Gout;
   T* Gam_out;
   int* last_mode;                  // out
@@ -207,6 +210,12 @@ __device__ __forceinline__ void gather_dispatch(const T* xs, int64_t Ip, int64_t
     case 7: gather_contract<T, ROWS, 7>(xs, Ip, In, fb, zw, RP, BPC, Mp, R, dbg); break;
     default: gather_contract<T, ROWS, 8>(xs, Ip, In, fb, zw, RP, BPC, Mp, R, dbg); break;
   }
+}
+
+template <typename T>
+__device__ __forceinline__ bool bits_equal(T a, T b) {
+  if constexpr (sizeof(T) == 8) return __double_as_longlong(a) == __double_as_longlong(b);
+  else return __float_as_uint(a) == __float_as_uint(b);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -421,89 +430,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     __syncthreads();
   };
 
-  int n = mode_of(r, 0);
-  int n_done = n;
-  sample_own(n, r);
-
-#pragma unroll 1
-  for (int s = 0; s < p.nsteps; ++s) {
-    F_MARK(0);
-    const int64_t In = p.dims[n];
-    const int64_t rpc = (In + CU - 1) / CU;
-    const int64_t r_beg = min((int64_t)q * rpc, In), r_end = min(r_beg + rpc, In);
-    const int nr = (int)(r_end - r_beg);
-    // ------------------------------------------------ (1) gather (Alg. 5) + partial contractions
-    cp_async_wait<0>();  // this batch's fiber segments (issued by sample_own)
-    __syncthreads();
-    // old rows (and adaptive accumulators) of the block this CTA updates: in flight during the gather
-    for (int e = tid; e < nr * R; e += kFThreads) {
-      const int il = e / R, c = e % R;
-      cp_async_small<sizeof(T)>(Aold + il * RS + c, p.factors[n] + (r_beg + il) * R + c, sizeof(T));
-      if (p.rule != 0) cp_async_small<sizeof(T)>(Sold + il * RS + c, p.S[n] + (r_beg + il) * R + c, sizeof(T));
-    }
-    cp_async_commit();
-    const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
-    gather_dispatch<T, ROWS>(xs, Ip, In, fb, zw, RP, p.BPC, Mp, R,
-                             (p.dbg && q == 0 && tid == 0 && s == 1) ? p.dbg : nullptr);
-    F_MARK(14);
-    {  // Gamma partial: 2 x 2 blocks (each entry still summed over the CTA's fibers in order)
-      const int h2 = (R + 1) >> 1;
-      for (int e = tid; e < h2 * h2; e += kFThreads) {
-        const int r1 = 2 * (e / h2), r2 = 2 * (e % h2);
-        const int r1b = r1 + 1 < R ? r1 + 1 : r1, r2b = r2 + 1 < R ? r2 + 1 : r2;
-        T g00 = T(0), g01 = T(0), g10 = T(0), g11 = T(0);
-        for (int lb = 0; lb < p.BPC; ++lb) {
-          const T w0 = zw[lb * RP + r1], w1 = zw[lb * RP + r1b], u0 = zu[lb * RP + r2], u1 = zu[lb * RP + r2b];
-          g00 += w0 * u0;
-          g01 += w0 * u1;
-          g10 += w1 * u0;
-          g11 += w1 * u1;
-        }
-        Gp[r1 * R + r2] = g00;
-        if (r2 + 1 < R) Gp[r1 * R + r2 + 1] = g01;
-        if (r1 + 1 < R) Gp[(r1 + 1) * R + r2] = g10;
-        if (r1 + 1 < R && r2 + 1 < R) Gp[(r1 + 1) * R + r2 + 1] = g11;
-      }
-    }
-    F_MARK(15);
-    cp_async_wait<0>();  // old rows / accumulators
-    F_MARK(1);
-    cluster.sync();  // #1: partials visible
-    F_MARK(2);
-    // ------------------------------------------------ (2) cluster reduction (rank order) + update
-    for (int e = tid; e < R * R; e += kFThreads) Gam[e] = cluster_sum(cluster, Gp, e, CU);
-    __syncthreads();
-    if (q == 0 && s == p.nsteps - 1)
-      for (int e = tid; e < R * R; e += kFThreads) p.Gam_out[e] = Gam[e];
-    for (int e = tid; e < nr * R; e += kFThreads) {
-      const int il = e / R, rr = e % R;
-      const int64_t i = r_beg + il;
-      const T m = cluster_sum(cluster, Mp, (int)(i * (R + 1) + rr), CU);
-      T ag = T(0);
-      for (int c = 0; c < R; ++c) ag += Aold[il * RS + c] * Gam[c * R + rr];
-      const T g = ag - m;
-      const int64_t gi = i * R + rr;
-      p.Gout[gi] = g;
-      const T a = Aold[il * RS + rr];
-      T an = a;
-      if (p.rule == 0) {
-        an = a - (T)alpha * g;
-      } else {
-        const T sv = Sold[il * RS + rr] + g * g;
-        p.S[n][gi] = sv;
-        if (sv > T(0)) {
-          T step;
-          if (p.eps == 0.0) step = (T)p.eta / sqrt((T)p.b + sv);
-          else step = (T)p.eta / (T)pow((double)((T)p.b + sv), 0.5 + p.eps);
-          an = a - step * g;
-        }
-      }
-      p.factors[n][gi] = an;
-      Anew[il * RS + rr] = an;
-    }
-    __syncthreads();
-    F_MARK(3);
-    // ------------------------------------------------ (3) importance table of the new A^(n)
+  // (a1) the table of the new A^(n) from this CTA's rows Anew (Gram / norm partials, cluster sums,
+  // sweep inverse, scores, quantisation, scan, resident CDF); s: the step index (phase marks), -1 for
+  // the rebuild prologue
+  auto build_table = [&](int n, int64_t In, int64_t rpc, int64_t r_beg, int nr, int s) {
     if (p.strategy != 0) {
       const bool lev = (p.strategy == 1 || p.strategy == 3);
       const int P = R * (R + 1) / 2;
@@ -658,6 +588,129 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
         if (st) atomicCAS(p.status, 0, st);
       }
     }
+  };
+
+  if (p.rebuild) {
+    // host input (cp_sgd_steps_host): each CTA compares its row block of every staged factor with the
+    // device copy; a mode with any difference anywhere is taken over and its table rebuilt (the
+    // tables are a function of the factors: an unchanged factor keeps its table)
+    __shared__ unsigned s_chg;
+    if (tid == 0) s_chg = 0u;
+    __syncthreads();
+    for (int k = 0; k < N; ++k) {
+      const int64_t In = p.dims[k];
+      const int64_t rpc = (In + CU - 1) / CU;
+      const int64_t r_beg = min((int64_t)q * rpc, In);
+      const int nr = (int)(min(r_beg + rpc, In) - r_beg);
+      bool diff = false;
+      for (int e = tid; e < nr * R; e += kFThreads)
+        diff |= !bits_equal(p.fstage[k][r_beg * R + e], p.factors[k][r_beg * R + e]);
+      if (__syncthreads_or(diff) && tid == 0) s_chg |= 1u << k;
+    }
+    cluster.sync();
+    unsigned chg = 0u;
+    for (int qq = 0; qq < CU; ++qq) chg |= *cluster.map_shared_rank(&s_chg, qq);
+    cluster.sync();  // every peer has read this CTA's flags
+    for (int k = 0; k < N; ++k) {
+      if (!((chg >> k) & 1u)) continue;
+      const int64_t In = p.dims[k];
+      const int64_t rpc = (In + CU - 1) / CU;
+      const int64_t r_beg = min((int64_t)q * rpc, In);
+      const int nr = (int)(min(r_beg + rpc, In) - r_beg);
+      for (int e = tid; e < nr * R; e += kFThreads) {
+        const T v = p.fstage[k][r_beg * R + e];
+        p.factors[k][r_beg * R + e] = v;
+        Anew[(e / R) * RS + e % R] = v;
+      }
+      __syncthreads();
+      if (p.strategy != 0) build_table(k, In, rpc, r_beg, nr, -1);
+      cluster.sync();  // new rows visible; the peers are done with this build's prefixes
+    }
+  }
+  int n = mode_of(r, 0);
+  int n_done = n;
+  sample_own(n, r);
+
+#pragma unroll 1
+  for (int s = 0; s < p.nsteps; ++s) {
+    F_MARK(0);
+    const int64_t In = p.dims[n];
+    const int64_t rpc = (In + CU - 1) / CU;
+    const int64_t r_beg = min((int64_t)q * rpc, In), r_end = min(r_beg + rpc, In);
+    const int nr = (int)(r_end - r_beg);
+    // ------------------------------------------------ (1) gather (Alg. 5) + partial contractions
+    cp_async_wait<0>();  // this batch's fiber segments (issued by sample_own)
+    __syncthreads();
+    // old rows (and adaptive accumulators) of the block this CTA updates: in flight during the gather
+    for (int e = tid; e < nr * R; e += kFThreads) {
+      const int il = e / R, c = e % R;
+      cp_async_small<sizeof(T)>(Aold + il * RS + c, p.factors[n] + (r_beg + il) * R + c, sizeof(T));
+      if (p.rule != 0) cp_async_small<sizeof(T)>(Sold + il * RS + c, p.S[n] + (r_beg + il) * R + c, sizeof(T));
+    }
+    cp_async_commit();
+    const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
+    gather_dispatch<T, ROWS>(xs, Ip, In, fb, zw, RP, p.BPC, Mp, R,
+                             (p.dbg && q == 0 && tid == 0 && s == 1) ? p.dbg : nullptr);
+    F_MARK(14);
+    {  // Gamma partial: 2 x 2 blocks (each entry still summed over the CTA's fibers in order)
+      const int h2 = (R + 1) >> 1;
+      for (int e = tid; e < h2 * h2; e += kFThreads) {
+        const int r1 = 2 * (e / h2), r2 = 2 * (e % h2);
+        const int r1b = r1 + 1 < R ? r1 + 1 : r1, r2b = r2 + 1 < R ? r2 + 1 : r2;
+        T g00 = T(0), g01 = T(0), g10 = T(0), g11 = T(0);
+        for (int lb = 0; lb < p.BPC; ++lb) {
+          const T w0 = zw[lb * RP + r1], w1 = zw[lb * RP + r1b], u0 = zu[lb * RP + r2], u1 = zu[lb * RP + r2b];
+          g00 += w0 * u0;
+          g01 += w0 * u1;
+          g10 += w1 * u0;
+          g11 += w1 * u1;
+        }
+        Gp[r1 * R + r2] = g00;
+        if (r2 + 1 < R) Gp[r1 * R + r2 + 1] = g01;
+        if (r1 + 1 < R) Gp[(r1 + 1) * R + r2] = g10;
+        if (r1 + 1 < R && r2 + 1 < R) Gp[(r1 + 1) * R + r2 + 1] = g11;
+      }
+    }
+    F_MARK(15);
+    cp_async_wait<0>();  // old rows / accumulators
+    F_MARK(1);
+    cluster.sync();  // #1: partials visible
+    F_MARK(2);
+    // ------------------------------------------------ (2) cluster reduction (rank order) + update
+    for (int e = tid; e < R * R; e += kFThreads) Gam[e] = cluster_sum(cluster, Gp, e, CU);
+    __syncthreads();
+    if (q == 0 && s == p.nsteps - 1)
+      for (int e = tid; e < R * R; e += kFThreads) p.Gam_out[e] = Gam[e];
+    for (int e = tid; e < nr * R; e += kFThreads) {
+      const int il = e / R, rr = e % R;
+      const int64_t i = r_beg + il;
+      const T m = cluster_sum(cluster, Mp, (int)(i * (R + 1) + rr), CU);
+      T ag = T(0);
+      for (int c = 0; c < R; ++c) ag += Aold[il * RS + c] * Gam[c * R + rr];
+      const T g = ag - m;
+      const int64_t gi = i * R + rr;
+      p.Gout[gi] = g;
+      const T a = Aold[il * RS + rr];
+      T an = a;
+      if (p.rule == 0) {
+        an = a - (T)alpha * g;
+      } else {
+        const T sv = Sold[il * RS + rr] + g * g;
+        p.S[n][gi] = sv;
+        if (sv > T(0)) {
+          T step;
+          if (p.eps == 0.0) step = (T)p.eta / sqrt((T)p.b + sv);
+          else step = (T)p.eta / (T)pow((double)((T)p.b + sv), 0.5 + p.eps);
+          an = a - step * g;
+        }
+      }
+      p.factors[n][gi] = an;
+      Anew[il * RS + rr] = an;
+    }
+    __syncthreads();
+    F_MARK(3);
+    // ------------------------------------------------ (3) importance table of the new A^(n)
+    build_table(n, In, rpc, r_beg, nr, s);
     ++r;
     n_done = n;
     const int n_next = mode_of(r, s + 1);

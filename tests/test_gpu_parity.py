@@ -295,6 +295,31 @@ def test_c4_full_size_tcgen05_step():
 
 
 # ------------------------------------------------------------------------------------------ e2e host path
+@pytest.mark.parametrize("fused", [True, False])
+def test_steps_host_takes_over_changed_factors(fused):
+    """cp_sgd_steps_host with host factors that differ from the device copy (one mode changed, then
+    all): the changed factors replace the device ones and their tables are rebuilt before the steps."""
+    cfg = synth.small((30, 20, 10), 4, dtype="f64", batch=32, rule="fixed", seed=8)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "leverage", seed=2, fused=fused)
+    rng = np.random.default_rng(5)
+    A1 = [a.copy() for a in A0]
+    A1[1] = A1[1] * np.exp(0.3 * rng.standard_normal(A1[1].shape))  # one mode changed
+    host = [torch.from_numpy(a.copy()).pin_memory() for a in A1]
+    h.steps_host(0, 3, host, 0.01)
+    fs, _, _ = oracle.run(X, A1, oracle.LEVERAGE, oracle.STEP_FIXED, cfg.batch, 3, alpha=0.01, seed=2)
+    for k in range(3):
+        assert rel_err(host[k].numpy(), fs[k], np.linalg.norm(fs[k])) <= 1e-10
+    A2 = [a * (1.0 + 0.1 * rng.standard_normal(a.shape)) for a in fs]  # every mode changed
+    host = [torch.from_numpy(a.copy()).pin_memory() for a in A2]
+    h.steps_host(0, 3, host, 0.01)
+    fs2, _, _ = oracle.run(X, A2, oracle.LEVERAGE, oracle.STEP_FIXED, cfg.batch, 3, alpha=0.01, seed=2, r0=3)
+    for k in range(3):
+        assert rel_err(host[k].numpy(), fs2[k], np.linalg.norm(fs2[k])) <= 1e-10
+    h.close()
+
+
 def test_steps_host_equals_device_path():
     cfg = synth.small((30, 20, 10), 4, dtype="f64", batch=32, rule="fixed", seed=8)
     X, A0 = make_problem(cfg)
