@@ -120,7 +120,8 @@ struct cp_sgd_s {
   uint32_t flags = 0;
   const void* X = nullptr;
   void* factors[kMaxOrder] = {};
-  void* fstage[kMaxOrder] = {};    // cp_sgd_steps_host staging of the host factors (fused path)
+  void* fstage[kMaxOrder] = {};    // cp_sgd_steps_host staging of the host factors (fused / wide path)
+  int* take_chg = nullptr;         // cp_sgd_steps_host (wide): per-mode "host factor differs" flags
   size_t esz = 4;
   // layout
   void* Xmm[kMaxOrder] = {};
@@ -705,7 +706,7 @@ bool uw_coresident(int R, int64_t In) {
 }
 
 template <typename T>
-cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
+cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, const int* take_chg = nullptr) {
   ProfScope ps(h, kKUpdateWide);
   UWParams<T> p;
   memset(&p, 0, sizeof p);
@@ -738,6 +739,9 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   p.Tout = h->Ttot + n;
   p.status = h->status_dev;
   p.qch = std::min<int64_t>(h->dims[n], 4096);
+  p.table_only = take_chg ? 1 : 0;  // cp_sgd_steps_host: take over the staged factor, rebuild its table
+  p.fstage = (const T*)h->fstage[n];
+  p.chg = take_chg;
   p.dbg = h->dbg;
   const size_t smem = uw_smem_bytes(h->R, sizeof(T), p.qch);
   static bool attr_set = false;
@@ -1425,6 +1429,7 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->fbase);
   cudaFree(h->zwp);
   for (int k = 0; k < kMaxOrder; ++k) cudaFree(h->fstage[k]);
+  cudaFree(h->take_chg);
   cudaFree(h->zimg);
   cudaFree(h->gam_next);
   cudaFree(h->Mpart);
@@ -1671,10 +1676,13 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
   if (st) return st;
   if (!factors_host) return h->fail(CP_EINVAL, "NULL factors_host");
   const bool fused = h->fused_cu && nsteps > 0;
+  bool wide = !fused && h->world_size == 1;  // every mode on the wide path: k_update_wide takes over
+  for (int k = 0; k < h->N; ++k) wide = wide && wide_mode(h, k);
+  const bool stage = fused || wide;
   for (int k = 0; k < h->N; ++k) {
     const size_t bytes = h->esz * h->dims[k] * h->R;
-    if (fused && !h->fstage[k]) CUDA_TRY(h, cudaMalloc(&h->fstage[k], bytes));
-    CUDA_TRY(h, cudaMemcpyAsync(fused ? h->fstage[k] : h->factors[k], factors_host[k], bytes, cudaMemcpyHostToDevice,
+    if (stage && !h->fstage[k]) CUDA_TRY(h, cudaMalloc(&h->fstage[k], bytes));
+    CUDA_TRY(h, cudaMemcpyAsync(stage ? h->fstage[k] : h->factors[k], factors_host[k], bytes, cudaMemcpyHostToDevice,
                                 h->stream));
   }
   h->pref_mode = -1;
@@ -1684,6 +1692,31 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
     if (st) return st;
     h->iter_host += nsteps;
     h->last_mode = (first_mode + nsteps - 1) % h->N;
+  } else if (wide) {  // changed factors (bitwise, per mode) taken over by k_update_wide, tables rebuilt
+    if (!h->take_chg) CUDA_TRY(h, cudaMalloc(&h->take_chg, sizeof(int) * kMaxOrder));
+    CUDA_TRY(h, cudaMemsetAsync(h->take_chg, 0, sizeof(int) * kMaxOrder, h->stream));
+    for (int k = 0; k < h->N; ++k) {
+      const int64_t ne = h->dims[k] * h->R;
+      const int blocks = (int)std::min<int64_t>(ceil_div(ne, 256), 148 * 4);
+      if (h->esz == 8)
+        k_take_compare<double><<<blocks, 256, 0, h->ls>>>((const double*)h->fstage[k], (const double*)h->factors[k], ne,
+                                                          h->take_chg + k);
+      else
+        k_take_compare<float><<<blocks, 256, 0, h->ls>>>((const float*)h->fstage[k], (const float*)h->factors[k], ne,
+                                                         h->take_chg + k);
+      h->launches++;
+      st = check_launch(h, "k_take_compare");
+      if (st) return st;
+    }
+    for (int k = 0; k < h->N; ++k) {
+      st = h->esz == 8 ? launch_uw_t<double>(h, k, 0.0, nullptr, h->take_chg + k)
+                       : launch_uw_t<float>(h, k, 0.0, nullptr, h->take_chg + k);
+      if (st) return st;
+    }
+    for (int s = 0; s < nsteps; ++s) {
+      st = cp_sgd_step(h, (first_mode + s) % h->N, alpha);
+      if (st) return st;
+    }
   } else {
     for (int k = 0; k < h->N; ++k) {
       st = launch_table_any(h, k);

@@ -63,8 +63,23 @@ struct UWParams {
   uint64_t* Tout;
   int* status;
   int64_t qch;        // last CTA's scan: q entries staged per round
+  int table_only;     // 1: no step; take over the staged rows fstage (if *chg) and rebuild the table
+  const T* fstage;
+  const int* chg;
   long long* dbg;
 };
+
+// cp_sgd_steps_host (wide path): chg[k] |= 1 when the staged host factor k differs bitwise from the
+// device copy (chg zeroed by the caller)
+template <typename T>
+__global__ void k_take_compare(const T* fstage, const T* A, int64_t n, int* chg) {
+  bool d = false;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    if constexpr (sizeof(T) == 8) d |= __double_as_longlong(fstage[e]) != __double_as_longlong(A[e]);
+    else d |= __float_as_uint(fstage[e]) != __float_as_uint(A[e]);
+  }
+  if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(chg, 1);
+}
 
 // (a6-a8) + (a1) up to the inverse: grid = ceil(I_n / kUWRows); dynamic shared memory = the step's
 // working set, or the last CTA's sweep workspace (Gram, sweep buffers), whichever is larger
@@ -325,100 +340,113 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
   double* sgp = reinterpret_cast<double*>(uw_sm + ((sizeof(T) * (3 * UR * RS + R * R) + 15) / 16) * 16);  // [P]
   __shared__ double sred[kWThreads / 32];
   cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
-  // rows of A and S, Gamma: every request in flight at once
-  for (int e = tid; e < nr * R; e += kWThreads) {
-    const int il = e / R, c = e % R;
-    cp_async_small<sizeof(T)>(sA + il * RS + c, p.A + (r0 + il) * R + c, sizeof(T));
-    if (p.rule != 0) cp_async_small<sizeof(T)>(sS + il * RS + c, p.S + (r0 + il) * R + c, sizeof(T));
-  }
-  for (int e = tid; e < R * R; e += kWThreads) cp_async_small<sizeof(T)>(sG + e, p.Gam + e, sizeof(T));
-  cp_async_commit();
-  // M = sum of the chunk partials, in chunk order (16-byte vectors of VW consecutive rows)
-  {
-    constexpr int VW = 16 / (int)sizeof(T);
-    using V = typename Vec<T>::type;
-    const int64_t tile = r0 / TI, lr0 = r0 % TI;
-    const int ng = (nr + VW - 1) / VW;
-    for (int t = tid; t < R * ng; t += kWThreads) {
-      const int r = t / ng, gq = t % ng;
-      const T* base = p.Mpart + ((tile * p.CK) * R + r) * TI + lr0 + gq * VW;
-      T acc[VW];
-#pragma unroll
-      for (int w = 0; w < VW; ++w) acc[w] = T(0);
-      for (int c0 = 0; c0 < p.CK; c0 += 8) {
-        V ld[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (c0 + k < p.CK) ld[k] = __ldcg(reinterpret_cast<const V*>(base + (int64_t)(c0 + k) * R * TI));
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (c0 + k < p.CK) {
-            const T* x = reinterpret_cast<const T*>(&ld[k]);
-#pragma unroll
-            for (int w = 0; w < VW; ++w) acc[w] += x[w];
-          }
-      }
-#pragma unroll
-      for (int w = 0; w < VW; ++w)
-        if (gq * VW + w < nr) sM[(gq * VW + w) * RS + r] = acc[w];
-    }
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  // G = A Gamma - M (each task owns its 4 x 4 block of M -> G in place)
   const int nb4 = (R + 3) >> 2;
-  for (int t = tid; t < ((nr + 3) >> 2) * nb4; t += kWThreads) {
-    const int a0 = 4 * (t / nb4), q0 = 4 * (t % nb4);
-    T acc[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][c] = T(0);
-    for (int k = 0; k < R; ++k) {
-      T x[4], y[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) x[a] = (a0 + a < nr) ? sA[(a0 + a) * RS + k] : T(0);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) y[c] = (q0 + c < R) ? sG[k * R + q0 + c] : T(0);
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c] = fma(x[a], y[c], acc[a][c]);
+  if (p.table_only) {
+    // cp_sgd_steps_host: the staged host rows replace the factor when any of them differs (the
+    // flag set by k_take_compare); an unchanged factor keeps its table: every CTA leaves here
+    if (__ldcg(p.chg) == 0) return;
+    for (int e = tid; e < nr * R; e += kWThreads) {
+      const int il = e / R, c = e % R;
+      const T v = p.fstage[(r0 + il) * R + c];
+      sA[il * RS + c] = v;
+      p.A[(r0 + il) * R + c] = v;
     }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (a0 + a < nr && q0 + c < R) sM[(a0 + a) * RS + q0 + c] = acc[a][c] - sM[(a0 + a) * RS + q0 + c];
-  }
-  __syncthreads();
-  // fixed (eq:proposed) / adaptive (eq:etaada/eq:Aada, :531-537, R12) update
-  const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
-  for (int e = tid; e < nr * R; e += kWThreads) {
-    const int il = e / R, r = e % R;
-    const int64_t gi = (r0 + il) * R + r;
-    const T g = sM[il * RS + r];
-    p.Gout[gi] = g;
-    const T a = sA[il * RS + r];
-    T an = a;
-    if (p.rule == 0) {
-      an = a - (T)alpha * g;
-    } else {
-      const T sv = sS[il * RS + r] + g * g;
-      p.S[gi] = sv;
-      if (sv > T(0)) {
-        T step;
-        if (p.eps == 0.0) step = (T)p.eta / sqrt((T)p.b + sv);
-        else step = (T)p.eta / (T)pow((double)((T)p.b + sv), 0.5 + p.eps);
-        an = a - step * g;
+    __syncthreads();
+  } else {
+    // rows of A and S, Gamma: every request in flight at once
+    for (int e = tid; e < nr * R; e += kWThreads) {
+      const int il = e / R, c = e % R;
+      cp_async_small<sizeof(T)>(sA + il * RS + c, p.A + (r0 + il) * R + c, sizeof(T));
+      if (p.rule != 0) cp_async_small<sizeof(T)>(sS + il * RS + c, p.S + (r0 + il) * R + c, sizeof(T));
+    }
+    for (int e = tid; e < R * R; e += kWThreads) cp_async_small<sizeof(T)>(sG + e, p.Gam + e, sizeof(T));
+    cp_async_commit();
+    // M = sum of the chunk partials, in chunk order (16-byte vectors of VW consecutive rows)
+    {
+      constexpr int VW = 16 / (int)sizeof(T);
+      using V = typename Vec<T>::type;
+      const int64_t tile = r0 / TI, lr0 = r0 % TI;
+      const int ng = (nr + VW - 1) / VW;
+      for (int t = tid; t < R * ng; t += kWThreads) {
+        const int r = t / ng, gq = t % ng;
+        const T* base = p.Mpart + ((tile * p.CK) * R + r) * TI + lr0 + gq * VW;
+        T acc[VW];
+  #pragma unroll
+        for (int w = 0; w < VW; ++w) acc[w] = T(0);
+        for (int c0 = 0; c0 < p.CK; c0 += 8) {
+          V ld[8];
+  #pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (c0 + k < p.CK) ld[k] = __ldcg(reinterpret_cast<const V*>(base + (int64_t)(c0 + k) * R * TI));
+  #pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (c0 + k < p.CK) {
+              const T* x = reinterpret_cast<const T*>(&ld[k]);
+  #pragma unroll
+              for (int w = 0; w < VW; ++w) acc[w] += x[w];
+            }
+        }
+  #pragma unroll
+        for (int w = 0; w < VW; ++w)
+          if (gq * VW + w < nr) sM[(gq * VW + w) * RS + r] = acc[w];
       }
     }
-    p.A[gi] = an;
-    sA[il * RS + r] = an;
+    cp_async_wait<0>();
+    __syncthreads();
+    // G = A Gamma - M (each task owns its 4 x 4 block of M -> G in place)
+    for (int t = tid; t < ((nr + 3) >> 2) * nb4; t += kWThreads) {
+      const int a0 = 4 * (t / nb4), q0 = 4 * (t % nb4);
+      T acc[4][4];
+  #pragma unroll
+      for (int a = 0; a < 4; ++a)
+  #pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = T(0);
+      for (int k = 0; k < R; ++k) {
+        T x[4], y[4];
+  #pragma unroll
+        for (int a = 0; a < 4; ++a) x[a] = (a0 + a < nr) ? sA[(a0 + a) * RS + k] : T(0);
+  #pragma unroll
+        for (int c = 0; c < 4; ++c) y[c] = (q0 + c < R) ? sG[k * R + q0 + c] : T(0);
+  #pragma unroll
+        for (int a = 0; a < 4; ++a)
+  #pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = fma(x[a], y[c], acc[a][c]);
+      }
+  #pragma unroll
+      for (int a = 0; a < 4; ++a)
+  #pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (a0 + a < nr && q0 + c < R) sM[(a0 + a) * RS + q0 + c] = acc[a][c] - sM[(a0 + a) * RS + q0 + c];
+    }
+    __syncthreads();
+    // fixed (eq:proposed) / adaptive (eq:etaada/eq:Aada, :531-537, R12) update
+    const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
+    for (int e = tid; e < nr * R; e += kWThreads) {
+      const int il = e / R, r = e % R;
+      const int64_t gi = (r0 + il) * R + r;
+      const T g = sM[il * RS + r];
+      p.Gout[gi] = g;
+      const T a = sA[il * RS + r];
+      T an = a;
+      if (p.rule == 0) {
+        an = a - (T)alpha * g;
+      } else {
+        const T sv = sS[il * RS + r] + g * g;
+        p.S[gi] = sv;
+        if (sv > T(0)) {
+          T step;
+          if (p.eps == 0.0) step = (T)p.eta / sqrt((T)p.b + sv);
+          else step = (T)p.eta / (T)pow((double)((T)p.b + sv), 0.5 + p.eps);
+          an = a - step * g;
+        }
+      }
+      p.A[gi] = an;
+      sA[il * RS + r] = an;
+    }
+    if (blockIdx.x == 0)
+      for (int e = tid; e < R * R; e += kWThreads) p.Gam_out[e] = sG[e];
+    __syncthreads();
   }
-  if (blockIdx.x == 0)
-    for (int e = tid; e < R * R; e += kWThreads) p.Gam_out[e] = sG[e];
-  __syncthreads();
   // table partials of the new rows (R9: the table of A^(n) is rebuilt after every update)
   if (p.strategy == 1 || p.strategy == 3) {  // leverage: partial fp64 Gram, packed upper triangle
     const int P = R * (R + 1) / 2;
