@@ -1713,9 +1713,14 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
                        : launch_uw_t<float>(h, k, 0.0, nullptr, h->take_chg + k);
       if (st) return st;
     }
-    for (int s = 0; s < nsteps; ++s) {
-      st = cp_sgd_step(h, (first_mode + s) % h->N, alpha);
+    if (first_mode == 0 && nsteps % h->N == 0 && alpha < 0.0) {  // whole cyclic sweeps: the sweep graph
+      st = cp_sgd_sweep(h, nsteps / h->N, CP_ORDER_CYCLIC, nullptr);
       if (st) return st;
+    } else {
+      for (int s = 0; s < nsteps; ++s) {
+        st = cp_sgd_step(h, (first_mode + s) % h->N, alpha);
+        if (st) return st;
+      }
     }
   } else {
     for (int k = 0; k < h->N; ++k) {
