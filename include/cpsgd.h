@@ -152,7 +152,9 @@ cp_status cp_sgd_sync(cp_sgd_t h);
 /* Host-buffer convenience path (the end-to-end call): copy the N factors from host buffers
  * (pinned recommended) to the device, run `nsteps` cyclic iterations starting at mode
  * `first_mode`, copy every factor back to the host buffers.  factors_host: N host pointers,
- * row-major I_n x R of cfg.dtype.  Synchronises. */
+ * row-major I_n x R of cfg.dtype.  A host factor that differs bitwise from the device copy
+ * replaces it and its table is rebuilt before the first iteration (R9: the tables are a function
+ * of the factors; an unchanged factor keeps its table).  Synchronises. */
 cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, double alpha,
                             void* const* factors_host);
 
