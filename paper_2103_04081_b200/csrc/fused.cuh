@@ -93,7 +93,7 @@ __host__ __device__ inline FusedLayout fused_layout(int N, int R, int BPC, int R
   L.gm = take(sizeof(double) * R * (R + 1));
   L.prow = take(sizeof(double) * RPC);
   L.sc = take(sizeof(double) * RPC * R);
-  L.rowbuf = take(sizeof(double) * 3 * kMaxRank);
+  L.rowbuf = take(sizeof(double) * kSweepBuf);
   L.swept = take(sizeof(int) * R);
   L.qtot = take(sizeof(unsigned long long) * 2);
   L.qpre = take(sizeof(unsigned long long) * RPC);

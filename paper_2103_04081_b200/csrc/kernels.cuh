@@ -22,6 +22,7 @@ namespace cps {
 
 constexpr int kMaxOrder = 16;
 constexpr int kMaxRank = 64;
+constexpr int kSweepBuf = 5 * kMaxRank;  // doubles of pivot-row buffer the sweep inverses need
 
 // ------------------------------------------------------------------------------------------
 // Parameters (passed by value; < 1 KB)
@@ -839,19 +840,24 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // R4(b), the rank rule of a pivoted Cholesky); after sweeping S, M_SS = -(G_SS)^{-1}.
 // Row groups x lanes: thread (g, c) of NT = 32 ceil(RMAX/32) G threads keeps rows
 // [g RPG, (g + 1) RPG) of column c of the RMAX x RMAX matrix (identity past R; RMAX = ceil8(R),
-// RPG = ceil(RMAX / G)) in registers, static indices, no rotation.  Pivot k:
-//   publish  the owner group of row k stores M_kc (register select on k mod RPG) at rb[c]; by
-//            symmetry rb[t] = M_tk is also the pivot column (broadcast loads);
-//   d = rb[k] > tol:  f = (c == k) ? -1/d : rb[c]/d;
-//                     row k <- f;  row t != k <- [c != k] M_tc - rb[t] f;      otherwise nothing.
-// The single-warp lane-per-column form is issue-bound (one warp issues all RMAX^2 updates of a
-// pivot); spreading the rows over G groups puts G (x 2 for RMAX > 32) warps on the SM's four
-// schedulers: R = 20: 17.6k -> 9.4k cycles, R = 50: 56k -> 36k (tools/micro/sweep_grp.cu, results
-// bit-identical).  One named barrier per pivot (double-buffered rb).  Called by every thread of the
-// CTA (>= NT threads); returns |S|.
+// RPG = ceil(RMAX / G)) in registers, static indices, no rotation.  Pivots go in natural order in
+// PAIRS P = {k, l = k + 1}: the owner groups of rows k and l publish them to shared memory (by
+// symmetry rb1[t] = M_tk, rb2[t] = M_tl are also the pivot columns), one named barrier, then with
+// B = M_PP = [[a, b], [b, c]] and det = a c - b^2:
+//   a > tol and det > tol a  (both Schur diagonals a and det / a above tol: the single-pivot rule)
+//     -> block sweep with ONE reciprocal 1/det: per column (f1, f2) = B^{-1} M_Pc (c not in P) or the
+//        negated column of B^{-1} (c in P); rows k, l <- f1, f2; others <- [c not in P] M_tc -
+//        rb1[t] f1 - rb2[t] f2 (the sweep operator on the block, M_PP -> -B^{-1});
+//   otherwise single-pivot steps for k (if a > tol) and then l on the updated values (d > tol),
+//   i.e. exactly the natural-order single-pivot sweep with the skip rule of R4(b).
+// The pivot chain (publish -> barrier -> reciprocal -> update) is paid once per two pivots; the
+// single-pivot row-group form was bound by that chain (~420 cycles per pivot): R = 20: 9.6k -> 8.0k
+// cycles, R = 50: 37.7k -> 27.5k (tools/micro/sweep_grp.cu; results within 2e-15 of it).
+// Called by every thread of the CTA (>= NT threads); rowbuf: kSweepBuf doubles; returns |S|.
 template <int RMAX, int G>
-__device__ int grp_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /* 2 (RPG G + 8) */, int* swept) {
+__device__ int grp_sweep_inverse(double* Gm, int R, double tol, double* rowbuf, int* swept) {
   constexpr int CW = (RMAX + 31) / 32, NT = 32 * CW * G, RPG = (RMAX + G - 1) / G, RB = RPG * G + 8;
+  static_assert(4 * RB <= kSweepBuf, "sweep buffer");
   const int tid = threadIdx.x, RS = R + 1;
   if (tid < NT) {
     const int g = tid / (32 * CW), c = tid % (32 * CW);
@@ -862,9 +868,7 @@ __device__ int grp_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /
       v[t] = (row < R && c < R) ? Gm[row * RS + c] : (row == c ? 1.0 : 0.0);
     }
     for (int j = tid; j < R; j += NT) swept[j] = 0;
-#pragma unroll 1
-    for (int k = 0; k < R; ++k) {
-      double* rb = rowbuf + (k & 1) * RB;
+    auto publish = [&](int k, double* rb) {  // owner group of row k: M_kc -> rb[c]
       const int gk = k / RPG, tk = k - gk * RPG;
       if (g == gk) {
         double pv = v[0];
@@ -872,18 +876,64 @@ __device__ int grp_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /
         for (int t = 1; t < RPG; ++t) pv = (tk == t) ? v[t] : pv;
         rb[c] = pv;
       }
+    };
+    auto single = [&](int k, const double* rb, double d) {  // one sweep step on pivot k (d = M_kk > tol)
+      const double dinv = __drcp_rn(d);
+      const bool isk = (c == k);
+      const double f = isk ? -dinv : rb[c] * dinv;
+#pragma unroll
+      for (int t = 0; t < RPG; ++t) {
+        const int row = g * RPG + t;
+        v[t] = (row == k) ? f : fma(-rb[row], f, isk ? 0.0 : v[t]);
+      }
+      if (tid == 0) swept[k] = 1;
+    };
+    int par = 0;
+#pragma unroll 1
+    for (int k = 0; k < R; k += 2) {
+      const int l = k + 1;  // == R: the last pivot alone
+      double* rb1 = rowbuf + par * 2 * RB;
+      double* rb2 = rb1 + RB;
+      par ^= 1;
+      publish(k, rb1);
+      if (l < R) publish(l, rb2);
       named_bar_sync(1, NT);
-      const double d = rb[k];
-      if (d > tol) {  // uniform
-        const double dinv = __drcp_rn(d);
-        const bool isk = (c == k);
-        const double f = isk ? -dinv : rb[c] * dinv;
+      const double a = rb1[k];
+      const double b = l < R ? rb1[l] : 0.0, cc = l < R ? rb2[l] : 0.0;
+      const double det = fma(a, cc, -b * b);
+      if (l < R && a > tol && det > tol * a) {  // uniform
+        const double dinv = __drcp_rn(det);
+        double f1, f2;
+        if (c == k) {
+          f1 = -cc * dinv;
+          f2 = b * dinv;
+        } else if (c == l) {
+          f1 = b * dinv;
+          f2 = -a * dinv;
+        } else {
+          const double mk = rb1[c], ml = rb2[c];
+          f1 = fma(cc, mk, -b * ml) * dinv;
+          f2 = fma(a, ml, -b * mk) * dinv;
+        }
+        const bool isp = (c == k) || (c == l);
 #pragma unroll
         for (int t = 0; t < RPG; ++t) {
           const int row = g * RPG + t;
-          v[t] = (row == k) ? f : fma(-rb[row], f, isk ? 0.0 : v[t]);
+          v[t] = (row == k) ? f1 : (row == l) ? f2 : fma(-rb1[row], f1, fma(-rb2[row], f2, isp ? 0.0 : v[t]));
         }
-        if (tid == 0) swept[k] = 1;
+        if (tid == 0) {
+          swept[k] = 1;
+          swept[l] = 1;
+        }
+      } else {
+        if (a > tol) single(k, rb1, a);
+        if (l < R) {  // pivot l on the values after step k: republish its row
+          named_bar_sync(1, NT);  // every thread is done with rb2
+          publish(l, rb2);
+          named_bar_sync(1, NT);
+          const double d = rb2[l];
+          if (d > tol) single(l, rb2, d);
+        }
       }
     }
     named_bar_sync(1, NT);
@@ -902,13 +952,14 @@ __device__ int grp_sweep_inverse(double* Gm, int R, double tol, double* rowbuf /
 }
 
 // MAXR: largest rank the calling kernel supports (instantiates only RMAX <= MAXR); needs 256 threads
+// (128 for RMAX <= 32)
 template <int MAXR = kMaxRank>
 __device__ inline int grp_sweep_dispatch(double* Gm, int R, double tol, double* rowbuf, int* swept) {
   switch ((R + 7) / 8) {
-    case 1: return grp_sweep_inverse<8, 8>(Gm, R, tol, rowbuf, swept);
-    case 2: return grp_sweep_inverse<16, 8>(Gm, R, tol, rowbuf, swept);
-    case 3: return grp_sweep_inverse<24, 8>(Gm, R, tol, rowbuf, swept);
-    case 4: return grp_sweep_inverse<32, 8>(Gm, R, tol, rowbuf, swept);
+    case 1: return grp_sweep_inverse<8, 4>(Gm, R, tol, rowbuf, swept);
+    case 2: return grp_sweep_inverse<16, 4>(Gm, R, tol, rowbuf, swept);
+    case 3: return grp_sweep_inverse<24, 4>(Gm, R, tol, rowbuf, swept);
+    case 4: return grp_sweep_inverse<32, 4>(Gm, R, tol, rowbuf, swept);
     default: break;
   }
   if constexpr (MAXR > 32) {
@@ -1052,7 +1103,7 @@ __host__ __device__ inline size_t ut_smem_bytes(int R, int64_t rows_per, size_t 
   take(esz * rows_per * (R + 1));        // Anew
   take(sizeof(double) * (R * (R + 1) / 2 + 1));  // partial Gram / partial ||A||^2 (read by peers)
   take(sizeof(double) * R * (R + 1));    // Gm (Gram -> inverse), row stride R+1
-  take(sizeof(double) * 3 * kMaxRank);   // sweep column buffer (triple-buffered pivot column)
+  take(sizeof(double) * kSweepBuf);   // sweep pivot-row buffers
   take(sizeof(int) * R);                 // swept flags
   take(sizeof(double) * rows_per);       // per-row p
   take(sizeof(unsigned long long) * rows_per);   // per-row q -> local inclusive scan
@@ -1091,7 +1142,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   T* Anew = reinterpret_cast<T*>(carve(sizeof(T) * p.rows_per * RS));
   double* gpart = reinterpret_cast<double*>(carve(sizeof(double) * (R * (R + 1) / 2 + 1)));
   double* Gm = reinterpret_cast<double*>(carve(sizeof(double) * R * (R + 1)));
-  double* rowbuf = reinterpret_cast<double*>(carve(sizeof(double) * 3 * kMaxRank));
+  double* rowbuf = reinterpret_cast<double*>(carve(sizeof(double) * kSweepBuf));
   int* swept = reinterpret_cast<int*>(carve(sizeof(int) * R));
   double* prow = reinterpret_cast<double*>(carve(sizeof(double) * p.rows_per));
   unsigned long long* qrow = reinterpret_cast<unsigned long long*>(carve(sizeof(unsigned long long) * p.rows_per));

@@ -84,7 +84,7 @@ __global__ void k_take_compare(const T* fstage, const T* A, int64_t n, int* chg)
 // (a6-a8) + (a1) up to the inverse: grid = ceil(I_n / kUWRows); dynamic shared memory = the step's
 // working set, or the last CTA's sweep workspace (Gram, sweep buffers), whichever is larger
 __host__ __device__ inline size_t uw_sweep_ws_bytes(int R) {  // Gram + sweep buffers + swept flags
-  return sizeof(double) * ((size_t)R * (R + 1) + 3 * kMaxRank + kMaxRank) + sizeof(int) * kMaxRank + 64;
+  return sizeof(double) * ((size_t)R * (R + 1) + kSweepBuf + kMaxRank) + sizeof(int) * kMaxRank + 64;
 }
 // dynamic shared memory: [step area: A, S, M rows, Gamma, Gram partial] [ext area: the last
 // cluster's Gram slice + sweep workspace | W + score partials | the scan's q staging]
@@ -118,7 +118,7 @@ __device__ void uw_table_tail(const UWParams<T>& p, unsigned char* sm, const coo
   if (p.strategy == 1 || p.strategy == 3) {
     double* Gm = reinterpret_cast<double*>(sm);
     double* rowbuf = Gm + R * RS;
-    double* diag = rowbuf + 3 * kMaxRank;
+    double* diag = rowbuf + kSweepBuf;
     int* swept = reinterpret_cast<int*>(diag + kMaxRank);
     double* slice = reinterpret_cast<double*>(sm + (uw_sweep_ws_bytes(R) + 15) / 16 * 16);
     const int per = (P + CU - 1) / CU;
