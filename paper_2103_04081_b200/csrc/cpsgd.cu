@@ -563,6 +563,9 @@ cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   p.Mpart = (T*)h->Mpart;
   p.cnt = h->gu_cnt;
   p.Gam = (const T*)h->gam_next;
+  p.gcl = (decltype(p.gcl))h->sw_gcl;
+  p.ncl = (int)ceil_div(ceil_div(h->bmax[n], kSWFibers), kSWCluster);
+  p.gam_sum = (decltype(p.gam_sum))h->gam_next;
   p.A = (T*)h->factors[n];
   p.S = (T*)h->S[n];
   p.Gout = (T*)h->Gout;
@@ -616,6 +619,9 @@ cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev
   p.Mpart = (float*)h->Mpart;
   p.cnt = h->gu_cnt;
   p.Gam = (const float*)h->gam_next;
+  p.gcl = (decltype(p.gcl))h->sw_gcl;
+  p.ncl = (int)ceil_div(ceil_div(h->bmax[n], kSWFibers), kSWCluster);
+  p.gam_sum = (decltype(p.gam_sum))h->gam_next;
   p.A = (float*)h->factors[n];
   p.S = (float*)h->S[n];
   p.Gout = (float*)h->Gout;

@@ -39,6 +39,9 @@ struct GUParams {
   int64_t bmax;           // rows of the batch buffers for this mode
   int64_t KB;             // fibers per chunk (= per CTA)
   const T* Gam;           // [R][R] Gamma of this batch (sampler)
+  const T* gcl;           // [ncl][R][R] the sampler's cluster partials of Gamma
+  int ncl;
+  T* gam_sum;             // out: Gamma = sum of the partials in cluster order (read by k_update_wide)
   T* A;                   // A^(n), row-major I_n x R, updated in place
   T* S;                   // adaptive accumulator or NULL
   T* Gout;                // G (debug hook)
@@ -68,6 +71,24 @@ __host__ __device__ inline size_t gu_smem_bytes(int64_t KB) {
   constexpr size_t a = gu_pipe_bytes<T, CPT>() > gu_epi_bytes<T, CPT>() ? gu_pipe_bytes<T, CPT>()
                                                                           : gu_epi_bytes<T, CPT>();
   return a + (size_t)kMaxRank * kMaxRank * sizeof(T) + (size_t)KB * sizeof(int64_t) + 64;
+}
+
+// Gamma = sum over the sampler's cluster partials in cluster order: entries [e0, E) with stride
+// es, every load of an entry in flight at once.  Run by threads the gather kernels leave idle (the
+// kernels themselves never read Gamma; k_update_wide does, after them).
+template <typename T>
+__device__ __forceinline__ void gu_gamma_sum(const GUParams<T>& p, int e0, int es) {
+  const int E = p.R * p.R;
+  for (int e = e0; e < E; e += es) {
+    T v[16], s = T(0);
+    for (int c0 = 0; c0 < p.ncl; c0 += 16) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = (c0 + k < p.ncl) ? __ldcg(p.gcl + (int64_t)(c0 + k) * E + e) : T(0);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) s += v[k];  // cluster order; zeros past ncl are exact
+    }
+    p.gam_sum[e] = s;
+  }
 }
 
 // Epilogue shared by both mainloops: this CTA's partial tile M_c (shared, [TI][MS]) -> the split-K
@@ -110,6 +131,10 @@ __global__ void __launch_bounds__(kGUThreads, 1) k_gather_update(GUParams<T> p) 
 
   pdl_trigger();
   pdl_wait();  // the batch comes from the previous kernel
+  {  // Gamma: one entry per thread over the whole grid
+    const int lin = (blockIdx.y * gridDim.x + blockIdx.x) * kGUThreads + tid;
+    gu_gamma_sum<T>(p, lin, gridDim.x * gridDim.y * kGUThreads);
+  }
   cp_async_u64(reinterpret_cast<uint64_t*>(sfb), reinterpret_cast<const uint64_t*>(p.fbase + c0), nfib, tid,
                kGUThreads);
   cp_async_wait<0>();

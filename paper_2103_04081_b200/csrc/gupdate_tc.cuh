@@ -234,7 +234,11 @@ __global__ void __launch_bounds__(kTCThreads, 1) k_gather_update_tc(GUParams<flo
     }
   } else if (wid == 12) {
     // ======================= A producer (one thread): the sampler's zh / zl image of the stage =======================
-    if (lane == 0) {
+    // (lanes 1-31: Gamma as the cluster-ordered sum of the sampler's partials, spread over the grid)
+    if (lane != 0) {
+      const int cta_lin = blockIdx.y * gridDim.x + blockIdx.x;
+      gu_gamma_sum<float>(p, cta_lin * 31 + lane - 1, gridDim.x * gridDim.y * 31);
+    } else {
       for (int st = 0; st < nst; ++st) {
         const int zs = st % NZ;
         if (st >= NZ) mbar_wait(&afree[zs], (uint32_t)(((st / NZ) - 1) & 1));

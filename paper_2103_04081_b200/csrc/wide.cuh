@@ -787,28 +787,9 @@ __global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
     }
   }
   SWM(6);
-  pdl_trigger();  // the batch is written: the gather may start its launch
-  __threadfence();
-  cluster.sync();  // the whole cluster partial is written
-  if (q == 0 && tid == 0) s_last = (atomicAdd(P.cnt, 1u) == (unsigned)(ncl - 1));
-  cluster.sync();
-  if (*cluster.map_shared_rank(&s_last, 0)) {  // this cluster arrived last: its CTAs sum all partials
-    __threadfence();
-    T* out = reinterpret_cast<T*>(sp.gam_next);
-    const int E = R * R, per = (E + CU - 1) / CU;
-    for (int e = q * per + tid; e < min(E, (q + 1) * per); e += kWThreads) {
-      T v[16], s = T(0);
-      for (int c0 = 0; c0 < ncl; c0 += 16) {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = (c0 + k < ncl) ? __ldcg(gcl + (int64_t)(c0 + k) * E + e) : T(0);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) s += v[k];  // cluster order; zeros past ncl are exact
-      }
-      out[e] = s;
-    }
-    if (q == 0 && tid == 0) *P.cnt = 0u;
-  }
-  cluster.sync();  // rank 0's s_last read by the peers before it exits
+  // the cross-cluster sum of the partials (cluster order) is done by idle lanes of the next
+  // kernel, the gather (gu_gamma_sum): it does not read Gamma, k_update_wide after it does
+  cluster.sync();  // peers are done reading this CTA's partial
   SWM(7);
   if (P.dbg && tid == 0 && blockIdx.x < 480) {
     long long gt1;
