@@ -106,7 +106,7 @@ __host__ __device__ inline size_t uw_smem_bytes(int R, size_t esz, int64_t qch) 
 
 // The last k_update_wide cluster to finish: the Gram of the new A^(n) as the cluster-ordered sum of
 // the cluster partials (each CTA sums a slice of the pairs, every load of a pair in flight at
-// once; rank 0 gathers the slices over DSMEM), then rank 0 inverts it by the symmetric sweep on the
+// once, and stores it into rank 0's Gram over DSMEM), then rank 0 inverts it by the symmetric sweep on the
 // numerically full-rank pivot set (R4(b)) -> W, |S| in global memory.  Euclidean: ||A||_F^2.
 // (Def. 2.3 / eq:lev, reading R4.)
 template <typename T>
@@ -120,7 +120,9 @@ __device__ void uw_table_tail(const UWParams<T>& p, unsigned char* sm, const coo
     double* rowbuf = Gm + R * RS;
     double* diag = rowbuf + kSweepBuf;
     int* swept = reinterpret_cast<int*>(diag + kMaxRank);
-    double* slice = reinterpret_cast<double*>(sm + (uw_sweep_ws_bytes(R) + 15) / 16 * 16);
+    // each CTA of the cluster sums a slice of the pairs and stores it straight into rank 0's Gram
+    // (DSMEM stores), one cluster barrier
+    double* Gm0 = cluster.map_shared_rank(Gm, 0);
     const int per = (P + CU - 1) / CU;
     for (int pair = q * per + tid; pair < min(P, (q + 1) * per); pair += kWThreads) {
       double v[16], s = 0.0;
@@ -130,20 +132,12 @@ __device__ void uw_table_tail(const UWParams<T>& p, unsigned char* sm, const coo
 #pragma unroll
         for (int k = 0; k < 16; ++k) s += v[k];  // cluster order; zeros past ncl are exact
       }
-      slice[pair - q * per] = s;
+      int r1 = 0, rem = pair;
+      while (rem >= R - r1) { rem -= R - r1; ++r1; }
+      Gm0[r1 * RS + r1 + rem] = s;
+      Gm0[(r1 + rem) * RS + r1] = s;
     }
-    cluster.sync();  // slices complete
-    if (q == 0) {
-      for (int pair = tid; pair < P; pair += kWThreads) {
-        const int owner = pair / per;
-        const double s = cluster.map_shared_rank(slice, owner)[pair - owner * per];
-        int r1 = 0, rem = pair;
-        while (rem >= R - r1) { rem -= R - r1; ++r1; }
-        Gm[r1 * RS + r1 + rem] = s;
-        Gm[(r1 + rem) * RS + r1] = s;
-      }
-    }
-    cluster.sync();  // rank 0 done reading the peers' slices
+    cluster.sync();  // rank 0's Gram complete
     if (q != 0) return;
     if (tid == 0) s_bad = 0;
     WMARK(true, 313);
