@@ -23,7 +23,7 @@ _LIB = os.path.join(_HERE, "liborc.so")
 
 UNIFORM, LEVERAGE, EUCLIDEAN, BLOCK_LEVERAGE, BLOCK_EUCLIDEAN = 0, 1, 2, 3, 4
 STRATEGIES = {"uniform": 0, "leverage": 1, "euclidean": 2, "block_leverage": 3, "block_euclidean": 4}
-STEP_FIXED, STEP_ADAPTIVE = 0, 1
+STEP_FIXED, STEP_ADAPTIVE, STEP_ALS = 0, 1, 2
 ORDER_CYCLIC, ORDER_RANDOM = 0, 1
 
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall"]
@@ -62,6 +62,8 @@ def lib():
         L.orc_gradient.argtypes = [i32, P, i32, P, P, i32, i32, i64, i64, P, P, P, P, P]
         L.orc_update_fixed.argtypes = [i64, i32, P, P, dbl]
         L.orc_update_adaptive.argtypes = [i64, i32, P, P, P, dbl, dbl, dbl]
+        L.orc_update_als.argtypes = [i64, i32, P, P, P]
+        L.orc_sym_pinv.argtypes = [i32, P, P]
         L.orc_fit.argtypes = [i32, P, P, i32, P, P, P, P]
         L.orc_random_mode.argtypes = [u64, u64, i32]
         L.orc_run.argtypes = [i32, P, i32, P, P, P, i32, i32, i32, i64, P, dbl, P, dbl, dbl, dbl, u64, u64, i64, P]
@@ -212,6 +214,26 @@ def update_fixed(A: np.ndarray, G: np.ndarray, alpha: float) -> np.ndarray:
     A = _f64(A).copy()
     G = _f64(G)
     lib().orc_update_fixed(A.shape[0], A.shape[1], _p(A), _p(G), alpha)
+    return A
+
+
+def sym_pinv(Gam: np.ndarray):
+    """Gamma^+ on the numerically full-rank pivot set (natural-order sweep, tol R eps max diag).
+    Returns (W, rank)."""
+    G = _f64(Gam)
+    W = np.zeros_like(G)
+    rk = lib().orc_sym_pinv(G.shape[0], _p(G), _p(W))
+    if rk < 0:
+        raise OracleError("sym_pinv: out of memory")
+    return W, int(rk)
+
+
+def update_als(M: np.ndarray, Gam: np.ndarray) -> np.ndarray:
+    """the sampled least-squares step A = M Gamma^+ (eq:lsq_krp on eq:gradient1/2's M, Gamma)."""
+    M = _f64(M)
+    G = _f64(Gam)
+    A = np.zeros_like(M)
+    _chk(lib().orc_update_als(M.shape[0], M.shape[1], _p(A), _p(M), _p(G)), "update_als")
     return A
 
 

@@ -40,6 +40,7 @@
 
 #define ORC_STEP_FIXED 0    /* eq:proposed (4.3) */
 #define ORC_STEP_ADAPTIVE 1 /* eq:etaada/eq:Aada (4.4) */
+#define ORC_STEP_ALS 2      /* sampled least squares: A = M Gamma^+ (eq:lsq_krp) */
 
 #define ORC_ORDER_CYCLIC 0
 #define ORC_ORDER_RANDOM 1 /* "uniformly sample n" */
@@ -493,6 +494,69 @@ int orc_gradient(int N, const int64_t* dims, int R, const double* X, const doubl
   return ORC_OK;
 }
 
+/* Gamma^+ of a symmetric R x R matrix on its numerically full-rank pivot set: the symmetric sweep
+ * operator in natural order, pivot k swept when its current diagonal exceeds
+ * tol = R * eps * max_i Gam_ii (reading R25: the rank rule of the sampled-ALS solve); on the swept
+ * set S, W_SS = (Gam_SS)^{-1}, zero elsewhere.  Plain O(R^3) loops.  Returns |S|. */
+int orc_sym_pinv(int R, const double* Gam, double* W) {
+  double* M = (double*)malloc(sizeof(double) * (size_t)(R * R));
+  double* rk = (double*)malloc(sizeof(double) * (size_t)R);
+  int* swept = (int*)calloc((size_t)R, sizeof(int));
+  if (!M || !rk || !swept) {
+    free(M); free(rk); free(swept);
+    return -1;
+  }
+  double dmax = 0.0;
+  for (int i = 0; i < R * R; ++i) M[i] = Gam[i];
+  for (int i = 0; i < R; ++i)
+    if (M[i * R + i] > dmax) dmax = M[i * R + i];
+  const double tol = (double)R * 2.220446049250313e-16 * dmax;
+  int rank = 0;
+  for (int k = 0; k < R; ++k) {
+    const double d = M[k * R + k];
+    if (!(d > tol)) continue;
+    for (int j = 0; j < R; ++j) rk[j] = M[k * R + j];  /* row k before the step (= column k) */
+    for (int i = 0; i < R; ++i) {
+      if (i == k) continue;
+      for (int j = 0; j < R; ++j) {
+        if (j == k) continue;
+        M[i * R + j] -= rk[i] * rk[j] / d;
+      }
+    }
+    for (int j = 0; j < R; ++j)
+      if (j != k) {
+        M[k * R + j] = rk[j] / d;
+        M[j * R + k] = rk[j] / d;
+      }
+    M[k * R + k] = -1.0 / d;
+    swept[k] = 1;
+    ++rank;
+  }
+  for (int i = 0; i < R; ++i)
+    for (int j = 0; j < R; ++j) W[i * R + j] = (swept[i] && swept[j]) ? -M[i * R + j] : 0.0;
+  free(M); free(rk); free(swept);
+  return rank;
+}
+
+/* The sampled least-squares step of eq:lsq_krp: the sampled normal equations
+ * A Gamma = M (Gamma, M of eq:gradient1/2, scaled alike) solved as A = M Gamma^+. */
+int orc_update_als(int64_t I, int R, double* A, const double* M, const double* Gam) {
+  double* W = (double*)malloc(sizeof(double) * (size_t)(R * R));
+  if (!W) return ORC_ENOMEM;
+  if (orc_sym_pinv(R, Gam, W) < 0) {
+    free(W);
+    return ORC_ENOMEM;
+  }
+  for (int64_t i = 0; i < I; ++i)
+    for (int r = 0; r < R; ++r) {
+      double s = 0.0;
+      for (int c = 0; c < R; ++c) s += M[i * R + c] * W[c * R + r];
+      A[i * R + r] = s;
+    }
+  free(W);
+  return ORC_OK;
+}
+
 /* eq:proposed (4.3): A <- A - alpha G */
 void orc_update_fixed(int64_t I, int R, double* A, const double* G, double alpha) {
   for (int64_t t = 0; t < I * R; ++t) A[t] = A[t] - alpha * G[t];
@@ -584,7 +648,9 @@ int orc_run(int N, const int64_t* dims, int R, const double* X, double* const* f
   double* w = (double*)malloc(sizeof(double) * (size_t)Bmax);
   double* pj = (double*)malloc(sizeof(double) * (size_t)Bmax);
   double* G = (double*)malloc(sizeof(double) * (size_t)(Imax * R));
-  int st = (!idx || !w || !pj || !G) ? ORC_ENOMEM : ORC_OK;
+  double* Gam = (double*)malloc(sizeof(double) * (size_t)(R * R));
+  double* Mm = (double*)malloc(sizeof(double) * (size_t)(Imax * R));
+  int st = (!idx || !w || !pj || !G || !Gam || !Mm) ? ORC_ENOMEM : ORC_OK;
   for (int k = 0; k < N && !st; ++k) st = orc_build_table(strategy, dims[k], R, factors[k], NULL, q[k], &T[k]);
   for (int64_t it = 0; it < iters && !st; ++it) {
     uint64_t r = r0 + (uint64_t)it;
@@ -593,15 +659,18 @@ int orc_run(int N, const int64_t* dims, int R, const double* X, double* const* f
     int64_t Beff = 0;
     st = orc_sample(N, dims, n, strategy, B, window, (const uint64_t* const*)q, T, seed, r, idx, w, pj, &Beff);
     if (st) break;
-    st = orc_gradient(N, dims, R, X, (const double* const*)factors, n, strategy, B, Beff, idx, pj, G, NULL, NULL);
+    st = orc_gradient(N, dims, R, X, (const double* const*)factors, n, strategy, B, Beff, idx, pj, G, Gam, Mm);
     if (st) break;
     if (rule == ORC_STEP_ADAPTIVE)
       orc_update_adaptive(dims[n], R, factors[n], S[n], G, eta, bpar, eps);
+    else if (rule == ORC_STEP_ALS)
+      st = orc_update_als(dims[n], R, factors[n], Mm, Gam);
     else
       orc_update_fixed(dims[n], R, factors[n], G, alpha ? alpha[it] : alpha0);
+    if (st) break;
     st = orc_build_table(strategy, dims[n], R, factors[n], NULL, q[n], &T[n]);
   }
   for (int k = 0; k < N; ++k) free(q[k]);
-  free(idx); free(w); free(pj); free(G);
+  free(idx); free(w); free(pj); free(G); free(Gam); free(Mm);
   return st;
 }

@@ -552,3 +552,57 @@ def test_gradient_from_fibers_matches_oracle(orc, strategy):
         G_o, Gam_o, M_o = orc.gradient(X, dims, fs, n, orc.STRATEGIES[strategy], B, idx, pj)
         for a, b in ((G, G_o), (Gam, Gam_o), (M, M_o)):
             assert np.allclose(a, b, rtol=1e-12, atol=1e-12 * np.abs(b).max())
+
+
+# ---------------------------------------------------------------------------------------- sampled ALS step
+def test_sym_pinv_closed_forms(orc):
+    """Gamma^+ by the natural-order sweep: the inverse of an SPD matrix; on a rank-deficient Gram the
+    Moore-Penrose conditions on the swept set (G W G = G, W G W = W) and the rank; zero -> zero."""
+    rng = np.random.default_rng(21)
+    Z = rng.standard_normal((40, 6))
+    G = Z.T @ Z
+    W, rk = orc.sym_pinv(G)
+    assert rk == 6
+    np.testing.assert_allclose(W, np.linalg.inv(G), rtol=1e-10, atol=1e-12 * np.abs(np.linalg.inv(G)).max())
+    Z[:, 4] = 2.0 * Z[:, 1] - Z[:, 0]  # exactly dependent column (in exact arithmetic)
+    G = Z.T @ Z
+    W, rk = orc.sym_pinv(G)
+    assert rk == 5
+    np.testing.assert_allclose(G @ W @ G, G, rtol=0, atol=1e-9 * np.abs(G).max())
+    np.testing.assert_allclose(W @ G @ W, W, rtol=0, atol=1e-9 * np.abs(W).max())
+    W0, rk0 = orc.sym_pinv(np.zeros((3, 3)))
+    assert rk0 == 0 and not W0.any()
+
+
+@pytest.mark.parametrize("n", [0, 1, 2])
+def test_als_step_single_window_is_exact_als(orc, n):
+    """one window per mode = every fiber once: the sampled normal equations are the exact ones, so
+    A = M Gamma^+ equals the ALS minimiser of eq:lsq_krp computed by lstsq."""
+    dims = (4, 3, 5)
+    fs = rand_factors(dims, 2, seed=31)
+    X = rand_tensor(dims, seed=32)
+    tabs = tables_for(orc, "block_euclidean", fs)
+    win = [d for k, d in enumerate(dims) if k != n]
+    B = int(np.prod(win))
+    idx, w, pj = orc.sample(dims, n, orc.BLOCK_EUCLIDEAN, B, tabs, seed=0, it=0, window=win)
+    _, Gam, M = orc.gradient(X, dims, fs, n, orc.BLOCK_EUCLIDEAN, B, idx, pj)
+    np.testing.assert_allclose(orc.update_als(M, Gam), defs.als_solution(X, dims, fs, n), rtol=1e-10, atol=1e-12)
+
+
+def test_run_wires_the_als_rule(orc):
+    """oracle.run with STEP_ALS applies sample -> eq:gradient1 -> A = M Gamma^+ -> table rebuild."""
+    dims = (6, 5, 4)
+    fs = rand_factors(dims, 3, seed=41)
+    X = rand_tensor(dims, seed=42)
+    out, _, _ = orc.run(X, fs, orc.LEVERAGE, orc.STEP_ALS, 12, 2, seed=7)
+    tabs = tables_for(orc, "leverage", fs)
+    f = [A.copy() for A in fs]
+    for it in range(2):
+        n = it % 3
+        idx, w, pj = orc.sample(dims, n, orc.LEVERAGE, 12, tabs, seed=7, it=it)
+        _, Gam, M = orc.gradient(X, dims, f, n, orc.LEVERAGE, 12, idx, pj)
+        f[n] = orc.update_als(M, Gam)
+        p_, q_, T_ = orc.build_table(orc.LEVERAGE, f[n])
+        tabs[n] = (q_, T_)
+    for k in range(3):
+        np.testing.assert_allclose(out[k], f[k], rtol=0, atol=0)
