@@ -318,7 +318,7 @@ def cpu_baseline(cfg, args, budget_s=12.0):
     A0 = synth.init_factors(cfg, X)
     X64 = X.astype(np.float64)
     st = oracle.STRATEGIES[args.sampler]
-    rule = oracle.STEP_ADAPTIVE if cfg.rule == "adaptive" else oracle.STEP_FIXED
+    rule = {"adaptive": oracle.STEP_ADAPTIVE, "als": oracle.STEP_ALS}.get(cfg.rule, oracle.STEP_FIXED)
     iters, t_used = 0, 0.0
     fs = A0
     while t_used < budget_s and iters < 3 * 200:
@@ -344,7 +344,7 @@ def run_reference(args, cfg):
     A0 = synth.init_factors(cfg, X)
     X64 = X.astype(np.float64)
     st = oracle.STRATEGIES[args.sampler]
-    rule = oracle.STEP_ADAPTIVE if cfg.rule == "adaptive" else oracle.STEP_FIXED
+    rule = {"adaptive": oracle.STEP_ADAPTIVE, "als": oracle.STEP_ALS}.get(cfg.rule, oracle.STEP_FIXED)
     fs = A0
     r = 0
     for _ in range(args.warmup):
@@ -386,9 +386,15 @@ def main():
                     help="auto: persistent single-cluster kernel when the problem fits one cluster; wide: the "
                          "gather (tcgen05) + table/sampling kernel pair")
     ap.add_argument("--no-tc", action="store_true", help="FFMA gather mainloop instead of tcgen05")
+    ap.add_argument("--rule", default="config", choices=["config", "fixed", "adaptive", "als"],
+                    help="update rule (config: the workload's; als: the sampled least-squares step, SURVEY 8f.3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = synth.CONFIGS[args.workload]
+    if args.rule != "config":
+        import dataclasses
+
+        cfg = dataclasses.replace(cfg, rule=args.rule)
     if args.impl == "reference":
         res = run_reference(args, cfg)
         if res is not None:

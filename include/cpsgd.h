@@ -60,7 +60,11 @@ typedef enum {
 
 /* fixed step = eq:proposed (BrawsCPD Alg. 6); adaptive = eq:etaada/eq:Aada
  * (AdawsCPD Alg. 7). */
-typedef enum { CP_STEP_FIXED = 0, CP_STEP_ADAPTIVE = 1 } cp_step_rule;
+/* CP_STEP_ALS: the sampled least-squares step of eq:lsq_krp on the same batch,
+ * A^(n) <- M Gamma^+ (M, Gamma of eq:gradient1/2; Gamma^+ by the natural-order symmetric sweep on its
+ * numerically full-rank pivot set, tol = R eps max_i Gamma_ii, reading R25).  Single
+ * GPU, fused or wide path only (CP_EINVAL otherwise). */
+typedef enum { CP_STEP_FIXED = 0, CP_STEP_ADAPTIVE = 1, CP_STEP_ALS = 2 } cp_step_rule;
 
 /* mode order of a sweep: cyclic 0..N-1, or n drawn uniformly per iteration */
 typedef enum { CP_ORDER_CYCLIC = 0, CP_ORDER_RANDOM = 1 } cp_mode_order;

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcpsgd.so")
 
 SAMPLERS = {"uniform": 0, "leverage": 1, "euclidean": 2, "block_leverage": 3, "block_euclidean": 4}
-RULES = {"fixed": 0, "adaptive": 1}
+RULES = {"fixed": 0, "adaptive": 1, "als": 2}
 ORDERS = {"cyclic": 0, "random": 1}
 FLAG_MODE_MAJOR, FLAG_NO_GRAPH, FLAG_EXTERNAL_COMM, FLAG_NO_FUSED, FLAG_NO_WIDE, FLAG_NO_TC = \
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20

@@ -1092,7 +1092,8 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
   if (cfg->dtype != CP_F32 && cfg->dtype != CP_F64) return init_fail(h, h->fail(CP_EINVAL, "bad dtype"));
   if (cfg->batch < 1) return init_fail(h, h->fail(CP_EINVAL, "batch B=%lld < 1", (long long)cfg->batch));
   if (cfg->sampler < 0 || cfg->sampler > 4) return init_fail(h, h->fail(CP_EINVAL, "bad sampler"));
-  if (cfg->rule != CP_STEP_FIXED && cfg->rule != CP_STEP_ADAPTIVE) return init_fail(h, h->fail(CP_EINVAL, "bad rule"));
+  if (cfg->rule != CP_STEP_FIXED && cfg->rule != CP_STEP_ADAPTIVE && cfg->rule != CP_STEP_ALS)
+    return init_fail(h, h->fail(CP_EINVAL, "bad rule"));
   if (!(cfg->alpha >= 0.0)) return init_fail(h, h->fail(CP_EINVAL, "alpha < 0"));
   if (cfg->rule == CP_STEP_ADAPTIVE && !(cfg->eta > 0.0)) return init_fail(h, h->fail(CP_EINVAL, "eta <= 0"));
   if (!(cfg->b >= 0.0) || !(cfg->eps >= 0.0)) return init_fail(h, h->fail(CP_EINVAL, "b or eps < 0"));
@@ -1344,6 +1345,14 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
     } else {
       h->use_tc = false;
     }
+  }
+  if (h->rule == CP_STEP_ALS) {  // the ALS step is implemented by the fused and wide kernels only
+    bool ok = h->fused_cu > 0;
+    if (!ok) {
+      ok = h->world_size == 1;
+      for (int n = 0; n < h->N; ++n) ok = ok && wide_mode(h, n);
+    }
+    if (!ok) return init_fail(h, h->fail(CP_EINVAL, "rule=als needs one GPU and the fused or wide path"));
   }
   // ---- optional mode-major copies (n >= 1; mode 0 fibers are already contiguous) ----
   if (h->flags & CP_FLAG_MODE_MAJOR) {
@@ -1814,7 +1823,7 @@ cp_status cp_sgd_get_grad(cp_sgd_t h, void* G_host, int32_t* mode_host, void* Ga
 cp_status cp_sgd_get_accum(cp_sgd_t h, int32_t mode, void* S_host) {
   cp_status st = check_mode(h, mode);
   if (st) return st;
-  if (!h->S[mode]) return h->fail(CP_ESTATE, "fixed rule has no accumulator");
+  if (!h->S[mode]) return h->fail(CP_ESTATE, "only the adaptive rule has an accumulator");
   st = cp_sgd_sync(h);
   if (st) return st;
   CUDA_TRY(h, cudaMemcpy(S_host, h->S[mode], h->esz * h->dims[mode] * h->R, cudaMemcpyDeviceToHost));

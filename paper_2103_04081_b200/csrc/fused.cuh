@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
   __shared__ const uint64_t* s_cp[kMaxOrder];
   __shared__ uint64_t s_T[kMaxOrder];
   __shared__ unsigned long long s_off[17];
+  __shared__ double s_tol_als;
   __shared__ int32_t s_start[kMaxOrder], s_len[kMaxOrder];
   __shared__ double s_wblk;
   __shared__ int64_t s_beff;
@@ -645,7 +646,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     for (int e = tid; e < nr * R; e += kFThreads) {
       const int il = e / R, c = e % R;
       cp_async_small<sizeof(T)>(Aold + il * RS + c, p.factors[n] + (r_beg + il) * R + c, sizeof(T));
-      if (p.rule != 0) cp_async_small<sizeof(T)>(Sold + il * RS + c, p.S[n] + (r_beg + il) * R + c, sizeof(T));
+      if (p.rule == 1) cp_async_small<sizeof(T)>(Sold + il * RS + c, p.S[n] + (r_beg + il) * R + c, sizeof(T));
     }
     cp_async_commit();
     const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
@@ -681,6 +682,20 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     __syncthreads();
     if (q == 0 && s == p.nsteps - 1)
       for (int e = tid; e < R * R; e += kFThreads) p.Gam_out[e] = Gam[e];
+    if (p.rule == 2) {
+      // sampled least squares (eq:lsq_krp; R25): W = Gamma^+ in fp64 by the
+      // natural-order sweep (tol R eps max diag), every CTA; the rows follow as A = M W below
+      for (int e = tid; e < R * R; e += kFThreads) Gm[(e / R) * RS + e % R] = (double)Gam[e];
+      __syncthreads();
+      if (wid == 0) {
+        double d0 = 0.0;
+        for (int j = lane; j < R; j += 32) d0 = fmax(d0, Gm[j * RS + j]);
+        for (int o = 16; o > 0; o >>= 1) d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
+        if (lane == 0) s_tol_als = (double)R * 2.220446049250313e-16 * d0;
+      }
+      __syncthreads();
+      grp_sweep_dispatch<32>(Gm, R, s_tol_als, rowbuf, swept);
+    }
     for (int e = tid; e < nr * R; e += kFThreads) {
       const int il = e / R, rr = e % R;
       const int64_t i = r_beg + il;
@@ -692,6 +707,10 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
       p.Gout[gi] = g;
       const T a = Aold[il * RS + rr];
       T an = a;
+      if (p.rule == 2) {
+        Sold[il * RS + rr] = m;  // the M rows (the accumulator buffer is unused by this rule)
+        continue;
+      }
       if (p.rule == 0) {
         an = a - (T)alpha * g;
       } else {
@@ -706,6 +725,16 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
       }
       p.factors[n][gi] = an;
       Anew[il * RS + rr] = an;
+    }
+    if (p.rule == 2) {
+      __syncthreads();
+      for (int e = tid; e < nr * R; e += kFThreads) {
+        const int il = e / R, rr = e % R;
+        double an = 0.0;
+        for (int c = 0; c < R; ++c) an = fma((double)Sold[il * RS + c], Gm[c * RS + rr], an);
+        p.factors[n][(r_beg + il) * R + rr] = (T)an;
+        Anew[il * RS + rr] = (T)an;
+      }
     }
     __syncthreads();
     F_MARK(3);

@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
     for (int e = tid; e < nr * R; e += kWThreads) {
       const int il = e / R, c = e % R;
       cp_async_small<sizeof(T)>(sA + il * RS + c, p.A + (r0 + il) * R + c, sizeof(T));
-      if (p.rule != 0) cp_async_small<sizeof(T)>(sS + il * RS + c, p.S + (r0 + il) * R + c, sizeof(T));
+      if (p.rule == 1) cp_async_small<sizeof(T)>(sS + il * RS + c, p.S + (r0 + il) * R + c, sizeof(T));
     }
     for (int e = tid; e < R * R; e += kWThreads) cp_async_small<sizeof(T)>(sG + e, p.Gam + e, sizeof(T));
     cp_async_commit();
@@ -387,6 +387,33 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
     }
     cp_async_wait<0>();
     __syncthreads();
+    if (p.rule == 2) {
+      // sampled least squares (eq:lsq_krp; R25): W = Gamma^+ in fp64 by the
+      // natural-order sweep (tol R eps max diag) in every CTA, then this CTA's rows A = M W (into
+      // sS, unused by this rule) before M is overwritten by G below
+      double* Gm = reinterpret_cast<double*>(uw_sm + uw_step_bytes(R, sizeof(T)));
+      double* rowbuf = Gm + R * RS;
+      int* swept = reinterpret_cast<int*>(rowbuf + kSweepBuf + kMaxRank);
+      __shared__ double s_tol_als;
+      for (int e = tid; e < R * R; e += kWThreads) Gm[(e / R) * RS + e % R] = (double)sG[e];
+      __syncthreads();
+      if (tid < 32) {
+        double d0 = 0.0;
+        for (int j = tid; j < R; j += 32) d0 = fmax(d0, Gm[j * RS + j]);
+  #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
+        if (tid == 0) s_tol_als = (double)R * 2.220446049250313e-16 * d0;
+      }
+      __syncthreads();
+      grp_sweep_dispatch(Gm, R, s_tol_als, rowbuf, swept);
+      for (int e = tid; e < nr * R; e += kWThreads) {
+        const int il = e / R, r = e % R;
+        double an = 0.0;
+        for (int c = 0; c < R; ++c) an = fma((double)sM[il * RS + c], Gm[c * RS + r], an);
+        sS[il * RS + r] = (T)an;
+      }
+      __syncthreads();
+    }
     // G = A Gamma - M (each task owns its 4 x 4 block of M -> G in place)
     for (int t = tid; t < ((nr + 3) >> 2) * nb4; t += kWThreads) {
       const int a0 = 4 * (t / nb4), q0 = 4 * (t % nb4);
@@ -422,7 +449,9 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
       p.Gout[gi] = g;
       const T a = sA[il * RS + r];
       T an = a;
-      if (p.rule == 0) {
+      if (p.rule == 2) {
+        an = sS[il * RS + r];
+      } else if (p.rule == 0) {
         an = a - (T)alpha * g;
       } else {
         const T sv = sS[il * RS + r] + g * g;

@@ -164,6 +164,63 @@ def test_one_step_per_mode(strategy, case, path):
         h.close()
 
 
+# ------------------------------------------------------------------------------------------ sampled ALS step (8f.3)
+ALS_CASES = [((60, 60, 60), 5, 64, "f64"), ((40, 30, 20), 12, 300, "f64"), ((130, 70, 45), 20, 512, "f32")]
+
+
+@pytest.mark.parametrize("strategy", ["uniform", "leverage", "euclidean", "block_leverage"])
+@pytest.mark.parametrize("case", ALS_CASES, ids=lambda c: "x".join(map(str, c[0])) + f"_R{c[1]}_B{c[2]}_{c[3]}")
+@pytest.mark.parametrize("path", ["fused", "split_mm", "split_ffma"])
+def test_als_step_per_mode(strategy, case, path):
+    """rule=als: one GPU step of mode n equals A = M Gamma^+ of the oracle from the same state; the
+    tolerance is the dtype's times the condition number of Gamma, the
+    factor by which a solve can amplify the input perturbation."""
+    dims, R, B, dt = case
+    cfg = synth.small(dims, R, dtype=dt, batch=B, rule="fixed", row_sigma=1.0, noise=1e-2, seed=13)
+    X, A0 = make_problem(cfg)
+    for n in range(len(dims)):
+        Xd, Ad = to_dev(X, A0)
+        h = handle(cfg, Xd, Ad, strategy, seed=55, rule="als", **PATHS[path])
+        it = 2 + n
+        h.iter = it
+        idx_o, w_o, G_o, Gam_o, M_o, tabs = oracle_step(X, dims, A0, n, strategy, B, 55, it)
+        h.step(n)
+        A_o = oracle.update_als(M_o, Gam_o)
+        kappa = np.linalg.cond(Gam_o)
+        A_g = Ad[n].cpu().numpy()
+        assert rel_err(A_g, A_o, np.linalg.norm(A_o)) <= TOL[dt] * max(1.0, kappa)
+        for k in range(len(dims)):
+            if k != n:
+                assert np.array_equal(Ad[k].cpu().numpy(), A0[k])
+        h.close()
+
+
+@pytest.mark.parametrize("path", ["fused", "split_mm"])
+def test_als_trajectory(path):
+    """rule=als, C1 shape (60^3 fp64, R5, B64, leverage), 4 cyclic sweeps free-running on both
+    sides: final factors within 1e-8 relative."""
+    cfg = synth.small((60, 60, 60), 5, dtype="f64", batch=64, rule="fixed", row_sigma=1.0, noise=1e-2, seed=0)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "leverage", seed=3, rule="als", **PATHS[path])
+    h.sweep(4)
+    h.sync()
+    fs, _, _ = oracle.run(X, A0, oracle.LEVERAGE, oracle.STEP_ALS, cfg.batch, 12, seed=3)
+    for k in range(3):
+        assert rel_err(Ad[k].cpu().numpy(), fs[k], np.linalg.norm(fs[k])) <= 1e-8
+    h.close()
+
+
+def test_als_needs_fused_or_wide_path():
+    from paper_2103_04081_b200 import CPError
+
+    cfg = synth.small((20, 18, 16), 3, dtype="f64", batch=32, rule="fixed", seed=2)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    with pytest.raises(CPError, match="EINVAL"):
+        handle(cfg, Xd, Ad, "leverage", rule="als", fused=False, wide=False)
+
+
 # ------------------------------------------------------------------------------------------ trajectories
 @pytest.mark.parametrize("strategy", S)
 @pytest.mark.parametrize("path", ["fused", "split_mm"])
