@@ -215,3 +215,27 @@ def init_factors_torch(cfg: Config, xnorm: float, device="cuda", seed: Optional[
     scale = (xnorm / math.sqrt(max(H.sum().item(), 1e-300))) ** (1.0 / cfg.order)
     tdt = torch.float64 if cfg.dtype == "f64" else torch.float32
     return [(A * scale).to(tdt).contiguous() for A in A0]
+
+
+def spread_magnitude(I: int, J: int, R: int, spread: int, magnitude: float, noise: float = 0.05,
+                     seed: int = 0):
+    """The paper's I x I x J experiment tensor with SPEC.md's
+    stand-in for the cited spread / magnitude rule: two I x R and one J x R factors with N(0,1)
+    entries, the first three columns zeroed, then in each zeroed column `spread` distinct rows
+    (uniform) set to magnitude * (random sign); X = [[A]] + noise ||X0|| / ||E|| E.
+    Returns (X flat first-index-fastest fp64, clean [[A]], factors)."""
+    if spread > min(I, J) or R < 3:
+        raise ValueError("spread exceeds a row count or R < 3")
+    rng = np.random.default_rng([seed, 11])
+    fs = []
+    for n_rows in (I, I, J):
+        A = rng.standard_normal((n_rows, R))
+        A[:, :3] = 0.0
+        for c in range(3):
+            rows = rng.choice(n_rows, size=spread, replace=False)
+            A[rows, c] = magnitude * rng.choice([-1.0, 1.0], size=spread)
+        fs.append(A)
+    X0 = cp_tensor(fs)
+    E = rng.standard_normal(X0.shape[0])
+    X = X0 + noise * (np.linalg.norm(X0) / np.linalg.norm(E)) * E if noise > 0.0 else X0.copy()
+    return X, X0, fs

@@ -606,3 +606,22 @@ def test_run_wires_the_als_rule(orc):
         tabs[n] = (q_, T_)
     for k in range(3):
         np.testing.assert_allclose(out[k], f[k], rtol=0, atol=0)
+
+
+# ---------------------------------------------------------------------------------------- 8(f).1 generator
+def test_spread_magnitude_generator():
+    """synth.spread_magnitude (PAPER.md:683-690 with SPEC.md's stand-in rule): exact relative noise
+    level, the first three columns zero except `spread` rows of +-magnitude, noiseless = [[A]]."""
+    import synth
+
+    X, X0, fs = synth.spread_magnitude(30, 12, 6, 5, 24.0, 0.05, seed=3)
+    assert abs(np.linalg.norm(X - X0) / np.linalg.norm(X0) - 0.05) < 1e-12
+    for A in fs:
+        for c in range(3):
+            nz = np.flatnonzero(A[:, c])
+            assert len(nz) == 5 and np.all(np.abs(A[nz, c]) == 24.0)
+    Xc, X0c, fc = synth.spread_magnitude(8, 7, 4, 0, 1.0, 0.0, seed=1)
+    assert np.array_equal(Xc, X0c) and all(not A[:, :3].any() for A in fc)
+    np.testing.assert_allclose(X0c, synth.cp_tensor(fc), rtol=0, atol=0)
+    with pytest.raises(ValueError):
+        synth.spread_magnitude(5, 4, 3, 6, 1.0)
