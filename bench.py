@@ -117,6 +117,53 @@ def make_inputs(cfg, device, seed_offset=0, slab=None):
 
 
 # ----------------------------------------------------------------------------------------------
+def run_chains(args, cfg):
+    """--chains K: K independent chains of the workload (same tensor, own factors
+    and seeds) in ONE k_sweep_fused_multi launch per call, one cluster each; value = fibers/s summed
+    over the chains.  Not the headline (that is one chain); a measure of the GPU's capacity."""
+    import torch
+
+    from paper_2103_04081_b200 import CPSGD
+
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(0)
+    Xd, Ad0, _, _ = make_inputs(cfg, dev)
+    hs, keep = [], []
+    for c in range(args.chains):
+        Ad = [a.clone() for a in Ad0]
+        h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=args.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta,
+                  seed=cfg.seed + 1000 * c, mode_major=not args.native_layout)
+        hs.append(h)
+        keep.append(Ad)
+    CPSGD.sweep_multi(hs, args.warmup)
+    for h in hs:
+        h.sync()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        ev0.record()
+        CPSGD.sweep_multi(hs, args.steps)
+        for h in hs:
+            h.sync()
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    N = cfg.order
+    fibers = args.chains * N * cfg.batch * args.steps
+    for h in hs:
+        h.close()
+    return {"metric": METRIC, "value": round(fibers / (ms / 1e3), 1), "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if cfg.dtype == "f64" else "f32", "data": "synthetic (seeded; synth/ recipe)",
+            "config": {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.dims))} {cfg.dtype}, R={cfg.rank}, "
+                                   f"B={cfg.batch}, {cfg.rule} step, {args.sampler} sampling, cyclic sweeps",
+                       "chains": args.chains, "step": f"one cyclic sweep of every chain ({N} SGD iterations x B "
+                       f"fibers each), all chains in one k_sweep_fused_multi launch (one 16-CTA cluster each)",
+                       "timing": "host-synchronised CUDA events around the call (all chains' streams)"},
+            "clocks": clk.summary(), "gpu_launches": 1, "e2e": None}
+
+
 def run_ours(args, cfg):
     import torch
 
@@ -386,6 +433,8 @@ def main():
                     help="auto: persistent single-cluster kernel when the problem fits one cluster; wide: the "
                          "gather (tcgen05) + table/sampling kernel pair")
     ap.add_argument("--no-tc", action="store_true", help="FFMA gather mainloop instead of tcgen05")
+    ap.add_argument("--chains", type=int, default=1,
+                    help="K > 1: K independent chains in one multi-chain launch (fused workloads; SURVEY 8f.2)")
     ap.add_argument("--rule", default="config", choices=["config", "fixed", "adaptive", "als"],
                     help="update rule (config: the workload's; als: the sampled least-squares step, SURVEY 8f.3)")
     args = ap.parse_args()
@@ -404,6 +453,9 @@ def main():
 
     ws, rank, _ = dist_env()
     __graft_entry__.build()  # idempotent (mtime check, atomic replace)
+    if args.chains > 1:
+        print(json.dumps(run_chains(args, cfg)), flush=True)
+        return
     if ws > 1:
         import torch.distributed  # noqa: F401
     res = run_ours(args, cfg)

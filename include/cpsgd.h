@@ -146,6 +146,14 @@ cp_status cp_sgd_step(cp_sgd_t h, int32_t mode, double alpha);
  * sweeps with a constant step are replayed from a captured CUDA graph.  Asynchronous. */
 cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double* alpha_per_iter);
 
+/* Many independent chains in ONE launch: nsweeps cyclic sweeps (constant step:
+ * cfg.alpha / the adaptive or ALS rule) of each of the nh handles, one thread-block cluster per
+ * chain.  Every handle must be on the fused single-GPU path with the same geometry (dtype, dims, R,
+ * fused plan); samplers, rules, seeds, tensors and factors may differ.  Launched on hs[0]'s stream
+ * after the other handles' streams are synchronised; their later work is ordered after it.
+ * Results equal nh separate cp_sgd_sweep calls bit for bit.  Asynchronous.  CP_EINVAL otherwise. */
+cp_status cp_sgd_sweep_multi(cp_sgd_t* hs, int32_t nh, int32_t nsweeps);
+
 /* fit = 1 - ||X - [[A]]||_F / ||X||_F (PAPER.md:118-127 objective, R14), fp64 accumulation,
  * summed over ranks when sharded.  Synchronises.  CP_EDEGENERATE when ||X|| = 0. */
 cp_status cp_fit(cp_sgd_t h, double* fit_host);

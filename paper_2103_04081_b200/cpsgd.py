@@ -28,7 +28,7 @@ STATUS = {0: "CP_OK", -1: "CP_EINVAL", -2: "CP_ERANGE", -3: "CP_EDEGENERATE", -4
           -6: "CP_ENCCL", -7: "CP_ESTATE", -8: "CP_ENONFINITE"}
 
 EXPORTS = ["cp_sgd_init", "cp_sgd_destroy", "cp_sgd_last_error", "cp_sgd_sample", "cp_sgd_step", "cp_sgd_sweep",
-           "cp_fit", "cp_sgd_sync", "cp_sgd_steps_host", "cp_sgd_step_phase", "cp_sgd_exchange_info",
+           "cp_fit", "cp_sgd_sync", "cp_sgd_steps_host", "cp_sgd_sweep_multi", "cp_sgd_step_phase", "cp_sgd_exchange_info",
            "cp_sgd_get_table", "cp_sgd_get_grad", "cp_sgd_get_accum", "cp_sgd_get_iter", "cp_sgd_set_iter",
            "cp_sgd_refresh_tables", "cp_sgd_get_launches", "cp_sgd_profile", "cp_sgd_profile_read",
            "cp_sgd_version", "cp_sgd_batch_max", "cp_sgd_debug_timers", "cp_sgd_exchange_copy"]
@@ -74,6 +74,7 @@ def load_library(path: str = LIB_PATH):
     L.cp_fit.argtypes = [P, C.POINTER(C.c_double)]
     L.cp_sgd_sync.argtypes = [P]
     L.cp_sgd_steps_host.argtypes = [P, i32, i32, dbl, P]
+    L.cp_sgd_sweep_multi.argtypes = [P, i32, i32]
     L.cp_sgd_step_phase.argtypes = [P, i32, i32, dbl]
     L.cp_sgd_exchange_info.argtypes = [P, i32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                        C.POINTER(C.c_int64)]
@@ -211,6 +212,14 @@ class CPSGD:
     def exchange_copy(self, mode: int, buf, to_lib: bool):
         """copy the phase-0 exchange buffer (partial M, [R][I_n]) to / from a torch CUDA tensor"""
         self._chk(self._L.cp_sgd_exchange_copy(self._h, mode, C.c_void_p(buf.data_ptr()), 1 if to_lib else 0))
+
+    @staticmethod
+    def sweep_multi(handles, nsweeps: int = 1):
+        """nsweeps cyclic sweeps of every handle in ONE launch, one cluster per chain (SURVEY 8(f).2);
+        the handles must share the fused geometry (dtype, dims, R)."""
+        hs = list(handles)
+        arr = (C.c_void_p * len(hs))(*[h._h for h in hs])
+        hs[0]._chk(hs[0]._L.cp_sgd_sweep_multi(arr, len(hs), int(nsweeps)))
 
     def sweep(self, nsweeps: int = 1, order: str = "cyclic", alphas=None):
         arr = None

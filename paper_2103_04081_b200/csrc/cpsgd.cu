@@ -106,6 +106,7 @@ size_t allow_max_dyn_smem(F* func) {
 struct cp_sgd_s {
   // configuration
   int N = 0, R = 0, dtype = 0, sampler = 0, rule = 0;
+  int device = 0;                // CUDA device of the handle (cp_sgd_sweep_multi checks it)
   int64_t dims[kMaxOrder] = {}, ldims[kMaxOrder] = {}, lstride[kMaxOrder] = {};
   int64_t lo_last = 0, hi_last = 0;
   int64_t B = 0;
@@ -122,6 +123,8 @@ struct cp_sgd_s {
   void* factors[kMaxOrder] = {};
   void* fstage[kMaxOrder] = {};    // cp_sgd_steps_host staging of the host factors (fused / wide path)
   int* take_chg = nullptr;         // cp_sgd_steps_host (wide): per-mode "host factor differs" flags
+  void* multi_params = nullptr;    // cp_sgd_sweep_multi: the chains' kernel parameters (device)
+  size_t multi_cap = 0;
   size_t esz = 4;
   // layout
   void* Xmm[kMaxOrder] = {};
@@ -824,11 +827,9 @@ cp_status launch_prefetch(cp_sgd_s* h, int n) {
 }
 
 // ---- persistent single-cluster sweep kernel (fused.cuh) ----------------------------------------
-template <typename T, int ROWS>
-cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev,
-                         int rebuild) {
-  ProfScope ps(h, kKFused);
-  FusedParams<T> p;
+template <typename T>
+void fill_fused_params(cp_sgd_s* h, FusedParams<T>& p, int nsteps, int first_mode, int order, double alpha,
+                       const double* alpha_dev, int rebuild) {
   memset(&p, 0, sizeof p);
   p.N = h->N;
   p.R = h->R;
@@ -878,6 +879,14 @@ cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, dou
   for (int k = 0; k < h->N; ++k) imax = std::max(imax, h->dims[k]);
   p.Imax = imax;
   p.dbg = h->dbg;
+}
+
+template <typename T, int ROWS>
+cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev,
+                         int rebuild) {
+  ProfScope ps(h, kKFused);
+  FusedParams<T> p;
+  fill_fused_params<T>(h, p, nsteps, first_mode, order, alpha, alpha_dev, rebuild);
   static bool attr_set = false;
   if (!attr_set) {
     allow_max_dyn_smem(k_sweep_fused<T, ROWS>);
@@ -919,6 +928,63 @@ cp_status launch_fused(cp_sgd_s* h, int nsteps, int first_mode, int order, doubl
                                     : launch_fused_r<float>(h, nsteps, first_mode, order, alpha, alpha_dev, rebuild);
   h->pref_mode = -1;
   return st;
+}
+
+// many independent chains in one launch: cluster c runs nsteps cyclic iterations of
+// handle hs[c] (same geometry for all: dtype, dims, R, fused plan; samplers, rules, seeds may differ)
+template <typename T, int ROWS>
+cp_status launch_fused_multi_t(cp_sgd_s* const* hs, int nh, int nsteps) {
+  cp_sgd_s* h0 = hs[0];
+  ProfScope ps(h0, kKFused);
+  std::vector<FusedParams<T>> prm(nh);
+  for (int i = 0; i < nh; ++i) fill_fused_params<T>(hs[i], prm[i], nsteps, 0, CP_ORDER_CYCLIC, hs[i]->alpha, nullptr, 0);
+  const size_t bytes = sizeof(FusedParams<T>) * (size_t)nh;
+  if (h0->multi_cap < bytes) {
+    cudaFree(h0->multi_params);
+    h0->multi_params = nullptr;
+    h0->multi_cap = 0;
+    CUDA_TRY(h0, cudaMalloc(&h0->multi_params, bytes));
+    h0->multi_cap = bytes;
+  }
+  for (int i = 1; i < nh; ++i) CUDA_TRY(h0, cudaStreamSynchronize(hs[i]->stream));  // their earlier work first
+  CUDA_TRY(h0, cudaMemcpyAsync(h0->multi_params, prm.data(), bytes, cudaMemcpyHostToDevice, h0->stream));
+  static bool attr_set = false;
+  if (!attr_set) {
+    allow_max_dyn_smem(k_sweep_fused_multi<T, ROWS>);
+    cudaFuncSetAttribute(k_sweep_fused_multi<T, ROWS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  size_t smem = 0;  // each cluster lays out its own shared memory (the CDF area depends on the sampler)
+  for (int i = 0; i < nh; ++i) smem = std::max(smem, (size_t)hs[i]->fused_smem);
+  lc.gridDim = dim3((unsigned)(nh * h0->fused_cu), 1, 1);
+  lc.blockDim = dim3(kFThreads, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = h0->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = h0->fused_cu;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_sweep_fused_multi<T, ROWS>, (const FusedParams<T>*)h0->multi_params,
+                                     h0->fused_cu);
+  h0->launches++;
+  if (e != cudaSuccess) return h0->fail(CP_ECUDA, "k_sweep_fused_multi launch (%d chains): %s", nh, cudaGetErrorString(e));
+  cp_status st = check_launch(h0, "k_sweep_fused_multi");
+  if (st) return st;
+  cudaEvent_t ev;  // the other handles' later work after this launch
+  CUDA_TRY(h0, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CUDA_TRY(h0, cudaEventRecord(ev, h0->stream));
+  for (int i = 1; i < nh; ++i) CUDA_TRY(h0, cudaStreamWaitEvent(hs[i]->stream, ev, 0));
+  cudaEventDestroy(ev);
+  for (int i = 0; i < nh; ++i) {
+    hs[i]->iter_host += nsteps;
+    hs[i]->last_mode = hs[i]->N - 1;
+    hs[i]->pref_mode = -1;
+  }
+  return CP_OK;
 }
 
 // geometry + eligibility of the fused kernel: one GPU, R <= 32, I_n <= 512, fits shared memory
@@ -1105,6 +1171,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
   h->esz = cfg->dtype == CP_F64 ? 8 : 4;
   h->sampler = cfg->sampler;
   h->rule = cfg->rule;
+  cudaGetDevice(&h->device);
   h->B = cfg->batch;
   h->alpha = cfg->alpha;
   h->eta = cfg->eta;
@@ -1445,6 +1512,7 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->zwp);
   for (int k = 0; k < kMaxOrder; ++k) cudaFree(h->fstage[k]);
   cudaFree(h->take_chg);
+  cudaFree(h->multi_params);
   cudaFree(h->zimg);
   cudaFree(h->gam_next);
   cudaFree(h->Mpart);
@@ -1683,6 +1751,31 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
   }
   if (nsweeps > 0) h->last_mode = h->N - 1;
   return CP_OK;
+}
+
+cp_status cp_sgd_sweep_multi(cp_sgd_t* hs, int32_t nh, int32_t nsweeps) {
+  if (!hs || nh < 1 || !hs[0]) return CP_EINVAL;
+  cp_sgd_s* h0 = hs[0];
+  if (nsweeps < 0) return h0->fail(CP_EINVAL, "nsweeps < 0");
+  for (int i = 0; i < nh; ++i) {
+    cp_sgd_s* h = hs[i];
+    if (!h) return h0->fail(CP_EINVAL, "NULL handle %d", i);
+    if (!h->fused_cu || h->world_size != 1)
+      return h0->fail(CP_EINVAL, "handle %d: multi-chain sweeps need the fused single-GPU path", i);
+    bool same = h->dtype == h0->dtype && h->N == h0->N && h->R == h0->R && h->fused_cu == h0->fused_cu &&
+                h->fused_bpc == h0->fused_bpc && h->fused_rpc == h0->fused_rpc && h->device == h0->device;
+    for (int k = 0; same && k < h->N; ++k) same = h->dims[k] == h0->dims[k];
+    if (!same) return h0->fail(CP_EINVAL, "handle %d: geometry differs from handle 0", i);
+    for (int j = 0; j < i; ++j)
+      if (hs[j] == h) return h0->fail(CP_EINVAL, "handle %d repeated", i);
+  }
+  if (nsweeps == 0) return CP_OK;
+  const int64_t nst = (int64_t)nsweeps * h0->N;
+  int64_t imax = 0;
+  for (int k = 0; k < h0->N; ++k) imax = std::max(imax, h0->dims[k]);
+  if (h0->dtype == CP_F64)
+    return imax > kFThreads ? launch_fused_multi_t<double, 2>(hs, nh, (int)nst) : launch_fused_multi_t<double, 1>(hs, nh, (int)nst);
+  return imax > kFThreads ? launch_fused_multi_t<float, 2>(hs, nh, (int)nst) : launch_fused_multi_t<float, 1>(hs, nh, (int)nst);
 }
 
 cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, double alpha,

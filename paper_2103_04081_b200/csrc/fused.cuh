@@ -227,7 +227,7 @@ __device__ __forceinline__ bool bits_equal(T a, T b) {
   } while (0)
 
 template <typename T, int ROWS>
-__global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) {
+__device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const int CU = p.CU;
@@ -760,6 +760,26 @@ __global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) 
     *p.iter = r;
     *p.last_mode = n_done;
   }
+}
+
+// one chain: the whole call in one cluster
+template <typename T, int ROWS>
+__global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused(FusedParams<T> p) {
+  fused_body<T, ROWS>(p);
+}
+
+// many independent chains: cluster c runs the call of chain c with its own
+// parameters (ps[c]: factors, tables, accumulators, seed, ...; one geometry for all)
+template <typename T, int ROWS>
+__global__ void __launch_bounds__(kFThreads, 1) k_sweep_fused_multi(const FusedParams<T>* ps, int cu) {
+  __shared__ __align__(16) FusedParams<T> sp;
+  const FusedParams<T>* src = ps + blockIdx.x / cu;
+  constexpr int W = (int)(sizeof(FusedParams<T>) / sizeof(int));
+  static_assert(sizeof(FusedParams<T>) % sizeof(int) == 0, "param copy");
+  for (int i = threadIdx.x; i < W; i += blockDim.x)
+    reinterpret_cast<int*>(&sp)[i] = reinterpret_cast<const int*>(src)[i];
+  __syncthreads();
+  fused_body<T, ROWS>(sp);
 }
 
 }  // namespace cps

@@ -221,6 +221,50 @@ def test_als_needs_fused_or_wide_path():
         handle(cfg, Xd, Ad, "leverage", rule="als", fused=False, wide=False)
 
 
+# ------------------------------------------------------------------------------------------ multi-chain (8f.2)
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_multi_chain_sweeps_equal_separate_runs(dt):
+    """cp_sgd_sweep_multi: four chains (different samplers, seeds, rules) in one launch equal four
+    separate cp_sgd_sweep calls bit for bit (the same per-cluster code on the same inputs)."""
+    from paper_2103_04081_b200 import CPSGD
+
+    cfg = synth.small((40, 30, 20), 6, dtype=dt, batch=64, rule="adaptive", eta=0.05, seed=4)
+    X, A0 = make_problem(cfg)
+    specs = [("leverage", 1, "adaptive"), ("euclidean", 2, "fixed"), ("uniform", 3, "adaptive"),
+             ("block_leverage", 4, "als")]
+    ref = []
+    for s, seed, rule in specs:
+        Xd, Ad = to_dev(X, A0)
+        h = handle(cfg, Xd, Ad, s, seed=seed, rule=rule)
+        h.sweep(3)
+        h.sync()
+        ref.append([a.cpu().numpy() for a in Ad])
+        h.close()
+    hs, Ads, Xs = [], [], []
+    for s, seed, rule in specs:
+        Xd, Ad = to_dev(X, A0)
+        hs.append(handle(cfg, Xd, Ad, s, seed=seed, rule=rule))
+        Ads.append(Ad)
+        Xs.append(Xd)
+    CPSGD.sweep_multi(hs, 3)
+    for i, h in enumerate(hs):
+        h.sync()
+        assert h.iter == 9
+        for k in range(3):
+            assert np.array_equal(Ads[i][k].cpu().numpy(), ref[i][k])
+    # a handle of another geometry is refused
+    cfg2 = synth.small((40, 30, 21), 6, dtype=dt, batch=64, rule="adaptive", eta=0.05, seed=4)
+    X2, A2 = make_problem(cfg2)
+    Xd2, Ad2 = to_dev(X2, A2)
+    h2 = handle(cfg2, Xd2, Ad2, "leverage", seed=9)
+    from paper_2103_04081_b200 import CPError
+
+    with pytest.raises(CPError, match="EINVAL"):
+        CPSGD.sweep_multi([hs[0], h2], 1)
+    for h in hs + [h2]:
+        h.close()
+
+
 # ------------------------------------------------------------------------------------------ trajectories
 @pytest.mark.parametrize("strategy", S)
 @pytest.mark.parametrize("path", ["fused", "split_mm"])
