@@ -166,7 +166,6 @@ struct cp_sgd_s {
   unsigned* sc_cnt = nullptr;    // wide path: k_update_wide score-phase CTA arrival counter
   unsigned* uw_flag = nullptr;   // wide path: W-ready epoch (monotonic)
   void* sw_gcl = nullptr;        // wide path: k_sample_wide cluster partials of Gamma
-  unsigned* sw_cnt = nullptr;    // wide path: k_sample_wide arrival counter
   bool use_tc = false;           // fp32 wide path on tcgen05 (k_gather_update_tc), else the FFMA mainloop
   float* zimg = nullptr;         // tcgen05 path: {zh; zl} A-operand images of the prefetched batch
   int fused_cu = 0, fused_bpc = 0, fused_rpc = 0;  // fused kernel geometry (0: not eligible)
@@ -790,7 +789,6 @@ cp_status launch_sw_t(cp_sgd_s* h, int n) {
   p.sp.zwp = h->zwp;
   p.sp.gam_next = h->gam_next;
   p.gcl = h->sw_gcl;
-  p.cnt = h->sw_cnt;
   p.dbg = h->dbg;
   p.cdf_elems = ts_cdf_elems(h, n);
   const size_t smem = sw_smem_bytes(h->N, h->R, p.cdf_elems, sizeof(T));
@@ -1393,8 +1391,6 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       int64_t ncl = 0;
       for (int n = 0; n < h->N; ++n) ncl = std::max(ncl, ceil_div(ceil_div(h->bmax[n], kSWFibers), kSWCluster));
       ALLOC(h->sw_gcl, h->esz * ncl * h->R * h->R);
-      ALLOC(h->sw_cnt, sizeof(unsigned));
-      cudaMemsetAsync(h->sw_cnt, 0, sizeof(unsigned), h->stream);
       ALLOC(h->Mpart, h->esz * mpart);
       ALLOC(h->gu_cnt, sizeof(unsigned) * ceil_div(Imax, kGUTI));
       cudaMemsetAsync(h->gu_cnt, 0, sizeof(unsigned) * ceil_div(Imax, kGUTI), h->stream);
@@ -1526,7 +1522,6 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->tw_stat);
   cudaFree(h->sc_q);
   cudaFree(h->sw_gcl);
-  cudaFree(h->sw_cnt);
   cudaFree(h->iter_dev);
   cudaFree(h->iter_tmp);
   cudaFree(h->status_dev);

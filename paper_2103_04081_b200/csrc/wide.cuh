@@ -583,7 +583,6 @@ struct SWParams {
   long long* dbg;
   SampleParams sp;          // batch of mode sp.n at the iteration in *sp.iter; zwp / gam_next set
   void* gcl;                // [clusters][R][R] cluster partials of Gamma (T)
-  unsigned* cnt;            // arrival counter (zero between launches)
   int64_t cdf_elems;        // staged CDF entries (sum of I_k, k != n; 0 = uniform)
 };
 
@@ -627,7 +626,6 @@ __global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
   T* zs = reinterpret_cast<T*>(carve(sizeof(T) * kSWFibers * RP));
   T* red = reinterpret_cast<T*>(carve(sizeof(T) * (size_t)zg_groups(R, kWThreads) * R * R));
   __shared__ const uint64_t* s_cp[kMaxOrder];
-  __shared__ int s_last;
   SWM(0);
   long long gt0 = 0;
   if (P.dbg && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
