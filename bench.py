@@ -132,7 +132,7 @@ def run_chains(args, cfg):
     for c in range(args.chains):
         Ad = [a.clone() for a in Ad0]
         h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=args.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta,
-                  seed=cfg.seed + 1000 * c, mode_major=not args.native_layout)
+                  seed=cfg.seed + 1000 * c, mode_major=not args.native_layout, fused_cluster=args.chain_cluster)
         hs.append(h)
         keep.append(Ad)
     CPSGD.sweep_multi(hs, args.warmup)
@@ -158,7 +158,7 @@ def run_chains(args, cfg):
             "dtype": "f64" if cfg.dtype == "f64" else "f32", "data": "synthetic (seeded; synth/ recipe)",
             "config": {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.dims))} {cfg.dtype}, R={cfg.rank}, "
                                    f"B={cfg.batch}, {cfg.rule} step, {args.sampler} sampling, cyclic sweeps",
-                       "chains": args.chains, "step": f"one cyclic sweep of every chain ({N} SGD iterations x B "
+                       "chains": args.chains, "chain_cluster": args.chain_cluster, "step": f"one cyclic sweep of every chain ({N} SGD iterations x B "
                        f"fibers each), all chains in one k_sweep_fused_multi launch (one 16-CTA cluster each)",
                        "timing": "host-synchronised CUDA events around the call (all chains' streams)"},
             "clocks": clk.summary(), "gpu_launches": 1, "e2e": None}
@@ -435,6 +435,8 @@ def main():
     ap.add_argument("--no-tc", action="store_true", help="FFMA gather mainloop instead of tcgen05")
     ap.add_argument("--chains", type=int, default=1,
                     help="K > 1: K independent chains in one multi-chain launch (fused workloads; SURVEY 8f.2)")
+    ap.add_argument("--chain-cluster", type=int, default=16, choices=[8, 16],
+                    help="--chains: CTAs per chain (8: two chains per GPC)")
     ap.add_argument("--rule", default="config", choices=["config", "fixed", "adaptive", "als"],
                     help="update rule (config: the workload's; als: the sampled least-squares step, SURVEY 8f.3)")
     args = ap.parse_args()

@@ -79,6 +79,8 @@ typedef enum { CP_ORDER_CYCLIC = 0, CP_ORDER_RANDOM = 1 } cp_mode_order;
 #define CP_FLAG_EXTERNAL_COMM 0x4u /* world > 1 without an internal NCCL communicator: the caller
                                      performs the exchange between the phases of cp_sgd_step_phase  */
 #define CP_FLAG_NO_TC 0x20u        /* fp32 wide path: FFMA mainloop instead of tcgen05 3xTF32       */
+#define CP_FLAG_FUSED_CU8 0x40u    /* fused path on 8-CTA clusters instead of 16: slower per chain, but
+                                      two chains fit one GPC (cp_sgd_sweep_multi throughput mode)   */
 #define CP_FLAG_NO_WIDE 0x10u      /* single GPU, split path: never use the fused gather + update kernel
                                      (k_gather_update); use the gather-partials + update-table pair */
 

@@ -19,8 +19,8 @@ LIB_PATH = os.path.join(_HERE, "libcpsgd.so")
 SAMPLERS = {"uniform": 0, "leverage": 1, "euclidean": 2, "block_leverage": 3, "block_euclidean": 4}
 RULES = {"fixed": 0, "adaptive": 1, "als": 2}
 ORDERS = {"cyclic": 0, "random": 1}
-FLAG_MODE_MAJOR, FLAG_NO_GRAPH, FLAG_EXTERNAL_COMM, FLAG_NO_FUSED, FLAG_NO_WIDE, FLAG_NO_TC = \
-    0x1, 0x2, 0x4, 0x8, 0x10, 0x20
+FLAG_MODE_MAJOR, FLAG_NO_GRAPH, FLAG_EXTERNAL_COMM, FLAG_NO_FUSED, FLAG_NO_WIDE, FLAG_NO_TC, FLAG_FUSED_CU8 = \
+    0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
 KERNEL_NAMES = ["k_sample", "k_gather", "k_update_table", "k_table", "k_reduce_partials", "nccl", "k_fit",
                 "k_sweep_fused", "k_gather_update", "k_zw_gamma", "k_gather_update_tc", "k_table_sample",
                 "k_update_wide", "k_scores_wide", "k_sample_wide"]
@@ -119,7 +119,7 @@ class CPSGD:
                  seed: int = 0, stream=None, world_rank: int = 0, world_size: int = 1, nccl_id: bytes = None,
                  slab=None, mode_major: bool = True, block_window=None, graphs: bool = True,
                  external_comm: bool = False, fused: bool = True, wide: bool = True,
-                 tc: bool = True):
+                 tc: bool = True, fused_cluster: int = 16):
         import torch
 
         L = load_library()
@@ -144,7 +144,8 @@ class CPSGD:
         self._nccl_id = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
         flags = (FLAG_MODE_MAJOR if mode_major else 0) | (0 if graphs else FLAG_NO_GRAPH) | \
                 (FLAG_EXTERNAL_COMM if external_comm else 0) | (0 if fused else FLAG_NO_FUSED) | \
-                (0 if wide else FLAG_NO_WIDE) | (0 if tc else FLAG_NO_TC)
+                (0 if wide else FLAG_NO_WIDE) | (0 if tc else FLAG_NO_TC) | \
+                (FLAG_FUSED_CU8 if fused_cluster == 8 else 0)
         lo, hi = (0, self.dims[-1]) if slab is None else (int(slab[0]), int(slab[1]))
         cfg = Config(self.N, self._dims_arr, self.R, self.dtype, X.data_ptr(), self._fac_arr, int(batch),
                      self._win_arr, SAMPLERS[sampler], RULES[rule], float(alpha), float(eta), float(b), float(eps),

@@ -997,7 +997,7 @@ void plan_fused(cp_sgd_s* h) {
     cdfmax += h->dims[n];
   }
   if (imax > 2 * kFThreads) return;
-  const int CU = 16;
+  const int CU = (h->flags & CP_FLAG_FUSED_CU8) ? 8 : 16;
   const int bpc = (int)ceil_div(bmx, CU);
   const int rpc = (int)ceil_div(imax, CU);
   if (bpc > 256 || rpc > kFThreads) return;

@@ -756,6 +756,9 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
     F_MARK(12);
     n = n_next;
   }
+  // no CTA may exit while a peer still reads its shared memory over DSMEM (the last step's CDF
+  // assembly reads every peer's prefixes after barrier #3 and ends with a CTA-local barrier only)
+  cluster.sync();
   if (q == 0 && tid == 0) {
     *p.iter = r;
     *p.last_mode = n_done;

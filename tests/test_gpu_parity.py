@@ -119,6 +119,7 @@ STEP_CASES = [
 
 
 PATHS = {"fused": dict(fused=True, mode_major=True),            # persistent single-cluster kernel
+         "fused_cu8": dict(fused=True, mode_major=True, fused_cluster=8),  # same on 8-CTA clusters
          "split_mm": dict(fused=False, mode_major=True),        # gather+update kernel, then table/sample kernel
          "split_native": dict(fused=False, mode_major=False),   # same, strided fibers in the native layout
          "split_ffma": dict(fused=False, tc=False, mode_major=True),  # wide path, FFMA mainloop (no tcgen05)
