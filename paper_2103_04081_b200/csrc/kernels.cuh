@@ -833,6 +833,15 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+__device__ __forceinline__ double rcp_nr(double x) {  // 1/x: MUFU approximation + two Newton steps
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
 // Inverse of the fp64 Gram on its numerically full-rank pivot set S by the symmetric sweep
 // operator (Gauss-Jordan with diagonal pivoting in natural order, Goodnight 1979): sweeping pivot k
 // maps M_ij -= M_ik M_kj / d (i, j != k), M_ik, M_kj /= d, M_kk = -1/d (d = M_kk).  The unswept
@@ -840,23 +849,29 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // R4(b), the rank rule of a pivoted Cholesky); after sweeping S, M_SS = -(G_SS)^{-1}.
 // Row groups x lanes: thread (g, c) of NT = 32 ceil(RMAX/32) G threads keeps rows
 // [g RPG, (g + 1) RPG) of column c of the RMAX x RMAX matrix (identity past R; RMAX = ceil8(R),
-// RPG = ceil(RMAX / G)) in registers, static indices, no rotation.  Pivots go in natural order in
-// PAIRS P = {k, l = k + 1}: the owner groups of rows k and l publish them to shared memory (by
-// symmetry rb1[t] = M_tk, rb2[t] = M_tl are also the pivot columns), one named barrier, then with
+// RPG = RMAX / G) in registers.  Pivots go in natural order in PAIRS P = {k, l = k + 1}; the pair
+// loop is unrolled over the owner group's rows, so the pivot rows sit at STATIC register indices:
+// the owner group publishes rows k and l interleaved (rb[2t] = M_kt, rb[2t+1] = M_lt; by symmetry
+// also the pivot columns) with one 16-byte store per thread, one named barrier, then with
 // B = M_PP = [[a, b], [b, c]] and det = a c - b^2:
 //   a > tol and det > tol a  (both Schur diagonals a and det / a above tol: the single-pivot rule)
-//     -> block sweep with ONE reciprocal 1/det: per column (f1, f2) = B^{-1} M_Pc (c not in P) or the
-//        negated column of B^{-1} (c in P); rows k, l <- f1, f2; others <- [c not in P] M_tc -
-//        rb1[t] f1 - rb2[t] f2 (the sweep operator on the block, M_PP -> -B^{-1});
+//     -> block sweep with ONE reciprocal 1/det (computed speculatively, before the test): per column
+//        (f1, f2) = B^{-1} m with m = M_Pc (c not in P) or m = -e_k, -e_l (c in P: the negated
+//        columns of B^{-1}); every held entry <- [c not in P] M_tc - rb[2t] f1 - rb[2t+1] f2 (two
+//        DFMA, one 16-byte broadcast load, no selects); the owner group then sets rows k, l <- f1, f2
+//        (the sweep operator on the block, M_PP -> -B^{-1});
 //   otherwise single-pivot steps for k (if a > tol) and then l on the updated values (d > tol),
 //   i.e. exactly the natural-order single-pivot sweep with the skip rule of R4(b).
-// The pivot chain (publish -> barrier -> reciprocal -> update) is paid once per two pivots; the
-// single-pivot row-group form was bound by that chain (~420 cycles per pivot): R = 20: 9.6k -> 8.0k
-// cycles, R = 50: 37.7k -> 27.5k (tools/micro/sweep_grp.cu; results within 2e-15 of it).
-// Called by every thread of the CTA (>= NT threads); rowbuf: kSweepBuf doubles; returns |S|.
+// Cost history at R = 20 / 50 (cycles, tools/micro/sweep_grp.cu, sweep_st.cu): one pivot per
+// barrier 9.6k / 37.7k -> 2x2 blocks 8.0k (8.7k) / 27.5k (29.2k) -> static pivot positions,
+// interleaved 16-byte pivot rows, select-free update, Newton reciprocal 5.6k / 18.2k (results
+// within 3e-16 relative of the previous form, same rank on rank-deficient inputs).
+// Called by every thread of the CTA (>= NT threads); rowbuf: kSweepBuf doubles, 16-byte aligned;
+// returns |S|.
 template <int RMAX, int G>
 __device__ int grp_sweep_inverse(double* Gm, int R, double tol, double* rowbuf, int* swept) {
-  constexpr int CW = (RMAX + 31) / 32, NT = 32 * CW * G, RPG = (RMAX + G - 1) / G, RB = RPG * G + 8;
+  constexpr int CW = (RMAX + 31) / 32, NT = 32 * CW * G, RPG = RMAX / G, RB = RMAX + 8;
+  static_assert(RMAX % (2 * G) == 0, "RMAX: a multiple of 2G (pivot pairs never straddle two groups)");
   static_assert(4 * RB <= kSweepBuf, "sweep buffer");
   const int tid = threadIdx.x, RS = R + 1;
   if (tid < NT) {
@@ -868,71 +883,71 @@ __device__ int grp_sweep_inverse(double* Gm, int R, double tol, double* rowbuf, 
       v[t] = (row < R && c < R) ? Gm[row * RS + c] : (row == c ? 1.0 : 0.0);
     }
     for (int j = tid; j < R; j += NT) swept[j] = 0;
-    auto publish = [&](int k, double* rb) {  // owner group of row k: M_kc -> rb[c]
-      const int gk = k / RPG, tk = k - gk * RPG;
-      if (g == gk) {
-        double pv = v[0];
+    // one sweep step on pivot k = gk RPG + tk (d = M_kk > tol); rb[2 i + o] = M_ki
+    auto single = [&](int gk, int k, int tk, const double* rb, int o, double d) {
+      const double dinv = rcp_nr(d);
+      const double f = (c == k) ? -dinv : rb[2 * c + o] * dinv;
+      if (c == k) {
 #pragma unroll
-        for (int t = 1; t < RPG; ++t) pv = (tk == t) ? v[t] : pv;
-        rb[c] = pv;
+        for (int t = 0; t < RPG; ++t) v[t] = 0.0;
       }
-    };
-    auto single = [&](int k, const double* rb, double d) {  // one sweep step on pivot k (d = M_kk > tol)
-      const double dinv = __drcp_rn(d);
-      const bool isk = (c == k);
-      const double f = isk ? -dinv : rb[c] * dinv;
 #pragma unroll
-      for (int t = 0; t < RPG; ++t) {
-        const int row = g * RPG + t;
-        v[t] = (row == k) ? f : fma(-rb[row], f, isk ? 0.0 : v[t]);
-      }
+      for (int t = 0; t < RPG; ++t) v[t] = fma(-rb[2 * (g * RPG + t) + o], f, v[t]);
+      if (g == gk) v[tk] = f;
       if (tid == 0) swept[k] = 1;
     };
     int par = 0;
 #pragma unroll 1
-    for (int k = 0; k < R; k += 2) {
-      const int l = k + 1;  // == R: the last pivot alone
-      double* rb1 = rowbuf + par * 2 * RB;
-      double* rb2 = rb1 + RB;
-      par ^= 1;
-      publish(k, rb1);
-      if (l < R) publish(l, rb2);
-      named_bar_sync(1, NT);
-      const double a = rb1[k];
-      const double b = l < R ? rb1[l] : 0.0, cc = l < R ? rb2[l] : 0.0;
-      const double det = fma(a, cc, -b * b);
-      if (l < R && a > tol && det > tol * a) {  // uniform
-        const double dinv = __drcp_rn(det);
-        double f1, f2;
-        if (c == k) {
-          f1 = -cc * dinv;
-          f2 = b * dinv;
-        } else if (c == l) {
-          f1 = b * dinv;
-          f2 = -a * dinv;
-        } else {
-          const double mk = rb1[c], ml = rb2[c];
-          f1 = fma(cc, mk, -b * ml) * dinv;
-          f2 = fma(a, ml, -b * mk) * dinv;
-        }
-        const bool isp = (c == k) || (c == l);
+    for (int gk = 0; gk < G; ++gk) {
 #pragma unroll
-        for (int t = 0; t < RPG; ++t) {
-          const int row = g * RPG + t;
-          v[t] = (row == k) ? f1 : (row == l) ? f2 : fma(-rb1[row], f1, fma(-rb2[row], f2, isp ? 0.0 : v[t]));
-        }
-        if (tid == 0) {
-          swept[k] = 1;
-          swept[l] = 1;
-        }
-      } else {
-        if (a > tol) single(k, rb1, a);
-        if (l < R) {  // pivot l on the values after step k: republish its row
-          named_bar_sync(1, NT);  // every thread is done with rb2
-          publish(l, rb2);
+      for (int tk = 0; tk < RPG; tk += 2) {
+        const int k = gk * RPG + tk, l = k + 1;  // l == R: the last pivot alone
+        if (k < R) {
+          // rows k and l interleaved: rb[2 i] = M_ki, rb[2 i + 1] = M_li (one 16-byte load per row i)
+          double* rb = rowbuf + par * 2 * RB;
+          double2* rb2 = reinterpret_cast<double2*>(rb);
+          par ^= 1;
+          if (g == gk && c < RMAX) rb2[c] = make_double2(v[tk], v[tk + 1]);  // owner group publishes
           named_bar_sync(1, NT);
-          const double d = rb2[l];
-          if (d > tol) single(l, rb2, d);
+          const double2 pk = rb2[k], pl = rb2[l];
+          const double a = pk.x, b = pk.y, cc = pl.y;  // l < RMAX: row l exists (identity past R)
+          const double det = fma(a, cc, -b * b);
+          const double2 m = rb2[c];
+          const double dinv = rcp_nr(det);  // speculative: overlaps the pivot test
+          if (l < R && a > tol && det > tol * a) {  // uniform
+            // (f1, f2) = B^{-1} m with m = M_Pc, or m = -e_k / -e_l on the pivot columns (the negated
+            // columns of B^{-1}); selects instead of a divergent branch
+            const double mx = (c == k) ? -1.0 : (c == l) ? 0.0 : m.x;
+            const double my = (c == k) ? 0.0 : (c == l) ? -1.0 : m.y;
+            const double f1 = fma(cc, mx, -b * my) * dinv;
+            const double f2 = fma(a, my, -b * mx) * dinv;
+            if (c == k || c == l) {  // the pivot columns start from 0 (M_PP -> -B^{-1})
+#pragma unroll
+              for (int t = 0; t < RPG; ++t) v[t] = 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < RPG; ++t) {
+              const double2 q = rb2[g * RPG + t];
+              v[t] = fma(-q.x, f1, fma(-q.y, f2, v[t]));
+            }
+            if (g == gk) {  // the pivot rows (static register indices)
+              v[tk] = f1;
+              v[tk + 1] = f2;
+            }
+            if (tid == 0) {
+              swept[k] = 1;
+              swept[l] = 1;
+            }
+          } else {
+            if (a > tol) single(gk, k, tk, rb, 0, a);
+            if (l < R) {  // pivot l on the values after step k: republish its row
+              named_bar_sync(1, NT);  // every thread is done with rb
+              if (g == gk && c < RMAX) rb[2 * c + 1] = v[tk + 1];
+              named_bar_sync(1, NT);
+              const double d = rb[2 * l + 1];
+              if (d > tol) single(gk, l, tk + 1, rb, 1, d);
+            }
+          }
         }
       }
     }
