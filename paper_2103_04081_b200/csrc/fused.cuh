@@ -678,7 +678,16 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
     cluster.sync();  // #1: partials visible
     F_MARK(2);
     // ------------------------------------------------ (2) cluster reduction (rank order) + update
-    for (int e = tid; e < R * R; e += kFThreads) Gam[e] = cluster_sum(cluster, Gp, e, CU);
+    // Gamma is symmetric: the upper triangle of the partials (the remote reads are the cost: the
+    // SM's DSMEM read rate, ~14 B/clk), mirrored
+    for (int pair = tid; pair < R * (R + 1) / 2; pair += kFThreads) {
+      int r1 = 0, rem = pair;
+      while (rem >= R - r1) { rem -= R - r1; ++r1; }
+      const int r2 = r1 + rem;
+      const T v = cluster_sum(cluster, Gp, r1 * R + r2, CU);
+      Gam[r1 * R + r2] = v;
+      Gam[r2 * R + r1] = v;
+    }
     __syncthreads();
     if (q == 0 && s == p.nsteps - 1)
       for (int e = tid; e < R * R; e += kFThreads) p.Gam_out[e] = Gam[e];
