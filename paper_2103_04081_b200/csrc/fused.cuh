@@ -301,7 +301,9 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
   }
   __syncthreads();
 
+  long long* sdbg = nullptr;  // debug phase marks of one sample_own call
   auto sample_own = [&](int n, uint64_t it) {
+    if (sdbg && tid == 0) sdbg[23] = clock64();
     if (block && tid == 0) {  // window draws (eq:bik, R2): common to the whole batch
       double prod = 1.0;
       int64_t beff = 1;
@@ -352,6 +354,7 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
       }
       __syncthreads();
     }
+    if (sdbg && tid == 0) sdbg[24] = clock64();
     for (int lb = tid; lb < p.BPC; lb += kFThreads) {
       const int64_t b = b0 + lb;
       int32_t* ib = ix + lb * NP;
@@ -384,6 +387,7 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
       fb[lb] = p.pitch[n] ? jrow * p.pitch[n] : offn;
     }
     __syncthreads();
+    if (sdbg && tid == 0) sdbg[25] = clock64();
     // TensorSamp (Alg. 5) issue: this CTA's fiber segments -> shared memory (xs[lb][i], pitch Ip) by
     // cp.async, completed at the gather.  The copies overlap the SKR rows and, for the next step's
     // batch, the whole tail of the current step.  (Direct loads at the gather were bound by the
@@ -411,24 +415,56 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
       }
       cp_async_commit();
     }
-    // SKR rows (Alg. 1): z = (*)_{k != n} A^(k)(i_k, :); zw = w z; padded to RP with zeros
-    for (int e = tid; e < p.BPC * RP; e += kFThreads) {
-      const int lb = e / RP, rr = e % RP;
-      T z = T(0), zwv = T(0);
-      if (rr < R && fb[lb] >= 0) {
-        const int32_t* ib = ix + lb * NP;
-        z = T(1);
-        int pos = 0;
-        for (int k = 0; k < N; ++k) {
-          if (k == n) continue;
-          z = z * __ldg(p.factors[k] + (int64_t)ib[pos++] * R + rr);
+    if (sdbg && tid == 0) sdbg[26] = clock64();
+    // SKR rows (Alg. 1): z = (*)_{k != n} A^(k)(i_k, :); zw = w z; padded to RP with zeros.  kSU
+    // entries per thread and two modes per round: their factor loads are issued together (one L2
+    // round trip per two modes instead of one per mode and entry); the products keep the mode order.
+    // The loads are coherent: rows of the mode updated in the previous step were written by peer CTAs
+    // inside this kernel (ordered by the cluster barriers); the non-coherent path may not see them.
+    {
+      constexpr int kSU = 4;
+      for (int e0 = 0; e0 < p.BPC * RP; e0 += kSU * kFThreads) {
+        T z[kSU];
+        bool act[kSU];
+        int lbu[kSU];
+#pragma unroll
+        for (int u = 0; u < kSU; ++u) {
+          const int e = e0 + u * kFThreads + tid;
+          const int lb = e / RP, rr = e % RP;
+          lbu[u] = lb;
+          act[u] = e < p.BPC * RP && rr < R && fb[lb] >= 0;
+          z[u] = act[u] ? T(1) : T(0);
         }
-        zwv = (T)wt[lb] * z;
+        for (int pos = 0; pos < NP; pos += 2) {
+          const int k0 = pos < n ? pos : pos + 1, k1 = pos + 1 < n ? pos + 1 : pos + 2;
+          const bool two = pos + 1 < NP;
+          T f0[kSU], f1[kSU];
+#pragma unroll
+          for (int u = 0; u < kSU; ++u) {
+            const int e = e0 + u * kFThreads + tid, rr = e % RP;
+            const int32_t* ib = ix + lbu[u] * NP;
+            f0[u] = act[u] ? p.factors[k0][(int64_t)ib[pos] * R + rr] : T(0);
+            f1[u] = (act[u] && two) ? p.factors[k1][(int64_t)ib[pos + 1] * R + rr] : T(0);
+          }
+#pragma unroll
+          for (int u = 0; u < kSU; ++u) {
+            if (!act[u]) continue;
+            z[u] = z[u] * f0[u];
+            if (two) z[u] = z[u] * f1[u];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kSU; ++u) {
+          const int e = e0 + u * kFThreads + tid;
+          if (e < p.BPC * RP) {
+            zu[e] = z[u];
+            zw[e] = act[u] ? (T)wt[lbu[u]] * z[u] : T(0);
+          }
+        }
       }
-      zu[e] = z;
-      zw[e] = zwv;
     }
     __syncthreads();
+    if (sdbg && tid == 0) sdbg[27] = clock64();
   };
 
   // (a1) the table of the new A^(n) from this CTA's rows Anew (Gram / norm partials, cluster sums,
@@ -761,7 +797,9 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
     if (p.strategy == 0) cluster.sync();
     else __syncthreads();
     F_MARK(11);
+    sdbg = (p.dbg && q == 0 && s == 1) ? p.dbg : nullptr;
     if (s + 1 < p.nsteps) sample_own(n_next, r);
+    sdbg = nullptr;
     F_MARK(12);
     n = n_next;
   }

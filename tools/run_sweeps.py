@@ -53,6 +53,7 @@ if os.environ.get("CPSGD_DEBUG_TIMERS") and os.environ.get("FUSED_TIMERS"):
     print(" | ".join(f"{names[i]}:{t[i + 1] - t[i]}" for i in range(12)), "| total", t[12] - t[0])
     print("gram-sum", t[13] - t[5], "sweep", t[6] - t[13], "| gather: contract", t[14] - t[0], "Gamma part", t[15] - t[14],
           "Aold", t[1] - t[15])
+    print("  sample: draws", t[24] - t[23], "weights/offsets", t[25] - t[24], "cp.async issue", t[26] - t[25], "SKR", t[27] - t[26])
     print("  contract: ld0", t[17] - t[16], "fma0", t[18] - t[17], "ld1", t[19] - t[18], "fma1", t[20] - t[19], "store", t[14] - t[20])
 elif os.environ.get("CPSGD_DEBUG_TIMERS"):
     h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=a.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta, seed=0,
