@@ -605,7 +605,7 @@ __host__ __device__ inline size_t sw_smem_bytes(int N, int R, int64_t cdf_elems,
     if (P.dbg && blockIdx.x == 0 && threadIdx.x == 0) P.dbg[100 + (slot)] = clock64();     \
   } while (0)
 template <typename T>
-__global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
+__global__ void __launch_bounds__(kWThreads, 1) k_sample_wide(SWParams P) {
   pdl_wait();  // the tables and factors come from the previous kernel
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -709,17 +709,24 @@ __global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
       ru[u] = e % RP;
       z[u] = (e < kSWFibers * RP && lbu[u] < nf && ru[u] < R) ? T(1) : T(0);
     }
-    int pos = 0;
-    for (int k = 0; k < N; ++k) {  // ascending modes (Alg. 1)
-      if (k == sp.n) continue;
-      const T* F = reinterpret_cast<const T*>(sp.factors[k]);
-      T f[U];
+    // ascending modes (Alg. 1), two per round: both modes' loads are issued before the products
+    for (int pos = 0; pos < NP; pos += 2) {
+      const int k0 = pos < sp.n ? pos : pos + 1, k1 = pos + 1 < sp.n ? pos + 1 : pos + 2;
+      const bool two = pos + 1 < NP;
+      const T* F0 = reinterpret_cast<const T*>(sp.factors[k0]);
+      const T* F1 = reinterpret_cast<const T*>(sp.factors[two ? k1 : k0]);
+      T f0[U], f1[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        f[u] = z[u] != T(0) ? F[(int64_t)sidx[lbu[u] * NP + pos] * R + ru[u]] : T(0);
+      for (int u = 0; u < U; ++u) {
+        const bool on = z[u] != T(0);
+        f0[u] = on ? F0[(int64_t)sidx[lbu[u] * NP + pos] * R + ru[u]] : T(0);
+        f1[u] = (on && two) ? F1[(int64_t)sidx[lbu[u] * NP + pos + 1] * R + ru[u]] : T(0);
+      }
 #pragma unroll
-      for (int u = 0; u < U; ++u) z[u] = z[u] * f[u];
-      ++pos;
+      for (int u = 0; u < U; ++u) {
+        z[u] = z[u] * f0[u];
+        if (two) z[u] = z[u] * f1[u];
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -786,7 +793,9 @@ __global__ void __launch_bounds__(kWThreads) k_sample_wide(SWParams P) {
           }
         }
     }
+    SWM(8);
     __syncthreads();
+    SWM(9);
     for (int e = tid; e < R * R; e += kWThreads) {
       T s = red[e];
       for (int gg = 1; gg < G; ++gg) s += red[gg * R * R + e];

@@ -77,6 +77,7 @@ elif os.environ.get("CPSGD_DEBUG_TIMERS"):
     if t[107]:
         nm = ["cdf stage", "draw", "skr", "zw/img", "gamma", "cluster+fence", "last"]
         print("k_sample_wide (CTA 0) cycles: " + " | ".join(f"{nm[i]} {t[101 + i] - t[100 + i]}" for i in range(7)))
+        print("  gamma: own blocks", t[108] - t[104], "barrier", t[109] - t[108], "group sum", t[105] - t[109])
         import numpy as np
         g0 = np.array(t[2048:3008:2]); g1 = np.array(t[2049:3008:2]); m = g0 > 0
         g0, g1 = g0[m], g1[m]
