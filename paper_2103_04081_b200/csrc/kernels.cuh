@@ -833,7 +833,10 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-__device__ __forceinline__ double rcp_nr(double x) {  // 1/x: MUFU approximation + two Newton steps
+// 1/x: MUFU approximation + two Newton steps (within ~1 ulp of 1/x).  The approximation flushes
+// subnormals: valid for 2^-1021 < |x| < 2^1021, i.e. Gram entries (and pivots) in the normal range;
+// a guard with a __drcp_rn fallback on the pivot chain measured ~15 % slower
+__device__ __forceinline__ double rcp_nr(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   double e = fma(-x, y, 1.0);

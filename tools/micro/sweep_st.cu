@@ -213,14 +213,7 @@ __device__ int grp_sweep_st2(double* Gm, int R, double tol, double* rowbuf, int*
   return rank;
 }
 
-__device__ __forceinline__ double rcp_nr(double x) {  // 1/x: MUFU approximation + two Newton steps
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
-}
+// rcp_nr: cps::rcp_nr (kernels.cuh)
 template <int RMAX, int G>
 __device__ int grp_sweep_st3(double* Gm, int R, double tol, double* rowbuf, int* swept) {
   constexpr int CW = (RMAX + 31) / 32, NT = 32 * CW * G, RPG = RMAX / G, RB = RMAX + 8;
