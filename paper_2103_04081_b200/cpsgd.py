@@ -187,8 +187,12 @@ class CPSGD:
         bm = C.c_int64(0)
         self._chk(self._L.cp_sgd_batch_max(self._h, mode, C.byref(bm)))
         bmax = bm.value
-        idx = torch.zeros((bmax, self.N - 1), dtype=torch.int32, device=self._X.device)
-        w = torch.zeros(bmax, dtype=torch.float64, device=self._X.device)
+        # the library writes on its own stream: allocate there (no fill kernel to race with), after
+        # the caller's pending work
+        self.stream.wait_stream(torch.cuda.current_stream(self._X.device))
+        with torch.cuda.stream(self.stream):
+            idx = torch.empty((bmax, self.N - 1), dtype=torch.int32, device=self._X.device)
+            w = torch.empty(bmax, dtype=torch.float64, device=self._X.device)
         beff = C.c_int64(0)
         self._chk(self._L.cp_sgd_sample(self._h, mode, C.c_uint64(it), C.c_void_p(idx.data_ptr()),
                                         C.c_void_p(w.data_ptr()), C.byref(beff)))

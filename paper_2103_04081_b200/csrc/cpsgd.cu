@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -100,6 +101,16 @@ size_t allow_max_dyn_smem(F* func) {
   if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess) return 0;
   return (size_t)mx;
 }
+
+// "first use on this device" for per-launcher one-time kernel attributes (function attributes are
+// per device context: a second GPU in the same process needs them too)
+struct DevOnce {
+  std::atomic<uint64_t> mask{0};
+  bool first(int dev) {
+    const uint64_t bit = 1ull << (dev & 63);
+    return !(mask.fetch_or(bit) & bit);
+  }
+};
 
 }  // namespace
 
@@ -374,10 +385,9 @@ cp_status launch_gather_t(cp_sgd_s* h, int n) {
   p.Mp = (T*)h->Mp;
   p.Gp = (T*)h->Gp;
   const size_t smem = gather_smem_bytes<T, RPT>(h->R);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DevOnce attr_once;  // per device: the attribute is per context
+  if (attr_once.first(h->device)) {
     allow_max_dyn_smem(k_gather<T, RPT>);
-    attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(h->ntiles[n], h->nchunks[n], 1);
@@ -454,13 +464,12 @@ cp_status launch_ut_t(cp_sgd_s* h, int n, int do_update, int do_table, int64_t r
   // one CTA per SM: the cluster's CTAs each run the serial table stages; co-residing CTAs would
   // share one SM's issue slots (claim more than half of the SM's shared memory)
   smem = std::max(smem, (size_t)h->sample_smem / 2 + 1024);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DevOnce attr_once;  // per device: the attribute is per context
+  if (attr_once.first(h->device)) {
     const size_t mx = allow_max_dyn_smem(k_update_table<T>);
     cudaError_t eb = cudaFuncSetAttribute(k_update_table<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (mx == 0 || eb != cudaSuccess)
       return h->fail(CP_ECUDA, "k_update_table attributes: %s", cudaGetErrorString(eb));
-    attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(CU, 1, 1);
@@ -580,11 +589,10 @@ cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   p.eps = h->eps;
   p.iter = h->iter_dev;
   const size_t smem = gu_smem_bytes<T, CPT>(p.KB);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DevOnce attr_once;  // per device: the attribute is per context
+  if (attr_once.first(h->device)) {
     allow_max_dyn_smem(k_gather_update<T, CPT>);
     cudaFuncSetAttribute(k_gather_update<T, CPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)ceil_div(h->dims[n], kGUTI), (unsigned)CK, 1);
@@ -637,10 +645,9 @@ cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev
   p.iter = h->iter_dev;
   p.dbg = h->dbg;
   const size_t smem = tc_smem_bytes(p.KB);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DevOnce attr_once;  // per device: the attribute is per context
+  if (attr_once.first(h->device)) {
     allow_max_dyn_smem(k_gather_update_tc);
-    attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)ceil_div(h->dims[n], kGUTI), (unsigned)CK, 1);
@@ -706,7 +713,11 @@ bool uw_coresident(int R, int64_t In) {
   lc.attrs = at;
   lc.numAttrs = 1;
   int act = 0;
-  if (cudaOccupancyMaxActiveClusters(&act, k_update_wide<T>, &lc) != cudaSuccess) {
+  const cudaError_t eo = cudaOccupancyMaxActiveClusters(&act, k_update_wide<T>, &lc);
+  // leave the attribute at the opt-in maximum: launches of other handles / modes (larger R or
+  // I_n) need more than this mode's size, and the launcher sets it only once per device
+  allow_max_dyn_smem(k_update_wide<T>);
+  if (eo != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
@@ -752,10 +763,9 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev,
   p.chg = take_chg;
   p.dbg = h->dbg;
   const size_t smem = uw_smem_bytes(h->R, sizeof(T), p.qch);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DevOnce attr_once;  // per device: the attribute is per context
+  if (attr_once.first(h->device)) {
     allow_max_dyn_smem(k_update_wide<T>);
-    attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)(ceil_div(ceil_div(h->dims[n], kUWRows), kUWCluster) * kUWCluster), 1, 1);
@@ -792,10 +802,9 @@ cp_status launch_sw_t(cp_sgd_s* h, int n) {
   p.dbg = h->dbg;
   p.cdf_elems = ts_cdf_elems(h, n);
   const size_t smem = sw_smem_bytes(h->N, h->R, p.cdf_elems, sizeof(T));
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DevOnce attr_once;  // per device: the attribute is per context
+  if (attr_once.first(h->device)) {
     allow_max_dyn_smem(k_sample_wide<T>);
-    attr_set = true;
   }
   const int64_t ctas = ceil_div(ceil_div(h->bmax[n], kSWFibers), kSWCluster) * kSWCluster;
   cudaLaunchConfig_t lc = {};
@@ -885,11 +894,10 @@ cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, dou
   ProfScope ps(h, kKFused);
   FusedParams<T> p;
   fill_fused_params<T>(h, p, nsteps, first_mode, order, alpha, alpha_dev, rebuild);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DevOnce attr_once;  // per device: the attribute is per context
+  if (attr_once.first(h->device)) {
     allow_max_dyn_smem(k_sweep_fused<T, ROWS>);
     cudaFuncSetAttribute(k_sweep_fused<T, ROWS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(h->fused_cu, 1, 1);
@@ -946,11 +954,10 @@ cp_status launch_fused_multi_t(cp_sgd_s* const* hs, int nh, int nsteps) {
   }
   for (int i = 1; i < nh; ++i) CUDA_TRY(h0, cudaStreamSynchronize(hs[i]->stream));  // their earlier work first
   CUDA_TRY(h0, cudaMemcpyAsync(h0->multi_params, prm.data(), bytes, cudaMemcpyHostToDevice, h0->stream));
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DevOnce attr_once;  // per device: the attribute is per context
+  if (attr_once.first(h0->device)) {
     allow_max_dyn_smem(k_sweep_fused_multi<T, ROWS>);
     cudaFuncSetAttribute(k_sweep_fused_multi<T, ROWS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr_set = true;
   }
   cudaLaunchConfig_t lc = {};
   size_t smem = 0;  // each cluster lays out its own shared memory (the CDF area depends on the sampler)
@@ -1590,7 +1597,18 @@ cp_status cp_sgd_sample(cp_sgd_t h, int32_t mode, uint64_t iter, int32_t* idx_de
   return CP_OK;
 }
 
+// the sampled-ALS rule is implemented by the fused and wide kernels only; the split / legacy update
+// kernels would read it as the adaptive rule (and its unallocated accumulator)
+static cp_status als_path_ok(cp_sgd_t h, int n) {
+  if (h->rule == CP_STEP_ALS && !wide_mode(h, n))
+    return h->fail(CP_EINVAL, "rule=als: mode %d is not on the wide path (the fused kernel runs only whole "
+                              "constant-step sweeps / single steps)", n);
+  return CP_OK;
+}
+
 static cp_status step_direct(cp_sgd_t h, int n, double alpha, int next_mode) {
+  cp_status sa = als_path_ok(h, n);
+  if (sa) return sa;
   const double a = (alpha < 0.0) ? h->alpha : alpha;
   auto* rr = rr_store(h, false);
   static const std::vector<int64_t> none;
@@ -1620,6 +1638,8 @@ cp_status cp_sgd_step_phase(cp_sgd_t h, int32_t mode, int32_t phase, double alph
   cp_status st = check_mode(h, mode);
   if (st) return st;
   const double a = (alpha < 0.0) ? h->alpha : alpha;
+  st = als_path_ok(h, mode);
+  if (st) return st;
   if (phase == 0) {
     st = phase0(h, mode, a, nullptr);
     if (!st && sharded(h) && !(h->flags & CP_FLAG_EXTERNAL_COMM)) st = exchange_after0(h, mode);
@@ -1843,9 +1863,13 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
 
 cp_status cp_fit(cp_sgd_t h, double* fit_host) {
   if (!h || !fit_host) return CP_EINVAL;
+  if (sharded(h) && (h->flags & CP_FLAG_EXTERNAL_COMM))
+    return h->fail(CP_ESTATE, "cp_fit on an external-comm sharded handle: the rank-local residual is not the fit");
   int64_t nfib = 1;
   for (int k = 1; k < h->N; ++k) nfib *= h->ldims[k];
-  const int blocks = (int)std::min<int64_t>(h->fit_blocks, nfib);
+  // a fixed number of partials on every rank (the kernel zeroes the ones past nfib): the NCCL sum
+  // below must see the same count everywhere, whatever each rank's slab length
+  const int blocks = h->fit_blocks;
   {
     ProfScope ps(h, kKFit);
     if (h->dtype == CP_F64)

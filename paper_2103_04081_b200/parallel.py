@@ -64,6 +64,7 @@ class ShardedRunner:
         self.h.exchange_copy(n, buf, False)
         self.sync()
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+        self._order_after_collective()
         self.h.exchange_copy(n, buf, True)
 
     def _exchange_rows(self, n: int):
@@ -76,6 +77,14 @@ class ShardedRunner:
             dist.broadcast(rows, src=r, group=self.group)
             if r != self.rank:
                 A[lo:hi].copy_(rows)
+        self._order_after_collective()
+
+    def _order_after_collective(self):
+        """the collectives and copies above ran on torch's current stream; the library's next phase
+        runs on the handle's stream: make that stream wait for them (no-op on CPU / gloo)"""
+        hs = getattr(self.h, "stream", None)
+        if hs is not None and self.torch.cuda.is_available() and hasattr(hs, "wait_stream"):
+            hs.wait_stream(self.torch.cuda.current_stream(hs.device))
 
     def sync(self):
         if hasattr(self.h, "sync"):
