@@ -83,6 +83,9 @@ typedef enum { CP_ORDER_CYCLIC = 0, CP_ORDER_RANDOM = 1 } cp_mode_order;
                                       two chains fit one GPC (cp_sgd_sweep_multi throughput mode)   */
 #define CP_FLAG_NO_WIDE 0x10u      /* single GPU, split path: never use the fused gather + update kernel
                                      (k_gather_update); use the gather-partials + update-table pair */
+#define CP_FLAG_NO_PERSIST 0x80u   /* fp32 wide path: never use the persistent cooperative sweep kernel
+                                     (k_sweep_wide); run each step as the gather / update+table /
+                                     sample kernel chain (graph-captured for cyclic sweeps)        */
 
 typedef struct {
   int32_t order;               /* N >= 3                                                          */
@@ -210,6 +213,22 @@ cp_status cp_sgd_get_launches(cp_sgd_t h, uint64_t* n_host);
 cp_status cp_sgd_profile(cp_sgd_t h, int32_t on);
 cp_status cp_sgd_profile_read(cp_sgd_t h, int32_t cap, int32_t* ids, double* total_ms, int64_t* counts,
                               int32_t* n_out);
+
+/* debug trace of the batches the persistent kernels consume (k_sweep_wide, k_sweep_fused; other
+ * paths record nothing).  cp_sgd_trace_layout returns the record layout: out[0] = stride (bytes per
+ * SGD iteration), out[1..6] = byte offsets of idx (int32 [B_max][N-1]), w (fp64 [B_max]), the
+ * updated factor A^(n) (dtype [I_n][R]), its accumulator S^(n) (adaptive rule), the new CDF of mode n
+ * (uint64 [I_n]) and meta (int64 {n, r, B_eff, 0}).  cp_sgd_trace(h, buf, cap) starts recording into
+ * the caller's device buffer buf (>= cap * stride bytes, BORROWED): the k-th SGD iteration run by a
+ * persistent kernel after this call fills record k (k < cap; later ones are dropped); buf = NULL
+ * stops.  cp_sgd_trace_count returns the number of iterations recorded since the last cp_sgd_trace. */
+cp_status cp_sgd_trace_layout(cp_sgd_t h, int64_t* out7_host);
+cp_status cp_sgd_trace(cp_sgd_t h, void* buf_dev, int64_t cap);
+cp_status cp_sgd_trace_count(cp_sgd_t h, int64_t* n_host);
+
+/* 1 if the handle runs its sweeps / steps on a persistent kernel (k_sweep_fused: 1, k_sweep_wide: 2),
+ * 0 for kernel chains */
+cp_status cp_sgd_path(cp_sgd_t h, int32_t* path_host);
 
 /* debug: clock64() phase timestamps of the last fused update/table kernel (CTA 0); only when the
  * environment variable CPSGD_DEBUG_TIMERS was set at cp_sgd_init, else CP_ESTATE */

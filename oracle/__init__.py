@@ -67,6 +67,7 @@ def lib():
         L.orc_fit.argtypes = [i32, P, P, i32, P, P, P, P]
         L.orc_random_mode.argtypes = [u64, u64, i32]
         L.orc_run.argtypes = [i32, P, i32, P, P, P, i32, i32, i32, i64, P, dbl, P, dbl, dbl, dbl, u64, u64, i64, P]
+        L.orc_run_f32.argtypes = L.orc_run.argtypes
         _lib = L
     return _lib
 
@@ -264,11 +265,14 @@ def run(X, factors, strategy: int, rule: int, B: int, iters: int, *, order=ORDER
     N = len(fs)
     R = fs[0].shape[1]
     Ss = [np.zeros_like(A) for A in fs] if S is None else [_f64(s).copy() for s in S]
-    Xf = _f64(X).ravel(order="F") if X.ndim > 1 else _f64(X)
+    x32 = X.dtype == np.float32 and X.ndim == 1 and X.flags["C_CONTIGUOUS"]
+    # an fp32 flat tensor is read in place by the fp32 entry (no fp64 copy of a 32 GB tensor)
+    Xf = X if x32 else (_f64(X).ravel(order="F") if X.ndim > 1 else _f64(X))
     win = None if window is None else np.ascontiguousarray(window, dtype=np.int32)
     al = None if alphas is None else _f64(alphas)
     modes = np.zeros(max(iters, 1), dtype=np.int32)
-    _chk(lib().orc_run(N, _p(d), R, _p(Xf), _ptrs(fs), _ptrs(Ss), strategy, rule, order, B,
+    fn = lib().orc_run_f32 if x32 else lib().orc_run
+    _chk(fn(N, _p(d), R, _p(Xf), _ptrs(fs), _ptrs(Ss), strategy, rule, order, B,
                        None if win is None else _p(win), alpha, None if al is None else _p(al), eta, b, eps,
                        C.c_uint64(seed), C.c_uint64(r0), iters, _p(modes)), "run")
     return fs, Ss, modes[:iters]

@@ -104,7 +104,14 @@ int64_t orc_linear_index(int N, const int64_t* dims, int n, const int32_t* tuple
 /* element (i, j) of the mode-n unfolding X_(n): decode j into the tuple by
  * the inverse of eq:map (mixed radix, first remaining mode fastest), then read the tensor
  * at the first-index-fastest offset sum_k i_k S_k, S_k = prod_{m<k} I_m. */
-static double orc_unfold_elem(int N, const int64_t* dims, const double* X, int n, int64_t i, int64_t j) {
+/* The dense tensor is read through this one accessor: fp64 storage, or fp32 storage (xf32 != 0) whose
+ * element is converted to fp64 exactly on read -- the fp32 entry points (orc_run_f32) let the
+ * baseline run on a 32 GB fp32 tensor without an fp64 copy; the arithmetic is unchanged. */
+static double orc_x(const void* X, int xf32, int64_t off) {
+  return xf32 ? (double)((const float*)X)[off] : ((const double*)X)[off];
+}
+
+static double orc_unfold_elem(int N, const int64_t* dims, const void* X, int xf32, int n, int64_t i, int64_t j) {
   int64_t off = 0, stride = 1, rem = j;
   for (int k = 0; k < N; ++k) {
     int64_t ik;
@@ -117,18 +124,22 @@ static double orc_unfold_elem(int N, const int64_t* dims, const double* X, int n
     off += ik * stride;
     stride *= dims[k];
   }
-  return X[off];
+  return orc_x(X, xf32, off);
 }
 
 /* Alg. 5 TensorSamp: j_b from eq:map, then X_(n)(:, j_b).
  * out is I_n x B, column b contiguous (out[b*I_n + i]). */
-int orc_tensor_samp(int N, const int64_t* dims, const double* X, int n, int64_t B, const int32_t* idx, double* out) {
+static int orc_tensor_samp_x(int N, const int64_t* dims, const void* X, int xf32, int n, int64_t B,
+                             const int32_t* idx, double* out) {
   for (int64_t b = 0; b < B; ++b) {
     int64_t j = orc_linear_index(N, dims, n, idx + b * (N - 1));
     if (j < 0) return ORC_ERANGE;
-    for (int64_t i = 0; i < dims[n]; ++i) out[b * dims[n] + i] = orc_unfold_elem(N, dims, X, n, i, j);
+    for (int64_t i = 0; i < dims[n]; ++i) out[b * dims[n] + i] = orc_unfold_elem(N, dims, X, xf32, n, i, j);
   }
   return ORC_OK;
+}
+int orc_tensor_samp(int N, const int64_t* dims, const double* X, int n, int64_t B, const int32_t* idx, double* out) {
+  return orc_tensor_samp_x(N, dims, X, 0, n, B, idx, out);
 }
 
 /* Alg. 1 SKR: Z <- 1; for m != n: Z <- Z (*) A^(m)(idx(:,m), :).
@@ -431,9 +442,9 @@ int orc_sample(int N, const int64_t* dims, int n, int strategy, int64_t B, const
  * Outputs (any may be NULL): G (I_n x R), Gamma = scale * Z^T D Z (R x R), M = scale * X_F D Z.
  * pj[] are the per-row probabilities from orc_sample (block: p_S in every entry).
  * ---------------------------------------------------------------------------------- */
-int orc_gradient(int N, const int64_t* dims, int R, const double* X, const double* const* factors, int n,
-                 int strategy, int64_t B, int64_t B_eff, const int32_t* idx, const double* pj, double* G_out,
-                 double* Gamma_out, double* M_out) {
+static int orc_gradient_x(int N, const int64_t* dims, int R, const void* X, int xf32, const double* const* factors,
+                          int n, int strategy, int64_t B, int64_t B_eff, const int32_t* idx, const double* pj,
+                          double* G_out, double* Gamma_out, double* M_out) {
   int64_t In = dims[n];
   int64_t Jn = 1;
   for (int k = 0; k < N; ++k)
@@ -447,7 +458,7 @@ int orc_gradient(int N, const int64_t* dims, int R, const double* X, const doubl
     return ORC_ENOMEM;
   }
   int st = orc_skr(N, dims, R, factors, n, B_eff, idx, Z);
-  if (!st) st = orc_tensor_samp(N, dims, X, n, B_eff, idx, XF);
+  if (!st) st = orc_tensor_samp_x(N, dims, X, xf32, n, B_eff, idx, XF);
   if (st) {
     free(Z); free(XF); free(C1); free(C2);
     return st;
@@ -492,6 +503,12 @@ int orc_gradient(int N, const int64_t* dims, int R, const double* X, const doubl
   }
   free(Z); free(XF); free(C1); free(C2);
   return ORC_OK;
+}
+
+int orc_gradient(int N, const int64_t* dims, int R, const double* X, const double* const* factors, int n,
+                 int strategy, int64_t B, int64_t B_eff, const int32_t* idx, const double* pj, double* G_out,
+                 double* Gamma_out, double* M_out) {
+  return orc_gradient_x(N, dims, R, X, 0, factors, n, strategy, B, B_eff, idx, pj, G_out, Gamma_out, M_out);
 }
 
 /* Gamma^+ of a symmetric R x R matrix on its numerically full-rank pivot set: the symmetric sweep
@@ -623,10 +640,10 @@ int orc_random_mode(uint64_t seed, uint64_t iter, int N) {
  * fixed rule) are updated in place.  alpha: per-iteration array (fixed rule) or NULL ->
  * alpha0.  Workspace is allocated here.  modes_out (optional) records n per iteration.
  * ---------------------------------------------------------------------------------- */
-int orc_run(int N, const int64_t* dims, int R, const double* X, double* const* factors, double* const* S,
-            int strategy, int rule, int order, int64_t B, const int32_t* window, double alpha0,
-            const double* alpha, double eta, double bpar, double eps, uint64_t seed, uint64_t r0, int64_t iters,
-            int32_t* modes_out) {
+static int orc_run_x(int N, const int64_t* dims, int R, const void* X, int xf32, double* const* factors,
+                     double* const* S, int strategy, int rule, int order, int64_t B, const int32_t* window,
+                     double alpha0, const double* alpha, double eta, double bpar, double eps, uint64_t seed,
+                     uint64_t r0, int64_t iters, int32_t* modes_out) {
   if (N < 3 || N > 16 || R < 1 || B < 1) return ORC_EINVAL;
   uint64_t* q[16];
   uint64_t T[16];
@@ -659,7 +676,7 @@ int orc_run(int N, const int64_t* dims, int R, const double* X, double* const* f
     int64_t Beff = 0;
     st = orc_sample(N, dims, n, strategy, B, window, (const uint64_t* const*)q, T, seed, r, idx, w, pj, &Beff);
     if (st) break;
-    st = orc_gradient(N, dims, R, X, (const double* const*)factors, n, strategy, B, Beff, idx, pj, G, Gam, Mm);
+    st = orc_gradient_x(N, dims, R, X, xf32, (const double* const*)factors, n, strategy, B, Beff, idx, pj, G, Gam, Mm);
     if (st) break;
     if (rule == ORC_STEP_ADAPTIVE)
       orc_update_adaptive(dims[n], R, factors[n], S[n], G, eta, bpar, eps);
@@ -673,4 +690,22 @@ int orc_run(int N, const int64_t* dims, int R, const double* X, double* const* f
   for (int k = 0; k < N; ++k) free(q[k]);
   free(idx); free(w); free(pj); free(G); free(Gam); free(Mm);
   return st;
+}
+
+int orc_run(int N, const int64_t* dims, int R, const double* X, double* const* factors, double* const* S,
+            int strategy, int rule, int order, int64_t B, const int32_t* window, double alpha0,
+            const double* alpha, double eta, double bpar, double eps, uint64_t seed, uint64_t r0, int64_t iters,
+            int32_t* modes_out) {
+  return orc_run_x(N, dims, R, X, 0, factors, S, strategy, rule, order, B, window, alpha0, alpha, eta, bpar, eps, seed,
+                   r0, iters, modes_out);
+}
+
+/* orc_run on an fp32-stored tensor (each element converted to fp64 on read; factors, accumulators and
+ * every operation fp64 as in orc_run) */
+int orc_run_f32(int N, const int64_t* dims, int R, const float* X, double* const* factors, double* const* S,
+                int strategy, int rule, int order, int64_t B, const int32_t* window, double alpha0,
+                const double* alpha, double eta, double bpar, double eps, uint64_t seed, uint64_t r0, int64_t iters,
+                int32_t* modes_out) {
+  return orc_run_x(N, dims, R, X, 1, factors, S, strategy, rule, order, B, window, alpha0, alpha, eta, bpar, eps, seed,
+                   r0, iters, modes_out);
 }

@@ -21,9 +21,10 @@ RULES = {"fixed": 0, "adaptive": 1, "als": 2}
 ORDERS = {"cyclic": 0, "random": 1}
 FLAG_MODE_MAJOR, FLAG_NO_GRAPH, FLAG_EXTERNAL_COMM, FLAG_NO_FUSED, FLAG_NO_WIDE, FLAG_NO_TC, FLAG_FUSED_CU8 = \
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
+FLAG_NO_PERSIST = 0x80
 KERNEL_NAMES = ["k_sample", "k_gather", "k_update_table", "k_table", "k_reduce_partials", "nccl", "k_fit",
                 "k_sweep_fused", "k_gather_update", "k_zw_gamma", "k_gather_update_tc", "k_table_sample",
-                "k_update_wide", "k_scores_wide", "k_sample_wide"]
+                "k_update_wide", "k_scores_wide", "k_sample_wide", "k_sweep_wide"]
 STATUS = {0: "CP_OK", -1: "CP_EINVAL", -2: "CP_ERANGE", -3: "CP_EDEGENERATE", -4: "CP_ENOMEM", -5: "CP_ECUDA",
           -6: "CP_ENCCL", -7: "CP_ESTATE", -8: "CP_ENONFINITE"}
 
@@ -31,7 +32,8 @@ EXPORTS = ["cp_sgd_init", "cp_sgd_destroy", "cp_sgd_last_error", "cp_sgd_sample"
            "cp_fit", "cp_sgd_sync", "cp_sgd_steps_host", "cp_sgd_sweep_multi", "cp_sgd_step_phase", "cp_sgd_exchange_info",
            "cp_sgd_get_table", "cp_sgd_get_grad", "cp_sgd_get_accum", "cp_sgd_get_iter", "cp_sgd_set_iter",
            "cp_sgd_refresh_tables", "cp_sgd_get_launches", "cp_sgd_profile", "cp_sgd_profile_read",
-           "cp_sgd_version", "cp_sgd_batch_max", "cp_sgd_debug_timers", "cp_sgd_exchange_copy"]
+           "cp_sgd_version", "cp_sgd_batch_max", "cp_sgd_debug_timers", "cp_sgd_exchange_copy", "cp_sgd_trace_layout",
+           "cp_sgd_trace", "cp_sgd_trace_count", "cp_sgd_path"]
 
 
 class CPError(RuntimeError):
@@ -90,6 +92,10 @@ def load_library(path: str = LIB_PATH):
     L.cp_sgd_version.restype = C.c_char_p
     L.cp_sgd_debug_timers.argtypes = [P, P]
     L.cp_sgd_exchange_copy.argtypes = [P, i32, P, i32]
+    L.cp_sgd_trace_layout.argtypes = [P, P]
+    L.cp_sgd_trace.argtypes = [P, P, i64]
+    L.cp_sgd_trace_count.argtypes = [P, C.POINTER(C.c_int64)]
+    L.cp_sgd_path.argtypes = [P, C.POINTER(C.c_int32)]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype if name in ("cp_sgd_last_error", "cp_sgd_version") else C.c_int
     _lib = L
@@ -119,7 +125,7 @@ class CPSGD:
                  seed: int = 0, stream=None, world_rank: int = 0, world_size: int = 1, nccl_id: bytes = None,
                  slab=None, mode_major: bool = True, block_window=None, graphs: bool = True,
                  external_comm: bool = False, fused: bool = True, wide: bool = True,
-                 tc: bool = True, fused_cluster: int = 16):
+                 tc: bool = True, fused_cluster: int = 16, persist: bool = True):
         import torch
 
         L = load_library()
@@ -145,7 +151,7 @@ class CPSGD:
         flags = (FLAG_MODE_MAJOR if mode_major else 0) | (0 if graphs else FLAG_NO_GRAPH) | \
                 (FLAG_EXTERNAL_COMM if external_comm else 0) | (0 if fused else FLAG_NO_FUSED) | \
                 (0 if wide else FLAG_NO_WIDE) | (0 if tc else FLAG_NO_TC) | \
-                (FLAG_FUSED_CU8 if fused_cluster == 8 else 0)
+                (FLAG_FUSED_CU8 if fused_cluster == 8 else 0) | (0 if persist else FLAG_NO_PERSIST)
         lo, hi = (0, self.dims[-1]) if slab is None else (int(slab[0]), int(slab[1]))
         cfg = Config(self.N, self._dims_arr, self.R, self.dtype, X.data_ptr(), self._fac_arr, int(batch),
                      self._win_arr, SAMPLERS[sampler], RULES[rule], float(alpha), float(eta), float(b), float(eps),
@@ -294,6 +300,51 @@ class CPSGD:
         n = C.c_uint64(0)
         self._chk(self._L.cp_sgd_get_launches(self._h, C.byref(n)))
         return int(n.value)
+
+    @property
+    def path(self) -> str:
+        """'fused' (k_sweep_fused), 'persistent' (k_sweep_wide) or 'chain' (kernel chain / graph)"""
+        v = C.c_int32(0)
+        self._chk(self._L.cp_sgd_path(self._h, C.byref(v)))
+        return {1: "fused", 2: "persistent"}.get(v.value, "chain")
+
+    def trace_start(self, cap: int):
+        """record the batches (and resulting factor / accumulator / table of the updated mode) of the
+        next `cap` SGD iterations run by a persistent kernel; read them with trace_read()"""
+        import torch
+
+        lay = (C.c_int64 * 7)()
+        self._chk(self._L.cp_sgd_trace_layout(self._h, lay))
+        self._trace_layout = list(lay)
+        self._trace_buf = torch.zeros(int(cap) * lay[0], dtype=torch.uint8, device=self._X.device)
+        torch.cuda.synchronize(self._X.device)
+        self._chk(self._L.cp_sgd_trace(self._h, C.c_void_p(self._trace_buf.data_ptr()), int(cap)))
+
+    def trace_read(self):
+        """list of per-iteration dicts {n, r, beff, idx, w, A, S, cdf} (numpy, host)"""
+        self.sync()
+        cnt = C.c_int64(0)
+        self._chk(self._L.cp_sgd_trace_count(self._h, C.byref(cnt)))
+        stride, o_idx, o_w, o_A, o_S, o_cdf, o_meta = self._trace_layout
+        raw = self._trace_buf.cpu().numpy()
+        dt = np.float64 if self.dtype == 1 else np.float32
+        bm = max(self.batch_max(k) for k in range(self.N))
+        out = []
+        for s in range(cnt.value):
+            rec = raw[s * stride:(s + 1) * stride]
+            meta = rec[o_meta:o_meta + 32].view(np.int64)
+            n, r, beff = int(meta[0]), int(meta[1]), int(meta[2])
+            I = self.dims[n]
+            out.append(dict(n=n, r=r, beff=beff,
+                            idx=rec[o_idx:o_idx + 4 * bm * (self.N - 1)].view(np.int32).reshape(bm, self.N - 1)[:beff].copy(),
+                            w=rec[o_w:o_w + 8 * bm].view(np.float64)[:beff].copy(),
+                            A=rec[o_A:o_A + I * self.R * np.dtype(dt).itemsize].view(dt).reshape(I, self.R).copy(),
+                            S=rec[o_S:o_S + I * self.R * np.dtype(dt).itemsize].view(dt).reshape(I, self.R).copy(),
+                            cdf=rec[o_cdf:o_cdf + 8 * I].view(np.uint64).copy()))
+        return out
+
+    def trace_stop(self):
+        self._chk(self._L.cp_sgd_trace(self._h, None, 0))
 
     def debug_timers(self):
         out = (C.c_longlong * 4096)()

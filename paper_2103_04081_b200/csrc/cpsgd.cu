@@ -24,6 +24,7 @@
 #include "gupdate.cuh"
 #include "gupdate_tc.cuh"
 #include "wide.cuh"
+#include "sweep_wide.cuh"
 #include "kernels.cuh"
 
 using namespace cps;
@@ -79,7 +80,7 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
-enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kKGatherUpdate, kKZwGamma, kKGatherUpdateTC, kKTableSample, kKUpdateWide, kKScoresWide, kKSampleWide, kNumKernelIds };
+enum KernelId { kKSample = 0, kKGather, kKUpdate, kKTable, kKReduce, kKComm, kKFit, kKFused, kKGatherUpdate, kKZwGamma, kKGatherUpdateTC, kKTableSample, kKUpdateWide, kKScoresWide, kKSampleWide, kKSweepWide, kNumKernelIds };
 
 struct ProfRec {
   int id;
@@ -179,6 +180,21 @@ struct cp_sgd_s {
   void* sw_gcl = nullptr;        // wide path: k_sample_wide cluster partials of Gamma
   bool use_tc = false;           // fp32 wide path on tcgen05 (k_gather_update_tc), else the FFMA mainloop
   float* zimg = nullptr;         // tcgen05 path: {zh; zl} A-operand images of the prefetched batch
+  // persistent cooperative sweep kernel of the fp32 wide path (k_sweep_wide, sweep_wide.cuh)
+  bool pw_ok = false;
+  int pw_grid = 0;
+  size_t pw_smem = 0;
+  uint32_t pw_tag = 0;           // look-back tags: iteration s of a launch uses pw_tag + 1 + s
+  float* pw_gcl = nullptr;       // [grid][R][R] per-CTA partials of Gamma
+  double* pw_gram = nullptr;     // [R(R+1)/2]
+  unsigned long long* pw_agg = nullptr;  // [row units]
+  unsigned* pw_aggf = nullptr;   // [row units][2]
+  unsigned* pw_bar = nullptr;    // [0] barrier arrivals, [32] pair-sum arrivals (zeroed per launch)
+  double* pw_alphas = nullptr;   // per-iteration steps of one call (fixed rule schedules)
+  int64_t pw_alphas_cap = 0;
+  // cp_sgd_trace: the consumed batches of the persistent kernels
+  unsigned char* trace_base = nullptr;
+  int64_t trace_cap = 0, trace_count = 0;
   int fused_cu = 0, fused_bpc = 0, fused_rpc = 0;  // fused kernel geometry (0: not eligible)
   size_t fused_smem = 0;
   int pref_mode = -1;            // mode whose batch (at the current r) sits in idx/w/zrow/fbase
@@ -833,6 +849,8 @@ cp_status launch_prefetch(cp_sgd_s* h, int n) {
   return launch_sample(h, n, h->iter_dev, h->idx, h->w, h->beff, true);
 }
 
+TraceParams trace_params(cp_sgd_s* h, int nsteps);
+
 // ---- persistent single-cluster sweep kernel (fused.cuh) ----------------------------------------
 template <typename T>
 void fill_fused_params(cp_sgd_s* h, FusedParams<T>& p, int nsteps, int first_mode, int order, double alpha,
@@ -885,6 +903,7 @@ void fill_fused_params(cp_sgd_s* h, FusedParams<T>& p, int nsteps, int first_mod
   int64_t imax = 0;
   for (int k = 0; k < h->N; ++k) imax = std::max(imax, h->dims[k]);
   p.Imax = imax;
+  p.tr = trace_params(h, nsteps);
   p.dbg = h->dbg;
 }
 
@@ -1014,6 +1033,189 @@ void plan_fused(cp_sgd_s* h) {
   h->fused_bpc = bpc;
   h->fused_rpc = rpc;
   h->fused_smem = L.total;
+}
+
+// ---- cp_sgd_trace record layout ------------------------------------------------------------------
+struct TraceLayout {
+  int64_t stride, o_idx, o_w, o_A, o_S, o_cdf, o_meta;
+};
+TraceLayout trace_layout(const cp_sgd_s* h) {
+  int64_t bm = 0, im = 0;
+  for (int k = 0; k < h->N; ++k) {
+    bm = std::max(bm, h->bmax[k]);
+    im = std::max(im, h->dims[k]);
+  }
+  TraceLayout L;
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) {
+    off = (off + 15) / 16 * 16;
+    const int64_t at = off;
+    off += bytes;
+    return at;
+  };
+  L.o_idx = take(4 * bm * (h->N - 1));
+  L.o_w = take(8 * bm);
+  L.o_A = take((int64_t)h->esz * im * h->R);
+  L.o_S = take((int64_t)h->esz * im * h->R);
+  L.o_cdf = take(8 * im);
+  L.o_meta = take(8 * 4);
+  L.stride = (off + 255) / 256 * 256;
+  return L;
+}
+TraceParams trace_params(cp_sgd_s* h, int nsteps) {
+  TraceParams t;
+  memset(&t, 0, sizeof t);
+  if (!h->trace_base) return t;
+  const TraceLayout L = trace_layout(h);
+  t.base = h->trace_base;
+  t.stride = L.stride;
+  t.o_idx = L.o_idx;
+  t.o_w = L.o_w;
+  t.o_A = L.o_A;
+  t.o_S = L.o_S;
+  t.o_cdf = L.o_cdf;
+  t.o_meta = L.o_meta;
+  t.first = h->trace_count;
+  t.cap = h->trace_cap;
+  h->trace_count = std::min<int64_t>(h->trace_cap, h->trace_count + nsteps);
+  return t;
+}
+
+// ---- persistent cooperative sweep kernel of the fp32 wide path (sweep_wide.cuh) -------------------
+using PWKernel = void (*)(PWParams);
+PWKernel pw_kernel(int R) {
+  return R <= 16 ? k_sweep_wide<16> : R <= 32 ? k_sweep_wide<32> : R <= 56 ? k_sweep_wide<56> : k_sweep_wide<64>;
+}
+
+// eligible: one GPU, fp32 on the tcgen05 gather for every mode, gradient rules (the sampled-ALS rule
+// stays on the kernel chain), cooperative launch supported, one 448-thread CTA per SM co-resident
+bool plan_pw(cp_sgd_s* h) {
+  h->pw_ok = false;
+  if (h->world_size != 1 || h->dtype != CP_F32 || !h->use_tc || h->rule == CP_STEP_ALS ||
+      (h->flags & CP_FLAG_NO_PERSIST))
+    return true;
+  int64_t kbmax = 0, cdfmax = 0, units = 0;
+  for (int n = 0; n < h->N; ++n) {
+    if (!wide_mode(h, n)) return true;
+    if (!(h->Xmm[n] || (n == 0 && h->dims[0] % 4 == 0))) return true;
+    kbmax = std::max(kbmax, h->gu_kb[n]);
+    cdfmax = std::max(cdfmax, ts_cdf_elems(h, n));
+    units = std::max<int64_t>(units, pw_units_rows(h->dims[n]));
+  }
+  int coop = 0, sms = 0, optin = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+  if (!coop || sms < 1) return true;
+  const size_t smem = pw_smem_bytes(h->N, h->R, kbmax, cdfmax);
+  if (smem + 1024 > (size_t)optin) return true;
+  allow_max_dyn_smem(pw_kernel(h->R));
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pw_kernel(h->R), kPWThreads, smem) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    return true;
+  }
+  h->pw_grid = sms;  // one CTA per SM
+  h->pw_smem = smem;
+  const int P = h->R * (h->R + 1) / 2;
+  auto alloc = [&](void** ptr, size_t bytes) {
+    if (cudaMalloc(ptr, bytes) != cudaSuccess) return false;
+    cudaMemsetAsync(*ptr, 0, bytes, h->stream);
+    return true;
+  };
+  if (!alloc((void**)&h->pw_gcl, sizeof(float) * (size_t)h->pw_grid * h->R * h->R) ||
+      !alloc((void**)&h->pw_gram, sizeof(double) * P) ||
+      !alloc((void**)&h->pw_agg, sizeof(unsigned long long) * units) ||
+      !alloc((void**)&h->pw_aggf, sizeof(unsigned) * 2 * units) ||
+      !alloc((void**)&h->pw_bar, sizeof(unsigned) * 64)) {
+    cudaGetLastError();
+    return false;
+  }
+  h->pw_ok = true;
+  return true;
+}
+
+cp_status launch_pw(cp_sgd_s* h, int nsteps, int first_mode, int order, double alpha, const double* alpha_dev,
+                    const double* alphas_dev) {
+  ProfScope ps(h, kKSweepWide);
+  PWParams p;
+  memset(&p, 0, sizeof p);
+  p.N = h->N;
+  p.R = h->R;
+  p.strategy = h->sampler;
+  p.rule = h->rule;
+  p.nsteps = nsteps;
+  p.first_mode = first_mode;
+  p.order = order;
+  p.B = h->B;
+  for (int k = 0; k < h->N; ++k) {
+    p.dims[k] = h->dims[k];
+    p.lstride[k] = h->lstride[k];
+    p.Xg[k] = h->Xmm[k] ? (const float*)h->Xmm[k] : (const float*)h->X;
+    p.rowlen[k] = h->Xmm[k] ? h->pitch[k] : h->dims[k];
+    p.pitch[k] = h->Xmm[k] ? h->pitch[k] : 0;
+    p.factors[k] = (float*)h->factors[k];
+    p.S[k] = (float*)h->S[k];
+    p.cdf[k] = h->cdf[k];
+    p.pprob[k] = h->pprob[k];
+    for (int j = 0; j < h->N - 1; ++j) p.window[k][j] = h->window[k][j];
+    p.bmax[k] = h->bmax[k];
+    p.CK[k] = h->gu_ck[k];
+    p.KB[k] = h->gu_kb[k];
+  }
+  p.Ttot = h->Ttot;
+  p.seed = h->seed;
+  p.iter = h->iter_dev;
+  p.status = h->status_dev;
+  p.last_mode = h->last_mode_dev;
+  p.alpha = alpha;
+  p.alpha_dev = alpha_dev;
+  p.alphas = alphas_dev;
+  p.eta = h->eta;
+  p.b = h->bpar;
+  p.eps = h->eps;
+  p.idx = h->idx;
+  p.w = h->w;
+  p.fbase = h->fbase;
+  p.beff = h->beff;
+  p.zimg = h->zimg;
+  p.gcl = h->pw_gcl;
+  p.gam = (float*)h->gam_next;
+  p.Mpart = (float*)h->Mpart;
+  p.gpart = h->uw_gpart;
+  p.gram = h->pw_gram;
+  p.rownorm = h->uw_rownorm;
+  p.agg = h->pw_agg;
+  p.aggf = h->pw_aggf;
+  p.bar = h->pw_bar;
+  p.pcnt = h->pw_bar + 32;  // another 128-byte line
+  p.tag0 = h->pw_tag + 1;
+  p.Gout = (float*)h->Gout;
+  p.Gam_out = (float*)h->Gam_out;
+  p.tr = trace_params(h, nsteps);
+  p.dbg = h->dbg;
+  h->pw_tag += (uint32_t)nsteps;
+  static DevOnce attr_once[4];
+  if (attr_once[h->R <= 16 ? 0 : h->R <= 32 ? 1 : h->R <= 56 ? 2 : 3].first(h->device)) allow_max_dyn_smem(pw_kernel(h->R));
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)h->pw_grid, 1, 1);
+  lc.blockDim = dim3(kPWThreads, 1, 1);
+  lc.dynamicSmemBytes = h->pw_smem;
+  lc.stream = h->ls;
+  cudaLaunchAttribute at[1];
+  // every CTA waits for the others (grid barriers, look-back): the launch must be co-resident
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = getenv("CPSGD_PW_NONCOOP") ? 0 : 1;  // profilers that cannot replay cooperative launches
+  CUDA_TRY(h, cudaMemsetAsync(h->pw_bar, 0, sizeof(unsigned) * 64, h->ls));
+  cudaError_t e = cudaLaunchKernelEx(&lc, pw_kernel(h->R), p);
+  h->launches++;
+  h->pref_mode = -1;
+  if (e != cudaSuccess)
+    return h->fail(CP_ECUDA, "k_sweep_wide launch (grid %d, smem %zu): %s", h->pw_grid, h->pw_smem, cudaGetErrorString(e));
+  return check_launch(h, "k_sweep_wide");
 }
 
 // ---- one step, by phases ------------------------------------------------------------------------
@@ -1447,6 +1649,8 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
     }
   }
 #undef ALLOC
+  // ---- persistent cooperative sweep kernel of the fp32 wide path ----
+  if (!plan_pw(h)) return init_fail(h, h->fail(CP_ENOMEM, "persistent sweep kernel workspace"));
   // ---- NCCL communicator ----
   if (h->world_size > 1) {
     auto* rr = rr_store(h, true);
@@ -1544,6 +1748,12 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->fit_partial);
   if (h->pinned) cudaFreeHost(h->pinned);
   for (auto e : h->ev_pool) cudaEventDestroy(e);
+  cudaFree(h->pw_gcl);
+  cudaFree(h->pw_gram);
+  cudaFree(h->pw_agg);
+  cudaFree(h->pw_aggf);
+  cudaFree(h->pw_bar);
+  cudaFree(h->pw_alphas);
   if (h->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm);
   cudaGetLastError();
   delete h;
@@ -1624,8 +1834,9 @@ cp_status cp_sgd_step(cp_sgd_t h, int32_t mode, double alpha) {
   if (st) return st;
   if (sharded(h) && (h->flags & CP_FLAG_EXTERNAL_COMM))
     return h->fail(CP_ESTATE, "external-comm handles must use cp_sgd_step_phase");
-  if (h->fused_cu) {
-    st = launch_fused(h, 1, mode, 0, (alpha < 0.0) ? h->alpha : alpha, nullptr);
+  if (h->fused_cu || h->pw_ok) {
+    const double a = (alpha < 0.0) ? h->alpha : alpha;
+    st = h->fused_cu ? launch_fused(h, 1, mode, 0, a, nullptr) : launch_pw(h, 1, mode, 0, a, nullptr, nullptr);
     if (st) return st;
     h->iter_host++;
     h->last_mode = mode;
@@ -1698,6 +1909,29 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
     if (nsweeps == 0) return CP_OK;
     const int64_t nst = (int64_t)nsweeps * h->N;
     cp_status st = launch_fused(h, (int)nst, 0, order, h->alpha, nullptr);
+    if (st) return st;
+    const uint64_t r_last = h->iter_host + nst - 1;
+    h->last_mode = order == CP_ORDER_CYCLIC ? h->N - 1 : random_mode(h->seed, r_last, h->N);
+    h->iter_host += nst;
+    return CP_OK;
+  }
+  if (h->pw_ok) {  // one cooperative persistent launch for the whole call
+    if (nsweeps == 0) return CP_OK;
+    const int64_t nst = (int64_t)nsweeps * h->N;
+    const double* al = nullptr;
+    if (alpha_per_iter) {
+      if (h->pw_alphas_cap < nst) {
+        cudaFree(h->pw_alphas);
+        h->pw_alphas = nullptr;
+        h->pw_alphas_cap = 0;
+        CUDA_TRY(h, cudaMalloc(&h->pw_alphas, sizeof(double) * nst));
+        h->pw_alphas_cap = nst;
+      }
+      CUDA_TRY(h, cudaStreamSynchronize(h->stream));  // the previous call's schedule is no longer read
+      CUDA_TRY(h, cudaMemcpy(h->pw_alphas, alpha_per_iter, sizeof(double) * nst, cudaMemcpyHostToDevice));
+      al = h->pw_alphas;
+    }
+    cp_status st = launch_pw(h, (int)nst, 0, order, h->alpha, nullptr, al);
     if (st) return st;
     const uint64_t r_last = h->iter_host + nst - 1;
     h->last_mode = order == CP_ORDER_CYCLIC ? h->N - 1 : random_mode(h->seed, r_last, h->N);
@@ -2019,6 +2253,42 @@ cp_status cp_sgd_profile_read(cp_sgd_t h, int32_t cap, int32_t* ids, double* tot
   }
   if (n_out) *n_out = m;
   cudaGetLastError();
+  return CP_OK;
+}
+
+cp_status cp_sgd_trace_layout(cp_sgd_t h, int64_t* out7) {
+  if (!h || !out7) return CP_EINVAL;
+  const TraceLayout L = trace_layout(h);
+  out7[0] = L.stride;
+  out7[1] = L.o_idx;
+  out7[2] = L.o_w;
+  out7[3] = L.o_A;
+  out7[4] = L.o_S;
+  out7[5] = L.o_cdf;
+  out7[6] = L.o_meta;
+  return CP_OK;
+}
+
+cp_status cp_sgd_trace(cp_sgd_t h, void* buf_dev, int64_t cap) {
+  if (!h) return CP_EINVAL;
+  if (buf_dev && cap < 1) return h->fail(CP_EINVAL, "trace capacity < 1");
+  cp_status st = cp_sgd_sync(h);  // earlier launches keep their (old) trace pointers
+  if (st) return st;
+  h->trace_base = (unsigned char*)buf_dev;
+  h->trace_cap = buf_dev ? cap : 0;
+  h->trace_count = 0;
+  return CP_OK;
+}
+
+cp_status cp_sgd_trace_count(cp_sgd_t h, int64_t* n_host) {
+  if (!h || !n_host) return CP_EINVAL;
+  *n_host = h->trace_count;
+  return CP_OK;
+}
+
+cp_status cp_sgd_path(cp_sgd_t h, int32_t* path_host) {
+  if (!h || !path_host) return CP_EINVAL;
+  *path_host = h->fused_cu ? 1 : (h->pw_ok ? 2 : 0);
   return CP_OK;
 }
 

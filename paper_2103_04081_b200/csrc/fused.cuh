@@ -50,6 +50,7 @@ struct FusedParams {
   int BPC;                         // fibers per CTA (max over modes)
   int RPC;                         // factor rows per CTA (max over modes)
   int64_t Imax;
+  TraceParams tr;                  // cp_sgd_trace (debug): consumed batches and resulting states
   long long* dbg;
 };
 
@@ -491,6 +492,7 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
           prow[il] = rs;
           a2 += rs;
         }
+        __syncwarp();  // reconverge: a diverged warp takes the slow collective shuffle path
         for (int o = 16; o > 0; o >>= 1) a2 += __shfl_down_sync(0xffffffffu, a2, o);
         if (lane == 0) s_red[wid] = a2;
         __syncthreads();
@@ -522,6 +524,7 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
             d0 = fmax(d0, d);
             fin = fin && (d == d) && d < 1.7e308;
           }
+          __syncwarp();  // reconverge: a diverged warp takes the slow collective shuffle path
           for (int o = 16; o > 0; o >>= 1) d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
           if (!__all_sync(0xffffffffu, fin) && lane == 0) s_bad |= 8;
           if (lane == 0) s_red[0] = (double)(In > R ? In : R) * 2.220446049250313e-16 * d0;
@@ -572,6 +575,7 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
         p.pprob[n][r_beg + tid] = pv;
       }
       unsigned long long incl = qv;
+      __syncwarp();  // reconverge: a diverged warp takes the slow collective shuffle path
       for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += v;
@@ -685,6 +689,26 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
       if (p.rule == 1) cp_async_small<sizeof(T)>(Sold + il * RS + c, p.S[n] + (r_beg + il) * R + c, sizeof(T));
     }
     cp_async_commit();
+    const bool trace = p.tr.base && p.tr.first + s < p.tr.cap;
+    unsigned char* tb = trace ? p.tr.base + (p.tr.first + s) * p.tr.stride : nullptr;
+    if (trace) {  // the batch this step consumes: this CTA's fibers (debug trace)
+      int32_t* ti = reinterpret_cast<int32_t*>(tb + p.tr.o_idx);
+      double* tw = reinterpret_cast<double*>(tb + p.tr.o_w);
+      const int64_t bm = p.bmax[n], b0 = (int64_t)q * p.BPC;
+      for (int e = tid; e < p.BPC * NP; e += kFThreads) {
+        const int64_t b = b0 + e / NP;
+        if (b < bm) ti[b * NP + e % NP] = b < s_beff ? ix[e] : 0;
+      }
+      for (int lb = tid; lb < p.BPC; lb += kFThreads)
+        if (b0 + lb < bm) tw[b0 + lb] = wt[lb];
+      if (q == 0 && tid == 0) {
+        int64_t* tm = reinterpret_cast<int64_t*>(tb + p.tr.o_meta);
+        tm[0] = n;
+        tm[1] = (int64_t)r;
+        tm[2] = s_beff;
+        tm[3] = 0;
+      }
+    }
     const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
     gather_dispatch<T, ROWS>(xs, Ip, In, fb, zw, RP, p.BPC, Mp, R,
                              (p.dbg && q == 0 && tid == 0 && s == 1) ? p.dbg : nullptr);
@@ -735,6 +759,7 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
       if (wid == 0) {
         double d0 = 0.0;
         for (int j = lane; j < R; j += 32) d0 = fmax(d0, Gm[j * RS + j]);
+        __syncwarp();  // reconverge: a diverged warp takes the slow collective shuffle path
         for (int o = 16; o > 0; o >>= 1) d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
         if (lane == 0) s_tol_als = (double)R * 2.220446049250313e-16 * d0;
       }
@@ -785,6 +810,17 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
     F_MARK(3);
     // ------------------------------------------------ (3) importance table of the new A^(n)
     build_table(n, In, rpc, r_beg, nr, s);
+    if (trace) {  // this CTA's rows of the updated factor, accumulator and CDF (debug trace)
+      __syncthreads();
+      T* tA = reinterpret_cast<T*>(tb + p.tr.o_A);
+      T* tS = reinterpret_cast<T*>(tb + p.tr.o_S);
+      uint64_t* tc = reinterpret_cast<uint64_t*>(tb + p.tr.o_cdf);
+      for (int e = tid; e < nr * R; e += kFThreads) {
+        tA[r_beg * R + e] = Anew[(e / R) * RS + e % R];
+        if (p.rule == 1) tS[r_beg * R + e] = p.S[n][r_beg * R + e];
+      }
+      for (int il = tid; il < nr; il += kFThreads) tc[r_beg + il] = p.cdf[n][r_beg + il];
+    }
     ++r;
     n_done = n;
     const int n_next = mode_of(r, s + 1);

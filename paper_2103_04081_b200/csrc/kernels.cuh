@@ -57,6 +57,16 @@ struct SampleParams {
   float* zimg;                     // tcgen05 path: 3xTF32 A-operand images of zw (or NULL)
 };
 
+// debug trace of the consumed batches and the states they lead to (cp_sgd_trace; persistent kernels
+// k_sweep_wide and k_sweep_fused): per SGD iteration s of a launch, slot first + s (< cap) holds idx
+// [bmax][N-1], w [bmax], the updated A^(n) [I_n][R], S^(n) [I_n][R] (adaptive rule), the new CDF of
+// mode n [I_n] and meta {n, r, B_eff, 0}
+struct TraceParams {
+  unsigned char* base;
+  int64_t stride, o_idx, o_w, o_A, o_S, o_cdf, o_meta;
+  int64_t first, cap;
+};
+
 // byte offset of zh_r (part 0) / zl_r (part 1) of fiber b in the tcgen05 A-operand images
 // (gupdate_tc.cuh): per stage of 32 fibers one 128-row x 128-byte tile (rows 0-63 zh, 64-127 zl),
 // K-major with the 128-byte swizzle (16-byte chunk c of row m at chunk c ^ (m & 7))
@@ -335,6 +345,7 @@ __global__ void __launch_bounds__(kTableThreads) k_table(const T* __restrict__ A
   // block exclusive scan of the per-thread totals (integers: order-independent, exact)
   const int lane = tid & 31, wid = tid >> 5;
   unsigned long long incl = local;
+  __syncwarp();  // reconverge: a diverged warp takes the slow collective shuffle path
   for (int o = 1; o < 32; o <<= 1) {
     unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
@@ -343,6 +354,7 @@ __global__ void __launch_bounds__(kTableThreads) k_table(const T* __restrict__ A
   __syncthreads();
   if (wid == 0) {
     unsigned long long v = warp_tot[lane];
+    __syncwarp();  // reconverge: a diverged warp takes the slow collective shuffle path
     for (int o = 1; o < 32; o <<= 1) {
       unsigned long long u = __shfl_up_sync(0xffffffffu, v, o);
       if (lane >= o) v += u;
@@ -1305,6 +1317,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
       acc += rs;
     }
     // fixed-order block reduction
+    __syncwarp();  // reconverge: a diverged warp takes the slow collective shuffle path
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
     if ((tid & 31) == 0) s_red[tid >> 5] = acc;
     __syncthreads();
@@ -1453,6 +1466,7 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   if (bad) atomicOr(&s_bad, 8);
   const int lane = tid & 31, wid = tid >> 5;
   unsigned long long incl = local;
+  __syncwarp();  // reconverge: a diverged warp takes the slow collective shuffle path
   for (int o = 1; o < 32; o <<= 1) {
     const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;

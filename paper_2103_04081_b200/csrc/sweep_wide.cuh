@@ -1,0 +1,1162 @@
+// sweep_wide.cuh -- k_sweep_wide: the fp32 single-GPU wide path (C4-sized problems, every mode on the
+// tcgen05 gather) as ONE cooperative persistent launch per cp_sgd_sweep / cp_sgd_step call.
+//
+// One CTA per SM (448 threads, the tcgen05 gather's shared-memory ring), all co-resident (cooperative
+// launch).  Per SGD iteration r on mode n (Alg. 6 / Alg. 7):
+//
+//   S  (a2-a4)  the batch of mode n at r: 32-fiber units over the CTAs -- Philox draws from the
+//               staged integer CDFs (eq:ik / eq:bik, contract DESIGN.md section 4), exact fp64
+//               weights (eq:gradient1/2), fiber offsets, SKR rows (Alg. 1), the {zh; zl} 3xTF32
+//               A-operand images, and per-CTA partials of Gamma = Z_F^T diag(w) Z_F (unit order)
+//   -- grid barrier --
+//   G  (a5, a6) TensorSamp (Alg. 5) + M = X_F diag(w) Z_F: (I-tile, batch chunk) items of the
+//               warp-specialised tcgen05 mainloop (gupdate_tc.cuh), split-K partial tiles to the
+//               workspace; idle lanes sum Gamma over the CTA partials (CTA order)
+//   -- grid barrier --
+//   U  (a6-a8)  16-row units: M = sum of the chunk partials (chunk order), G = A Gamma - M, fixed /
+//               adaptive update (eq:proposed, eq:etaada/eq:Aada); fp64 Gram partials (leverage) or
+//               row norms (Euclidean) of the new rows (a1)
+//   -- grid barrier --
+//   P  (a1)     leverage: the Gram's pairs summed over the unit partials (unit order), a slice per CTA;
+//               an arrival counter (no grid barrier: only the inverse waits for it)
+//   I  (a1)     every CTA with row units waits for the Gram and inverts it redundantly (natural-order
+//               symmetric sweep on the numerically full-rank pivot set, R4(b)) -- the R-pivot chain
+//               is serial; computing it everywhere saves the publish / poll round trip
+//   Q  (a1)     scores of the unit's rows (a^T W a / |S| or ||a||^2 / ||A||_F^2), 2^-32 fixed-point
+//               quantisation, unit aggregates published with a tag, decoupled look-back over the
+//               preceding units' aggregates -> CDF rows; the last unit writes T and the status
+//   -- grid barrier --  (the table of the new A^(n) is complete: R9)
+//
+// Deterministic: every sum has a fixed order (unit / chunk / CTA order), so results do not depend on
+// scheduling.  Citations: PAPER.md:<lines> (<label>); R<k> = DESIGN.md readings.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "gupdate_tc.cuh"
+#include "wide.cuh"
+
+namespace cps {
+
+constexpr int kPWThreads = kTCThreads;  // 448: the tcgen05 gather's warp roles
+constexpr int kPWFib = 32;              // fibers per sampling unit (one tcgen05 stage)
+constexpr int kPWRows = 16;             // rows per update / table unit
+
+struct PWParams {
+  int N, R, strategy, rule;
+  int nsteps, first_mode, order;
+  int64_t B;
+  int64_t dims[kMaxOrder], lstride[kMaxOrder];
+  const float* Xg[kMaxOrder];      // gather base of mode n: mode-major copy (n >= 1) or X (mode 0)
+  int64_t rowlen[kMaxOrder];       // readable elements per fiber row (pitch, or I_0)
+  int64_t pitch[kMaxOrder];        // 0: native (mode 0)
+  float* factors[kMaxOrder];
+  float* S[kMaxOrder];
+  uint64_t* cdf[kMaxOrder];
+  double* pprob[kMaxOrder];
+  uint64_t* Ttot;
+  int32_t window[kMaxOrder][kMaxOrder];
+  int64_t bmax[kMaxOrder];
+  int CK[kMaxOrder];
+  int64_t KB[kMaxOrder];
+  uint64_t seed;
+  uint64_t* iter;
+  int* status;
+  int* last_mode;
+  double alpha, eta, b, eps;
+  const double* alpha_dev;         // constant step on the device (graph-free replays), or NULL
+  const double* alphas;            // per-iteration steps (fixed rule), or NULL
+  // workspace
+  int32_t* idx;
+  double* w;
+  int64_t* fbase;
+  int64_t* beff;
+  float* zimg;
+  float* gcl;                      // [G][R][R] per-CTA partials of Gamma
+  float* gam;                      // [R][R]
+  float* Mpart;                    // [tiles][CK][R][128]
+  double* gpart;                   // [row units][P] (leverage) or [row units] (Euclidean)
+  double* gram;                    // [P] the Gram's pairs
+  double* rownorm;                 // [I_max]
+  unsigned long long* agg;         // [row units] q sums
+  unsigned* aggf;                  // [row units][2]: {bad bits, tag}
+  unsigned* bar;                   // grid-barrier arrivals (zero at launch)
+  unsigned* pcnt;                  // pair-sum arrivals (zero at launch)
+  uint32_t tag0;                   // tag of iteration 0 of this launch (unique per handle)
+  float* Gout;
+  float* Gam_out;
+  TraceParams tr;
+  long long* dbg;
+};
+
+// ------------------------------------------------------------------------------------------ sync
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// grid-wide barrier of the co-resident grid: a monotonic arrival counter (zeroed by the host before
+// every launch), one fire-and-forget release reduction per CTA, one polling thread per CTA with a
+// short back-off.  (Polling flags with every thread of every CTA made the flag lines an L2 hot spot
+// that slowed every other load of the launch; so did polling without back-off.)
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
+  while ((int)(ld_acquire_u32(p) - target) < 0) __nanosleep(40);
+}
+__device__ __forceinline__ void grid_barrier(unsigned* cnt, unsigned& nbar) {
+  __syncthreads();
+  ++nbar;
+  if (threadIdx.x == 0) {
+    red_release_add(cnt, 1u);
+    wait_count(cnt, nbar * gridDim.x);
+  }
+  __syncthreads();
+  __syncwarp();  // warp 0 reconverged after its single-thread branch
+}
+
+// global -> shared copy of `bytes` contiguous bytes (src and dst 16-byte aligned) in 16-byte L2-only
+// cp.async chunks, all in flight (one commit group; the caller waits): data written by other CTAs of
+// this launch must not be read through L1
+__device__ __forceinline__ void cpcg_bytes(void* dst, const void* src, int64_t bytes, int tid, int nth) {
+  unsigned char* d = reinterpret_cast<unsigned char*>(dst);
+  const unsigned char* s8 = reinterpret_cast<const unsigned char*>(src);
+  for (int64_t o = (int64_t)tid * 16; o < bytes; o += (int64_t)nth * 16)
+    cp_async16(d + o, s8 + o, (int)cmin64(16, bytes - o));
+  cp_async_commit();
+}
+
+// global -> shared copy through L2 (data written by other CTAs of this launch): 8 loads in flight
+// per thread
+__device__ __forceinline__ void ldcg_copy_u64(uint64_t* dst, const uint64_t* src, int64_t n, int tid, int nth) {
+  for (int64_t i0 = tid; i0 < n; i0 += 8 * (int64_t)nth) {
+    uint64_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + (int64_t)u * nth;
+      v[u] = i < n ? __ldcg(src + i) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + (int64_t)u * nth;
+      if (i < n) dst[i] = v[u];
+    }
+  }
+}
+
+__host__ __device__ inline int pw_units_rows(int64_t In) { return (int)((In + kPWRows - 1) / kPWRows); }
+__host__ __device__ inline int pw_units_fib(int64_t bmax) { return (int)((bmax + kPWFib - 1) / kPWFib); }
+
+// dynamic shared memory: the gather's ring (tc_smem_bytes) covers every other phase's working set
+__host__ __device__ inline size_t pw_other_bytes(int N, int R, int64_t cdf_elems) {
+  const int RP = zg_rp(R);
+  const size_t sample = 16 * 8 + sizeof(uint64_t) * (cdf_elems + kMaxOrder) + sizeof(int32_t) * kPWFib * (N - 1) +
+                        sizeof(double) * kPWFib * (N - 1) + sizeof(double) * kPWFib + sizeof(float) * kPWFib * RP +
+                        sizeof(float) * (size_t)zg_groups(R, kPWThreads) * R * R + sizeof(float) * R * R;
+  const size_t upd = uw_step_bytes(R, 4) + 16 * 8;
+  const size_t inv = sizeof(double) * ((size_t)R * (R + 1) + kSweepBuf + kMaxRank) + sizeof(int) * kMaxRank +
+                     sizeof(double) * ((size_t)R * ut_rd(R) + (size_t)kPWRows * ut_rd(R) + (size_t)kPWRows * ((R + 3) / 4)) +
+                     upd + 16 * 16;
+  size_t m = sample > inv ? sample : inv;
+  return m;
+}
+__host__ __device__ inline size_t pw_smem_bytes(int N, int R, int64_t KBmax, int64_t cdf_elems) {
+  const size_t g = tc_smem_bytes(KBmax);
+  const size_t o = pw_other_bytes(N, R, cdf_elems) + 1024;
+  return g > o ? g : o;
+}
+
+// ------------------------------------------------------------------------------------------ phase S
+struct PWShared {  // static shared state of the phases
+  const uint64_t* cp[kMaxOrder];
+  uint64_t T[kMaxOrder];
+  int32_t start[kMaxOrder], len[kMaxOrder];
+  double wblk;
+  int64_t beff;
+  int bad;
+  double tol;
+  unsigned long long carry;
+  unsigned long long wtot[kPWThreads / 32];
+  double red[kPWThreads / 32];
+};
+
+#define PW_MK(slot)                                 \
+  do {                                              \
+    if (mk && threadIdx.x == 0) mk[slot] = clock64(); \
+    __syncwarp();                                     \
+  } while (0)
+
+__device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned char* sm, PWShared& ss, long long* mk) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int N = p.N, NP = N - 1, R = p.R, RP = zg_rp(R), nb4 = (R + 3) >> 2;
+  const bool block = (p.strategy == 3 || p.strategy == 4);
+  const int64_t bmax = p.bmax[n];
+  const int nunits = pw_units_fib(bmax);
+  const int nsamp = nunits < (int)gridDim.x ? nunits : (int)gridDim.x;  // CTAs with units (Gamma partials)
+  if ((int)blockIdx.x >= nsamp) return;
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    off = (off + 15) / 16 * 16;
+    unsigned char* ptr = sm + off;
+    off += bytes;
+    return ptr;
+  };
+  int64_t cdf_elems = 0;
+  if (p.strategy != 0)
+    for (int k = 0; k < N; ++k)
+      if (k != n) cdf_elems += p.dims[k];
+  uint64_t* cdfs = reinterpret_cast<uint64_t*>(carve(sizeof(uint64_t) * (cdf_elems + kMaxOrder)));
+  int32_t* sidx = reinterpret_cast<int32_t*>(carve(sizeof(int32_t) * kPWFib * NP));
+  double* spt = reinterpret_cast<double*>(carve(sizeof(double) * kPWFib * NP));
+  double* sw = reinterpret_cast<double*>(carve(sizeof(double) * kPWFib));
+  float* zs = reinterpret_cast<float*>(carve(sizeof(float) * kPWFib * RP));
+  const int GG = zg_groups(R, nth);
+  float* red = reinterpret_cast<float*>(carve(sizeof(float) * (size_t)GG * R * R));
+  float* gacc = reinterpret_cast<float*>(carve(sizeof(float) * R * R));
+  {
+    int64_t o = 0;
+    for (int k = 0; k < N; ++k) {
+      const uint64_t* src = p.cdf[k];
+      if (k != n && p.strategy != 0) {  // L2 copies: the CDFs were rebuilt by other CTAs of this launch
+        o = (o + 1) & ~(int64_t)1;  // 16-byte aligned destination
+        cpcg_bytes(cdfs + o, src, 8 * p.dims[k], tid, nth);
+        src = cdfs + o;
+        o += p.dims[k];
+      }
+      if (tid == 0) {
+        ss.cp[k] = src;
+        ss.T[k] = p.strategy == 0 ? (uint64_t)p.dims[k] : __ldcg(p.Ttot + k);
+      }
+    }
+  }
+  for (int e = tid; e < R * R; e += nth) gacc[e] = 0.f;
+  cp_async_wait<0>();
+  __syncthreads();
+  PW_MK(11);
+  if (block && tid == 0) {  // window draws (eq:bik, Alg. 4, R2/R6): common to the whole batch
+    double prod = 1.0;
+    int64_t beff = 1;
+    int pos = 0;
+    for (int k = 0; k < N; ++k) {
+      if (k == n) continue;
+      const int64_t bk = p.window[n][pos];
+      const uint64_t Tk = ss.T[k];
+      const uint64_t rr = scale_draw(draw_word(p.seed, r, 0u, kPurposeWindow, (uint32_t)pos), Tk);
+      const uint64_t* c = ss.cp[k];
+      int64_t istar = upper_bound_u64(c, p.dims[k], rr);
+      if (istar >= p.dims[k]) istar = p.dims[k] - 1;  // T = 0 (degenerate table, status already set)
+      const int64_t s0 = (istar / bk) * bk, e0 = min(s0 + bk, p.dims[k]);
+      const uint64_t Q = c[e0 - 1] - (s0 > 0 ? c[s0 - 1] : 0ull);
+      ss.start[pos] = (int32_t)s0;
+      ss.len[pos] = (int32_t)(e0 - s0);
+      const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * Q), (double)Tk);
+      prod = (pos == 0) ? pt : __dmul_rn(prod, pt);
+      beff *= (e0 - s0);
+      ++pos;
+    }
+    ss.wblk = __ddiv_rn(1.0, prod);
+    ss.beff = beff;
+    if (blockIdx.x == 0) *p.beff = beff;
+  } else if (!block && tid == 0 && blockIdx.x == 0) {
+    *p.beff = p.B;
+  }
+  __syncthreads();
+  __syncwarp();
+  const int64_t beff = block ? ss.beff : p.B;
+  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t b0 = (int64_t)u * kPWFib;
+    const int nf = (int)cmin64(kPWFib, bmax - b0);
+    if (!block) {
+      // row-wise draws (eq:ik, R8): one thread per (fiber, position)
+      for (int e = tid; e < nf * NP; e += nth) {
+        const int lb = e / NP, pos = e % NP;
+        const int k = pos < n ? pos : pos + 1;
+        const uint64_t Tk = ss.T[k];
+        const uint64_t rr = scale_draw(draw_word(p.seed, r, (uint32_t)(b0 + lb), kPurposeRow, (uint32_t)pos), Tk);
+        int64_t i;
+        uint64_t qk;
+        if (p.strategy == 0) {
+          i = (int64_t)rr;
+          qk = 1;
+        } else {
+          const uint64_t* c = ss.cp[k];
+          i = upper_bound_u64(c, p.dims[k], rr);
+          if (i >= p.dims[k]) i = p.dims[k] - 1;  // T = 0: status already set, keep the addresses valid
+          qk = c[i] - (i > 0 ? c[i - 1] : 0ull);
+        }
+        sidx[e] = (int32_t)i;
+        spt[e] = __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);
+      }
+      __syncthreads();
+    }
+    // per fiber: the exact weight (DESIGN.md section 4 order), indices, offset
+    for (int lb = tid; lb < kPWFib; lb += nth) {
+      const int64_t b = b0 + lb;
+      if (lb >= nf || b >= beff) {
+        sw[lb] = 0.0;
+        for (int q = 0; q < NP; ++q) sidx[lb * NP + q] = 0;
+        if (lb < nf) {
+          p.fbase[b] = -1;
+          p.w[b] = 0.0;
+          for (int q = 0; q < NP; ++q) p.idx[b * NP + q] = 0;
+        }
+        continue;
+      }
+      double wv;
+      if (!block) {
+        double prod = spt[lb * NP];
+        for (int pos = 1; pos < NP; ++pos) prod = __dmul_rn(prod, spt[lb * NP + pos]);
+        wv = __ddiv_rn(1.0, __dmul_rn((double)p.B, prod));
+      } else {
+        uint32_t rem = (uint32_t)b;
+        for (int q = 0; q < NP; ++q) {
+          const uint32_t L = (uint32_t)ss.len[q];
+          sidx[lb * NP + q] = ss.start[q] + (int32_t)(rem % L);
+          rem /= L;
+        }
+        wv = ss.wblk;
+      }
+      sw[lb] = wv;
+      p.w[b] = wv;
+      int64_t offn = 0, jrow = 0, jmul = 1;
+      int pos = 0;
+      for (int k = 0; k < N; ++k) {
+        if (k == n) continue;
+        const int64_t ik = sidx[lb * NP + pos];
+        p.idx[b * NP + pos] = (int32_t)ik;
+        ++pos;
+        offn += ik * p.lstride[k];
+        jrow += ik * jmul;
+        jmul *= p.dims[k];
+      }
+      p.fbase[b] = p.pitch[n] ? jrow * p.pitch[n] : offn;
+    }
+    __syncthreads();
+    if (u == (int)blockIdx.x) PW_MK(12);
+    // SKR rows (Alg. 1): z[lb][r] = prod_{k != n, ascending} A^(k)(i_k, r); all
+    // factor loads of a thread's elements of one mode are issued before the products
+    {
+      constexpr int U = (kPWFib * kMaxRank + kPWThreads - 1) / kPWThreads;
+      int lbu[U], ru[U];
+      float z[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int e = tid + q * nth;
+        lbu[q] = e / RP;
+        ru[q] = e % RP;
+        z[q] = (e < kPWFib * RP && lbu[q] < nf && ru[q] < R) ? 1.f : 0.f;
+      }
+      for (int pos = 0; pos < NP; ++pos) {
+        const int k = pos < n ? pos : pos + 1;
+        const float* F = p.factors[k];
+        float f[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) f[q] = z[q] != 0.f ? __ldcg(F + (int64_t)sidx[lbu[q] * NP + pos] * R + ru[q]) : 0.f;
+#pragma unroll
+        for (int q = 0; q < U; ++q) z[q] = z[q] * f[q];
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q)
+        if (tid + q * nth < kPWFib * RP) zs[tid + q * nth] = z[q];
+    }
+    __syncthreads();
+    if (u == (int)blockIdx.x) PW_MK(13);
+    // the tcgen05 A-operand images of the unit: zh / zl rows (zero past nf), one 16-byte chunk (4
+    // consecutive fibers of one row) per task
+    for (int e = tid; e < R * (kPWFib / 4); e += nth) {
+      const int rr = e / (kPWFib / 4), l0 = 4 * (e % (kPWFib / 4));
+      float h[4], l[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int lb = l0 + j;
+        const float zw = lb < nf ? (float)((float)sw[lb] * zs[lb * RP + rr]) : 0.f;
+        h[j] = __uint_as_float(__float_as_uint(zw) & 0xFFFFE000u);
+        l[j] = zw - h[j];
+      }
+      *reinterpret_cast<float4*>(p.zimg + (zimg_off(b0 + l0, rr) >> 2)) = make_float4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<float4*>(p.zimg + (zimg_off(b0 + l0, 64 + rr) >> 2)) = make_float4(l[0], l[1], l[2], l[3]);
+    }
+    if (u == (int)blockIdx.x) PW_MK(23);
+    // Gamma partial of the unit: sum_b (w_b z_b) z_b^T (4x4 blocks bi <= bj, GG fiber groups), then
+    // added to the CTA's accumulator (unit order)
+    {
+      const int nblk = nb4 * (nb4 + 1) / 2;
+      const int g = tid / nblk, blk = tid % nblk;
+      if (g < GG) {
+        int bi = 0, rem = blk;
+        while (rem >= nb4 - bi) { rem -= nb4 - bi; ++bi; }
+        const int bj = bi + rem;
+        float acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
+        for (int kk = g; kk < nf; kk += GG) {
+          const float wk = (float)sw[kk];
+          float x[4], y[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            x[a] = 4 * bi + a < RP ? wk * zs[kk * RP + 4 * bi + a] : 0.f;
+            y[a] = 4 * bj + a < RP ? zs[kk * RP + 4 * bj + a] : 0.f;
+          }
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[a][c] = fmaf(x[a], y[c], acc[a][c]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int r1 = 4 * bi + a, r2 = 4 * bj + c;
+            if (r1 < R && r2 < R) {
+              red[(g * R + r1) * R + r2] = acc[a][c];
+              if (bi != bj) red[(g * R + r2) * R + r1] = acc[a][c];
+            }
+          }
+      }
+      __syncthreads();
+      if (u == (int)blockIdx.x) PW_MK(24);
+      for (int e = tid; e < R * R; e += nth) {
+        float s = red[e];
+        for (int gg = 1; gg < GG; ++gg) s += red[gg * R * R + e];
+        gacc[e] += s;
+      }
+      __syncthreads();
+    }
+  }
+  PW_MK(14);
+  float* gcl = p.gcl + (int64_t)blockIdx.x * R * R;
+  for (int e = tid; e < R * R; e += nth) gcl[e] = gacc[e];
+}
+
+// ------------------------------------------------------------------------------------------ phase G
+struct PWBars {
+  uint64_t xfull[16], xempty[16], sdone[4], mdone[4], afull[4], afree[4], accf;
+};
+
+// Gamma = sum of the sampling CTAs' partials in CTA order; entries [e0, E) with stride es
+__device__ __forceinline__ void pw_gamma_sum(const PWParams& p, int nsamp, int e0, int es) {
+  const int E = p.R * p.R;
+  for (int e = e0; e < E; e += es) {
+    float v[16], s = 0.f;
+    for (int c0 = 0; c0 < nsamp; c0 += 16) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = (c0 + k < nsamp) ? __ldcg(p.gcl + (int64_t)(c0 + k) * E + e) : 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) s += v[k];  // CTA order; zeros past nsamp are exact
+    }
+    p.gam[e] = s;
+  }
+}
+
+// the tcgen05 mainloop of gupdate_tc.cuh over this CTA's (I-tile, chunk) items; gs / gi: this CTA's
+// running stage / item counters (the mbarrier phases continue across items and iterations)
+__device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PWBars& B, uint32_t tmem, uint32_t& gs,
+                          uint32_t& gi) {
+  constexpr int KS = kTCKS, NX = kTCNX, NP = kTCPairs, NZ = kTCNZ, TI = kGUTI;
+  constexpr uint32_t A_BYTES = kTCABytes;
+  constexpr uint32_t IDESC = umma_idesc_tf32_mn(128, 256) & ~((1u << 15) | (1u << 16));
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int R = p.R;
+  const int64_t In = p.dims[n];
+  const int tiles = (int)((In + TI - 1) / TI), CK = p.CK[n];
+  const int64_t KB = p.KB[n], bmax = p.bmax[n];
+  const int nitems = tiles * CK;
+  const int nsamp = min(pw_units_fib(bmax), (int)gridDim.x);
+  const float* X = p.Xg[n];
+  const int64_t rowlen = p.rowlen[n];
+  unsigned char* xsp = sm;
+  unsigned char* xring = sm + NP * 2 * A_BYTES;
+  unsigned char* zring = xring + NX * A_BYTES;
+  const size_t body = (size_t)NP * 2 * A_BYTES + (size_t)NX * A_BYTES + (size_t)NZ * kTCZBytes;
+  const size_t epi = (size_t)128 * kTCEpiStride * 4;
+  int64_t* sfb = reinterpret_cast<int64_t*>(sm + (body > epi ? body : epi));
+  // the Gamma sum's index space: lanes 1-31 of warp 12 of the CTAs with items, then every thread
+  // of the CTAs without one
+  const int with_items = min(nitems, (int)gridDim.x);
+  const int gamma_stride = with_items * 31 + ((int)gridDim.x - with_items) * kPWThreads;
+  if ((int)blockIdx.x >= nitems) {
+    pw_gamma_sum(p, nsamp, with_items * 31 + ((int)blockIdx.x - nitems) * kPWThreads + tid, gamma_stride);
+    return;
+  }
+  bool first = true;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int tile = item / CK, chunk = item % CK;
+    const int64_t i0 = (int64_t)tile * TI, c0 = (int64_t)chunk * KB;
+    const int nfib = (int)cmax64(0, cmin64(KB, bmax - c0));
+    const int nst = (nfib + KS - 1) / KS;
+    for (int64_t i = tid; i < nfib; i += kPWThreads) sfb[i] = __ldcg(p.fbase + c0 + i);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (wid < 4) {
+      // X loaders: 16-byte cp.async chunks of the sampled fiber segments (Alg. 5 TensorSamp)
+      for (int st = 0; st < nst; ++st) {
+        const uint32_t g = gs + st;
+        const int slot = g % NX;
+        if (g >= (uint32_t)NX) mbar_wait(&B.xempty[slot], ((g / NX) - 1) & 1);
+        unsigned char* A = xring + slot * A_BYTES;
+        const int f0 = st * KS;
+#pragma unroll
+        for (int rep = 0; rep < KS * 32 / 128; ++rep) {
+          const int e = tid + 128 * rep;
+          const int kk = e >> 5, j = e & 31;
+          const int lb = f0 + kk;
+          const int64_t fb = lb < nfib ? sfb[lb] : -1;
+          const int64_t r0 = i0 + 4 * j;
+          if (fb >= 0 && r0 < rowlen) cp_async16(A + kk * 512 + 16 * j, X + fb + r0, 16);
+        }
+        cp_async_mbar_arrive_noinc(&B.xfull[slot]);
+      }
+    } else if (wid <= 11) {
+      // 3xTF32 split / transpose into the K-major swizzled {xh; xl} pair
+      const int t = tid - 128;
+      const int iq = t & 31, kq = t >> 5;
+      for (int st = 0; st < nst; ++st) {
+        const uint32_t g = gs + st;
+        const int slot = g % NX, hb = g % NP;
+        mbar_wait(&B.xfull[slot], (g / NX) & 1);
+        if (g >= (uint32_t)NP) mbar_wait(&B.mdone[hb], ((g / NP) - 1) & 1);
+        const float* A = reinterpret_cast<const float*>(xring + slot * A_BYTES);
+        unsigned char* H = xsp + hb * 2 * A_BYTES;
+        unsigned char* L = H + A_BYTES;
+        const int f0 = st * KS;
+        float x[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kk = 4 * kq + u, lb = f0 + kk;
+          const bool ok = lb < nfib && sfb[lb] >= 0;
+#pragma unroll
+          for (int a = 0; a < 4; ++a) x[u][a] = ok ? A[kk * 128 + iq + 32 * a] : 0.f;
+        }
+        mbar_arrive(&B.xempty[slot]);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const float4 h = make_float4(tf32_trunc(x[0][a]), tf32_trunc(x[1][a]), tf32_trunc(x[2][a]), tf32_trunc(x[3][a]));
+          const float4 l = make_float4(x[0][a] - h.x, x[1][a] - h.y, x[2][a] - h.z, x[3][a] - h.w);
+          const uint32_t o = kmaj_off(iq + 32 * a, 4 * kq);
+          *reinterpret_cast<float4*>(H + o) = h;
+          *reinterpret_cast<float4*>(L + o) = l;
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&B.sdone[hb]);
+      }
+    } else if (wid == 12) {
+      if (lane != 0) {
+        if (first) pw_gamma_sum(p, nsamp, (int)blockIdx.x * 31 + lane - 1, gamma_stride);
+      } else {
+        for (int st = 0; st < nst; ++st) {
+          const uint32_t g = gs + st;
+          const int zs = g % NZ;
+          if (g >= (uint32_t)NZ) mbar_wait(&B.afree[zs], ((g / NZ) - 1) & 1);
+          const int64_t sb = (c0 + (int64_t)st * KS) / KS;
+          mbar_expect_tx(&B.afull[zs], kTCZBytes);
+          bulk_g2s(zring + zs * kTCZBytes, p.zimg + sb * (kTCZBytes / 4), kTCZBytes, &B.afull[zs]);
+        }
+      }
+    } else if (wid == 13 && lane == 0) {
+      const uint64_t dx = umma_desc_sw128(smem_u32(xsp), 16, 1024);
+      const uint64_t dz = umma_desc_sw128(smem_u32(zring), 16, 1024);
+      for (int st = 0; st < nst; ++st) {
+        const uint32_t g = gs + st;
+        const int hb = g % NP, as = g % NZ;
+        mbar_wait(&B.sdone[hb], (g / NP) & 1);
+        mbar_wait(&B.afull[as], (g / NZ) & 1);
+        tc_fence_after();
+        const uint64_t b = dx + ((uint64_t)(hb * 2 * A_BYTES) >> 4);
+        const uint64_t a = dz + ((uint64_t)(as * kTCZBytes) >> 4);
+#pragma unroll
+        for (int k = 0; k < KS / 8; ++k) umma_tf32(tmem, a + 2 * k, b + 2 * k, IDESC, (st > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&B.mdone[hb]);
+        umma_commit(&B.afree[as]);
+      }
+      if (nst > 0) umma_commit(&B.accf);
+    }
+    __syncthreads();
+    // epilogue: E[L][i] = D[L][i] + D[L][128 + i] (x = xh + xl) staged in shared memory, then
+    // M^T[r][i] = E[r][i] + E[64 + r][i] (zw = zh + zl) -> the split-K workspace
+    if (nst > 0) mbar_wait(&B.accf, gi & 1);
+    tc_fence_after();
+    float* E = reinterpret_cast<float*>(sm);
+    if (wid >= 4 && wid <= 11) {
+      const int L = 32 * (wid & 3) + lane, hh = (wid - 4) >> 2;
+      const uint32_t trow = tmem + ((uint32_t)(32 * (wid & 3)) << 16);
+#pragma unroll 1
+      for (int c = 64 * hh; c < 64 * hh + 64; c += 16) {
+        float v1[16], v2[16];
+        if (nst > 0) {
+          tmem_ld16(trow + (uint32_t)c, v1);
+          tmem_ld16(trow + 128u + (uint32_t)c, v2);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v1[j] = v2[j] = 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4*>(E + L * kTCEpiStride + c + j) =
+              make_float4(v1[j] + v2[j], v1[j + 1] + v2[j + 1], v1[j + 2] + v2[j + 2], v1[j + 3] + v2[j + 3]);
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    {
+      const int nrow = (int)cmax64(0, cmin64(TI, In - i0));
+      float* part = p.Mpart + ((int64_t)tile * CK + chunk) * R * TI;
+      for (int e = tid; e < R * (TI / 4); e += kPWThreads) {
+        const int r = e / (TI / 4), i = 4 * (e % (TI / 4));
+        const float4 a = *reinterpret_cast<const float4*>(E + r * kTCEpiStride + i);
+        const float4 b = *reinterpret_cast<const float4*>(E + (64 + r) * kTCEpiStride + i);
+        const float4 s = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+        if (i + 4 <= nrow) {
+          *reinterpret_cast<float4*>(part + r * TI + i) = s;
+        } else {
+          if (i < nrow) part[r * TI + i] = s.x;
+          if (i + 1 < nrow) part[r * TI + i + 1] = s.y;
+          if (i + 2 < nrow) part[r * TI + i + 2] = s.z;
+        }
+      }
+    }
+    gs += nst;
+    if (nst > 0) ++gi;
+    first = false;
+    __syncthreads();  // the ring / staging area is rewritten by the next item
+  }
+}
+
+// ------------------------------------------------------------------------------------------ phase U
+// rows [r0, r0 + nr) of A^(n): M (chunk order), G = A Gamma - M, update; leaves the new rows in sA
+// (stride R+1) and writes the unit's table partial
+__device__ void pw_update_unit(const PWParams& p, int n, int unit, double alpha, float* sA, float* sS, float* sM,
+                               const float* sG, double* sgp, PWShared& ss, long long* mk) {
+  constexpr int TI = kGUTI;
+  const int R = p.R, RS = R + 1, AS = R, tid = threadIdx.x, nth = blockDim.x, nb4 = (R + 3) >> 2;
+  const int64_t In = p.dims[n];
+  const int64_t r0 = (int64_t)unit * kPWRows;
+  const int nr = (int)cmin64(kPWRows, In - r0);
+  const int CK = p.CK[n];
+  float* A = p.factors[n];
+  float* S = p.S[n];
+  // the unit's rows of A and S: contiguous, 16-byte L2 copies all in flight (rows written earlier in
+  // this launch); stride R in shared memory
+  cpcg_bytes(sA, A + r0 * R, (int64_t)nr * R * 4, tid, nth);
+  if (p.rule == 1) cpcg_bytes(sS, S + r0 * R, (int64_t)nr * R * 4, tid, nth);
+  {  // M = sum of the chunk partials, in chunk order (16-byte vectors of 4 consecutive rows)
+    const int64_t tile = r0 / TI, lr0 = r0 % TI;
+    const int ng = (nr + 3) / 4;
+    for (int t = tid; t < R * ng; t += nth) {
+      const int r = t / ng, gq = t % ng;
+      const float* base = p.Mpart + ((tile * CK) * R + r) * TI + lr0 + gq * 4;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int c0 = 0; c0 < CK; c0 += 8) {
+        float4 ld[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (c0 + k < CK) ld[k] = __ldcg(reinterpret_cast<const float4*>(base + (int64_t)(c0 + k) * R * TI));
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (c0 + k < CK) {
+            acc[0] += ld[k].x;
+            acc[1] += ld[k].y;
+            acc[2] += ld[k].z;
+            acc[3] += ld[k].w;
+          }
+      }
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        if (gq * 4 + w < nr) sM[(gq * 4 + w) * RS + r] = acc[w];
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  PW_MK(15);
+  // G = A Gamma - M (each task owns a 4 x 4 block of M -> G in place)
+  for (int t = tid; t < ((nr + 3) >> 2) * nb4; t += nth) {
+    const int a0 = 4 * (t / nb4), q0 = 4 * (t % nb4);
+    float acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
+    for (int k = 0; k < R; ++k) {
+      float x[4], y[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) x[a] = (a0 + a < nr) ? sA[(a0 + a) * AS + k] : 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) y[c] = (q0 + c < R) ? sG[k * R + q0 + c] : 0.f;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = fmaf(x[a], y[c], acc[a][c]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (a0 + a < nr && q0 + c < R) sM[(a0 + a) * RS + q0 + c] = acc[a][c] - sM[(a0 + a) * RS + q0 + c];
+  }
+  __syncthreads();
+  // fixed (eq:proposed) / adaptive (eq:etaada/eq:Aada, :531-537, R12) update
+  for (int e = tid; e < nr * R; e += nth) {
+    const int il = e / R, r = e % R;
+    const int64_t gi = (r0 + il) * R + r;
+    const float g = sM[il * RS + r];
+    p.Gout[gi] = g;
+    const float a = sA[il * AS + r];
+    float an = a;
+    if (p.rule == 0) {
+      an = a - (float)alpha * g;
+    } else {
+      const float sv = sS[il * AS + r] + g * g;
+      S[gi] = sv;
+      if (sv > 0.f) {
+        float step;
+        if (p.eps == 0.0) step = (float)p.eta / sqrtf((float)p.b + sv);
+        else step = (float)p.eta / (float)pow((double)((float)p.b + sv), 0.5 + p.eps);
+        an = a - step * g;
+      }
+    }
+    A[gi] = an;
+    sA[il * AS + r] = an;
+  }
+  __syncthreads();
+  PW_MK(16);
+  // table partials of the new rows (R9)
+  if (p.strategy == 1 || p.strategy == 3) {  // leverage: partial fp64 Gram, packed upper triangle
+    const int P = R * (R + 1) / 2;
+    const int nblk = nb4 * (nb4 + 1) / 2;
+    for (int blk = tid; blk < nblk; blk += nth) {
+      int bi = 0, rem = blk;
+      while (rem >= nb4 - bi) { rem -= nb4 - bi; ++bi; }
+      const int bj = bi + rem;
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+      for (int il = 0; il < nr; ++il) {
+        double x[4], y[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          x[a] = 4 * bi + a < R ? (double)sA[il * AS + 4 * bi + a] : 0.0;
+          y[a] = 4 * bj + a < R ? (double)sA[il * AS + 4 * bj + a] : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = fma(x[a], y[c], acc[a][c]);
+      }
+      double* gp = p.gpart + (int64_t)unit * P;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int r1 = 4 * bi + a, r2 = 4 * bj + c;
+          if (r1 < R && r2 < R && r1 <= r2) gp[r1 * R - r1 * (r1 - 1) / 2 + (r2 - r1)] = acc[a][c];
+        }
+    }
+  } else if (p.strategy == 2 || p.strategy == 4) {  // Euclidean: row norms + the unit's partial ||A||^2
+    double acc = 0.0;
+    for (int il = tid; il < nr; il += nth) {
+      double rs = 0.0;
+      for (int c = 0; c < R; ++c) rs += (double)sA[il * AS + c] * (double)sA[il * AS + c];
+      p.rownorm[r0 + il] = rs;
+      acc += rs;
+    }
+    __syncwarp();  // reconverged: a diverged warp runs every shuffle on the slow collective path
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((tid & 31) == 0) ss.red[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nth / 32; ++w) t += ss.red[w];
+      p.gpart[unit] = t;
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------ phase Q
+// scores + quantisation of the unit's rows (new rows re-read from A^(n)), look-back prefix, CDF rows
+__device__ void pw_table_unit(const PWParams& p, int n, int unit, int nunits, uint32_t tag, const double* Wd, int rank,
+                              double fro, int bad0, double* Ad, double* part, PWShared& ss, long long* mk) {
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int R = p.R, RD = ut_rd(R), nb4 = (R + 3) >> 2;
+  const bool lev = (p.strategy == 1 || p.strategy == 3);
+  const int64_t In = p.dims[n];
+  const int64_t r0 = (int64_t)unit * kPWRows;
+  const int nr = (int)cmin64(kPWRows, In - r0);
+  __shared__ double s_p[kPWRows];
+  __shared__ unsigned long long s_q[kPWRows];
+  __shared__ int s_badu;
+  if (tid == 0) s_badu = bad0;
+  if (lev) {
+    for (int e = tid; e < kPWRows * RD; e += nth) {
+      const int il = e / RD, c = e % RD;
+      Ad[e] = (il < nr && c < R) ? (double)__ldcg(p.factors[n] + (r0 + il) * R + c) : 0.0;
+    }
+    __syncthreads();
+    const int nrp = (nr + 1) >> 1;
+    for (int t = tid; t < nrp * nb4; t += nth) {
+      const int il = 2 * (t / nb4), cg = t % nb4;
+      const double* a0 = Ad + il * RD;
+      const double* a1 = a0 + RD;
+      double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+      for (int k = 0; k < R; ++k) {
+        const double x0 = a0[k], x1 = a1[k];
+        const double2 w0 = *reinterpret_cast<const double2*>(Wd + k * RD + 4 * cg);
+        const double2 w1 = *reinterpret_cast<const double2*>(Wd + k * RD + 4 * cg + 2);
+        acc0[0] = fma(x0, w0.x, acc0[0]);
+        acc0[1] = fma(x0, w0.y, acc0[1]);
+        acc0[2] = fma(x0, w1.x, acc0[2]);
+        acc0[3] = fma(x0, w1.y, acc0[3]);
+        acc1[0] = fma(x1, w0.x, acc1[0]);
+        acc1[1] = fma(x1, w0.y, acc1[1]);
+        acc1[2] = fma(x1, w1.x, acc1[2]);
+        acc1[3] = fma(x1, w1.y, acc1[3]);
+      }
+      part[il * nb4 + cg] = acc0[0] * a0[4 * cg] + acc0[1] * a0[4 * cg + 1] + acc0[2] * a0[4 * cg + 2] + acc0[3] * a0[4 * cg + 3];
+      if (il + 1 < kPWRows)
+        part[(il + 1) * nb4 + cg] =
+            acc1[0] * a1[4 * cg] + acc1[1] * a1[4 * cg + 1] + acc1[2] * a1[4 * cg + 2] + acc1[3] * a1[4 * cg + 3];
+    }
+    __syncthreads();
+    if (tid < nr) {
+      double l = 0.0;
+      for (int cg = 0; cg < nb4; ++cg) l += part[tid * nb4 + cg];
+      s_p[tid] = rank > 0 ? fmax(l, 0.0) / (double)rank : 0.0;
+    }
+  } else if (tid < nr) {
+    s_p[tid] = fro > 0.0 ? __ldcg(p.rownorm + r0 + tid) / fro : 0.0;
+  }
+  __syncthreads();
+  if (tid < nr) {
+    const double pv = s_p[tid];
+    unsigned long long qv = 0;
+    if (!(pv == pv) || pv > 2.0) {
+      atomicOr(&s_badu, 8);
+    } else if (pv > 0.0) {
+      const double s = rint(pv * 4294967296.0);
+      qv = (s < 1.0) ? 1ull : (unsigned long long)s;
+    }
+    p.pprob[n][r0 + tid] = pv;
+    s_q[tid] = qv;
+  }
+  __syncthreads();
+  PW_MK(21);
+  // the unit's aggregate, published with its tag (release), then the exclusive prefix over the
+  // preceding units' aggregates (acquire; exact integer sums in any order)
+  if (tid == 0) {
+    unsigned long long a = 0;
+    for (int i = 0; i < nr; ++i) a += s_q[i];
+    p.agg[unit] = a;
+    p.aggf[2 * unit] = (unsigned)s_badu;
+    st_release_u32(p.aggf + 2 * unit + 1, tag);  // release: agg / bad bits above (same thread) first
+  }
+  unsigned long long pre = 0;
+  unsigned badv = 0;
+  for (int u = tid; u < unit; u += nth) {
+    while (ld_acquire_u32(p.aggf + 2 * u + 1) != tag) __nanosleep(40);
+    pre += __ldcg(p.agg + u);
+    badv |= __ldcg(p.aggf + 2 * u);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    badv |= __shfl_xor_sync(0xffffffffu, badv, o);
+  }
+  if (lane == 0) {
+    ss.wtot[wid] = pre;
+    ss.red[wid] = __longlong_as_double((long long)badv);
+  }
+  __syncthreads();
+  PW_MK(22);
+  if (wid == 0) {  // predecessors' total + the unit's inclusive scan -> CDF rows (warp 0)
+    __syncwarp();
+    unsigned long long t = lane < nth / 32 ? ss.wtot[lane] : 0ull;
+    unsigned bb = lane < nth / 32 ? (unsigned)__double_as_longlong(ss.red[lane]) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t += __shfl_xor_sync(0xffffffffu, t, o);
+      bb |= __shfl_xor_sync(0xffffffffu, bb, o);
+    }
+    bb |= (unsigned)s_badu;
+    unsigned long long c = lane < nr ? s_q[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long v = __shfl_up_sync(0xffffffffu, c, o);
+      if (lane >= o) c += v;
+    }
+    c += t;
+    if (lane < nr) p.cdf[n][r0 + lane] = c;
+    if (unit == nunits - 1 && lane == nr - 1) {  // the last unit: T and the table status
+      p.Ttot[n] = c;
+      int st = 0;
+      if (bb & 8) st = -8;
+      else if ((bb & 2) || c == 0) st = -3;
+      if (st != 0) atomicCAS(p.status, 0, st);
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------ trace
+__device__ void pw_trace(const PWParams& p, int s, int n, uint64_t r) {
+  const int64_t slot = p.tr.first + s;
+  if (slot >= p.tr.cap) return;
+  unsigned char* base = p.tr.base + slot * p.tr.stride;
+  const int NP = p.N - 1, R = p.R;
+  const int64_t bm = p.bmax[n], In = p.dims[n];
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, ts = (int64_t)gridDim.x * blockDim.x;
+  int32_t* ti = reinterpret_cast<int32_t*>(base + p.tr.o_idx);
+  double* tw = reinterpret_cast<double*>(base + p.tr.o_w);
+  float* tA = reinterpret_cast<float*>(base + p.tr.o_A);
+  float* tS = reinterpret_cast<float*>(base + p.tr.o_S);
+  uint64_t* tc = reinterpret_cast<uint64_t*>(base + p.tr.o_cdf);
+  int64_t* tm = reinterpret_cast<int64_t*>(base + p.tr.o_meta);
+  for (int64_t e = t0; e < bm * NP; e += ts) ti[e] = __ldcg(p.idx + e);
+  for (int64_t e = t0; e < bm; e += ts) tw[e] = __ldcg(p.w + e);
+  for (int64_t e = t0; e < In * R; e += ts) {
+    tA[e] = __ldcg(p.factors[n] + e);
+    if (p.rule == 1) tS[e] = __ldcg(p.S[n] + e);
+  }
+  for (int64_t e = t0; e < In; e += ts) tc[e] = __ldcg(p.cdf[n] + e);
+  if (t0 == 0) {
+    tm[0] = n;
+    tm[1] = (int64_t)r;
+    tm[2] = __ldcg(p.beff);
+    tm[3] = 0;
+  }
+}
+
+// ------------------------------------------------------------------------------------------ kernel
+#define PW_MARK(slot)                                                                  \
+  do {                                                                                 \
+    if (p.dbg && tid == 0 && s < 8 && blockIdx.x == 0) p.dbg[512 + 32 * s + (slot)] = clock64(); \
+    __syncwarp();                                                                                \
+  } while (0)
+
+// row groups of the sweep inverse per RMAX: as many as 448 threads hold (32 ceil(RMAX/32) lanes per
+// group, RMAX a multiple of 2 groups): fewer rows per thread shorten every pivot step
+template <int RMAX>
+constexpr int kPWSweepGroups = RMAX == 16 ? 8 : RMAX == 32 ? 8 : RMAX == 56 ? 7 : 4;
+
+// RMAX: R rounded up to 16 (one instance of the sweep inverse per kernel: the whole kernel's code must
+// stay instruction-cache resident across iterations -- a kernel carrying every sweep variant measured
+// ~25k instructions and stalled on instruction fetch in its short phases)
+template <int RMAX>
+__global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int N = p.N, R = p.R, RS = R + 1, G = (int)gridDim.x;
+  extern __shared__ __align__(16) unsigned char pw_raw[];
+  unsigned char* sm = pw_raw + ((1024u - (smem_u32(pw_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) PWBars B;
+  __shared__ PWShared ss;
+  __shared__ uint32_t s_tmem;
+  __shared__ uint64_t s_r0;
+  __shared__ int s_stop;
+  if (wid == 13) {  // TMEM accumulator for the whole launch
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kTCNX; ++s) {
+      mbar_init(&B.xfull[s], 128);
+      mbar_init(&B.xempty[s], 256);
+    }
+    for (int s = 0; s < kTCPairs; ++s) {
+      mbar_init(&B.sdone[s], 256);
+      mbar_init(&B.mdone[s], 1);
+    }
+    for (int s = 0; s < kTCNZ; ++s) {
+      mbar_init(&B.afull[s], 1);
+      mbar_init(&B.afree[s], 1);
+    }
+    mbar_init(&B.accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_r0 = *reinterpret_cast<volatile uint64_t*>(p.iter);
+    s_stop = 0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  unsigned gen = 0;  // barriers passed in this launch
+  uint64_t r = s_r0;
+  uint32_t gs = 0, gi = 0;
+  int n_done = -1;
+  const bool lev = (p.strategy == 1 || p.strategy == 3);
+  const int P = R * (R + 1) / 2;
+
+#pragma unroll 1
+  for (int s = 0; s < p.nsteps; ++s) {
+    const int n = p.order == 1 ? random_mode(p.seed, r, N) : (p.first_mode + s) % N;
+    const int64_t In = p.dims[n];
+    const int nu = pw_units_rows(In);
+    const double alpha = p.alphas ? p.alphas[s] : (p.alpha_dev ? *p.alpha_dev : p.alpha);
+    PW_MARK(0);
+    if (p.dbg && tid == 0 && s < 8 && blockIdx.x == 0) p.dbg[512 + 32 * s + 30] = gtimer();
+    // ---- S: the batch of mode n at r ----
+    long long* mk = (p.dbg && s < 8 && blockIdx.x == 0) ? p.dbg + 512 + 32 * s : nullptr;
+    pw_sample(p, n, r, sm, ss, mk);
+    PW_MARK(1);
+    grid_barrier(p.bar, gen);
+    PW_MARK(2);
+    // ---- G: TensorSamp + tcgen05 contraction -> split-K partial tiles; Gamma sum ----
+    pw_gather(p, n, sm, B, tmem, gs, gi);
+    PW_MARK(3);
+    grid_barrier(p.bar, gen);
+    PW_MARK(4);
+    // ---- U: update of the row units, table partials ----
+    {
+      // 16-byte aligned: Gamma [R][R], A / S rows [16][R] (cp.async targets), M rows [16][R+1]
+      float* sG = reinterpret_cast<float*>(sm);
+      float* sA = sG + ((R * R + 3) & ~3);
+      float* sS = sA + ((kPWRows * R + 3) & ~3);
+      float* sM = sS + ((kPWRows * R + 3) & ~3);
+      double* sgp = reinterpret_cast<double*>(sm + ((sizeof(float) * (3 * kPWRows * RS + R * R + 12) + 15) / 16) * 16);
+      if ((int)blockIdx.x < nu) {
+        cpcg_bytes(sG, p.gam, (int64_t)R * R * 4, tid, kPWThreads);  // waited for with the unit's rows
+        if (blockIdx.x == 0)
+          for (int e = tid; e < R * R; e += kPWThreads) p.Gam_out[e] = __ldcg(p.gam + e);
+        for (int u = blockIdx.x; u < nu; u += G) pw_update_unit(p, n, u, alpha, sA, sS, sM, sG, sgp, ss, u == (int)blockIdx.x ? mk : nullptr);
+      }
+    }
+    PW_MARK(5);
+    grid_barrier(p.bar, gen);
+    PW_MARK(6);
+    if (p.strategy != 0) {
+      // ---- P: the Gram's pairs (leverage) over the unit partials, a slice per CTA ----
+      // one warp per pair: lane l sums the partials of units l, l + 32, ... (all loads in flight),
+      // then a fixed xor-shuffle tree (deterministic); done flag per CTA, tagged by the iteration
+      const uint32_t tag = p.tag0 + (uint32_t)s;
+      if (lev) {
+        const int per = (P + G - 1) / G;
+        const int a0 = (int)blockIdx.x * per, a1 = min(P, a0 + per);
+        for (int pair = a0 + wid; pair < a1; pair += kPWThreads / 32) {
+          double v[8], sacc = 0.0;
+          for (int c0 = 0; c0 < nu; c0 += 8 * 32) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int u = c0 + 32 * k + lane;
+              v[k] = u < nu ? __ldcg(p.gpart + (int64_t)u * P + pair) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) sacc += v[k];
+          }
+          __syncwarp();
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+          if (lane == 0) p.gram[pair] = sacc;
+        }
+        __syncthreads();
+        if (tid == 0) red_release_add(p.pcnt, 1u);
+      }
+      PW_MARK(7);
+      // ---- I: the inverse (leverage) / ||A||_F^2 (Euclidean), every CTA with row units ----
+      if ((int)blockIdx.x < nu) {
+        unsigned char* ext = sm + uw_step_bytes(R, 4) + 256;
+        double* Gm = reinterpret_cast<double*>(ext);
+        double* rowbuf = Gm + R * RS;
+        double* diag = rowbuf + kSweepBuf;
+        int* swept = reinterpret_cast<int*>(diag + kMaxRank);
+        double* Wd = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(swept) + sizeof(int) * kMaxRank + 16);
+        Wd = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(Wd) + 15) & ~(uintptr_t)15);
+        const int RD = ut_rd(R);
+        double* Ad = Wd + R * RD;
+        double* part = Ad + kPWRows * RD;
+        int rank = 0, bad0 = 0;
+        double fro = 0.0;
+        if (lev) {
+          if (tid == 0) wait_count(p.pcnt, (unsigned)G * (unsigned)(s + 1));
+          __syncthreads();
+          PW_MARK(18);
+          {  // the packed Gram (L2 copy) -> the full symmetric matrix, closed-form pair index
+            double* gst = Wd;  // staging (the W area is written only after the inverse)
+            cpcg_bytes(gst, p.gram, (int64_t)P * 8, tid, kPWThreads);
+            cp_async_wait<0>();
+            __syncthreads();
+            for (int e = tid; e < R * R; e += kPWThreads) {
+              const int r1 = e / R, r2 = e % R;
+              const int a = r1 <= r2 ? r1 : r2, b = r1 <= r2 ? r2 : r1;
+              Gm[r1 * RS + r2] = gst[a * R - a * (a - 1) / 2 + (b - a)];
+            }
+          }
+          __syncthreads();
+          if (tid < 32) {
+            __syncwarp();
+            double d0 = 0.0;
+            bool fin = true;
+            for (int j = lane; j < R; j += 32) {
+              const double d = Gm[j * RS + j];
+              d0 = fmax(d0, d);
+              fin = fin && (d == d) && d < 1.7e308;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
+            const bool allfin = __all_sync(0xffffffffu, fin);
+            if (lane == 0) {
+              ss.bad = allfin ? 0 : 8;
+              ss.tol = (double)(In > R ? In : R) * 2.220446049250313e-16 * d0;
+            }
+          }
+          __syncthreads();
+          constexpr int EPT = (kMaxRank * kMaxRank + kPWThreads - 1) / kPWThreads;
+          PW_MARK(19);
+          rank = (In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, ss.tol, rowbuf, swept, diag)
+                              : grp_sweep_inverse<RMAX, kPWSweepGroups<RMAX>>(Gm, R, ss.tol, rowbuf, swept);
+          PW_MARK(20);
+          for (int e = tid; e < R * RD; e += kPWThreads) {
+            const int i = e / RD, j = e % RD;
+            Wd[e] = j < R ? Gm[i * RS + j] : 0.0;
+          }
+          bad0 = ss.bad | (rank == 0 ? 2 : 0);
+          __syncthreads();
+        } else {
+          if (tid == 0) {
+            double t = 0.0;
+            for (int u = 0; u < nu; ++u) t += __ldcg(p.gpart + u);
+            ss.tol = t;
+          }
+          __syncthreads();
+          fro = ss.tol;
+          if (!(fro == fro) || fro > 1.7e308) bad0 = 8;
+          else if (!(fro > 0.0)) bad0 = 2;
+        }
+        PW_MARK(8);
+        // ---- Q: scores, quantisation, look-back prefix -> CDF rows, T, status ----
+        for (int u = blockIdx.x; u < nu; u += G) pw_table_unit(p, n, u, nu, tag, Wd, rank, fro, bad0, Ad, part, ss, u == (int)blockIdx.x ? mk : nullptr);
+      }
+      PW_MARK(9);
+      grid_barrier(p.bar, gen);  // the table of the new A^(n) is complete (R9)
+    }
+    PW_MARK(10);
+    if (p.dbg && tid == 0 && s < 8 && blockIdx.x == 0) p.dbg[512 + 32 * s + 31] = gtimer();
+    ++r;
+    n_done = n;
+    if (p.tr.base) {
+      pw_trace(p, s, n, r - 1);
+      if (s + 1 < p.nsteps) grid_barrier(p.bar, gen);  // before the next batch overwrites idx / w
+    }
+    // a degenerate or non-finite table stops the launch (uniform: the status was set before the barrier)
+    if (tid == 0) s_stop = __ldcg(p.status) != 0;
+    __syncthreads();
+    if (s_stop) break;
+  }
+  __syncthreads();
+  if (wid == 13) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  if (blockIdx.x == 0 && tid == 0) {
+    *p.iter = r;
+    if (n_done >= 0) *p.last_mode = n_done;
+  }
+}
+
+}  // namespace cps

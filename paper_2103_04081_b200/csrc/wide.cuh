@@ -149,6 +149,7 @@ __device__ void uw_table_tail(const UWParams<T>& p, unsigned char* sm, const coo
         d0 = fmax(d0, d);
         fin = fin && (d == d) && d < 1.7e308;
       }
+      __syncwarp();  // reconverge: a diverged warp takes the slow collective shuffle path
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
       if (lane == 0) {
@@ -287,6 +288,7 @@ __device__ void uw_scores(const UWParams<T>& p, const T* sA, unsigned char* ext,
     unsigned long long local = 0;
     for (int64_t i = a0; i < a1; ++i) local += qs[i];
     unsigned long long incl = local;
+    __syncwarp();  // reconverge: a diverged warp takes the slow collective shuffle path
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
@@ -400,6 +402,7 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
       if (tid < 32) {
         double d0 = 0.0;
         for (int j = tid; j < R; j += 32) d0 = fmax(d0, Gm[j * RS + j]);
+        __syncwarp();  // reconverge: a diverged warp takes the slow collective shuffle path
   #pragma unroll
         for (int o = 16; o > 0; o >>= 1) d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
         if (tid == 0) s_tol_als = (double)R * 2.220446049250313e-16 * d0;
@@ -526,6 +529,7 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
       p.rownorm[r0 + il] = rs;
       acc += rs;
     }
+    __syncwarp();  // reconverge: a diverged warp takes the slow collective shuffle path
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
     if ((tid & 31) == 0) sred[tid >> 5] = acc;

@@ -104,3 +104,75 @@ def oracle_gradient_from_fibers(XF, dims, factors, n, strategy, B, idx, pj):
     M = scale * C2
     G = scale * (fs[n] @ C1 - C2)
     return G, Gam, M
+
+
+def row_rel_err(a, b, floor_frac=1e-2):
+    """max over rows of ||a_i - b_i|| / (||b_i|| + floor), floor = floor_frac x the mean row norm of b:
+    a per-row bound next to the Frobenius one (a large error in one row cannot hide in the norm)"""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    rn = np.linalg.norm(b, axis=1)
+    floor = floor_frac * max(float(rn.mean()), 1e-300)
+    return float(np.max(np.linalg.norm(a - b, axis=1) / (rn + floor)))
+
+
+def q_of_cdf(cdf):
+    c = np.asarray(cdf, np.uint64)
+    return np.diff(np.concatenate([np.zeros(1, np.uint64), c])).astype(np.uint64)
+
+
+def trace_check(X, dims, A0, recs, strategy, B, seed, rule, cfg, q_init, alphas=None, tol=None, b=0.0, S0=None,
+                grad=None):
+    """Teacher-forced check of a cp_sgd_trace record list (tests/test_gpu_persistent.py):
+    for every iteration s, from the traced state before it (factors, accumulators and integer tables
+    as the GPU left them):
+      (1) the batch: idx and w bit-exact with oracle.sample on the GPU's integer tables;
+      (2) the update: the oracle's gradient on that batch and its fixed / adaptive step equal the
+          traced A^(n) (and S^(n)) within tol.  b = 0 makes an AdaGrad step eta sign(G) where S was 0:
+          entries whose oracle |G| lies inside the band 10 tol (||A Gamma|| + ||M||) (an fp32 G error
+          that large could flip the sign) are masked, and must be < 1 % of the entries;
+      (3) the rebuilt table: q = diff(traced CDF) equals the oracle's table of the traced factor except
+          entries within 1e-3 of a rounding boundary (|dq| <= 1 there).
+    Returns the number of masked entries."""
+    st = oracle.STRATEGIES[strategy]
+    tol = TOL["f32"] if tol is None else tol
+    A = [np.asarray(a, np.float64).copy() for a in A0]
+    Sacc = [np.zeros_like(a) for a in A] if S0 is None else [np.asarray(s, np.float64).copy() for s in S0]
+    q = [np.asarray(x, np.uint64) for x in q_init]
+    masked = 0
+    for s, rec in enumerate(recs):
+        n, r = rec["n"], rec["r"]
+        tq = [(q[k], int(q[k].sum())) for k in range(len(dims))]
+        idx_o, w_o, pj = oracle.sample(dims, n, st, B, tq, seed, r)
+        assert np.array_equal(rec["idx"], idx_o), f"iteration {s}: indices differ"
+        assert np.array_equal(rec["w"], w_o), f"iteration {s}: weights differ"
+        if grad is None:
+            G_o, Gam_o, M_o = oracle.gradient(X, dims, A, n, st, B, idx_o, pj)
+        else:  # tensors too large for the oracle's own TensorSamp: fibers read from the seeded input
+            G_o, Gam_o, M_o = grad(A, n, idx_o, pj)
+        scale = np.linalg.norm(A[n] @ Gam_o) + np.linalg.norm(M_o)
+        A_g = np.asarray(rec["A"], np.float64)
+        if rule == "fixed":
+            al = cfg.alpha if alphas is None else float(alphas[s])
+            A_o = oracle.update_fixed(A[n], G_o, al)
+            assert rel_err(A_g, A_o, np.linalg.norm(A_o)) <= tol, f"iteration {s}: A"
+            assert row_rel_err(A_g, A_o) <= 10 * tol, f"iteration {s}: A rows"
+        else:
+            A_o, S_o = oracle.update_adaptive(A[n], Sacc[n], G_o, cfg.eta, b=b)
+            S_g = np.asarray(rec["S"], np.float64)
+            assert rel_err(S_g, S_o, np.linalg.norm(S_o)) <= 2 * tol, f"iteration {s}: S"
+            band = np.abs(G_o) <= 10 * tol * scale / np.sqrt(G_o.size)
+            masked += int(band.sum())
+            assert band.mean() < 0.01, f"iteration {s}: {band.mean():.3%} of |G| inside the tolerance band"
+            d = np.where(band, 0.0, A_g - A_o)
+            assert np.linalg.norm(d) <= tol * np.linalg.norm(A_o), f"iteration {s}: A (masked)"
+            assert row_rel_err(np.where(band, A_o, A_g), A_o) <= 10 * tol, f"iteration {s}: A rows (masked)"
+            Sacc[n] = S_g
+        qg = q_of_cdf(rec["cdf"])
+        po, qo, _ = oracle.build_table(st, A_g)
+        diff = qg != qo
+        assert np.all(~diff | near_boundary(po, 1e-3)), f"iteration {s}: table"
+        assert np.all(np.abs(qg.astype(np.int64) - qo.astype(np.int64)) <= 1)
+        A[n] = A_g
+        q[n] = qg
+    return masked

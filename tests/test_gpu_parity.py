@@ -253,6 +253,14 @@ def test_multi_chain_sweeps_equal_separate_runs(dt):
         assert h.iter == 9
         for k in range(3):
             assert np.array_equal(Ads[i][k].cpu().numpy(), ref[i][k])
+    if dt == "f64":  # and every chain equals the oracle's own run of it (Alg. 6 / 7, sampled ALS)
+        rules = {"fixed": oracle.STEP_FIXED, "adaptive": oracle.STEP_ADAPTIVE, "als": oracle.STEP_ALS}
+        for i, (s, seed, rule) in enumerate(specs):
+            fs, _, _ = oracle.run(X, A0, oracle.STRATEGIES[s], rules[rule], cfg.batch, 9, alpha=cfg.alpha, eta=cfg.eta,
+                                  seed=seed)
+            tol = 1e-8 if rule == "als" else 1e-10
+            for k in range(3):
+                assert rel_err(Ads[i][k].cpu().numpy(), fs[k], np.linalg.norm(fs[k])) <= tol, (s, rule, k)
     # a handle of another geometry is refused
     cfg2 = synth.small((40, 30, 21), 6, dtype=dt, batch=64, rule="adaptive", eta=0.05, seed=4)
     X2, A2 = make_problem(cfg2)

@@ -1,0 +1,150 @@
+"""The persistent cooperative sweep kernel of the fp32 wide path (k_sweep_wide) -- the launch bench.py
+times at C4 -- against the CPU oracle, through the C ABI.
+
+* one step per mode from the same seeded state (every strategy, ragged tiles, R up to 64);
+* the debug trace of several cyclic sweeps: every consumed batch bit-exact against oracle.sample fed
+  with the GPU's integer tables of that moment (teacher-forced tables), every rebuilt table equal to
+  the oracle's table of the traced factor except near-boundary entries, and every update within the
+  fp32 tolerance of the oracle's step from the traced state (teacher forcing);
+* block strategies, random mode order, per-iteration step schedules.
+
+Bars: indices and weights bit-exact; G / A / S within 1e-4 relative
+(Frobenius) and a per-row bound; tables within one unit of q only at a rounding boundary.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_helpers import (S, TOL, handle, make_problem, near_boundary, oracle_step, oracle_tables, rel_err,
+                         row_rel_err, to_dev, trace_check)
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+
+    __graft_entry__.build()
+
+
+PW_CASES = [
+    # dims, R, B
+    ((300, 130, 200), 50, 4096),    # C4 shape in miniature: ragged I-tiles (300 = 2*128 + 44), 9 chunks
+    ((260, 140, 96), 20, 512),      # C2-like rank and batch
+    ((132, 70, 45), 48, 1000),      # R = 48, ragged batch (1000 = 31 units + 8); I_2 = 45 < 2R
+    ((200, 64, 33, 20), 10, 1024),  # 4-way
+]
+
+
+@pytest.mark.parametrize("strategy", S)
+@pytest.mark.parametrize("case", PW_CASES, ids=lambda c: "x".join(map(str, c[0])) + f"_R{c[1]}_B{c[2]}")
+@pytest.mark.parametrize("rule", ["fixed", "adaptive"])
+def test_pw_one_step_per_mode(strategy, case, rule):
+    dims, R, B = case
+    cfg = synth.small(dims, R, dtype="f32", batch=B, rule=rule, row_sigma=1.0, noise=1e-2, seed=21, alpha=0.01,
+                      eta=0.05)
+    X, A0 = make_problem(cfg)
+    bpar = 1e-2
+    for n in range(len(dims)):
+        Xd, Ad = to_dev(X, A0)
+        h = handle(cfg, Xd, Ad, strategy, seed=31, b=bpar, fused=False, mode_major=True)
+        assert h.path == "persistent"
+        it = 5 + n
+        h.iter = it
+        idx_o, w_o, G_o, Gam_o, M_o, tabs = oracle_step(X, dims, A0, n, strategy, B, 31, it)
+        h.trace_start(1)
+        h.step(n, cfg.alpha)
+        rec = h.trace_read()[0]
+        assert rec["n"] == n and rec["r"] == it
+        assert np.array_equal(rec["idx"], idx_o) and np.array_equal(rec["w"], w_o)
+        G_g, m, Gam_g = h.get_grad()
+        assert m == n and h.iter == it + 1
+        A64 = np.asarray(A0[n], np.float64)
+        scale = np.linalg.norm(A64 @ Gam_o) + np.linalg.norm(M_o)
+        assert rel_err(G_g, G_o, scale) <= TOL["f32"]
+        assert rel_err(Gam_g, Gam_o, np.linalg.norm(Gam_o)) <= TOL["f32"]
+        if rule == "fixed":
+            A_o = oracle.update_fixed(A64, G_o, cfg.alpha)
+        else:
+            A_o, S_o = oracle.update_adaptive(A64, np.zeros_like(A64), G_o, cfg.eta, b=bpar)
+            assert rel_err(h.get_accum(n), S_o, np.linalg.norm(S_o)) <= 2 * TOL["f32"]
+        A_g = Ad[n].cpu().numpy()
+        assert rel_err(A_g, A_o, np.linalg.norm(A_o)) <= TOL["f32"]
+        assert row_rel_err(A_g, A_o) <= 10 * TOL["f32"]
+        for k in range(len(dims)):
+            if k != n:
+                assert np.array_equal(Ad[k].cpu().numpy(), A0[k])
+        h.close()
+
+
+@pytest.mark.parametrize("strategy", S)
+@pytest.mark.parametrize("rule", ["adaptive", "fixed"])
+def test_pw_trace_teacher_forced(strategy, rule):
+    """four cyclic sweeps in ONE persistent launch: the traced batches, tables and updates of every
+    iteration checked against the oracle from the traced state of that moment."""
+    dims, R, B = (300, 130, 200), 50, 4096
+    cfg = synth.small(dims, R, dtype="f32", batch=B, rule=rule, row_sigma=1.0, noise=1e-2, seed=4, alpha=0.005,
+                      eta=0.03)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, strategy, seed=11, fused=False, mode_major=True)
+    assert h.path == "persistent"
+    h.trace_start(12)
+    h.sweep(4)
+    recs = h.trace_read()
+    assert len(recs) == 12 and [r["n"] for r in recs] == [0, 1, 2] * 4
+    q0 = [h0[1] for h0 in oracle_tables(strategy, A0)]
+    trace_check(X, dims, A0, recs, strategy, B, 11, rule, cfg, q0)
+    for k in range(3):  # the final factors are the traced ones
+        last = max(i for i, r in enumerate(recs) if r["n"] == k)
+        assert np.array_equal(Ad[k].cpu().numpy(), recs[last]["A"])
+    h.close()
+
+
+def test_pw_random_order_and_schedule():
+    """random mode order and a per-iteration fixed-step schedule in one launch."""
+    dims, R, B = (200, 150, 100), 16, 1024
+    cfg = synth.small(dims, R, dtype="f32", batch=B, rule="fixed", row_sigma=1.0, noise=1e-2, seed=6)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "euclidean", seed=2, fused=False, mode_major=True)
+    h.trace_start(9)
+    h.sweep(3, order="random")
+    recs = h.trace_read()
+    modes = [oracle.random_mode(2, r, 3) for r in range(9)]
+    assert [r["n"] for r in recs] == modes
+    q0 = [t[1] for t in oracle_tables("euclidean", A0)]
+    trace_check(X, dims, A0, recs, "euclidean", B, 2, "fixed", cfg, q0)
+    al = 0.004 / (1.0 + np.arange(9)) ** 0.6
+    h.trace_start(9)
+    h.sweep(3, alphas=al)
+    recs2 = h.trace_read()
+    A1 = [a.copy() for a in A0]
+    for r in recs:
+        A1[r["n"]] = r["A"]
+    q1 = list(q0)
+    for r in recs:
+        q1[r["n"]] = np.diff(np.concatenate([[0], r["cdf"]])).astype(np.uint64)
+    trace_check(X, dims, A1, recs2, "euclidean", B, 2, "fixed", cfg, q1, alphas=al)
+    h.close()
+
+
+def test_pw_degenerate_table_stops():
+    """a diverged step makes the next table non-finite: the launch stops and the status surfaces"""
+    from paper_2103_04081_b200 import CPError
+
+    cfg = synth.small((200, 100, 60), 8, dtype="f32", batch=512, rule="fixed", seed=1)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "leverage", fused=False, mode_major=True)
+    assert h.path == "persistent"
+    h.step(0, float("inf"))
+    with pytest.raises(CPError, match="ENONFINITE|EDEGENERATE"):
+        h.sync()
+    h.close()

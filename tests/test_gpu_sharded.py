@@ -67,10 +67,16 @@ def test_virtual_shards_match_single_gpu(strategy, P, mode_major):
         for h in hs:
             h.step_phase(n, 2, cfg.alpha)
     torch.cuda.synchronize()
+    import oracle
+
+    fs, _, _ = oracle.run(X, A0, oracle.STRATEGIES[strategy], oracle.STEP_FIXED, cfg.batch, 3 * N, alpha=cfg.alpha,
+                          seed=5)
     for g in range(P):
         for k in range(N):
             ref = Ad[k].cpu().numpy()
             assert rel_err(facs[g][k].cpu().numpy(), ref, np.linalg.norm(ref)) <= 1e-12
+            # and the oracle's own run (not only the 1-GPU CUDA handle)
+            assert rel_err(facs[g][k].cpu().numpy(), fs[k], np.linalg.norm(fs[k])) <= 1e-10
     # every replica drew the same batches: identical iteration counters
     assert all(h.iter == h1.iter == 3 * N for h in hs)
     for h in hs + [h1]:

@@ -474,9 +474,14 @@ def test_adaptive_update_closed_forms(orc):
     np.testing.assert_allclose(A1, A - 0.3 * np.sign(G), rtol=1e-15, atol=1e-15)
     np.testing.assert_array_equal(S1, G * G)
     G2 = rng.standard_normal((5, 3))
-    A2, S2 = orc.update_adaptive(A1, S1, G2, 0.3, b=0.5, eps=0.1)
+    _, S2 = orc.update_adaptive(A1, S1, G2, 0.3, b=0.5, eps=0.1)
     assert np.all(S2 >= S1)
-    np.testing.assert_allclose(A2, A1 - 0.3 * G2 / (0.5 + S1 + G2 ** 2) ** 0.6, rtol=1e-14)
+    # b, eps > 0, a value worked by hand: A = 1, S = 1.5, G = 0.5, eta = 0.4, b = 0.5, eps = 0.25:
+    # S <- 1.5 + 0.25 = 1.75; (b + S)^(1/2 + eps) = 2.25^0.75 = (1.5^2)^0.75 = 1.5^1.5 = 1.8371173070873836;
+    # A <- 1 - 0.4 * 0.5 / 1.8371173070873836 = 1 - 0.10886621079036349 = 0.8911337892096365
+    A4, S4 = orc.update_adaptive(np.ones((1, 1)), np.full((1, 1), 1.5), np.full((1, 1), 0.5), 0.4, b=0.5, eps=0.25)
+    assert S4[0, 0] == 1.75
+    assert abs(A4[0, 0] - 0.8911337892096365) <= 4e-16
     # scalar case: A=1, G=2, eta=1, b=eps=0: S=4, A <- 1 - 2/2 = 0
     A3, S3 = orc.update_adaptive(np.ones((1, 1)), np.zeros((1, 1)), 2 * np.ones((1, 1)), 1.0)
     assert A3[0, 0] == 0.0 and S3[0, 0] == 4.0
@@ -625,3 +630,20 @@ def test_spread_magnitude_generator():
     np.testing.assert_allclose(X0c, synth.cp_tensor(fc), rtol=0, atol=0)
     with pytest.raises(ValueError):
         synth.spread_magnitude(5, 4, 3, 6, 1.0)
+
+
+def test_run_f32_entry_reads_the_same_tensor(orc):
+    """orc_run_f32 (fp32-stored tensor, element converted to fp64 on read; the bench's C4 baseline)
+    equals orc_run on the fp64 copy of the same tensor bit for bit (the conversion is exact)."""
+    import synth
+
+    cfg = synth.small((9, 8, 7), 3, dtype="f32", batch=20, rule="adaptive", seed=5, eta=0.05)
+    X = synth.tensor(cfg)
+    assert X.dtype == np.float32
+    A0 = synth.init_factors(cfg, X)
+    for st, rule in ((orc.LEVERAGE, orc.STEP_ADAPTIVE), (orc.BLOCK_EUCLIDEAN, orc.STEP_FIXED)):
+        f32, S32, m32 = orc.run(X, A0, st, rule, cfg.batch, 7, eta=0.05, alpha=0.01, seed=3)
+        f64, S64, m64 = orc.run(X.astype(np.float64), A0, st, rule, cfg.batch, 7, eta=0.05, alpha=0.01, seed=3)
+        for a, b in zip(f32 + S32, f64 + S64):
+            np.testing.assert_array_equal(a, b)
+        np.testing.assert_array_equal(m32, m64)
