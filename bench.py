@@ -7,15 +7,17 @@
 A "step" is one cyclic sweep: N_modes SGD iterations (one per mode), each running the whole hot
 path -- table refresh (a1), sampling (a2, a3), SKR + fiber gather + contractions (a4-a6),
 fixed/adaptive update (a7, a8) -- i.e. every SURVEY §8(a) row including the mode loop (a9).
-metric = sampled fibers/s (whole job).  Default workload: BASELINE.json configs[1] (C2, 400^3
-fp32, R = 20, B = 512, adaptive step), seeded synthetic data.
+metric = sampled fibers/s (whole job).  Default workload: BASELINE.json configs[3] (C4, 2000^3 fp32
+= 32 GB, R = 50, B = 4096, adaptive step, leverage sampling) -- the largest configuration that fits one
+GPU and the one whose fiber gather is HBM-bound; seeded synthetic data.
 
 Multi-GPU (torchrun, one process per GPU): workloads that fit one GPU (C1-C4) run one independent
 chain per GPU (different Philox seed, no collective; "scaling": "weak"); C5 runs slab-sharded
 along the last mode with the NCCL allreduce / row broadcast inside the library ("strong").
 
 --impl reference times the CPU oracle (oracle/liborc.so, single thread) on rank 0 on the same
-workload (the paper publishes no GPU baseline).
+workload, one SGD iteration (B fibers) per step (the paper publishes no GPU baseline; DESIGN.md
+"Measurement").
 """
 from __future__ import annotations
 
@@ -116,6 +118,47 @@ def make_inputs(cfg, device, seed_offset=0, slab=None):
     return Xd, A0, None, None
 
 
+def workload_str(cfg, sampler):
+    """identical in both arms (the driver compares them)"""
+    return (f"{cfg.name}: {'x'.join(map(str, cfg.dims))} {cfg.dtype}, R={cfg.rank}, B={cfg.batch}, {cfg.rule} step, "
+            f"{sampler} sampling, cyclic mode order")
+
+
+def host_info():
+    info = {"nproc": os.cpu_count()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu"] = line.split(":", 1)[1].strip()
+                break
+        info["mem_gb"] = round(os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2 ** 30, 1)
+    except Exception:
+        pass
+    return info
+
+
+def host_inputs(cfg):
+    """the seeded tensor and initial factors on the host (numpy): the numpy recipe for tensors up to
+    2e8 elements; larger ones are generated by the torch recipe on the GPU and copied to the host
+    (fp32, read in place by the oracle's fp32 entry)"""
+    if cfg.numel <= 200_000_000:
+        X = synth.tensor(cfg)
+        return X, synth.init_factors(cfg, X)
+    import torch
+
+    dev = torch.device("cuda:0")
+    Xd, _, xn = synth.tensor_torch(cfg, device=dev)
+    A0 = [a.cpu().numpy() for a in synth.init_factors_torch(cfg, xn, device=dev)]
+    X = np.empty(cfg.numel, dtype=np.float32 if cfg.dtype == "f32" else np.float64)
+    Xt = torch.from_numpy(X)
+    chunk = 1 << 28
+    for a in range(0, cfg.numel, chunk):
+        Xt[a:a + chunk].copy_(Xd[a:a + chunk])
+    del Xd
+    torch.cuda.empty_cache()
+    return X, A0
+
+
 # ----------------------------------------------------------------------------------------------
 def run_chains(args, cfg):
     """--chains K: K independent chains of the workload (same tensor, own factors
@@ -206,6 +249,7 @@ def run_ours(args, cfg):
                   nccl_id=nccl_id, slab=slab, mode_major=not args.native_layout, fused=args.path == "auto",
                   tc=not args.no_tc)
     init_s = time.time() - t0
+    h_path = h.path
     N = cfg.order
     fibers_per_step = sum(h.batch_max(n) for n in range(N)) if args.sampler.startswith("block") else N * cfg.batch
 
@@ -266,11 +310,12 @@ def run_ours(args, cfg):
     gather_bytes = (fibers_per_step / N) * In_avg * esz
     useful_gbs = value * (sum(cfg.dims) / N) * esz / 1e9
     GATHERS = ("k_gather_update_tc", "k_gather_update", "k_gather")
+    PERSISTENT = ("k_sweep_fused", "k_sweep_wide")  # whole sweeps per launch
 
     def roofline_of(name):
         """HBM roofline of one kernel: algorithmic bytes per launch (the sampled fibers it gathers,
         B_eff x I_n x sizeof per SGD iteration) / its average CUDA-event duration."""
-        if name == "k_sweep_fused":
+        if name in PERSISTENT:
             per_launch = prof_sweeps * fibers_per_step * (sum(cfg.dims) / N) * esz
         elif name in GATHERS:
             per_launch = gather_bytes
@@ -303,9 +348,10 @@ def run_ours(args, cfg):
         if gname in kern:
             gather_roof = roofline_of(gname)
             break
-    if roof is not None and dominant == "k_sweep_fused":
-        roof["note"] = ("latency-bound chain: per-step phases are serial (sample -> gather -> reduce -> update -> "
-                        "table -> sample); see DESIGN.md 'Roofline'")
+    if roof is not None and dominant in PERSISTENT:
+        roof["note"] = ("one launch runs every phase of every SGD iteration of the timed sweeps (sample -> gather -> "
+                        "update -> table -> sample, serial by the method: R9); achieved = the sampled fibers' "
+                        "bytes over the whole launch. The gather phase alone: phases.gather_roofline")
     # ---- e2e: host-buffer C-ABI call, H2D of all factors + D2H every step ----
     host = [a.detach().cpu().pin_memory() for a in Ad]
     h2d = sum(a.numel() * esz for a in host)
@@ -334,9 +380,9 @@ def run_ours(args, cfg):
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None,
             "dtype": "f64" if cfg.dtype == "f64" else "f32", "data": "synthetic (seeded; synth/ recipe)",
-            "config": {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.dims))} {cfg.dtype}, R={cfg.rank}, "
-                                   f"B={cfg.batch}, {cfg.rule} step, {args.sampler} sampling, cyclic sweeps",
+            "config": {"workload": workload_str(cfg, args.sampler),
                        "step": f"one cyclic sweep = {N} SGD iterations x B fibers",
+                       "sampler": args.sampler,
                        "iterations_per_s": round(N * args.steps * (1 if sharded else ws) / (ms / 1e3), 1),
                        "useful_GBps": round(useful_gbs, 2),
                        "layout": "native" if args.native_layout else "mode-major copies (CP_FLAG_MODE_MAJOR)",
@@ -349,6 +395,8 @@ def run_ours(args, cfg):
             "kernels": {k: {"avg_us": round(v["avg_us"], 3), "share": round(v["share"], 4), "count": v["count"]}
                         for k, v in kern.items()},
             "kernel_timing": f"CUDA events around each launch on the library stream, {prof_sweeps} direct-launch sweeps",
+            "path": h_path,
+            "phases": None,
             "clocks": clocks,
             "e2e": {"value": round(e2e_val, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": h2d,
@@ -356,67 +404,108 @@ def run_ours(args, cfg):
             "gpu_launches": launches,
         }
     h.close()
+    if res is not None and h_path == "persistent" and not args.no_phases:
+        res["phases"] = phase_profile(args, cfg, Xd, Ad, stream, fibers_per_step / N, In_avg, esz, peaks)
     return res
 
 
-def cpu_baseline(cfg, args, budget_s=12.0):
-    """the oracle as it stands, single thread, on a bounded sample of the same workload."""
+def phase_profile(args, cfg, Xd, Ad, stream, fibers_per_iter, In_avg, esz, peaks, sweeps=3):
+    """in-kernel phase timeline of the persistent wide kernel (CTA 0, clock64 at the phase boundaries; a
+    second handle built with CPSGD_DEBUG_TIMERS on the same inputs, after the measured one): per SGD
+    iteration, microseconds per phase, and the gather phase's HBM roofline (the sampled fibers' bytes /
+    the time from the sampling barrier to the gather barrier, every CTA's gather included)"""
+    import torch
+
+    from paper_2103_04081_b200 import CPSGD
+
+    os.environ["CPSGD_DEBUG_TIMERS"] = "1"
+    try:
+        with torch.cuda.stream(stream):
+            h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=args.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta,
+                      seed=cfg.seed + 7, stream=stream, mode_major=not args.native_layout, fused=args.path == "auto",
+                      tc=not args.no_tc)
+    finally:
+        del os.environ["CPSGD_DEBUG_TIMERS"]
+    h.sweep(sweeps)
+    h.sync()
+    d = np.array(h.debug_timers()[512:512 + 256], dtype=np.int64).reshape(8, 32)
+    h.close()
+    its = [s for s in range(1, min(8, 3 * sweeps)) if d[s, 0] and d[s, 10] and d[s, 30] and d[s, 31]]
+    if not its:
+        return None
+    ghz = float(np.mean([(d[s, 10] - d[s, 0]) / (d[s, 31] - d[s, 30]) for s in its]))
+    seq = [("sample", 0, 1), ("barrier_S", 1, 2), ("gather", 2, 3), ("barrier_G", 3, 4), ("update", 4, 5),
+           ("barrier_U", 5, 6), ("gram_pairs", 6, 7), ("inverse_scores_scan", 7, 9), ("barrier_Q", 9, 10)]
+    out = {k: round(float(np.mean([(d[s, b] - d[s, a]) / ghz / 1e3 for s in its])), 2) for k, a, b in seq}
+    out["iteration_us"] = round(float(np.mean([(d[s, 10] - d[s, 0]) / ghz / 1e3 for s in its])), 2)
+    t_g = float(np.mean([(d[s, 4] - d[s, 2]) / ghz for s in its])) * 1e-9
+    ach = fibers_per_iter * In_avg * esz / t_g / 1e9
+    out["gather_roofline"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                              "frac": round(ach / peaks["hbm_gbs"], 4),
+                              "window": "sampling barrier -> gather barrier (every CTA's gather + the barrier)"}
+    out["how"] = ("clock64 marks of CTA 0 at the phase boundaries of iterations 1..; CPSGD_DEBUG_TIMERS handle "
+                  f"(SM clock {round(ghz * 1e3)} MHz)")
+    return out
+
+
+def cpu_baseline(cfg, args, budget_s=15.0, inputs=None):
+    """the oracle as it stands (single thread, fp64 arithmetic) on a bounded sample of the same workload:
+    whole SGD iterations (one mode update of B fibers each, cyclic modes) until ~budget_s of CPU time"""
     import oracle
 
-    X = synth.tensor(cfg)
-    A0 = synth.init_factors(cfg, X)
-    X64 = X.astype(np.float64)
+    X, A0 = inputs if inputs is not None else host_inputs(cfg)
     st = oracle.STRATEGIES[args.sampler]
     rule = {"adaptive": oracle.STEP_ADAPTIVE, "als": oracle.STEP_ALS}.get(cfg.rule, oracle.STEP_FIXED)
     iters, t_used = 0, 0.0
-    fs = A0
+    fs, S = A0, None
     while t_used < budget_s and iters < 3 * 200:
         t0 = time.perf_counter()
-        fs, _, _ = oracle.run(X64, fs, st, rule, cfg.batch, cfg.order, alpha=cfg.alpha, eta=cfg.eta,
-                              seed=cfg.seed, r0=iters)
+        fs, S, _ = oracle.run(X, fs, st, rule, cfg.batch, 1, alpha=cfg.alpha, eta=cfg.eta, seed=cfg.seed, r0=iters,
+                              S=S, first_mode=iters % cfg.order)
         t_used += time.perf_counter() - t0
-        iters += cfg.order
+        iters += 1
     fib = iters * cfg.batch
     return {"value": round(fib / t_used, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{iters} oracle iterations ({iters // cfg.order} cyclic sweeps) of {cfg.name}, "
-                      f"{args.sampler}, fp64 single-threaded C (-O2), tensor host-resident; per-iteration "
-                      f"table rebuild by Householder QR included", "seconds": round(t_used, 2)}
+            "sample": f"{iters} oracle SGD iterations (cyclic modes from 0, B = {cfg.batch} fibers each) of "
+                      f"{workload_str(cfg, args.sampler)}; fp64 single-threaded C (-O2), tensor host-resident "
+                      f"({'fp32, read in place' if X.dtype == np.float32 else 'fp64'}); per-iteration table rebuild "
+                      f"by Householder QR included", "seconds": round(t_used, 2), "host": host_info()}
 
 
 def run_reference(args, cfg):
+    """the reference arm: the CPU oracle (there is no reference implementation: the paper is the
+    reference) on the same workload, one SGD iteration of B fibers per step, rank 0 only"""
     ws, rank, _ = dist_env()
     if rank != 0:
         return None
     import oracle
 
-    X = synth.tensor(cfg)
-    A0 = synth.init_factors(cfg, X)
-    X64 = X.astype(np.float64)
+    X, A0 = host_inputs(cfg)
     st = oracle.STRATEGIES[args.sampler]
     rule = {"adaptive": oracle.STEP_ADAPTIVE, "als": oracle.STEP_ALS}.get(cfg.rule, oracle.STEP_FIXED)
-    fs = A0
+    fs, S = A0, None
     r = 0
     for _ in range(args.warmup):
-        fs, _, _ = oracle.run(X64, fs, st, rule, cfg.batch, cfg.order, alpha=cfg.alpha, eta=cfg.eta, seed=cfg.seed,
-                              r0=r)
-        r += cfg.order
+        fs, S, _ = oracle.run(X, fs, st, rule, cfg.batch, 1, alpha=cfg.alpha, eta=cfg.eta, seed=cfg.seed, r0=r, S=S,
+                              first_mode=r % cfg.order)
+        r += 1
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        fs, _, _ = oracle.run(X64, fs, st, rule, cfg.batch, cfg.order, alpha=cfg.alpha, eta=cfg.eta, seed=cfg.seed,
-                              r0=r)
-        r += cfg.order
+        fs, S, _ = oracle.run(X, fs, st, rule, cfg.batch, 1, alpha=cfg.alpha, eta=cfg.eta, seed=cfg.seed, r0=r, S=S,
+                              first_mode=r % cfg.order)
+        r += 1
     dt = time.perf_counter() - t0
-    fib = args.steps * cfg.order * cfg.batch
+    fib = args.steps * cfg.batch
     val = fib / dt
     return {"impl": "reference", "metric": METRIC, "value": round(val, 1), "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded; synth/ recipe)",
-            "config": {"workload": f"{cfg.name}: {'x'.join(map(str, cfg.dims))}, R={cfg.rank}, B={cfg.batch}, "
-                                   f"{cfg.rule} step, {args.sampler} sampling, cyclic sweeps",
-                       "step": f"one cyclic sweep = {cfg.order} SGD iterations x B fibers"},
+            "config": {"workload": workload_str(cfg, args.sampler),
+                       "step": f"one SGD iteration = B = {cfg.batch} fibers (modes cyclic)"},
             "cpu_baseline": {"value": round(val, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} full sweeps of {cfg.name} (fp64 oracle, single thread)"},
+                             "sample": f"{args.steps} SGD iterations of {cfg.name} (fp64 oracle, single thread)",
+                             "host": host_info()},
             "e2e": {"value": round(val, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -426,11 +515,12 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C2", choices=list(synth.CONFIGS))
+    ap.add_argument("--workload", default="C4", choices=list(synth.CONFIGS))
     ap.add_argument("--sampler", default="leverage",
                     choices=["uniform", "leverage", "euclidean", "block_leverage", "block_euclidean"])
     ap.add_argument("--native-layout", action="store_true", help="no mode-major copies")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-phases", action="store_true", help="skip the in-kernel phase timeline of the persistent kernel")
     ap.add_argument("--path", default="auto", choices=["auto", "wide"],
                     help="auto: persistent single-cluster kernel when the problem fits one cluster; wide: the "
                          "gather (tcgen05) + table/sampling kernel pair")
@@ -464,7 +554,7 @@ def main():
         import torch.distributed  # noqa: F401
     res = run_ours(args, cfg)
     if rank == 0:
-        if not args.no_cpu_baseline and ws == 1 and cfg.numel <= 200_000_000:
+        if not args.no_cpu_baseline and ws == 1:
             res["cpu_baseline"] = cpu_baseline(cfg, args)
         print(json.dumps(res), flush=True)
     if ws > 1:

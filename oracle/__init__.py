@@ -68,6 +68,8 @@ def lib():
         L.orc_random_mode.argtypes = [u64, u64, i32]
         L.orc_run.argtypes = [i32, P, i32, P, P, P, i32, i32, i32, i64, P, dbl, P, dbl, dbl, dbl, u64, u64, i64, P]
         L.orc_run_f32.argtypes = L.orc_run.argtypes
+        L.orc_run_from.argtypes = [i32, P, i32, P, i32, P, P, i32, i32, i32, i32, i64, P, dbl, P, dbl, dbl, dbl, u64,
+                                   u64, i64, P]
         _lib = L
     return _lib
 
@@ -258,7 +260,7 @@ def random_mode(seed: int, it: int, N: int) -> int:
 
 
 def run(X, factors, strategy: int, rule: int, B: int, iters: int, *, order=ORDER_CYCLIC, window=None,
-        alpha=0.0, alphas=None, eta=0.1, b=0.0, eps=0.0, seed=0, r0=0, S=None):
+        alpha=0.0, alphas=None, eta=0.1, b=0.0, eps=0.0, seed=0, r0=0, S=None, first_mode=0):
     """Alg. 6 / Alg. 7 for `iters` iterations.  Returns (factors, S, modes); inputs are copied."""
     fs = [_f64(A).copy() for A in factors]
     d = _dims([A.shape[0] for A in fs])
@@ -271,8 +273,8 @@ def run(X, factors, strategy: int, rule: int, B: int, iters: int, *, order=ORDER
     win = None if window is None else np.ascontiguousarray(window, dtype=np.int32)
     al = None if alphas is None else _f64(alphas)
     modes = np.zeros(max(iters, 1), dtype=np.int32)
-    fn = lib().orc_run_f32 if x32 else lib().orc_run
-    _chk(fn(N, _p(d), R, _p(Xf), _ptrs(fs), _ptrs(Ss), strategy, rule, order, B,
+    _chk(lib().orc_run_from(N, _p(d), R, _p(Xf), 1 if x32 else 0, _ptrs(fs), _ptrs(Ss), strategy, rule, order,
+                            int(first_mode), B,
                        None if win is None else _p(win), alpha, None if al is None else _p(al), eta, b, eps,
                        C.c_uint64(seed), C.c_uint64(r0), iters, _p(modes)), "run")
     return fs, Ss, modes[:iters]

@@ -641,9 +641,9 @@ int orc_random_mode(uint64_t seed, uint64_t iter, int N) {
  * alpha0.  Workspace is allocated here.  modes_out (optional) records n per iteration.
  * ---------------------------------------------------------------------------------- */
 static int orc_run_x(int N, const int64_t* dims, int R, const void* X, int xf32, double* const* factors,
-                     double* const* S, int strategy, int rule, int order, int64_t B, const int32_t* window,
-                     double alpha0, const double* alpha, double eta, double bpar, double eps, uint64_t seed,
-                     uint64_t r0, int64_t iters, int32_t* modes_out) {
+                     double* const* S, int strategy, int rule, int order, int first_mode, int64_t B,
+                     const int32_t* window, double alpha0, const double* alpha, double eta, double bpar, double eps,
+                     uint64_t seed, uint64_t r0, int64_t iters, int32_t* modes_out) {
   if (N < 3 || N > 16 || R < 1 || B < 1) return ORC_EINVAL;
   uint64_t* q[16];
   uint64_t T[16];
@@ -671,7 +671,7 @@ static int orc_run_x(int N, const int64_t* dims, int R, const void* X, int xf32,
   for (int k = 0; k < N && !st; ++k) st = orc_build_table(strategy, dims[k], R, factors[k], NULL, q[k], &T[k]);
   for (int64_t it = 0; it < iters && !st; ++it) {
     uint64_t r = r0 + (uint64_t)it;
-    int n = (order == ORC_ORDER_RANDOM) ? orc_random_mode(seed, r, N) : (int)(it % N);
+    int n = (order == ORC_ORDER_RANDOM) ? orc_random_mode(seed, r, N) : (int)((first_mode + it) % N);
     if (modes_out) modes_out[it] = n;
     int64_t Beff = 0;
     st = orc_sample(N, dims, n, strategy, B, window, (const uint64_t* const*)q, T, seed, r, idx, w, pj, &Beff);
@@ -696,8 +696,8 @@ int orc_run(int N, const int64_t* dims, int R, const double* X, double* const* f
             int strategy, int rule, int order, int64_t B, const int32_t* window, double alpha0,
             const double* alpha, double eta, double bpar, double eps, uint64_t seed, uint64_t r0, int64_t iters,
             int32_t* modes_out) {
-  return orc_run_x(N, dims, R, X, 0, factors, S, strategy, rule, order, B, window, alpha0, alpha, eta, bpar, eps, seed,
-                   r0, iters, modes_out);
+  return orc_run_x(N, dims, R, X, 0, factors, S, strategy, rule, order, 0, B, window, alpha0, alpha, eta, bpar, eps,
+                   seed, r0, iters, modes_out);
 }
 
 /* orc_run on an fp32-stored tensor (each element converted to fp64 on read; factors, accumulators and
@@ -706,6 +706,17 @@ int orc_run_f32(int N, const int64_t* dims, int R, const float* X, double* const
                 int strategy, int rule, int order, int64_t B, const int32_t* window, double alpha0,
                 const double* alpha, double eta, double bpar, double eps, uint64_t seed, uint64_t r0, int64_t iters,
                 int32_t* modes_out) {
-  return orc_run_x(N, dims, R, X, 1, factors, S, strategy, rule, order, B, window, alpha0, alpha, eta, bpar, eps, seed,
-                   r0, iters, modes_out);
+  return orc_run_x(N, dims, R, X, 1, factors, S, strategy, rule, order, 0, B, window, alpha0, alpha, eta, bpar, eps,
+                   seed, r0, iters, modes_out);
+}
+
+/* orc_run / orc_run_f32 with the cyclic order starting at mode first_mode (iteration it of the call
+ * updates mode (first_mode + it) mod N): a run split into calls continues the sweep */
+int orc_run_from(int N, const int64_t* dims, int R, const void* X, int xf32, double* const* factors,
+                 double* const* S, int strategy, int rule, int order, int first_mode, int64_t B,
+                 const int32_t* window, double alpha0, const double* alpha, double eta, double bpar, double eps,
+                 uint64_t seed, uint64_t r0, int64_t iters, int32_t* modes_out) {
+  if (first_mode < 0 || first_mode >= N) return ORC_EINVAL;
+  return orc_run_x(N, dims, R, X, xf32, factors, S, strategy, rule, order, first_mode, B, window, alpha0, alpha, eta,
+                   bpar, eps, seed, r0, iters, modes_out);
 }

@@ -129,8 +129,8 @@ def trace_check(X, dims, A0, recs, strategy, B, seed, rule, cfg, q_init, alphas=
       (1) the batch: idx and w bit-exact with oracle.sample on the GPU's integer tables;
       (2) the update: the oracle's gradient on that batch and its fixed / adaptive step equal the
           traced A^(n) (and S^(n)) within tol.  b = 0 makes an AdaGrad step eta sign(G) where S was 0:
-          entries whose oracle |G| lies inside the band 10 tol (||A Gamma|| + ||M||) (an fp32 G error
-          that large could flip the sign) are masked, and must be < 1 % of the entries;
+          such entries whose oracle |G| lies inside the band 10 tol (||A Gamma|| + ||M||) / sqrt(I_n R)
+          (an fp32 G error that large could flip the sign) are masked, and must be < 5 % of the entries;
       (3) the rebuilt table: q = diff(traced CDF) equals the oracle's table of the traced factor except
           entries within 1e-3 of a rounding boundary (|dq| <= 1 there).
     Returns the number of masked entries."""
@@ -161,9 +161,11 @@ def trace_check(X, dims, A0, recs, strategy, B, seed, rule, cfg, q_init, alphas=
             A_o, S_o = oracle.update_adaptive(A[n], Sacc[n], G_o, cfg.eta, b=b)
             S_g = np.asarray(rec["S"], np.float64)
             assert rel_err(S_g, S_o, np.linalg.norm(S_o)) <= 2 * tol, f"iteration {s}: S"
-            band = np.abs(G_o) <= 10 * tol * scale / np.sqrt(G_o.size)
+            # sign-sensitive entries: never updated before (S = 0: the step is eta sign(G)) and |G| inside
+            # the band an fp32 G error could cross
+            band = (Sacc[n] == 0.0) & (np.abs(G_o) <= 10 * tol * scale / np.sqrt(G_o.size))
             masked += int(band.sum())
-            assert band.mean() < 0.01, f"iteration {s}: {band.mean():.3%} of |G| inside the tolerance band"
+            assert band.mean() < 0.05, f"iteration {s}: {band.mean():.3%} of the entries masked"
             d = np.where(band, 0.0, A_g - A_o)
             assert np.linalg.norm(d) <= tol * np.linalg.norm(A_o), f"iteration {s}: A (masked)"
             assert row_rel_err(np.where(band, A_o, A_g), A_o) <= 10 * tol, f"iteration {s}: A rows (masked)"

@@ -647,3 +647,23 @@ def test_run_f32_entry_reads_the_same_tensor(orc):
         for a, b in zip(f32 + S32, f64 + S64):
             np.testing.assert_array_equal(a, b)
         np.testing.assert_array_equal(m32, m64)
+
+
+def test_run_split_into_calls_continues_the_sweep(orc):
+    """orc_run_from: 7 single-iteration calls (first mode r mod N, accumulators carried, counter r0 = r)
+    equal one 7-iteration cyclic run bit for bit (the bench's bounded baseline samples run this way)."""
+    import synth
+
+    cfg = synth.small((8, 7, 6), 3, dtype="f64", batch=16, rule="adaptive", seed=2, eta=0.05)
+    X = synth.tensor(cfg)
+    A0 = synth.init_factors(cfg, X)
+    ref, Sref, mref = orc.run(X, A0, orc.EUCLIDEAN, orc.STEP_ADAPTIVE, cfg.batch, 7, eta=0.05, seed=9)
+    fs, S = A0, None
+    modes = []
+    for r in range(7):
+        fs, S, m = orc.run(X, fs, orc.EUCLIDEAN, orc.STEP_ADAPTIVE, cfg.batch, 1, eta=0.05, seed=9, r0=r, S=S,
+                           first_mode=r % 3)
+        modes.append(int(m[0]))
+    assert modes == list(mref)
+    for a, b in zip(fs + S, ref + Sref):
+        np.testing.assert_array_equal(a, b)
