@@ -133,7 +133,10 @@ __device__ __forceinline__ void gather_contract(const T* xs, int64_t Ip, int64_t
 #pragma unroll
       for (int u = 0; u < ROWS; ++u) {
         const int i = tid + u * kFThreads;
-        xv[c][u] = (lb < BPC && i < In) ? xs[lb * Ip + i] : T(0);  // padding fibers are staged as zeros
+        // clamped unconditional load, then select (a conditional load compiles to a branch per load);
+        // padding fibers are staged as zeros
+        const T t = xs[(lb < BPC ? lb : BPC - 1) * Ip + (i < In ? i : In - 1)];
+        xv[c][u] = (lb < BPC && i < In) ? t : T(0);
       }
     }
     if (dbg && c0 < 2 * CH) {
@@ -317,7 +320,8 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
         const uint64_t* c = s_cp[k];
         const int64_t istar = upper_bound_u64(c, p.dims[k], rr);
         const int64_t s0 = (istar / bk) * bk, e0 = min(s0 + bk, p.dims[k]);
-        const uint64_t Q = c[e0 - 1] - (s0 > 0 ? c[s0 - 1] : 0ull);
+        const uint64_t cprev = c[s0 > 0 ? s0 - 1 : 0];  // unconditional load, then select
+        const uint64_t Q = c[e0 - 1] - (s0 > 0 ? cprev : 0ull);
         s_start[pos] = (int32_t)s0;
         s_len[pos] = (int32_t)(e0 - s0);
         const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * Q), (double)Tk);
@@ -348,7 +352,8 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
         } else {
           const uint64_t* c = s_cp[k];
           i = upper_bound_u64(c, p.dims[k], rr);
-          qk = c[i] - (i > 0 ? c[i - 1] : 0ull);
+          const uint64_t cprev = c[i > 0 ? i - 1 : 0];  // unconditional load, then select
+          qk = c[i] - (i > 0 ? cprev : 0ull);
         }
         ix[e] = (int32_t)i;
         ptm[e] = __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);
@@ -443,9 +448,15 @@ __device__ __forceinline__ void fused_body(const FusedParams<T>& p) {
 #pragma unroll
           for (int u = 0; u < kSU; ++u) {
             const int e = e0 + u * kFThreads + tid, rr = e % RP;
-            const int32_t* ib = ix + lbu[u] * NP;
-            f0[u] = act[u] ? p.factors[k0][(int64_t)ib[pos] * R + rr] : T(0);
-            f1[u] = (act[u] && two) ? p.factors[k1][(int64_t)ib[pos + 1] * R + rr] : T(0);
+            // every load issued (a valid address: row 0 for inactive entries), then selected: a
+            // conditional load compiles to a branch per load
+            const int32_t* ibs = ix + (lbu[u] < p.BPC ? lbu[u] : p.BPC - 1) * NP;
+            const int rc = rr < R ? rr : R - 1;
+            const int32_t i0 = ibs[pos], i1 = two ? ibs[pos + 1] : 0;
+            const T t0 = p.factors[k0][(int64_t)(act[u] ? i0 : 0) * R + rc];
+            const T t1 = p.factors[two ? k1 : k0][(int64_t)((act[u] && two) ? i1 : 0) * R + rc];
+            f0[u] = act[u] ? t0 : T(0);
+            f1[u] = (act[u] && two) ? t1 : T(0);
           }
 #pragma unroll
           for (int u = 0; u < kSU; ++u) {

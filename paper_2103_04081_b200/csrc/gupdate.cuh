@@ -83,7 +83,10 @@ __device__ __forceinline__ void gu_gamma_sum(const GUParams<T>& p, int e0, int e
     T v[16], s = T(0);
     for (int c0 = 0; c0 < p.ncl; c0 += 16) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = (c0 + k < p.ncl) ? __ldcg(p.gcl + (int64_t)(c0 + k) * E + e) : T(0);
+      for (int k = 0; k < 16; ++k) {  // clamped unconditional loads, then masked (no branch per load)
+        const T t = __ldcg(p.gcl + (int64_t)(c0 + k < p.ncl ? c0 + k : p.ncl - 1) * E + e);
+        v[k] = c0 + k < p.ncl ? t : T(0);
+      }
 #pragma unroll
       for (int k = 0; k < 16; ++k) s += v[k];  // cluster order; zeros past ncl are exact
     }

@@ -217,7 +217,10 @@ __global__ void __launch_bounds__(kTCThreads, 1) k_gather_update_tc(GUParams<flo
         const int kk = 4 * kq + u, lb = f0 + kk;
         const bool ok = lb < nfib && sfb[lb] >= 0;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) x[u][a] = ok ? A[kk * 128 + iq + 32 * a] : 0.f;
+        for (int a = 0; a < 4; ++a) {  // load unconditionally (inside the ring), then select: a
+          const float t = A[kk * 128 + iq + 32 * a];  // conditional load compiles to a branch per load
+          x[u][a] = ok ? t : 0.f;
+        }
       }
       mbar_arrive(&xempty[slot]);  // raw stage consumed (values are in registers)
 #pragma unroll

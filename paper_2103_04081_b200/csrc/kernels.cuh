@@ -423,7 +423,8 @@ __device__ __forceinline__ void draw_rows(const SampleParams& p, const uint64_t*
       const int64_t istar = upper_bound_u64(c, p.dims[k], rr);   // == window draw (R6)
       const int64_t s0 = (istar / bk) * bk;
       const int64_t e0 = min(s0 + bk, p.dims[k]);
-      const uint64_t Q = c[e0 - 1] - (s0 > 0 ? c[s0 - 1] : 0ull);
+      const uint64_t cprev = c[s0 > 0 ? s0 - 1 : 0];  // unconditional load, then select
+      const uint64_t Q = c[e0 - 1] - (s0 > 0 ? cprev : 0ull);
       start[pos] = (int32_t)s0;
       len[pos] = (int32_t)(e0 - s0);
       const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * Q), (double)Tk);
@@ -459,7 +460,8 @@ __device__ __forceinline__ void draw_rows(const SampleParams& p, const uint64_t*
         } else {
           const uint64_t* c = cdfp[k];
           i = upper_bound_u64(c, p.dims[k], rr);
-          qk = c[i] - (i > 0 ? c[i - 1] : 0ull);
+          const uint64_t cprev = c[i > 0 ? i - 1 : 0];  // unconditional load, then select
+          qk = c[i] - (i > 0 ? cprev : 0ull);
         }
         ib[pos] = (int32_t)i;
         const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);

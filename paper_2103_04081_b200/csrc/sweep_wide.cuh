@@ -106,7 +106,8 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
-  while ((int)(ld_acquire_u32(p) - target) < 0) __nanosleep(40);
+  while ((int)(ld_acquire_u32(p) - target) < 0) {
+  }
 }
 __device__ __forceinline__ void grid_barrier(unsigned* cnt, unsigned& nbar) {
   __syncthreads();
@@ -138,7 +139,7 @@ __device__ __forceinline__ void ldcg_copy_u64(uint64_t* dst, const uint64_t* src
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int64_t i = i0 + (int64_t)u * nth;
-      v[u] = i < n ? __ldcg(src + i) : 0ull;
+      v[u] = __ldcg(src + (i < n ? i : n - 1));  // unconditional (clamped) load: no branch per load
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -157,9 +158,11 @@ __host__ __device__ inline size_t pw_other_bytes(int N, int R, int64_t cdf_elems
   const size_t sample = 16 * 8 + sizeof(uint64_t) * (cdf_elems + kMaxOrder) + sizeof(int32_t) * kPWFib * (N - 1) +
                         sizeof(double) * kPWFib * (N - 1) + sizeof(double) * kPWFib + sizeof(float) * kPWFib * RP +
                         sizeof(float) * (size_t)zg_groups(R, kPWThreads) * R * R + sizeof(float) * R * R;
-  const size_t upd = uw_step_bytes(R, 4) + 16 * 8;
+  const size_t scratch_g = sizeof(float) * 8 * kPWRows * (size_t)R;
+  const size_t scratch_p = sizeof(double) * ((size_t)kPWRows * ut_rd(R) + 4 * (size_t)(R * (R + 1) / 2));
+  const size_t upd = uw_step_bytes(R, 4) + 16 * 8 + (scratch_g > scratch_p ? scratch_g : scratch_p) + 64;
   const size_t inv = sizeof(double) * ((size_t)R * (R + 1) + kSweepBuf + kMaxRank) + sizeof(int) * kMaxRank +
-                     sizeof(double) * ((size_t)R * ut_rd(R) + (size_t)kPWRows * ut_rd(R) + (size_t)kPWRows * ((R + 3) / 4)) +
+                     sizeof(double) * ((size_t)R * ut_rd(R) + (size_t)kPWRows * ut_rd(R) + 4 * (size_t)kPWRows * ((R + 3) / 4)) +
                      upd + 16 * 16;
   size_t m = sample > inv ? sample : inv;
   return m;
@@ -173,6 +176,7 @@ __host__ __device__ inline size_t pw_smem_bytes(int N, int R, int64_t KBmax, int
 // ------------------------------------------------------------------------------------------ phase S
 struct PWShared {  // static shared state of the phases
   const uint64_t* cp[kMaxOrder];
+  int64_t coff[kMaxOrder];         // offset of mode k's staged CDF in the shared CDF area
   uint64_t T[kMaxOrder];
   int32_t start[kMaxOrder], len[kMaxOrder];
   double wblk;
@@ -229,6 +233,7 @@ __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned char* s
       }
       if (tid == 0) {
         ss.cp[k] = src;
+        ss.coff[k] = src == p.cdf[k] ? 0 : (int64_t)(src - cdfs);
         ss.T[k] = p.strategy == 0 ? (uint64_t)p.dims[k] : __ldcg(p.Ttot + k);
       }
     }
@@ -246,11 +251,12 @@ __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned char* s
       const int64_t bk = p.window[n][pos];
       const uint64_t Tk = ss.T[k];
       const uint64_t rr = scale_draw(draw_word(p.seed, r, 0u, kPurposeWindow, (uint32_t)pos), Tk);
-      const uint64_t* c = ss.cp[k];
+      const uint64_t* c = cdfs + ss.coff[k];  // indexed from the shared array: LDS, not generic loads
       int64_t istar = upper_bound_u64(c, p.dims[k], rr);
       if (istar >= p.dims[k]) istar = p.dims[k] - 1;  // T = 0 (degenerate table, status already set)
       const int64_t s0 = (istar / bk) * bk, e0 = min(s0 + bk, p.dims[k]);
-      const uint64_t Q = c[e0 - 1] - (s0 > 0 ? c[s0 - 1] : 0ull);
+      const uint64_t cprev = c[s0 > 0 ? s0 - 1 : 0];  // unconditional load, then select
+      const uint64_t Q = c[e0 - 1] - (s0 > 0 ? cprev : 0ull);
       ss.start[pos] = (int32_t)s0;
       ss.len[pos] = (int32_t)(e0 - s0);
       const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * Q), (double)Tk);
@@ -283,10 +289,11 @@ __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned char* s
           i = (int64_t)rr;
           qk = 1;
         } else {
-          const uint64_t* c = ss.cp[k];
+          const uint64_t* c = cdfs + ss.coff[k];  // indexed from the shared array: LDS, not generic loads
           i = upper_bound_u64(c, p.dims[k], rr);
           if (i >= p.dims[k]) i = p.dims[k] - 1;  // T = 0: status already set, keep the addresses valid
-          qk = c[i] - (i > 0 ? c[i - 1] : 0ull);
+          const uint64_t cprev = c[i > 0 ? i - 1 : 0];  // unconditional load, then select
+          qk = c[i] - (i > 0 ? cprev : 0ull);
         }
         sidx[e] = (int32_t)i;
         spt[e] = __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);
@@ -355,7 +362,11 @@ __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned char* s
         const float* F = p.factors[k];
         float f[U];
 #pragma unroll
-        for (int q = 0; q < U; ++q) f[q] = z[q] != 0.f ? __ldcg(F + (int64_t)sidx[lbu[q] * NP + pos] * R + ru[q]) : 0.f;
+        for (int q = 0; q < U; ++q) {  // every load issued (clamped address), then selected: no branch per load
+          const int lb = lbu[q] < kPWFib ? lbu[q] : kPWFib - 1, rr = ru[q] < R ? ru[q] : R - 1;
+          const float v = __ldcg(F + (int64_t)sidx[lb * NP + pos] * R + rr);
+          f[q] = z[q] != 0.f ? v : 0.f;
+        }
 #pragma unroll
         for (int q = 0; q < U; ++q) z[q] = z[q] * f[q];
       }
@@ -400,8 +411,8 @@ __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned char* s
           float x[4], y[4];
 #pragma unroll
           for (int a = 0; a < 4; ++a) {
-            x[a] = 4 * bi + a < RP ? wk * zs[kk * RP + 4 * bi + a] : 0.f;
-            y[a] = 4 * bj + a < RP ? zs[kk * RP + 4 * bj + a] : 0.f;
+            x[a] = wk * zs[kk * RP + 4 * bi + a];  // 4 ceil(R/4) <= RP: always inside the padded row
+            y[a] = zs[kk * RP + 4 * bj + a];
           }
 #pragma unroll
           for (int a = 0; a < 4; ++a)
@@ -446,7 +457,10 @@ __device__ __forceinline__ void pw_gamma_sum(const PWParams& p, int nsamp, int e
     float v[16], s = 0.f;
     for (int c0 = 0; c0 < nsamp; c0 += 16) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = (c0 + k < nsamp) ? __ldcg(p.gcl + (int64_t)(c0 + k) * E + e) : 0.f;
+      for (int k = 0; k < 16; ++k) {  // clamped unconditional loads (no branch per load), then masked
+        const float t = __ldcg(p.gcl + (int64_t)(c0 + k < nsamp ? c0 + k : nsamp - 1) * E + e);
+        v[k] = c0 + k < nsamp ? t : 0.f;
+      }
 #pragma unroll
       for (int k = 0; k < 16; ++k) s += v[k];  // CTA order; zeros past nsamp are exact
     }
@@ -507,7 +521,8 @@ __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PWBars& B
           const int e = tid + 128 * rep;
           const int kk = e >> 5, j = e & 31;
           const int lb = f0 + kk;
-          const int64_t fb = lb < nfib ? sfb[lb] : -1;
+          const int64_t fbv = sfb[lb < nfib ? lb : 0];  // unconditional load, then select
+          const int64_t fb = lb < nfib ? fbv : -1;
           const int64_t r0 = i0 + 4 * j;
           if (fb >= 0 && r0 < rowlen) cp_async16(A + kk * 512 + 16 * j, X + fb + r0, 16);
         }
@@ -532,7 +547,10 @@ __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PWBars& B
           const int kk = 4 * kq + u, lb = f0 + kk;
           const bool ok = lb < nfib && sfb[lb] >= 0;
 #pragma unroll
-          for (int a = 0; a < 4; ++a) x[u][a] = ok ? A[kk * 128 + iq + 32 * a] : 0.f;
+          for (int a = 0; a < 4; ++a) {  // load unconditionally (inside the ring), then select
+            const float t = A[kk * 128 + iq + 32 * a];
+            x[u][a] = ok ? t : 0.f;
+          }
         }
         mbar_arrive(&B.xempty[slot]);
 #pragma unroll
@@ -632,7 +650,8 @@ __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PWBars& B
 // rows [r0, r0 + nr) of A^(n): M (chunk order), G = A Gamma - M, update; leaves the new rows in sA
 // (stride R+1) and writes the unit's table partial
 __device__ void pw_update_unit(const PWParams& p, int n, int unit, double alpha, float* sA, float* sS, float* sM,
-                               const float* sG, double* sgp, PWShared& ss, long long* mk) {
+                               const float* sG, double* sgp_d, PWShared& ss, long long* mk) {
+  float* sgp_f = reinterpret_cast<float*>(sgp_d);  // scratch (16-byte aligned): the G partials, then the Gram's
   constexpr int TI = kGUTI;
   const int R = p.R, RS = R + 1, AS = R, tid = threadIdx.x, nth = blockDim.x, nb4 = (R + 3) >> 2;
   const int64_t In = p.dims[n];
@@ -674,30 +693,46 @@ __device__ void pw_update_unit(const PWParams& p, int n, int unit, double alpha,
   cp_async_wait<0>();
   __syncthreads();
   PW_MK(15);
-  // G = A Gamma - M (each task owns a 4 x 4 block of M -> G in place)
-  for (int t = tid; t < ((nr + 3) >> 2) * nb4; t += nth) {
-    const int a0 = 4 * (t / nb4), q0 = 4 * (t % nb4);
-    float acc[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
-    for (int k = 0; k < R; ++k) {
-      float x[4], y[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) x[a] = (a0 + a < nr) ? sA[(a0 + a) * AS + k] : 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) y[c] = (q0 + c < R) ? sG[k * R + q0 + c] : 0.f;
+  // G = A Gamma - M: task = (4 x 4 block of G, k group); KG groups split the R-long contraction (short
+  // dependent chains), their partials summed in group order
+  {
+    const int nbt = ((nr + 3) >> 2) * nb4;
+    const int KG = max(1, min(8, nth / max(1, nbt)));
+    const int kper = (R + KG - 1) / KG;
+    float* redG = sgp_f;  // [KG][16][R]
+    for (int t = tid; t < nbt * KG; t += nth) {
+      const int g = t / nbt, bt = t % nbt;
+      const int a0 = 4 * (bt / nb4), q0 = 4 * (bt % nb4);
+      const int k0 = g * kper, k1 = min(R, k0 + kper);
+      float acc[4][4];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c] = fmaf(x[a], y[c], acc[a][c]);
+        for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
+      for (int k = k0; k < k1; ++k) {
+        float x[4], y[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) x[a] = sA[(a0 + a) * AS + k];  // rows < 16: inside the buffer
+#pragma unroll
+        for (int c = 0; c < 4; ++c) y[c] = sG[k * R + min(q0 + c, R - 1)];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = fmaf(x[a], y[c], acc[a][c]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (q0 + c < R) redG[(g * kPWRows + a0 + a) * R + q0 + c] = acc[a][c];
     }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (a0 + a < nr && q0 + c < R) sM[(a0 + a) * RS + q0 + c] = acc[a][c] - sM[(a0 + a) * RS + q0 + c];
+    __syncthreads();
+    for (int e = tid; e < nr * R; e += nth) {
+      const int il = e / R, r = e % R;
+      float sum = 0.f;
+      for (int g = 0; g < KG; ++g) sum += redG[(g * kPWRows + il) * R + r];
+      sM[il * RS + r] = sum - sM[il * RS + r];
+    }
   }
   __syncthreads();
   // fixed (eq:proposed) / adaptive (eq:etaada/eq:Aada, :531-537, R12) update
@@ -727,9 +762,22 @@ __device__ void pw_update_unit(const PWParams& p, int n, int unit, double alpha,
   PW_MK(16);
   // table partials of the new rows (R9)
   if (p.strategy == 1 || p.strategy == 3) {  // leverage: partial fp64 Gram, packed upper triangle
+    // task = (4 x 4 block bi <= bj, row group): the rows split into RG groups (short chains), an fp64
+    // copy of the rows (converted once), the group partials summed in group order
     const int P = R * (R + 1) / 2;
+    const int RD = ut_rd(R);
     const int nblk = nb4 * (nb4 + 1) / 2;
-    for (int blk = tid; blk < nblk; blk += nth) {
+    const int RG = max(1, min(4, nth / nblk));
+    double* sAd = sgp_d;                              // [16][RD], zero past R
+    double* redP = sgp_d + kPWRows * RD;              // [RG][P]
+    for (int e = tid; e < kPWRows * RD; e += nth) {
+      const int il = e / RD, c = e % RD;
+      const float v = sA[il * AS + min(c, R - 1)];  // rows < 16: inside the buffer
+      sAd[e] = (il < nr && c < R) ? (double)v : 0.0;
+    }
+    __syncthreads();
+    for (int t = tid; t < nblk * RG; t += nth) {
+      const int g = t / nblk, blk = t % nblk;
       int bi = 0, rem = blk;
       while (rem >= nb4 - bi) { rem -= nb4 - bi; ++bi; }
       const int bj = bi + rem;
@@ -738,26 +786,31 @@ __device__ void pw_update_unit(const PWParams& p, int n, int unit, double alpha,
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
-      for (int il = 0; il < nr; ++il) {
-        double x[4], y[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          x[a] = 4 * bi + a < R ? (double)sA[il * AS + 4 * bi + a] : 0.0;
-          y[a] = 4 * bj + a < R ? (double)sA[il * AS + 4 * bj + a] : 0.0;
-        }
+      for (int il = g; il < nr; il += RG) {
+        const double2 x01 = *reinterpret_cast<const double2*>(sAd + il * RD + 4 * bi);
+        const double2 x23 = *reinterpret_cast<const double2*>(sAd + il * RD + 4 * bi + 2);
+        const double2 y01 = *reinterpret_cast<const double2*>(sAd + il * RD + 4 * bj);
+        const double2 y23 = *reinterpret_cast<const double2*>(sAd + il * RD + 4 * bj + 2);
+        const double x[4] = {x01.x, x01.y, x23.x, x23.y}, y[4] = {y01.x, y01.y, y23.x, y23.y};
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
           for (int c = 0; c < 4; ++c) acc[a][c] = fma(x[a], y[c], acc[a][c]);
       }
-      double* gp = p.gpart + (int64_t)unit * P;
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int r1 = 4 * bi + a, r2 = 4 * bj + c;
-          if (r1 < R && r2 < R && r1 <= r2) gp[r1 * R - r1 * (r1 - 1) / 2 + (r2 - r1)] = acc[a][c];
+          if (r1 < R && r2 < R && r1 <= r2) redP[g * P + r1 * R - r1 * (r1 - 1) / 2 + (r2 - r1)] = acc[a][c];
         }
+    }
+    __syncthreads();
+    double* gp = p.gpart + (int64_t)unit * P;
+    for (int e = tid; e < P; e += nth) {
+      double sum = 0.0;
+      for (int g = 0; g < RG; ++g) sum += redP[g * P + e];
+      gp[e] = sum;
     }
   } else if (p.strategy == 2 || p.strategy == 4) {  // Euclidean: row norms + the unit's partial ||A||^2
     double acc = 0.0;
@@ -798,17 +851,24 @@ __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nunits, ui
   if (lev) {
     for (int e = tid; e < kPWRows * RD; e += nth) {
       const int il = e / RD, c = e % RD;
-      Ad[e] = (il < nr && c < R) ? (double)__ldcg(p.factors[n] + (r0 + il) * R + c) : 0.0;
+      const float v = __ldcg(p.factors[n] + (r0 + min(il, nr - 1)) * R + min(c, R - 1));  // clamped, then select
+      Ad[e] = (il < nr && c < R) ? (double)v : 0.0;
     }
     __syncthreads();
+    // task = (row pair, column group, k group): KG groups split the R-long contraction (short chains);
+    // partials summed in (k group, column group) order
     const int nrp = (nr + 1) >> 1;
-    for (int t = tid; t < nrp * nb4; t += nth) {
-      const int il = 2 * (t / nb4), cg = t % nb4;
+    const int KG = max(1, min(4, nth / max(1, nrp * nb4)));
+    const int kper = (R + KG - 1) / KG;
+    for (int t = tid; t < nrp * nb4 * KG; t += nth) {
+      const int g = t / (nrp * nb4), tt = t % (nrp * nb4);
+      const int il = 2 * (tt / nb4), cg = tt % nb4;
+      const int k0 = g * kper, k1 = min(R, k0 + kper);
       const double* a0 = Ad + il * RD;
       const double* a1 = a0 + RD;
       double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
-      for (int k = 0; k < R; ++k) {
+#pragma unroll 2
+      for (int k = k0; k < k1; ++k) {
         const double x0 = a0[k], x1 = a1[k];
         const double2 w0 = *reinterpret_cast<const double2*>(Wd + k * RD + 4 * cg);
         const double2 w1 = *reinterpret_cast<const double2*>(Wd + k * RD + 4 * cg + 2);
@@ -821,15 +881,17 @@ __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nunits, ui
         acc1[2] = fma(x1, w1.x, acc1[2]);
         acc1[3] = fma(x1, w1.y, acc1[3]);
       }
-      part[il * nb4 + cg] = acc0[0] * a0[4 * cg] + acc0[1] * a0[4 * cg + 1] + acc0[2] * a0[4 * cg + 2] + acc0[3] * a0[4 * cg + 3];
+      part[(g * kPWRows + il) * nb4 + cg] =
+          acc0[0] * a0[4 * cg] + acc0[1] * a0[4 * cg + 1] + acc0[2] * a0[4 * cg + 2] + acc0[3] * a0[4 * cg + 3];
       if (il + 1 < kPWRows)
-        part[(il + 1) * nb4 + cg] =
+        part[(g * kPWRows + il + 1) * nb4 + cg] =
             acc1[0] * a1[4 * cg] + acc1[1] * a1[4 * cg + 1] + acc1[2] * a1[4 * cg + 2] + acc1[3] * a1[4 * cg + 3];
     }
     __syncthreads();
     if (tid < nr) {
       double l = 0.0;
-      for (int cg = 0; cg < nb4; ++cg) l += part[tid * nb4 + cg];
+      for (int g = 0; g < KG; ++g)
+        for (int cg = 0; cg < nb4; ++cg) l += part[(g * kPWRows + tid) * nb4 + cg];
       s_p[tid] = rank > 0 ? fmax(l, 0.0) / (double)rank : 0.0;
     }
   } else if (tid < nr) {
@@ -862,7 +924,8 @@ __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nunits, ui
   unsigned long long pre = 0;
   unsigned badv = 0;
   for (int u = tid; u < unit; u += nth) {
-    while (ld_acquire_u32(p.aggf + 2 * u + 1) != tag) __nanosleep(40);
+    while (ld_acquire_u32(p.aggf + 2 * u + 1) != tag) {
+    }
     pre += __ldcg(p.agg + u);
     badv |= __ldcg(p.aggf + 2 * u);
   }
@@ -1047,7 +1110,8 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const int u = c0 + 32 * k + lane;
-              v[k] = u < nu ? __ldcg(p.gpart + (int64_t)u * P + pair) : 0.0;
+              const double t = __ldcg(p.gpart + (int64_t)(u < nu ? u : nu - 1) * P + pair);
+              v[k] = u < nu ? t : 0.0;
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) sacc += v[k];
@@ -1068,8 +1132,11 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
         double* rowbuf = Gm + R * RS;
         double* diag = rowbuf + kSweepBuf;
         int* swept = reinterpret_cast<int*>(diag + kMaxRank);
-        double* Wd = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(swept) + sizeof(int) * kMaxRank + 16);
-        Wd = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(Wd) + 15) & ~(uintptr_t)15);
+        // W at a 16-byte aligned OFFSET from the shared base (an integer-cast pointer would turn every
+        // access into a generic load)
+        const size_t offW = ((uw_step_bytes(R, 4) + 256 + sizeof(double) * ((size_t)R * RS + kSweepBuf + kMaxRank) +
+                              sizeof(int) * kMaxRank + 16) + 15) / 16 * 16;
+        double* Wd = reinterpret_cast<double*>(sm + offW);
         const int RD = ut_rd(R);
         double* Ad = Wd + R * RD;
         double* part = Ad + kPWRows * RD;

@@ -128,7 +128,10 @@ __device__ void uw_table_tail(const UWParams<T>& p, unsigned char* sm, const coo
       double v[16], s = 0.0;
       for (int c0 = 0; c0 < ncl; c0 += 16) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = (c0 + k < ncl) ? __ldcg(p.gpart + (int64_t)(c0 + k) * P + pair) : 0.0;
+        for (int k = 0; k < 16; ++k) {  // clamped unconditional loads, then masked (no branch per load)
+          const double t = __ldcg(p.gpart + (int64_t)(c0 + k < ncl ? c0 + k : ncl - 1) * P + pair);
+          v[k] = (c0 + k < ncl) ? t : 0.0;
+        }
 #pragma unroll
         for (int k = 0; k < 16; ++k) s += v[k];  // cluster order; zeros past ncl are exact
       }
@@ -428,9 +431,15 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
       for (int k = 0; k < R; ++k) {
         T x[4], y[4];
   #pragma unroll
-        for (int a = 0; a < 4; ++a) x[a] = (a0 + a < nr) ? sA[(a0 + a) * RS + k] : T(0);
+        for (int a = 0; a < 4; ++a) {
+          const T t = sA[(a0 + a) * RS + k];  // rows < kUWRows: inside the buffer; load, then select
+          x[a] = (a0 + a < nr) ? t : T(0);
+        }
   #pragma unroll
-        for (int c = 0; c < 4; ++c) y[c] = (q0 + c < R) ? sG[k * R + q0 + c] : T(0);
+        for (int c = 0; c < 4; ++c) {
+          const T t = sG[k * R + (q0 + c < R ? q0 + c : R - 1)];
+          y[c] = (q0 + c < R) ? t : T(0);
+        }
   #pragma unroll
         for (int a = 0; a < 4; ++a)
   #pragma unroll
@@ -490,8 +499,10 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
         double x[4], y[4];
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-          x[a] = 4 * bi + a < R ? (double)sA[il * RS + 4 * bi + a] : 0.0;
-          y[a] = 4 * bj + a < R ? (double)sA[il * RS + 4 * bj + a] : 0.0;
+          const T tx = sA[il * RS + (4 * bi + a < R ? 4 * bi + a : R - 1)];  // clamped, then select
+          const T ty = sA[il * RS + (4 * bj + a < R ? 4 * bj + a : R - 1)];
+          x[a] = 4 * bi + a < R ? (double)tx : 0.0;
+          y[a] = 4 * bj + a < R ? (double)ty : 0.0;
         }
 #pragma unroll
         for (int a = 0; a < 4; ++a)
@@ -670,7 +681,8 @@ __global__ void __launch_bounds__(kWThreads, 1) k_sample_wide(SWParams P) {
       } else {
         const uint64_t* c = s_cp[k];
         i = upper_bound_u64(c, sp.dims[k], rr);
-        qk = c[i] - (i > 0 ? c[i - 1] : 0ull);
+        const uint64_t cprev = c[i > 0 ? i - 1 : 0];  // unconditional load, then select
+        qk = c[i] - (i > 0 ? cprev : 0ull);
       }
       sidx[e] = (int32_t)i;
       spt[e] = __ddiv_rn((double)((uint64_t)sp.dims[k] * qk), (double)Tk);

@@ -62,6 +62,7 @@ def main():
             print("phase us (CTA 0, mean over iterations 1..7):")
             for (nm, _, _), v in zip(seq, rows.mean(0)):
                 print(f"  {nm:8s} {v:8.2f}")
+
             print("  total", round(float((d[1:8, 31] - d[1:8, 30]).mean()) / 1e3, 2), "us; SM clock", round(ghz * 1e3), "MHz")
         h.close()
         del Ad
