@@ -1,31 +1,84 @@
-"""Build libcpsgd.so in-tree with nvcc for sm_100a (B200).  No GPU needed (cross-compiles)."""
+"""Build libcpsgd.so in-tree with nvcc for sm_100a (B200).  No GPU needed (cross-compiles).
+
+The library is several translation units (csrc/*.cu: the host code and the chain kernels in
+cpsgd.cu, each heavy persistent-kernel family in its own k_*.cu) compiled in parallel to objects
+under build/ and linked with nvcc -shared.  A unit is recompiled when it, a header it includes
+(transitively), the ABI header or this file changed."""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import os
+import re
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "cpsgd.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in sorted(os.listdir(os.path.join(HERE, "csrc")))] + \
-       [os.path.join(ROOT, "include", "cpsgd.h"), os.path.abspath(__file__)]
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build")
 OUT = os.path.join(HERE, "libcpsgd.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ABI = os.path.join(ROOT, "include", "cpsgd.h")
 
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-         "-Xcompiler", "-Wall", "-shared", "-diag-suppress", "177"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+         "-diag-suppress", "177"]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(d) for d in DEPS):
-        return OUT
-    tmp = OUT + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, SRC, "-ldl"]
+def _units():
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+
+
+def _deps(path, seen=None):
+    """the file and every local header it includes, transitively"""
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    with open(path) as f:
+        for inc in re.findall(r'^\s*#include\s+"([^"]+)"', f.read(), re.M):
+            _deps(os.path.normpath(os.path.join(os.path.dirname(path), inc)), seen)
+    return seen
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _compile(src, obj, verbose):
+    tmp = obj + f".tmp{os.getpid()}"
+    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", "-o", tmp, src]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, OUT)
+    os.replace(tmp, obj)
+    return obj
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    me = os.path.abspath(__file__)
+    units = _units()
+    objs, todo = [], []
+    for src in units:
+        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        if force or _stale(obj, _deps(src) | {ABI, me}):
+            todo.append((src, obj))
+    if todo:
+        with cf.ThreadPoolExecutor(max_workers=min(len(todo), os.cpu_count() or 4)) as ex:
+            for fut in [ex.submit(_compile, s, o, verbose) for s, o in todo]:
+                fut.result()
+    if force or todo or _stale(OUT, set(objs)):
+        tmp = OUT + f".tmp{os.getpid()}"
+        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
+        os.replace(tmp, OUT)
     return OUT
 
 

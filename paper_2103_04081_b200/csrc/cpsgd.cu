@@ -24,8 +24,9 @@
 #include "gupdate.cuh"
 #include "gupdate_tc.cuh"
 #include "wide.cuh"
-#include "sweep_wide.cuh"
+#include "sweep_wide_params.cuh"
 #include "kernels.cuh"
+#include "kptr.h"
 
 using namespace cps;
 
@@ -663,7 +664,7 @@ cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev
   const size_t smem = tc_smem_bytes(p.KB);
   static DevOnce attr_once;  // per device: the attribute is per context
   if (attr_once.first(h->device)) {
-    allow_max_dyn_smem(k_gather_update_tc);
+    allow_max_dyn_smem(k_gather_update_tc<0>);
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)ceil_div(h->dims[n], kGUTI), (unsigned)CK, 1);
@@ -675,7 +676,7 @@ cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev
   at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
   lc.attrs = at;
   lc.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&lc, k_gather_update_tc, p);
+  cudaError_t e = cudaLaunchKernelEx(&lc, k_gather_update_tc<0>, p);
   h->launches++;
   if (e != cudaSuccess)
     return h->fail(CP_ECUDA, "k_gather_update_tc launch (chunks %d, smem %zu): %s", CK, smem, cudaGetErrorString(e));
@@ -915,8 +916,8 @@ cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, dou
   fill_fused_params<T>(h, p, nsteps, first_mode, order, alpha, alpha_dev, rebuild);
   static DevOnce attr_once;  // per device: the attribute is per context
   if (attr_once.first(h->device)) {
-    allow_max_dyn_smem(k_sweep_fused<T, ROWS>);
-    cudaFuncSetAttribute(k_sweep_fused<T, ROWS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    allow_max_dyn_smem(fused_k<T, ROWS>());
+    cudaFuncSetAttribute(fused_k<T, ROWS>(), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(h->fused_cu, 1, 1);
@@ -930,7 +931,7 @@ cp_status launch_fused_t(cp_sgd_s* h, int nsteps, int first_mode, int order, dou
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&lc, k_sweep_fused<T, ROWS>, p);
+  cudaError_t e = cudaLaunchKernelEx(&lc, fused_k<T, ROWS>(), p);
   h->launches++;
   if (e != cudaSuccess)
     return h->fail(CP_ECUDA, "k_sweep_fused launch (cluster %d, smem %zu): %s", h->fused_cu, h->fused_smem,
@@ -975,8 +976,8 @@ cp_status launch_fused_multi_t(cp_sgd_s* const* hs, int nh, int nsteps) {
   CUDA_TRY(h0, cudaMemcpyAsync(h0->multi_params, prm.data(), bytes, cudaMemcpyHostToDevice, h0->stream));
   static DevOnce attr_once;  // per device: the attribute is per context
   if (attr_once.first(h0->device)) {
-    allow_max_dyn_smem(k_sweep_fused_multi<T, ROWS>);
-    cudaFuncSetAttribute(k_sweep_fused_multi<T, ROWS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    allow_max_dyn_smem(fused_multi_k<T, ROWS>());
+    cudaFuncSetAttribute(fused_multi_k<T, ROWS>(), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   cudaLaunchConfig_t lc = {};
   size_t smem = 0;  // each cluster lays out its own shared memory (the CDF area depends on the sampler)
@@ -992,7 +993,7 @@ cp_status launch_fused_multi_t(cp_sgd_s* const* hs, int nh, int nsteps) {
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&lc, k_sweep_fused_multi<T, ROWS>, (const FusedParams<T>*)h0->multi_params,
+  cudaError_t e = cudaLaunchKernelEx(&lc, fused_multi_k<T, ROWS>(), (const FusedParams<T>*)h0->multi_params,
                                      h0->fused_cu);
   h0->launches++;
   if (e != cudaSuccess) return h0->fail(CP_ECUDA, "k_sweep_fused_multi launch (%d chains): %s", nh, cudaGetErrorString(e));
@@ -1082,10 +1083,7 @@ TraceParams trace_params(cp_sgd_s* h, int nsteps) {
 }
 
 // ---- persistent cooperative sweep kernel of the fp32 wide path (sweep_wide.cuh) -------------------
-using PWKernel = void (*)(PWParams);
-PWKernel pw_kernel(int R) {
-  return R <= 16 ? k_sweep_wide<16> : R <= 32 ? k_sweep_wide<32> : R <= 56 ? k_sweep_wide<56> : k_sweep_wide<64>;
-}
+// pw_kernel(R): k_pw.cu (its own translation unit)
 
 // eligible: one GPU, fp32 on the tcgen05 gather for every mode, gradient rules (the sampled-ALS rule
 // stays on the kernel chain), cooperative launch supported, one 448-thread CTA per SM co-resident

@@ -107,6 +107,8 @@ __host__ __device__ inline size_t tc_smem_bytes(int64_t KB) {
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// a template (one instance, V = 0) so that only the translation unit that launches it emits it
+template <int V = 0>
 __global__ void __launch_bounds__(kTCThreads, 1) k_gather_update_tc(GUParams<float> p) {
   constexpr int KS = kTCKS, NX = kTCNX, NP = kTCPairs, NZ = kTCNZ, TI = kGUTI;
   constexpr uint32_t A_BYTES = kTCABytes;

@@ -32,61 +32,9 @@
 #pragma once
 #include <cooperative_groups.h>
 
-#include "gupdate_tc.cuh"
-#include "wide.cuh"
+#include "sweep_wide_params.cuh"
 
 namespace cps {
-
-constexpr int kPWThreads = kTCThreads;  // 448: the tcgen05 gather's warp roles
-constexpr int kPWFib = 32;              // fibers per sampling unit (one tcgen05 stage)
-constexpr int kPWRows = 16;             // rows per update / table unit
-
-struct PWParams {
-  int N, R, strategy, rule;
-  int nsteps, first_mode, order;
-  int64_t B;
-  int64_t dims[kMaxOrder], lstride[kMaxOrder];
-  const float* Xg[kMaxOrder];      // gather base of mode n: mode-major copy (n >= 1) or X (mode 0)
-  int64_t rowlen[kMaxOrder];       // readable elements per fiber row (pitch, or I_0)
-  int64_t pitch[kMaxOrder];        // 0: native (mode 0)
-  float* factors[kMaxOrder];
-  float* S[kMaxOrder];
-  uint64_t* cdf[kMaxOrder];
-  double* pprob[kMaxOrder];
-  uint64_t* Ttot;
-  int32_t window[kMaxOrder][kMaxOrder];
-  int64_t bmax[kMaxOrder];
-  int CK[kMaxOrder];
-  int64_t KB[kMaxOrder];
-  uint64_t seed;
-  uint64_t* iter;
-  int* status;
-  int* last_mode;
-  double alpha, eta, b, eps;
-  const double* alpha_dev;         // constant step on the device (graph-free replays), or NULL
-  const double* alphas;            // per-iteration steps (fixed rule), or NULL
-  // workspace
-  int32_t* idx;
-  double* w;
-  int64_t* fbase;
-  int64_t* beff;
-  float* zimg;
-  float* gcl;                      // [G][R][R] per-CTA partials of Gamma
-  float* gam;                      // [R][R]
-  float* Mpart;                    // [tiles][CK][R][128]
-  double* gpart;                   // [row units][P] (leverage) or [row units] (Euclidean)
-  double* gram;                    // [P] the Gram's pairs
-  double* rownorm;                 // [I_max]
-  unsigned long long* agg;         // [row units] q sums
-  unsigned* aggf;                  // [row units][2]: {bad bits, tag}
-  unsigned* bar;                   // grid-barrier arrivals (zero at launch)
-  unsigned* pcnt;                  // pair-sum arrivals (zero at launch)
-  uint32_t tag0;                   // tag of iteration 0 of this launch (unique per handle)
-  float* Gout;
-  float* Gam_out;
-  TraceParams tr;
-  long long* dbg;
-};
 
 // ------------------------------------------------------------------------------------------ sync
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -149,30 +97,6 @@ __device__ __forceinline__ void ldcg_copy_u64(uint64_t* dst, const uint64_t* src
   }
 }
 
-__host__ __device__ inline int pw_units_rows(int64_t In) { return (int)((In + kPWRows - 1) / kPWRows); }
-__host__ __device__ inline int pw_units_fib(int64_t bmax) { return (int)((bmax + kPWFib - 1) / kPWFib); }
-
-// dynamic shared memory: the gather's ring (tc_smem_bytes) covers every other phase's working set
-__host__ __device__ inline size_t pw_other_bytes(int N, int R, int64_t cdf_elems) {
-  const int RP = zg_rp(R);
-  const size_t sample = 16 * 8 + sizeof(uint64_t) * (cdf_elems + kMaxOrder) + sizeof(int32_t) * kPWFib * (N - 1) +
-                        sizeof(double) * kPWFib * (N - 1) + sizeof(double) * kPWFib + sizeof(float) * kPWFib * RP +
-                        sizeof(float) * (size_t)zg_groups(R, kPWThreads) * R * R + sizeof(float) * R * R;
-  const size_t scratch_g = sizeof(float) * 8 * kPWRows * (size_t)R;
-  const size_t scratch_p = sizeof(double) * ((size_t)kPWRows * ut_rd(R) + 4 * (size_t)(R * (R + 1) / 2));
-  const size_t upd = uw_step_bytes(R, 4) + 16 * 8 + (scratch_g > scratch_p ? scratch_g : scratch_p) + 64;
-  const size_t inv = sizeof(double) * ((size_t)R * (R + 1) + kSweepBuf + kMaxRank) + sizeof(int) * kMaxRank +
-                     sizeof(double) * ((size_t)R * ut_rd(R) + (size_t)kPWRows * ut_rd(R) + 4 * (size_t)kPWRows * ((R + 3) / 4)) +
-                     upd + 16 * 16;
-  size_t m = sample > inv ? sample : inv;
-  return m;
-}
-__host__ __device__ inline size_t pw_smem_bytes(int N, int R, int64_t KBmax, int64_t cdf_elems) {
-  const size_t g = tc_smem_bytes(KBmax);
-  const size_t o = pw_other_bytes(N, R, cdf_elems) + 1024;
-  return g > o ? g : o;
-}
-
 // ------------------------------------------------------------------------------------------ phase S
 struct PWShared {  // static shared state of the phases
   const uint64_t* cp[kMaxOrder];
@@ -194,7 +118,7 @@ struct PWShared {  // static shared state of the phases
     __syncwarp();                                     \
   } while (0)
 
-__device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned char* sm, PWShared& ss, long long* mk) {
+static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned char* sm, PWShared& ss, long long* mk) {
   const int tid = threadIdx.x, nth = blockDim.x;
   const int N = p.N, NP = N - 1, R = p.R, RP = zg_rp(R), nb4 = (R + 3) >> 2;
   const bool block = (p.strategy == 3 || p.strategy == 4);
@@ -470,7 +394,7 @@ __device__ __forceinline__ void pw_gamma_sum(const PWParams& p, int nsamp, int e
 
 // the tcgen05 mainloop of gupdate_tc.cuh over this CTA's (I-tile, chunk) items; gs / gi: this CTA's
 // running stage / item counters (the mbarrier phases continue across items and iterations)
-__device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PWBars& B, uint32_t tmem, uint32_t& gs,
+static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PWBars& B, uint32_t tmem, uint32_t& gs,
                           uint32_t& gi) {
   constexpr int KS = kTCKS, NX = kTCNX, NP = kTCPairs, NZ = kTCNZ, TI = kGUTI;
   constexpr uint32_t A_BYTES = kTCABytes;
@@ -649,7 +573,7 @@ __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PWBars& B
 // ------------------------------------------------------------------------------------------ phase U
 // rows [r0, r0 + nr) of A^(n): M (chunk order), G = A Gamma - M, update; leaves the new rows in sA
 // (stride R+1) and writes the unit's table partial
-__device__ void pw_update_unit(const PWParams& p, int n, int unit, double alpha, float* sA, float* sS, float* sM,
+static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double alpha, float* sA, float* sS, float* sM,
                                const float* sG, double* sgp_d, PWShared& ss, long long* mk) {
   float* sgp_f = reinterpret_cast<float*>(sgp_d);  // scratch (16-byte aligned): the G partials, then the Gram's
   constexpr int TI = kGUTI;
@@ -836,7 +760,7 @@ __device__ void pw_update_unit(const PWParams& p, int n, int unit, double alpha,
 
 // ------------------------------------------------------------------------------------------ phase Q
 // scores + quantisation of the unit's rows (new rows re-read from A^(n)), look-back prefix, CDF rows
-__device__ void pw_table_unit(const PWParams& p, int n, int unit, int nunits, uint32_t tag, const double* Wd, int rank,
+static __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nunits, uint32_t tag, const double* Wd, int rank,
                               double fro, int bad0, double* Ad, double* part, PWShared& ss, long long* mk) {
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int R = p.R, RD = ut_rd(R), nb4 = (R + 3) >> 2;
@@ -971,7 +895,7 @@ __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nunits, ui
 }
 
 // ------------------------------------------------------------------------------------------ trace
-__device__ void pw_trace(const PWParams& p, int s, int n, uint64_t r) {
+static __device__ void pw_trace(const PWParams& p, int s, int n, uint64_t r) {
   const int64_t slot = p.tr.first + s;
   if (slot >= p.tr.cap) return;
   unsigned char* base = p.tr.base + slot * p.tr.stride;

@@ -1,0 +1,85 @@
+// sweep_wide_params.cuh -- the host-visible part of k_sweep_wide (sweep_wide.cuh): the launch parameters,
+// the unit counts and the shared-memory plan.  The host code includes only this; the kernel body lives
+// in sweep_wide.cuh, compiled in k_pw.cu.
+#pragma once
+#include "gupdate_tc.cuh"
+#include "wide.cuh"
+
+namespace cps {
+
+constexpr int kPWThreads = kTCThreads;  // 448: the tcgen05 gather's warp roles
+constexpr int kPWFib = 32;              // fibers per sampling unit (one tcgen05 stage)
+constexpr int kPWRows = 16;             // rows per update / table unit
+
+struct PWParams {
+  int N, R, strategy, rule;
+  int nsteps, first_mode, order;
+  int64_t B;
+  int64_t dims[kMaxOrder], lstride[kMaxOrder];
+  const float* Xg[kMaxOrder];      // gather base of mode n: mode-major copy (n >= 1) or X (mode 0)
+  int64_t rowlen[kMaxOrder];       // readable elements per fiber row (pitch, or I_0)
+  int64_t pitch[kMaxOrder];        // 0: native (mode 0)
+  float* factors[kMaxOrder];
+  float* S[kMaxOrder];
+  uint64_t* cdf[kMaxOrder];
+  double* pprob[kMaxOrder];
+  uint64_t* Ttot;
+  int32_t window[kMaxOrder][kMaxOrder];
+  int64_t bmax[kMaxOrder];
+  int CK[kMaxOrder];
+  int64_t KB[kMaxOrder];
+  uint64_t seed;
+  uint64_t* iter;
+  int* status;
+  int* last_mode;
+  double alpha, eta, b, eps;
+  const double* alpha_dev;         // constant step on the device (graph-free replays), or NULL
+  const double* alphas;            // per-iteration steps (fixed rule), or NULL
+  // workspace
+  int32_t* idx;
+  double* w;
+  int64_t* fbase;
+  int64_t* beff;
+  float* zimg;
+  float* gcl;                      // [G][R][R] per-CTA partials of Gamma
+  float* gam;                      // [R][R]
+  float* Mpart;                    // [tiles][CK][R][128]
+  double* gpart;                   // [row units][P] (leverage) or [row units] (Euclidean)
+  double* gram;                    // [P] the Gram's pairs
+  double* rownorm;                 // [I_max]
+  unsigned long long* agg;         // [row units] q sums
+  unsigned* aggf;                  // [row units][2]: {bad bits, tag}
+  unsigned* bar;                   // grid-barrier arrivals (zero at launch)
+  unsigned* pcnt;                  // pair-sum arrivals (zero at launch)
+  uint32_t tag0;                   // tag of iteration 0 of this launch (unique per handle)
+  float* Gout;
+  float* Gam_out;
+  TraceParams tr;
+  long long* dbg;
+};
+
+__host__ __device__ inline int pw_units_rows(int64_t In) { return (int)((In + kPWRows - 1) / kPWRows); }
+__host__ __device__ inline int pw_units_fib(int64_t bmax) { return (int)((bmax + kPWFib - 1) / kPWFib); }
+
+// dynamic shared memory: the gather's ring (tc_smem_bytes) covers every other phase's working set
+__host__ __device__ inline size_t pw_other_bytes(int N, int R, int64_t cdf_elems) {
+  const int RP = zg_rp(R);
+  const size_t sample = 16 * 8 + sizeof(uint64_t) * (cdf_elems + kMaxOrder) + sizeof(int32_t) * kPWFib * (N - 1) +
+                        sizeof(double) * kPWFib * (N - 1) + sizeof(double) * kPWFib + sizeof(float) * kPWFib * RP +
+                        sizeof(float) * (size_t)zg_groups(R, kPWThreads) * R * R + sizeof(float) * R * R;
+  const size_t scratch_g = sizeof(float) * 8 * kPWRows * (size_t)R;
+  const size_t scratch_p = sizeof(double) * ((size_t)kPWRows * ut_rd(R) + 4 * (size_t)(R * (R + 1) / 2));
+  const size_t upd = uw_step_bytes(R, 4) + 16 * 8 + (scratch_g > scratch_p ? scratch_g : scratch_p) + 64;
+  const size_t inv = sizeof(double) * ((size_t)R * (R + 1) + kSweepBuf + kMaxRank) + sizeof(int) * kMaxRank +
+                     sizeof(double) * ((size_t)R * ut_rd(R) + (size_t)kPWRows * ut_rd(R) + 4 * (size_t)kPWRows * ((R + 3) / 4)) +
+                     upd + 16 * 16;
+  size_t m = sample > inv ? sample : inv;
+  return m;
+}
+__host__ __device__ inline size_t pw_smem_bytes(int N, int R, int64_t KBmax, int64_t cdf_elems) {
+  const size_t g = tc_smem_bytes(KBmax);
+  const size_t o = pw_other_bytes(N, R, cdf_elems) + 1024;
+  return g > o ? g : o;
+}
+
+}  // namespace cps
