@@ -1123,7 +1123,7 @@ bool plan_pw(cp_sgd_s* h) {
     return true;
   };
   if (!alloc((void**)&h->pw_gcl, sizeof(float) * (size_t)h->pw_grid * h->R * h->R) ||
-      !alloc((void**)&h->pw_gram, sizeof(double) * P) ||
+      !alloc((void**)&h->pw_gram, sizeof(double) * ((P + 1) & ~1)) ||  // even: whole 16-byte bulk copies
       !alloc((void**)&h->pw_agg, sizeof(unsigned long long) * units) ||
       !alloc((void**)&h->pw_aggf, sizeof(unsigned) * 2 * units) ||
       !alloc((void**)&h->pw_bar, sizeof(unsigned) * 64)) {
@@ -1477,7 +1477,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       return init_fail(h, h->fail(CP_ENOMEM, "cudaMalloc(%zu): %s", (size_t)(bytes), cudaGetErrorString(e_))); \
   } while (0)
   for (int k = 0; k < h->N; ++k) {
-    ALLOC(h->cdf[k], sizeof(uint64_t) * h->dims[k]);
+    ALLOC(h->cdf[k], sizeof(uint64_t) * ((h->dims[k] + 1) & ~1));  // even: whole 16-byte bulk copies
     ALLOC(h->pprob[k], sizeof(double) * h->dims[k]);
     if (h->rule == CP_STEP_ADAPTIVE) {
       ALLOC(h->S[k], h->esz * h->dims[k] * h->R);
@@ -1602,7 +1602,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       ALLOC(h->gu_cnt, sizeof(unsigned) * ceil_div(Imax, kGUTI));
       cudaMemsetAsync(h->gu_cnt, 0, sizeof(unsigned) * ceil_div(Imax, kGUTI), h->stream);
       ALLOC(h->zwp, h->esz * Bmax_all * zg_rp(h->R));
-      ALLOC(h->gam_next, h->esz * h->R * h->R);
+      ALLOC(h->gam_next, (h->esz * h->R * h->R + 15) / 16 * 16);  // whole 16-byte bulk copies
       cudaMemsetAsync(h->zwp, 0, h->esz * Bmax_all * zg_rp(h->R), h->stream);
       if (h->use_tc) {  // A images: every chunk rounded up to whole stages; rows r >= R stay zero
         int64_t rows = 0;

@@ -978,9 +978,11 @@ __device__ int grp_sweep_inverse(double* Gm, int R, double tol, double* rowbuf, 
     }
   }
   __syncthreads();
-  int rank = 0;
-  for (int j = 0; j < R; ++j) rank += swept[j];
-  return rank;
+  // |S| = popcount of the swept flags (two ballots per warp, R <= 64), not an R-long serial loop
+  const int lane = tid & 31;
+  const unsigned b0 = __ballot_sync(0xffffffffu, lane < R && swept[lane] != 0);
+  const unsigned b1 = __ballot_sync(0xffffffffu, lane + 32 < R && swept[min(lane + 32, kMaxRank - 1)] != 0);
+  return __popc(b0) + __popc(b1);
 }
 
 // MAXR: largest rank the calling kernel supports (instantiates only RMAX <= MAXR); needs 256 threads

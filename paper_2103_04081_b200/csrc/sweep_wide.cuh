@@ -97,6 +97,27 @@ __device__ __forceinline__ void ldcg_copy_u64(uint64_t* dst, const uint64_t* src
   }
 }
 
+// Broadcast reads (data every CTA fetches at the same moment: the CDFs, Gamma, the Gram): ONE thread
+// issues TMA bulk copies completing on the CTA's mbarrier, every thread waits on its phase.  Per-thread
+// 16-byte requests from every CTA queue on the few L2 lines holding such data; a bulk copy is one request
+// stream per CTA.  The generic-proxy writes of other CTAs were acquired at the preceding barrier; the
+// proxy fence orders them before the async-proxy reads.  bytes: multiples of 16, 16-byte aligned.
+struct PWBulk {
+  uint64_t* bar;
+  uint32_t ph;  // parity of the next phase (identical in every thread of the CTA)
+};
+__device__ __forceinline__ void pw_bulk_begin(const PWBulk& b, uint32_t total_bytes) {  // one thread
+  // all state spaces: the global data (see above) and the shared destination's earlier generic accesses
+  // (the caller passed a CTA barrier after them)
+  asm volatile("fence.proxy.async;" ::: "memory");
+  mbar_expect_tx(b.bar, total_bytes);
+}
+__device__ __forceinline__ void pw_bulk_wait(PWBulk& b) {  // every thread
+  mbar_wait(b.bar, b.ph);
+  b.ph ^= 1u;
+}
+__host__ __device__ inline uint32_t pw_b16(int64_t bytes) { return (uint32_t)((bytes + 15) / 16 * 16); }
+
 // ------------------------------------------------------------------------------------------ phase S
 struct PWShared {  // static shared state of the phases
   const uint64_t* cp[kMaxOrder];
@@ -118,7 +139,8 @@ struct PWShared {  // static shared state of the phases
     __syncwarp();                                     \
   } while (0)
 
-static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned char* sm, PWShared& ss, long long* mk) {
+static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned char* sm, PWShared& ss, PWBulk& bk,
+                                 long long* mk) {
   const int tid = threadIdx.x, nth = blockDim.x;
   const int N = p.N, NP = N - 1, R = p.R, RP = zg_rp(R), nb4 = (R + 3) >> 2;
   const bool block = (p.strategy == 3 || p.strategy == 4);
@@ -146,14 +168,19 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
   float* red = reinterpret_cast<float*>(carve(sizeof(float) * (size_t)GG * R * R));
   float* gacc = reinterpret_cast<float*>(carve(sizeof(float) * R * R));
   {
+    // the CDFs of the sampled modes (rebuilt by other CTAs of this launch): bulk copies, each mode's area
+    // a whole number of 16-byte units (the allocations are even-length)
     int64_t o = 0;
+    uint32_t tot = 0;
+    for (int k = 0; k < N; ++k)
+      if (k != n && p.strategy != 0) tot += pw_b16(8 * p.dims[k]);
+    if (tid == 0 && tot) pw_bulk_begin(bk, tot);
     for (int k = 0; k < N; ++k) {
       const uint64_t* src = p.cdf[k];
-      if (k != n && p.strategy != 0) {  // L2 copies: the CDFs were rebuilt by other CTAs of this launch
-        o = (o + 1) & ~(int64_t)1;  // 16-byte aligned destination
-        cpcg_bytes(cdfs + o, src, 8 * p.dims[k], tid, nth);
+      if (k != n && p.strategy != 0) {
+        if (tid == 0) bulk_g2s(cdfs + o, src, pw_b16(8 * p.dims[k]), bk.bar);
         src = cdfs + o;
-        o += p.dims[k];
+        o += (p.dims[k] + 1) & ~(int64_t)1;
       }
       if (tid == 0) {
         ss.cp[k] = src;
@@ -161,9 +188,9 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
         ss.T[k] = p.strategy == 0 ? (uint64_t)p.dims[k] : __ldcg(p.Ttot + k);
       }
     }
+    for (int e = tid; e < R * R; e += nth) gacc[e] = 0.f;
+    if (tot) pw_bulk_wait(bk);
   }
-  for (int e = tid; e < R * R; e += nth) gacc[e] = 0.f;
-  cp_async_wait<0>();
   __syncthreads();
   PW_MK(11);
   if (block && tid == 0) {  // window draws (eq:bik, Alg. 4, R2/R6): common to the whole batch
@@ -371,7 +398,7 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
 
 // ------------------------------------------------------------------------------------------ phase G
 struct PWBars {
-  uint64_t xfull[16], xempty[16], sdone[4], mdone[4], afull[4], afree[4], accf;
+  uint64_t xfull[16], xempty[16], sdone[4], mdone[4], afull[4], afree[4], accf, bc;
 };
 
 // Gamma = sum of the sampling CTAs' partials in CTA order; entries [e0, E) with stride es
@@ -574,7 +601,7 @@ static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PW
 // rows [r0, r0 + nr) of A^(n): M (chunk order), G = A Gamma - M, update; leaves the new rows in sA
 // (stride R+1) and writes the unit's table partial
 static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double alpha, float* sA, float* sS, float* sM,
-                               const float* sG, double* sgp_d, PWShared& ss, long long* mk) {
+                               const float* sG, double* sgp_d, PWShared& ss, PWBulk* bkw, long long* mk) {
   float* sgp_f = reinterpret_cast<float*>(sgp_d);  // scratch (16-byte aligned): the G partials, then the Gram's
   constexpr int TI = kGUTI;
   const int R = p.R, RS = R + 1, AS = R, tid = threadIdx.x, nth = blockDim.x, nb4 = (R + 3) >> 2;
@@ -615,6 +642,7 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
     }
   }
   cp_async_wait<0>();
+  if (bkw) pw_bulk_wait(*bkw);  // Gamma (first unit of the CTA)
   __syncthreads();
   PW_MK(15);
   // G = A Gamma - M: task = (4 x 4 block of G, k group); KG groups split the R-long contraction (short
@@ -759,11 +787,12 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
 }
 
 // ------------------------------------------------------------------------------------------ phase Q
-// scores + quantisation of the unit's rows (new rows re-read from A^(n)), look-back prefix, CDF rows
-static __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nunits, uint32_t tag, const double* Wd, int rank,
-                              double fro, int bad0, double* Ad, double* part, PWShared& ss, long long* mk) {
+// scores + quantisation of the unit's rows, look-back prefix, CDF rows
+static __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nunits, uint32_t tag, const double* Wm,
+                                     int rank, double fro, int bad0, double* Ad, const float* sAu, PWShared& ss,
+                                     long long* mk) {
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5;
-  const int R = p.R, RD = ut_rd(R), nb4 = (R + 3) >> 2;
+  const int R = p.R, RS = R + 1, RD = ut_rd(R);
   const bool lev = (p.strategy == 1 || p.strategy == 3);
   const int64_t In = p.dims[n];
   const int64_t r0 = (int64_t)unit * kPWRows;
@@ -773,50 +802,65 @@ static __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nun
   __shared__ int s_badu;
   if (tid == 0) s_badu = bad0;
   if (lev) {
+    // the unit's new rows in fp64 (stride RD, zero padded): from this CTA's own update phase (sAu, stride
+    // R, still in shared memory when this is the CTA's last unit) or re-read through L2
     for (int e = tid; e < kPWRows * RD; e += nth) {
       const int il = e / RD, c = e % RD;
-      const float v = __ldcg(p.factors[n] + (r0 + min(il, nr - 1)) * R + min(c, R - 1));  // clamped, then select
+      const int ilc = min(il, nr - 1), cc = min(c, R - 1);  // clamped, then select
+      const float v = sAu ? sAu[ilc * R + cc] : __ldcg(p.factors[n] + (r0 + ilc) * R + cc);
       Ad[e] = (il < nr && c < R) ? (double)v : 0.0;
     }
     __syncthreads();
-    // task = (row pair, column group, k group): KG groups split the R-long contraction (short chains);
-    // partials summed in (k group, column group) order
-    const int nrp = (nr + 1) >> 1;
-    const int KG = max(1, min(4, nth / max(1, nrp * nb4)));
-    const int kper = (R + KG - 1) / KG;
-    for (int t = tid; t < nrp * nb4 * KG; t += nth) {
-      const int g = t / (nrp * nb4), tt = t % (nrp * nb4);
-      const int il = 2 * (tt / nb4), cg = tt % nb4;
-      const int k0 = g * kper, k1 = min(R, k0 + kper);
+    // l_i = a_i^T W a_i: warp w takes rows 2w, 2w + 1; lane c holds columns c and c + 32 of y = W a
+    // (W symmetric: W_kc read along a row of the inverse, consecutive lanes -> consecutive words), k split
+    // into even / odd chains, then l = sum_c a_c y_c by a fixed xor-shuffle tree (deterministic)
+    if (wid < ((nr + 1) >> 1)) {
+      const int il = 2 * wid;
       const double* a0 = Ad + il * RD;
-      const double* a1 = a0 + RD;
-      double acc0[4] = {0.0, 0.0, 0.0, 0.0}, acc1[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* a1 = a0 + RD;  // row il + 1 < 16: inside the buffer (zeros past nr)
+      const int c0 = lane, c1 = lane + 32;
+      const int c0c = min(c0, R - 1), c1c = min(c1, R - 1);
+      double y[2][2][2] = {};  // [row][column][k parity]
+      if (R > 32) {
 #pragma unroll 2
-      for (int k = k0; k < k1; ++k) {
-        const double x0 = a0[k], x1 = a1[k];
-        const double2 w0 = *reinterpret_cast<const double2*>(Wd + k * RD + 4 * cg);
-        const double2 w1 = *reinterpret_cast<const double2*>(Wd + k * RD + 4 * cg + 2);
-        acc0[0] = fma(x0, w0.x, acc0[0]);
-        acc0[1] = fma(x0, w0.y, acc0[1]);
-        acc0[2] = fma(x0, w1.x, acc0[2]);
-        acc0[3] = fma(x0, w1.y, acc0[3]);
-        acc1[0] = fma(x1, w0.x, acc1[0]);
-        acc1[1] = fma(x1, w0.y, acc1[1]);
-        acc1[2] = fma(x1, w1.x, acc1[2]);
-        acc1[3] = fma(x1, w1.y, acc1[3]);
+        for (int k = 0; k < R; ++k) {
+          const int pk = k & 1;
+          const double x0 = a0[k], x1 = a1[k];
+          const double w0 = Wm[k * RS + c0c], w1 = Wm[k * RS + c1c];
+          y[0][0][pk] = fma(w0, x0, y[0][0][pk]);
+          y[0][1][pk] = fma(w1, x0, y[0][1][pk]);
+          y[1][0][pk] = fma(w0, x1, y[1][0][pk]);
+          y[1][1][pk] = fma(w1, x1, y[1][1][pk]);
+        }
+      } else {
+#pragma unroll 2
+        for (int k = 0; k < R; ++k) {
+          const int pk = k & 1;
+          const double x0 = a0[k], x1 = a1[k];
+          const double w0 = Wm[k * RS + c0c];
+          y[0][0][pk] = fma(w0, x0, y[0][0][pk]);
+          y[1][0][pk] = fma(w0, x1, y[1][0][pk]);
+        }
       }
-      part[(g * kPWRows + il) * nb4 + cg] =
-          acc0[0] * a0[4 * cg] + acc0[1] * a0[4 * cg + 1] + acc0[2] * a0[4 * cg + 2] + acc0[3] * a0[4 * cg + 3];
-      if (il + 1 < kPWRows)
-        part[(g * kPWRows + il + 1) * nb4 + cg] =
-            acc1[0] * a1[4 * cg] + acc1[1] * a1[4 * cg + 1] + acc1[2] * a1[4 * cg + 2] + acc1[3] * a1[4 * cg + 3];
-    }
-    __syncthreads();
-    if (tid < nr) {
-      double l = 0.0;
-      for (int g = 0; g < KG; ++g)
-        for (int cg = 0; cg < nb4; ++cg) l += part[(g * kPWRows + tid) * nb4 + cg];
-      s_p[tid] = rank > 0 ? fmax(l, 0.0) / (double)rank : 0.0;
+      double l0 = 0.0, l1 = 0.0;
+      if (c0 < R) {
+        l0 = a0[c0] * (y[0][0][0] + y[0][0][1]);
+        l1 = a1[c0] * (y[1][0][0] + y[1][0][1]);
+      }
+      if (c1 < R) {
+        l0 += a0[c1] * (y[0][1][0] + y[0][1][1]);
+        l1 += a1[c1] * (y[1][1][0] + y[1][1][1]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+      }
+      if (lane == 0) {
+        s_p[il] = rank > 0 ? fmax(l0, 0.0) / (double)rank : 0.0;
+        if (il + 1 < nr) s_p[il + 1] = rank > 0 ? fmax(l1, 0.0) / (double)rank : 0.0;
+      }
     }
   } else if (tid < nr) {
     s_p[tid] = fro > 0.0 ? __ldcg(p.rownorm + r0 + tid) / fro : 0.0;
@@ -968,6 +1012,7 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
       mbar_init(&B.afree[s], 1);
     }
     mbar_init(&B.accf, 1);
+    mbar_init(&B.bc, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_r0 = *reinterpret_cast<volatile uint64_t*>(p.iter);
     s_stop = 0;
@@ -979,6 +1024,7 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
   unsigned gen = 0;  // barriers passed in this launch
   uint64_t r = s_r0;
   uint32_t gs = 0, gi = 0;
+  PWBulk bk{&B.bc, 0u};
   int n_done = -1;
   const bool lev = (p.strategy == 1 || p.strategy == 3);
   const int P = R * (R + 1) / 2;
@@ -993,7 +1039,7 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
     if (p.dbg && tid == 0 && s < 8 && blockIdx.x == 0) p.dbg[512 + 32 * s + 30] = gtimer();
     // ---- S: the batch of mode n at r ----
     long long* mk = (p.dbg && s < 8 && blockIdx.x == 0) ? p.dbg + 512 + 32 * s : nullptr;
-    pw_sample(p, n, r, sm, ss, mk);
+    pw_sample(p, n, r, sm, ss, bk, mk);
     PW_MARK(1);
     grid_barrier(p.bar, gen);
     PW_MARK(2);
@@ -1011,10 +1057,14 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
       float* sM = sS + ((kPWRows * R + 3) & ~3);
       double* sgp = reinterpret_cast<double*>(sm + ((sizeof(float) * (3 * kPWRows * RS + R * R + 12) + 15) / 16) * 16);
       if ((int)blockIdx.x < nu) {
-        cpcg_bytes(sG, p.gam, (int64_t)R * R * 4, tid, kPWThreads);  // waited for with the unit's rows
+        if (tid == 0) {  // Gamma (every CTA reads it now): a bulk copy, waited for with the unit's rows
+          pw_bulk_begin(bk, pw_b16((int64_t)R * R * 4));
+          bulk_g2s(sG, p.gam, pw_b16((int64_t)R * R * 4), bk.bar);
+        }
         if (blockIdx.x == 0)
           for (int e = tid; e < R * R; e += kPWThreads) p.Gam_out[e] = __ldcg(p.gam + e);
-        for (int u = blockIdx.x; u < nu; u += G) pw_update_unit(p, n, u, alpha, sA, sS, sM, sG, sgp, ss, u == (int)blockIdx.x ? mk : nullptr);
+        for (int u = blockIdx.x; u < nu; u += G) pw_update_unit(p, n, u, alpha, sA, sS, sM, sG, sgp, ss, u == (int)blockIdx.x ? &bk : nullptr,
+                                                                 u == (int)blockIdx.x ? mk : nullptr);
       }
     }
     PW_MARK(5);
@@ -1063,18 +1113,19 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
         double* Wd = reinterpret_cast<double*>(sm + offW);
         const int RD = ut_rd(R);
         double* Ad = Wd + R * RD;
-        double* part = Ad + kPWRows * RD;
         int rank = 0, bad0 = 0;
         double fro = 0.0;
         if (lev) {
           if (tid == 0) wait_count(p.pcnt, (unsigned)G * (unsigned)(s + 1));
           __syncthreads();
           PW_MARK(18);
-          {  // the packed Gram (L2 copy) -> the full symmetric matrix, closed-form pair index
-            double* gst = Wd;  // staging (the W area is written only after the inverse)
-            cpcg_bytes(gst, p.gram, (int64_t)P * 8, tid, kPWThreads);
-            cp_async_wait<0>();
-            __syncthreads();
+          {  // the packed Gram (a bulk copy: every CTA reads it now) -> the full symmetric matrix
+            double* gst = Wd;  // staging
+            if (tid == 0) {
+              pw_bulk_begin(bk, pw_b16((int64_t)P * 8));
+              bulk_g2s(gst, p.gram, pw_b16((int64_t)P * 8), bk.bar);
+            }
+            pw_bulk_wait(bk);
             for (int e = tid; e < R * R; e += kPWThreads) {
               const int r1 = e / R, r2 = e % R;
               const int a = r1 <= r2 ? r1 : r2, b = r1 <= r2 ? r2 : r1;
@@ -1105,17 +1156,15 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
           rank = (In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, ss.tol, rowbuf, swept, diag)
                               : grp_sweep_inverse<RMAX, kPWSweepGroups<RMAX>>(Gm, R, ss.tol, rowbuf, swept);
           PW_MARK(20);
-          for (int e = tid; e < R * RD; e += kPWThreads) {
-            const int i = e / RD, j = e % RD;
-            Wd[e] = j < R ? Gm[i * RS + j] : 0.0;
-          }
           bad0 = ss.bad | (rank == 0 ? 2 : 0);
-          __syncthreads();
         } else {
-          if (tid == 0) {
+          if (wid == 0) {  // ||A||_F^2: lane-strided unit partials, then a fixed xor tree (deterministic)
+            __syncwarp();
             double t = 0.0;
-            for (int u = 0; u < nu; ++u) t += __ldcg(p.gpart + u);
-            ss.tol = t;
+            for (int u = lane; u < nu; u += 32) t += __ldcg(p.gpart + u);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == 0) ss.tol = t;
           }
           __syncthreads();
           fro = ss.tol;
@@ -1124,7 +1173,12 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
         }
         PW_MARK(8);
         // ---- Q: scores, quantisation, look-back prefix -> CDF rows, T, status ----
-        for (int u = blockIdx.x; u < nu; u += G) pw_table_unit(p, n, u, nu, tag, Wd, rank, fro, bad0, Ad, part, ss, u == (int)blockIdx.x ? mk : nullptr);
+        // the update phase left the new rows of this CTA's last unit in shared memory (sA, stride R; the
+        // pair sums and the inverse use the area past uw_step_bytes only)
+        const float* sAlast = reinterpret_cast<const float*>(sm) + ((R * R + 3) & ~3);
+        for (int u = blockIdx.x; u < nu; u += G)
+          pw_table_unit(p, n, u, nu, tag, Gm, rank, fro, bad0, Ad, u + G >= nu ? sAlast : nullptr, ss,
+                        u == (int)blockIdx.x ? mk : nullptr);
       }
       PW_MARK(9);
       grid_barrier(p.bar, gen);  // the table of the new A^(n) is complete (R9)
