@@ -59,6 +59,7 @@ def lib():
         L.orc_build_table.argtypes = [i32, i64, i32, P, P, P, P]
         L.orc_default_windows.argtypes = [i32, P, i32, i64, P]
         L.orc_sample.argtypes = [i32, P, i32, i32, i64, P, P, P, u64, u64, P, P, P, P]
+        L.orc_sample_stratified.argtypes = [i32, P, i32, i32, i64, P, P, u64, u64, i32, P, P, P, P]
         L.orc_gradient.argtypes = [i32, P, i32, P, P, i32, i32, i64, i64, P, P, P, P, P]
         L.orc_update_fixed.argtypes = [i64, i32, P, P, dbl]
         L.orc_update_adaptive.argtypes = [i64, i32, P, P, P, dbl, dbl, dbl]
@@ -196,6 +197,22 @@ def sample(dims, n: int, strategy: int, B: int, tables, seed: int, it: int, wind
                           C.c_uint64(seed), C.c_uint64(it), _p(idx), _p(w), _p(pj), C.byref(Beff)), "sample")
     b = Beff.value
     return idx[:b].copy(), w[:b].copy(), pj[:b].copy()
+
+
+def sample_stratified(dims, n: int, strategy: int, B: int, tables, seed: int, it: int, slab_lo):
+    """stratified per-slab draws (orc_sample_stratified; reading R26).  slab_lo: P+1 slab bounds of the
+    last mode.  Returns idx (B, N-1) int32, w (B,) fp64, pj (B,) with 1/(B J_n pj) = w."""
+    d = _dims(dims)
+    N = len(d)
+    qs = [np.ascontiguousarray(t[0], dtype=np.uint64) for t in tables]
+    T = np.ascontiguousarray([t[1] for t in tables], dtype=np.uint64)
+    lo = np.ascontiguousarray(slab_lo, dtype=np.int64)
+    idx = np.zeros((B, N - 1), dtype=np.int32)
+    w = np.zeros(B)
+    pj = np.zeros(B)
+    _chk(lib().orc_sample_stratified(N, _p(d), n, strategy, B, _ptrs(qs), _p(T), C.c_uint64(seed), C.c_uint64(it),
+                                     len(lo) - 1, _p(lo), _p(idx), _p(w), _p(pj)), "sample_stratified")
+    return idx, w, pj
 
 
 def gradient(X: np.ndarray, dims, factors, n: int, strategy: int, B: int, idx, pj):

@@ -434,6 +434,82 @@ int orc_sample(int N, const int64_t* dims, int n, int strategy, int64_t B, const
 }
 
 /* ------------------------------------------------------------------------------------
+ * Stratified per-slab sampling (reading R26 in DESIGN.md): the row-wise draws of
+ * eq:ik with the batch split into P strata, one per slab of the LAST mode.
+ *   slabs    : P contiguous ranges [lo_g, hi_g) of the last mode's index, lo[0] = 0, lo[P] = I_{N-1}
+ *   strata   : stratum g = batch rows [off_g, off_g + B_g), B_g = floor(B/P) + (g < B mod P), B >= P
+ *   draws    : every remaining mode k < N-1 exactly as orc_sample (same Philox counter of row b and
+ *              position); the last mode from the slab's conditional law q_i / Q_g (i in slab g,
+ *              Q_g = sum of q over the slab): r = (q_0 + ... + q_{lo_g - 1}) + floor(u Q_g / 2^64), i =
+ *              #{i : cdf_i <= r}, which lies in the slab.
+ *   estimator: unbiased stratum by stratum (the argument of Theorem 5.1, applied
+ *              to each stratum: E over stratum g of (1/B_g) sum_b g_{j_b} / P_g(j_b) = sum_{j in g} g_j),
+ *              so w_b = 1/(B_g prod_k ptilde_k) with ptilde_k = I_k q_k/T_k (k < N-1) and
+ *              ptilde_{N-1} = I_{N-1} q_i / Q_g, in that order (contract of DESIGN.md section 4);
+ *              pj_b = (B_g / B) prod_k (q_k/T_k or q_i/Q_g), so that orc_gradient's 1/(B J_n pj_b) = w_b.
+ *   Q_g = 0  : the slab has probability 0 (no fibers of it could be drawn unstratified either): the
+ *              stratum's rows take i = lo_g, w = 0, pj = +inf (they contribute nothing).
+ * Mode n == N-1 (every fiber spans all slabs): no strata, identical to orc_sample.  Row-wise
+ * strategies only (uniform / leverage / Euclidean); ORC_EINVAL otherwise, or when B < P.
+ * ---------------------------------------------------------------------------------- */
+int orc_sample_stratified(int N, const int64_t* dims, int n, int strategy, int64_t B, const uint64_t* const* q,
+                          const uint64_t* T, uint64_t seed, uint64_t iter, int P, const int64_t* slab_lo,
+                          int32_t* idx, double* w, double* pj) {
+  if (N < 3 || n < 0 || n >= N || B < 1 || P < 1) return ORC_EINVAL;
+  if (!(strategy == ORC_UNIFORM || strategy == ORC_LEVERAGE || strategy == ORC_EUCLIDEAN)) return ORC_EINVAL;
+  if (n == N - 1 || P == 1) return orc_sample(N, dims, n, strategy, B, NULL, q, T, seed, iter, idx, w, pj, NULL);
+  if (B < P || slab_lo[0] != 0 || slab_lo[P] != dims[N - 1]) return ORC_EINVAL;
+  for (int g = 0; g < P; ++g)
+    if (slab_lo[g + 1] <= slab_lo[g]) return ORC_EINVAL;
+  const int64_t IL = dims[N - 1];
+  int64_t b = 0;
+  for (int g = 0; g < P; ++g) {
+    const int64_t Bg = B / P + (g < B % P ? 1 : 0);
+    const int64_t lo = slab_lo[g], hi = slab_lo[g + 1];
+    uint64_t base = 0, Qg = 0;
+    for (int64_t i = 0; i < lo; ++i) base += q[N - 1][i];
+    for (int64_t i = lo; i < hi; ++i) Qg += q[N - 1][i];
+    for (int64_t t = 0; t < Bg; ++t, ++b) {
+      double prod = 1.0, pprod = 1.0;
+      int pos = 0;
+      for (int k = 0; k < N; ++k) {
+        if (k == n) continue;
+        uint64_t u = orc_word(seed, iter, (uint32_t)b, 0, (uint32_t)pos);
+        int64_t i;
+        double pt, pk;
+        if (k < N - 1) {
+          uint64_t r = orc_scale(u, T[k]);
+          i = orc_count_le(q[k], dims[k], r);
+          pt = (double)((uint64_t)dims[k] * q[k][i]) / (double)T[k];
+          pk = (double)q[k][i] / (double)T[k];
+        } else if (Qg > 0) {
+          uint64_t r = base + orc_scale(u, Qg);
+          i = orc_count_le(q[k], IL, r);
+          pt = (double)((uint64_t)IL * q[k][i]) / (double)Qg;
+          pk = (double)q[k][i] / (double)Qg;
+        } else {
+          i = lo;
+          pt = 0.0;
+          pk = 0.0;
+        }
+        idx[b * (N - 1) + pos] = (int32_t)i;
+        prod = (pos == 0) ? pt : prod * pt;
+        pprod = (pos == 0) ? pk : pprod * pk;
+        ++pos;
+      }
+      if (Qg > 0) {
+        w[b] = 1.0 / ((double)Bg * prod);
+        if (pj) pj[b] = ((double)Bg / (double)B) * pprod;
+      } else {
+        w[b] = 0.0;
+        if (pj) pj[b] = INFINITY;
+      }
+    }
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------------------
  * Stochastic gradient, literally as eq:gradient1 (4.1) for the row-wise
  * strategies and uniform (BrasCPD, :155, reading R1) and eq:gradient2 (4.2, :450-457) for the
  * block strategies; D placed as Z^T D Z and X D Z (reading R2 of the garbled :442):
