@@ -83,6 +83,17 @@ typedef enum { CP_ORDER_CYCLIC = 0, CP_ORDER_RANDOM = 1 } cp_mode_order;
                                       two chains fit one GPC (cp_sgd_sweep_multi throughput mode)   */
 #define CP_FLAG_NO_WIDE 0x10u      /* single GPU, split path: never use the fused gather + update kernel
                                      (k_gather_update); use the gather-partials + update-table pair */
+#define CP_FLAG_STRATIFIED 0x100u  /* world > 1 (slab sharding), row-wise samplers: stratified per-slab sampling
+                                      (reading R26 in DESIGN.md): for modes n < N-1 the batch
+                                      is split into world_size strata, B_g = floor(B/P) (+1 for g < B mod P)
+                                      rows each, and stratum g draws the last mode from the conditional law
+                                      of slab g (q_i / Q_g); weights omega_b = 1/(B_g prod_k ptilde_k) with
+                                      ptilde_{N-1} = I_{N-1} q_i / Q_g -- unbiased stratum by stratum
+                                      (Theorem 5.1); a zero-mass slab gives its rows
+                                      omega = 0.  Every rank then gathers exactly B_g fibers (its own
+                                      stratum): balanced owner-computes.  Mode N-1 is unchanged.  Needs
+                                      slab_bounds with CP_FLAG_EXTERNAL_COMM; CP_EINVAL for block samplers,
+                                      B < world_size or world_size > 16. */
 #define CP_FLAG_NO_PERSIST 0x80u   /* fp32 wide path: never use the persistent cooperative sweep kernel
                                      (k_sweep_wide); run each step as the gather / update+table /
                                      sample kernel chain (graph-captured for cyclic sweeps)        */
@@ -112,6 +123,11 @@ typedef struct {
   int64_t slab_begin, slab_end;/* local range of the LAST mode's index (slab sharding); ignored
                                   (whole tensor) when world_size == 1                              */
   uint32_t flags;              /* CP_FLAG_*                                                        */
+  const int64_t* slab_bounds;  /* host, world_size + 1 entries: slab g = [slab_bounds[g], slab_bounds[g+1])
+                                  of the last mode, contiguous in rank order, slab_bounds[0] = 0 and
+                                  slab_bounds[world_size] = I_{N-1}, this rank's entry equal to
+                                  [slab_begin, slab_end); or NULL (the ranks' ranges are exchanged over the
+                                  internal communicator).  Read at init only.                      */
 } cp_sgd_config;
 
 /* Create a handle: validates cfg (CP_EINVAL: N < 3 or > 16, R < 1 or > 64, B < 1, eta <= 0,
@@ -163,6 +179,13 @@ cp_status cp_sgd_sweep_multi(cp_sgd_t* hs, int32_t nh, int32_t nsweeps);
  * summed over ranks when sharded.  Synchronises.  CP_EDEGENERATE when ||X|| = 0. */
 cp_status cp_fit(cp_sgd_t h, double* fit_host);
 
+/* Squared Frobenius norms of the last-mode slices of a first-index-fastest tensor (or of a rank's local
+ * slab): out_dev[i] = sum of x^2 over slice i (fp64, a fixed summation order), i < nslices <= 65535,
+ * slice_len = product of the other dims.  No handle; enqueued on `stream` (cudaStream_t).  The data-side
+ * proxy of the sampling mass the last factor's rows converge to, for mass-balanced contiguous slabs
+ * (SURVEY 8(e) mitigation 2; host logic: paper_2103_04081_b200.parallel.balanced_slab_ranges). */
+cp_status cp_slice_sqnorms(const void* X_dev, int32_t dtype, int64_t nslices, int64_t slice_len, double* out_dev,
+                           void* stream);
 /* Wait for the stream; report device-side errors of earlier asynchronous calls. */
 cp_status cp_sgd_sync(cp_sgd_t h);
 

@@ -22,6 +22,7 @@ ORDERS = {"cyclic": 0, "random": 1}
 FLAG_MODE_MAJOR, FLAG_NO_GRAPH, FLAG_EXTERNAL_COMM, FLAG_NO_FUSED, FLAG_NO_WIDE, FLAG_NO_TC, FLAG_FUSED_CU8 = \
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
 FLAG_NO_PERSIST = 0x80
+FLAG_STRATIFIED = 0x100
 KERNEL_NAMES = ["k_sample", "k_gather", "k_update_table", "k_table", "k_reduce_partials", "nccl", "k_fit",
                 "k_sweep_fused", "k_gather_update", "k_zw_gamma", "k_gather_update_tc", "k_table_sample",
                 "k_update_wide", "k_scores_wide", "k_sample_wide", "k_sweep_wide"]
@@ -33,7 +34,7 @@ EXPORTS = ["cp_sgd_init", "cp_sgd_destroy", "cp_sgd_last_error", "cp_sgd_sample"
            "cp_sgd_get_table", "cp_sgd_get_grad", "cp_sgd_get_accum", "cp_sgd_get_iter", "cp_sgd_set_iter",
            "cp_sgd_refresh_tables", "cp_sgd_get_launches", "cp_sgd_profile", "cp_sgd_profile_read",
            "cp_sgd_version", "cp_sgd_batch_max", "cp_sgd_debug_timers", "cp_sgd_exchange_copy", "cp_sgd_trace_layout",
-           "cp_sgd_trace", "cp_sgd_trace_count", "cp_sgd_path"]
+           "cp_sgd_trace", "cp_sgd_trace_count", "cp_sgd_path", "cp_slice_sqnorms"]
 
 
 class CPError(RuntimeError):
@@ -50,6 +51,7 @@ class Config(C.Structure):
         ("alpha", C.c_double), ("eta", C.c_double), ("b", C.c_double), ("eps", C.c_double),
         ("seed", C.c_uint64), ("stream", C.c_void_p), ("world_rank", C.c_int32), ("world_size", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("slab_begin", C.c_int64), ("slab_end", C.c_int64), ("flags", C.c_uint32),
+        ("slab_bounds", C.POINTER(C.c_int64)),
     ]
 
 
@@ -96,6 +98,7 @@ def load_library(path: str = LIB_PATH):
     L.cp_sgd_trace.argtypes = [P, P, i64]
     L.cp_sgd_trace_count.argtypes = [P, C.POINTER(C.c_int64)]
     L.cp_sgd_path.argtypes = [P, C.POINTER(C.c_int32)]
+    L.cp_slice_sqnorms.argtypes = [P, i32, i64, i64, P, P]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype if name in ("cp_sgd_last_error", "cp_sgd_version") else C.c_int
     _lib = L
@@ -125,7 +128,8 @@ class CPSGD:
                  seed: int = 0, stream=None, world_rank: int = 0, world_size: int = 1, nccl_id: bytes = None,
                  slab=None, mode_major: bool = True, block_window=None, graphs: bool = True,
                  external_comm: bool = False, fused: bool = True, wide: bool = True,
-                 tc: bool = True, fused_cluster: int = 16, persist: bool = True):
+                 tc: bool = True, fused_cluster: int = 16, persist: bool = True, stratified: bool = False,
+                 slab_bounds=None):
         import torch
 
         L = load_library()
@@ -151,12 +155,14 @@ class CPSGD:
         flags = (FLAG_MODE_MAJOR if mode_major else 0) | (0 if graphs else FLAG_NO_GRAPH) | \
                 (FLAG_EXTERNAL_COMM if external_comm else 0) | (0 if fused else FLAG_NO_FUSED) | \
                 (0 if wide else FLAG_NO_WIDE) | (0 if tc else FLAG_NO_TC) | \
-                (FLAG_FUSED_CU8 if fused_cluster == 8 else 0) | (0 if persist else FLAG_NO_PERSIST)
+                (FLAG_FUSED_CU8 if fused_cluster == 8 else 0) | (0 if persist else FLAG_NO_PERSIST) | \
+                (FLAG_STRATIFIED if stratified else 0)
         lo, hi = (0, self.dims[-1]) if slab is None else (int(slab[0]), int(slab[1]))
         cfg = Config(self.N, self._dims_arr, self.R, self.dtype, X.data_ptr(), self._fac_arr, int(batch),
                      self._win_arr, SAMPLERS[sampler], RULES[rule], float(alpha), float(eta), float(b), float(eps),
                      int(seed) & (2 ** 64 - 1), stream.cuda_stream, int(world_rank), int(world_size),
-                     None if self._nccl_id is None else C.cast(self._nccl_id, C.c_void_p), lo, hi, flags)
+                     None if self._nccl_id is None else C.cast(self._nccl_id, C.c_void_p), lo, hi, flags,
+                     None if slab_bounds is None else self._bounds_arr(slab_bounds))
         h = C.c_void_p()
         st = L.cp_sgd_init(C.byref(cfg), C.byref(h))
         if st != 0:
@@ -168,6 +174,10 @@ class CPSGD:
         self.rule = rule
         self.slab = (lo, hi)
         self.world_size = world_size
+
+    def _bounds_arr(self, bounds):
+        self._bounds = (C.c_int64 * len(bounds))(*[int(b) for b in bounds])
+        return C.cast(self._bounds, C.POINTER(C.c_int64))
 
     # -- plumbing -----------------------------------------------------------------------------
     def _chk(self, st):
@@ -362,3 +372,21 @@ class CPSGD:
         n = C.c_int32(0)
         self._chk(self._L.cp_sgd_profile_read(self._h, cap, ids, tot, cnt, C.byref(n)))
         return {KERNEL_NAMES[ids[i]]: (tot[i], int(cnt[i])) for i in range(n.value)}
+
+
+def slice_sqnorms(X, nslices: int, stream=None):
+    """cp_slice_sqnorms: fp64 squared norms of the nslices last-mode slices of the CUDA tensor X (a
+    torch tensor; marshalling only -- the sums run in the library's kernels)."""
+    import torch
+
+    L = load_library()
+    if not X.is_cuda or not X.is_contiguous():
+        raise ValueError("X must be a contiguous CUDA tensor")
+    out = torch.empty(int(nslices), dtype=torch.float64, device=X.device)
+    s = torch.cuda.current_stream(X.device) if stream is None else stream
+    st = L.cp_slice_sqnorms(X.data_ptr(), _dtype_code(X), int(nslices), X.numel() // int(nslices), out.data_ptr(),
+                            s.cuda_stream)
+    if st != 0:
+        raise CPError(st, "cp_slice_sqnorms")
+    return out
+

@@ -232,6 +232,7 @@ struct cp_sgd_s {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
   std::vector<int64_t> row_ranges;  // [2*world]: slab [lo, hi) of every rank
+  int64_t strat_lo[kMaxStrata + 1] = {};  // CP_FLAG_STRATIFIED: slab bounds of the ranks (R26)
 
   cp_status fail(cp_status st, const char* fmt, ...) {
     char buf[512];
@@ -338,6 +339,10 @@ void fill_sample_params(cp_sgd_s* h, SampleParams& p, int n, const uint64_t* ite
   p.lo_last = h->lo_last;
   p.mode_major = h->Xmm[n] ? 1 : 0;
   p.pitch = h->pitch[n];
+  if (h->flags & CP_FLAG_STRATIFIED) {  // R26: one stratum per rank's slab
+    p.strat_P = h->world_size;
+    for (int g = 0; g <= h->world_size; ++g) p.strat_lo[g] = h->strat_lo[g];
+  }
   if (prefetch) {
     p.zrow = h->zrow;
     p.fbase = h->fbase;
@@ -1680,6 +1685,32 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       for (size_t i = 0; i < one.size(); ++i) (*rr)[i] = (int64_t)one[i];
     }
   }
+  // ---- stratified per-slab sampling (R26): the slab bounds of every rank ----
+  if (h->flags & CP_FLAG_STRATIFIED) {
+    const int P = h->world_size;
+    const int64_t IL = h->dims[h->N - 1];
+    if (P < 2 || P > kMaxStrata || block || h->B < P)
+      return init_fail(h, h->fail(CP_EINVAL, "CP_FLAG_STRATIFIED needs 2 <= world_size <= %d, a row-wise sampler and "
+                                             "batch >= world_size", kMaxStrata));
+    if (cfg->slab_bounds) {
+      for (int g = 0; g <= P; ++g) h->strat_lo[g] = cfg->slab_bounds[g];
+    } else if (!(h->flags & CP_FLAG_EXTERNAL_COMM)) {
+      const auto& rr = h->row_ranges;
+      for (int g = 0; g < P; ++g) {
+        if (g > 0 && rr[2 * g] != rr[2 * g - 1])
+          return init_fail(h, h->fail(CP_EINVAL, "stratified sampling needs contiguous slabs in rank order"));
+        h->strat_lo[g] = rr[2 * g];
+      }
+      h->strat_lo[P] = rr[2 * P - 1];
+    } else {
+      return init_fail(h, h->fail(CP_EINVAL, "CP_FLAG_STRATIFIED with CP_FLAG_EXTERNAL_COMM needs slab_bounds"));
+    }
+    bool ok = h->strat_lo[0] == 0 && h->strat_lo[P] == IL && h->strat_lo[h->world_rank] == h->lo_last &&
+              h->strat_lo[h->world_rank + 1] == h->hi_last;
+    for (int g = 0; g < P; ++g) ok = ok && h->strat_lo[g + 1] > h->strat_lo[g];
+    if (!ok) return init_fail(h, h->fail(CP_EINVAL, "slab_bounds: not a contiguous rank-order cover of [0, I_last) "
+                                                    "matching this rank's slab"));
+  }
   // ---- initial tables of every mode ----
   for (int k = 0; k < h->N; ++k) {
     cp_status st = launch_table_any(h, k);
@@ -2091,6 +2122,24 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
     CUDA_TRY(h, cudaMemcpyAsync(factors_host[k], h->factors[k], h->esz * h->dims[k] * h->R, cudaMemcpyDeviceToHost,
                                 h->stream));
   return cp_sgd_sync(h);
+}
+
+cp_status cp_slice_sqnorms(const void* X_dev, int32_t dtype, int64_t nslices, int64_t slice_len, double* out_dev,
+                           void* stream) {
+  if (!X_dev || !out_dev || nslices < 1 || slice_len < 1 || nslices > 65535 || (dtype != CP_F32 && dtype != CP_F64))
+    return CP_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  double* part = nullptr;
+  if (cudaMallocAsync((void**)&part, sizeof(double) * (size_t)nslices * kSliceChunks, st) != cudaSuccess)
+    return CP_ENOMEM;
+  const dim3 grid(kSliceChunks, (unsigned)nslices);
+  if (dtype == CP_F64)
+    k_slice_sq<double><<<grid, 256, 0, st>>>((const double*)X_dev, slice_len, part);
+  else
+    k_slice_sq<float><<<grid, 256, 0, st>>>((const float*)X_dev, slice_len, part);
+  k_slice_sum<0><<<(unsigned)((nslices + 255) / 256), 256, 0, st>>>(part, nslices, out_dev);
+  cudaFreeAsync(part, st);
+  return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ECUDA;
 }
 
 cp_status cp_fit(cp_sgd_t h, double* fit_host) {

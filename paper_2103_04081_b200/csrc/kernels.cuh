@@ -22,6 +22,7 @@ namespace cps {
 
 constexpr int kMaxOrder = 16;
 constexpr int kMaxRank = 64;
+constexpr int kMaxStrata = 16;  // slabs of the stratified sampler (ranks of one box)
 constexpr int kSweepBuf = 5 * kMaxRank;  // doubles of pivot-row buffer the sweep inverses need
 
 // ------------------------------------------------------------------------------------------
@@ -55,6 +56,11 @@ struct SampleParams {
   void* zwp;                       // T [B_max][ceil8(R)]
   void* gam_next;                  // T [R][R]
   float* zimg;                     // tcgen05 path: 3xTF32 A-operand images of zw (or NULL)
+  // stratified per-slab sampling (CP_FLAG_STRATIFIED; reading R26): strat_P > 1 strata, stratum g = batch
+  // rows [off_g, off_g + B_g), B_g = B/P (+1 for g < B mod P), drawing the last mode from slab
+  // [strat_lo[g], strat_lo[g + 1]) (modes n < N-1 only; 0 = off)
+  int strat_P;
+  int64_t strat_lo[kMaxStrata + 1];
 };
 
 // debug trace of the consumed batches and the states they lead to (cp_sgd_trace; persistent kernels
@@ -445,16 +451,40 @@ __device__ __forceinline__ void draw_rows(const SampleParams& p, const uint64_t*
     }
     int32_t* ib = p.idx + b * (N - 1);
     if (!block) {
+      // stratified (R26): this row's stratum g and the slab's CDF base / mass (exact integers)
+      const bool strat = p.strat_P > 1 && n != N - 1;
+      int64_t Bw = p.B, slo = 0, shi = 0;
+      uint64_t sbase = 0, smass = 0;
+      if (strat) {
+        const int64_t P = p.strat_P, q0 = p.B / P, rm = p.B % P;
+        const int64_t g = b < rm * (q0 + 1) ? b / (q0 + 1) : rm + (b - rm * (q0 + 1)) / q0;
+        Bw = q0 + (g < rm ? 1 : 0);
+        slo = p.strat_lo[g];
+        shi = p.strat_lo[g + 1];
+        if (p.strategy == 0) {
+          sbase = (uint64_t)slo;
+          smass = (uint64_t)(shi - slo);
+        } else {
+          const uint64_t* c = cdfp[N - 1];
+          const uint64_t cb = c[slo > 0 ? slo - 1 : 0];  // unconditional load, then select
+          sbase = slo > 0 ? cb : 0ull;
+          smass = c[shi - 1] - sbase;
+        }
+      }
       double prod = 1.0;
       int pos = 0;
       for (int k = 0; k < N; ++k) {
         if (k == n) continue;
-        const uint64_t Tk = (p.strategy == 0) ? (uint64_t)p.dims[k] : p.Ttot[k];
+        const bool sk = strat && k == N - 1;
+        const uint64_t Tk = sk ? smass : (p.strategy == 0) ? (uint64_t)p.dims[k] : p.Ttot[k];
         const uint64_t u = draw_word(p.seed, r_it, (uint32_t)b, kPurposeRow, (uint32_t)pos);
-        const uint64_t rr = scale_draw(u, Tk);
+        const uint64_t rr = (sk ? sbase : 0ull) + scale_draw(u, Tk);
         int64_t i;
         uint64_t qk;
-        if (p.strategy == 0) {
+        if (sk && smass == 0) {  // a zero-mass slab: no fiber of it can be drawn; the row carries w = 0
+          i = slo;
+          qk = 0;
+        } else if (p.strategy == 0) {
           i = (int64_t)rr;
           qk = 1;
         } else {
@@ -464,12 +494,13 @@ __device__ __forceinline__ void draw_rows(const SampleParams& p, const uint64_t*
           qk = c[i] - (i > 0 ? cprev : 0ull);
         }
         ib[pos] = (int32_t)i;
-        const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);
+        const double pt = qk == 0 ? 0.0 : __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);
         prod = (pos == 0) ? pt : __dmul_rn(prod, pt);
         ++pos;
       }
-      p.w[b] = __ddiv_rn(1.0, __dmul_rn((double)p.B, prod));
-      if (sw) sw[b - b0] = __ddiv_rn(1.0, __dmul_rn((double)p.B, prod));
+      const double wv = prod == 0.0 ? 0.0 : __ddiv_rn(1.0, __dmul_rn((double)Bw, prod));
+      p.w[b] = wv;
+      if (sw) sw[b - b0] = wv;
     } else {
       int64_t rem = b;
       for (int q = 0; q < N - 1; ++q) {
@@ -1524,6 +1555,41 @@ __global__ void __launch_bounds__(kUTThreads) k_update_table(UTParams<T> p) {
   if (p.do_update) {
     if (!synced) cluster.sync();   // all CTAs have read r_now
     if (q == 0 && tid == 0) *p.iter = r_now + 1;  // r <- r + 1 (Alg. 6/7)
+  }
+}
+
+// squared Frobenius norms of the last-mode slices (cp_slice_sqnorms; SURVEY 8(e) mitigation 2, the
+// data-side proxy of the slab masses): block (x, y) sums chunk x of slice y in fp64 -> part[y][x]
+constexpr int kSliceChunks = 32;
+template <typename T>
+__global__ void __launch_bounds__(256) k_slice_sq(const T* __restrict__ X, int64_t slice_len, double* __restrict__ part) {
+  const int64_t s = blockIdx.y, c = blockIdx.x;
+  const int64_t per = (slice_len + kSliceChunks - 1) / kSliceChunks;
+  const int64_t a = c * per, b = min(slice_len, a + per);
+  const T* x = X + s * slice_len;
+  double acc = 0.0;
+  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+    const double v = (double)x[i];
+    acc = fma(v, v, acc);
+  }
+  __shared__ double red[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[s * kSliceChunks + c] = t;
+  }
+}
+template <int V = 0>  // headers hold only templates of __global__ functions (one emitting unit each)
+__global__ void k_slice_sum(const double* __restrict__ part, int64_t nslices, double* __restrict__ out) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nslices) {
+    double t = 0.0;
+    for (int c = 0; c < kSliceChunks; ++c) t += part[s * kSliceChunks + c];  // chunk order
+    out[s] = t;
   }
 }
 

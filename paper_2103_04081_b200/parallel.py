@@ -28,6 +28,57 @@ def slab_ranges(I_last: int, world: int) -> List[Tuple[int, int]]:
     return out
 
 
+def balanced_slab_ranges(weights, world: int, max_len: int = None) -> List[Tuple[int, int]]:
+    """Mass-balanced contiguous slabs (SURVEY 8(e) mitigation 2): rank-order ranges [lo, hi) of the last mode
+    whose total `weights` (e.g. the slice energies ||X(:, ..., :, i)||^2 from cp_slice_sqnorms, the proxy of
+    the sampling mass the last factor converges to) are as equal as the contiguity allows.  Boundary g is
+    the index whose cumulative weight is closest to g/world of the total, kept inside the feasible range
+    (every slab non-empty and at most max_len long, so each rank's slab fits its memory).  With stratified
+    sampling (CP_FLAG_STRATIFIED) equal-mass slabs make the equal per-rank strata close to proportional
+    allocation, which never has a larger variance than unstratified sampling."""
+    w = [float(x) for x in weights]
+    n = len(w)
+    if world < 1 or n < world:
+        raise ValueError("need 1 <= world <= number of slices")
+    if any(x < 0 or x != x for x in w):
+        raise ValueError("weights must be finite and >= 0")
+    cap = n if max_len is None else int(max_len)
+    if cap * world < n:
+        raise ValueError("max_len too small: the slabs cannot cover every slice")
+    cum = [0.0]
+    for x in w:
+        cum.append(cum[-1] + x)
+    tot = cum[-1]
+    bounds = [0]
+    for g in range(1, world):
+        lo_ok = max(bounds[-1] + 1, n - (world - g) * cap)  # later slabs must still fit
+        hi_ok = min(bounds[-1] + cap, n - (world - g))      # later slabs non-empty
+        if tot > 0:
+            target = tot * g / world
+            b = min(max(lo_ok, 1), hi_ok)
+            best, bd = b, abs(cum[b] - target)
+            for c in range(lo_ok, hi_ok + 1):  # plain scan: the closest feasible cumulative weight
+                d = abs(cum[c] - target)
+                if d < bd:
+                    best, bd = c, d
+            b = best
+        else:
+            b = min(max(lo_ok, (n * g) // world), hi_ok)
+        bounds.append(b)
+    bounds.append(n)
+    return [(bounds[g], bounds[g + 1]) for g in range(world)]
+
+
+def slab_bounds(ranges) -> List[int]:
+    """[lo_0, lo_1, ..., lo_{P-1}, hi_{P-1}]: the cp_sgd_config.slab_bounds array of contiguous ranges"""
+    out = [int(ranges[0][0])]
+    for (lo, hi), nxt in zip(ranges, list(ranges[1:]) + [None]):
+        if nxt is not None and int(nxt[0]) != int(hi):
+            raise ValueError("slab ranges are not contiguous")
+        out.append(int(hi))
+    return out
+
+
 def owned_fibers(idx_last, lo: int, hi: int):
     """mask of sampled fibers whose last-mode index falls in this rank's slab (owner computes)."""
     return (idx_last >= lo) & (idx_last < hi)
