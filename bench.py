@@ -220,34 +220,38 @@ def run_ours(args, cfg):
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.Stream(device=dev)
+    # N > 1: C5 (256 GB) slab-sharded along the last mode (BASELINE configs[4]); every other workload ONE
+    # chain on whole-tensor replicas with a batch split + allreduce of M (CP_FLAG_REPLICA; BASELINE
+    # configs[3] "at 1/2/4/8 GPUs ... + allreduce", SURVEY 8(e) "C4 alternative"); --independent: one
+    # unrelated chain per GPU (weak scaling)
     sharded = (cfg.name == "C5" and ws > 1)
+    replica = (ws > 1 and not sharded and not args.independent)
     slab = None
     nccl_id = None
     if sharded:
-        I_last = cfg.dims[-1]
-        per = I_last // ws
-        slab = (rank * per, I_last if rank == ws - 1 else (rank + 1) * per)
+        from paper_2103_04081_b200.parallel import slab_ranges
+
+        slab = slab_ranges(cfg.dims[-1], ws)[rank]
+    if sharded or replica:
         import torch.distributed as dist
+
+        from paper_2103_04081_b200.cpsgd import nccl_unique_id
 
         idt = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
-            import ctypes as C
-
-            nccl = C.CDLL("libnccl.so.2")
-            buf = C.create_string_buffer(128)
-            assert nccl.ncclGetUniqueId(buf) == 0
-            idt.copy_(torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8))
+            idt.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().numpy().tobytes())
     Xd, Ad, Xh, A0h = make_inputs(cfg, dev, slab=slab)
     torch.cuda.synchronize()
-    seed = cfg.seed if sharded else cfg.seed + 1000 * rank  # independent chains when replicated
+    one_chain = sharded or replica
+    seed = cfg.seed if one_chain else cfg.seed + 1000 * rank  # independent chains: their own seeds
     t0 = time.time()
     with torch.cuda.stream(stream):
         h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=args.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta,
-                  seed=seed, stream=stream, world_rank=rank if sharded else 0, world_size=ws if sharded else 1,
+                  seed=seed, stream=stream, world_rank=rank if one_chain else 0, world_size=ws if one_chain else 1,
                   nccl_id=nccl_id, slab=slab, mode_major=not args.native_layout, fused=args.path == "auto",
-                  tc=not args.no_tc)
+                  tc=not args.no_tc, replica=replica)
     init_s = time.time() - t0
     h_path = h.path
     N = cfg.order
@@ -285,7 +289,7 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    total_fibers = fibers_per_step * args.steps * (1 if sharded else ws)
+    total_fibers = fibers_per_step * args.steps * (1 if one_chain else ws)
     value = total_fibers / (ms / 1e3)
 
     # ---- per-kernel device durations (CUDA events on the launch stream, direct launches) ----
@@ -307,7 +311,7 @@ def run_ours(args, cfg):
         In_avg = (sum(cfg.dims[:-1]) + (slab[1] - slab[0])) / N
     # algorithmic bytes per k_gather launch: the sampled fibers (B_eff x I_n x sizeof); per the
     # sharded path only the locally owned part
-    gather_bytes = (fibers_per_step / N) * In_avg * esz
+    gather_bytes = (fibers_per_step / N) * In_avg * esz / (ws if replica else 1)  # replicas: this rank's chunks
     useful_gbs = value * (sum(cfg.dims) / N) * esz / 1e9
     GATHERS = ("k_gather_update_tc", "k_gather_update", "k_gather")
     PERSISTENT = ("k_sweep_fused", "k_sweep_wide")  # whole sweeps per launch
@@ -371,23 +375,24 @@ def run_ours(args, cfg):
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_val = fibers_per_step * e2e_steps * (1 if sharded else ws) / (e2e_ms / 1e3)
+    e2e_val = fibers_per_step * e2e_steps * (1 if one_chain else ws) / (e2e_ms / 1e3)
     clocks = clk.summary()
     res = None
     if rank == 0:
         res = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
-            "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+            "scaling": "strong" if one_chain else "weak", "vs_baseline": None,
             "dtype": "f64" if cfg.dtype == "f64" else "f32", "data": "synthetic (seeded; synth/ recipe)",
             "config": {"workload": workload_str(cfg, args.sampler),
                        "step": f"one cyclic sweep = {N} SGD iterations x B fibers",
                        "sampler": args.sampler,
-                       "iterations_per_s": round(N * args.steps * (1 if sharded else ws) / (ms / 1e3), 1),
+                       "iterations_per_s": round(N * args.steps * (1 if one_chain else ws) / (ms / 1e3), 1),
                        "useful_GBps": round(useful_gbs, 2),
                        "layout": "native" if args.native_layout else "mode-major copies (CP_FLAG_MODE_MAJOR)",
                        "parallelism": (f"slab-sharded x{ws} (NCCL)" if sharded else
-                                       (f"{ws} independent chains" if ws > 1 else "1 GPU")),
+                                       f"one chain on {ws} whole-tensor replicas, batch split + ncclAllReduce of M"
+                                       if replica else (f"{ws} independent chains" if ws > 1 else "1 GPU")),
                        "l2": "inputs larger than L2 (tensor + mode-major copies >> 126 MB); fresh fibers per step",
                        "init_s": round(init_s, 3)},
             "roofline": roof,
@@ -525,6 +530,8 @@ def main():
                     help="auto: persistent single-cluster kernel when the problem fits one cluster; wide: the "
                          "gather (tcgen05) + table/sampling kernel pair")
     ap.add_argument("--no-tc", action="store_true", help="FFMA gather mainloop instead of tcgen05")
+    ap.add_argument("--independent", action="store_true",
+                    help="N > 1: one unrelated chain per GPU (weak scaling) instead of one chain on N replicas")
     ap.add_argument("--chains", type=int, default=1,
                     help="K > 1: K independent chains in one multi-chain launch (fused workloads; SURVEY 8f.2)")
     ap.add_argument("--chain-cluster", type=int, default=16, choices=[8, 16],

@@ -72,7 +72,9 @@ typedef enum { CP_ORDER_CYCLIC = 0, CP_ORDER_RANDOM = 1 } cp_mode_order;
 /* flags */
 #define CP_FLAG_MODE_MAJOR 0x1u   /* keep mode-major copies X_(n)^T ([J_n][I_n], fiber-contiguous) for
                                      n >= 1 so every sampled fiber is one contiguous row (DESIGN.md
-                                     "Data layout"); costs (N-1) extra tensor-sized buffers          */
+                                     "Data layout"); costs (N-1) extra tensor-sized buffers; a mode whose
+                                     copy does not fit the free device memory (less 2 GiB) keeps the native
+                                     layout                                                         */
 #define CP_FLAG_NO_GRAPH 0x2u     /* never capture CUDA graphs for sweeps                              */
 #define CP_FLAG_NO_FUSED 0x8u      /* never use the persistent single-cluster sweep kernel (small problems
                                      otherwise run whole step sequences in one launch)               */
@@ -94,6 +96,19 @@ typedef enum { CP_ORDER_CYCLIC = 0, CP_ORDER_RANDOM = 1 } cp_mode_order;
                                       stratum): balanced owner-computes.  Mode N-1 is unchanged.  Needs
                                       slab_bounds with CP_FLAG_EXTERNAL_COMM; CP_EINVAL for block samplers,
                                       B < world_size or world_size > 16. */
+#define CP_FLAG_REPLICA 0x200u     /* world > 1 with the WHOLE tensor on every rank (BASELINE C4 at 2-8 GPUs;
+                                      SURVEY 8(e) "C4 alternative"): every rank draws the same global batch and
+                                      runs the replicated update / table / next batch, but gathers and contracts
+                                      only the wide path's batch chunks c = rank, rank + P, ... (perfect balance,
+                                      any strategy); M = the sum over ranks of each rank's chunk sum (ncclAllReduce
+                                      on the library stream, or by the caller between phases 0 and 1 with
+                                      CP_FLAG_EXTERNAL_COMM: cp_sgd_exchange_info / _copy expose that buffer,
+                                      [ceil(I_n/128)][R][128] of cfg.dtype).  slab_begin/end are ignored.  Needs
+                                      the wide path for every mode (CP_EINVAL otherwise); excludes STRATIFIED. */
+#define CP_FLAG_FORCE_COMM 0x400u  /* test hook: a world_size == 1 handle that still takes the multi-rank code
+                                      path (slab sharding, or REPLICA) with a 1-rank NCCL communicator from
+                                      nccl_unique_id (or the caller's exchanges with EXTERNAL_COMM), so the
+                                      library's NCCL calls run on a one-GPU machine */
 #define CP_FLAG_NO_PERSIST 0x80u   /* fp32 wide path: never use the persistent cooperative sweep kernel
                                      (k_sweep_wide); run each step as the gather / update+table /
                                      sample kernel chain (graph-captured for cyclic sweeps)        */
@@ -179,6 +194,9 @@ cp_status cp_sgd_sweep_multi(cp_sgd_t* hs, int32_t nh, int32_t nsweeps);
  * summed over ranks when sharded.  Synchronises.  CP_EDEGENERATE when ||X|| = 0. */
 cp_status cp_fit(cp_sgd_t h, double* fit_host);
 
+/* A fresh 128-byte ncclUniqueId from the NCCL library this library uses (rank 0 creates it and
+ * broadcasts it to the other ranks, e.g. through torch.distributed, before cp_sgd_init). */
+cp_status cp_nccl_unique_id(void* out128_host);
 /* Squared Frobenius norms of the last-mode slices of a first-index-fastest tensor (or of a rank's local
  * slab): out_dev[i] = sum of x^2 over slice i (fp64, a fixed summation order), i < nslices <= 65535,
  * slice_len = product of the other dims.  No handle; enqueued on `stream` (cudaStream_t).  The data-side

@@ -23,6 +23,8 @@ FLAG_MODE_MAJOR, FLAG_NO_GRAPH, FLAG_EXTERNAL_COMM, FLAG_NO_FUSED, FLAG_NO_WIDE,
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
 FLAG_NO_PERSIST = 0x80
 FLAG_STRATIFIED = 0x100
+FLAG_REPLICA = 0x200
+FLAG_FORCE_COMM = 0x400
 KERNEL_NAMES = ["k_sample", "k_gather", "k_update_table", "k_table", "k_reduce_partials", "nccl", "k_fit",
                 "k_sweep_fused", "k_gather_update", "k_zw_gamma", "k_gather_update_tc", "k_table_sample",
                 "k_update_wide", "k_scores_wide", "k_sample_wide", "k_sweep_wide"]
@@ -34,7 +36,7 @@ EXPORTS = ["cp_sgd_init", "cp_sgd_destroy", "cp_sgd_last_error", "cp_sgd_sample"
            "cp_sgd_get_table", "cp_sgd_get_grad", "cp_sgd_get_accum", "cp_sgd_get_iter", "cp_sgd_set_iter",
            "cp_sgd_refresh_tables", "cp_sgd_get_launches", "cp_sgd_profile", "cp_sgd_profile_read",
            "cp_sgd_version", "cp_sgd_batch_max", "cp_sgd_debug_timers", "cp_sgd_exchange_copy", "cp_sgd_trace_layout",
-           "cp_sgd_trace", "cp_sgd_trace_count", "cp_sgd_path", "cp_slice_sqnorms"]
+           "cp_sgd_trace", "cp_sgd_trace_count", "cp_sgd_path", "cp_slice_sqnorms", "cp_nccl_unique_id"]
 
 
 class CPError(RuntimeError):
@@ -99,6 +101,7 @@ def load_library(path: str = LIB_PATH):
     L.cp_sgd_trace_count.argtypes = [P, C.POINTER(C.c_int64)]
     L.cp_sgd_path.argtypes = [P, C.POINTER(C.c_int32)]
     L.cp_slice_sqnorms.argtypes = [P, i32, i64, i64, P, P]
+    L.cp_nccl_unique_id.argtypes = [P]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype if name in ("cp_sgd_last_error", "cp_sgd_version") else C.c_int
     _lib = L
@@ -129,7 +132,7 @@ class CPSGD:
                  slab=None, mode_major: bool = True, block_window=None, graphs: bool = True,
                  external_comm: bool = False, fused: bool = True, wide: bool = True,
                  tc: bool = True, fused_cluster: int = 16, persist: bool = True, stratified: bool = False,
-                 slab_bounds=None):
+                 slab_bounds=None, replica: bool = False, force_comm: bool = False):
         import torch
 
         L = load_library()
@@ -156,7 +159,8 @@ class CPSGD:
                 (FLAG_EXTERNAL_COMM if external_comm else 0) | (0 if fused else FLAG_NO_FUSED) | \
                 (0 if wide else FLAG_NO_WIDE) | (0 if tc else FLAG_NO_TC) | \
                 (FLAG_FUSED_CU8 if fused_cluster == 8 else 0) | (0 if persist else FLAG_NO_PERSIST) | \
-                (FLAG_STRATIFIED if stratified else 0)
+                (FLAG_STRATIFIED if stratified else 0) | (FLAG_REPLICA if replica else 0) | \
+                (FLAG_FORCE_COMM if force_comm else 0)
         lo, hi = (0, self.dims[-1]) if slab is None else (int(slab[0]), int(slab[1]))
         cfg = Config(self.N, self._dims_arr, self.R, self.dtype, X.data_ptr(), self._fac_arr, int(batch),
                      self._win_arr, SAMPLERS[sampler], RULES[rule], float(alpha), float(eta), float(b), float(eps),
@@ -230,8 +234,13 @@ class CPSGD:
         self._chk(self._L.cp_sgd_exchange_info(self._h, mode, C.byref(buf), C.byref(cnt), C.byref(rb), C.byref(re)))
         return buf.value, cnt.value, rb.value, re.value
 
+    def exchange_count(self, mode: int) -> int:
+        """elements of the phase-0 exchange buffer of `mode` (slabs: partial M, R x I_n; replicas: the rank's
+        chunk sum of M, ceil(I_n/128) x R x 128)"""
+        return int(self.exchange_info(mode)[1])
+
     def exchange_copy(self, mode: int, buf, to_lib: bool):
-        """copy the phase-0 exchange buffer (partial M, [R][I_n]) to / from a torch CUDA tensor"""
+        """copy the phase-0 exchange buffer (exchange_count(mode) elements) to / from a torch CUDA tensor"""
         self._chk(self._L.cp_sgd_exchange_copy(self._h, mode, C.c_void_p(buf.data_ptr()), 1 if to_lib else 0))
 
     @staticmethod
@@ -389,4 +398,14 @@ def slice_sqnorms(X, nslices: int, stream=None):
     if st != 0:
         raise CPError(st, "cp_slice_sqnorms")
     return out
+
+
+def nccl_unique_id() -> bytes:
+    """cp_nccl_unique_id: a fresh 128-byte ncclUniqueId from the library's own NCCL"""
+    L = load_library()
+    buf = C.create_string_buffer(128)
+    st = L.cp_nccl_unique_id(buf)
+    if st != 0:
+        raise CPError(st, "cp_nccl_unique_id")
+    return bytes(buf.raw)
 

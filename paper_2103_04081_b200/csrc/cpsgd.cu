@@ -44,6 +44,7 @@ enum { kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0 };
 struct NcclApi {
   void* dl = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
@@ -75,6 +76,7 @@ struct NcclApi {
     CPS_SYM(GroupEnd, "ncclGroupEnd");
     CPS_SYM(CommDestroy, "ncclCommDestroy");
     CPS_SYM(GetErrorString, "ncclGetErrorString");
+    CPS_SYM(GetUniqueId, "ncclGetUniqueId");
 #undef CPS_SYM
     return true;
   }
@@ -232,6 +234,7 @@ struct cp_sgd_s {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
   std::vector<int64_t> row_ranges;  // [2*world]: slab [lo, hi) of every rank
+  void* Mred = nullptr;             // replicas (CP_FLAG_REPLICA): this rank's chunk sum of M, [tiles][R][128]
   int64_t strat_lo[kMaxStrata + 1] = {};  // CP_FLAG_STRATIFIED: slab bounds of the ranks (R26)
 
   cp_status fail(cp_status st, const char* fmt, ...) {
@@ -305,6 +308,9 @@ cp_status launch_ut(cp_sgd_s* h, int n, int do_update, int do_table, int64_t row
                     const double* alpha_dev, bool use_sum, int next_mode);
 bool ut_fits(const cp_sgd_s* h, int64_t In);
 bool wide_mode(const cp_sgd_s* h, int n);
+bool multi(const cp_sgd_s* h);
+bool sharded(const cp_sgd_s* h);
+bool replica(const cp_sgd_s* h);
 
 cp_status launch_table_any(cp_sgd_s* h, int k) {
   if (h->sampler == CP_UNIFORM) return CP_OK;
@@ -567,10 +573,37 @@ cp_status launch_reduce(cp_sgd_s* h, int n) {
   return check_launch(h, "k_reduce_partials");
 }
 
-bool sharded(const cp_sgd_s* h) { return h->world_size > 1; }
+// several ranks (or one rank forced onto the multi-rank path with a 1-rank communicator: a test hook)
+bool multi(const cp_sgd_s* h) { return h->world_size > 1 || (h->flags & CP_FLAG_FORCE_COMM); }
+// slab sharding of the tensor along the last mode
+bool sharded(const cp_sgd_s* h) { return multi(h) && !(h->flags & CP_FLAG_REPLICA); }
+// whole-tensor replicas with a batch split of the wide path (CP_FLAG_REPLICA)
+bool replica(const cp_sgd_s* h) { return multi(h) && (h->flags & CP_FLAG_REPLICA); }
 
 // ---- wide single-GPU path: k_gather_update (gather + split-K + update) and the zw / Gamma epilogue ----
 bool wide_mode(const cp_sgd_s* h, int n) { return n >= 0 && h->gu_ck[n] > 0; }
+
+// the batch chunks this launch covers: all CK of them, or (replicas with a batch split) chunks rank, rank + P, ...
+template <typename PP>
+int gu_set_chunks(const cp_sgd_s* h, int n, PP& p) {
+  p.CK = h->gu_ck[n];
+  p.c_first = replica(h) ? h->world_rank : 0;
+  p.c_step = replica(h) ? h->world_size : 1;
+  return (int)ceil_div(p.CK - p.c_first, p.c_step);
+}
+
+// replicas: this rank's chunk partials summed in chunk order -> Mred [tiles][R][TI] (the exchange buffer)
+template <typename T>
+__global__ void k_chunk_sum(const T* __restrict__ Mpart, int CK, int c_first, int c_step, int R, int64_t tiles,
+                            T* __restrict__ Mred) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)R * kGUTI;
+  if (e >= tiles * per) return;
+  const int64_t tile = e / per, o = e % per;
+  T acc = T(0);
+  for (int c = c_first; c < CK; c += c_step) acc += Mpart[(tile * CK + c) * per + o];
+  Mred[e] = acc;
+}
 
 template <typename T, int CPT>
 cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
@@ -610,6 +643,7 @@ cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   p.b = h->bpar;
   p.eps = h->eps;
   p.iter = h->iter_dev;
+  const int ny = gu_set_chunks(h, n, p);
   const size_t smem = gu_smem_bytes<T, CPT>(p.KB);
   static DevOnce attr_once;  // per device: the attribute is per context
   if (attr_once.first(h->device)) {
@@ -617,7 +651,7 @@ cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
     cudaFuncSetAttribute(k_gather_update<T, CPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)ceil_div(h->dims[n], kGUTI), (unsigned)CK, 1);
+  lc.gridDim = dim3((unsigned)ceil_div(h->dims[n], kGUTI), (unsigned)ny, 1);
   lc.blockDim = dim3(kGUThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
@@ -666,13 +700,14 @@ cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev
   p.eps = h->eps;
   p.iter = h->iter_dev;
   p.dbg = h->dbg;
+  const int ny = gu_set_chunks(h, n, p);
   const size_t smem = tc_smem_bytes(p.KB);
   static DevOnce attr_once;  // per device: the attribute is per context
   if (attr_once.first(h->device)) {
     allow_max_dyn_smem(k_gather_update_tc<0>);
   }
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)ceil_div(h->dims[n], kGUTI), (unsigned)CK, 1);
+  lc.gridDim = dim3((unsigned)ceil_div(h->dims[n], kGUTI), (unsigned)ny, 1);
   lc.blockDim = dim3(kTCThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
@@ -755,8 +790,8 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev,
   p.strategy = h->sampler;
   p.rule = h->rule;
   p.In = h->dims[n];
-  p.Mpart = (const T*)h->Mpart;
-  p.CK = h->gu_ck[n];
+  p.Mpart = (const T*)(replica(h) ? h->Mred : h->Mpart);  // replicas: the rank-summed M, one "chunk"
+  p.CK = replica(h) ? 1 : h->gu_ck[n];
   p.Gam = (const T*)h->gam_next;
   p.A = (T*)h->factors[n];
   p.S = (T*)h->S[n];
@@ -1020,7 +1055,7 @@ cp_status launch_fused_multi_t(cp_sgd_s* const* hs, int nh, int nsteps) {
 // geometry + eligibility of the fused kernel: one GPU, R <= 32, I_n <= 512, fits shared memory
 void plan_fused(cp_sgd_s* h) {
   h->fused_cu = 0;
-  if (h->world_size > 1 || (h->flags & CP_FLAG_NO_FUSED)) return;
+  if (multi(h) || (h->flags & CP_FLAG_NO_FUSED)) return;
   if (fused_rp(h->R, h->esz) / (h->esz == 8 ? 2 : 4) > 8) return;  // gather_contract supports <= 8 vector groups
   int64_t imax = 0, bmx = 0, cdfmax = 0;  // cdfmax: the resident CDFs of every mode
   for (int n = 0; n < h->N; ++n) {
@@ -1094,7 +1129,7 @@ TraceParams trace_params(cp_sgd_s* h, int nsteps) {
 // stays on the kernel chain), cooperative launch supported, one 448-thread CTA per SM co-resident
 bool plan_pw(cp_sgd_s* h) {
   h->pw_ok = false;
-  if (h->world_size != 1 || h->dtype != CP_F32 || !h->use_tc || h->rule == CP_STEP_ALS ||
+  if (multi(h) || h->dtype != CP_F32 || !h->use_tc || h->rule == CP_STEP_ALS ||
       (h->flags & CP_FLAG_NO_PERSIST))
     return true;
   int64_t kbmax = 0, cdfmax = 0, units = 0;
@@ -1229,9 +1264,21 @@ cp_status phase0(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
     if (st) return st;
     h->pref_mode = n;
   }
-  if (wide_mode(h, n)) {  // gather + contraction + split-K + update in one launch
+  if (wide_mode(h, n)) {  // gather + contraction + split-K partials (replicas: this rank's chunks)
     st = h->dtype == CP_F64 ? launch_gu<double>(h, n, alpha, alpha_dev) : launch_gu<float>(h, n, alpha, alpha_dev);
     h->pref_mode = -1;
+    if (!st && replica(h)) {  // -> Mred, summed over ranks before phase 1
+      const int64_t tiles = ceil_div(h->dims[n], kGUTI), tot = tiles * h->R * kGUTI;
+      const int CK = h->gu_ck[n];
+      if (h->dtype == CP_F64)
+        k_chunk_sum<double><<<(unsigned)ceil_div(tot, 256), 256, 0, h->ls>>>(
+            (const double*)h->Mpart, CK, h->world_rank, h->world_size, h->R, tiles, (double*)h->Mred);
+      else
+        k_chunk_sum<float><<<(unsigned)ceil_div(tot, 256), 256, 0, h->ls>>>(
+            (const float*)h->Mpart, CK, h->world_rank, h->world_size, h->R, tiles, (float*)h->Mred);
+      h->launches++;
+      st = check_launch(h, "k_chunk_sum");
+    }
     return st;
   }
   st = h->dtype == CP_F64 ? launch_gather<double>(h, n) : launch_gather<float>(h, n);
@@ -1285,6 +1332,12 @@ cp_status nccl_check(cp_sgd_s* h, ncclResult_t r, const char* what) {
 }
 
 cp_status exchange_after0(cp_sgd_s* h, int n) {
+  if (replica(h) && !(h->flags & CP_FLAG_EXTERNAL_COMM)) {  // M = sum over ranks of the chunk sums
+    ProfScope ps(h, kKComm);
+    const int dt = h->dtype == CP_F64 ? kNcclFloat64 : kNcclFloat32;
+    const size_t cnt = (size_t)ceil_div(h->dims[n], kGUTI) * h->R * kGUTI;
+    return nccl_check(h, g_nccl.AllReduce(h->Mred, h->Mred, cnt, dt, kNcclSum, h->comm, h->ls), "ncclAllReduce(M)");
+  }
   if (!sharded(h) || (h->flags & CP_FLAG_EXTERNAL_COMM) || n == h->N - 1) return CP_OK;
   ProfScope ps(h, kKComm);
   const int dt = h->dtype == CP_F64 ? kNcclFloat64 : kNcclFloat32;
@@ -1404,7 +1457,9 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
     h->factors[k] = cfg->factors[k];
     h->ldims[k] = cfg->dims[k];
   }
-  if (h->world_size > 1) {
+  if ((h->flags & CP_FLAG_REPLICA) && (h->flags & CP_FLAG_STRATIFIED))
+    return init_fail(h, h->fail(CP_EINVAL, "CP_FLAG_REPLICA and CP_FLAG_STRATIFIED exclude each other"));
+  if (sharded(h)) {
     if (cfg->slab_begin < 0 || cfg->slab_end > h->dims[h->N - 1] || cfg->slab_begin >= cfg->slab_end)
       return init_fail(h, h->fail(CP_EINVAL, "bad slab range [%lld,%lld)", (long long)cfg->slab_begin,
                                   (long long)cfg->slab_end));
@@ -1554,7 +1609,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
   }
   plan_fused(h);
   // ---- wide single-GPU path (k_gather_update) eligibility and buffers ----
-  if (h->world_size == 1 && !(h->flags & CP_FLAG_NO_WIDE)) {
+  if ((!multi(h) || replica(h)) && !(h->flags & CP_FLAG_NO_WIDE)) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -1567,6 +1622,8 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       // chunks per I-tile: one wave of CTAs (tcgen05 kernel: one CTA per SM; FFMA kernel: two)
       const int64_t slots = tc ? 148 : 296;
       int64_t CK = std::max<int64_t>(1, std::min<int64_t>(slots / nt, 64));
+      // replicas: P times as many chunks, every rank one wave of its own (chunks rank, rank + P, ...)
+      if (replica(h)) CK *= h->world_size;
       const int64_t gran = tc ? kTCKS : 8;
       int64_t KB = ceil_div(ceil_div(h->bmax[n], CK), gran) * gran;
       CK = ceil_div(h->bmax[n], KB);  // no empty chunk
@@ -1580,7 +1637,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       const size_t us = std::max(uw_smem_bytes(h->R, h->esz, std::min<int64_t>(h->dims[n], 4096)),
                                  sw_smem_bytes(h->N, h->R, cdfmax, h->esz));
       const bool cores = h->esz == 8 ? uw_coresident<double>(h->R, h->dims[n]) : uw_coresident<float>(h->R, h->dims[n]);
-      if (gs + 1024 <= (size_t)optin && us <= (size_t)h->sample_smem && cores) {
+      if (gs + 1024 <= (size_t)optin && us <= (size_t)h->sample_smem && cores && (!replica(h) || CK >= h->world_size)) {
         h->gu_ck[n] = (int)CK;
         h->gu_kb[n] = KB;
         mpart = std::max(mpart, nt * CK * kGUTI * h->R);
@@ -1604,6 +1661,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       for (int n = 0; n < h->N; ++n) ncl = std::max(ncl, ceil_div(ceil_div(h->bmax[n], kSWFibers), kSWCluster));
       ALLOC(h->sw_gcl, h->esz * ncl * h->R * h->R);
       ALLOC(h->Mpart, h->esz * mpart);
+      if (replica(h)) ALLOC(h->Mred, h->esz * ceil_div(Imax, kGUTI) * kGUTI * h->R);
       ALLOC(h->gu_cnt, sizeof(unsigned) * ceil_div(Imax, kGUTI));
       cudaMemsetAsync(h->gu_cnt, 0, sizeof(unsigned) * ceil_div(Imax, kGUTI), h->stream);
       ALLOC(h->zwp, h->esz * Bmax_all * zg_rp(h->R));
@@ -1621,10 +1679,16 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       h->use_tc = false;
     }
   }
+  if (replica(h)) {  // the batch split lives in the wide path's gather launch
+    bool ok = true;
+    for (int n = 0; n < h->N; ++n) ok = ok && wide_mode(h, n);
+    if (!ok) return init_fail(h, h->fail(CP_EINVAL, "CP_FLAG_REPLICA needs the wide path for every mode (and a batch of "
+                                                    "at least world_size chunks)"));
+  }
   if (h->rule == CP_STEP_ALS) {  // the ALS step is implemented by the fused and wide kernels only
     bool ok = h->fused_cu > 0;
     if (!ok) {
-      ok = h->world_size == 1;
+      ok = !sharded(h);
       for (int n = 0; n < h->N; ++n) ok = ok && wide_mode(h, n);
     }
     if (!ok) return init_fail(h, h->fail(CP_EINVAL, "rule=als needs one GPU and the fused or wide path"));
@@ -1638,7 +1702,15 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       for (int k = n + 1; k < h->N; ++k) outer *= h->ldims[k];
       const int64_t align = 16 / (int64_t)h->esz;
       h->pitch[n] = ceil_div(In, align) * align;
-      ALLOC(h->Xmm[n], h->esz * h->pitch[n] * inner * outer);
+      // only where it fits (e.g. C5 slabs at P < 8): a mode without a copy gathers from the native layout
+      size_t mem_free = 0, mem_tot = 0;
+      const size_t bytes = h->esz * h->pitch[n] * inner * outer;
+      if (cudaMemGetInfo(&mem_free, &mem_tot) != cudaSuccess || bytes + ((size_t)2 << 30) > mem_free) {
+        cudaGetLastError();
+        h->pitch[n] = 0;
+        continue;
+      }
+      ALLOC(h->Xmm[n], bytes);
       dim3 tb(32, 8);
       dim3 grid((unsigned)ceil_div(inner, 32), (unsigned)ceil_div(In, 32), (unsigned)std::min<int64_t>(outer, 65535));
       if (h->dtype == CP_F64)
@@ -1655,7 +1727,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
   // ---- persistent cooperative sweep kernel of the fp32 wide path ----
   if (!plan_pw(h)) return init_fail(h, h->fail(CP_ENOMEM, "persistent sweep kernel workspace"));
   // ---- NCCL communicator ----
-  if (h->world_size > 1) {
+  if (multi(h)) {
     auto* rr = rr_store(h, true);
     rr->assign(2 * h->world_size, 0);
     if (!(h->flags & CP_FLAG_EXTERNAL_COMM)) {
@@ -1664,6 +1736,10 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       if (!g_nccl.load(e)) return init_fail(h, h->fail(CP_ENCCL, "%s", e.c_str()));
       ncclUniqueId id;
       memcpy(&id, cfg->nccl_unique_id, sizeof id);
+      // replicas stay bitwise identical only if every run reduces in the same order: pin the ring
+      // algorithm and one protocol unless the caller chose
+      setenv("NCCL_ALGO", "Ring", 0);
+      setenv("NCCL_PROTO", "LL128", 0);
       ncclResult_t r = g_nccl.CommInitRank(&h->comm, h->world_size, id, h->world_rank);
       if (r != 0) return init_fail(h, h->fail(CP_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)));
       // exchange the slab ranges (allreduce of a one-hot vector)
@@ -1752,6 +1828,7 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->zimg);
   cudaFree(h->gam_next);
   cudaFree(h->Mpart);
+  cudaFree(h->Mred);
   cudaFree(h->gu_cnt);
   cudaFree(h->uw_gpart);
   cudaFree(h->uw_rownorm);
@@ -1861,7 +1938,7 @@ static cp_status step_direct(cp_sgd_t h, int n, double alpha, int next_mode) {
 cp_status cp_sgd_step(cp_sgd_t h, int32_t mode, double alpha) {
   cp_status st = check_mode(h, mode);
   if (st) return st;
-  if (sharded(h) && (h->flags & CP_FLAG_EXTERNAL_COMM))
+  if (multi(h) && (h->flags & CP_FLAG_EXTERNAL_COMM))
     return h->fail(CP_ESTATE, "external-comm handles must use cp_sgd_step_phase");
   if (h->fused_cu || h->pw_ok) {
     const double a = (alpha < 0.0) ? h->alpha : alpha;
@@ -1882,7 +1959,7 @@ cp_status cp_sgd_step_phase(cp_sgd_t h, int32_t mode, int32_t phase, double alph
   if (st) return st;
   if (phase == 0) {
     st = phase0(h, mode, a, nullptr);
-    if (!st && sharded(h) && !(h->flags & CP_FLAG_EXTERNAL_COMM)) st = exchange_after0(h, mode);
+    if (!st && multi(h) && !(h->flags & CP_FLAG_EXTERNAL_COMM)) st = exchange_after0(h, mode);
     return st;
   }
   if (phase == 1) {
@@ -1909,6 +1986,13 @@ cp_status cp_sgd_exchange_info(cp_sgd_t h, int32_t mode, void** buf_dev, int64_t
                                int64_t* row_end) {
   cp_status st = check_mode(h, mode);
   if (st) return st;
+  if (replica(h)) {  // this rank's chunk sum of M, [tiles][R][128], to be summed over ranks
+    if (buf_dev) *buf_dev = h->Mred;
+    if (count) *count = ceil_div(h->dims[mode], kGUTI) * h->R * kGUTI;
+    if (row_begin) *row_begin = 0;
+    if (row_end) *row_end = h->dims[mode];
+    return CP_OK;
+  }
   if (buf_dev) *buf_dev = (mode == h->N - 1 && sharded(h)) ? nullptr : h->Msum;
   if (count) *count = (mode == h->N - 1 && sharded(h)) ? 0 : (int64_t)h->R * h->In_local[mode];
   if (row_begin) *row_begin = h->row0[mode];
@@ -1920,11 +2004,13 @@ cp_status cp_sgd_exchange_copy(cp_sgd_t h, int32_t mode, void* buf_dev, int32_t 
   cp_status st = check_mode(h, mode);
   if (st) return st;
   if (!buf_dev) return h->fail(CP_EINVAL, "NULL buffer");
-  const size_t bytes = h->esz * (size_t)h->R * (size_t)h->In_local[mode];
+  void* lib = replica(h) ? h->Mred : h->Msum;
+  const size_t bytes = replica(h) ? h->esz * (size_t)(ceil_div(h->dims[mode], kGUTI) * h->R * kGUTI)
+                                  : h->esz * (size_t)h->R * (size_t)h->In_local[mode];
   if (to_lib)
-    CUDA_TRY(h, cudaMemcpyAsync(h->Msum, buf_dev, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(lib, buf_dev, bytes, cudaMemcpyDeviceToDevice, h->stream));
   else
-    CUDA_TRY(h, cudaMemcpyAsync(buf_dev, h->Msum, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    CUDA_TRY(h, cudaMemcpyAsync(buf_dev, lib, bytes, cudaMemcpyDeviceToDevice, h->stream));
   return CP_OK;
 }
 
@@ -1932,7 +2018,7 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
   if (!h) return CP_EINVAL;
   if (nsweeps < 0) return h->fail(CP_EINVAL, "nsweeps < 0");
   if (order != CP_ORDER_CYCLIC && order != CP_ORDER_RANDOM) return h->fail(CP_EINVAL, "bad order");
-  if (sharded(h) && (h->flags & CP_FLAG_EXTERNAL_COMM))
+  if (multi(h) && (h->flags & CP_FLAG_EXTERNAL_COMM))
     return h->fail(CP_ESTATE, "external-comm handles must use cp_sgd_step_phase");
   if (h->fused_cu && !alpha_per_iter) {
     if (nsweeps == 0) return CP_OK;
@@ -2122,6 +2208,16 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
     CUDA_TRY(h, cudaMemcpyAsync(factors_host[k], h->factors[k], h->esz * h->dims[k] * h->R, cudaMemcpyDeviceToHost,
                                 h->stream));
   return cp_sgd_sync(h);
+}
+
+cp_status cp_nccl_unique_id(void* out128_host) {
+  if (!out128_host) return CP_EINVAL;
+  std::string e;
+  if (!g_nccl.load(e)) return CP_ENCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != 0) return CP_ENCCL;
+  memcpy(out128_host, &id, sizeof id < 128 ? sizeof id : 128);
+  return CP_OK;
 }
 
 cp_status cp_slice_sqnorms(const void* X_dev, int32_t dtype, int64_t nslices, int64_t slice_len, double* out_dev,

@@ -53,6 +53,9 @@ struct GUParams {
   uint64_t* iter;         // r <- r + 1 (Alg. 6/7)
   T* Mpart;               // [tiles][chunks][TI][R] partial tiles (split-K workspace)
   unsigned* cnt;          // [tiles] arrival counters (zero between launches)
+  // replicas with a batch split (CP_FLAG_REPLICA): this launch's y-index q covers batch chunk c_first +
+  // q c_step of the CK chunks (1 GPU: 0 + q 1, all of them)
+  int CK, c_first, c_step;
   long long* dbg;         // optional phase timestamps (CTA (0,0), thread 0)
 };
 
@@ -94,6 +97,9 @@ __device__ __forceinline__ void gu_gamma_sum(const GUParams<T>& p, int e0, int e
   }
 }
 
+template <typename T>
+__device__ __forceinline__ int gu_chunk(const GUParams<T>& p) { return p.c_first + (int)blockIdx.y * p.c_step; }
+
 // Epilogue shared by both mainloops: this CTA's partial tile M_c (shared, [TI][MS]) -> the split-K
 // workspace p.Mpart[tile][chunk][R][TI] (row-contiguous, coalesced).  The chunk partials are summed
 // in chunk order, and G = A Gamma - M and the update applied, by k_table_sample (the next launch).
@@ -101,7 +107,7 @@ template <typename T>
 __device__ __forceinline__ void gu_finish(const GUParams<T>& p, const T* Mt, int MS, int64_t i0, int tid, int nth) {
   const int R = p.R, TI = kGUTI;
   const int nrow = (int)cmax64(0, cmin64(TI, p.In - i0));
-  T* part = p.Mpart + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * R * TI;
+  T* part = p.Mpart + ((int64_t)blockIdx.x * p.CK + gu_chunk(p)) * R * TI;
   for (int e = tid; e < R * TI; e += nth) {
     const int r = e / TI, rl = e % TI;
     if (rl < nrow) part[e] = Mt[rl * MS + r];
@@ -127,7 +133,7 @@ __global__ void __launch_bounds__(kGUThreads, 1) k_gather_update(GUParams<T> p) 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int R = p.R;
   const int64_t i0 = (int64_t)blockIdx.x * TI;
-  const int64_t c0 = (int64_t)blockIdx.y * p.KB;
+  const int64_t c0 = (int64_t)gu_chunk(p) * p.KB;
   const int64_t c1 = min(c0 + p.KB, p.bmax);
   const int nfib = (int)cmax64(0, c1 - c0);
   const int nst = (nfib + KS - 1) / KS;

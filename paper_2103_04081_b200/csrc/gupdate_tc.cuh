@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kTCThreads, 1) k_gather_update_tc(GUParams<flo
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int R = p.R;
   const int64_t i0 = (int64_t)blockIdx.x * TI;
-  const int64_t c0 = (int64_t)blockIdx.y * p.KB;
+  const int64_t c0 = (int64_t)gu_chunk(p) * p.KB;
   const int nfib = (int)cmax64(0, cmin64(p.KB, p.bmax - c0));
   const int nst = (nfib + KS - 1) / KS;
   const bool mark = p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && tid == 128;
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kTCThreads, 1) k_gather_update_tc(GUParams<flo
   if (mark) p.dbg[35] = clock64();
   {
     const int nrow = (int)cmax64(0, cmin64(TI, p.In - i0));
-    float* part = p.Mpart + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * R * TI;
+    float* part = p.Mpart + ((int64_t)blockIdx.x * p.CK + gu_chunk(p)) * R * TI;
     for (int e = tid; e < R * (TI / 4); e += kTCThreads) {
       const int r = e / (TI / 4), i = 4 * (e % (TI / 4));
       const float4 a = *reinterpret_cast<const float4*>(E + r * kTCEpiStride + i);
