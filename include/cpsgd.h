@@ -271,7 +271,8 @@ cp_status cp_sgd_trace_count(cp_sgd_t h, int64_t* n_host);
  * 0 for kernel chains */
 cp_status cp_sgd_path(cp_sgd_t h, int32_t* path_host);
 
-/* debug: clock64() phase timestamps of the last fused update/table kernel (CTA 0); only when the
+/* debug: clock64() phase timestamps of the last kernels (4096 kernel-specific entries, then the persistent
+ * kernel's per-CTA marks [8 iterations][160 CTAs][32]: out16 holds 4096 + 40960 entries); only when the
  * environment variable CPSGD_DEBUG_TIMERS was set at cp_sgd_init, else CP_ESTATE */
 cp_status cp_sgd_debug_timers(cp_sgd_t h, long long* out64_host);
 

@@ -366,7 +366,7 @@ class CPSGD:
         self._chk(self._L.cp_sgd_trace(self._h, None, 0))
 
     def debug_timers(self):
-        out = (C.c_longlong * 4096)()
+        out = (C.c_longlong * (4096 + 8 * 160 * 32))()
         self._chk(self._L.cp_sgd_debug_timers(self._h, out))
         return list(out)
 

@@ -192,7 +192,7 @@ struct cp_sgd_s {
   double* pw_gram = nullptr;     // [R(R+1)/2]
   unsigned long long* pw_agg = nullptr;  // [row units]
   unsigned* pw_aggf = nullptr;   // [row units][2]
-  unsigned* pw_bar = nullptr;    // [0] barrier arrivals, [32] pair-sum arrivals (zeroed per launch)
+  unsigned* pw_bar = nullptr;    // [0] barrier arrivals, [32] pair-sum, [64] table-unit arrivals (zeroed per launch)
   double* pw_alphas = nullptr;   // per-iteration steps of one call (fixed rule schedules)
   int64_t pw_alphas_cap = 0;
   // cp_sgd_trace: the consumed batches of the persistent kernels
@@ -829,18 +829,21 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev,
   lc.blockDim = dim3(kWThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = kUWCluster;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
-  // every CTA waits for the Gram inverse of the last cluster: the grid must be co-resident, which
-  // init checked (uw_coresident; a cooperative launch attribute would say the same but is not
-  // replayable by ncu)
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+  // every CTA waits for the Gram inverse of the last cluster: a cooperative launch, so the runtime
+  // guarantees co-residency (or refuses the launch) even with other work on the device (init also
+  // checked the occupancy: uw_coresident); CPSGD_PW_NONCOOP=1 drops the attribute for profilers that
+  // cannot replay cooperative launches
+  at[2].id = cudaLaunchAttributeCooperative;
+  at[2].val.cooperative = 1;
   lc.attrs = at;
-  lc.numAttrs = 2;
+  lc.numAttrs = getenv("CPSGD_PW_NONCOOP") ? 2 : 3;
   cudaError_t e = cudaLaunchKernelEx(&lc, k_update_wide<T>, p);
   h->launches++;
   if (e != cudaSuccess) return h->fail(CP_ECUDA, "k_update_wide launch: %s", cudaGetErrorString(e));
@@ -1123,6 +1126,12 @@ TraceParams trace_params(cp_sgd_s* h, int nsteps) {
 }
 
 // ---- persistent cooperative sweep kernel of the fp32 wide path (sweep_wide.cuh) -------------------
+// row units of the largest mode (the stride of the persistent kernel's unit-fastest pair partials)
+int64_t units_max_of(const cp_sgd_s* h) {
+  int64_t u = 1;
+  for (int k = 0; k < h->N; ++k) u = std::max<int64_t>(u, pw_units_rows(h->dims[k]));
+  return u;
+}
 // pw_kernel(R): k_pw.cu (its own translation unit)
 
 // eligible: one GPU, fp32 on the tcgen05 gather for every mode, gradient rules (the sampled-ALS rule
@@ -1166,7 +1175,7 @@ bool plan_pw(cp_sgd_s* h) {
       !alloc((void**)&h->pw_gram, sizeof(double) * ((P + 1) & ~1)) ||  // even: whole 16-byte bulk copies
       !alloc((void**)&h->pw_agg, sizeof(unsigned long long) * units) ||
       !alloc((void**)&h->pw_aggf, sizeof(unsigned) * 2 * units) ||
-      !alloc((void**)&h->pw_bar, sizeof(unsigned) * 64)) {
+      !alloc((void**)&h->pw_bar, sizeof(unsigned) * 128)) {
     cudaGetLastError();
     return false;
   }
@@ -1228,11 +1237,14 @@ cp_status launch_pw(cp_sgd_s* h, int nsteps, int first_mode, int order, double a
   p.aggf = h->pw_aggf;
   p.bar = h->pw_bar;
   p.pcnt = h->pw_bar + 32;  // another 128-byte line
+  p.qcnt = h->pw_bar + 64;  // another 128-byte line
+  p.gstride = units_max_of(h);
   p.tag0 = h->pw_tag + 1;
   p.Gout = (float*)h->Gout;
   p.Gam_out = (float*)h->Gam_out;
   p.tr = trace_params(h, nsteps);
   p.dbg = h->dbg;
+  p.ablate = getenv("CPSGD_PW_ABLATE_MASK") ? (unsigned)strtoul(getenv("CPSGD_PW_ABLATE_MASK"), nullptr, 0) : 0u;
   h->pw_tag += (uint32_t)nsteps;
   static DevOnce attr_once[4];
   if (attr_once[h->R <= 16 ? 0 : h->R <= 32 ? 1 : h->R <= 56 ? 2 : 3].first(h->device)) allow_max_dyn_smem(pw_kernel(h->R));
@@ -1247,7 +1259,7 @@ cp_status launch_pw(cp_sgd_s* h, int nsteps, int first_mode, int order, double a
   at[0].val.cooperative = 1;
   lc.attrs = at;
   lc.numAttrs = getenv("CPSGD_PW_NONCOOP") ? 0 : 1;  // profilers that cannot replay cooperative launches
-  CUDA_TRY(h, cudaMemsetAsync(h->pw_bar, 0, sizeof(unsigned) * 64, h->ls));
+  CUDA_TRY(h, cudaMemsetAsync(h->pw_bar, 0, sizeof(unsigned) * 128, h->ls));
   cudaError_t e = cudaLaunchKernelEx(&lc, pw_kernel(h->R), p);
   h->launches++;
   h->pref_mode = -1;
@@ -1552,8 +1564,8 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
   ALLOC(h->last_mode_dev, sizeof(int));
   if (getenv("CPSGD_PDL")) h->pdl = true;
   if (getenv("CPSGD_DEBUG_TIMERS")) {
-    ALLOC(h->dbg, sizeof(long long) * 4096);
-    cudaMemsetAsync(h->dbg, 0, sizeof(long long) * 4096, h->stream);
+    ALLOC(h->dbg, sizeof(long long) * kDbgEntries);
+    cudaMemsetAsync(h->dbg, 0, sizeof(long long) * kDbgEntries, h->stream);
   }
   ALLOC(h->zrow, h->esz * Bmax_all * h->R);
   ALLOC(h->fbase, sizeof(int64_t) * Bmax_all);
@@ -2352,7 +2364,7 @@ cp_status cp_sgd_debug_timers(cp_sgd_t h, long long* out16) {
   if (!h || !out16) return CP_EINVAL;
   if (!h->dbg) return h->fail(CP_ESTATE, "CPSGD_DEBUG_TIMERS was not set at init");
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-  CUDA_TRY(h, cudaMemcpy(out16, h->dbg, sizeof(long long) * 4096, cudaMemcpyDeviceToHost));
+  CUDA_TRY(h, cudaMemcpy(out16, h->dbg, sizeof(long long) * kDbgEntries, cudaMemcpyDeviceToHost));
   return CP_OK;
 }
 

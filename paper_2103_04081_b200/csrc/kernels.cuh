@@ -22,7 +22,10 @@ namespace cps {
 
 constexpr int kMaxOrder = 16;
 constexpr int kMaxRank = 64;
-constexpr int kMaxStrata = 16;  // slabs of the stratified sampler (ranks of one box)
+constexpr int kMaxStrata = 16;
+// debug timers (CPSGD_DEBUG_TIMERS): 4096 kernel-specific slots, then k_sweep_wide's per-CTA marks
+// [8 iterations][160 CTAs][32 slots]
+constexpr int kDbgEntries = 4096 + 8 * 160 * 32;  // slabs of the stratified sampler (ranks of one box)
 constexpr int kSweepBuf = 5 * kMaxRank;  // doubles of pivot-row buffer the sweep inverses need
 
 // ------------------------------------------------------------------------------------------

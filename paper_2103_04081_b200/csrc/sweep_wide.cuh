@@ -475,7 +475,7 @@ static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PW
           const int64_t fbv = sfb[lb < nfib ? lb : 0];  // unconditional load, then select
           const int64_t fb = lb < nfib ? fbv : -1;
           const int64_t r0 = i0 + 4 * j;
-          if (fb >= 0 && r0 < rowlen) cp_async16(A + kk * 512 + 16 * j, X + fb + r0, 16);
+          if (fb >= 0 && r0 < rowlen && !(p.ablate & 2u)) cp_async16(A + kk * 512 + 16 * j, X + fb + r0, 16);
         }
         cp_async_mbar_arrive_noinc(&B.xfull[slot]);
       }
@@ -622,13 +622,13 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
       const int r = t / ng, gq = t % ng;
       const float* base = p.Mpart + ((tile * CK) * R + r) * TI + lr0 + gq * 4;
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int c0 = 0; c0 < CK; c0 += 8) {
-        float4 ld[8];
+      for (int c0 = 0; c0 < CK; c0 += 16) {  // CK <= 16 at one wave: every chunk's load in flight at once
+        float4 ld[16];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (c0 + k < CK) ld[k] = __ldcg(reinterpret_cast<const float4*>(base + (int64_t)(c0 + k) * R * TI));
+        for (int k = 0; k < 16; ++k)  // clamped unconditional loads, then masked adds (chunk order)
+          ld[k] = __ldcg(reinterpret_cast<const float4*>(base + (int64_t)min(c0 + k, CK - 1) * R * TI));
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
+        for (int k = 0; k < 16; ++k)
           if (c0 + k < CK) {
             acc[0] += ld[k].x;
             acc[1] += ld[k].y;
@@ -713,7 +713,7 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
   __syncthreads();
   PW_MK(16);
   // table partials of the new rows (R9)
-  if (p.strategy == 1 || p.strategy == 3) {  // leverage: partial fp64 Gram, packed upper triangle
+  if ((p.strategy == 1 || p.strategy == 3) && !(p.ablate & 8u)) {  // leverage: partial fp64 Gram, packed upper triangle
     // task = (4 x 4 block bi <= bj, row group): the rows split into RG groups (short chains), an fp64
     // copy of the rows (converted once), the group partials summed in group order
     const int P = R * (R + 1) / 2;
@@ -758,11 +758,11 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
         }
     }
     __syncthreads();
-    double* gp = p.gpart + (int64_t)unit * P;
+    double* gp = p.gpart + unit;  // [P][gstride]: the pair sums read each pair's unit partials contiguously
     for (int e = tid; e < P; e += nth) {
       double sum = 0.0;
       for (int g = 0; g < RG; ++g) sum += redP[g * P + e];
-      gp[e] = sum;
+      gp[(int64_t)e * p.gstride] = sum;
     }
   } else if (p.strategy == 2 || p.strategy == 4) {  // Euclidean: row norms + the unit's partial ||A||^2
     double acc = 0.0;
@@ -814,7 +814,7 @@ static __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nun
     // l_i = a_i^T W a_i: warp w takes rows 2w, 2w + 1; lane c holds columns c and c + 32 of y = W a
     // (W symmetric: W_kc read along a row of the inverse, consecutive lanes -> consecutive words), k split
     // into even / odd chains, then l = sum_c a_c y_c by a fixed xor-shuffle tree (deterministic)
-    if (wid < ((nr + 1) >> 1)) {
+    if (wid < ((nr + 1) >> 1) && !(p.ablate & 16u)) {
       const int il = 2 * wid;
       const double* a0 = Ad + il * RD;
       const double* a1 = a0 + RD;  // row il + 1 < 16: inside the buffer (zeros past nr)
@@ -880,23 +880,34 @@ static __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nun
   }
   __syncthreads();
   PW_MK(21);
-  // the unit's aggregate, published with its tag (release), then the exclusive prefix over the
-  // preceding units' aggregates (acquire; exact integer sums in any order)
+  // the unit's raw q rows (into its CDF rows, converted by pw_table_prefix), aggregate and bad bits:
+  // plain stores, published for the whole CTA by one release on the arrival counter (kernel)
+  if (tid < nr) p.cdf[n][r0 + tid] = s_q[tid];
   if (tid == 0) {
     unsigned long long a = 0;
     for (int i = 0; i < nr; ++i) a += s_q[i];
     p.agg[unit] = a;
     p.aggf[2 * unit] = (unsigned)s_badu;
-    st_release_u32(p.aggf + 2 * unit + 1, tag);  // release: agg / bad bits above (same thread) first
   }
+  __syncthreads();
+}
+
+// after every unit of this launch's iteration has published (arrival counter): the exclusive prefix of
+// the unit over the preceding units' aggregates (plain L2 loads, all in flight; exact integer sums in any
+// order) + the unit's inclusive scan -> CDF rows; the last unit writes T and the table status
+static __device__ void pw_table_prefix(const PWParams& p, int n, int unit, int nunits, PWShared& ss) {
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t In = p.dims[n];
+  const int64_t r0 = (int64_t)unit * kPWRows;
+  const int nr = (int)cmin64(kPWRows, In - r0);
   unsigned long long pre = 0;
   unsigned badv = 0;
   for (int u = tid; u < unit; u += nth) {
-    while (ld_acquire_u32(p.aggf + 2 * u + 1) != tag) {
-    }
     pre += __ldcg(p.agg + u);
     badv |= __ldcg(p.aggf + 2 * u);
   }
+  if (unit == nunits - 1)  // the last unit also collects its own bad bits
+    for (int u = tid; u == unit; u += nth) badv |= __ldcg(p.aggf + 2 * u);
   __syncwarp();
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -908,18 +919,16 @@ static __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nun
     ss.red[wid] = __longlong_as_double((long long)badv);
   }
   __syncthreads();
-  PW_MK(22);
   if (wid == 0) {  // predecessors' total + the unit's inclusive scan -> CDF rows (warp 0)
     __syncwarp();
     unsigned long long t = lane < nth / 32 ? ss.wtot[lane] : 0ull;
     unsigned bb = lane < nth / 32 ? (unsigned)__double_as_longlong(ss.red[lane]) : 0u;
+    unsigned long long c = lane < nr ? __ldcg(p.cdf[n] + r0 + min(lane, nr - 1)) : 0ull;  // the unit's raw q
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       t += __shfl_xor_sync(0xffffffffu, t, o);
       bb |= __shfl_xor_sync(0xffffffffu, bb, o);
     }
-    bb |= (unsigned)s_badu;
-    unsigned long long c = lane < nr ? s_q[lane] : 0ull;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned long long v = __shfl_up_sync(0xffffffffu, c, o);
@@ -968,10 +977,14 @@ static __device__ void pw_trace(const PWParams& p, int s, int n, uint64_t r) {
 }
 
 // ------------------------------------------------------------------------------------------ kernel
-#define PW_MARK(slot)                                                                  \
-  do {                                                                                 \
-    if (p.dbg && tid == 0 && s < 8 && blockIdx.x == 0) p.dbg[512 + 32 * s + (slot)] = clock64(); \
-    __syncwarp();                                                                                \
+#define PW_MARK(slot)                                                                              \
+  do {                                                                                             \
+    if (p.dbg && tid == 0 && s < 8) {                                                              \
+      const long long t_ = clock64();                                                              \
+      if (blockIdx.x == 0) p.dbg[512 + 32 * s + (slot)] = t_;                                      \
+      if (blockIdx.x < 160) p.dbg[4096 + ((int64_t)s * 160 + blockIdx.x) * 32 + (slot)] = t_;      \
+    }                                                                                              \
+    __syncwarp();                                                                                  \
   } while (0)
 
 // row groups of the sweep inverse per RMAX: as many as 448 threads hold (32 ceil(RMAX/32) lanes per
@@ -1025,6 +1038,7 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
   uint64_t r = s_r0;
   uint32_t gs = 0, gi = 0;
   PWBulk bk{&B.bc, 0u};
+  unsigned qtarget = 0;  // table-unit arrivals expected before this iteration (all iterations so far)
   int n_done = -1;
   const bool lev = (p.strategy == 1 || p.strategy == 3);
   const int P = R * (R + 1) / 2;
@@ -1056,13 +1070,15 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
       float* sS = sA + ((kPWRows * R + 3) & ~3);
       float* sM = sS + ((kPWRows * R + 3) & ~3);
       double* sgp = reinterpret_cast<double*>(sm + ((sizeof(float) * (3 * kPWRows * RS + R * R + 12) + 15) / 16) * 16);
+      // the Gamma debug hook: the last CTA (idle here whenever nu < G), off the update's critical path
+      if ((int)blockIdx.x == G - 1)
+        for (int e = tid; e < R * R; e += kPWThreads) p.Gam_out[e] = __ldcg(p.gam + e);
       if ((int)blockIdx.x < nu) {
         if (tid == 0) {  // Gamma (every CTA reads it now): a bulk copy, waited for with the unit's rows
           pw_bulk_begin(bk, pw_b16((int64_t)R * R * 4));
           bulk_g2s(sG, p.gam, pw_b16((int64_t)R * R * 4), bk.bar);
         }
-        if (blockIdx.x == 0)
-          for (int e = tid; e < R * R; e += kPWThreads) p.Gam_out[e] = __ldcg(p.gam + e);
+
         for (int u = blockIdx.x; u < nu; u += G) pw_update_unit(p, n, u, alpha, sA, sS, sM, sG, sgp, ss, u == (int)blockIdx.x ? &bk : nullptr,
                                                                  u == (int)blockIdx.x ? mk : nullptr);
       }
@@ -1075,7 +1091,7 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
       // one warp per pair: lane l sums the partials of units l, l + 32, ... (all loads in flight),
       // then a fixed xor-shuffle tree (deterministic); done flag per CTA, tagged by the iteration
       const uint32_t tag = p.tag0 + (uint32_t)s;
-      if (lev) {
+      if (lev && !(p.ablate & 4u)) {
         const int per = (P + G - 1) / G;
         const int a0 = (int)blockIdx.x * per, a1 = min(P, a0 + per);
         for (int pair = a0 + wid; pair < a1; pair += kPWThreads / 32) {
@@ -1084,7 +1100,7 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const int u = c0 + 32 * k + lane;
-              const double t = __ldcg(p.gpart + (int64_t)(u < nu ? u : nu - 1) * P + pair);
+              const double t = __ldcg(p.gpart + (int64_t)pair * p.gstride + (u < nu ? u : nu - 1));
               v[k] = u < nu ? t : 0.0;
             }
 #pragma unroll
@@ -1116,16 +1132,16 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
         int rank = 0, bad0 = 0;
         double fro = 0.0;
         if (lev) {
-          if (tid == 0) wait_count(p.pcnt, (unsigned)G * (unsigned)(s + 1));
+          if (tid == 0 && !(p.ablate & 4u)) wait_count(p.pcnt, (unsigned)G * (unsigned)(s + 1));
           __syncthreads();
           PW_MARK(18);
           {  // the packed Gram (a bulk copy: every CTA reads it now) -> the full symmetric matrix
             double* gst = Wd;  // staging
-            if (tid == 0) {
+            if (tid == 0 && !(p.ablate & 4u)) {
               pw_bulk_begin(bk, pw_b16((int64_t)P * 8));
               bulk_g2s(gst, p.gram, pw_b16((int64_t)P * 8), bk.bar);
             }
-            pw_bulk_wait(bk);
+            if (!(p.ablate & 4u)) pw_bulk_wait(bk);
             for (int e = tid; e < R * R; e += kPWThreads) {
               const int r1 = e / R, r2 = e % R;
               const int a = r1 <= r2 ? r1 : r2, b = r1 <= r2 ? r2 : r1;
@@ -1153,8 +1169,10 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
           __syncthreads();
           constexpr int EPT = (kMaxRank * kMaxRank + kPWThreads - 1) / kPWThreads;
           PW_MARK(19);
-          rank = (In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, ss.tol, rowbuf, swept, diag)
-                              : grp_sweep_inverse<RMAX, kPWSweepGroups<RMAX>>(Gm, R, ss.tol, rowbuf, swept);
+          if (p.ablate & 1u) rank = R;
+          else
+            rank = (In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, ss.tol, rowbuf, swept, diag)
+                                : grp_sweep_inverse<RMAX, kPWSweepGroups<RMAX>>(Gm, R, ss.tol, rowbuf, swept);
           PW_MARK(20);
           bad0 = ss.bad | (rank == 0 ? 2 : 0);
         } else {
@@ -1179,8 +1197,17 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
         for (int u = blockIdx.x; u < nu; u += G)
           pw_table_unit(p, n, u, nu, tag, Gm, rank, fro, bad0, Ad, u + G >= nu ? sAlast : nullptr, ss,
                         u == (int)blockIdx.x ? mk : nullptr);
+        // every unit of the iteration published: one release per CTA, one polling thread per CTA
+        if (tid == 0) {
+          red_release_add(p.qcnt, (unsigned)((nu - 1 - (int)blockIdx.x) / G + 1));
+          wait_count(p.qcnt, qtarget + (unsigned)nu);
+        }
+        __syncthreads();
+        if (mk && tid == 0) mk[22] = clock64();
+        for (int u = blockIdx.x; u < nu; u += G) pw_table_prefix(p, n, u, nu, ss);
       }
       PW_MARK(9);
+      qtarget += (unsigned)nu;
       grid_barrier(p.bar, gen);  // the table of the new A^(n) is complete (R9)
     }
     PW_MARK(10);
@@ -1192,7 +1219,7 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
       if (s + 1 < p.nsteps) grid_barrier(p.bar, gen);  // before the next batch overwrites idx / w
     }
     // a degenerate or non-finite table stops the launch (uniform: the status was set before the barrier)
-    if (tid == 0) s_stop = __ldcg(p.status) != 0;
+    if (tid == 0) s_stop = __ldcg(p.status) != 0 && !(p.ablate & 0x100u);
     __syncthreads();
     if (s_stop) break;
   }

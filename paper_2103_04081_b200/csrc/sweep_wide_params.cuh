@@ -51,11 +51,17 @@ struct PWParams {
   unsigned* aggf;                  // [row units][2]: {bad bits, tag}
   unsigned* bar;                   // grid-barrier arrivals (zero at launch)
   unsigned* pcnt;                  // pair-sum arrivals (zero at launch)
+  unsigned* qcnt;                  // table-unit arrivals (zero at launch)
+  int64_t gstride;                 // gpart: [P][gstride] (leverage pair partials, unit fastest)
   uint32_t tag0;                   // tag of iteration 0 of this launch (unique per handle)
   float* Gout;
   float* Gam_out;
   TraceParams tr;
   long long* dbg;
+  // timing experiments only (CPSGD_PW_ABLATE_MASK; results are garbage): 1 skip the sweep inverse, 2 skip the
+  // fiber loads of the gather, 4 skip the pair sums and the Gram load, 8 skip the update's Gram partials,
+  // 16 skip the scores, 0x100 never stop on a bad status
+  unsigned ablate;
 };
 
 __host__ __device__ inline int pw_units_rows(int64_t In) { return (int)((In + kPWRows - 1) / kPWRows); }

@@ -10,3 +10,4 @@ CPSGD_PW_ABLATE=1 timeout 300 python tools/pw_phases.py C4 leverage > gpurun_out
 CPSGD_PW_ABLATE=1 timeout 300 python tools/pw_phases.py C2 leverage > gpurun_out/q_phases_c2.txt 2>&1
 timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline --no-phases > gpurun_out/q_bench.json 2> gpurun_out/q_bench.err
 tail -2 gpurun_out/q_pytest.log
+timeout 300 python tools/pw_cta.py C4 > gpurun_out/q_cta_c4.txt 2>&1
