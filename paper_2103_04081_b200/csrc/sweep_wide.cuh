@@ -422,7 +422,7 @@ __device__ __forceinline__ void pw_gamma_sum(const PWParams& p, int nsamp, int e
 // the tcgen05 mainloop of gupdate_tc.cuh over this CTA's (I-tile, chunk) items; gs / gi: this CTA's
 // running stage / item counters (the mbarrier phases continue across items and iterations)
 static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PWBars& B, uint32_t tmem, uint32_t& gs,
-                          uint32_t& gi) {
+                          uint32_t& gi, long long* mk) {
   constexpr int KS = kTCKS, NX = kTCNX, NP = kTCPairs, NZ = kTCNZ, TI = kGUTI;
   constexpr uint32_t A_BYTES = kTCABytes;
   constexpr uint32_t IDESC = umma_idesc_tf32_mn(128, 256) & ~((1u << 15) | (1u << 16));
@@ -459,6 +459,7 @@ static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PW
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (mk && first && tid == 0) mk[25] = clock64();
     if (wid < 4) {
       // X loaders: 16-byte cp.async chunks of the sampled fiber segments (Alg. 5 TensorSamp)
       for (int st = 0; st < nst; ++st) {
@@ -487,12 +488,14 @@ static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PW
         const uint32_t g = gs + st;
         const int slot = g % NX, hb = g % NP;
         mbar_wait(&B.xfull[slot], (g / NX) & 1);
+        if (mk && first && t == 0 && st == 0) mk[26] = clock64();
         if (g >= (uint32_t)NP) mbar_wait(&B.mdone[hb], ((g / NP) - 1) & 1);
         const float* A = reinterpret_cast<const float*>(xring + slot * A_BYTES);
         unsigned char* H = xsp + hb * 2 * A_BYTES;
         unsigned char* L = H + A_BYTES;
         const int f0 = st * KS;
         float x[4][4];
+        for (int rep = (p.ablate & 64u) ? 0 : 1; rep < 2; ++rep) {  // timing experiment (64): the split twice
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int kk = 4 * kq + u, lb = f0 + kk;
@@ -503,7 +506,7 @@ static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PW
             x[u][a] = ok ? t : 0.f;
           }
         }
-        mbar_arrive(&B.xempty[slot]);
+        if (rep == 1) mbar_arrive(&B.xempty[slot]);
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           const float4 h = make_float4(tf32_trunc(x[0][a]), tf32_trunc(x[1][a]), tf32_trunc(x[2][a]), tf32_trunc(x[3][a]));
@@ -512,8 +515,10 @@ static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PW
           *reinterpret_cast<float4*>(H + o) = h;
           *reinterpret_cast<float4*>(L + o) = l;
         }
+        }
         fence_proxy_async_smem();
         mbar_arrive(&B.sdone[hb]);
+        if (mk && first && t == 0 && st == nst - 1) mk[27] = clock64();
       }
     } else if (wid == 12) {
       if (lane != 0) {
@@ -524,8 +529,12 @@ static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PW
           const int zs = g % NZ;
           if (g >= (uint32_t)NZ) mbar_wait(&B.afree[zs], ((g / NZ) - 1) & 1);
           const int64_t sb = (c0 + (int64_t)st * KS) / KS;
-          mbar_expect_tx(&B.afull[zs], kTCZBytes);
-          bulk_g2s(zring + zs * kTCZBytes, p.zimg + sb * (kTCZBytes / 4), kTCZBytes, &B.afull[zs]);
+          if (p.ablate & 128u) {  // timing experiment: no A-image copy (stale images)
+            mbar_arrive(&B.afull[zs]);
+          } else {
+            mbar_expect_tx(&B.afull[zs], kTCZBytes);
+            bulk_g2s(zring + zs * kTCZBytes, p.zimg + sb * (kTCZBytes / 4), kTCZBytes, &B.afull[zs]);
+          }
         }
       }
     } else if (wid == 13 && lane == 0) {
@@ -541,6 +550,8 @@ static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PW
         const uint64_t a = dz + ((uint64_t)(as * kTCZBytes) >> 4);
 #pragma unroll
         for (int k = 0; k < KS / 8; ++k) umma_tf32(tmem, a + 2 * k, b + 2 * k, IDESC, (st > 0 || k > 0) ? 1u : 0u);
+        if (p.ablate & 32u)  // timing experiment: every MMA twice
+          for (int k = 0; k < KS / 8; ++k) umma_tf32(tmem, a + 2 * k, b + 2 * k, IDESC, 1u);
         umma_commit(&B.mdone[hb]);
         umma_commit(&B.afree[as]);
       }
@@ -551,6 +562,7 @@ static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PW
     // M^T[r][i] = E[r][i] + E[64 + r][i] (zw = zh + zl) -> the split-K workspace
     if (nst > 0) mbar_wait(&B.accf, gi & 1);
     tc_fence_after();
+    if (mk && first && tid == 0) mk[28] = clock64();
     float* E = reinterpret_cast<float*>(sm);
     if (wid >= 4 && wid <= 11) {
       const int L = 32 * (wid & 3) + lane, hh = (wid - 4) >> 2;
@@ -592,6 +604,7 @@ static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PW
     }
     gs += nst;
     if (nst > 0) ++gi;
+    if (mk && first && tid == 0) mk[29] = clock64();
     first = false;
     __syncthreads();  // the ring / staging area is rewritten by the next item
   }
@@ -1058,7 +1071,7 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
     grid_barrier(p.bar, gen);
     PW_MARK(2);
     // ---- G: TensorSamp + tcgen05 contraction -> split-K partial tiles; Gamma sum ----
-    pw_gather(p, n, sm, B, tmem, gs, gi);
+    pw_gather(p, n, sm, B, tmem, gs, gi, mk);
     PW_MARK(3);
     grid_barrier(p.bar, gen);
     PW_MARK(4);
