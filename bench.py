@@ -232,7 +232,8 @@ def run_ours(args, cfg):
         from paper_2103_04081_b200.parallel import slab_ranges
 
         slab = slab_ranges(cfg.dims[-1], ws)[rank]
-    if sharded or replica:
+    p2p = replica and args.exchange == "p2p"
+    if sharded or (replica and not p2p):
         import torch.distributed as dist
 
         from paper_2103_04081_b200.cpsgd import nccl_unique_id
@@ -251,7 +252,11 @@ def run_ours(args, cfg):
         h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=args.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta,
                   seed=seed, stream=stream, world_rank=rank if one_chain else 0, world_size=ws if one_chain else 1,
                   nccl_id=nccl_id, slab=slab, mode_major=not args.native_layout, fused=args.path == "auto",
-                  tc=not args.no_tc, replica=replica)
+                  tc=not args.no_tc, replica=replica, p2p=p2p)
+    if p2p:  # map every rank's exchange buffer (IPC handles all-gathered through torch.distributed)
+        from paper_2103_04081_b200.parallel import p2p_connect
+
+        p2p_connect(h)
     init_s = time.time() - t0
     h_path = h.path
     N = cfg.order
@@ -391,7 +396,8 @@ def run_ours(args, cfg):
                        "useful_GBps": round(useful_gbs, 2),
                        "layout": "native" if args.native_layout else "mode-major copies (CP_FLAG_MODE_MAJOR)",
                        "parallelism": (f"slab-sharded x{ws} (NCCL)" if sharded else
-                                       f"one chain on {ws} whole-tensor replicas, batch split + ncclAllReduce of M"
+                                       f"one chain on {ws} whole-tensor replicas, batch split + "
+                                       + ("M summed from peer memory in the update kernel" if p2p else "ncclAllReduce of M")
                                        if replica else (f"{ws} independent chains" if ws > 1 else "1 GPU")),
                        "l2": "inputs larger than L2 (tensor + mode-major copies >> 126 MB); fresh fibers per step",
                        "init_s": round(init_s, 3)},
@@ -530,6 +536,9 @@ def main():
                     help="auto: persistent single-cluster kernel when the problem fits one cluster; wide: the "
                          "gather (tcgen05) + table/sampling kernel pair")
     ap.add_argument("--no-tc", action="store_true", help="FFMA gather mainloop instead of tcgen05")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1 replicas: M by ncclAllReduce, or over peer memory summed inside the update kernel "
+                         "(CP_FLAG_P2P, IPC-mapped symmetric buffers)")
     ap.add_argument("--independent", action="store_true",
                     help="N > 1: one unrelated chain per GPU (weak scaling) instead of one chain on N replicas")
     ap.add_argument("--chains", type=int, default=1,

@@ -109,6 +109,15 @@ typedef enum { CP_ORDER_CYCLIC = 0, CP_ORDER_RANDOM = 1 } cp_mode_order;
                                       path (slab sharding, or REPLICA) with a 1-rank NCCL communicator from
                                       nccl_unique_id (or the caller's exchanges with EXTERNAL_COMM), so the
                                       library's NCCL calls run on a one-GPU machine */
+#define CP_FLAG_P2P 0x800u        /* with CP_FLAG_REPLICA: M is exchanged over peer memory (NVLink / NVSwitch)
+                                      instead of an allreduce -- each rank publishes its chunk sum in its own
+                                      symmetric buffer (cp_sgd_p2p_buffer) and the update kernel sums the P
+                                      ranks' copies in rank order straight from their memory (the collective
+                                      fused into its consumer; bitwise identical M on every rank).  The caller
+                                      maps the peers' buffers once (cp_ipc_get_handle + cp_sgd_p2p_open across
+                                      processes, or cp_sgd_p2p_peers with pointers it can already address)
+                                      before the first step; phases 0 and 1 of cp_sgd_step_phase then need no
+                                      exchange in between.                                            */
 #define CP_FLAG_NO_PERSIST 0x80u   /* fp32 wide path: never use the persistent cooperative sweep kernel
                                      (k_sweep_wide); run each step as the gather / update+table /
                                      sample kernel chain (graph-captured for cyclic sweeps)        */
@@ -194,6 +203,19 @@ cp_status cp_sgd_sweep_multi(cp_sgd_t* hs, int32_t nh, int32_t nsweeps);
  * summed over ranks when sharded.  Synchronises.  CP_EDEGENERATE when ||X|| = 0. */
 cp_status cp_fit(cp_sgd_t h, double* fit_host);
 
+/* ---- replicas over peer memory (CP_FLAG_P2P) ------------------------------------------------------
+ * cp_sgd_p2p_buffer: this handle's symmetric exchange buffer (device pointer, bytes) -- flags, then two
+ *   parity copies of the rank's chunk sum of M; owned by the handle.
+ * cp_ipc_get_handle: the 64-byte cudaIpcMemHandle of a device allocation (to send to the other ranks).
+ * cp_sgd_p2p_open: map the world_size handles (64 bytes each, rank order; this rank's entry ignored) with
+ *   cudaIpcOpenMemHandle (peer access enabled) and register them; the mappings are closed by destroy.
+ * cp_sgd_p2p_peers: register world_size device pointers the calling process can address directly (rank
+ *   order; entry world_rank must be this handle's own buffer).  Errors: CP_ESTATE on a handle without
+ *   CP_FLAG_P2P, CP_EINVAL on NULL entries, CP_ECUDA when a mapping fails. */
+cp_status cp_sgd_p2p_buffer(cp_sgd_t h, void** buf_dev, int64_t* bytes);
+cp_status cp_ipc_get_handle(const void* dev_ptr, void* out64_host);
+cp_status cp_sgd_p2p_open(cp_sgd_t h, const void* handles64_host);
+cp_status cp_sgd_p2p_peers(cp_sgd_t h, void* const* peer_bufs_dev);
 /* A fresh 128-byte ncclUniqueId from the NCCL library this library uses (rank 0 creates it and
  * broadcasts it to the other ranks, e.g. through torch.distributed, before cp_sgd_init). */
 cp_status cp_nccl_unique_id(void* out128_host);

@@ -25,6 +25,7 @@ FLAG_NO_PERSIST = 0x80
 FLAG_STRATIFIED = 0x100
 FLAG_REPLICA = 0x200
 FLAG_FORCE_COMM = 0x400
+FLAG_P2P = 0x800
 KERNEL_NAMES = ["k_sample", "k_gather", "k_update_table", "k_table", "k_reduce_partials", "nccl", "k_fit",
                 "k_sweep_fused", "k_gather_update", "k_zw_gamma", "k_gather_update_tc", "k_table_sample",
                 "k_update_wide", "k_scores_wide", "k_sample_wide", "k_sweep_wide"]
@@ -36,7 +37,8 @@ EXPORTS = ["cp_sgd_init", "cp_sgd_destroy", "cp_sgd_last_error", "cp_sgd_sample"
            "cp_sgd_get_table", "cp_sgd_get_grad", "cp_sgd_get_accum", "cp_sgd_get_iter", "cp_sgd_set_iter",
            "cp_sgd_refresh_tables", "cp_sgd_get_launches", "cp_sgd_profile", "cp_sgd_profile_read",
            "cp_sgd_version", "cp_sgd_batch_max", "cp_sgd_debug_timers", "cp_sgd_exchange_copy", "cp_sgd_trace_layout",
-           "cp_sgd_trace", "cp_sgd_trace_count", "cp_sgd_path", "cp_slice_sqnorms", "cp_nccl_unique_id"]
+           "cp_sgd_trace", "cp_sgd_trace_count", "cp_sgd_path", "cp_slice_sqnorms", "cp_nccl_unique_id", "cp_sgd_p2p_buffer",
+           "cp_ipc_get_handle", "cp_sgd_p2p_open", "cp_sgd_p2p_peers"]
 
 
 class CPError(RuntimeError):
@@ -102,6 +104,10 @@ def load_library(path: str = LIB_PATH):
     L.cp_sgd_path.argtypes = [P, C.POINTER(C.c_int32)]
     L.cp_slice_sqnorms.argtypes = [P, i32, i64, i64, P, P]
     L.cp_nccl_unique_id.argtypes = [P]
+    L.cp_sgd_p2p_buffer.argtypes = [P, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]
+    L.cp_ipc_get_handle.argtypes = [P, P]
+    L.cp_sgd_p2p_open.argtypes = [P, P]
+    L.cp_sgd_p2p_peers.argtypes = [P, P]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype if name in ("cp_sgd_last_error", "cp_sgd_version") else C.c_int
     _lib = L
@@ -132,7 +138,7 @@ class CPSGD:
                  slab=None, mode_major: bool = True, block_window=None, graphs: bool = True,
                  external_comm: bool = False, fused: bool = True, wide: bool = True,
                  tc: bool = True, fused_cluster: int = 16, persist: bool = True, stratified: bool = False,
-                 slab_bounds=None, replica: bool = False, force_comm: bool = False):
+                 slab_bounds=None, replica: bool = False, force_comm: bool = False, p2p: bool = False):
         import torch
 
         L = load_library()
@@ -160,7 +166,7 @@ class CPSGD:
                 (0 if wide else FLAG_NO_WIDE) | (0 if tc else FLAG_NO_TC) | \
                 (FLAG_FUSED_CU8 if fused_cluster == 8 else 0) | (0 if persist else FLAG_NO_PERSIST) | \
                 (FLAG_STRATIFIED if stratified else 0) | (FLAG_REPLICA if replica else 0) | \
-                (FLAG_FORCE_COMM if force_comm else 0)
+                (FLAG_FORCE_COMM if force_comm else 0) | (FLAG_P2P if p2p else 0)
         lo, hi = (0, self.dims[-1]) if slab is None else (int(slab[0]), int(slab[1]))
         cfg = Config(self.N, self._dims_arr, self.R, self.dtype, X.data_ptr(), self._fac_arr, int(batch),
                      self._win_arr, SAMPLERS[sampler], RULES[rule], float(alpha), float(eta), float(b), float(eps),
@@ -233,6 +239,31 @@ class CPSGD:
         buf, cnt, rb, re = C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int64()
         self._chk(self._L.cp_sgd_exchange_info(self._h, mode, C.byref(buf), C.byref(cnt), C.byref(rb), C.byref(re)))
         return buf.value, cnt.value, rb.value, re.value
+
+    def p2p_buffer(self):
+        """(device pointer, bytes) of this replica's symmetric exchange buffer (CP_FLAG_P2P)"""
+        buf, nb = C.c_void_p(), C.c_int64()
+        self._chk(self._L.cp_sgd_p2p_buffer(self._h, C.byref(buf), C.byref(nb)))
+        return buf.value, nb.value
+
+    def p2p_ipc_handle(self) -> bytes:
+        """64-byte cudaIpcMemHandle of the exchange buffer, to send to the other ranks"""
+        out = C.create_string_buffer(64)
+        buf, _ = self.p2p_buffer()
+        st = self._L.cp_ipc_get_handle(C.c_void_p(buf), out)
+        if st != 0:
+            raise CPError(st, "cp_ipc_get_handle")
+        return bytes(out.raw)
+
+    def p2p_open(self, handles):
+        """map every rank's exchange buffer from its IPC handle (rank order, 64 bytes each)"""
+        blob = b"".join(bytes(hd) for hd in handles)
+        self._chk(self._L.cp_sgd_p2p_open(self._h, C.create_string_buffer(blob, len(blob))))
+
+    def p2p_peers(self, ptrs):
+        """register device pointers of every rank's exchange buffer (rank order) addressable here"""
+        arr = (C.c_void_p * len(ptrs))(*[int(x) for x in ptrs])
+        self._chk(self._L.cp_sgd_p2p_peers(self._h, arr))
 
     def exchange_count(self, mode: int) -> int:
         """elements of the phase-0 exchange buffer of `mode` (slabs: partial M, R x I_n; replicas: the rank's

@@ -235,6 +235,14 @@ struct cp_sgd_s {
   size_t ev_next = 0;
   std::vector<int64_t> row_ranges;  // [2*world]: slab [lo, hi) of every rank
   void* Mred = nullptr;             // replicas (CP_FLAG_REPLICA): this rank's chunk sum of M, [tiles][R][128]
+  // CP_FLAG_P2P: this rank's symmetric exchange buffer (flags + 2 parity copies), the peers' buffers
+  void* p2p_buf = nullptr;
+  int64_t p2p_msz = 0;
+  void* peer[kMaxStrata] = {};
+  bool peers_set = false;
+  std::vector<void*> peer_opened;   // IPC mappings to close
+  unsigned long long* p2p_epoch = nullptr;
+  unsigned* p2p_cnt = nullptr;      // [0] chunk-sum arrivals, [32] update arrivals
   int64_t strat_lo[kMaxStrata + 1] = {};  // CP_FLAG_STRATIFIED: slab bounds of the ranks (R26)
 
   cp_status fail(cp_status st, const char* fmt, ...) {
@@ -605,6 +613,40 @@ __global__ void k_chunk_sum(const T* __restrict__ Mpart, int CK, int c_first, in
   Mred[e] = acc;
 }
 
+// replicas over peer memory (CP_FLAG_P2P, wide.cuh "replicas exchanging M over peer memory"): the chunk
+// sum into this rank's symmetric buffer (parity of epoch e), published by the last CTA (ready = e)
+template <typename T>
+__global__ void k_chunk_sum_p2p(const T* __restrict__ Mpart, int CK, int c_first, int c_step, int R, int64_t tiles,
+                                void* buf, int64_t msz, int npeer, const unsigned long long* epoch, unsigned* cnt) {
+  __shared__ unsigned long long s_e;
+  if (threadIdx.x == 0) {
+    const unsigned long long e = *reinterpret_cast<const volatile unsigned long long*>(epoch) + 1;
+    s_e = e;
+    if (e > 2)  // this parity was published at e - 2: every reader must be done with it
+      for (int r = 0; r < npeer; ++r)
+        while (ld_acquire_sys_u64(p2p_done_flag(buf, r)) < e - 2) {
+        }
+  }
+  __syncthreads();
+  T* dst = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(buf) + kP2PHead) + (int64_t)(s_e & 1ull) * msz;
+  const int64_t per = (int64_t)R * kGUTI;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tiles * per; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tile = e / per, o = e % per;
+    T acc = T(0);
+    for (int c = c_first; c < CK; c += c_step) acc += Mpart[(tile * CK + c) * per + o];
+    dst[e] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(cnt, 1u) == gridDim.x - 1) {  // every CTA's part written: publish
+      *cnt = 0;
+      __threadfence_system();
+      st_release_sys_u64(reinterpret_cast<unsigned long long*>(buf), s_e);
+    }
+  }
+}
+
 template <typename T, int CPT>
 cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
   ProfScope ps(h, kKGatherUpdate);
@@ -792,6 +834,14 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev,
   p.In = h->dims[n];
   p.Mpart = (const T*)(replica(h) ? h->Mred : h->Mpart);  // replicas: the rank-summed M, one "chunk"
   p.CK = replica(h) ? 1 : h->gu_ck[n];
+  if (replica(h) && (h->flags & CP_FLAG_P2P) && !take_chg) {  // M summed from the peers' buffers
+    p.npeer = h->world_size;
+    p.rank = h->world_rank;
+    for (int g = 0; g < h->world_size; ++g) p.peer[g] = h->peer[g];
+    p.p2p_msz = h->p2p_msz;
+    p.p2p_epoch = h->p2p_epoch;
+    p.p2p_cnt = h->p2p_cnt + 32;
+  }
   p.Gam = (const T*)h->gam_next;
   p.A = (T*)h->factors[n];
   p.S = (T*)h->S[n];
@@ -1279,6 +1329,21 @@ cp_status phase0(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
   if (wide_mode(h, n)) {  // gather + contraction + split-K partials (replicas: this rank's chunks)
     st = h->dtype == CP_F64 ? launch_gu<double>(h, n, alpha, alpha_dev) : launch_gu<float>(h, n, alpha, alpha_dev);
     h->pref_mode = -1;
+    if (!st && replica(h) && (h->flags & CP_FLAG_P2P)) {  // -> this rank's symmetric buffer, published
+      if (!h->peers_set) return h->fail(CP_ESTATE, "CP_FLAG_P2P: the peers' buffers were not set (cp_sgd_p2p_peers)");
+      const int64_t tiles = ceil_div(h->dims[n], kGUTI), tot = tiles * h->R * kGUTI;
+      const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(tot, 256), 296);
+      if (h->dtype == CP_F64)
+        k_chunk_sum_p2p<double><<<blocks, 256, 0, h->ls>>>((const double*)h->Mpart, h->gu_ck[n], h->world_rank,
+                                                           h->world_size, h->R, tiles, h->p2p_buf, h->p2p_msz,
+                                                           h->world_size, h->p2p_epoch, h->p2p_cnt);
+      else
+        k_chunk_sum_p2p<float><<<blocks, 256, 0, h->ls>>>((const float*)h->Mpart, h->gu_ck[n], h->world_rank,
+                                                          h->world_size, h->R, tiles, h->p2p_buf, h->p2p_msz,
+                                                          h->world_size, h->p2p_epoch, h->p2p_cnt);
+      h->launches++;
+      return check_launch(h, "k_chunk_sum_p2p");
+    }
     if (!st && replica(h)) {  // -> Mred, summed over ranks before phase 1
       const int64_t tiles = ceil_div(h->dims[n], kGUTI), tot = tiles * h->R * kGUTI;
       const int CK = h->gu_ck[n];
@@ -1344,6 +1409,7 @@ cp_status nccl_check(cp_sgd_s* h, ncclResult_t r, const char* what) {
 }
 
 cp_status exchange_after0(cp_sgd_s* h, int n) {
+  if (replica(h) && (h->flags & CP_FLAG_P2P)) return CP_OK;  // summed by k_update_wide from peer memory
   if (replica(h) && !(h->flags & CP_FLAG_EXTERNAL_COMM)) {  // M = sum over ranks of the chunk sums
     ProfScope ps(h, kKComm);
     const int dt = h->dtype == CP_F64 ? kNcclFloat64 : kNcclFloat32;
@@ -1469,6 +1535,8 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
     h->factors[k] = cfg->factors[k];
     h->ldims[k] = cfg->dims[k];
   }
+  if ((h->flags & CP_FLAG_P2P) && !(h->flags & CP_FLAG_REPLICA))
+    return init_fail(h, h->fail(CP_EINVAL, "CP_FLAG_P2P is the replicas' exchange: it needs CP_FLAG_REPLICA"));
   if ((h->flags & CP_FLAG_REPLICA) && (h->flags & CP_FLAG_STRATIFIED))
     return init_fail(h, h->fail(CP_EINVAL, "CP_FLAG_REPLICA and CP_FLAG_STRATIFIED exclude each other"));
   if (sharded(h)) {
@@ -1674,6 +1742,16 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       ALLOC(h->sw_gcl, h->esz * ncl * h->R * h->R);
       ALLOC(h->Mpart, h->esz * mpart);
       if (replica(h)) ALLOC(h->Mred, h->esz * ceil_div(Imax, kGUTI) * kGUTI * h->R);
+      if (replica(h) && (h->flags & CP_FLAG_P2P)) {
+        h->p2p_msz = ceil_div(Imax, kGUTI) * kGUTI * h->R;
+        const size_t bytes = kP2PHead + 2 * h->esz * (size_t)h->p2p_msz;
+        ALLOC(h->p2p_buf, bytes);
+        cudaMemsetAsync(h->p2p_buf, 0, bytes, h->stream);
+        ALLOC(h->p2p_epoch, sizeof(unsigned long long));
+        cudaMemsetAsync(h->p2p_epoch, 0, sizeof(unsigned long long), h->stream);
+        ALLOC(h->p2p_cnt, sizeof(unsigned) * 64);
+        cudaMemsetAsync(h->p2p_cnt, 0, sizeof(unsigned) * 64, h->stream);
+      }
       ALLOC(h->gu_cnt, sizeof(unsigned) * ceil_div(Imax, kGUTI));
       cudaMemsetAsync(h->gu_cnt, 0, sizeof(unsigned) * ceil_div(Imax, kGUTI), h->stream);
       ALLOC(h->zwp, h->esz * Bmax_all * zg_rp(h->R));
@@ -1742,7 +1820,8 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
   if (multi(h)) {
     auto* rr = rr_store(h, true);
     rr->assign(2 * h->world_size, 0);
-    if (!(h->flags & CP_FLAG_EXTERNAL_COMM)) {
+    // no communicator for external-comm handles, nor for replicas exchanging over peer memory
+    if (!(h->flags & CP_FLAG_EXTERNAL_COMM) && !(h->flags & CP_FLAG_P2P)) {
       if (!cfg->nccl_unique_id) return init_fail(h, h->fail(CP_EINVAL, "world_size > 1 needs nccl_unique_id"));
       std::string e;
       if (!g_nccl.load(e)) return init_fail(h, h->fail(CP_ENCCL, "%s", e.c_str()));
@@ -1841,6 +1920,10 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->gam_next);
   cudaFree(h->Mpart);
   cudaFree(h->Mred);
+  for (void* q : h->peer_opened) cudaIpcCloseMemHandle(q);
+  cudaFree(h->p2p_buf);
+  cudaFree(h->p2p_epoch);
+  cudaFree(h->p2p_cnt);
   cudaFree(h->gu_cnt);
   cudaFree(h->uw_gpart);
   cudaFree(h->uw_rownorm);
@@ -2220,6 +2303,57 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
     CUDA_TRY(h, cudaMemcpyAsync(factors_host[k], h->factors[k], h->esz * h->dims[k] * h->R, cudaMemcpyDeviceToHost,
                                 h->stream));
   return cp_sgd_sync(h);
+}
+
+cp_status cp_sgd_p2p_buffer(cp_sgd_t h, void** buf_dev, int64_t* bytes) {
+  if (!h || !buf_dev) return CP_EINVAL;
+  if (!h->p2p_buf) return h->fail(CP_ESTATE, "not a CP_FLAG_P2P replica handle");
+  *buf_dev = h->p2p_buf;
+  if (bytes) *bytes = kP2PHead + 2 * (int64_t)h->esz * h->p2p_msz;
+  return CP_OK;
+}
+
+cp_status cp_sgd_p2p_peers(cp_sgd_t h, void* const* peer_bufs_dev) {
+  if (!h || !peer_bufs_dev) return CP_EINVAL;
+  if (!h->p2p_buf) return h->fail(CP_ESTATE, "not a CP_FLAG_P2P replica handle");
+  for (int g = 0; g < h->world_size; ++g) {
+    if (!peer_bufs_dev[g]) return h->fail(CP_EINVAL, "peer buffer %d is NULL", g);
+    h->peer[g] = peer_bufs_dev[g];
+  }
+  if (h->peer[h->world_rank] != h->p2p_buf) return h->fail(CP_EINVAL, "entry world_rank must be this handle's buffer");
+  h->peers_set = true;
+  return CP_OK;
+}
+
+cp_status cp_ipc_get_handle(const void* dev_ptr, void* out64_host) {
+  if (!dev_ptr || !out64_host) return CP_EINVAL;
+  cudaIpcMemHandle_t hd;
+  if (cudaIpcGetMemHandle(&hd, const_cast<void*>(dev_ptr)) != cudaSuccess) {
+    cudaGetLastError();
+    return CP_ECUDA;
+  }
+  memcpy(out64_host, &hd, sizeof hd);
+  return CP_OK;
+}
+
+cp_status cp_sgd_p2p_open(cp_sgd_t h, const void* handles64_host) {
+  if (!h || !handles64_host) return CP_EINVAL;
+  if (!h->p2p_buf) return h->fail(CP_ESTATE, "not a CP_FLAG_P2P replica handle");
+  std::vector<void*> ptrs(h->world_size);
+  for (int g = 0; g < h->world_size; ++g) {
+    if (g == h->world_rank) {
+      ptrs[g] = h->p2p_buf;
+      continue;
+    }
+    cudaIpcMemHandle_t hd;
+    memcpy(&hd, (const unsigned char*)handles64_host + 64 * g, sizeof hd);
+    void* q = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&q, hd, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return h->fail(CP_ECUDA, "cudaIpcOpenMemHandle(rank %d): %s", g, cudaGetErrorString(e));
+    h->peer_opened.push_back(q);
+    ptrs[g] = q;
+  }
+  return cp_sgd_p2p_peers(h, ptrs.data());
 }
 
 cp_status cp_nccl_unique_id(void* out128_host) {

@@ -36,6 +36,28 @@ constexpr int kSWFibers = 32;   // fibers per k_sample_wide CTA
 constexpr int kSWCluster = 8;
 constexpr int kUWCluster = 8;   // k_update_wide CTAs per cluster (table partials summed over DSMEM)
 
+// ---- replicas exchanging M over peer memory (CP_FLAG_P2P, NVLink / NVSwitch) ----------------------------
+// Every rank owns a symmetric buffer: 64-bit flags (ready epoch at word 0; done[r] at word 16 + 16 r, each
+// on its own 128-byte line, written by reader r into the owner's buffer) and, from byte kP2PHead, two parity
+// copies of its chunk sum of M.  Exchange e (a device-side epoch, advanced in lockstep on every rank):
+// the chunk-sum kernel waits until every reader has finished epoch e - 2 of this parity, writes the sum,
+// and its last CTA publishes ready = e (release, system scope); k_update_wide waits for every peer's
+// ready >= e (acquire, system scope), sums the P copies in rank order straight from peer memory (the
+// collective fused into its consumer: bitwise identical M on every rank), and its last CTA writes
+// done[rank] = e into every peer's buffer.
+constexpr int kP2PHead = 4096;
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__host__ __device__ inline unsigned long long* p2p_done_flag(void* buf, int reader) {
+  return reinterpret_cast<unsigned long long*>(buf) + 16 + 16 * reader;
+}
+
 template <typename T>
 struct UWParams {
   int R, strategy, rule;
@@ -67,6 +89,12 @@ struct UWParams {
   const T* fstage;
   const int* chg;
   long long* dbg;
+  // CP_FLAG_P2P (npeer > 0): M = sum over the peers' symmetric buffers (rank order) instead of Mpart
+  int npeer, rank;
+  void* peer[kMaxStrata];
+  int64_t p2p_msz;                  // elements of one parity copy
+  unsigned long long* p2p_epoch;    // device epoch of the last completed exchange
+  unsigned* p2p_cnt;                // CTA arrivals after the peer reads (zero between launches)
 };
 
 // cp_sgd_steps_host (wide path): chg[k] |= 1 when the staged host factor k differs bitwise from the
@@ -360,8 +388,49 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
     }
     for (int e = tid; e < R * R; e += kWThreads) cp_async_small<sizeof(T)>(sG + e, p.Gam + e, sizeof(T));
     cp_async_commit();
-    // M = sum of the chunk partials, in chunk order (16-byte vectors of VW consecutive rows)
-    {
+    __shared__ unsigned long long s_pe;
+    if (p.npeer > 0) {  // peer-memory exchange: every peer's copy of epoch e published
+      if (tid == 0) {
+        const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(p.p2p_epoch) + 1;
+        s_pe = e;
+        for (int g = 0; g < p.npeer; ++g)
+          while (ld_acquire_sys_u64(reinterpret_cast<const unsigned long long*>(p.peer[g])) < e) {
+          }
+      }
+      __syncthreads();
+    }
+    // M = sum of the chunk partials, in chunk order (16-byte vectors of VW consecutive rows); P2P: the
+    // sum of the peers' chunk sums, in rank order, loaded from their memory
+    if (p.npeer > 0) {
+      constexpr int VW = 16 / (int)sizeof(T);
+      using V = typename Vec<T>::type;
+      const int64_t tile = r0 / TI, lr0 = r0 % TI;
+      const int ng = (nr + VW - 1) / VW;
+      const int64_t off = (int64_t)(s_pe & 1ull) * p.p2p_msz + tile * R * TI + lr0;
+      for (int t = tid; t < R * ng; t += kWThreads) {
+        const int r = t / ng, gq = t % ng;
+        T acc[VW];
+  #pragma unroll
+        for (int w = 0; w < VW; ++w) acc[w] = T(0);
+        V ld[kMaxStrata];
+  #pragma unroll
+        for (int g = 0; g < kMaxStrata; ++g)  // every peer's load in flight, then summed in rank order
+          if (g < p.npeer)
+            ld[g] = __ldcg(reinterpret_cast<const V*>(reinterpret_cast<const T*>(
+                                                          reinterpret_cast<const unsigned char*>(p.peer[g]) + kP2PHead) +
+                                                      off + (int64_t)r * TI + gq * VW));
+  #pragma unroll
+        for (int g = 0; g < kMaxStrata; ++g)
+          if (g < p.npeer) {
+            const T* x = reinterpret_cast<const T*>(&ld[g]);
+  #pragma unroll
+            for (int w = 0; w < VW; ++w) acc[w] += x[w];
+          }
+  #pragma unroll
+        for (int w = 0; w < VW; ++w)
+          if (gq * VW + w < nr) sM[(gq * VW + w) * RS + r] = acc[w];
+      }
+    } else {
       constexpr int VW = 16 / (int)sizeof(T);
       using V = typename Vec<T>::type;
       const int64_t tile = r0 / TI, lr0 = r0 % TI;
@@ -392,6 +461,13 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
     }
     cp_async_wait<0>();
     __syncthreads();
+    if (p.npeer > 0 && tid == 0) {  // this CTA's peer reads are complete; the last CTA signals every peer
+      if (atomicAdd(p.p2p_cnt, 1u) == gridDim.x - 1) {
+        *p.p2p_cnt = 0;
+        for (int g = 0; g < p.npeer; ++g) st_release_sys_u64(p2p_done_flag(p.peer[g], p.rank), s_pe);
+        *reinterpret_cast<volatile unsigned long long*>(p.p2p_epoch) = s_pe;  // every CTA read it at its start
+      }
+    }
     if (p.rule == 2) {
       // sampled least squares (eq:lsq_krp; R25): W = Gamma^+ in fp64 by the
       // natural-order sweep (tol R eps max diag) in every CTA, then this CTA's rows A = M W (into

@@ -154,3 +154,18 @@ class ShardedRunner:
         for _ in range(nsweeps):
             for n in range(self.N):
                 self.step(n, alpha)
+
+
+def p2p_connect(handle, group=None):
+    """Map every rank's CP_FLAG_P2P exchange buffer into this process (one call per rank, collective over
+    `group`): the 64-byte IPC handles are all-gathered through torch.distributed (rank order) and opened by
+    the library (cp_sgd_p2p_open).  `handle` needs p2p_ipc_handle() and p2p_open(list)."""
+    import torch.distributed as dist
+
+    mine = handle.p2p_ipc_handle()
+    world = dist.get_world_size(group)
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    handle.p2p_open(allh)
+    return allh
+

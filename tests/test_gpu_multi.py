@@ -209,3 +209,91 @@ def test_replica_refused_configs():
         X32, A32 = make_problem(cfg32)
         Xd32, Ad32 = to_dev(X32, A32)
         handle(cfg32, Xd32, Ad32, "leverage", **base)
+
+
+# ------------------------------------------------------------- replicas over peer memory (CP_FLAG_P2P)
+def _p2p_run(cfg, X, A0, strategy, P, seed, iters, rule_kw):
+    """P replica handles exchanging M through each other's symmetric buffers (addressable directly: one
+    process, one GPU), all on ONE stream so every rank's phase 0 (publish) completes before any rank's
+    phase 1 (peer reads) starts -- no kernel ever waits on another running kernel"""
+    from paper_2103_04081_b200 import CPSGD
+
+    dev = torch.device("cuda:0")
+    stream = torch.cuda.current_stream(dev)
+    Xd = torch.from_numpy(X).to(dev)
+    hs, facs = [], []
+    for g in range(P):
+        Ag = [torch.from_numpy(np.ascontiguousarray(a).copy()).to(dev) for a in A0]
+        facs.append(Ag)
+        hs.append(CPSGD(Xd, cfg.dims, Ag, cfg.batch, sampler=strategy, seed=seed, world_rank=g, world_size=P,
+                        replica=True, p2p=True, fused=False, stream=stream, **rule_kw))
+    bufs = [h.p2p_buffer()[0] for h in hs]
+    for h in hs:
+        h.p2p_peers(bufs)
+    N = len(cfg.dims)
+    for it in range(iters):
+        n = it % N
+        for ph in range(3):
+            for h in hs:
+                h.step_phase(n, ph)
+    torch.cuda.synchronize()
+    out = [[a.cpu().numpy() for a in Ag] for Ag in facs]
+    for h in hs:
+        h.close()
+    return out
+
+
+@pytest.mark.parametrize("strategy", ["leverage", "euclidean", "uniform"])
+@pytest.mark.parametrize("P", [2, 3])
+def test_p2p_replicas_match_single_gpu_and_oracle(strategy, P):
+    cfg = synth.small((40, 30, 24), 6, dtype="f64", batch=96, rule="fixed", alpha=0.002, seed=5)
+    X, A0 = make_problem(cfg)
+    outs = _p2p_run(cfg, X, A0, strategy, P, 6, 12, dict(rule="fixed", alpha=cfg.alpha))  # > 2 epochs per parity
+    Xd, Ad = to_dev(X, A0)
+    h1 = handle(cfg, Xd, Ad, strategy, seed=6, fused=False, persist=False)
+    h1.sweep(4)
+    h1.sync()
+    fs, _, _ = oracle.run(X, A0, oracle.STRATEGIES[strategy], oracle.STEP_FIXED, cfg.batch, 12, alpha=cfg.alpha,
+                          seed=6)
+    for g in range(P):
+        for k in range(3):
+            assert np.array_equal(outs[g][k], outs[0][k])  # the same bytes on every rank (rank-order sum)
+            ref = Ad[k].cpu().numpy()
+            assert rel_err(outs[g][k], ref, np.linalg.norm(ref)) <= 1e-12
+            assert rel_err(outs[g][k], fs[k], np.linalg.norm(fs[k])) <= 1e-10
+    h1.close()
+
+
+def test_p2p_replicas_f32_adaptive_trajectory_equals_nccl_style_sum():
+    """fp32 tcgen05 replicas: the peer-memory exchange gives the same factors as the caller-summed
+    (external-comm) exchange -- both sum the ranks' chunk sums in rank order"""
+    cfg = synth.small((300, 130, 200), 20, dtype="f32", batch=1024, rule="adaptive", eta=0.03, seed=8)
+    X, A0 = make_problem(cfg)
+    a = _p2p_run(cfg, X, A0, "leverage", 2, 9, 6, dict(rule="adaptive", eta=cfg.eta))
+    b = _replica_run(cfg, X, A0, "leverage", 2, 9, 6, dict(rule="adaptive", eta=cfg.eta))
+    for g in range(2):
+        for k in range(3):
+            assert np.array_equal(a[g][k], b[g][k])
+
+
+def test_p2p_api_errors_and_ipc_handle():
+    from paper_2103_04081_b200 import CPError
+
+    cfg = synth.small((40, 30, 24), 6, dtype="f64", batch=96, rule="fixed", seed=5)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    with pytest.raises(CPError, match="EINVAL"):  # P2P without replicas
+        handle(cfg, Xd, Ad, "leverage", world_rank=0, world_size=2, external_comm=True, p2p=True, fused=False)
+    h = handle(cfg, Xd, Ad, "leverage", world_rank=0, world_size=2, replica=True, p2p=True, fused=False)
+    with pytest.raises(CPError, match="ESTATE"):  # peers not registered yet
+        h.step_phase(0, 0)
+    buf, nbytes = h.p2p_buffer()
+    assert buf and nbytes > 4096
+    assert len(h.p2p_ipc_handle()) == 64
+    with pytest.raises(CPError, match="EINVAL"):  # entry world_rank must be the handle's own buffer
+        h.p2p_peers([buf + 4096, buf])
+    h.close()
+    h2 = handle(cfg, Xd, Ad, "leverage", fused=False)
+    with pytest.raises(CPError, match="ESTATE"):
+        h2.p2p_buffer()
+    h2.close()

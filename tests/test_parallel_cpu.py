@@ -200,3 +200,39 @@ def test_sharded_runner_gloo_stratified():
     for r in range(world):
         for k in range(3):
             np.testing.assert_allclose(out[r][k], A[k], rtol=1e-11, atol=1e-13)
+
+
+class _StubP2P:
+    def __init__(self, rank):
+        self.rank = rank
+        self.opened = None
+
+    def p2p_ipc_handle(self):
+        return bytes([self.rank + 1]) * 64
+
+    def p2p_open(self, handles):
+        self.opened = list(handles)
+
+
+def _worker_p2p(rank, world, port, out):
+    from paper_2103_04081_b200.parallel import p2p_connect
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    h = _StubP2P(rank)
+    p2p_connect(h)
+    out[rank] = h.opened
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_p2p_connect_gathers_handles_in_rank_order():
+    """host logic of the peer-memory exchange setup (CP_FLAG_P2P): every rank opens every rank's 64-byte IPC
+    handle, in rank order (world 3 over gloo)"""
+    world = 3
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_p2p, args=(world, _free_port(), out), nprocs=world, join=True)
+    want = [bytes([g + 1]) * 64 for g in range(world)]
+    for r in range(world):
+        assert out[r] == want
