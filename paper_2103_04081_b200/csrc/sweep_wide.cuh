@@ -1182,10 +1182,14 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
           __syncthreads();
           constexpr int EPT = (kMaxRank * kMaxRank + kPWThreads - 1) / kPWThreads;
           PW_MARK(19);
-          if (p.ablate & 1u) rank = R;
-          else
-            rank = (In < 2 * R) ? cta_sweep_inverse_pivoted<EPT>(Gm, R, ss.tol, rowbuf, swept, diag)
-                                : grp_sweep_inverse<RMAX, kPWSweepGroups<RMAX>>(Gm, R, ss.tol, rowbuf, swept);
+          constexpr int SG = kPWSweepGroups<RMAX>;
+          if (p.ablate & 1u) {
+            rank = R;
+          } else if (In < 2 * R) {
+            rank = cta_sweep_inverse_pivoted<EPT>(Gm, R, ss.tol, rowbuf, swept, diag);
+          } else {
+            rank = grp_sweep_inverse<RMAX, SG>(Gm, R, ss.tol, rowbuf, swept);
+          }
           PW_MARK(20);
           bad0 = ss.bad | (rank == 0 ? 2 : 0);
         } else {

@@ -125,7 +125,7 @@ def traffic(report: str, key: str, sweeps: int | None) -> str:
         seen.add(name)
         b = sum(_to_bytes(r[ix[k]], units[ix[k]]) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         ent = {"bytes": b}
-        if sweeps and name == "k_sweep_fused":
+        if sweeps and name in ("k_sweep_fused", "k_sweep_wide"):
             ent["sweeps"] = sweeps
         data[f"{key}/{name}"] = ent
     json.dump(data, open(tfile, "w"), indent=1, sort_keys=True)
