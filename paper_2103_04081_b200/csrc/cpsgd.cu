@@ -190,6 +190,8 @@ struct cp_sgd_s {
   uint32_t pw_tag = 0;           // look-back tags: iteration s of a launch uses pw_tag + 1 + s
   float* pw_gcl = nullptr;       // [grid][R][R] per-CTA partials of Gamma
   double* pw_gram = nullptr;     // [R(R+1)/2]
+  uint64_t* pw_qraw = nullptr;   // [I_max rounded to 16]: raw q rows of the table being rebuilt
+  uint64_t* pw_coarse[kMaxOrder] = {};  // per mode [units]: coarse CDFs of the persistent kernel
   unsigned long long* pw_agg = nullptr;  // [row units]
   unsigned* pw_aggf = nullptr;   // [row units][2]
   unsigned* pw_bar = nullptr;    // [0] barrier arrivals, [32] pair-sum, [64] table-unit arrivals (zeroed per launch)
@@ -1223,6 +1225,8 @@ bool plan_pw(cp_sgd_s* h) {
   };
   if (!alloc((void**)&h->pw_gcl, sizeof(float) * (size_t)h->pw_grid * h->R * h->R) ||
       !alloc((void**)&h->pw_gram, sizeof(double) * ((P + 1) & ~1)) ||  // even: whole 16-byte bulk copies
+      !alloc((void**)&h->pw_qraw, sizeof(uint64_t) * (size_t)(units_max_of(h) * kPWRows)) ||
+      !alloc((void**)&h->pw_coarse[0], sizeof(uint64_t) * (size_t)(units_max_of(h) * h->N)) ||
       !alloc((void**)&h->pw_agg, sizeof(unsigned long long) * units) ||
       !alloc((void**)&h->pw_aggf, sizeof(unsigned) * 2 * units) ||
       !alloc((void**)&h->pw_bar, sizeof(unsigned) * 128)) {
@@ -1288,6 +1292,8 @@ cp_status launch_pw(cp_sgd_s* h, int nsteps, int first_mode, int order, double a
   p.bar = h->pw_bar;
   p.pcnt = h->pw_bar + 32;  // another 128-byte line
   p.qcnt = h->pw_bar + 64;  // another 128-byte line
+  p.qraw = h->pw_qraw;
+  for (int k = 0; k < h->N; ++k) p.coarse[k] = h->pw_coarse[0] + (size_t)k * units_max_of(h);
   p.gstride = units_max_of(h);
   p.tag0 = h->pw_tag + 1;
   p.Gout = (float*)h->Gout;
@@ -1617,7 +1623,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       return init_fail(h, h->fail(CP_ENOMEM, "cudaMalloc(%zu): %s", (size_t)(bytes), cudaGetErrorString(e_))); \
   } while (0)
   for (int k = 0; k < h->N; ++k) {
-    ALLOC(h->cdf[k], sizeof(uint64_t) * ((h->dims[k] + 1) & ~1));  // even: whole 16-byte bulk copies
+    ALLOC(h->cdf[k], sizeof(uint64_t) * ((h->dims[k] + 15) & ~15));  // whole 16-row blocks (two-level search)
     ALLOC(h->pprob[k], sizeof(double) * h->dims[k]);
     if (h->rule == CP_STEP_ADAPTIVE) {
       ALLOC(h->S[k], h->esz * h->dims[k] * h->R);
@@ -1951,6 +1957,8 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   cudaFree(h->pw_gcl);
   cudaFree(h->pw_gram);
+  cudaFree(h->pw_qraw);
+  cudaFree(h->pw_coarse[0]);
   cudaFree(h->pw_agg);
   cudaFree(h->pw_aggf);
   cudaFree(h->pw_bar);

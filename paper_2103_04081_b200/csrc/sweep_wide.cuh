@@ -139,8 +139,61 @@ struct PWShared {  // static shared state of the phases
     __syncwarp();                                     \
   } while (0)
 
+// Two-level CDF search (no staging of whole CDFs): coarse[j] = the inclusive CDF at the end of 16-row block j
+// (staged in shared memory), then the block's 16 entries straight from L2 -- the CDF rows of a mode, or, for the
+// mode rebuilt in the previous iteration (pend), its raw q rows with the block's base coarse[j - 1].  Returns
+// exactly the full search's i = #{i : CDF[i] <= r} and q_i (eq:ik under the contract of DESIGN.md section 4).
+// Rows past I are padding of the 16-row allocations and are masked.
+__device__ __forceinline__ void pw_cdf_search(const uint64_t* src, bool pend, const uint64_t* coarse, int ncb,
+                                              int64_t I, uint64_t r, int64_t& i, uint64_t& qk) {
+  int j = (int)upper_bound_u64(coarse, ncb, r);
+  if (j >= ncb) j = ncb - 1;  // T = 0 (degenerate table, the status is set): keep the addresses valid
+  const uint64_t cb = coarse[j > 0 ? j - 1 : 0];  // unconditional load, then select
+  const uint64_t base = j > 0 ? cb : 0ull;
+  const int64_t lo = (int64_t)j * kPWRows;
+  const int cnt = (int)cmin64(kPWRows, I - lo);
+  uint64_t v[kPWRows];
+#pragma unroll
+  for (int t = 0; t < kPWRows; t += 2) {
+    const ulonglong2 x = __ldcg(reinterpret_cast<const ulonglong2*>(src + lo + t));
+    v[t] = x.x;
+    v[t + 1] = x.y;
+  }
+  int idx = 0;
+  uint64_t c = base, qsel = 0, prev = base;
+#pragma unroll
+  for (int t = 0; t < kPWRows; ++t) {
+    const uint64_t e = pend ? c + v[t] : v[t];  // the inclusive CDF at row lo + t
+    if (t < cnt) {
+      if (e <= r) {
+        idx = t + 1;
+        prev = e;
+      } else if (idx == t) {
+        qsel = e - prev;
+      }
+    }
+    c = e;
+  }
+  if (idx >= cnt) {  // r beyond the table (T = 0): the last row, q of it
+    idx = cnt - 1;
+    qsel = 0;
+  }
+  i = lo + idx;
+  qk = qsel;
+}
+
+// the inclusive CDF at row x (block windows, eq:bik): coarse base + the block's entries up to x
+__device__ __forceinline__ uint64_t pw_cdf_at(const uint64_t* src, bool pend, const uint64_t* coarse, int64_t x) {
+  if (x < 0) return 0ull;
+  const int j = (int)(x / kPWRows);
+  if (!pend) return __ldcg(src + x);
+  uint64_t c = j > 0 ? coarse[j - 1] : 0ull;
+  for (int64_t t = (int64_t)j * kPWRows; t <= x; ++t) c += __ldcg(src + t);
+  return c;
+}
+
 static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned char* sm, PWShared& ss, PWBulk& bk,
-                                 long long* mk) {
+                                 long long* mk, int pend) {
   const int tid = threadIdx.x, nth = blockDim.x;
   const int N = p.N, NP = N - 1, R = p.R, RP = zg_rp(R), nb4 = (R + 3) >> 2;
   const bool block = (p.strategy == 3 || p.strategy == 4);
@@ -168,28 +221,41 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
   float* red = reinterpret_cast<float*>(carve(sizeof(float) * (size_t)GG * R * R));
   float* gacc = reinterpret_cast<float*>(carve(sizeof(float) * R * R));
   {
-    // the CDFs of the sampled modes (rebuilt by other CTAs of this launch): bulk copies, each mode's area
-    // a whole number of 16-byte units (the allocations are even-length)
+    // coarse CDFs of the sampled modes (the inclusive CDF at the end of every 16-row block): for the mode rebuilt in
+    // the previous iteration, the inclusive scan of its unit aggregates (its CDF rows are written concurrently, from
+    // its raw q rows); for the others, every 16th row of their CDF.  All loads of a thread in flight at once.
     int64_t o = 0;
-    uint32_t tot = 0;
-    for (int k = 0; k < N; ++k)
-      if (k != n && p.strategy != 0) tot += pw_b16(8 * p.dims[k]);
-    if (tid == 0 && tot) pw_bulk_begin(bk, tot);
     for (int k = 0; k < N; ++k) {
-      const uint64_t* src = p.cdf[k];
-      if (k != n && p.strategy != 0) {
-        if (tid == 0) bulk_g2s(cdfs + o, src, pw_b16(8 * p.dims[k]), bk.bar);
-        src = cdfs + o;
-        o += (p.dims[k] + 1) & ~(int64_t)1;
+      if (k == n || p.strategy == 0) {
+        if (tid == 0) ss.T[k] = p.strategy == 0 ? (uint64_t)p.dims[k] : 0ull;
+        continue;
       }
-      if (tid == 0) {
-        ss.cp[k] = src;
-        ss.coff[k] = src == p.cdf[k] ? 0 : (int64_t)(src - cdfs);
-        ss.T[k] = p.strategy == 0 ? (uint64_t)p.dims[k] : __ldcg(p.Ttot + k);
+      const int ncb = (int)((p.dims[k] + kPWRows - 1) / kPWRows);
+      uint64_t* co = cdfs + o;
+      if (tid == 0) ss.coff[k] = o;
+      if (k == pend) {  // warp 0: inclusive scan of the aggregates (unit order; exact integers)
+        if (tid < 32) {
+          uint64_t carry = 0;
+          for (int u0 = 0; u0 < ncb; u0 += 32) {
+            const int u = u0 + tid;
+            uint64_t a = u < ncb ? __ldcg(p.agg + u) : 0ull;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const uint64_t t = __shfl_up_sync(0xffffffffu, a, d);
+              if (tid >= d) a += t;
+            }
+            if (u < ncb) co[u] = carry + a;
+            carry += __shfl_sync(0xffffffffu, a, 31);
+          }
+          if (tid == 0) ss.T[k] = carry;
+        }
+      } else {
+        for (int j = tid; j < ncb; j += nth) co[j] = __ldcg(p.coarse[k] + j);  // contiguous: coalesced
+        if (tid == 0) ss.T[k] = __ldcg(p.Ttot + k);
       }
+      o += (ncb + 1) & ~1;
     }
     for (int e = tid; e < R * R; e += nth) gacc[e] = 0.f;
-    if (tot) pw_bulk_wait(bk);
   }
   __syncthreads();
   PW_MK(11);
@@ -202,12 +268,14 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
       const int64_t bk = p.window[n][pos];
       const uint64_t Tk = ss.T[k];
       const uint64_t rr = scale_draw(draw_word(p.seed, r, 0u, kPurposeWindow, (uint32_t)pos), Tk);
-      const uint64_t* c = cdfs + ss.coff[k];  // indexed from the shared array: LDS, not generic loads
-      int64_t istar = upper_bound_u64(c, p.dims[k], rr);
-      if (istar >= p.dims[k]) istar = p.dims[k] - 1;  // T = 0 (degenerate table, status already set)
+      const uint64_t* co = cdfs + ss.coff[k];
+      const bool pk = (k == pend);
+      const uint64_t* src = pk ? p.qraw : p.cdf[k];
+      int64_t istar;
+      uint64_t qdummy;
+      pw_cdf_search(src, pk, co, (int)((p.dims[k] + kPWRows - 1) / kPWRows), p.dims[k], rr, istar, qdummy);
       const int64_t s0 = (istar / bk) * bk, e0 = min(s0 + bk, p.dims[k]);
-      const uint64_t cprev = c[s0 > 0 ? s0 - 1 : 0];  // unconditional load, then select
-      const uint64_t Q = c[e0 - 1] - (s0 > 0 ? cprev : 0ull);
+      const uint64_t Q = pw_cdf_at(src, pk, co, e0 - 1) - pw_cdf_at(src, pk, co, s0 - 1);
       ss.start[pos] = (int32_t)s0;
       ss.len[pos] = (int32_t)(e0 - s0);
       const double pt = __ddiv_rn((double)((uint64_t)p.dims[k] * Q), (double)Tk);
@@ -240,11 +308,9 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
           i = (int64_t)rr;
           qk = 1;
         } else {
-          const uint64_t* c = cdfs + ss.coff[k];  // indexed from the shared array: LDS, not generic loads
-          i = upper_bound_u64(c, p.dims[k], rr);
-          if (i >= p.dims[k]) i = p.dims[k] - 1;  // T = 0: status already set, keep the addresses valid
-          const uint64_t cprev = c[i > 0 ? i - 1 : 0];  // unconditional load, then select
-          qk = c[i] - (i > 0 ? cprev : 0ull);
+          const bool pk = (k == pend);
+          pw_cdf_search(pk ? p.qraw : p.cdf[k], pk, cdfs + ss.coff[k], (int)((p.dims[k] + kPWRows - 1) / kPWRows),
+                        p.dims[k], rr, i, qk);
         }
         sidx[e] = (int32_t)i;
         spt[e] = __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);
@@ -895,17 +961,19 @@ static __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nun
   PW_MK(21);
   // the unit's raw q rows (into its CDF rows, converted by pw_table_prefix), aggregate and bad bits:
   // plain stores, published for the whole CTA by one release on the arrival counter (kernel)
-  if (tid < nr) p.cdf[n][r0 + tid] = s_q[tid];
+  if (tid < nr) p.qraw[r0 + tid] = s_q[tid];
   if (tid == 0) {
     unsigned long long a = 0;
     for (int i = 0; i < nr; ++i) a += s_q[i];
     p.agg[unit] = a;
     p.aggf[2 * unit] = (unsigned)s_badu;
+    // a bad table is visible to every CTA as soon as the arrivals are (the launch stops before drawing from it)
+    if (s_badu) atomicCAS(p.status, 0, (s_badu & 8) ? -8 : -3);
   }
   __syncthreads();
 }
 
-// after every unit of this launch's iteration has published (arrival counter): the exclusive prefix of
+// after every unit of an iteration has published (arrival counter; run during the next sampling phase): the exclusive prefix of
 // the unit over the preceding units' aggregates (plain L2 loads, all in flight; exact integer sums in any
 // order) + the unit's inclusive scan -> CDF rows; the last unit writes T and the table status
 static __device__ void pw_table_prefix(const PWParams& p, int n, int unit, int nunits, PWShared& ss) {
@@ -936,7 +1004,7 @@ static __device__ void pw_table_prefix(const PWParams& p, int n, int unit, int n
     __syncwarp();
     unsigned long long t = lane < nth / 32 ? ss.wtot[lane] : 0ull;
     unsigned bb = lane < nth / 32 ? (unsigned)__double_as_longlong(ss.red[lane]) : 0u;
-    unsigned long long c = lane < nr ? __ldcg(p.cdf[n] + r0 + min(lane, nr - 1)) : 0ull;  // the unit's raw q
+    unsigned long long c = lane < nr ? __ldcg(p.qraw + r0 + min(lane, nr - 1)) : 0ull;  // the unit's raw q
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       t += __shfl_xor_sync(0xffffffffu, t, o);
@@ -949,6 +1017,7 @@ static __device__ void pw_table_prefix(const PWParams& p, int n, int unit, int n
     }
     c += t;
     if (lane < nr) p.cdf[n][r0 + lane] = c;
+    if (lane == nr - 1) p.coarse[n][unit] = c;  // the inclusive CDF at the unit's last row
     if (unit == nunits - 1 && lane == nr - 1) {  // the last unit: T and the table status
       p.Ttot[n] = c;
       int st = 0;
@@ -1052,10 +1121,21 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
   uint32_t gs = 0, gi = 0;
   PWBulk bk{&B.bc, 0u};
   unsigned qtarget = 0;  // table-unit arrivals expected before this iteration (all iterations so far)
+  int pend = -1;         // mode whose table was rebuilt by the previous iteration, CDF rows not yet written
   int n_done = -1;
   const bool lev = (p.strategy == 1 || p.strategy == 3);
   const int P = R * (R + 1) / 2;
 
+  // the coarse CDFs of every mode (the inclusive CDF at the end of each 16-row block) from the tables as the
+  // launch found them (built by init or by other kernels); kept current by the table phase from here on
+  if (p.strategy != 0) {
+    for (int k = 0; k < N; ++k) {
+      const int nb = pw_units_rows(p.dims[k]);
+      for (int j = (int)blockIdx.x * kPWThreads + tid; j < nb; j += G * kPWThreads)
+        p.coarse[k][j] = __ldcg(p.cdf[k] + min((int64_t)j * kPWRows + kPWRows - 1, p.dims[k] - 1));
+    }
+    grid_barrier(p.bar, gen);
+  }
 #pragma unroll 1
   for (int s = 0; s < p.nsteps; ++s) {
     const int n = p.order == 1 ? random_mode(p.seed, r, N) : (p.first_mode + s) % N;
@@ -1064,9 +1144,24 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
     const double alpha = p.alphas ? p.alphas[s] : (p.alpha_dev ? *p.alpha_dev : p.alpha);
     PW_MARK(0);
     if (p.dbg && tid == 0 && s < 8 && blockIdx.x == 0) p.dbg[512 + 32 * s + 30] = gtimer();
-    // ---- S: the batch of mode n at r ----
     long long* mk = (p.dbg && s < 8 && blockIdx.x == 0) ? p.dbg + 512 + 32 * s : nullptr;
-    pw_sample(p, n, r, sm, ss, bk, mk);
+    // ---- the table rebuilt in the previous iteration (mode pend): every unit has published its raw q rows and
+    // aggregate (arrival counter, no grid barrier); a bad table stops the launch before anything is drawn ----
+    if (pend >= 0) {
+      if (tid == 0) {
+        wait_count(p.qcnt, qtarget);
+        s_stop = __ldcg(p.status) != 0 && !(p.ablate & 0x100u);
+      }
+      __syncthreads();
+      if (s_stop) break;
+    }
+    // ---- S: the batch of mode n at r (from the coarse CDFs; pend: from its aggregates / raw q rows) ----
+    pw_sample(p, n, r, sm, ss, bk, mk, pend);
+    // ---- the pending table's CDF rows, T and status (read from the next sampling phase on) ----
+    if (pend >= 0) {
+      for (int u = blockIdx.x; u < pw_units_rows(p.dims[pend]); u += G) pw_table_prefix(p, pend, u, pw_units_rows(p.dims[pend]), ss);
+      pend = -1;
+    }
     PW_MARK(1);
     grid_barrier(p.bar, gen);
     PW_MARK(2);
@@ -1214,31 +1309,39 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
         for (int u = blockIdx.x; u < nu; u += G)
           pw_table_unit(p, n, u, nu, tag, Gm, rank, fro, bad0, Ad, u + G >= nu ? sAlast : nullptr, ss,
                         u == (int)blockIdx.x ? mk : nullptr);
-        // every unit of the iteration published: one release per CTA, one polling thread per CTA
-        if (tid == 0) {
-          red_release_add(p.qcnt, (unsigned)((nu - 1 - (int)blockIdx.x) / G + 1));
-          wait_count(p.qcnt, qtarget + (unsigned)nu);
-        }
-        __syncthreads();
-        if (mk && tid == 0) mk[22] = clock64();
-        for (int u = blockIdx.x; u < nu; u += G) pw_table_prefix(p, n, u, nu, ss);
+        // this CTA's units published: one release (no wait: the next sampling phase waits for all of them)
+        if (tid == 0) red_release_add(p.qcnt, (unsigned)((nu - 1 - (int)blockIdx.x) / G + 1));
       }
       PW_MARK(9);
       qtarget += (unsigned)nu;
-      grid_barrier(p.bar, gen);  // the table of the new A^(n) is complete (R9)
+      pend = n;  // the table of the new A^(n) is complete once every unit has arrived (R9)
     }
     PW_MARK(10);
     if (p.dbg && tid == 0 && s < 8 && blockIdx.x == 0) p.dbg[512 + 32 * s + 31] = gtimer();
     ++r;
     n_done = n;
-    if (p.tr.base) {
+    if (p.tr.base) {  // debug trace: complete the table first, then record the iteration
+      if (pend >= 0) {
+        if (tid == 0) wait_count(p.qcnt, qtarget);
+        __syncthreads();
+        for (int u = blockIdx.x; u < pw_units_rows(p.dims[pend]); u += G) pw_table_prefix(p, pend, u, pw_units_rows(p.dims[pend]), ss);
+        pend = -1;
+      }
+      grid_barrier(p.bar, gen);
       pw_trace(p, s, n, r - 1);
       if (s + 1 < p.nsteps) grid_barrier(p.bar, gen);  // before the next batch overwrites idx / w
     }
-    // a degenerate or non-finite table stops the launch (uniform: the status was set before the barrier)
-    if (tid == 0) s_stop = __ldcg(p.status) != 0 && !(p.ablate & 0x100u);
+    if (p.strategy == 0) {  // uniform (no table): the barrier after the update orders it before the next batch
+      if (tid == 0) s_stop = __ldcg(p.status) != 0 && !(p.ablate & 0x100u);
+      __syncthreads();
+      if (s_stop) break;
+    }
+  }
+  // the last iteration's table (or the one the stop found bad): its CDF rows, T and status
+  if (pend >= 0) {
+    if (tid == 0) wait_count(p.qcnt, qtarget);
     __syncthreads();
-    if (s_stop) break;
+    for (int u = blockIdx.x; u < pw_units_rows(p.dims[pend]); u += G) pw_table_prefix(p, pend, u, pw_units_rows(p.dims[pend]), ss);
   }
   __syncthreads();
   if (wid == 13) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));

@@ -52,6 +52,8 @@ struct PWParams {
   unsigned* bar;                   // grid-barrier arrivals (zero at launch)
   unsigned* pcnt;                  // pair-sum arrivals (zero at launch)
   unsigned* qcnt;                  // table-unit arrivals (zero at launch)
+  uint64_t* qraw;                  // [I_max padded to 16]: raw q rows of the table being rebuilt
+  uint64_t* coarse[kMaxOrder];     // per mode [units]: the inclusive CDF at the end of each 16-row block
   int64_t gstride;                 // gpart: [P][gstride] (leverage pair partials, unit fastest)
   uint32_t tag0;                   // tag of iteration 0 of this launch (unique per handle)
   float* Gout;
