@@ -46,7 +46,7 @@ t0 = time.time()
 for name, variants in [("C2", [dict(), dict(fused_cluster=8), dict(fused=False)]), ("C3", [dict()]),
                        ("C4", [dict()])]:
     cfg, Xd, A0d = problem(name)
-    for sampler in (["leverage", "euclidean", "block_leverage", "uniform"] if name != "C4" else ["leverage"]):
+    for sampler in (["leverage", "euclidean", "block_leverage", "uniform"] if name != "C4" else ["leverage", "euclidean", "block_euclidean"]):
         for kw in variants:
             a = run(cfg, Xd, A0d, sampler, **kw)
             b = run(cfg, Xd, A0d, sampler, **kw)
