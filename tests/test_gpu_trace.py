@@ -111,3 +111,74 @@ def test_c3_full_size_one_step_per_mode():
         assert rel_err(h.get_accum(n), S_o, np.linalg.norm(S_o)) <= 2 * TOL["f32"]
         h.close()
         del Xd
+
+
+def test_c5_slab_rank0_full_size():
+    """C5 (4000^3 fp32 = 256 GB, R32, B8192, adaptive): rank 0 of the 8-way slab split run on one GPU -- its
+    32 GB slab X[..., 0:500] (+ mode-major copies), an external-comm handle.  The global batch is bit-exact
+    with the oracle; phase 0 of mode 0 leaves the partial M over the fibers the rank owns (i_3 in its slab);
+    phases 0-1 of the last mode update the rank's rows A^(3)[0:500] from its fiber segments -- both against the
+    oracle's gradient on the same sampled fibers read from the seeded slab (fp32 tolerance; b = 0 band mask)."""
+    from paper_2103_04081_b200 import CPSGD
+    from paper_2103_04081_b200.parallel import slab_ranges
+
+    cfg = synth.CONFIGS["C5"]
+    dims, R, B = cfg.dims, cfg.rank, cfg.batch
+    lo, hi = slab_ranges(dims[-1], 8)[0]
+    ldims = (dims[0], dims[1], hi - lo)
+    dev = torch.device("cuda:0")
+    Xd, _, xn = synth.tensor_torch(cfg, device=dev, slab=(lo, hi))
+    Ad = synth.init_factors_torch(cfg, xn, device=dev)
+    A0 = [a.cpu().numpy() for a in Ad]
+    fs = [np.asarray(a, np.float64) for a in A0]
+    h = CPSGD(Xd, dims, Ad, B, sampler="leverage", rule="adaptive", eta=cfg.eta, seed=2, world_rank=0, world_size=8,
+              slab=(lo, hi), external_comm=True, fused=False)
+    tabs = oracle_tables("leverage", A0)
+    tq = [(t[1], t[2]) for t in tabs]
+    Jn = float(dims[1] * dims[2])
+    # ---- mode 0 at r = 0: the batch, then the partial M over the owned fibers ----
+    idx_o, w_o, pj = oracle.sample(dims, 0, oracle.LEVERAGE, B, tq, 2, 0)
+    ig, wg = h.sample(0, 0)
+    assert np.array_equal(ig.cpu().numpy(), idx_o) and np.array_equal(wg.cpu().numpy(), w_o)
+    h.step_phase(0, 0)
+    buf = torch.empty(h.exchange_count(0), dtype=torch.float32, device=dev)
+    h.exchange_copy(0, buf, False)
+    M_g = buf.cpu().numpy().astype(np.float64).reshape(R, dims[0]).T
+    own = (idx_o[:, 1] >= lo) & (idx_o[:, 1] < hi)
+    li = idx_o[own].copy()
+    li[:, 1] -= lo
+    XF = gather_fibers_torch(Xd, ldims, 0, li)                     # (owned, I_0) from the seeded slab
+    Z = oracle.skr(fs, 0, idx_o[own])
+    d = 1.0 / pj[own]
+    M_o = (XF.T @ (d[:, None] * Z)) / (B * Jn)
+    assert 0.05 < own.mean() < 0.3                                 # the slab's share of the leverage mass
+    assert rel_err(M_g, M_o, np.linalg.norm(M_o)) <= TOL["f32"]
+    assert row_rel_err(M_g, M_o) <= 10 * TOL["f32"]
+    h.close()
+    # ---- the last mode at r = 1: every fiber's slab segment, the rank's rows of A^(3) updated ----
+    h = CPSGD(Xd, dims, Ad, B, sampler="leverage", rule="adaptive", eta=cfg.eta, seed=2, world_rank=0, world_size=8,
+              slab=(lo, hi), external_comm=True, fused=False)
+    h.iter = 1
+    idx_o, w_o, pj = oracle.sample(dims, 2, oracle.LEVERAGE, B, tq, 2, 1)
+    h.step_phase(2, 0)
+    h.step_phase(2, 1)
+    torch.cuda.synchronize()
+    XF = gather_fibers_torch(Xd, ldims, 2, idx_o)                 # (B, 500): the fibers' slab segments
+    Z = oracle.skr(fs, 2, idx_o)
+    d = 1.0 / pj
+    scale = 1.0 / (B * float(dims[0] * dims[1]))
+    C1 = Z.T @ (d[:, None] * Z)
+    C2 = XF.T @ (d[:, None] * Z)
+    Arows = fs[2][lo:hi]
+    G_o = scale * (Arows @ C1 - C2)
+    A_o, _ = oracle.update_adaptive(Arows, np.zeros_like(Arows), G_o, cfg.eta)
+    sc = np.linalg.norm(scale * (Arows @ C1)) + np.linalg.norm(scale * C2)
+    band = np.abs(G_o) <= 10 * TOL["f32"] * sc / np.sqrt(G_o.size)  # b = 0: eta sign(G) (gpu_helpers.trace_check)
+    assert band.mean() < 0.05
+    A_g = Ad[2][lo:hi].cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(np.where(band, 0.0, A_g - A_o)) <= TOL["f32"] * np.linalg.norm(A_o)
+    assert row_rel_err(np.where(band, A_o, A_g), A_o) <= 10 * TOL["f32"]
+    assert np.array_equal(Ad[2][hi:].cpu().numpy(), A0[2][hi:])   # rows of the other ranks: untouched
+    h.close()
+    del Xd, Ad
+    torch.cuda.empty_cache()
