@@ -207,6 +207,58 @@ def run_chains(args, cfg):
             "clocks": clk.summary(), "gpu_launches": 1, "e2e": None}
 
 
+def run_slab(args, cfg):
+    """one rank's share of a slab-sharded run on ONE GPU -- rank 0 of the P-way split of the
+    last mode (its slab of X, mode-major copies, an external-comm handle), timing the per-GPU sharded step (phases
+    0-2 of every mode: the global batch's draws, the owned fibers' gather + contraction, the update, the table)
+    with the exchanges left out.  value = the GLOBAL batch rate a P-GPU job would sustain if the exchanges were
+    free (informational, not the driver's line)."""
+    import torch
+
+    from paper_2103_04081_b200 import CPSGD
+    from paper_2103_04081_b200.parallel import slab_ranges
+
+    P = args.slab_of
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(0)
+    lo, hi = slab_ranges(cfg.dims[-1], P)[0]
+    Xd, _, xn = synth.tensor_torch(cfg, device=dev, slab=(lo, hi))
+    Ad = synth.init_factors_torch(cfg, xn, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=args.sampler, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta,
+                  seed=cfg.seed, stream=stream, world_rank=0, world_size=P, slab=(lo, hi), external_comm=True,
+                  fused=False)
+    N = cfg.order
+
+    def sweeps(k):
+        for _ in range(k):
+            for n in range(N):
+                for ph in range(3):
+                    h.step_phase(n, ph)
+
+    sweeps(args.warmup)
+    h.sync()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        ev0.record(stream)
+        sweeps(args.steps)
+        ev1.record(stream)
+        stream.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = h.launches
+    h.close()
+    return {"metric": METRIC + " [one rank of a slab-sharded run, exchanges excluded]",
+            "value": round(N * cfg.batch * args.steps / (ms / 1e3), 1), "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
+            "data": "synthetic (seeded; synth/ recipe)",
+            "config": {"workload": workload_str(cfg, args.sampler) + f"; rank 0 of {P} slabs [{lo}, {hi})",
+                       "step": "one cyclic sweep of the rank's phases 0-2 (cp_sgd_step_phase), no exchange",
+                       "slab_GB": round(Xd.numel() * 4 / 1e9, 2)},
+            "clocks": clk.summary(), "gpu_launches": launches, "e2e": None}
+
+
 def run_ours(args, cfg):
     import torch
 
@@ -545,6 +597,8 @@ def main():
                     help="K > 1: K independent chains in one multi-chain launch (fused workloads; SURVEY 8f.2)")
     ap.add_argument("--chain-cluster", type=int, default=16, choices=[8, 16],
                     help="--chains: CTAs per chain (8: two chains per GPC)")
+    ap.add_argument("--slab-of", type=int, default=0,
+                    help="P > 1: time rank 0's share of a P-way slab-sharded run on one GPU (exchanges excluded)")
     ap.add_argument("--rule", default="config", choices=["config", "fixed", "adaptive", "als"],
                     help="update rule (config: the workload's; als: the sampled least-squares step, SURVEY 8f.3)")
     args = ap.parse_args()
@@ -565,6 +619,9 @@ def main():
     __graft_entry__.build()  # idempotent (mtime check, atomic replace)
     if args.chains > 1:
         print(json.dumps(run_chains(args, cfg)), flush=True)
+        return
+    if args.slab_of > 1:
+        print(json.dumps(run_slab(args, cfg)), flush=True)
         return
     if ws > 1:
         import torch.distributed  # noqa: F401
