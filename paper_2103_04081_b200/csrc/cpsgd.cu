@@ -236,7 +236,8 @@ struct cp_sgd_s {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
   std::vector<int64_t> row_ranges;  // [2*world]: slab [lo, hi) of every rank
-  void* Mred = nullptr;             // replicas (CP_FLAG_REPLICA): this rank's chunk sum of M, [tiles][R][128]
+  void* Mred = nullptr;             // replicas / slab shards on the wide path: this rank's chunk sum of M, [tiles][R][128]
+  int* one_dev = nullptr;           // a device 1 (table-only rebuild of the current factor)
   // CP_FLAG_P2P: this rank's symmetric exchange buffer (flags + 2 parity copies), the peers' buffers
   void* p2p_buf = nullptr;
   int64_t p2p_msz = 0;
@@ -655,7 +656,7 @@ cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
   GUParams<T> p;
   memset(&p, 0, sizeof p);
   p.R = h->R;
-  p.In = h->dims[n];
+  p.In = h->In_local[n];  // slab shards, last mode: the rank's rows
   if (h->Xmm[n]) {
     p.X = (const T*)h->Xmm[n];
     p.es = 1;
@@ -695,7 +696,7 @@ cp_status launch_gu_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev)
     cudaFuncSetAttribute(k_gather_update<T, CPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)ceil_div(h->dims[n], kGUTI), (unsigned)ny, 1);
+  lc.gridDim = dim3((unsigned)ceil_div(h->In_local[n], kGUTI), (unsigned)ny, 1);
   lc.blockDim = dim3(kGUThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
@@ -715,7 +716,7 @@ cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev
   GUParams<float> p;
   memset(&p, 0, sizeof p);
   p.R = h->R;
-  p.In = h->dims[n];
+  p.In = h->In_local[n];  // slab shards, last mode: the rank's rows
   p.X = h->Xmm[n] ? (const float*)h->Xmm[n] : (const float*)h->X;
   p.es = 1;
   p.vec = 1;
@@ -751,7 +752,7 @@ cp_status launch_gu_tc(cp_sgd_s* h, int n, double alpha, const double* alpha_dev
     allow_max_dyn_smem(k_gather_update_tc<0>);
   }
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)ceil_div(h->dims[n], kGUTI), (unsigned)ny, 1);
+  lc.gridDim = dim3((unsigned)ceil_div(h->In_local[n], kGUTI), (unsigned)ny, 1);
   lc.blockDim = dim3(kTCThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
@@ -826,16 +827,22 @@ bool uw_coresident(int R, int64_t In) {
 }
 
 template <typename T>
-cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, const int* take_chg = nullptr) {
+cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, const int* take_chg = nullptr,
+                      bool from_self = false) {
   ProfScope ps(h, kKUpdateWide);
   UWParams<T> p;
   memset(&p, 0, sizeof p);
   p.R = h->R;
   p.strategy = h->sampler;
   p.rule = h->rule;
-  p.In = h->dims[n];
-  p.Mpart = (const T*)(replica(h) ? h->Mred : h->Mpart);  // replicas: the rank-summed M, one "chunk"
-  p.CK = replica(h) ? 1 : h->gu_ck[n];
+  // slab shards, last mode: the update of the rank's rows only (the table follows the row exchange: phase 2)
+  const bool own_rows = sharded(h) && n == h->N - 1 && !take_chg;
+  const int64_t r0 = own_rows ? h->row0[n] : 0;
+  p.In = own_rows ? h->In_local[n] : h->dims[n];
+  const bool red = replica(h) || (sharded(h) && n < h->N - 1);  // the rank-summed M, one "chunk"
+  p.Mpart = (const T*)(red ? h->Mred : h->Mpart);
+  p.CK = red ? 1 : h->gu_ck[n];
+  p.update_only = own_rows ? 1 : 0;
   if (replica(h) && (h->flags & CP_FLAG_P2P) && !take_chg) {  // M summed from the peers' buffers
     p.npeer = h->world_size;
     p.rank = h->world_rank;
@@ -845,9 +852,9 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev,
     p.p2p_cnt = h->p2p_cnt + 32;
   }
   p.Gam = (const T*)h->gam_next;
-  p.A = (T*)h->factors[n];
-  p.S = (T*)h->S[n];
-  p.Gout = (T*)h->Gout;
+  p.A = (T*)h->factors[n] + r0 * h->R;
+  p.S = h->S[n] ? (T*)h->S[n] + r0 * h->R : nullptr;
+  p.Gout = (T*)h->Gout + r0 * h->R;
   p.Gam_out = (T*)h->Gam_out;
   p.alpha = alpha;
   p.alpha_dev = alpha_dev;
@@ -868,7 +875,7 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev,
   p.status = h->status_dev;
   p.qch = std::min<int64_t>(h->dims[n], 4096);
   p.table_only = take_chg ? 1 : 0;  // cp_sgd_steps_host: take over the staged factor, rebuild its table
-  p.fstage = (const T*)h->fstage[n];
+  p.fstage = from_self ? (const T*)h->factors[n] : (const T*)h->fstage[n];  // from_self: the factor as it is
   p.chg = take_chg;
   p.dbg = h->dbg;
   const size_t smem = uw_smem_bytes(h->R, sizeof(T), p.qch);
@@ -877,7 +884,7 @@ cp_status launch_uw_t(cp_sgd_s* h, int n, double alpha, const double* alpha_dev,
     allow_max_dyn_smem(k_update_wide<T>);
   }
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)(ceil_div(ceil_div(h->dims[n], kUWRows), kUWCluster) * kUWCluster), 1, 1);
+  lc.gridDim = dim3((unsigned)(ceil_div(ceil_div(p.In, kUWRows), kUWCluster) * kUWCluster), 1, 1);
   lc.blockDim = dim3(kWThreads, 1, 1);
   lc.dynamicSmemBytes = smem;
   lc.stream = h->ls;
@@ -1350,15 +1357,16 @@ cp_status phase0(cp_sgd_s* h, int n, double alpha, const double* alpha_dev) {
       h->launches++;
       return check_launch(h, "k_chunk_sum_p2p");
     }
-    if (!st && replica(h)) {  // -> Mred, summed over ranks before phase 1
+    if (!st && (replica(h) || (sharded(h) && n < h->N - 1))) {  // -> Mred, summed over ranks before phase 1
       const int64_t tiles = ceil_div(h->dims[n], kGUTI), tot = tiles * h->R * kGUTI;
       const int CK = h->gu_ck[n];
+      const int c0 = replica(h) ? h->world_rank : 0, cs = replica(h) ? h->world_size : 1;
       if (h->dtype == CP_F64)
         k_chunk_sum<double><<<(unsigned)ceil_div(tot, 256), 256, 0, h->ls>>>(
-            (const double*)h->Mpart, CK, h->world_rank, h->world_size, h->R, tiles, (double*)h->Mred);
+            (const double*)h->Mpart, CK, c0, cs, h->R, tiles, (double*)h->Mred);
       else
         k_chunk_sum<float><<<(unsigned)ceil_div(tot, 256), 256, 0, h->ls>>>(
-            (const float*)h->Mpart, CK, h->world_rank, h->world_size, h->R, tiles, (float*)h->Mred);
+            (const float*)h->Mpart, CK, c0, cs, h->R, tiles, (float*)h->Mred);
       h->launches++;
       st = check_launch(h, "k_chunk_sum");
     }
@@ -1376,6 +1384,7 @@ cp_status phase1(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, int 
   if (wide_mode(h, n)) {  // update, table of the updated A^(n), the next batch (+ its zw rows and Gamma)
     const bool f64 = h->dtype == CP_F64;
     cp_status st = f64 ? launch_uw_t<double>(h, n, alpha, alpha_dev) : launch_uw_t<float>(h, n, alpha, alpha_dev);
+    if (sharded(h) && n == h->N - 1) return st;  // the rank's rows only: the table waits for the row exchange
     if (!st && next_mode >= 0) {
       st = launch_prefetch(h, next_mode);
       if (!st) h->pref_mode = next_mode;
@@ -1398,7 +1407,19 @@ cp_status phase1(cp_sgd_s* h, int n, double alpha, const double* alpha_dev, int 
 
 // table refresh of mode n when it could not be fused into phase 1 (rows gathered first / legacy)
 cp_status phase2(cp_sgd_s* h, int n, int next_mode) {
-  if (wide_mode(h, n)) return CP_OK;
+  if (wide_mode(h, n)) {
+    if (!(sharded(h) && n == h->N - 1)) return CP_OK;
+    // slab shards, last mode: the rows of every rank are in place -- the table of the whole A^(N-1) (a
+    // table-only k_update_wide taking over the factor from itself), then the next batch
+    const bool f64 = h->dtype == CP_F64;
+    cp_status st = f64 ? launch_uw_t<double>(h, n, 0.0, nullptr, h->one_dev, true)
+                       : launch_uw_t<float>(h, n, 0.0, nullptr, h->one_dev, true);
+    if (!st && next_mode >= 0) {
+      st = launch_prefetch(h, next_mode);
+      if (!st) h->pref_mode = next_mode;
+    }
+    return st;
+  }
   const bool last_sharded = sharded(h) && n == h->N - 1;
   if (ut_fits(h, h->In_local[n])) {
     if (!last_sharded) return CP_OK;
@@ -1425,6 +1446,10 @@ cp_status exchange_after0(cp_sgd_s* h, int n) {
   if (!sharded(h) || (h->flags & CP_FLAG_EXTERNAL_COMM) || n == h->N - 1) return CP_OK;
   ProfScope ps(h, kKComm);
   const int dt = h->dtype == CP_F64 ? kNcclFloat64 : kNcclFloat32;
+  if (wide_mode(h, n))  // the wide path's rank chunk sums (owned fibers only)
+    return nccl_check(h, g_nccl.AllReduce(h->Mred, h->Mred, (size_t)ceil_div(h->dims[n], kGUTI) * h->R * kGUTI, dt,
+                                          kNcclSum, h->comm, h->ls),
+                      "ncclAllReduce(M)");
   return nccl_check(h, g_nccl.AllReduce(h->Msum, h->Msum, (size_t)h->R * h->In_local[n], dt, kNcclSum, h->comm,
                                         h->ls),
                     "ncclAllReduce(M)");
@@ -1695,7 +1720,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
   }
   plan_fused(h);
   // ---- wide single-GPU path (k_gather_update) eligibility and buffers ----
-  if ((!multi(h) || replica(h)) && !(h->flags & CP_FLAG_NO_WIDE)) {
+  if (!(h->flags & CP_FLAG_NO_WIDE)) {  // single GPU, replicas, and slab shards (the last mode on the rank's rows)
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -1704,7 +1729,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
     h->use_tc = tc;
     int64_t mpart = 0;
     for (int n = 0; n < h->N; ++n) {
-      const int64_t nt = ceil_div(h->dims[n], kGUTI);
+      const int64_t nt = ceil_div(h->In_local[n], kGUTI);
       // chunks per I-tile: one wave of CTAs (tcgen05 kernel: one CTA per SM; FFMA kernel: two)
       const int64_t slots = tc ? 148 : 296;
       int64_t CK = std::max<int64_t>(1, std::min<int64_t>(slots / nt, 64));
@@ -1747,7 +1772,12 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
       for (int n = 0; n < h->N; ++n) ncl = std::max(ncl, ceil_div(ceil_div(h->bmax[n], kSWFibers), kSWCluster));
       ALLOC(h->sw_gcl, h->esz * ncl * h->R * h->R);
       ALLOC(h->Mpart, h->esz * mpart);
-      if (replica(h)) ALLOC(h->Mred, h->esz * ceil_div(Imax, kGUTI) * kGUTI * h->R);
+      if (multi(h)) ALLOC(h->Mred, h->esz * ceil_div(Imax, kGUTI) * kGUTI * h->R);
+      if (sharded(h)) {
+        ALLOC(h->one_dev, sizeof(int));
+        const int one = 1;
+        cudaMemcpy(h->one_dev, &one, sizeof(int), cudaMemcpyHostToDevice);
+      }
       if (replica(h) && (h->flags & CP_FLAG_P2P)) {
         h->p2p_msz = ceil_div(Imax, kGUTI) * kGUTI * h->R;
         const size_t bytes = kP2PHead + 2 * h->esz * (size_t)h->p2p_msz;
@@ -1926,6 +1956,7 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->gam_next);
   cudaFree(h->Mpart);
   cudaFree(h->Mred);
+  cudaFree(h->one_dev);
   for (void* q : h->peer_opened) cudaIpcCloseMemHandle(q);
   cudaFree(h->p2p_buf);
   cudaFree(h->p2p_epoch);
@@ -2089,7 +2120,7 @@ cp_status cp_sgd_exchange_info(cp_sgd_t h, int32_t mode, void** buf_dev, int64_t
                                int64_t* row_end) {
   cp_status st = check_mode(h, mode);
   if (st) return st;
-  if (replica(h)) {  // this rank's chunk sum of M, [tiles][R][128], to be summed over ranks
+  if (replica(h) || (sharded(h) && wide_mode(h, mode) && mode < h->N - 1)) {  // the rank's chunk sum of M, [tiles][R][128]
     if (buf_dev) *buf_dev = h->Mred;
     if (count) *count = ceil_div(h->dims[mode], kGUTI) * h->R * kGUTI;
     if (row_begin) *row_begin = 0;
@@ -2107,9 +2138,11 @@ cp_status cp_sgd_exchange_copy(cp_sgd_t h, int32_t mode, void* buf_dev, int32_t 
   cp_status st = check_mode(h, mode);
   if (st) return st;
   if (!buf_dev) return h->fail(CP_EINVAL, "NULL buffer");
-  void* lib = replica(h) ? h->Mred : h->Msum;
-  const size_t bytes = replica(h) ? h->esz * (size_t)(ceil_div(h->dims[mode], kGUTI) * h->R * kGUTI)
-                                  : h->esz * (size_t)h->R * (size_t)h->In_local[mode];
+  const bool red = replica(h) || (sharded(h) && wide_mode(h, mode) && mode < h->N - 1);
+  if (sharded(h) && mode == h->N - 1) return h->fail(CP_EINVAL, "the last mode has no M exchange (owned rows)");
+  void* lib = red ? h->Mred : h->Msum;
+  const size_t bytes = red ? h->esz * (size_t)(ceil_div(h->dims[mode], kGUTI) * h->R * kGUTI)
+                           : h->esz * (size_t)h->R * (size_t)h->In_local[mode];
   if (to_lib)
     CUDA_TRY(h, cudaMemcpyAsync(lib, buf_dev, bytes, cudaMemcpyDeviceToDevice, h->stream));
   else

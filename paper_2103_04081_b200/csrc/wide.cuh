@@ -86,6 +86,7 @@ struct UWParams {
   int* status;
   int64_t qch;        // last CTA's scan: q entries staged per round
   int table_only;     // 1: no step; take over the staged rows fstage (if *chg) and rebuild the table
+  int update_only;    // 1: the step of rows [0, In) of a row block (A, S, Gout offset by the caller), no table
   const T* fstage;
   const int* chg;
   long long* dbg;
@@ -636,7 +637,7 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
     cluster.sync();
   }
   WMARK(blockIdx.x == 0, 311);
-  if (p.strategy == 0) return;  // uniform tables are constant
+  if (p.strategy == 0 || p.update_only) return;  // uniform tables are constant; row blocks: no table here
   unsigned char* ext = uw_sm + uw_step_bytes(R, sizeof(T));
   {  // the last cluster: the inverse (leverage) / the Frobenius norm (Euclidean)
     __shared__ int s_last;
@@ -738,7 +739,9 @@ __global__ void __launch_bounds__(kWThreads, 1) k_sample_wide(SWParams P) {
 
   const int64_t b0 = cmin64((int64_t)blockIdx.x * kSWFibers, sp.bmax), b1 = cmin64(b0 + kSWFibers, sp.bmax);
   const int nf = (int)(b1 - b0);
-  if (sp.strategy == 3 || sp.strategy == 4) {
+  // block windows, stratified draws and slab shards (owned fibers, local offsets): the general draw_rows; the
+  // single-GPU row-wise case below draws the N-1 positions of a fiber in parallel
+  if (sp.strategy == 3 || sp.strategy == 4 || sp.strat_P > 1 || sp.ldims[N - 1] != sp.dims[N - 1] || sp.lo_last != 0) {
     draw_rows(sp, s_cp, r_now, b0, b1, tid, kWThreads, sidx, sw);
   } else {
     // row-wise draws (eq:ik, R8): one thread per (fiber, position) -- the N-1 draws of a fiber run

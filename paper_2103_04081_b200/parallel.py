@@ -107,10 +107,11 @@ class ShardedRunner:
     def _exchange_sum(self, n: int):
         import torch.distributed as dist
 
-        I_local = self.dims[n] if n < self.N - 1 else self.slabs[self.rank][1] - self.slabs[self.rank][0]
-        key = (n, I_local)
+        # the library's exchange-buffer size (the wide path: the rank's chunk sum, ceil(I_n/128) x R x 128)
+        count = self.h.exchange_count(n) if hasattr(self.h, "exchange_count") else self.R * self.dims[n]
+        key = (n, count)
         if key not in self._buf:
-            self._buf[key] = self.torch.empty(self.R * I_local, dtype=self.dtype, device=self.device)
+            self._buf[key] = self.torch.empty(count, dtype=self.dtype, device=self.device)
         buf = self._buf[key]
         self.h.exchange_copy(n, buf, False)
         self.sync()

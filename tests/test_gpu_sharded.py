@@ -47,7 +47,7 @@ def test_virtual_shards_match_single_gpu(strategy, P, mode_major):
         if n < N - 1:
             bufs = []
             for h in hs:
-                b = torch.empty(cfg.rank * dims[n], dtype=torch.float64, device=dev)
+                b = torch.empty(h.exchange_count(n), dtype=torch.float64, device=dev)
                 h.exchange_copy(n, b, False)
                 bufs.append(b)
             torch.cuda.synchronize()
@@ -153,7 +153,7 @@ def test_virtual_shards_stratified_match_oracle(strategy, P, balanced):
         if n < N - 1:
             bufs = []
             for h in hs:
-                b = torch.empty(cfg.rank * dims[n], dtype=torch.float64, device=dev)
+                b = torch.empty(h.exchange_count(n), dtype=torch.float64, device=dev)
                 h.exchange_copy(n, b, False)
                 bufs.append(b)
             torch.cuda.synchronize()

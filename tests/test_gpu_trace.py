@@ -113,6 +113,13 @@ def test_c3_full_size_one_step_per_mode():
         del Xd
 
 
+def exchange_rows(buf, I, R):
+    """the library's phase-0 exchange buffer of a wide-path rank ([ceil(I/128)][R][128]: its chunk sum of
+    M^T by 128-row tile) as the I x R matrix"""
+    t = (I + 127) // 128
+    return np.asarray(buf, np.float64).reshape(t, R, 128).transpose(1, 0, 2).reshape(R, t * 128)[:, :I].T
+
+
 def test_c5_slab_rank0_full_size():
     """C5 (4000^3 fp32 = 256 GB, R32, B8192, adaptive): rank 0 of the 8-way slab split run on one GPU -- its
     32 GB slab X[..., 0:500] (+ mode-major copies), an external-comm handle.  The global batch is bit-exact
@@ -143,7 +150,7 @@ def test_c5_slab_rank0_full_size():
     h.step_phase(0, 0)
     buf = torch.empty(h.exchange_count(0), dtype=torch.float32, device=dev)
     h.exchange_copy(0, buf, False)
-    M_g = buf.cpu().numpy().astype(np.float64).reshape(R, dims[0]).T
+    M_g = exchange_rows(buf.cpu().numpy(), dims[0], R)
     own = (idx_o[:, 1] >= lo) & (idx_o[:, 1] < hi)
     li = idx_o[own].copy()
     li[:, 1] -= lo
