@@ -238,6 +238,7 @@ struct cp_sgd_s {
   std::vector<int64_t> row_ranges;  // [2*world]: slab [lo, hi) of every rank
   void* Mred = nullptr;             // replicas / slab shards on the wide path: this rank's chunk sum of M, [tiles][R][128]
   int* one_dev = nullptr;           // a device 1 (table-only rebuild of the current factor)
+  int* chg_host = nullptr;          // pinned: cp_sgd_steps_host's per-mode 'host factor differs' flags
   // CP_FLAG_P2P: this rank's symmetric exchange buffer (flags + 2 parity copies), the peers' buffers
   void* p2p_buf = nullptr;
   int64_t p2p_msz = 0;
@@ -1957,6 +1958,7 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->Mpart);
   cudaFree(h->Mred);
   cudaFree(h->one_dev);
+  if (h->chg_host) cudaFreeHost(h->chg_host);
   for (void* q : h->peer_opened) cudaIpcCloseMemHandle(q);
   cudaFree(h->p2p_buf);
   cudaFree(h->p2p_epoch);
@@ -2316,7 +2318,13 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
       st = check_launch(h, "k_take_compare");
       if (st) return st;
     }
+    // the usual case (the host holds what the last call returned): nothing changed -- read the flags (one small
+    // copy + sync) and launch the take-over / table rebuild only for the modes that differ
+    if (!h->chg_host) CUDA_TRY(h, cudaMallocHost(&h->chg_host, sizeof(int) * kMaxOrder));
+    CUDA_TRY(h, cudaMemcpyAsync(h->chg_host, h->take_chg, sizeof(int) * h->N, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
     for (int k = 0; k < h->N; ++k) {
+      if (!h->chg_host[k]) continue;
       st = h->esz == 8 ? launch_uw_t<double>(h, k, 0.0, nullptr, h->take_chg + k)
                        : launch_uw_t<float>(h, k, 0.0, nullptr, h->take_chg + k);
       if (st) return st;

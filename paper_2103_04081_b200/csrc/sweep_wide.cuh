@@ -1347,9 +1347,14 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
     }
     // ---- S: the batch of mode n at r (from the coarse CDFs; pend: from its aggregates / raw q rows) ----
     pw_sample(p, n, r, sm, ss, bk, mk, pend);
-    // ---- the pending table's CDF rows, T and status (read from the next sampling phase on) ----
+    // ---- the pending table's CDF rows, T and status (read from the next sampling phase on): by the CTAs without
+    // sampling units when there are any (off the sampling phase's critical path), else by every CTA ----
     if (pend >= 0) {
-      for (int u = blockIdx.x; u < pw_units_rows(p.dims[pend]); u += G) pw_table_prefix(p, pend, u, pw_units_rows(p.dims[pend]), ss);
+      const int nsamp = min(pw_units_fib(p.bmax[n]), G);
+      const int c0 = nsamp < G ? nsamp : 0, nc = G - c0;
+      const int nup = pw_units_rows(p.dims[pend]);
+      if ((int)blockIdx.x >= c0)
+        for (int u = (int)blockIdx.x - c0; u < nup; u += nc) pw_table_prefix(p, pend, u, nup, ss);
       pend = -1;
     }
     PW_MARK(1);
