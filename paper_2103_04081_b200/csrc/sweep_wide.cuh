@@ -409,12 +409,14 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
       *reinterpret_cast<float4*>(p.zimg + (zimg_off(b0 + l0, 64 + rr) >> 2)) = make_float4(l[0], l[1], l[2], l[3]);
     }
     if (u == (int)blockIdx.x) PW_MK(23);
-    // Gamma partial of the unit: sum_b (w_b z_b) z_b^T (4x4 blocks bi <= bj, GG fiber groups), then
-    // added to the CTA's accumulator (unit order)
+    // Gamma partial of the unit: sum_b (w_b z_b) z_b^T over 4x4 blocks bi <= bj.  Large R (>= 64 blocks): one
+    // thread per block over all the unit's fibers, straight into the CTA's accumulator; small R: GG fiber groups
+    // per block (more threads busy), their partials summed in group order.  Unit order either way.
     {
       const int nblk = nb4 * (nb4 + 1) / 2;
+      const int GE = nblk >= 64 ? 1 : GG;
       const int g = tid / nblk, blk = tid % nblk;
-      if (g < GG) {
+      if (g < GE) {
         int bi = 0, rem = blk;
         while (rem >= nb4 - bi) { rem -= nb4 - bi; ++bi; }
         const int bj = bi + rem;
@@ -423,7 +425,7 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
         for (int a = 0; a < 4; ++a)
 #pragma unroll
           for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
-        for (int kk = g; kk < nf; kk += GG) {
+        for (int kk = g; kk < nf; kk += GE) {
           const float wk = (float)sw[kk];
           float x[4], y[4];
 #pragma unroll
@@ -442,19 +444,26 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
           for (int c = 0; c < 4; ++c) {
             const int r1 = 4 * bi + a, r2 = 4 * bj + c;
             if (r1 < R && r2 < R) {
-              red[(g * R + r1) * R + r2] = acc[a][c];
-              if (bi != bj) red[(g * R + r2) * R + r1] = acc[a][c];
+              if (GE == 1) {
+                gacc[r1 * R + r2] += acc[a][c];
+                if (bi != bj) gacc[r2 * R + r1] += acc[a][c];
+              } else {
+                red[(g * R + r1) * R + r2] = acc[a][c];
+                if (bi != bj) red[(g * R + r2) * R + r1] = acc[a][c];
+              }
             }
           }
       }
       __syncthreads();
       if (u == (int)blockIdx.x) PW_MK(24);
-      for (int e = tid; e < R * R; e += nth) {
-        float s = red[e];
-        for (int gg = 1; gg < GG; ++gg) s += red[gg * R * R + e];
-        gacc[e] += s;
+      if (GE > 1) {
+        for (int e = tid; e < R * R; e += nth) {
+          float s = red[e];
+          for (int gg = 1; gg < GE; ++gg) s += red[gg * R * R + e];
+          gacc[e] += s;
+        }
+        __syncthreads();
       }
-      __syncthreads();
     }
   }
   PW_MK(14);
