@@ -10,6 +10,8 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref
 timeout 300 python bench.py --workload C2 --no-cpu-baseline > $O/bench_c2.json 2> $O/bench_c2.err
 timeout 300 python bench.py --workload C3 --no-cpu-baseline > $O/bench_c3.json 2> $O/bench_c3.err
 timeout 600 python tools/pw_cta.py C4 > $O/cta_c4.txt 2>&1
+timeout 600 python tools/pw_ablate.py C4 > $O/sensitivity_c4.txt 2>&1
+timeout 600 python bench.py --workload C5 --slab-of 8 --steps 20 --warmup 3 > $O/bench_c5_slab8.json 2> $O/bench_c5_slab8.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c4.csv \
     python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-phases > $O/ncu_launch_c4.log 2>&1
 CPSGD_PW_NONCOOP=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_wide -s 1 -c 1 \
