@@ -685,195 +685,6 @@ static __device__ void pw_gather(const PWParams& p, int n, unsigned char* sm, PW
   }
 }
 
-// The gather with the fibers as the TMEM A operand (".ts" MMAs): loader warps 0-3 stream the sampled fiber
-// segments into a deep raw ring (16-byte cp.async, as pw_gather); warps 4-11 (two warpgroups, 16 fibers each)
-// read their TMEM lane's row i of the stage from the raw ring (conflict-free: consecutive lanes, consecutive
-// rows), split it into {xh, xl} (3xTF32) and store both with tcgen05.st into one of kPWTSSlots A slots; one
-// thread issues per 8-fiber K-step two M128 x N128 x K8 MMAs, xh . {zh; zl} and xl . {zh; zl}, accumulating
-// D = x . [w z]_hl in TMEM (the A images of the sampler are the shared-memory B operand).  The x operand never
-// makes a second trip through shared memory (pw_gather writes {xh; xl} back as the K-major B operand): per
-// 32-fiber stage ~80 KB of shared-memory traffic instead of ~128 KB.  Epilogue: warps 4-7 read their lane's row
-// of D and write M^T[r][i] = D[i][r] + D[i][64 + r] straight to the split-K partial tile.
-// Measured at C4 (kPWGatherTS): parity green, but the stream phase 12.9 vs 11.0 us per iteration of pw_gather and
-// insensitive to the MMA count, the fiber loads and the A images alike -- the transposers' TMEM store / wait::st
-// round trip per stage paces it; pw_gather stays the default.
-constexpr int kPWTSSlots = 3;                              // TMEM A slots (64 columns each: xh 32, xl 32)
-constexpr uint32_t kPWTSD = 0, kPWTSA = 256;               // TMEM columns: D [0, 128), A slots from 256
-__device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
-                                             uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-          taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-      : "memory");
-}
-__host__ __device__ inline int pw_ts_nx() {  // raw-ring stages of the .ts gather (200 KB less the A-image ring)
-  return (int)((200u * 1024u - kTCNZ * kTCZBytes) / kTCABytes);
-}
-
-static __device__ void pw_gather_ts(const PWParams& p, int n, unsigned char* sm, PWBars& B, uint32_t tmem, uint32_t& gs,
-                                    uint32_t& gi, long long* mk) {
-  constexpr int KS = kTCKS, NZ = kTCNZ, TI = kGUTI, NA = kPWTSSlots;
-  constexpr uint32_t A_BYTES = kTCABytes;
-  constexpr uint32_t IDESC = umma_idesc_tf32_mn(128, 128) & ~((1u << 15) | (1u << 16));
-  const int NX = pw_ts_nx();
-  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-  const int R = p.R;
-  const int64_t In = p.dims[n];
-  const int tiles = (int)((In + TI - 1) / TI), CK = p.CK[n];
-  const int64_t KB = p.KB[n], bmax = p.bmax[n];
-  const int nitems = tiles * CK;
-  const int nsamp = min(pw_units_fib(bmax), (int)gridDim.x);
-  const float* X = p.Xg[n];
-  const int64_t rowlen = p.rowlen[n];
-  unsigned char* xring = sm;
-  unsigned char* zring = xring + (size_t)NX * A_BYTES;
-  int64_t* sfb = reinterpret_cast<int64_t*>(zring + (size_t)NZ * kTCZBytes);
-  const int with_items = min(nitems, (int)gridDim.x);
-  const int gamma_stride = with_items * 31 + ((int)gridDim.x - with_items) * kPWThreads;
-  if ((int)blockIdx.x >= nitems) {
-    pw_gamma_sum(p, nsamp, with_items * 31 + ((int)blockIdx.x - nitems) * kPWThreads + tid, gamma_stride);
-    return;
-  }
-  bool first = true;
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int tile = item / CK, chunk = item % CK;
-    const int64_t i0 = (int64_t)tile * TI, c0 = (int64_t)chunk * KB;
-    const int nfib = (int)cmax64(0, cmin64(KB, bmax - c0));
-    const int nst = (nfib + KS - 1) / KS;
-    for (int64_t i = tid; i < nfib; i += kPWThreads) sfb[i] = __ldcg(p.fbase + c0 + i);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    if (mk && first && tid == 0) mk[25] = clock64();
-    if (wid < 4) {
-      // X loaders: 16-byte cp.async chunks of the sampled fiber segments (Alg. 5 TensorSamp)
-      for (int st = 0; st < nst; ++st) {
-        const uint32_t g = gs + st;
-        const int slot = (int)(g % (uint32_t)NX);
-        if (g >= (uint32_t)NX) mbar_wait(&B.xempty[slot], ((g / NX) - 1) & 1);
-        unsigned char* A = xring + slot * A_BYTES;
-        const int f0 = st * KS;
-#pragma unroll
-        for (int rep = 0; rep < KS * 32 / 128; ++rep) {
-          const int e = tid + 128 * rep;
-          const int kk = e >> 5, j = e & 31;
-          const int lb = f0 + kk;
-          const int64_t fbv = sfb[lb < nfib ? lb : 0];  // unconditional load, then select
-          const int64_t fb = lb < nfib ? fbv : -1;
-          const int64_t r0 = i0 + 4 * j;
-          if (fb >= 0 && r0 < rowlen && !(p.ablate & 2u)) cp_async16(A + kk * 512 + 16 * j, X + fb + r0, 16);
-        }
-        cp_async_mbar_arrive_noinc(&B.xfull[slot]);
-      }
-    } else if (wid <= 11) {
-      // transposers: TMEM lane i = 32 (warp % 4) + lane (row i of the tile), fibers [16 wg, 16 wg + 16)
-      const int wg = (wid - 4) >> 2, q = wid & 3;
-      const int i = 32 * q + lane;
-      const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
-      for (int st = 0; st < nst; ++st) {
-        const uint32_t g = gs + st;
-        const int slot = (int)(g % (uint32_t)NX), hb = (int)(g % NA);
-        mbar_wait(&B.xfull[slot], (g / NX) & 1);
-        if (mk && first && wid == 4 && lane == 0 && st == 0) mk[26] = clock64();
-        const float* A = reinterpret_cast<const float*>(xring + slot * A_BYTES);
-        const int f0 = st * KS + 16 * wg;
-        uint32_t hv[16], lv[16];
-#pragma unroll
-        for (int f = 0; f < 16; ++f) {  // load unconditionally (inside the ring), then select
-          const int lb = f0 + f;
-          const bool ok = lb < nfib && sfb[lb < nfib ? lb : 0] >= 0;
-          const float t = A[(16 * wg + f) * 128 + i];
-          const float x = ok ? t : 0.f;
-          const float h = tf32_trunc(x);
-          hv[f] = __float_as_uint(h);
-          lv[f] = __float_as_uint(x - h);
-        }
-        mbar_arrive(&B.xempty[slot]);
-        if (g >= (uint32_t)NA) mbar_wait(&B.mdone[hb], ((g / NA) - 1) & 1);  // the slot's MMAs retired
-        tmem_st16(tlane + kPWTSA + 64u * hb + 16u * wg, hv);
-        tmem_st16(tlane + kPWTSA + 64u * hb + 32u + 16u * wg, lv);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        mbar_arrive(&B.sdone[hb]);
-        if (mk && first && wid == 4 && lane == 0 && st == nst - 1) mk[27] = clock64();
-      }
-    } else if (wid == 12) {
-      if (lane != 0) {
-        if (first) pw_gamma_sum(p, nsamp, (int)blockIdx.x * 31 + lane - 1, gamma_stride);
-      } else {
-        for (int st = 0; st < nst; ++st) {
-          const uint32_t g = gs + st;
-          const int zs = g % NZ;
-          if (g >= (uint32_t)NZ) mbar_wait(&B.afree[zs], ((g / NZ) - 1) & 1);
-          const int64_t sb = (c0 + (int64_t)st * KS) / KS;
-          mbar_expect_tx(&B.afull[zs], kTCZBytes);
-          bulk_g2s(zring + zs * kTCZBytes, p.zimg + sb * (kTCZBytes / 4), kTCZBytes, &B.afull[zs]);
-        }
-      }
-    } else if (wid == 13 && lane == 0) {
-      const uint64_t dz = umma_desc_sw128(smem_u32(zring), 16, 1024);
-      for (int st = 0; st < nst; ++st) {
-        const uint32_t g = gs + st;
-        const int hb = (int)(g % NA), as = g % NZ;
-        mbar_wait(&B.sdone[hb], (g / NA) & 1);
-        mbar_wait(&B.afull[as], (g / NZ) & 1);
-        tc_fence_after();
-        const uint64_t b = dz + ((uint64_t)(as * kTCZBytes) >> 4);
-        const uint32_t ah = tmem + kPWTSA + 64u * hb, al = ah + 32u;
-#pragma unroll
-        for (int k = 0; k < KS / 8; ++k) {
-          umma_tf32_ts(tmem + kPWTSD, ah + 8u * k, b + 2 * k, IDESC, (st > 0 || k > 0) ? 1u : 0u);
-          if (!(p.ablate & 32u)) umma_tf32_ts(tmem + kPWTSD, al + 8u * k, b + 2 * k, IDESC, 1u);  // 32: timing only
-        }
-        umma_commit(&B.mdone[hb]);
-        umma_commit(&B.afree[as]);
-      }
-      if (nst > 0) umma_commit(&B.accf);
-    }
-    __syncthreads();
-    if (nst > 0) mbar_wait(&B.accf, gi & 1);
-    tc_fence_after();
-    if (mk && first && tid == 0) mk[28] = clock64();
-    // epilogue: warps 4-7, TMEM lane i = row i: M^T[r][i] = D[i][r] + D[i][64 + r] -> the split-K partial tile
-    if (wid >= 4 && wid <= 7) {
-      const int q = wid & 3, i = 32 * q + lane;
-      const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16) + kPWTSD;
-      const int nrow = (int)cmax64(0, cmin64(TI, In - i0));
-      float* part = p.Mpart + ((int64_t)tile * CK + chunk) * R * TI;
-#pragma unroll 1
-      for (int c = 0; c < R; c += 16) {
-        float v1[16], v2[16];
-        if (nst > 0) {
-          tmem_ld16(tlane + (uint32_t)c, v1);
-          tmem_ld16(tlane + 64u + (uint32_t)c, v2);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v1[j] = v2[j] = 0.f;
-        }
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (c + j < R && i < nrow) part[(c + j) * TI + i] = v1[j] + v2[j];
-      }
-    }
-    gs += nst;
-    if (nst > 0) ++gi;
-    if (mk && first && tid == 0) mk[29] = clock64();
-    first = false;
-    tc_fence_before();
-    __syncthreads();  // the ring / TMEM accumulator are reused by the next item
-    tc_fence_after();
-  }
-}
-
 // ------------------------------------------------------------------------------------------ phase U
 // rows [r0, r0 + nr) of A^(n): M (chunk order), G = A Gamma - M, update; leaves the new rows in sA
 // (stride R+1) and writes the unit's table partial
@@ -1288,16 +1099,15 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
   __shared__ int s_stop;
   if (wid == 13) {  // TMEM accumulator for the whole launch
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
-                 "r"(kPWGatherTS ? 512u : 256u));
+                 "r"(256));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    const int nx = kPWGatherTS ? pw_ts_nx() : kTCNX, np = kPWGatherTS ? kPWTSSlots : kTCPairs;
-    for (int s = 0; s < nx; ++s) {
+    for (int s = 0; s < kTCNX; ++s) {
       mbar_init(&B.xfull[s], 128);
       mbar_init(&B.xempty[s], 256);
     }
-    for (int s = 0; s < np; ++s) {
+    for (int s = 0; s < kTCPairs; ++s) {
       mbar_init(&B.sdone[s], 256);
       mbar_init(&B.mdone[s], 1);
     }
@@ -1370,8 +1180,7 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
     grid_barrier(p.bar, gen);
     PW_MARK(2);
     // ---- G: TensorSamp + tcgen05 contraction -> split-K partial tiles; Gamma sum ----
-    if (kPWGatherTS) pw_gather_ts(p, n, sm, B, tmem, gs, gi, mk);
-    else pw_gather(p, n, sm, B, tmem, gs, gi, mk);
+    pw_gather(p, n, sm, B, tmem, gs, gi, mk);
     PW_MARK(3);
     grid_barrier(p.bar, gen);
     PW_MARK(4);
@@ -1549,7 +1358,7 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
     for (int u = blockIdx.x; u < pw_units_rows(p.dims[pend]); u += G) pw_table_prefix(p, pend, u, pw_units_rows(p.dims[pend]), ss);
   }
   __syncthreads();
-  if (wid == 13) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kPWGatherTS ? 512u : 256u));
+  if (wid == 13) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
   if (blockIdx.x == 0 && tid == 0) {
     *p.iter = r;
     if (n_done >= 0) *p.last_mode = n_done;

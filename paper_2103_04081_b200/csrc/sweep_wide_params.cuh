@@ -10,7 +10,6 @@ namespace cps {
 constexpr int kPWThreads = kTCThreads;  // 448: the tcgen05 gather's warp roles
 constexpr int kPWFib = 32;              // fibers per sampling unit (one tcgen05 stage)
 constexpr int kPWRows = 16;             // rows per update / table unit
-constexpr bool kPWGatherTS = false;     // gather mainloop: fibers as the TMEM A operand (pw_gather_ts; measured slower, kept off)
 
 struct PWParams {
   int N, R, strategy, rule;

@@ -22,7 +22,7 @@ else:
 h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler="leverage", rule=cfg.rule, eta=cfg.eta, seed=1, fused=False)
 assert h.path == "persistent"
 # sensitivity experiments that keep the data path sane (results stay finite): doubled work, stale images
-MASKS = [(0, "full"), (0x120, "MMA twice / TS: no xl MMA"), (0x140, "split twice"),
+MASKS = [(0, "full"), (0x120, "MMA twice"), (0x140, "split twice"),
          (0x180, "no A-image copies (stale)"), (0x102, "no fiber loads"), (0, "full again")]
 if len(sys.argv) > 2 and sys.argv[2] == "destructive":  # garbage data: indicative only
     MASKS = [(0, "full"), (0x101, "no inverse"), (0x102, "no fiber loads"), (0x104, "no pair sums / Gram load"),
