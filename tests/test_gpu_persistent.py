@@ -39,6 +39,7 @@ PW_CASES = [
     ((260, 140, 96), 20, 512),      # C2-like rank and batch
     ((132, 70, 45), 48, 1000),      # R = 48, ragged batch (1000 = 31 units + 8); I_2 = 45 < 2R
     ((200, 64, 33, 20), 10, 1024),  # 4-way
+    ((2600, 40, 30), 16, 1024),     # I_0 > 148 x 16: CTAs with two row units (shared rows re-read, prefix loop)
 ]
 
 
@@ -148,3 +149,22 @@ def test_pw_degenerate_table_stops():
     with pytest.raises(CPError, match="ENONFINITE|EDEGENERATE"):
         h.sync()
     h.close()
+
+
+def test_pw_trace_two_units_per_cta():
+    """a mode with more row units than CTAs (2600 rows = 163 units on 148 CTAs) over three traced sweeps: the
+    second unit of a CTA re-reads its rows, the table prefix runs over several units per CTA"""
+    dims, R, B = (2600, 40, 30), 16, 1024
+    cfg = synth.small(dims, R, dtype="f32", batch=B, rule="adaptive", row_sigma=1.0, noise=1e-2, seed=12, eta=0.03)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "leverage", seed=13, fused=False, mode_major=True)
+    assert h.path == "persistent"
+    h.trace_start(9)
+    h.sweep(3)
+    recs = h.trace_read()
+    assert [r["n"] for r in recs] == [0, 1, 2] * 3
+    q0 = [t[1] for t in oracle_tables("leverage", A0)]
+    trace_check(X, dims, A0, recs, "leverage", B, 13, "adaptive", cfg, q0)
+    h.close()
+
