@@ -40,6 +40,7 @@ PW_CASES = [
     ((132, 70, 45), 48, 1000),      # R = 48, ragged batch (1000 = 31 units + 8); I_2 = 45 < 2R
     ((200, 64, 33, 20), 10, 1024),  # 4-way
     ((2600, 40, 30), 16, 1024),     # I_0 > 148 x 16: CTAs with two row units (shared rows re-read, prefix loop)
+    ((260, 140, 130), 64, 1024),    # R = 64 = kMaxRank (the RMAX = 64 sweep instance)
 ]
 
 
