@@ -290,7 +290,8 @@ cp_status cp_sgd_trace(cp_sgd_t h, void* buf_dev, int64_t cap);
 cp_status cp_sgd_trace_count(cp_sgd_t h, int64_t* n_host);
 
 /* 1 if the handle runs its sweeps / steps on a persistent kernel (k_sweep_fused: 1, k_sweep_wide: 2),
- * 0 for kernel chains */
+ * 0 for kernel chains (also after the device refused k_sweep_wide's cooperative launch because its grid could not
+ * be co-resident, e.g. with other work holding SMs: the handle then runs the same steps on the chain) */
 cp_status cp_sgd_path(cp_sgd_t h, int32_t* path_host);
 
 /* debug: clock64() phase timestamps of the last kernels (4096 kernel-specific entries, then the persistent

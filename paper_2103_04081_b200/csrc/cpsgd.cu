@@ -1324,7 +1324,16 @@ cp_status launch_pw(cp_sgd_s* h, int nsteps, int first_mode, int order, double a
   lc.attrs = at;
   lc.numAttrs = getenv("CPSGD_PW_NONCOOP") ? 0 : 1;  // profilers that cannot replay cooperative launches
   CUDA_TRY(h, cudaMemsetAsync(h->pw_bar, 0, sizeof(unsigned) * 128, h->ls));
-  cudaError_t e = cudaLaunchKernelEx(&lc, pw_kernel(h->R), p);
+  cudaError_t e = getenv("CPSGD_PW_FORCE_FALLBACK") ? cudaErrorCooperativeLaunchTooLarge
+                                                    : cudaLaunchKernelEx(&lc, pw_kernel(h->R), p);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {
+    // the grid cannot be co-resident right now (other work holds SMs, e.g. another process under MPS): this and
+    // every later call of the handle run the same steps on the kernel chain instead (cp_sgd_path reports it)
+    cudaGetLastError();
+    h->pw_ok = false;
+    h->pw_tag -= (uint32_t)nsteps;
+    return CP_OK;
+  }
   h->launches++;
   h->pref_mode = -1;
   if (e != cudaSuccess)
@@ -2080,9 +2089,11 @@ cp_status cp_sgd_step(cp_sgd_t h, int32_t mode, double alpha) {
     const double a = (alpha < 0.0) ? h->alpha : alpha;
     st = h->fused_cu ? launch_fused(h, 1, mode, 0, a, nullptr) : launch_pw(h, 1, mode, 0, a, nullptr, nullptr);
     if (st) return st;
-    h->iter_host++;
-    h->last_mode = mode;
-    return CP_OK;
+    if (h->fused_cu || h->pw_ok) {
+      h->iter_host++;
+      h->last_mode = mode;
+      return CP_OK;
+    }  // else: the persistent grid was not co-resident -- the chain
   }
   return step_direct(h, mode, alpha, (mode + 1) % h->N);  // prefetch guess: the cyclic successor
 }
@@ -2186,10 +2197,12 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
     }
     cp_status st = launch_pw(h, (int)nst, 0, order, h->alpha, nullptr, al);
     if (st) return st;
-    const uint64_t r_last = h->iter_host + nst - 1;
-    h->last_mode = order == CP_ORDER_CYCLIC ? h->N - 1 : random_mode(h->seed, r_last, h->N);
-    h->iter_host += nst;
-    return CP_OK;
+    if (h->pw_ok) {
+      const uint64_t r_last = h->iter_host + nst - 1;
+      h->last_mode = order == CP_ORDER_CYCLIC ? h->N - 1 : random_mode(h->seed, r_last, h->N);
+      h->iter_host += nst;
+      return CP_OK;
+    }  // else: not co-resident -- the chain below
   }
   const bool use_graph = order == CP_ORDER_CYCLIC && !alpha_per_iter && !(h->flags & CP_FLAG_NO_GRAPH) && !h->prof;
   if (!use_graph) {

@@ -169,3 +169,31 @@ def test_pw_trace_two_units_per_cta():
     trace_check(X, dims, A0, recs, "leverage", B, 13, "adaptive", cfg, q0)
     h.close()
 
+
+
+def test_pw_falls_back_to_the_chain_when_not_coresident(monkeypatch):
+    """a cooperative launch the device refuses (grid not co-resident, simulated by CPSGD_PW_FORCE_FALLBACK) runs the
+    same steps on the kernel chain: same batches, results within the fp32 tolerance of the persistent run"""
+    dims, R, B = (300, 130, 200), 20, 1024
+    cfg = synth.small(dims, R, dtype="f32", batch=B, rule="adaptive", row_sigma=1.0, noise=1e-2, seed=3, eta=0.03)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "leverage", seed=5, fused=False, mode_major=True)
+    assert h.path == "persistent"
+    h.sweep(2)
+    h.sync()
+    ref = [a.cpu().numpy().astype(np.float64) for a in Ad]
+    h.close()
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "leverage", seed=5, fused=False, mode_major=True)
+    monkeypatch.setenv("CPSGD_PW_FORCE_FALLBACK", "1")
+    h.sweep(1)
+    h.step(0)
+    h.step(1)
+    h.step(2)
+    h.sync()
+    monkeypatch.delenv("CPSGD_PW_FORCE_FALLBACK")
+    assert h.path == "chain" and h.iter == 6
+    for k in range(3):
+        assert rel_err(Ad[k].cpu().numpy(), ref[k], np.linalg.norm(ref[k])) <= 1e-3
+    h.close()
