@@ -394,6 +394,7 @@ def run_ours(args, cfg):
                 traffic = ent["bytes"] / ent.get("sweeps", 1) * (prof_sweeps if "sweeps" in ent else 1)
         return {"kernel": name, "bound": "hbm", "achieved": round(ach, 2), "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": traffic,
+                "frac_of_8TBs": round(ach / 8000.0, 4),  # also against the nominal ~8 TB/s
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "_fallback" not in peaks else "fallback",
                 "algorithmic_bytes_per_launch": per_launch}
 
@@ -501,6 +502,12 @@ def phase_profile(args, cfg, Xd, Ad, stream, fibers_per_iter, In_avg, esz, peaks
            ("barrier_U", 5, 6), ("gram_pairs", 6, 7), ("inverse_scores_scan", 7, 9), ("barrier_Q", 9, 10)]
     out = {k: round(float(np.mean([(d[s, b] - d[s, a]) / ghz / 1e3 for s in its])), 2) for k, a, b in seq}
     out["iteration_us"] = round(float(np.mean([(d[s, 10] - d[s, 0]) / ghz / 1e3 for s in its])), 2)
+    # BASELINE's "SGD steps/s per mode": iteration s of the launch updates mode s mod N (cyclic from 0)
+    per = {}
+    for s in its:
+        per.setdefault(s % cfg.order, []).append((d[s, 10] - d[s, 0]) / ghz / 1e3)
+    out["per_mode"] = {str(k): {"iteration_us": round(float(np.mean(v)), 2),
+                                "steps_per_s": round(1e6 / float(np.mean(v)), 1)} for k, v in sorted(per.items())}
     t_g = float(np.mean([(d[s, 4] - d[s, 2]) / ghz for s in its])) * 1e-9
     ach = fibers_per_iter * In_avg * esz / t_g / 1e9
     out["gather_roofline"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
