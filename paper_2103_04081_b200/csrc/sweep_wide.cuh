@@ -737,7 +737,7 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
   // dependent chains), their partials summed in group order
   {
     const int nbt = ((nr + 3) >> 2) * nb4;
-    const int KG = max(1, min(8, nth / max(1, nbt)));
+    const int KG = max(1, min(kPWUpdKG, nth / max(1, nbt)));
     const int kper = (R + KG - 1) / KG;
     float* redG = sgp_f;  // [KG][16][R]
     for (int t = tid; t < nbt * KG; t += nth) {

@@ -10,6 +10,7 @@ namespace cps {
 constexpr int kPWThreads = kTCThreads;  // 448: the tcgen05 gather's warp roles
 constexpr int kPWFib = 32;              // fibers per sampling unit (one tcgen05 stage)
 constexpr int kPWRows = 16;             // rows per update / table unit
+constexpr int kPWUpdKG = 8;             // k groups of the update's G = A Gamma - M (short chains vs. partial traffic)
 
 struct PWParams {
   int N, R, strategy, rule;
