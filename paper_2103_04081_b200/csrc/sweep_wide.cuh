@@ -233,19 +233,33 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
       const int ncb = (int)((p.dims[k] + kPWRows - 1) / kPWRows);
       uint64_t* co = cdfs + o;
       if (tid == 0) ss.coff[k] = o;
-      if (k == pend) {  // warp 0: inclusive scan of the aggregates (unit order; exact integers)
+      if (k == pend) {  // warp 0: inclusive scan of the aggregates (unit order; exact integers): every load of a
+                        // chunk of 256 units in flight at once (lane-owned runs of 8), then one warp scan
         if (tid < 32) {
           uint64_t carry = 0;
-          for (int u0 = 0; u0 < ncb; u0 += 32) {
-            const int u = u0 + tid;
-            uint64_t a = u < ncb ? __ldcg(p.agg + u) : 0ull;
+          for (int u0 = 0; u0 < ncb; u0 += 256) {
+            uint64_t a[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // clamped unconditional loads, then masked
+              const int u = u0 + 8 * tid + j;
+              const uint64_t t = __ldcg(p.agg + (u < ncb ? u : ncb - 1));
+              a[j] = u < ncb ? t : 0ull;
+            }
+#pragma unroll
+            for (int j = 1; j < 8; ++j) a[j] += a[j - 1];
+            uint64_t sc = a[7];
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-              const uint64_t t = __shfl_up_sync(0xffffffffu, a, d);
-              if (tid >= d) a += t;
+              const uint64_t t = __shfl_up_sync(0xffffffffu, sc, d);
+              if (tid >= d) sc += t;
             }
-            if (u < ncb) co[u] = carry + a;
-            carry += __shfl_sync(0xffffffffu, a, 31);
+            const uint64_t ex = carry + sc - a[7];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int u = u0 + 8 * tid + j;
+              if (u < ncb) co[u] = ex + a[j];
+            }
+            carry += __shfl_sync(0xffffffffu, sc, 31);
           }
           if (tid == 0) ss.T[k] = carry;
         }
@@ -374,18 +388,23 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
         ru[q] = e % RP;
         z[q] = (e < kPWFib * RP && lbu[q] < nf && ru[q] < R) ? 1.f : 0.f;
       }
-      for (int pos = 0; pos < NP; ++pos) {
-        const int k = pos < n ? pos : pos + 1;
+      // two modes per round (one L2 round trip for N = 3), products in ascending mode order
+      for (int pos = 0; pos < NP; pos += 2) {
+        const int pos2 = pos + 1 < NP ? pos + 1 : pos;
+        const int k = pos < n ? pos : pos + 1, k2 = pos2 < n ? pos2 : pos2 + 1;
         const float* F = p.factors[k];
-        float f[U];
+        const float* F2 = p.factors[k2];
+        float f[U], f2[U];
 #pragma unroll
         for (int q = 0; q < U; ++q) {  // every load issued (clamped address), then selected: no branch per load
           const int lb = lbu[q] < kPWFib ? lbu[q] : kPWFib - 1, rr = ru[q] < R ? ru[q] : R - 1;
           const float v = __ldcg(F + (int64_t)sidx[lb * NP + pos] * R + rr);
+          const float v2 = __ldcg(F2 + (int64_t)sidx[lb * NP + pos2] * R + rr);
           f[q] = z[q] != 0.f ? v : 0.f;
+          f2[q] = (z[q] != 0.f && pos2 != pos) ? v2 : 1.f;
         }
 #pragma unroll
-        for (int q = 0; q < U; ++q) z[q] = z[q] * f[q];
+        for (int q = 0; q < U; ++q) z[q] = (z[q] * f[q]) * f2[q];
       }
 #pragma unroll
       for (int q = 0; q < U; ++q)
@@ -425,18 +444,28 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
         for (int a = 0; a < 4; ++a)
 #pragma unroll
           for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
-        for (int kk = g; kk < nf; kk += GE) {
-          const float wk = (float)sw[kk];
-          float x[4], y[4];
+        // four fibers per round: every shared-memory load of the round issued before its FMAs (16-byte vectors:
+        // 4 ceil(R/4) <= RP, always inside the padded row); fibers past nf have zero rows and weight
+#pragma unroll 1
+        for (int k0 = g; k0 < nf; k0 += 4 * GE) {
+          float4 xv[4], yv[4];
+          float wk[4];
 #pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            x[a] = wk * zs[kk * RP + 4 * bi + a];  // 4 ceil(R/4) <= RP: always inside the padded row
-            y[a] = zs[kk * RP + 4 * bj + a];
+          for (int j = 0; j < 4; ++j) {
+            const int kk = min(k0 + j * GE, kPWFib - 1);
+            wk[j] = k0 + j * GE < nf ? (float)sw[kk] : 0.f;
+            xv[j] = *reinterpret_cast<const float4*>(zs + kk * RP + 4 * bi);
+            yv[j] = *reinterpret_cast<const float4*>(zs + kk * RP + 4 * bj);
           }
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
+          for (int j = 0; j < 4; ++j) {
+            const float x[4] = {wk[j] * xv[j].x, wk[j] * xv[j].y, wk[j] * xv[j].z, wk[j] * xv[j].w};
+            const float y[4] = {yv[j].x, yv[j].y, yv[j].z, yv[j].w};
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[a][c] = fmaf(x[a], y[c], acc[a][c]);
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) acc[a][c] = fmaf(x[a], y[c], acc[a][c]);
+          }
         }
 #pragma unroll
         for (int a = 0; a < 4; ++a)
