@@ -470,7 +470,42 @@ def run_ours(args, cfg):
     h.close()
     if res is not None and h_path == "persistent" and not args.no_phases:
         res["phases"] = phase_profile(args, cfg, Xd, Ad, stream, fibers_per_step / N, In_avg, esz, peaks)
+    if res is not None and ws == 1 and args.other_samplers:
+        res["other_samplers"] = other_samplers(args, cfg, Xd, Ad, stream, esz)
     return res
+
+
+def other_samplers(args, cfg, Xd, Ad, stream, esz):
+    """The same workload under the other sampling strategies (BASELINE configs[3]: "leverage-style and norm-style
+    strategies"): fibers/s and us per cyclic sweep on the device clock (CUDA events, one launch per call), from the
+    factors the headline run left.  Context next to the headline line, not a second headline."""
+    import torch
+
+    from paper_2103_04081_b200 import CPSGD
+
+    out = {}
+    K = max(5, min(args.steps, 100))
+    for smp in [s for s in args.other_samplers.split(",") if s and s != args.sampler]:
+        with torch.cuda.stream(stream):
+            h = CPSGD(Xd, cfg.dims, Ad, cfg.batch, sampler=smp, rule=cfg.rule, alpha=cfg.alpha, eta=cfg.eta,
+                      seed=cfg.seed, stream=stream, mode_major=not args.native_layout, fused=args.path == "auto",
+                      tc=not args.no_tc)
+        N = cfg.order
+        fps = sum(h.batch_max(n) for n in range(N)) if smp.startswith("block") else N * cfg.batch
+        h.sweep(max(3, args.warmup))
+        h.sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        h.sweep(K)
+        e1.record(stream)
+        stream.synchronize()
+        h.sync()
+        ms = e0.elapsed_time(e1)
+        out[smp] = {"value": round(fps * K / (ms / 1e3), 1), "unit": UNIT, "us_per_sweep": round(ms * 1e3 / K, 2),
+                    "sweeps": K, "path": h.path,
+                    "achieved_GBps": round(fps * K * (sum(cfg.dims) / N) * esz / (ms / 1e3) / 1e9, 2)}
+        h.close()
+    return out
 
 
 def phase_profile(args, cfg, Xd, Ad, stream, fibers_per_iter, In_avg, esz, peaks, sweeps=3):
@@ -590,6 +625,8 @@ def main():
                     choices=["uniform", "leverage", "euclidean", "block_leverage", "block_euclidean"])
     ap.add_argument("--native-layout", action="store_true", help="no mode-major copies")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--other-samplers", default="euclidean,uniform",
+                    help="comma list of strategies also timed on the same workload (N = 1; '' to skip)")
     ap.add_argument("--no-phases", action="store_true", help="skip the in-kernel phase timeline of the persistent kernel")
     ap.add_argument("--path", default="auto", choices=["auto", "wide"],
                     help="auto: persistent single-cluster kernel when the problem fits one cluster; wide: the "

@@ -5,7 +5,7 @@ cd "$(dirname "$0")/.."
 O=gpurun_out/r02
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
-timeout 600 python bench.py > $O/bench_c4.json 2> $O/bench_c4.err
+timeout 900 python bench.py > $O/bench_c4.json 2> $O/bench_c4.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
 timeout 300 python bench.py --workload C2 --no-cpu-baseline > $O/bench_c2.json 2> $O/bench_c2.err
 timeout 300 python bench.py --workload C3 --no-cpu-baseline > $O/bench_c3.json 2> $O/bench_c3.err
