@@ -1194,6 +1194,14 @@ int64_t units_max_of(const cp_sgd_s* h) {
 }
 // pw_kernel(R): k_pw.cu (its own translation unit)
 
+// SMs one handle's persistent / wide launches are planned for: the B200's 148, or CPSGD_SMS (read at init) so that
+// several handles can run their cooperative launches side by side on disjoint SMs (independent chains)
+int sm_budget() {
+  const char* e = getenv("CPSGD_SMS");
+  const int v = e ? atoi(e) : 148;
+  return v >= 8 && v <= 148 ? v : 148;
+}
+
 // eligible: one GPU, fp32 on the tcgen05 gather for every mode, gradient rules (the sampled-ALS rule
 // stays on the kernel chain), cooperative launch supported, one 448-thread CTA per SM co-resident
 bool plan_pw(cp_sgd_s* h) {
@@ -1223,7 +1231,7 @@ bool plan_pw(cp_sgd_s* h) {
     cudaGetLastError();
     return true;
   }
-  h->pw_grid = sms;  // one CTA per SM
+  h->pw_grid = std::min(sms, sm_budget());  // one CTA per SM (of the handle's SM budget)
   h->pw_smem = smem;
   const int P = h->R * (h->R + 1) / 2;
   auto alloc = [&](void** ptr, size_t bytes) {
@@ -1741,7 +1749,7 @@ cp_status cp_sgd_init(const cp_sgd_config* cfg, cp_sgd_t* out) {
     for (int n = 0; n < h->N; ++n) {
       const int64_t nt = ceil_div(h->In_local[n], kGUTI);
       // chunks per I-tile: one wave of CTAs (tcgen05 kernel: one CTA per SM; FFMA kernel: two)
-      const int64_t slots = tc ? 148 : 296;
+      const int64_t slots = tc ? sm_budget() : 2 * sm_budget();
       int64_t CK = std::max<int64_t>(1, std::min<int64_t>(slots / nt, 64));
       // replicas: P times as many chunks, every rank one wave of its own (chunks rank, rank + P, ...)
       if (replica(h)) CK *= h->world_size;

@@ -1321,7 +1321,13 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
           constexpr int EPT = (kMaxRank * kMaxRank + kPWThreads - 1) / kPWThreads;
           PW_MARK(19);
           constexpr int SG = kPWSweepGroups<RMAX>;
-          if (p.ablate & 1u) {
+          if (p.ablate & 1u) {  // timing experiment: no sweep; W = diag(1 / G_jj) (a valid table, no degenerate draws)
+            for (int e = tid; e < R * R; e += kPWThreads) {
+              const int r1 = e / R, r2 = e % R;
+              if (r1 != r2) Gm[r1 * RS + r2] = 0.0;
+            }
+            for (int j = tid; j < R; j += kPWThreads) Gm[j * RS + j] = 1.0 / Gm[j * RS + j];
+            __syncthreads();
             rank = R;
           } else if (In < 2 * R) {
             rank = cta_sweep_inverse_pivoted<EPT>(Gm, R, ss.tol, rowbuf, swept, diag);

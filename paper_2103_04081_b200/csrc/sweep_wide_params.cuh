@@ -61,7 +61,7 @@ struct PWParams {
   float* Gam_out;
   TraceParams tr;
   long long* dbg;
-  // timing experiments only (CPSGD_PW_ABLATE_MASK; results are garbage): 1 skip the sweep inverse, 2 skip the
+  // timing experiments only (CPSGD_PW_ABLATE_MASK; results are garbage): 1 skip the sweep inverse (W = diag(1 / G_jj)), 2 skip the
   // fiber loads of the gather, 4 skip the pair sums and the Gram load, 8 skip the update's Gram partials,
   // 16 skip the scores, 0x100 never stop on a bad status
   unsigned ablate;

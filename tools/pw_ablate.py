@@ -25,7 +25,7 @@ assert h.path == "persistent"
 MASKS = [(0, "full"), (0x120, "MMA twice"), (0x140, "split twice"),
          (0x180, "no A-image copies (stale)"), (0x102, "no fiber loads"), (0, "full again")]
 if len(sys.argv) > 2 and sys.argv[2] == "destructive":  # garbage data: indicative only
-    MASKS = [(0, "full"), (0x101, "no inverse"), (0x102, "no fiber loads"), (0x104, "no pair sums / Gram load"),
+    MASKS = [(0, "full"), (0x101, "no inverse (W = diag)"), (0x102, "no fiber loads"), (0x104, "no pair sums / Gram load"),
              (0x108, "no update Gram partials"), (0x110, "no scores"), (0x105, "no P + inverse"),
              (0x11f, "all of the above off")]
 for mask, what in MASKS:
