@@ -931,7 +931,40 @@ static __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nun
     // l_i = a_i^T W a_i: warp w takes rows 2w, 2w + 1; lane c holds columns c and c + 32 of y = W a
     // (W symmetric: W_kc read along a row of the inverse, consecutive lanes -> consecutive words), k split
     // into even / odd chains, then l = sum_c a_c y_c by a fixed xor-shuffle tree (deterministic)
-    if (wid < ((nr + 1) >> 1) && !(p.ablate & 16u)) {
+    if (R > 32 && !(p.ablate & 0x210u)) {
+      // R > 32 on fp64 tensor cores (mma.sync m8n8k4 f64): Y = A_u W as 8x8 tiles (rows 8 rb.., columns 8 cb..),
+      // one tile per warp, the k-steps chained in order; l_i = sum_c a_ic y_ic: per tile a quad xor-tree over
+      // its 8 columns, then the column blocks summed in order (deterministic)
+      __shared__ double s_part[kMaxRank / 8][kPWRows];
+      const int ncb = (R + 7) >> 3, gr = lane >> 2, gc = lane & 3;
+      for (int t = wid; t < 2 * ncb; t += nth >> 5) {
+        const int rb = t / ncb, cb = t % ncb;
+        const int col = 8 * cb + gr, colc = min(col, R - 1);
+        double y0 = 0.0, y1 = 0.0;
+        const double* arow = Ad + (8 * rb + gr) * RD;
+#pragma unroll 4
+        for (int k0 = 0; k0 < RD; k0 += 4) {
+          const int kr = k0 + gc, krc = min(kr, R - 1);
+          const double wv = Wm[krc * RS + colc];  // clamped unconditional load, then select
+          const double bv = (kr < R && col < R) ? wv : 0.0;
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(y0), "+d"(y1)
+                       : "d"(arow[k0 + gc]), "d"(bv));
+        }
+        // lane (gr, gc) holds y[8 rb + gr][8 cb + 2 gc + {0, 1}] (Ad is zero past R and past nr)
+        double part = arow[8 * cb + 2 * gc] * y0 + arow[8 * cb + 2 * gc + 1] * y1;
+        if (8 * cb + 2 * gc >= RD) part = 0.0;  // columns past the padded row (R > RD - 8)
+        part += __shfl_xor_sync(0xffffffffu, part, 1);
+        part += __shfl_xor_sync(0xffffffffu, part, 2);
+        if (gc == 0) s_part[cb][8 * rb + gr] = part;
+      }
+      __syncthreads();
+      if (tid < nr) {
+        double l = 0.0;
+        for (int cb = 0; cb < ncb; ++cb) l += s_part[cb][tid];
+        s_p[tid] = rank > 0 ? fmax(l, 0.0) / (double)rank : 0.0;
+      }
+    } else if (wid < ((nr + 1) >> 1) && !(p.ablate & 16u)) {
       const int il = 2 * wid;
       const double* a0 = Ad + il * RD;
       const double* a1 = a0 + RD;  // row il + 1 < 16: inside the buffer (zeros past nr)
