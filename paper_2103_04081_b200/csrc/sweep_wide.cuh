@@ -845,6 +845,32 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
       sAd[e] = (il < nr && c < R) ? (double)v : 0.0;
     }
     __syncthreads();
+    if (R > 32 && !(p.ablate & 0x200u)) {
+      // R > 32 on fp64 tensor cores (mma.sync m8n8k4 f64): the unit's Gram = sAd^T sAd as 8x8 tiles I <= J (one
+      // per warp, round robin), the 16 rows in four k-steps; stored straight into the packed pair partials
+      const int ncb = (R + 7) >> 3, ntile = ncb * (ncb + 1) / 2, lane = tid & 31, gr = lane >> 2, gc = lane & 3;
+      double* gp = p.gpart + unit;  // [P][gstride]: the pair sums read each pair's unit partials contiguously
+      for (int t = tid >> 5; t < ntile; t += nth >> 5) {
+        int I = 0, rem = t;
+        while (rem >= ncb - I) { rem -= ncb - I; ++I; }
+        const int J = I + rem;
+        const int ca = 8 * I + gr, cb = 8 * J + gr, cac = min(ca, R - 1), cbc = min(cb, R - 1);
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int k0 = 0; k0 < kPWRows; k0 += 4) {  // A[r][k] = sAd[k][8I + r], B[k][n] = sAd[k][8J + n]
+          const double av = sAd[(k0 + gc) * RD + cac], bv = sAd[(k0 + gc) * RD + cbc];  // clamped, then select
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(d0), "+d"(d1)
+                       : "d"(ca < R ? av : 0.0), "d"(cb < R ? bv : 0.0));
+        }
+        const int r1 = 8 * I + gr;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int r2 = 8 * J + 2 * gc + i;
+          if (r1 < R && r2 < R && r1 <= r2) gp[(int64_t)(r1 * R - r1 * (r1 - 1) / 2 + (r2 - r1)) * p.gstride] = i ? d1 : d0;
+        }
+      }
+    } else {
     for (int t = tid; t < nblk * RG; t += nth) {
       const int g = t / nblk, blk = t % nblk;
       int bi = 0, rem = blk;
@@ -880,6 +906,7 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
       double sum = 0.0;
       for (int g = 0; g < RG; ++g) sum += redP[g * P + e];
       gp[(int64_t)e * p.gstride] = sum;
+    }
     }
   } else if (p.strategy == 2 || p.strategy == 4) {  // Euclidean: row norms + the unit's partial ||A||^2
     double acc = 0.0;
