@@ -428,10 +428,38 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
       *reinterpret_cast<float4*>(p.zimg + (zimg_off(b0 + l0, 64 + rr) >> 2)) = make_float4(l[0], l[1], l[2], l[3]);
     }
     if (u == (int)blockIdx.x) PW_MK(23);
-    // Gamma partial of the unit: sum_b (w_b z_b) z_b^T over 4x4 blocks bi <= bj.  Large R (>= 64 blocks): one
-    // thread per block over all the unit's fibers, straight into the CTA's accumulator; small R: GG fiber groups
-    // per block (more threads busy), their partials summed in group order.  Unit order either way.
-    {
+    // Gamma partial of the unit: sum_b (w_b z_b) z_b^T.  R > 32: on fp64 tensor cores (mma.sync m8n8k4 f64), 8x8
+    // tiles I <= J one per warp, the unit's fibers in k-steps of 4 (products and sums in fp64: the fp32 operands
+    // and w_b are exact there), each tile rounded once into the CTA's fp32 accumulator (both triangles).
+    if (R > 32 && !(p.ablate & 0x200u)) {
+      const int ncb = (R + 7) >> 3, ntile = ncb * (ncb + 1) / 2, lane = tid & 31, gr = lane >> 2, gc = lane & 3;
+      for (int t = tid >> 5; t < ntile; t += nth >> 5) {
+        int I = 0, rem = t;
+        while (rem >= ncb - I) { rem -= ncb - I; ++I; }
+        const int J = I + rem;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int k0 = 0; k0 < kPWFib; k0 += 4) {  // zs rows past nf and columns past R are zero, sw past nf too
+          const int kk = k0 + gc;
+          const double av = sw[kk] * (double)zs[kk * RP + 8 * I + gr], bv = (double)zs[kk * RP + 8 * J + gr];
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(d0), "+d"(d1)
+                       : "d"(av), "d"(bv));
+        }
+        const int r1 = 8 * I + gr;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int r2 = 8 * J + 2 * gc + i;
+          if (r1 < R && r2 < R) {
+            const float v = (float)(i ? d1 : d0);
+            gacc[r1 * R + r2] += v;
+            if (I != J) gacc[r2 * R + r1] += v;
+          }
+        }
+      }
+      __syncthreads();
+      if (u == (int)blockIdx.x) PW_MK(24);
+    } else {
       const int nblk = nb4 * (nb4 + 1) / 2;
       const int GE = nblk >= 64 ? 1 : GG;
       const int g = tid / nblk, blk = tid % nblk;
@@ -762,9 +790,33 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
   if (bkw) pw_bulk_wait(*bkw);  // Gamma (first unit of the CTA)
   __syncthreads();
   PW_MK(15);
-  // G = A Gamma - M: task = (4 x 4 block of G, k group); KG groups split the R-long contraction (short
-  // dependent chains), their partials summed in group order
-  {
+  // G = A Gamma - M.  R > 32: on fp64 tensor cores (mma.sync m8n8k4 f64; 8x8 tiles of the 16 x R block, one per warp,
+  // the R-long contraction in k-steps of 4, the fp32 operands exact in fp64), G = (float)(A Gamma - M) rounded once,
+  // left in sM.  Else: task = (4 x 4 block of G, k group); KG groups split the R-long contraction (short dependent
+  // chains), their partials summed in group order
+  if (R > 32 && !(p.ablate & 0x200u)) {
+    const int ncb = (R + 7) >> 3, lane = tid & 31, gr = lane >> 2, gc = lane & 3;
+    const int kr4 = (R + 3) & ~3;
+    for (int t = tid >> 5; t < 2 * ncb; t += nth >> 5) {
+      const int rb = t / ncb, cb = t % ncb;
+      const int row = 8 * rb + gr, col = 8 * cb + gr, rowc = min(row, nr - 1), colc = min(col, R - 1);
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll 4
+      for (int k0 = 0; k0 < kr4; k0 += 4) {  // A[r][k] = sA[row][k], B[k][n] = Gamma[k][col]; clamped loads, then select
+        const int k = k0 + gc, kc = min(k, R - 1);
+        const float av = sA[rowc * AS + kc], bv = sG[kc * R + colc];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                     : "+d"(d0), "+d"(d1)
+                     : "d"((row < nr && k < R) ? (double)av : 0.0), "d"((k < R && col < R) ? (double)bv : 0.0));
+      }
+      const int c0 = 8 * cb + 2 * gc;
+      __syncwarp();
+      if (row < nr) {
+        if (c0 < R) sM[row * RS + c0] = (float)(d0 - (double)sM[row * RS + c0]);
+        if (c0 + 1 < R) sM[row * RS + c0 + 1] = (float)(d1 - (double)sM[row * RS + c0 + 1]);
+      }
+    }
+  } else {
     const int nbt = ((nr + 3) >> 2) * nb4;
     const int KG = max(1, min(kPWUpdKG, nth / max(1, nbt)));
     const int kper = (R + KG - 1) / KG;
