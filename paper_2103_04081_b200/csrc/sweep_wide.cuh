@@ -1219,6 +1219,184 @@ static __device__ void pw_trace(const PWParams& p, int s, int n, uint64_t r) {
     __syncwarp();                                                                                  \
   } while (0)
 
+// ------------------------------------------------------------------------------------------ inverse (R > 32)
+// The same symmetric sweep (natural pivot order, reading R4(b)) in 8-pivot blocks on fp64 tensor cores (mma.sync
+// m8n8k4 f64) with a look-ahead pivot warp.  The RMAX x RMAX matrix lives in DMMA accumulator fragments: the
+// upper-triangle 8x8 tiles round robin over warps 1..13 (the owners).  Warp 0 (the pivot warp) runs the serial
+// chain: it sweeps the 8x8 pivot block B_kb in registers (one pivot per step, shuffles), publishes -B_kb^-1, and
+// forms the NEXT pivot block itself, B_kb+1 = D - Q^T B_kb^-1 Q (Q: the published block row's next column block,
+// D: the next diagonal tile as published) with the same DMMA sequence the owners apply to that tile (bitwise the
+// same values), so it sweeps B_kb+1 while the owners form F = B^-1 M_P,: (one column block per warp, 2 DMMA) and
+// update their tiles (C -= M_:,P F, 2 DMMA; the pivot row / column blocks <- F / F^T, the pivot block <- -B^-1)
+// and publish the next block row.  Block operations = the sweep operator on the pivot block (Goodnight 1979), so
+// the result is the natural-order sweep's to rounding.  Returns |S| = R, or -1 when a pivot fails the single-pivot
+// rule (d > tol, checked per pivot inside the blocks): the caller then runs grp_sweep_inverse from the Gram.
+// Measured (tools/micro/dmma_la.cu, R = 50): 14.8k vs 18.2k cycles for the 2x2-pivot register sweep.
+struct PWInvBars {
+  uint64_t rows[kMaxRank / 8], binv[kMaxRank / 8];
+};
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__host__ __device__ constexpr size_t pw_dinv_bytes(int rmax) {  // Prow, Dd, Sw, Fb, scratch (doubles)
+  return sizeof(double) * ((size_t)(rmax / 8) * 8 * (rmax + 2) + 2 * (size_t)(rmax / 8) * 64 + 8 * (size_t)(rmax + 2) + 64);
+}
+template <int RMAX>
+__device__ int dmma_sweep_inverse(double* Gm, int R, double tol, double* buf, PWInvBars& bars, int* s_fail) {
+  constexpr int NB = RMAX / 8, NT = NB * (NB + 1) / 2, NO = kPWThreads / 32 - 1, TPW = (NT + NO - 1) / NO,
+                LD = RMAX + 2;
+  static_assert(RMAX % 8 == 0 && NB <= NO, "8x8 tiles");
+  double* Prow = buf;                   // [NB][8][LD] block row kb as published
+  double* Dd = Prow + NB * 8 * LD;      // [NB][64] diagonal tile kb + 1 as published with block row kb
+  double* Sw = Dd + NB * 64;            // [NB][64] -B_kb^-1
+  double* Fb = Sw + NB * 64;            // [8][LD] F of the current step
+  double* scr = Fb + 8 * LD;            // [64] the pivot warp's scratch
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, gr = lane >> 2, gc = lane & 3, RS = R + 1;
+  if (tid == 0) {
+    *s_fail = 0;
+    for (int k = 0; k < NB; ++k) {
+      mbar_init(&bars.rows[k], 32 * NO);
+      mbar_init(&bars.binv[k], 32);
+    }
+  }
+  int tI[TPW], tJ[TPW];
+  double c0[TPW], c1[TPW];
+#pragma unroll
+  for (int j = 0; j < TPW; ++j) {
+    const int t = (w - 1) + NO * j;
+    int I = 0, rem = t;
+    while (I < NB && rem >= NB - I) { rem -= NB - I; ++I; }
+    tI[j] = (w >= 1 && t < NT) ? I : -1;
+    tJ[j] = I + rem;
+    const int r = 8 * I + gr, c = 8 * tJ[j] + 2 * gc;
+    const int rc = min(r, R - 1), cc0 = min(c, R - 1), cc1 = min(c + 1, R - 1);
+    const double g0 = Gm[rc * RS + cc0], g1 = Gm[rc * RS + cc1];  // clamped, then select (identity past R)
+    c0[j] = tI[j] < 0 ? 0.0 : (r < R && c < R) ? g0 : (r == c ? 1.0 : 0.0);
+    c1[j] = tI[j] < 0 ? 0.0 : (r < R && c + 1 < R) ? g1 : (r == c + 1 ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  if (w == 0) {  // ---------------- the pivot warp
+    mbar_wait(&bars.rows[0], 0);
+    double b0 = Prow[gr * LD + 2 * gc], b1 = Prow[gr * LD + 2 * gc + 1];
+#pragma unroll 1
+    for (int kb = 0; kb < NB; ++kb) {
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // the pivot block's sweep, one pivot per step
+        const double d = __shfl_sync(0xffffffffu, (k & 1) ? b1 : b0, 4 * k + (k >> 1));
+        const double rk0 = __shfl_sync(0xffffffffu, b0, 4 * k + gc), rk1 = __shfl_sync(0xffffffffu, b1, 4 * k + gc);
+        const double ck = __shfl_sync(0xffffffffu, (k & 1) ? b1 : b0, 4 * gr + (k >> 1));
+        if (8 * kb + k < R && !(d > tol)) ok = false;
+        const double dinv = rcp_nr(d);
+        const double f = ck * dinv;
+        const bool pr = (gr == k);
+        const double n0 = pr ? rk0 * dinv : fma(-f, rk0, b0), n1 = pr ? rk1 * dinv : fma(-f, rk1, b1);
+        b0 = (2 * gc == k) ? (pr ? -dinv : f) : n0;
+        b1 = (2 * gc + 1 == k) ? (pr ? -dinv : f) : n1;
+      }
+      if (!ok && lane == 0) *s_fail = 1;
+      Sw[kb * 64 + gr * 8 + 2 * gc] = b0;
+      Sw[kb * 64 + gr * 8 + 2 * gc + 1] = b1;
+      mbar_arrive(&bars.binv[kb]);
+      if (!ok || kb + 1 == NB) break;
+      mbar_wait(&bars.rows[kb], 0);
+      const double* P = Prow + kb * 8 * LD;
+      const int J = kb + 1;
+      double f0 = 0.0, f1 = 0.0;
+      dmma_f64(f0, f1, -Sw[kb * 64 + gr * 8 + gc], P[gc * LD + 8 * J + gr]);
+      dmma_f64(f0, f1, -Sw[kb * 64 + gr * 8 + gc + 4], P[(gc + 4) * LD + 8 * J + gr]);
+      scr[gr * 8 + 2 * gc] = f0;
+      scr[gr * 8 + 2 * gc + 1] = f1;
+      __syncwarp();
+      double d0 = Dd[J * 64 + gr * 8 + 2 * gc], d1 = Dd[J * 64 + gr * 8 + 2 * gc + 1];
+      dmma_f64(d0, d1, -P[gc * LD + 8 * J + gr], scr[gc * 8 + gr]);
+      dmma_f64(d0, d1, -P[(gc + 4) * LD + 8 * J + gr], scr[(gc + 4) * 8 + gr]);
+      __syncwarp();
+      b0 = d0;
+      b1 = d1;
+    }
+  } else {  // ---------------- the owners
+#pragma unroll 1
+    for (int kb = 0; kb < NB; ++kb) {
+      double* P = Prow + kb * 8 * LD;
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {  // publish block row kb and the next diagonal tile
+        const int I = tI[j], J = tJ[j];
+        if (I < 0) continue;
+        if (I == kb) {
+          P[gr * LD + 8 * J + 2 * gc] = c0[j];
+          P[gr * LD + 8 * J + 2 * gc + 1] = c1[j];
+        } else if (J == kb) {
+          P[(2 * gc) * LD + 8 * I + gr] = c0[j];
+          P[(2 * gc + 1) * LD + 8 * I + gr] = c1[j];
+        }
+        if (I == kb + 1 && J == kb + 1) {
+          Dd[(kb + 1) * 64 + gr * 8 + 2 * gc] = c0[j];
+          Dd[(kb + 1) * 64 + gr * 8 + 2 * gc + 1] = c1[j];
+        }
+      }
+      mbar_arrive(&bars.rows[kb]);
+      mbar_wait(&bars.rows[kb], 0);
+      mbar_wait(&bars.binv[kb], 0);
+      if (*s_fail) break;
+      if (w <= NB) {  // F_J = B^-1 P[:, block J], J = w - 1
+        const int J = w - 1;
+        double f0 = 0.0, f1 = 0.0;
+        dmma_f64(f0, f1, -Sw[kb * 64 + gr * 8 + gc], P[gc * LD + 8 * J + gr]);
+        dmma_f64(f0, f1, -Sw[kb * 64 + gr * 8 + gc + 4], P[(gc + 4) * LD + 8 * J + gr]);
+        Fb[gr * LD + 8 * J + 2 * gc] = f0;
+        Fb[gr * LD + 8 * J + 2 * gc + 1] = f1;
+      }
+      named_bar_sync(2, 32 * NO);
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        const int I = tI[j], J = tJ[j];
+        if (I < 0) continue;
+        if (I == kb && J == kb) {
+          c0[j] = Sw[kb * 64 + gr * 8 + 2 * gc];
+          c1[j] = Sw[kb * 64 + gr * 8 + 2 * gc + 1];
+        } else if (I == kb) {
+          c0[j] = Fb[gr * LD + 8 * J + 2 * gc];
+          c1[j] = Fb[gr * LD + 8 * J + 2 * gc + 1];
+        } else if (J == kb) {  // (F_I)^T
+          c0[j] = Fb[(2 * gc) * LD + 8 * I + gr];
+          c1[j] = Fb[(2 * gc + 1) * LD + 8 * I + gr];
+        } else {
+          dmma_f64(c0[j], c1[j], -P[gc * LD + 8 * I + gr], Fb[gc * LD + 8 * J + gr]);
+          dmma_f64(c0[j], c1[j], -P[(gc + 4) * LD + 8 * I + gr], Fb[(gc + 4) * LD + 8 * J + gr]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const bool failed = *s_fail != 0;
+  if (tid == 0)
+    for (int k = 0; k < NB; ++k) {  // the barriers are initialised again by the next call
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars.rows[k])) : "memory");
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars.binv[k])) : "memory");
+    }
+  if (failed) return -1;
+  // W = -M on the first R rows / columns (both triangles from the upper tiles)
+#pragma unroll
+  for (int j = 0; j < TPW; ++j) {
+    const int I = tI[j], J = tJ[j];
+    if (I < 0) continue;
+    const int r = 8 * I + gr, c = 8 * J + 2 * gc;
+    if (r < R && c < R) {
+      Gm[r * RS + c] = -c0[j];
+      Gm[c * RS + r] = -c0[j];
+    }
+    if (r < R && c + 1 < R) {
+      Gm[r * RS + c + 1] = -c1[j];
+      Gm[(c + 1) * RS + r] = -c1[j];
+    }
+  }
+  __syncthreads();
+  return R;
+}
+
 // row groups of the sweep inverse per RMAX: as many as 448 threads hold (32 ceil(RMAX/32) lanes per
 // group, RMAX a multiple of 2 groups): fewer rows per thread shorten every pivot step
 template <int RMAX>
@@ -1238,6 +1416,8 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
   __shared__ uint32_t s_tmem;
   __shared__ uint64_t s_r0;
   __shared__ int s_stop;
+  __shared__ __align__(8) PWInvBars s_invb;  // dmma_sweep_inverse's barriers (initialised per call)
+  __shared__ int s_invfail;
   if (wid == 13) {  // TMEM accumulator for the whole launch
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
                  "r"(256));
@@ -1444,7 +1624,23 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
           } else if (In < 2 * R) {
             rank = cta_sweep_inverse_pivoted<EPT>(Gm, R, ss.tol, rowbuf, swept, diag);
           } else {
-            rank = grp_sweep_inverse<RMAX, SG>(Gm, R, ss.tol, rowbuf, swept);
+            rank = -1;
+            if (R > 32 && !(p.ablate & 0x200u)) {
+              double* dbuf = reinterpret_cast<double*>(
+                  sm + (offW + sizeof(double) * ((size_t)(R + kPWRows) * RD + 4 * (size_t)kPWRows * ((R + 3) / 4)) + 15) / 16 * 16);
+              rank = dmma_sweep_inverse<RMAX>(Gm, R, ss.tol, dbuf, s_invb, &s_invfail);
+              if (rank < 0) {  // a pivot failed the rule inside a block: the pivot-by-pivot sweep from the Gram again
+                for (int e = tid; e < R * R; e += kPWThreads) {
+                  const int r1 = e / R, r2 = e % R;
+                  const int a = r1 <= r2 ? r1 : r2, b = r1 <= r2 ? r2 : r1;
+                  Gm[r1 * RS + r2] = Wd[a * R - a * (a - 1) / 2 + (b - a)];
+                }
+                __syncthreads();
+              } else {
+                for (int j = tid; j < R; j += kPWThreads) swept[j] = 1;
+              }
+            }
+            if (rank < 0) rank = grp_sweep_inverse<RMAX, SG>(Gm, R, ss.tol, rowbuf, swept);
           }
           PW_MARK(20);
           bad0 = ss.bad | (rank == 0 ? 2 : 0);

@@ -63,7 +63,8 @@ struct PWParams {
   long long* dbg;
   // timing experiments only (CPSGD_PW_ABLATE_MASK; results are garbage): 1 skip the sweep inverse (W = diag(1 / G_jj)), 2 skip the
   // fiber loads of the gather, 4 skip the pair sums and the Gram load, 8 skip the update's Gram partials,
-  // 16 skip the scores, 0x100 never stop on a bad status
+  // 16 skip the scores, 0x100 never stop on a bad status, 0x200 the CUDA-core forms of the R > 32 tensor-core
+  // phases (scores, Gram partials, Gamma partials, G, inverse: timing comparison)
   unsigned ablate;
 };
 
@@ -79,9 +80,16 @@ __host__ __device__ inline size_t pw_other_bytes(int N, int R, int64_t cdf_elems
   const size_t scratch_g = sizeof(float) * 8 * kPWRows * (size_t)R;
   const size_t scratch_p = sizeof(double) * ((size_t)kPWRows * ut_rd(R) + 4 * (size_t)(R * (R + 1) / 2));
   const size_t upd = uw_step_bytes(R, 4) + 16 * 8 + (scratch_g > scratch_p ? scratch_g : scratch_p) + 64;
-  const size_t inv = sizeof(double) * ((size_t)R * (R + 1) + kSweepBuf + kMaxRank) + sizeof(int) * kMaxRank +
-                     sizeof(double) * ((size_t)R * ut_rd(R) + (size_t)kPWRows * ut_rd(R) + 4 * (size_t)kPWRows * ((R + 3) / 4)) +
-                     upd + 16 * 16;
+  // the inverse / table phases (k_sweep_wide's layout): Gm, the sweep buffer, diag and swept past the update's step
+  // area; W and the unit rows from offW; then the tensor-core inverse's buffers (dmma_sweep_inverse: block rows,
+  // diagonal tiles, -B^-1, F, scratch; RMAX of k_pw.cu)
+  const int rmax = R <= 16 ? 16 : R <= 32 ? 32 : R <= 56 ? 56 : 64;
+  const size_t dinv = sizeof(double) * ((size_t)(rmax / 8) * 8 * (rmax + 2) + 2 * (size_t)(rmax / 8) * 64 + 8 * (size_t)(rmax + 2) + 64);
+  const size_t offW = (uw_step_bytes(R, 4) + 256 + sizeof(double) * ((size_t)R * (R + 1) + kSweepBuf + kMaxRank) +
+                       sizeof(int) * kMaxRank + 16 + 15) / 16 * 16;
+  const size_t inv = (offW + sizeof(double) * ((size_t)(R + kPWRows) * ut_rd(R) + 4 * (size_t)kPWRows * ((R + 3) / 4)) + 15) / 16 * 16 +
+                     (R > 32 ? dinv : 0) + 64;
+  if (upd > inv) return sample > upd ? sample : upd;
   size_t m = sample > inv ? sample : inv;
   return m;
 }

@@ -109,6 +109,30 @@ def test_pw_trace_teacher_forced(strategy, rule):
     h.close()
 
 
+def test_pw_rank_deficient_factor_tables():
+    """Leverage tables of rank-deficient factors at R > 32 with I_n >= 2R (the tensor-core block inverse): a
+    duplicated column makes a pivot fail the single-pivot rule inside an 8-pivot block, the kernel re-runs the
+    pivot-by-pivot sweep from the Gram (reading R4(b): the pivot is skipped) and every rebuilt table equals the
+    oracle's (QR with column pivoting, numerical rank R - 1).  alpha = 0: the factors stay rank-deficient."""
+    dims, R, B = (152, 100, 90), 40, 512  # I_0 % 4 == 0: the persistent path gathers mode 0 in place
+    cfg = synth.small(dims, R, dtype="f32", batch=B, rule="fixed", row_sigma=1.0, noise=1e-2, seed=8, alpha=0.0)
+    X, A0 = make_problem(cfg)
+    for A in A0:
+        A[:, 21] = A[:, 6]  # inside the block of pivots 16..23: the second of the pair fails
+    Xd, Ad = to_dev(X, A0)
+    for strategy in ("leverage", "block_leverage"):
+        h = handle(cfg, Xd, Ad, strategy, seed=3, fused=False, mode_major=True)
+        assert h.path == "persistent"
+        h.trace_start(6)
+        h.sweep(2)
+        recs = h.trace_read()
+        q0 = [t[1] for t in oracle_tables(strategy, A0)]
+        trace_check(X, dims, A0, recs, strategy, B, 3, "fixed", cfg, q0)
+        for k in range(3):
+            assert np.array_equal(Ad[k].cpu().numpy(), A0[k])
+        h.close()
+
+
 def test_pw_random_order_and_schedule():
     """random mode order and a per-iteration fixed-step schedule in one launch."""
     dims, R, B = (200, 150, 100), 16, 1024
