@@ -2339,13 +2339,10 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
       st = check_launch(h, "k_take_compare");
       if (st) return st;
     }
-    // the usual case (the host holds what the last call returned): nothing changed -- read the flags (one small
-    // copy + sync) and launch the take-over / table rebuild only for the modes that differ
-    if (!h->chg_host) CUDA_TRY(h, cudaMallocHost(&h->chg_host, sizeof(int) * kMaxOrder));
-    CUDA_TRY(h, cudaMemcpyAsync(h->chg_host, h->take_chg, sizeof(int) * h->N, cudaMemcpyDeviceToHost, h->stream));
-    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    // the take-over / table rebuild of every mode, decided on the device: a mode whose flag is clear (the usual
+    // case: the host holds what the last call returned) leaves the kernel at once -- no host round trip between
+    // the copies in and the sweep
     for (int k = 0; k < h->N; ++k) {
-      if (!h->chg_host[k]) continue;
       st = h->esz == 8 ? launch_uw_t<double>(h, k, 0.0, nullptr, h->take_chg + k)
                        : launch_uw_t<float>(h, k, 0.0, nullptr, h->take_chg + k);
       if (st) return st;

@@ -19,3 +19,21 @@ h.profile(True)
 h.steps_host(0, len(cfg.dims), host)
 print(h.profile_read())
 h.profile(False)
+# the pieces on the device clock: pinned copies in / out, one sweep
+st = h.stream
+e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+for _ in range(3):
+    e[0].record(st)
+    with torch.cuda.stream(st):
+        for a, b in zip(Ad, host):
+            a.copy_(b, non_blocking=True)
+    e[1].record(st)
+    h.sweep(1)
+    e[2].record(st)
+    with torch.cuda.stream(st):
+        for a, b in zip(Ad, host):
+            b.copy_(a, non_blocking=True)
+    e[3].record(st)
+    torch.cuda.synchronize()
+    print(f"H2D {e[0].elapsed_time(e[1]) * 1e3:.1f} us, sweep {e[1].elapsed_time(e[2]) * 1e3:.1f} us, "
+          f"D2H {e[2].elapsed_time(e[3]) * 1e3:.1f} us")
