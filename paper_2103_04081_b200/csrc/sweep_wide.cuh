@@ -121,6 +121,10 @@ __host__ __device__ inline uint32_t pw_b16(int64_t bytes) { return (uint32_t)((b
 // ------------------------------------------------------------------------------------------ phase S
 struct PWShared {  // static shared state of the phases
   const uint64_t* cp[kMaxOrder];
+  // per-mode parameters the sampling phase indexes with run-time modes, staged once per phase (register-indexed
+  // constant-bank loads on the draw chain miss in the constant cache)
+  int64_t dims[kMaxOrder], lstride[kMaxOrder];
+  const float* fac[kMaxOrder];
   int64_t coff[kMaxOrder];         // offset of mode k's staged CDF in the shared CDF area
   uint64_t T[kMaxOrder];
   int32_t start[kMaxOrder], len[kMaxOrder];
@@ -138,6 +142,11 @@ struct PWShared {  // static shared state of the phases
     if (mk && threadIdx.x == 0) mk[slot] = clock64(); \
     __syncwarp();                                     \
   } while (0)
+// finer marks of thread 0 of CTA 0 (no warp sync; a second block of 32 slots per iteration: dbg[3072 + 32 s + slot])
+#define PW_MK2(slot)                                               \
+  do {                                                             \
+    if (mk && threadIdx.x == 0) mk[2560 + (slot)] = clock64();     \
+  } while (0)
 
 // Two-level CDF search (no staging of whole CDFs): coarse[j] = the inclusive CDF at the end of 16-row block j
 // (staged in shared memory), then the block's 16 entries straight from L2 -- the CDF rows of a mode, or, for the
@@ -146,7 +155,14 @@ struct PWShared {  // static shared state of the phases
 // Rows past I are padding of the 16-row allocations and are masked.
 __device__ __forceinline__ void pw_cdf_search(const uint64_t* src, bool pend, const uint64_t* coarse, int ncb,
                                               int64_t I, uint64_t r, int64_t& i, uint64_t& qk) {
-  int j = (int)upper_bound_u64(coarse, ncb, r);
+  // j = #{blocks whose inclusive end <= r}: a branch-free binary search with a fixed step count (every lane of a warp
+  // walks the same instruction stream: no divergence per step)
+  int j = 0;
+  for (int step = 1 << (31 - __clz(ncb)); step > 0; step >>= 1) {
+    const int c = j + step;
+    const uint64_t v = coarse[min(c, ncb) - 1];
+    j = (c <= ncb && v <= r) ? c : j;
+  }
   if (j >= ncb) j = ncb - 1;  // T = 0 (degenerate table, the status is set): keep the addresses valid
   const uint64_t cb = coarse[j > 0 ? j - 1 : 0];  // unconditional load, then select
   const uint64_t base = j > 0 ? cb : 0ull;
@@ -159,19 +175,16 @@ __device__ __forceinline__ void pw_cdf_search(const uint64_t* src, bool pend, co
     v[t] = x.x;
     v[t + 1] = x.y;
   }
+  // idx = #{t < cnt : CDF[lo + t] <= r} and q of row lo + idx, by selects only (the CDF is monotone)
   int idx = 0;
   uint64_t c = base, qsel = 0, prev = base;
 #pragma unroll
   for (int t = 0; t < kPWRows; ++t) {
     const uint64_t e = pend ? c + v[t] : v[t];  // the inclusive CDF at row lo + t
-    if (t < cnt) {
-      if (e <= r) {
-        idx = t + 1;
-        prev = e;
-      } else if (idx == t) {
-        qsel = e - prev;
-      }
-    }
+    const bool in = t < cnt, le = in && e <= r;
+    qsel = (in && !le && idx == t) ? e - prev : qsel;
+    prev = le ? e : prev;
+    idx = le ? t + 1 : idx;
     c = e;
   }
   if (idx >= cnt) {  // r beyond the table (T = 0): the last row, q of it
@@ -270,6 +283,12 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
       o += (ncb + 1) & ~1;
     }
     for (int e = tid; e < R * R; e += nth) gacc[e] = 0.f;
+    if (tid < N) {
+      ss.dims[tid] = p.dims[tid];
+      ss.lstride[tid] = p.lstride[tid];
+      ss.fac[tid] = p.factors[tid];
+      ss.cp[tid] = (tid == pend) ? p.qraw : p.cdf[tid];
+    }
   }
   __syncthreads();
   PW_MK(11);
@@ -311,11 +330,17 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
     const int nf = (int)cmin64(kPWFib, bmax - b0);
     if (!block) {
       // row-wise draws (eq:ik, R8): one thread per (fiber, position)
+      const bool m2 = u == (int)blockIdx.x;
+      if (m2) PW_MK2(0);
       for (int e = tid; e < nf * NP; e += nth) {
         const int lb = e / NP, pos = e % NP;
         const int k = pos < n ? pos : pos + 1;
         const uint64_t Tk = ss.T[k];
         const uint64_t rr = scale_draw(draw_word(p.seed, r, (uint32_t)(b0 + lb), kPurposeRow, (uint32_t)pos), Tk);
+        if (m2 && mk && e == 0) {  // timing marks of element 0 (stores wait for their operands: issue order)
+          ss.carry = rr;
+          PW_MK2(1);
+        }
         int64_t i;
         uint64_t qk;
         if (p.strategy == 0) {
@@ -323,13 +348,16 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
           qk = 1;
         } else {
           const bool pk = (k == pend);
-          pw_cdf_search(pk ? p.qraw : p.cdf[k], pk, cdfs + ss.coff[k], (int)((p.dims[k] + kPWRows - 1) / kPWRows),
-                        p.dims[k], rr, i, qk);
+          const int64_t Ik = ss.dims[k];
+          pw_cdf_search(ss.cp[k], pk, cdfs + ss.coff[k], (int)((Ik + kPWRows - 1) / kPWRows), Ik, rr, i, qk);
         }
         sidx[e] = (int32_t)i;
-        spt[e] = __ddiv_rn((double)((uint64_t)p.dims[k] * qk), (double)Tk);
+        if (m2 && e == 0) PW_MK2(2);
+        spt[e] = __ddiv_rn((double)((uint64_t)ss.dims[k] * qk), (double)Tk);
+        if (m2 && e == 0) PW_MK2(3);
       }
       __syncthreads();
+      if (m2) PW_MK2(4);
     }
     // per fiber: the exact weight (DESIGN.md section 4 order), indices, offset
     for (int lb = tid; lb < kPWFib; lb += nth) {
@@ -367,9 +395,9 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
         const int64_t ik = sidx[lb * NP + pos];
         p.idx[b * NP + pos] = (int32_t)ik;
         ++pos;
-        offn += ik * p.lstride[k];
+        offn += ik * ss.lstride[k];
         jrow += ik * jmul;
-        jmul *= p.dims[k];
+        jmul *= ss.dims[k];
       }
       p.fbase[b] = p.pitch[n] ? jrow * p.pitch[n] : offn;
     }
@@ -392,8 +420,8 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
       for (int pos = 0; pos < NP; pos += 2) {
         const int pos2 = pos + 1 < NP ? pos + 1 : pos;
         const int k = pos < n ? pos : pos + 1, k2 = pos2 < n ? pos2 : pos2 + 1;
-        const float* F = p.factors[k];
-        const float* F2 = p.factors[k2];
+        const float* F = ss.fac[k];
+        const float* F2 = ss.fac[k2];
         float f[U], f2[U];
 #pragma unroll
         for (int q = 0; q < U; ++q) {  // every load issued (clamped address), then selected: no branch per load

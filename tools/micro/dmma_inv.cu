@@ -69,55 +69,42 @@ __global__ void __launch_bounds__(kThreads, 1) kinv(const double* G, int R, doub
     }
     __syncthreads();
     long long ta = clock64();
-    if (w < NB) {
+    if (w == 0) {
       // the 8x8 pivot block B = P[:, 8kb..]: lane (gr, gc) holds B[gr][2gc], B[gr][2gc+1]; natural-order sweep
       double b0 = P[gr * LD + 8 * kb + 2 * gc], b1 = P[gr * LD + 8 * kb + 2 * gc + 1];
       bool bad = false;
-      // 2x2 sub-pivots {k, k+1}: Bp = [[a, b], [b, c]], one reciprocal of det per pair (the single-pivot skip rule:
-      // a > tol and det > tol a); lane (gr, gc) holds columns 2gc, 2gc+1 -- the pair's columns are lane 4r + k/2's
 #pragma unroll
-      for (int k = 0; k < (TIMING_ONE_WARP && w > 0 ? 0 : 8); k += 2) {
+      for (int k = 0; k < 8; k += 2) {
         const int h = k >> 1;
         const double rk0 = __shfl_sync(0xffffffffu, b0, 4 * k + gc), rk1 = __shfl_sync(0xffffffffu, b1, 4 * k + gc);
         const double rl0 = __shfl_sync(0xffffffffu, b0, 4 * (k + 1) + gc), rl1 = __shfl_sync(0xffffffffu, b1, 4 * (k + 1) + gc);
-        const double mk = __shfl_sync(0xffffffffu, b0, 4 * gr + h), ml = __shfl_sync(0xffffffffu, b1, 4 * gr + h);  // M_rk, M_rl
+        const double mk = __shfl_sync(0xffffffffu, b0, 4 * gr + h), ml = __shfl_sync(0xffffffffu, b1, 4 * gr + h);
         const double a = __shfl_sync(0xffffffffu, b0, 4 * k + h), bb = __shfl_sync(0xffffffffu, b1, 4 * k + h);
         const double cc = __shfl_sync(0xffffffffu, b1, 4 * (k + 1) + h);
         const double det = fma(a, cc, -bb * bb);
         if (8 * kb + k < R && !(a > tol && det > tol * a)) bad = true;
         const double dinv = rcp_nr(det);
-        // row coefficients g = [M_rk, M_rl] Bp^-1 (for rows r not in the pair); pivot rows: Bp^-1 [M_kc; M_lc]
         const double g1 = fma(cc, mk, -bb * ml) * dinv, g2 = fma(a, ml, -bb * mk) * dinv;
         const bool pr = (gr == k || gr == k + 1);
-        auto upd = [&](double m, double rkv, double rlv, int col) {
-          // col in the pair: pivot column -> (r in pair: -Bp^-1 entry; else g); else: r in pair -> Bp^-1 [rk; rl], else m - g.[rk; rl]
-          if (col == k || col == k + 1) {
-            if (pr) {
-              const double e = (gr == col) ? ((col == k) ? cc : a) : -bb;  // adj entry
-              return -e * dinv;
-            }
-            return (col == k) ? g1 : g2;
-          }
-          if (pr) return (gr == k) ? fma(cc, rkv, -bb * rlv) * dinv : fma(a, rlv, -bb * rkv) * dinv;
-          return fma(-g1, rkv, fma(-g2, rlv, m));
-        };
-        const double n0 = upd(b0, rk0, rl0, 2 * gc), n1 = upd(b1, rk1, rl1, 2 * gc + 1);
-        b0 = n0;
-        b1 = n1;
+        // select-free: pivot-row values, pivot-column values, general values, then one select per entry
+        const double adj0 = (gr == 2 * gc) ? ((2 * gc == k) ? cc : a) : -bb;
+        const double adj1 = (gr == 2 * gc + 1) ? ((2 * gc + 1 == k) ? cc : a) : -bb;
+        const double prow0 = (gr == k) ? fma(cc, rk0, -bb * rl0) * dinv : fma(a, rl0, -bb * rk0) * dinv;
+        const double prow1 = (gr == k) ? fma(cc, rk1, -bb * rl1) * dinv : fma(a, rl1, -bb * rk1) * dinv;
+        const double gen0 = fma(-g1, rk0, fma(-g2, rl0, b0)), gen1 = fma(-g1, rk1, fma(-g2, rl1, b1));
+        const bool pc0 = (2 * gc == k || 2 * gc == k + 1), pc1 = (2 * gc + 1 == k || 2 * gc + 1 == k + 1);
+        b0 = pc0 ? (pr ? -adj0 * dinv : (2 * gc == k ? g1 : g2)) : (pr ? prow0 : gen0);
+        b1 = pc1 ? (pr ? -adj1 * dinv : (2 * gc + 1 == k ? g1 : g2)) : (pr ? prow1 : gen1);
       }
       if (bad && lane == 0) s_fail = 1;
+      NB_[gr * 8 + 2 * gc] = b0;  // -B^-1
+      NB_[gr * 8 + 2 * gc + 1] = b1;
       if (tid == 0) tacc[0] += clock64() - ta;
-      // B^-1 = -sweep(B): A-fragment layout for F = B^-1 P (row-major a[gr][gc + 4h]) via a shuffle
-      // lane (gr, gc) holds (-b0, -b1) = B^-1[gr][2gc], [gr][2gc+1]; needs B^-1[gr][gc] and B^-1[gr][gc + 4]
-      // (the source lane cannot select by the requester's gc: fetch both components, select here)
-      const double x0 = __shfl_sync(0xffffffffu, b0, 4 * gr + (gc >> 1)), x1 = __shfl_sync(0xffffffffu, b1, 4 * gr + (gc >> 1));
-      const double y0 = __shfl_sync(0xffffffffu, b0, 4 * gr + 2 + (gc >> 1)), y1 = __shfl_sync(0xffffffffu, b1, 4 * gr + 2 + (gc >> 1));
-      const double a_lo = -((gc & 1) ? x1 : x0), a_hi = -((gc & 1) ? y1 : y0);
-      if (w == 0) {
-        NB_[gr * 8 + 2 * gc] = b0;
-        NB_[gr * 8 + 2 * gc + 1] = b1;
-      }
-      // F_J for J = w: B operand b[k = gc + 4h][n = gr] = P[gc + 4h][8J + gr]
+    }
+    __syncthreads();
+    if (w < NB) {
+      // F_J for J = w: A = B^-1 row-major a[gr][gc + 4h], B operand b[k = gc + 4h][n = gr] = P[gc + 4h][8J + gr]
+      const double a_lo = -NB_[gr * 8 + gc], a_hi = -NB_[gr * 8 + gc + 4];
       const int J = w;
       double f0 = 0.0, f1 = 0.0;
       dmma(f0, f1, a_lo, P[gc * LD + 8 * J + gr]);
