@@ -205,10 +205,13 @@ __device__ __forceinline__ uint64_t pw_cdf_at(const uint64_t* src, bool pend, co
   return c;
 }
 
+// NT: the tensor order as a compile-time constant (3: the benchmark shapes -- position loops unrolled, no run-time
+// division by N - 1 on the draw chain) or 0 (any order up to kMaxOrder)
+template <int NT>
 static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned char* sm, PWShared& ss, PWBulk& bk,
                                  long long* mk, int pend) {
   const int tid = threadIdx.x, nth = blockDim.x;
-  const int N = p.N, NP = N - 1, R = p.R, RP = zg_rp(R), nb4 = (R + 3) >> 2;
+  const int N = NT > 0 ? NT : p.N, NP = N - 1, R = p.R, RP = zg_rp(R), nb4 = (R + 3) >> 2;
   const bool block = (p.strategy == 3 || p.strategy == 4);
   const int64_t bmax = p.bmax[n];
   const int nunits = pw_units_fib(bmax);
@@ -1139,11 +1142,14 @@ static __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nun
   PW_MK(21);
   // the unit's raw q rows (into its CDF rows, converted by pw_table_prefix), aggregate and bad bits:
   // plain stores, published for the whole CTA by one release on the arrival counter (kernel)
-  if (tid < nr) p.qraw[r0 + tid] = s_q[tid];
+  if (tid < 32) {  // warp 0: raw q rows, the unit aggregate by a xor tree (exact integers: any order)
+    unsigned long long a = tid < nr ? s_q[tid] : 0ull;
+    if (tid < nr) p.qraw[r0 + tid] = a;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (tid == 0) p.agg[unit] = a;
+  }
   if (tid == 0) {
-    unsigned long long a = 0;
-    for (int i = 0; i < nr; ++i) a += s_q[i];
-    p.agg[unit] = a;
     p.aggf[2 * unit] = (unsigned)s_badu;
     // a bad table is visible to every CTA as soon as the arrivals are (the launch stops before drawing from it)
     if (s_badu) atomicCAS(p.status, 0, (s_badu & 8) ? -8 : -3);
@@ -1514,7 +1520,8 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
       if (s_stop) break;
     }
     // ---- S: the batch of mode n at r (from the coarse CDFs; pend: from its aggregates / raw q rows) ----
-    pw_sample(p, n, r, sm, ss, bk, mk, pend);
+    if (N == 3) pw_sample<3>(p, n, r, sm, ss, bk, mk, pend);
+    else pw_sample<0>(p, n, r, sm, ss, bk, mk, pend);
     // ---- the pending table's CDF rows, T and status (read from the next sampling phase on): by the CTAs without
     // sampling units when there are any (off the sampling phase's critical path), else by every CTA ----
     if (pend >= 0) {
