@@ -1278,7 +1278,8 @@ __host__ __device__ constexpr size_t pw_dinv_bytes(int rmax) {  // Prow, Dd, Sw,
   return sizeof(double) * ((size_t)(rmax / 8) * 8 * (rmax + 2) + 2 * (size_t)(rmax / 8) * 64 + 8 * (size_t)(rmax + 2) + 64);
 }
 template <int RMAX>
-__device__ int dmma_sweep_inverse(double* Gm, int R, double tol, double* buf, PWInvBars& bars, int* s_fail) {
+__device__ int dmma_sweep_inverse(double* Gm, const double* gpk, int R, double tol, double* buf, PWInvBars& bars,
+                                  int* s_fail) {
   constexpr int NB = RMAX / 8, NT = NB * (NB + 1) / 2, NO = kPWThreads / 32 - 1, TPW = (NT + NO - 1) / NO,
                 LD = RMAX + 2;
   static_assert(RMAX % 8 == 0 && NB <= NO, "8x8 tiles");
@@ -1306,7 +1307,10 @@ __device__ int dmma_sweep_inverse(double* Gm, int R, double tol, double* buf, PW
     tJ[j] = I + rem;
     const int r = 8 * I + gr, c = 8 * tJ[j] + 2 * gc;
     const int rc = min(r, R - 1), cc0 = min(c, R - 1), cc1 = min(c + 1, R - 1);
-    const double g0 = Gm[rc * RS + cc0], g1 = Gm[rc * RS + cc1];  // clamped, then select (identity past R)
+    // the packed upper triangle (row a <= column b at a R - a (a - 1) / 2 + b - a); clamped, then select (identity
+    // past R)
+    auto pk = [&](int a, int b) { return gpk[(a <= b) ? a * R - a * (a - 1) / 2 + (b - a) : b * R - b * (b - 1) / 2 + (a - b)]; };
+    const double g0 = pk(rc, cc0), g1 = pk(rc, cc1);
     c0[j] = tI[j] < 0 ? 0.0 : (r < R && c < R) ? g0 : (r == c ? 1.0 : 0.0);
     c1[j] = tI[j] < 0 ? 0.0 : (r < R && c + 1 < R) ? g1 : (r == c + 1 ? 1.0 : 0.0);
   }
@@ -1609,6 +1613,8 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
         double* Ad = Wd + R * RD;
         int rank = 0, bad0 = 0;
         double fro = 0.0;
+        // the tensor-core block inverse (R > 32, I_n >= 2R): its tiles straight from the packed Gram
+        const bool dpath = R > 32 && In >= 2 * R && !(p.ablate & 0x201u);
         if (lev) {
           if (tid == 0 && !(p.ablate & 4u)) wait_count(p.pcnt, (unsigned)G * (unsigned)(s + 1));
           __syncthreads();
@@ -1620,11 +1626,12 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
               bulk_g2s(gst, p.gram, pw_b16((int64_t)P * 8), bk.bar);
             }
             if (!(p.ablate & 4u)) pw_bulk_wait(bk);
-            for (int e = tid; e < R * R; e += kPWThreads) {
-              const int r1 = e / R, r2 = e % R;
-              const int a = r1 <= r2 ? r1 : r2, b = r1 <= r2 ? r2 : r1;
-              Gm[r1 * RS + r2] = gst[a * R - a * (a - 1) / 2 + (b - a)];
-            }
+            if (!dpath)  // the tensor-core inverse reads its tiles from the packed Gram itself
+              for (int e = tid; e < R * R; e += kPWThreads) {
+                const int r1 = e / R, r2 = e % R;
+                const int a = r1 <= r2 ? r1 : r2, b = r1 <= r2 ? r2 : r1;
+                Gm[r1 * RS + r2] = gst[a * R - a * (a - 1) / 2 + (b - a)];
+              }
           }
           __syncthreads();
           if (tid < 32) {
@@ -1632,7 +1639,7 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
             double d0 = 0.0;
             bool fin = true;
             for (int j = lane; j < R; j += 32) {
-              const double d = Gm[j * RS + j];
+              const double d = Wd[j * R - j * (j - 1) / 2];  // the packed diagonal
               d0 = fmax(d0, d);
               fin = fin && (d == d) && d < 1.7e308;
             }
@@ -1660,10 +1667,10 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
             rank = cta_sweep_inverse_pivoted<EPT>(Gm, R, ss.tol, rowbuf, swept, diag);
           } else {
             rank = -1;
-            if (R > 32 && !(p.ablate & 0x200u)) {
+            if (dpath) {
               double* dbuf = reinterpret_cast<double*>(
                   sm + (offW + sizeof(double) * ((size_t)(R + kPWRows) * RD + 4 * (size_t)kPWRows * ((R + 3) / 4)) + 15) / 16 * 16);
-              rank = dmma_sweep_inverse<RMAX>(Gm, R, ss.tol, dbuf, s_invb, &s_invfail);
+              rank = dmma_sweep_inverse<RMAX>(Gm, Wd, R, ss.tol, dbuf, s_invb, &s_invfail);
               if (rank < 0) {  // a pivot failed the rule inside a block: the pivot-by-pivot sweep from the Gram again
                 for (int e = tid; e < R * R; e += kPWThreads) {
                   const int r1 = e / R, r2 = e % R;
