@@ -1521,6 +1521,7 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
         s_stop = __ldcg(p.status) != 0 && !(p.ablate & 0x100u);
       }
       __syncthreads();
+      PW_MK2(6);
       if (s_stop) break;
     }
     // ---- S: the batch of mode n at r (from the coarse CDFs; pend: from its aggregates / raw q rows) ----

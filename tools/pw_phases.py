@@ -47,7 +47,7 @@ def main():
             # marks: 0 start, 11 cdf staged, 12 draws, 13 skr, 14 gamma, 1 S end, 2 bar, 3 G end, 4 bar,
             # 15 U loads, 16 U update, 5 U end, 6 bar, 7 P end, 18 pair wait, 19 gram load, 20 inverse,
             # 21 scores, 22 lookback, 8 I+Q end, 9, 10 bar
-            seq = [("S:cdf", 0, 11), ("S:d-entry", 11, 32), ("S:d-philox", 32, 33), ("S:d-search", 33, 34), ("S:d-div", 34, 35), ("S:d-sync", 35, 36), ("S:weights", 36, 12), ("S:skr", 12, 13), ("S:img", 13, 23), ("S:gblk", 23, 24), ("S:gred", 24, 14), ("S:tail", 14, 1),
+            seq = [("S:wait", 0, 38), ("S:stage", 38, 11), ("S:d-entry", 11, 32), ("S:d-philox", 32, 33), ("S:d-search", 33, 34), ("S:d-div", 34, 35), ("S:d-sync", 35, 36), ("S:weights", 36, 12), ("S:skr", 12, 13), ("S:img", 13, 23), ("S:gblk", 23, 24), ("S:gred", 24, 14), ("S:tail", 14, 1),
                    ("barS", 1, 2), ("G:sfb", 2, 25), ("G:first", 25, 26), ("G:stream", 26, 27), ("G:mma", 27, 28),
                    ("G:epi", 28, 29), ("G:tail", 29, 3), ("barG", 3, 4), ("U:load", 4, 15), ("U:upd", 15, 16),
                    ("U:gram", 16, 5), ("barU", 5, 6), ("P", 6, 7), ("I:wait", 7, 18), ("I:load", 18, 19),
