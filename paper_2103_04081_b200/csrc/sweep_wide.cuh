@@ -887,9 +887,11 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
     }
   }
   __syncthreads();
-  // fixed (eq:proposed) / adaptive (eq:etaada/eq:Aada, :531-537, R12) update
-  for (int e = tid; e < nr * R; e += nth) {
-    const int il = e / R, r = e % R;
+  // fixed (eq:proposed) / adaptive (eq:etaada/eq:Aada, :531-537, R12) update; thread -> (row
+  // tid / 28, columns tid % 28 + 28 j): 448 = 16 rows x 28, no run-time division per element
+  static_assert(kPWThreads == kPWRows * 28, "16 rows x 28 columns per pass");
+  const int ilt = tid / 28, rt0 = tid % 28;
+  for (int r = rt0, il = ilt; il < nr && r < R; r += 28) {
     const int64_t gi = (r0 + il) * R + r;
     const float g = sM[il * RS + r];
     p.Gout[gi] = g;
@@ -922,10 +924,9 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
     const int RG = max(1, min(4, nth / nblk));
     double* sAd = sgp_d;                              // [16][RD], zero past R
     double* redP = sgp_d + kPWRows * RD;              // [RG][P]
-    for (int e = tid; e < kPWRows * RD; e += nth) {
-      const int il = e / RD, c = e % RD;
+    for (int c = tid % 28, il = tid / 28; c < RD; c += 28) {  // 16 rows x 28 threads (no division per element)
       const float v = sA[il * AS + min(c, R - 1)];  // rows < 16: inside the buffer
-      sAd[e] = (il < nr && c < R) ? (double)v : 0.0;
+      sAd[il * RD + c] = (il < nr && c < R) ? (double)v : 0.0;
     }
     __syncthreads();
     if (R > 32 && !(p.ablate & 0x200u)) {
@@ -1031,11 +1032,10 @@ static __device__ void pw_table_unit(const PWParams& p, int n, int unit, int nun
   if (lev) {
     // the unit's new rows in fp64 (stride RD, zero padded): from this CTA's own update phase (sAu, stride
     // R, still in shared memory when this is the CTA's last unit) or re-read through L2
-    for (int e = tid; e < kPWRows * RD; e += nth) {
-      const int il = e / RD, c = e % RD;
+    for (int c = tid % 28, il = tid / 28; c < RD; c += 28) {  // 16 rows x 28 threads (no division per element)
       const int ilc = min(il, nr - 1), cc = min(c, R - 1);  // clamped, then select
       const float v = sAu ? sAu[ilc * R + cc] : __ldcg(p.factors[n] + (r0 + ilc) * R + cc);
-      Ad[e] = (il < nr && c < R) ? (double)v : 0.0;
+      Ad[il * RD + c] = (il < nr && c < R) ? (double)v : 0.0;
     }
     __syncthreads();
     // l_i = a_i^T W a_i: warp w takes rows 2w, 2w + 1; lane c holds columns c and c + 32 of y = W a
