@@ -185,6 +185,7 @@ struct cp_sgd_s {
   float* zimg = nullptr;         // tcgen05 path: {zh; zl} A-operand images of the prefetched batch
   // persistent cooperative sweep kernel of the fp32 wide path (k_sweep_wide, sweep_wide.cuh)
   bool pw_ok = false;
+  const int* pw_chg = nullptr;     // cp_sgd_steps_host's optimistic persistent launch: the take-over flags
   int pw_grid = 0;
   size_t pw_smem = 0;
   uint32_t pw_tag = 0;           // look-back tags: iteration s of a launch uses pw_tag + 1 + s
@@ -1316,6 +1317,7 @@ cp_status launch_pw(cp_sgd_s* h, int nsteps, int first_mode, int order, double a
   p.Gam_out = (float*)h->Gam_out;
   p.tr = trace_params(h, nsteps);
   p.dbg = h->dbg;
+  p.chg = h->pw_chg;
   p.ablate = getenv("CPSGD_PW_ABLATE_MASK") ? (unsigned)strtoul(getenv("CPSGD_PW_ABLATE_MASK"), nullptr, 0) : 0u;
   h->pw_tag += (uint32_t)nsteps;
   static DevOnce attr_once[4];
@@ -2339,15 +2341,40 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
       st = check_launch(h, "k_take_compare");
       if (st) return st;
     }
-    // the take-over / table rebuild of every mode, decided on the device: a mode whose flag is clear (the usual
-    // case: the host holds what the last call returned) leaves the kernel at once -- no host round trip between
-    // the copies in and the sweep
+    const bool whole = first_mode == 0 && nsteps % h->N == 0 && alpha < 0.0;
+    if (whole && h->pw_ok) {
+      // optimistic (the usual case: the host holds what the last call returned): the persistent launch itself checks
+      // the flags and does nothing if any is set (status kPWTakeOver) -- no take-over launches, no host round trip
+      const uint64_t it0 = h->iter_host;
+      const int lm0 = h->last_mode;
+      h->pw_chg = h->take_chg;
+      st = cp_sgd_sweep(h, nsteps / h->N, CP_ORDER_CYCLIC, nullptr);
+      h->pw_chg = nullptr;
+      if (st) return st;
+      if (h->pw_ok) {  // (a refused cooperative launch ran the chain, flags unread: the take-over path below)
+        for (int k = 0; k < h->N; ++k)
+          CUDA_TRY(h, cudaMemcpyAsync(factors_host[k], h->factors[k], h->esz * h->dims[k] * h->R, cudaMemcpyDeviceToHost,
+                                      h->stream));
+        // the status with the factors (pinned, same stream): one host round trip for the whole call
+        if (!h->chg_host) CUDA_TRY(h, cudaMallocHost(&h->chg_host, sizeof(int) * kMaxOrder));
+        CUDA_TRY(h, cudaMemcpyAsync(h->chg_host, h->status_dev, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+        const int status = h->chg_host[0];
+        if (status == 0) return CP_OK;
+        if (status != kPWTakeOver) return cp_sgd_sync(h);  // reports (and clears) the device status
+        CUDA_TRY(h, cudaMemsetAsync(h->status_dev, 0, sizeof(int), h->stream));
+        h->iter_host = it0;  // nothing ran: take over, then the sweeps
+        h->last_mode = lm0;
+      }
+    }
+    // the take-over / table rebuild of every mode, decided on the device: a mode whose flag is clear leaves the
+    // kernel at once -- no host round trip between the copies in and the sweep
     for (int k = 0; k < h->N; ++k) {
       st = h->esz == 8 ? launch_uw_t<double>(h, k, 0.0, nullptr, h->take_chg + k)
                        : launch_uw_t<float>(h, k, 0.0, nullptr, h->take_chg + k);
       if (st) return st;
     }
-    if (first_mode == 0 && nsteps % h->N == 0 && alpha < 0.0) {  // whole cyclic sweeps: the sweep graph
+    if (whole) {  // whole cyclic sweeps: the sweep graph
       st = cp_sgd_sweep(h, nsteps / h->N, CP_ORDER_CYCLIC, nullptr);
       if (st) return st;
     } else {

@@ -1484,6 +1484,19 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
+  if (p.chg) {  // cp_sgd_steps_host, optimistic: changed host factors -> nothing done, the host takes over and re-runs
+    if (tid == 0) {
+      int any = 0;
+      for (int k = 0; k < p.N; ++k) any |= __ldcg(p.chg + k);
+      s_stop = any;
+      if (any && blockIdx.x == 0) atomicCAS(p.status, 0, kPWTakeOver);
+    }
+    __syncthreads();
+    if (s_stop) {
+      if (wid == 13) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+      return;
+    }
+  }
   unsigned gen = 0;  // barriers passed in this launch
   uint64_t r = s_r0;
   uint32_t gs = 0, gi = 0;

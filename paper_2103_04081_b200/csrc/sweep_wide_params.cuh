@@ -60,6 +60,8 @@ struct PWParams {
   float* Gout;
   float* Gam_out;
   TraceParams tr;
+  const int* chg;                  // cp_sgd_steps_host: per-mode "staged host factor differs" flags, or NULL; any set
+                                   // -> the launch does nothing but report kPWTakeOver (the host takes over, re-runs)
   long long* dbg;
   // timing experiments only (CPSGD_PW_ABLATE_MASK; results are garbage): 1 skip the sweep inverse (W = diag(1 / G_jj)), 2 skip the
   // fiber loads of the gather, 4 skip the pair sums and the Gram load, 8 skip the update's Gram partials,
@@ -67,6 +69,8 @@ struct PWParams {
   // phases (scores, Gram partials, Gamma partials, G, inverse: timing comparison)
   unsigned ablate;
 };
+
+constexpr int kPWTakeOver = -99;  // device status: the optimistic cp_sgd_steps_host launch found changed host factors
 
 __host__ __device__ inline int pw_units_rows(int64_t In) { return (int)((In + kPWRows - 1) / kPWRows); }
 __host__ __device__ inline int pw_units_fib(int64_t bmax) { return (int)((bmax + kPWFib - 1) / kPWFib); }

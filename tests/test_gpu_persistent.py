@@ -221,3 +221,41 @@ def test_pw_falls_back_to_the_chain_when_not_coresident(monkeypatch):
     for k in range(3):
         assert rel_err(Ad[k].cpu().numpy(), ref[k], np.linalg.norm(ref[k])) <= 1e-3
     h.close()
+
+
+def test_pw_steps_host_optimistic_and_take_over():
+    """cp_sgd_steps_host on the persistent path (whole cyclic sweeps): with host factors equal to the device copy the
+    one launch runs the sweep (bitwise the device-path sweep of an identical handle); with changed host factors the
+    launch does nothing (the flags say so), the changed factors are taken over with their tables rebuilt and the
+    sweep runs -- the result equals a fresh handle started from those factors at the same iteration."""
+    dims, R, B = (152, 100, 90), 40, 512
+    cfg = synth.small(dims, R, dtype="f32", batch=B, rule="fixed", row_sigma=1.0, noise=1e-2, seed=9, alpha=0.004)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "leverage", seed=4, fused=False, mode_major=True)
+    assert h.path == "persistent"
+    host = [torch.from_numpy(a.copy()).pin_memory() for a in A0]
+    h.steps_host(0, 3, host)
+    _, Ar = to_dev(X, A0)
+    ref = handle(cfg, Xd, Ar, "leverage", seed=4, fused=False, mode_major=True)
+    ref.sweep(1)
+    ref.sync()
+    for k in range(3):
+        assert np.array_equal(host[k].numpy(), Ar[k].cpu().numpy())
+        assert np.array_equal(Ad[k].cpu().numpy(), Ar[k].cpu().numpy())
+    ref.close()
+    rng = np.random.default_rng(7)
+    A1 = [host[k].numpy() * (1.0 + 0.05 * rng.standard_normal(A0[k].shape)).astype(np.float32) for k in range(3)]
+    host = [torch.from_numpy(a.copy()).pin_memory() for a in A1]
+    h.steps_host(0, 3, host)
+    assert h.iter == 6
+    _, Ar = to_dev(X, A1)
+    ref = handle(cfg, Xd, Ar, "leverage", seed=4, fused=False, mode_major=True)
+    ref.iter = 3
+    ref.sweep(1)
+    ref.sync()
+    for k in range(3):
+        a, b = host[k].numpy().astype(np.float64), Ar[k].cpu().numpy().astype(np.float64)
+        assert np.linalg.norm(a - b) <= 1e-4 * np.linalg.norm(b)
+    ref.close()
+    h.close()
