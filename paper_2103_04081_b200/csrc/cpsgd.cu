@@ -2328,17 +2328,29 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
   } else if (wide) {  // changed factors (bitwise, per mode) taken over by k_update_wide, tables rebuilt
     if (!h->take_chg) CUDA_TRY(h, cudaMalloc(&h->take_chg, sizeof(int) * kMaxOrder));
     CUDA_TRY(h, cudaMemsetAsync(h->take_chg, 0, sizeof(int) * kMaxOrder, h->stream));
-    for (int k = 0; k < h->N; ++k) {
-      const int64_t ne = h->dims[k] * h->R;
-      const int blocks = (int)std::min<int64_t>(ceil_div(ne, 256), 148 * 4);
-      if (h->esz == 8)
-        k_take_compare<double><<<blocks, 256, 0, h->ls>>>((const double*)h->fstage[k], (const double*)h->factors[k], ne,
-                                                          h->take_chg + k);
-      else
-        k_take_compare<float><<<blocks, 256, 0, h->ls>>>((const float*)h->fstage[k], (const float*)h->factors[k], ne,
-                                                         h->take_chg + k);
+    {  // every mode in one launch
+      int64_t nmax = 0;
+      for (int k = 0; k < h->N; ++k) nmax = std::max<int64_t>(nmax, h->dims[k] * h->R);
+      const dim3 grid((unsigned)std::min<int64_t>(ceil_div(nmax, 256), 148 * 2), (unsigned)h->N);
+      if (h->esz == 8) {
+        TakeAll<double> a{};
+        for (int k = 0; k < h->N; ++k) {
+          a.fstage[k] = (const double*)h->fstage[k];
+          a.A[k] = (const double*)h->factors[k];
+          a.n[k] = h->dims[k] * h->R;
+        }
+        k_take_compare_all<double><<<grid, 256, 0, h->ls>>>(a, h->take_chg);
+      } else {
+        TakeAll<float> a{};
+        for (int k = 0; k < h->N; ++k) {
+          a.fstage[k] = (const float*)h->fstage[k];
+          a.A[k] = (const float*)h->factors[k];
+          a.n[k] = h->dims[k] * h->R;
+        }
+        k_take_compare_all<float><<<grid, 256, 0, h->ls>>>(a, h->take_chg);
+      }
       h->launches++;
-      st = check_launch(h, "k_take_compare");
+      st = check_launch(h, "k_take_compare_all");
       if (st) return st;
     }
     const bool whole = first_mode == 0 && nsteps % h->N == 0 && alpha < 0.0;

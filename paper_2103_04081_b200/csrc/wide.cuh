@@ -98,16 +98,22 @@ struct UWParams {
   unsigned* p2p_cnt;                // CTA arrivals after the peer reads (zero between launches)
 };
 
-// cp_sgd_steps_host (wide path): chg[k] |= 1 when the staged host factor k differs bitwise from the
-// device copy (chg zeroed by the caller)
+// cp_sgd_steps_host (wide path): every mode in one launch (blockIdx.y = mode): chg[k] |= 1 when staged host factor k differs bitwise
 template <typename T>
-__global__ void k_take_compare(const T* fstage, const T* A, int64_t n, int* chg) {
+struct TakeAll {
+  const T* fstage[kMaxOrder];
+  const T* A[kMaxOrder];
+  int64_t n[kMaxOrder];
+};
+template <typename T>
+__global__ void k_take_compare_all(TakeAll<T> a, int* chg) {
+  const int k = blockIdx.y;
   bool d = false;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    if constexpr (sizeof(T) == 8) d |= __double_as_longlong(fstage[e]) != __double_as_longlong(A[e]);
-    else d |= __float_as_uint(fstage[e]) != __float_as_uint(A[e]);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.n[k]; e += (int64_t)gridDim.x * blockDim.x) {
+    if constexpr (sizeof(T) == 8) d |= __double_as_longlong(a.fstage[k][e]) != __double_as_longlong(a.A[k][e]);
+    else d |= __float_as_uint(a.fstage[k][e]) != __float_as_uint(a.A[k][e]);
   }
-  if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(chg, 1);
+  if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(chg + k, 1);
 }
 
 // (a6-a8) + (a1) up to the inverse: grid = ceil(I_n / kUWRows); dynamic shared memory = the step's
@@ -371,7 +377,7 @@ __global__ void __launch_bounds__(kWThreads) k_update_wide(UWParams<T> p) {
   const int nb4 = (R + 3) >> 2;
   if (p.table_only) {
     // cp_sgd_steps_host: the staged host rows replace the factor when any of them differs (the
-    // flag set by k_take_compare); an unchanged factor keeps its table: every CTA leaves here
+    // flag set by k_take_compare_all); an unchanged factor keeps its table: every CTA leaves here
     if (__ldcg(p.chg) == 0) return;
     for (int e = tid; e < nr * R; e += kWThreads) {
       const int il = e / R, c = e % R;
