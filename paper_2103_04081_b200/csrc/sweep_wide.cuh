@@ -1315,9 +1315,16 @@ __device__ int dmma_sweep_inverse(double* Gm, const double* gpk, int R, double t
     c1[j] = tI[j] < 0 ? 0.0 : (r < R && c + 1 < R) ? g1 : (r == c + 1 ? 1.0 : 0.0);
   }
   __syncthreads();
+  // the Gram's entry (r, c) as the tiles start (identity past R)
+  auto gval = [&](int r, int c) {
+    const int rc = min(r, R - 1), cc = min(c, R - 1);
+    const int a = rc <= cc ? rc : cc, b = rc <= cc ? cc : rc;
+    const double v = gpk[a * R - a * (a - 1) / 2 + (b - a)];  // clamped, then select
+    return (r < R && c < R) ? v : (r == c ? 1.0 : 0.0);
+  };
   if (w == 0) {  // ---------------- the pivot warp
-    mbar_wait(&bars.rows[0], 0);
-    double b0 = Prow[gr * LD + 2 * gc], b1 = Prow[gr * LD + 2 * gc + 1];
+    // block 0 and its Schur step read the Gram itself (the same values the owners publish): no wait to start
+    double b0 = gval(gr, 2 * gc), b1 = gval(gr, 2 * gc + 1);
 #pragma unroll 1
     for (int kb = 0; kb < NB; ++kb) {
       bool ok = true;
@@ -1339,18 +1346,29 @@ __device__ int dmma_sweep_inverse(double* Gm, const double* gpk, int R, double t
       Sw[kb * 64 + gr * 8 + 2 * gc + 1] = b1;
       mbar_arrive(&bars.binv[kb]);
       if (!ok || kb + 1 == NB) break;
-      mbar_wait(&bars.rows[kb], 0);
       const double* P = Prow + kb * 8 * LD;
       const int J = kb + 1;
+      double q0, q1, d0, d1;  // Q = block row kb's column block J (rows gc, gc + 4; column gr), D = tile (J, J)
+      if (kb == 0) {
+        q0 = gval(gc, 8 * J + gr);
+        q1 = gval(gc + 4, 8 * J + gr);
+        d0 = gval(8 * J + gr, 8 * J + 2 * gc);
+        d1 = gval(8 * J + gr, 8 * J + 2 * gc + 1);
+      } else {
+        mbar_wait(&bars.rows[kb], 0);
+        q0 = P[gc * LD + 8 * J + gr];
+        q1 = P[(gc + 4) * LD + 8 * J + gr];
+        d0 = Dd[J * 64 + gr * 8 + 2 * gc];
+        d1 = Dd[J * 64 + gr * 8 + 2 * gc + 1];
+      }
       double f0 = 0.0, f1 = 0.0;
-      dmma_f64(f0, f1, -Sw[kb * 64 + gr * 8 + gc], P[gc * LD + 8 * J + gr]);
-      dmma_f64(f0, f1, -Sw[kb * 64 + gr * 8 + gc + 4], P[(gc + 4) * LD + 8 * J + gr]);
+      dmma_f64(f0, f1, -Sw[kb * 64 + gr * 8 + gc], q0);
+      dmma_f64(f0, f1, -Sw[kb * 64 + gr * 8 + gc + 4], q1);
       scr[gr * 8 + 2 * gc] = f0;
       scr[gr * 8 + 2 * gc + 1] = f1;
       __syncwarp();
-      double d0 = Dd[J * 64 + gr * 8 + 2 * gc], d1 = Dd[J * 64 + gr * 8 + 2 * gc + 1];
-      dmma_f64(d0, d1, -P[gc * LD + 8 * J + gr], scr[gc * 8 + gr]);
-      dmma_f64(d0, d1, -P[(gc + 4) * LD + 8 * J + gr], scr[(gc + 4) * 8 + gr]);
+      dmma_f64(d0, d1, -q0, scr[gc * 8 + gr]);
+      dmma_f64(d0, d1, -q1, scr[(gc + 4) * 8 + gr]);
       __syncwarp();
       b0 = d0;
       b1 = d1;
