@@ -41,6 +41,8 @@ PW_CASES = [
     ((200, 64, 33, 20), 10, 1024),  # 4-way
     ((2600, 40, 30), 16, 1024),     # I_0 > 148 x 16: CTAs with two row units (shared rows re-read, prefix loop)
     ((260, 140, 130), 64, 1024),    # R = 64 = kMaxRank (the RMAX = 64 sweep instance)
+    ((200, 120, 80), 33, 768),      # R = 33: the smallest rank on the fp64 tensor-core phases (most 8x8 tiles padding)
+    ((240, 160, 120), 56, 1024),    # R = 56 = RMAX: no padding column in the last 8x8 block
 ]
 
 
