@@ -924,14 +924,10 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
     const int RG = max(1, min(4, nth / nblk));
     double* sAd = sgp_d;                              // [16][RD], zero past R
     double* redP = sgp_d + kPWRows * RD;              // [RG][P]
-    for (int c = tid % 28, il = tid / 28; c < RD; c += 28) {  // 16 rows x 28 threads (no division per element)
-      const float v = sA[il * AS + min(c, R - 1)];  // rows < 16: inside the buffer
-      sAd[il * RD + c] = (il < nr && c < R) ? (double)v : 0.0;
-    }
-    __syncthreads();
     if (R > 32 && !(p.ablate & 0x200u)) {
-      // R > 32 on fp64 tensor cores (mma.sync m8n8k4 f64): the unit's Gram = sAd^T sAd as 8x8 tiles I <= J (one
-      // per warp, round robin), the 16 rows in four k-steps; stored straight into the packed pair partials
+      // R > 32 on fp64 tensor cores (mma.sync m8n8k4 f64): the unit's Gram = A_u^T A_u as 8x8 tiles I <= J (one
+      // per warp, round robin), the 16 rows in four k-steps, the fp32 rows read as operands directly (exact in fp64);
+      // stored straight into the packed pair partials
       const int ncb = (R + 7) >> 3, ntile = ncb * (ncb + 1) / 2, lane = tid & 31, gr = lane >> 2, gc = lane & 3;
       double* gp = p.gpart + unit;  // [P][gstride]: the pair sums read each pair's unit partials contiguously
       for (int t = tid >> 5; t < ntile; t += nth >> 5) {
@@ -941,11 +937,12 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
         const int ca = 8 * I + gr, cb = 8 * J + gr, cac = min(ca, R - 1), cbc = min(cb, R - 1);
         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-        for (int k0 = 0; k0 < kPWRows; k0 += 4) {  // A[r][k] = sAd[k][8I + r], B[k][n] = sAd[k][8J + n]
-          const double av = sAd[(k0 + gc) * RD + cac], bv = sAd[(k0 + gc) * RD + cbc];  // clamped, then select
+        for (int k0 = 0; k0 < kPWRows; k0 += 4) {  // A[r][k] = A_u[k][8I + r], B[k][n] = A_u[k][8J + n]
+          const int kr = k0 + gc;
+          const float av = sA[kr * AS + cac], bv = sA[kr * AS + cbc];  // rows < 16: inside the buffer; clamped
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                        : "+d"(d0), "+d"(d1)
-                       : "d"(ca < R ? av : 0.0), "d"(cb < R ? bv : 0.0));
+                       : "d"((ca < R && kr < nr) ? (double)av : 0.0), "d"((cb < R && kr < nr) ? (double)bv : 0.0));
         }
         const int r1 = 8 * I + gr;
 #pragma unroll
@@ -955,6 +952,11 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
         }
       }
     } else {
+    for (int c = tid % 28, il = tid / 28; c < RD; c += 28) {  // 16 rows x 28 threads (no division per element)
+      const float v = sA[il * AS + min(c, R - 1)];  // rows < 16: inside the buffer
+      sAd[il * RD + c] = (il < nr && c < R) ? (double)v : 0.0;
+    }
+    __syncthreads();
     for (int t = tid; t < nblk * RG; t += nth) {
       const int g = t / nblk, blk = t % nblk;
       int bi = 0, rem = blk;
