@@ -43,6 +43,7 @@ PW_CASES = [
     ((260, 140, 130), 64, 1024),    # R = 64 = kMaxRank (the RMAX = 64 sweep instance)
     ((200, 120, 80), 33, 768),      # R = 33: the smallest rank on the fp64 tensor-core phases (most 8x8 tiles padding)
     ((240, 160, 120), 56, 1024),    # R = 56 = RMAX: no padding column in the last 8x8 block
+    ((120, 96, 84, 20), 40, 512),   # 4-way (the generic sampling code) with the tensor-core phases; I_3 < 2R
 ]
 
 
