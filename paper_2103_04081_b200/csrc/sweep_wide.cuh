@@ -817,8 +817,11 @@ static __device__ void pw_update_unit(const PWParams& p, int n, int unit, double
         if (gq * 4 + w < nr) sM[(gq * 4 + w) * RS + r] = acc[w];
     }
   }
+  PW_MK2(7);
   cp_async_wait<0>();
+  PW_MK2(8);
   if (bkw) pw_bulk_wait(*bkw);  // Gamma (first unit of the CTA)
+  PW_MK2(9);
   __syncthreads();
   PW_MK(15);
   // G = A Gamma - M.  R > 32: on fp64 tensor cores (mma.sync m8n8k4 f64; 8x8 tiles of the 16 x R block, one per warp,
@@ -1590,7 +1593,8 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
       if ((int)blockIdx.x == G - 1)
         for (int e = tid; e < R * R; e += kPWThreads) p.Gam_out[e] = __ldcg(p.gam + e);
       if ((int)blockIdx.x < nu) {
-        if (tid == 0) {  // Gamma (every CTA reads it now): a bulk copy, waited for with the unit's rows
+        if (tid == kPWThreads - 32) {  // Gamma (every CTA reads it now): a bulk copy, waited for with the unit's rows
+                                       // (issued by a thread without M-sum work: the proxy fence stalls its issuer)
           pw_bulk_begin(bk, pw_b16((int64_t)R * R * 4));
           bulk_g2s(sG, p.gam, pw_b16((int64_t)R * R * 4), bk.bar);
         }

@@ -49,7 +49,7 @@ def main():
             # 21 scores, 22 lookback, 8 I+Q end, 9, 10 bar
             seq = [("S:wait", 0, 38), ("S:stage", 38, 11), ("S:d-entry", 11, 32), ("S:d-philox", 32, 33), ("S:d-search", 33, 34), ("S:d-div", 34, 35), ("S:d-sync", 35, 36), ("S:weights", 36, 12), ("S:skr", 12, 13), ("S:img", 13, 23), ("S:gblk", 23, 24), ("S:gred", 24, 14), ("S:tail", 14, 1),
                    ("barS", 1, 2), ("G:sfb", 2, 25), ("G:first", 25, 26), ("G:stream", 26, 27), ("G:mma", 27, 28),
-                   ("G:epi", 28, 29), ("G:tail", 29, 3), ("barG", 3, 4), ("U:load", 4, 15), ("U:upd", 15, 16),
+                   ("G:epi", 28, 29), ("G:tail", 29, 3), ("barG", 3, 4), ("U:issue+M", 4, 39), ("U:cpwait", 39, 40), ("U:gamwait", 40, 41), ("U:sync", 41, 15), ("U:upd", 15, 16),
                    ("U:gram", 16, 5), ("barU", 5, 6), ("P", 6, 7), ("I:wait", 7, 18), ("I:load", 18, 19),
                    ("I:inv", 19, 20), ("Q:score", 20, 21), ("Q:lookb", 21, 22), ("Q:tail", 22, 9),
                    ("barQ", 9, 10)]
