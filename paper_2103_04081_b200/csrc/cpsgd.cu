@@ -2213,6 +2213,7 @@ cp_status cp_sgd_sweep(cp_sgd_t h, int32_t nsweeps, int32_t order, const double*
       h->iter_host += nst;
       return CP_OK;
     }  // else: not co-resident -- the chain below
+    if (h->pw_chg) return CP_OK;  // cp_sgd_steps_host's optimistic call: nothing ran, it takes over and re-runs
   }
   const bool use_graph = order == CP_ORDER_CYCLIC && !alpha_per_iter && !(h->flags & CP_FLAG_NO_GRAPH) && !h->prof;
   if (!use_graph) {
@@ -2363,7 +2364,7 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
       st = cp_sgd_sweep(h, nsteps / h->N, CP_ORDER_CYCLIC, nullptr);
       h->pw_chg = nullptr;
       if (st) return st;
-      if (h->pw_ok) {  // (a refused cooperative launch ran the chain, flags unread: the take-over path below)
+      if (h->pw_ok) {  // (a refused cooperative launch ran nothing: the take-over path below, on the chain)
         for (int k = 0; k < h->N; ++k)
           CUDA_TRY(h, cudaMemcpyAsync(factors_host[k], h->factors[k], h->esz * h->dims[k] * h->R, cudaMemcpyDeviceToHost,
                                       h->stream));

@@ -262,3 +262,31 @@ def test_pw_steps_host_optimistic_and_take_over():
         assert np.linalg.norm(a - b) <= 1e-4 * np.linalg.norm(b)
     ref.close()
     h.close()
+
+
+def test_pw_steps_host_refused_launch_takes_over(monkeypatch):
+    """cp_sgd_steps_host's optimistic persistent launch refused (grid not co-resident, simulated): nothing runs in
+    the optimistic call, the changed host factors are taken over and the sweep runs once on the kernel chain --
+    equal to a fresh handle started from those factors at the same iteration."""
+    dims, R, B = (152, 100, 90), 40, 512
+    cfg = synth.small(dims, R, dtype="f32", batch=B, rule="fixed", row_sigma=1.0, noise=1e-2, seed=9, alpha=0.004)
+    X, A0 = make_problem(cfg)
+    Xd, Ad = to_dev(X, A0)
+    h = handle(cfg, Xd, Ad, "leverage", seed=4, fused=False, mode_major=True)
+    assert h.path == "persistent"
+    rng = np.random.default_rng(11)
+    A1 = [(a * (1.0 + 0.05 * rng.standard_normal(a.shape))).astype(np.float32) for a in A0]
+    host = [torch.from_numpy(a.copy()).pin_memory() for a in A1]
+    monkeypatch.setenv("CPSGD_PW_FORCE_FALLBACK", "1")
+    h.steps_host(0, 3, host)
+    monkeypatch.delenv("CPSGD_PW_FORCE_FALLBACK")
+    assert h.iter == 3 and h.path == "chain"
+    _, Ar = to_dev(X, A1)
+    ref = handle(cfg, Xd, Ar, "leverage", seed=4, fused=False, mode_major=True)
+    ref.sweep(1)
+    ref.sync()
+    for k in range(3):
+        a, b = host[k].numpy().astype(np.float64), Ar[k].cpu().numpy().astype(np.float64)
+        assert np.linalg.norm(a - b) <= 1e-4 * np.linalg.norm(b)
+    ref.close()
+    h.close()
