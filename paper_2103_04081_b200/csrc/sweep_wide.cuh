@@ -285,13 +285,9 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
       }
       o += (ncb + 1) & ~1;
     }
-    for (int e = tid; e < R * R; e += nth) gacc[e] = 0.f;
-    if (tid < N) {
-      ss.dims[tid] = p.dims[tid];
-      ss.lstride[tid] = p.lstride[tid];
-      ss.fac[tid] = p.factors[tid];
-      ss.cp[tid] = (tid == pend) ? p.qraw : p.cdf[tid];
-    }
+    // the CTA's Gamma accumulator starts at zero (R > 32: the first unit's tensor-core partial is stored, not added)
+    if (!(R > 32 && !(p.ablate & 0x200u)))
+      for (int e = tid; e < R * R; e += nth) gacc[e] = 0.f;
   }
   __syncthreads();
   PW_MK(11);
@@ -352,7 +348,7 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
         } else {
           const bool pk = (k == pend);
           const int64_t Ik = ss.dims[k];
-          pw_cdf_search(ss.cp[k], pk, cdfs + ss.coff[k], (int)((Ik + kPWRows - 1) / kPWRows), Ik, rr, i, qk);
+          pw_cdf_search(pk ? p.qraw : ss.cp[k], pk, cdfs + ss.coff[k], (int)((Ik + kPWRows - 1) / kPWRows), Ik, rr, i, qk);
         }
         sidx[e] = (int32_t)i;
         if (m2 && e == 0) PW_MK2(2);
@@ -483,8 +479,9 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
           const int r2 = 8 * J + 2 * gc + i;
           if (r1 < R && r2 < R) {
             const float v = (float)(i ? d1 : d0);
-            gacc[r1 * R + r2] += v;
-            if (I != J) gacc[r2 * R + r1] += v;
+            const bool fu = u == (int)blockIdx.x;  // the CTA's first unit: store (no zeroing pass)
+            gacc[r1 * R + r2] = fu ? v : gacc[r1 * R + r2] + v;
+            if (I != J) gacc[r2 * R + r1] = fu ? v : gacc[r2 * R + r1] + v;
           }
         }
       }
@@ -1501,6 +1498,12 @@ __global__ void __launch_bounds__(kPWThreads, 1) k_sweep_wide(PWParams p) {
     mbar_init(&B.bc, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_r0 = *reinterpret_cast<volatile uint64_t*>(p.iter);
+    for (int k = 0; k < p.N; ++k) {  // per-mode parameters of the sampling phase, staged once per launch
+      ss.dims[k] = p.dims[k];
+      ss.lstride[k] = p.lstride[k];
+      ss.fac[k] = p.factors[k];
+      ss.cp[k] = p.cdf[k];
+    }
     s_stop = 0;
   }
   tc_fence_before();
