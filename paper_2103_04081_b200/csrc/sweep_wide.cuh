@@ -321,8 +321,10 @@ static __device__ void pw_sample(const PWParams& p, int n, uint64_t r, unsigned 
   } else if (!block && tid == 0 && blockIdx.x == 0) {
     *p.beff = p.B;
   }
-  __syncthreads();
-  __syncwarp();
+  if (block) {  // (uniform) the windows of thread 0 for every thread
+    __syncthreads();
+    __syncwarp();
+  }
   const int64_t beff = block ? ss.beff : p.B;
   for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
     const int64_t b0 = (int64_t)u * kPWFib;
