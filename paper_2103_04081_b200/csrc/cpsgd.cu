@@ -1969,7 +1969,7 @@ cp_status cp_sgd_destroy(cp_sgd_t h) {
   cudaFree(h->zrow);
   cudaFree(h->fbase);
   cudaFree(h->zwp);
-  for (int k = 0; k < kMaxOrder; ++k) cudaFree(h->fstage[k]);
+  cudaFree(h->fstage[0]);  // one block for every mode (cp_sgd_steps_host)
   cudaFree(h->take_chg);
   cudaFree(h->multi_params);
   cudaFree(h->zimg);
@@ -2304,6 +2304,27 @@ cp_status cp_sgd_sweep_multi(cp_sgd_t* hs, int32_t nh, int32_t nsweeps) {
   return imax > kFThreads ? launch_fused_multi_t<float, 2>(hs, nh, (int)nst) : launch_fused_multi_t<float, 1>(hs, nh, (int)nst);
 }
 
+// the factors' host <-> device copies of cp_sgd_steps_host: ONE transfer when both sides hold the modes back to back
+// (a per-transfer cost of several us dominates 400 KB copies), else one per mode
+static cp_status copy_factors(cp_sgd_t h, void* const* dst, void* const* src, cudaMemcpyKind kind) {
+  bool packed = true;
+  size_t tot = 0;
+  for (int k = 0; k < h->N; ++k) {
+    const size_t b = h->esz * h->dims[k] * h->R;
+    if (k > 0 && ((const char*)dst[k - 1] + tot != dst[k] || (const char*)src[k - 1] + tot != src[k])) packed = false;
+    tot = b;
+  }
+  if (packed) {
+    size_t all = 0;
+    for (int k = 0; k < h->N; ++k) all += h->esz * h->dims[k] * h->R;
+    CUDA_TRY(h, cudaMemcpyAsync(dst[0], src[0], all, kind, h->stream));
+    return CP_OK;
+  }
+  for (int k = 0; k < h->N; ++k)
+    CUDA_TRY(h, cudaMemcpyAsync(dst[k], src[k], h->esz * h->dims[k] * h->R, kind, h->stream));
+  return CP_OK;
+}
+
 cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, double alpha,
                             void* const* factors_host) {
   cp_status st = check_mode(h, first_mode);
@@ -2313,11 +2334,18 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
   bool wide = !fused && h->world_size == 1;  // every mode on the wide path: k_update_wide takes over
   for (int k = 0; k < h->N; ++k) wide = wide && wide_mode(h, k);
   const bool stage = fused || wide;
-  for (int k = 0; k < h->N; ++k) {
-    const size_t bytes = h->esz * h->dims[k] * h->R;
-    if (stage && !h->fstage[k]) CUDA_TRY(h, cudaMalloc(&h->fstage[k], bytes));
-    CUDA_TRY(h, cudaMemcpyAsync(stage ? h->fstage[k] : h->factors[k], factors_host[k], bytes, cudaMemcpyHostToDevice,
-                                h->stream));
+  if (stage && !h->fstage[0]) {  // the staging of every mode in one block, packed back to back
+    size_t tot = 0;
+    for (int k = 0; k < h->N; ++k) tot += h->esz * h->dims[k] * h->R;
+    CUDA_TRY(h, cudaMalloc(&h->fstage[0], tot));
+    for (int k = 1; k < h->N; ++k)
+      h->fstage[k] = (char*)h->fstage[k - 1] + h->esz * h->dims[k - 1] * h->R;
+  }
+  {
+    void* dst[kMaxOrder];
+    for (int k = 0; k < h->N; ++k) dst[k] = stage ? h->fstage[k] : h->factors[k];
+    st = copy_factors(h, dst, factors_host, cudaMemcpyHostToDevice);
+    if (st) return st;
   }
   h->pref_mode = -1;
   // the host factors may differ from the device ones: rebuild the tables
@@ -2365,9 +2393,8 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
       h->pw_chg = nullptr;
       if (st) return st;
       if (h->pw_ok) {  // (a refused cooperative launch ran nothing: the take-over path below, on the chain)
-        for (int k = 0; k < h->N; ++k)
-          CUDA_TRY(h, cudaMemcpyAsync(factors_host[k], h->factors[k], h->esz * h->dims[k] * h->R, cudaMemcpyDeviceToHost,
-                                      h->stream));
+        st = copy_factors(h, factors_host, h->factors, cudaMemcpyDeviceToHost);
+        if (st) return st;
         // the status with the factors (pinned, same stream): one host round trip for the whole call
         if (!h->chg_host) CUDA_TRY(h, cudaMallocHost(&h->chg_host, sizeof(int) * kMaxOrder));
         CUDA_TRY(h, cudaMemcpyAsync(h->chg_host, h->status_dev, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
@@ -2406,9 +2433,8 @@ cp_status cp_sgd_steps_host(cp_sgd_t h, int32_t first_mode, int32_t nsteps, doub
       if (st) return st;
     }
   }
-  for (int k = 0; k < h->N; ++k)
-    CUDA_TRY(h, cudaMemcpyAsync(factors_host[k], h->factors[k], h->esz * h->dims[k] * h->R, cudaMemcpyDeviceToHost,
-                                h->stream));
+  st = copy_factors(h, factors_host, h->factors, cudaMemcpyDeviceToHost);
+  if (st) return st;
   return cp_sgd_sync(h);
 }
 

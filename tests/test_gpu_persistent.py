@@ -290,3 +290,34 @@ def test_pw_steps_host_refused_launch_takes_over(monkeypatch):
         assert np.linalg.norm(a - b) <= 1e-4 * np.linalg.norm(b)
     ref.close()
     h.close()
+
+
+def test_pw_steps_host_packed_factors_one_transfer():
+    """cp_sgd_steps_host with the factors back to back on both sides (views into one device block and one pinned host
+    block): one transfer each way -- the same bits as the per-mode copies of separate buffers."""
+    dims, R, B = (152, 100, 90), 40, 512
+    cfg = synth.small(dims, R, dtype="f32", batch=B, rule="fixed", row_sigma=1.0, noise=1e-2, seed=9, alpha=0.004)
+    X, A0 = make_problem(cfg)
+    Xd = torch.from_numpy(X).to("cuda")
+    flat = torch.empty(sum(a.size for a in A0), dtype=torch.float32, device="cuda")
+    hflat = torch.empty(flat.numel(), dtype=torch.float32).pin_memory()
+    Ad, host, o = [], [], 0
+    for a in A0:
+        Ad.append(flat[o:o + a.size].view(a.shape))
+        host.append(hflat[o:o + a.size].view(a.shape))
+        Ad[-1].copy_(torch.from_numpy(a))
+        host[-1].copy_(torch.from_numpy(a))
+        o += a.size
+    h = handle(cfg, Xd, Ad, "leverage", seed=4, fused=False, mode_major=True)
+    assert h.path == "persistent"
+    h.steps_host(0, 3, host)
+    h.steps_host(0, 3, host)
+    _, As = to_dev(X, A0)
+    ref = handle(cfg, Xd, As, "leverage", seed=4, fused=False, mode_major=True)
+    hs = [torch.from_numpy(a.copy()).pin_memory() for a in A0]
+    ref.steps_host(0, 3, hs)
+    ref.steps_host(0, 3, hs)
+    for k in range(3):
+        assert np.array_equal(host[k].numpy(), hs[k].numpy())
+    ref.close()
+    h.close()
