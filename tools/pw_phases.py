@@ -51,7 +51,7 @@ def main():
                    ("barS", 1, 2), ("G:sfb", 2, 25), ("G:first", 25, 26), ("G:stream", 26, 27), ("G:mma", 27, 28),
                    ("G:epi", 28, 29), ("G:tail", 29, 3), ("barG", 3, 4), ("U:issue+M", 4, 39), ("U:cpwait", 39, 40), ("U:gamwait", 40, 41), ("U:sync", 41, 15), ("U:upd", 15, 16),
                    ("U:gram", 16, 5), ("barU", 5, 6), ("P", 6, 7), ("I:wait", 7, 18), ("I:load", 18, 19),
-                   ("I:inv", 19, 20), ("Q:score", 20, 21), ("Q:lookb", 21, 22), ("Q:tail", 22, 9),
+                   ("I:inv", 19, 20), ("Q:score", 20, 21), ("Q:tail", 21, 9),
                    ("barQ", 9, 10)]
             rows = []
             for s in range(1, 8):
